@@ -1,0 +1,417 @@
+"""ctypes front-end for the CPU checker — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs import this module.  The product package
+(paper_2505_03360_b200) never does.
+
+Two libraries are exposed:
+
+* :class:`Oracle`  — ``oracle/liboracle.so``, the C restatement
+  (``oracle/hk_oracle.c``), each function citing the reference file:line.
+* :class:`RefLib`  — ``oracle/_ref/libhykin_ref.so``, the reference's own
+  sources compiled with the FFTW3/Eigen API shims (``oracle/Makefile``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libhykin_ref.so")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+    if a.dtype == np.float64:
+        return a.ctypes.data_as(_dp)
+    if a.dtype == np.int32:
+        return a.ctypes.data_as(_ip)
+    raise TypeError(a.dtype)
+
+
+class _Kernel(C.Structure):
+    _fields_ = [
+        ("n", C.c_int), ("a1", C.c_int), ("a2", C.c_int),
+        ("vmax", C.c_double), ("r_phys", C.c_double), ("r", C.c_double),
+        ("jacobian", C.c_double), ("weight", C.c_double),
+        ("alpha", _dp), ("alpha_prime", _dp), ("loss_diag", _dp),
+    ]
+
+
+class _Moments(C.Structure):
+    _fields_ = [("rho", C.c_double), ("u", C.c_double * 3), ("T", C.c_double)]
+
+
+def build(quiet: bool = True) -> None:
+    """Builds liboracle.so (and _ref when /root/reference is present)."""
+    import subprocess
+
+    targets = ["oracle"]
+    if os.path.isdir("/root/reference/proj/core/src"):
+        targets.append("ref")
+    subprocess.run(["make", "-C", HERE, "-j8", *targets], check=True,
+                   stdout=subprocess.DEVNULL if quiet else None)
+
+
+class OracleKernel:
+    """Owns an ``hko_kernel`` (weight tables of src/spectral.cpp:53-112)."""
+
+    def __init__(self, lib, n, vmax, a1, a2, r_phys, closed_form=True, nthreads=8):
+        self._lib = lib
+        self._k = _Kernel()
+        st = lib.hko_precompute(n, C.c_double(vmax), a1, a2, C.c_double(r_phys),
+                                int(bool(closed_form)), nthreads, C.byref(self._k))
+        self.status = st
+        if st:
+            self._k = None
+            return
+        self.n, self.a1, self.a2, self.vmax = n, a1, a2, vmax
+        total = n ** 3
+        d = a1 * a2
+        self.alpha = np.ctypeslib.as_array(self._k.alpha, shape=(d, total)).copy()
+        self.alpha_prime = np.ctypeslib.as_array(self._k.alpha_prime, shape=(d, total)).copy()
+        self.loss_diag = np.ctypeslib.as_array(self._k.loss_diag, shape=(total,)).copy()
+        self.r, self.jacobian, self.weight = self._k.r, self._k.jacobian, self._k.weight
+
+    def __del__(self):
+        if getattr(self, "_k", None) is not None:
+            self._lib.hko_kernel_free(C.byref(self._k))
+            self._k = None
+
+    @property
+    def ref(self):
+        return C.byref(self._k)
+
+
+class Oracle:
+    def __init__(self, path: str = ORACLE_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+        L = self.lib = C.CDLL(path)
+        L.hko_precompute.restype = C.c_int
+        L.hko_spectral_collision.restype = C.c_int
+        L.hko_collision_batch.restype = C.c_int
+        L.hko_closed_radial.restype = C.c_double
+        L.hko_closed_planar.restype = C.c_double
+        L.hko_gk15_radial.restype = C.c_double
+        L.hko_gk15_planar.restype = C.c_double
+        L.hko_node.restype = C.c_double
+        L.hko_lambda_b.restype = C.c_double
+        for fn in ("hko_closed_radial", "hko_closed_planar", "hko_gk15_radial", "hko_gk15_planar"):
+            getattr(L, fn).argtypes = [C.c_double, C.c_double, C.c_double]
+
+    # --- kernel / collision -------------------------------------------------
+    def kernel(self, n, vmax, a1, a2, r_phys, closed_form=True, nthreads=8):
+        return OracleKernel(self.lib, n, vmax, a1, a2, r_phys, closed_form, nthreads)
+
+    def collision(self, k: OracleKernel, f):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        out = np.empty_like(f)
+        res = C.c_double(0.0)
+        st = self.lib.hko_spectral_collision(k.ref, _ptr(f), _ptr(out), C.byref(res))
+        return out, st, res.value
+
+    def collision_batch(self, k: OracleKernel, f, nthreads=8):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        nb = k.n ** 3
+        ncells = f.size // nb
+        q = np.empty_like(f)
+        st = np.zeros(ncells, np.int32)
+        res = np.zeros(ncells, np.float64)
+        self.lib.hko_collision_batch(k.ref, _ptr(f), _ptr(q), C.c_long(ncells), nthreads,
+                                     _ptr(st), _ptr(res))
+        return q, st, res
+
+    def fft3d(self, x, sign):
+        x = np.ascontiguousarray(x, dtype=np.complex128).copy()
+        n = round(x.size ** (1 / 3))
+        self.lib.hko_fft_3d(n, x.ctypes.data_as(_dp), sign)
+        return x
+
+    # --- moments ------------------------------------------------------------
+    def moments(self, n, vmax, f):
+        m = _Moments()
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        st = self.lib.hko_moments_of(n, C.c_double(vmax), _ptr(f), C.byref(m))
+        return st, (m.rho, m.u[0], m.u[1], m.u[2], m.T)
+
+    def second_moment(self, n, vmax, f):
+        s = np.zeros(9)
+        self.lib.hko_second_moment(n, C.c_double(vmax), _ptr(np.ascontiguousarray(f)), _ptr(s))
+        return s.reshape(3, 3)
+
+    def maxwellian(self, n, vmax, mom5):
+        m = _Moments(mom5[0], (C.c_double * 3)(*mom5[1:4]), mom5[4])
+        out = np.empty(n ** 3)
+        st = self.lib.hko_maxwellian(C.byref(m), n, C.c_double(vmax), _ptr(out))
+        return st, out
+
+    def realizability(self, n, vmax, f):
+        st, mom = self.moments(n, vmax, f)
+        m = _Moments(mom[0], (C.c_double * 3)(*mom[1:4]), mom[4])
+        a = np.zeros(9); b = np.zeros(3); c = C.c_double(0.0)
+        self.lib.hko_realizability_matrix(_ptr(np.ascontiguousarray(f)), n, C.c_double(vmax),
+                                          C.byref(m), _ptr(a), _ptr(b), C.byref(c))
+        return st, a.reshape(3, 3), b, c.value
+
+    def match_moments(self, n, vmax, f, rho, mom3, energy):
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        m3 = np.ascontiguousarray(mom3, dtype=np.float64)
+        st = self.lib.hko_match_moments(_ptr(f), n, C.c_double(vmax), C.c_double(rho), _ptr(m3),
+                                        C.c_double(energy))
+        return st, f
+
+    def penalized_residual(self, k: OracleKernel, f, pen_coeff=2 * np.pi):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        out = np.empty_like(f)
+        res = C.c_double(0.0)
+        st = self.lib.hko_penalized_residual(k.ref, _ptr(f), C.c_double(pen_coeff), _ptr(out),
+                                             C.byref(res))
+        return out, st, res.value
+
+    def penalized_stage_solve(self, n, vmax, f_star, a, eps, pen_coeff=2 * np.pi):
+        f_star = np.ascontiguousarray(f_star, dtype=np.float64)
+        out = np.empty_like(f_star)
+        m = _Moments()
+        st = self.lib.hko_penalized_stage_solve(_ptr(f_star), C.c_double(a), C.c_double(eps),
+                                                C.c_double(pen_coeff), n, C.c_double(vmax),
+                                                _ptr(out), C.byref(m))
+        return out, st
+
+    def esbgk_stage_solve(self, n, vmax, f_star, a, eps, beta=-0.5, nu_coeff=0.5 * np.pi):
+        f_star = np.ascontiguousarray(f_star, dtype=np.float64)
+        out = np.empty_like(f_star)
+        m = _Moments()
+        fb = C.c_int(0)
+        st = self.lib.hko_esbgk_stage_solve(_ptr(f_star), C.c_double(a), C.c_double(eps),
+                                            C.c_double(beta), C.c_double(nu_coeff), n,
+                                            C.c_double(vmax), _ptr(out), C.byref(m), C.byref(fb))
+        return out, st, fb.value
+
+    def l1_distance(self, n, vmax, f):
+        out = C.c_double(0.0)
+        st = self.lib.hko_l1_distance(_ptr(np.ascontiguousarray(f)), n, C.c_double(vmax),
+                                      C.byref(out))
+        return st, out.value
+
+    def indicators(self, prim5x4, dx, dy, eps, mu0=1.0, kappa0=1.0, signed_sum=False):
+        p = np.ascontiguousarray(prim5x4, dtype=np.float64).reshape(5, 4)
+        d = np.zeros(11)
+        rows = [np.ascontiguousarray(p[i]) for i in range(5)]
+        self.lib.hko_spatial_derivatives(*[_ptr(r) for r in rows], C.c_double(dx), C.c_double(dy),
+                                         _ptr(d))
+        lam = np.zeros(3)
+        self.lib.hko_v_eps1_eigenvalues(_ptr(d), _ptr(rows[0]), C.c_double(eps), C.c_double(mu0),
+                                        C.c_double(kappa0), _ptr(lam))
+        lb = self.lib.hko_lambda_b(_ptr(d), _ptr(rows[0]), C.c_double(eps), int(signed_sum))
+        return d, lam, lb
+
+    def regime_update(self, r, lam=None, lambda_b=None, l1=None, eta0=1e-3, eta1=1e-2,
+                      delta0=1e-3):
+        lam_a = None if lam is None else np.ascontiguousarray(lam, dtype=np.float64)
+        lb = None if lambda_b is None else C.byref(C.c_double(lambda_b))
+        l1p = None if l1 is None else C.byref(C.c_double(l1))
+        out = C.c_int(-1)
+        st = self.lib.hko_regime_update(r, _ptr(lam_a) if lam_a is not None else None, lb, l1p,
+                                        C.c_double(eta0), C.c_double(eta1), C.c_double(delta0),
+                                        C.byref(out))
+        return st, out.value
+
+    def transport_rhs_periodic(self, f, nx, ny, n, vmax, dx, dy, eps_weno=1e-6):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        out = np.empty_like(f)
+        self.lib.hko_transport_rhs_periodic(_ptr(f), nx, ny, n, C.c_double(vmax), C.c_double(dx),
+                                            C.c_double(dy), C.c_double(eps_weno), _ptr(out))
+        return out
+
+    def penalized_imex_step(self, k: OracleKernel, f, nx, ny, dx, dy, dt, eps_cell,
+                            pen_coeff=2 * np.pi, eps_weno=1e-6):
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        e = np.ascontiguousarray(eps_cell, dtype=np.float64)
+        st = self.lib.hko_penalized_imex_step(_ptr(f), nx, ny, k.ref, C.c_double(dx),
+                                              C.c_double(dy), C.c_double(dt), _ptr(e),
+                                              C.c_double(pen_coeff), C.c_double(eps_weno), 1)
+        return f, st
+
+    def esbgk_imex_step(self, f, nx, ny, n, vmax, dx, dy, dt, eps_cell, beta=-0.5,
+                        nu_coeff=0.5 * np.pi, eps_weno=1e-6):
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        e = np.ascontiguousarray(eps_cell, dtype=np.float64)
+        st = self.lib.hko_esbgk_imex_step(_ptr(f), nx, ny, n, C.c_double(vmax), C.c_double(dx),
+                                          C.c_double(dy), C.c_double(dt), _ptr(e),
+                                          C.c_double(beta), C.c_double(nu_coeff),
+                                          C.c_double(eps_weno), 1)
+        return f, st
+
+
+class RefKernel:
+    def __init__(self, lib, n, vmax, a1, a2, r_phys):
+        self._lib = lib
+        st = C.c_int(0)
+        lib.href_kernel_create.restype = C.c_void_p
+        self.h = lib.href_kernel_create(n, C.c_double(vmax), a1, a2, C.c_double(r_phys),
+                                        C.byref(st))
+        self.status = st.value
+        self.n, self.a1, self.a2, self.vmax = n, a1, a2, vmax
+
+    def tables(self):
+        d, total = self.a1 * self.a2, self.n ** 3
+        a = np.empty((d, total)); ap = np.empty((d, total)); ld = np.empty(total)
+        self._lib.href_kernel_tables(C.c_void_p(self.h), _ptr(a), _ptr(ap), _ptr(ld))
+        sc = np.empty(4)
+        self._lib.href_kernel_scalars(C.c_void_p(self.h), _ptr(sc))
+        return a, ap, ld, sc
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.href_kernel_free(C.c_void_p(self.h))
+            self.h = None
+
+
+class RefLib:
+    """The reference's own code (oracle/_ref/libhykin_ref.so)."""
+
+    def __init__(self, path: str = REF_SO):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where /root/reference exists")
+        self.lib = C.CDLL(path)
+
+    def kernel(self, n, vmax, a1, a2, r_phys):
+        return RefKernel(self.lib, n, vmax, a1, a2, r_phys)
+
+    def collision_batch(self, k: RefKernel, f, nthreads=1):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        ncells = f.size // k.n ** 3
+        q = np.empty_like(f)
+        st = np.zeros(ncells, np.int32)
+        self.lib.href_collision_batch(C.c_void_p(k.h), _ptr(f), _ptr(q), C.c_int64(ncells),
+                                      nthreads, _ptr(st))
+        return q, st
+
+    def penalized_residual_batch(self, k: RefKernel, f, pen_coeff=2 * np.pi, nthreads=1):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        ncells = f.size // k.n ** 3
+        out = np.empty_like(f)
+        st = np.zeros(ncells, np.int32)
+        self.lib.href_penalized_residual_batch(C.c_void_p(k.h), _ptr(f), _ptr(out),
+                                               C.c_int64(ncells), C.c_double(pen_coeff), nthreads,
+                                               _ptr(st))
+        return out, st
+
+    def moments(self, n, vmax, f):
+        m = np.zeros(5)
+        st = self.lib.href_moments(n, C.c_double(vmax), _ptr(np.ascontiguousarray(f)), _ptr(m))
+        return st, tuple(m)
+
+    def second_moment(self, n, vmax, f):
+        s = np.zeros(9)
+        self.lib.href_second_moment(n, C.c_double(vmax), _ptr(np.ascontiguousarray(f)), _ptr(s))
+        return s.reshape(3, 3)
+
+    def maxwellian(self, n, vmax, mom5):
+        out = np.empty(n ** 3)
+        st = self.lib.href_maxwellian(n, C.c_double(vmax), _ptr(np.asarray(mom5, np.float64)),
+                                      _ptr(out))
+        return st, out
+
+    def realizability(self, n, vmax, f):
+        o = np.zeros(13)
+        st = self.lib.href_realizability(n, C.c_double(vmax), _ptr(np.ascontiguousarray(f)), _ptr(o))
+        return st, o[:9].reshape(3, 3), o[9:12], o[12]
+
+    def match_moments(self, n, vmax, f, rho, mom3, energy):
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        st = self.lib.href_match_moments(n, C.c_double(vmax), _ptr(f), C.c_double(rho),
+                                         _ptr(np.asarray(mom3, np.float64)), C.c_double(energy))
+        return st, f
+
+    def penalized_stage_solve(self, n, vmax, f_star, a, eps, pen_coeff=2 * np.pi):
+        f_star = np.ascontiguousarray(f_star, dtype=np.float64)
+        out = np.empty_like(f_star)
+        m = np.zeros(5)
+        st = self.lib.href_penalized_stage_solve(n, C.c_double(vmax), _ptr(f_star), C.c_double(a),
+                                                 C.c_double(eps), C.c_double(pen_coeff), _ptr(out),
+                                                 _ptr(m))
+        return out, st
+
+    def esbgk_stage_solve(self, n, vmax, f_star, a, eps, beta=-0.5, nu_coeff=0.5 * np.pi):
+        f_star = np.ascontiguousarray(f_star, dtype=np.float64)
+        out = np.empty_like(f_star)
+        m = np.zeros(5)
+        fb = C.c_int(0)
+        st = self.lib.href_esbgk_stage_solve(n, C.c_double(vmax), _ptr(f_star), C.c_double(a),
+                                             C.c_double(eps), C.c_double(beta),
+                                             C.c_double(nu_coeff), _ptr(out), _ptr(m), C.byref(fb))
+        return out, st, fb.value
+
+    def esbgk_stage_batch(self, n, vmax, f_star, a, eps_cell, beta=-0.5, nu_coeff=0.5 * np.pi,
+                          nthreads=1):
+        f_star = np.ascontiguousarray(f_star, dtype=np.float64)
+        ncells = f_star.size // n ** 3
+        out = np.empty_like(f_star)
+        st = np.zeros(ncells, np.int32)
+        fb = np.zeros(ncells, np.int32)
+        self.lib.href_esbgk_stage_batch(n, C.c_double(vmax), _ptr(f_star), _ptr(out),
+                                        C.c_int64(ncells), C.c_double(a),
+                                        _ptr(np.ascontiguousarray(eps_cell, dtype=np.float64)),
+                                        C.c_double(beta), C.c_double(nu_coeff), nthreads,
+                                        _ptr(st), _ptr(fb))
+        return out, st, fb
+
+    def l1_distance(self, n, vmax, f):
+        out = C.c_double(0.0)
+        st = self.lib.href_l1_distance(n, C.c_double(vmax), _ptr(np.ascontiguousarray(f)),
+                                       C.byref(out))
+        return st, out.value
+
+    def indicators(self, prim5x4, dx, dy, eps, mu0=1.0, kappa0=1.0, signed_sum=False):
+        lam = np.zeros(3)
+        lb = C.c_double(0.0)
+        self.lib.href_indicators(_ptr(np.ascontiguousarray(prim5x4, dtype=np.float64).ravel()),
+                                 C.c_double(dx), C.c_double(dy), C.c_double(eps), C.c_double(mu0),
+                                 C.c_double(kappa0), int(signed_sum), _ptr(lam), C.byref(lb))
+        return lam, lb.value
+
+    def regime_update(self, r, lam=None, lambda_b=None, l1=None, eta0=1e-3, eta1=1e-2,
+                      delta0=1e-3):
+        mask = (lam is not None) | ((lambda_b is not None) << 1) | ((l1 is not None) << 2)
+        lam_a = np.asarray(lam if lam is not None else [0, 0, 0], np.float64)
+        out = C.c_int(-1)
+        st = self.lib.href_regime_update(r, mask, _ptr(lam_a), C.c_double(lambda_b or 0.0),
+                                         C.c_double(l1 or 0.0), C.c_double(eta0), C.c_double(eta1),
+                                         C.c_double(delta0), C.byref(out))
+        return st, out.value
+
+    def transport_rhs_periodic(self, f, nx, ny, n, vmax, dx, dy, eps_weno=1e-6):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        out = np.empty_like(f)
+        self.lib.href_transport_rhs_periodic(n, C.c_double(vmax), _ptr(f), nx, ny, C.c_double(dx),
+                                             C.c_double(dy), C.c_double(eps_weno), _ptr(out))
+        return out
+
+    def penalized_imex_step(self, k: RefKernel, f, nx, ny, dx, dy, dt, eps_cell,
+                            pen_coeff=2 * np.pi, eps_weno=1e-6):
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        st = self.lib.href_penalized_imex_step(C.c_void_p(k.h), _ptr(f), nx, ny, C.c_double(dx),
+                                               C.c_double(dy), C.c_double(dt),
+                                               _ptr(np.ascontiguousarray(eps_cell, np.float64)),
+                                               C.c_double(pen_coeff), C.c_double(eps_weno))
+        return f, st
+
+    def esbgk_imex_step(self, f, nx, ny, n, vmax, dx, dy, dt, eps_cell, beta=-0.5,
+                        nu_coeff=0.5 * np.pi, eps_weno=1e-6):
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        st = self.lib.href_esbgk_imex_step(n, C.c_double(vmax), _ptr(f), nx, ny, C.c_double(dx),
+                                           C.c_double(dy), C.c_double(dt),
+                                           _ptr(np.ascontiguousarray(eps_cell, np.float64)),
+                                           C.c_double(beta), C.c_double(nu_coeff),
+                                           C.c_double(eps_weno))
+        return f, st

@@ -1,0 +1,434 @@
+// ref_driver.cpp — C entry points over the reference's OWN sources.
+//
+// TEST INFRASTRUCTURE ONLY.  Built by oracle/Makefile into
+// oracle/_ref/libhykin_ref.so from the unmodified reference .cpp files under
+// /root/reference/proj/core/src plus the FFTW3 / Eigen API shims in
+// oracle/shim (both libraries are absent from this image).  Used to pin the
+// oracle restatement (tests/) and as the CPU baseline (bench.py
+// --impl reference, cpu_baseline.kind = "reference").
+//
+// Error semantics: the reference throws numerical_consistency_error from
+// spectral_collision AFTER writing `out` (src/spectral.cpp:142-153); the
+// wrappers here catch and continue, recording a per-cell status.  Because a
+// throw inside penalized_residual aborts the rest of that function, the
+// residual and the IMEX step are restated around the catching wrapper, call
+// for call (src/boltzmann.cpp:9-27, 47-110), using the reference's own
+// building blocks.
+#include <algorithm>
+#include <array>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "hykin/boltzmann.hpp"
+#include "hykin/errors.hpp"
+#include "hykin/esbgk.hpp"
+#include "hykin/indicators.hpp"
+#include "hykin/moments.hpp"
+#include "hykin/regime.hpp"
+#include "hykin/spectral.hpp"
+#include "hykin/threading.hpp"
+#include "hykin/transport.hpp"
+
+using namespace hykin;
+
+namespace {
+
+int status_of(const std::exception_ptr& e) {
+    try {
+        std::rethrow_exception(e);
+    } catch (const aliasing_config_error&) {
+        return 2;
+    } catch (const config_error&) {
+        return 1;
+    } catch (const degenerate_state_error&) {
+        return 3;
+    } catch (const numerical_consistency_error&) {
+        return 4;
+    } catch (const contract_violation&) {
+        return 5;
+    } catch (const positivity_error&) {
+        return 8;
+    } catch (...) {
+        return 99;
+    }
+}
+
+struct RefKernel {
+    VelocityGrid vgrid;
+    SpectralKernel kernel;
+};
+
+// spectral_collision with catch-and-continue; out is complete before the throw.
+int collide(const RefKernel& h, std::span<const double> f, std::span<double> out) {
+    try {
+        spectral_collision(f, h.kernel, out);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+// src/boltzmann.cpp:9-27 around the catching wrapper.
+int residual(const RefKernel& h, std::span<const double> f, double pen_coeff,
+             std::span<double> out) {
+    const int cst = collide(h, f, out);
+    if (cst != 0 && cst != 4) return cst;
+    PenalizationRule rule;
+    rule.coeff = pen_coeff;
+    const Moments m = moments_of(f, h.vgrid);
+    const double beta = rule.rate(m.rho);
+    std::vector<double> eq(f.size());
+    maxwellian(m, h.vgrid, eq);
+    match_moments(eq, h.vgrid, m.rho, m.rho * m.u, m.energy());
+    for (size_t k = 0; k < out.size(); ++k) out[k] += beta * (f[k] - eq[k]);
+    remove_invariant_moments(out, eq, h.vgrid, m.u);
+    return cst;
+}
+
+} // namespace
+
+extern "C" {
+
+void* href_kernel_create(int n, double vmax, int a1, int a2, double r_phys, int* status) {
+    try {
+        auto* h = new RefKernel;
+        h->vgrid = make_velocity_grid(n, vmax);
+        h->kernel = precompute_kernel(h->vgrid, n, a1, a2, r_phys);
+        *status = 0;
+        return h;
+    } catch (...) {
+        *status = status_of(std::current_exception());
+        return nullptr;
+    }
+}
+
+void href_kernel_free(void* p) { delete static_cast<RefKernel*>(p); }
+
+void href_kernel_scalars(void* p, double* out4) {
+    const auto& k = static_cast<RefKernel*>(p)->kernel;
+    out4[0] = k.r;
+    out4[1] = k.jacobian;
+    out4[2] = k.weight;
+    out4[3] = k.r_phys;
+}
+
+void href_kernel_tables(void* p, double* alpha, double* alpha_prime, double* loss_diag) {
+    const auto& k = static_cast<RefKernel*>(p)->kernel;
+    const size_t total = size_t(k.modes());
+    for (int d = 0; d < k.dirs(); ++d) {
+        std::memcpy(alpha + d * total, k.alpha[d].data(), total * sizeof(double));
+        std::memcpy(alpha_prime + d * total, k.alpha_prime[d].data(), total * sizeof(double));
+    }
+    std::memcpy(loss_diag, k.loss_diag.data(), total * sizeof(double));
+}
+
+// Batched Q(f) over cells with the reference WorkerPool (inc/threading.hpp:25-56).
+int href_collision_batch(void* p, const double* f, double* q, int64_t ncells, int nthreads,
+                         int* st) {
+    const auto& h = *static_cast<RefKernel*>(p);
+    const int64_t nb = h.kernel.modes();
+    WorkerPool pool(nthreads);
+    pool.parallel_for(int(ncells), [&](int b, int e) {
+        for (int c = b; c < e; ++c) {
+            const int s = collide(h, std::span<const double>(f + c * nb, nb),
+                                  std::span<double>(q + c * nb, nb));
+            if (st) st[c] = s;
+        }
+    });
+    return 0;
+}
+
+int href_penalized_residual_batch(void* p, const double* f, double* out, int64_t ncells,
+                                  double pen_coeff, int nthreads, int* st) {
+    const auto& h = *static_cast<RefKernel*>(p);
+    const int64_t nb = h.kernel.modes();
+    WorkerPool pool(nthreads);
+    pool.parallel_for(int(ncells), [&](int b, int e) {
+        for (int c = b; c < e; ++c) {
+            int s;
+            try {
+                s = residual(h, std::span<const double>(f + c * nb, nb),
+                             pen_coeff, std::span<double>(out + c * nb, nb));
+            } catch (...) {
+                s = status_of(std::current_exception());
+            }
+            if (st) st[c] = s;
+        }
+    });
+    return 0;
+}
+
+int href_penalized_stage_solve(int n, double vmax, const double* f_star, double a, double eps,
+                               double pen_coeff, double* out, double* mom5) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        PenalizationRule rule;
+        rule.coeff = pen_coeff;
+        const int64_t nb = g.size();
+        const Moments m = penalized_stage_solve(std::span<const double>(f_star, nb), a, eps, rule,
+                                                g, std::span<double>(out, nb));
+        mom5[0] = m.rho; mom5[1] = m.u.x(); mom5[2] = m.u.y(); mom5[3] = m.u.z(); mom5[4] = m.T;
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_esbgk_stage_solve(int n, double vmax, const double* f_star, double a, double eps,
+                           double beta, double nu_coeff, double* out, double* mom5,
+                           int* fallback) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        EsbgkParams prm;
+        prm.beta = beta;
+        prm.nu_coeff = nu_coeff;
+        const int64_t nb = g.size();
+        const EsbgkStageInfo info = esbgk_stage_solve(std::span<const double>(f_star, nb), a, eps,
+                                                      prm, g, std::span<double>(out, nb));
+        mom5[0] = info.m.rho; mom5[1] = info.m.u.x(); mom5[2] = info.m.u.y();
+        mom5[3] = info.m.u.z(); mom5[4] = info.m.T;
+        *fallback = info.gaussian_fallback ? 1 : 0;
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_esbgk_stage_batch(int n, double vmax, const double* f_star, double* out,
+                           int64_t ncells, double a, const double* eps_cell, double beta,
+                           double nu_coeff, int nthreads, int* st, int* fallback) {
+    const VelocityGrid g = make_velocity_grid(n, vmax);
+    EsbgkParams prm;
+    prm.beta = beta;
+    prm.nu_coeff = nu_coeff;
+    const int64_t nb = g.size();
+    WorkerPool pool(nthreads);
+    pool.parallel_for(int(ncells), [&](int b, int e) {
+        for (int c = b; c < e; ++c) {
+            int s = 0, fb = 0;
+            try {
+                const EsbgkStageInfo info =
+                    esbgk_stage_solve(std::span<const double>(f_star + c * nb, nb), a,
+                                      eps_cell[c], prm, g, std::span<double>(out + c * nb, nb));
+                fb = info.gaussian_fallback ? 1 : 0;
+            } catch (...) {
+                s = status_of(std::current_exception());
+            }
+            if (st) st[c] = s;
+            if (fallback) fallback[c] = fb;
+        }
+    });
+    return 0;
+}
+
+int href_moments(int n, double vmax, const double* f, double* mom5) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        const Moments m = moments_of(std::span<const double>(f, g.size()), g);
+        mom5[0] = m.rho; mom5[1] = m.u.x(); mom5[2] = m.u.y(); mom5[3] = m.u.z(); mom5[4] = m.T;
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_second_moment(int n, double vmax, const double* f, double* s9) {
+    const VelocityGrid g = make_velocity_grid(n, vmax);
+    const Eigen::Matrix3d s = second_moment(std::span<const double>(f, g.size()), g);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) s9[3 * i + j] = s(i, j);
+    return 0;
+}
+
+int href_maxwellian(int n, double vmax, const double* mom5, double* out) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        Moments m;
+        m.rho = mom5[0];
+        m.u = Eigen::Vector3d(mom5[1], mom5[2], mom5[3]);
+        m.T = mom5[4];
+        maxwellian(m, g, std::span<double>(out, g.size()));
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_match_moments(int n, double vmax, double* f, double rho, const double* mom3,
+                       double energy) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        match_moments(std::span<double>(f, g.size()), g, rho,
+                      Eigen::Vector3d(mom3[0], mom3[1], mom3[2]), energy);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_realizability(int n, double vmax, const double* f, double* out13) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        const std::span<const double> fs(f, g.size());
+        const Moments m = moments_of(fs, g);
+        const RealizabilityMatrix r = realizability_matrix(fs, g, m);
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) out13[3 * i + j] = r.a_bar(i, j);
+        out13[9] = r.b_bar.x(); out13[10] = r.b_bar.y(); out13[11] = r.b_bar.z();
+        out13[12] = r.c_bar;
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+// Indicators for one cell: prims are (rho, ux, uy, T) of centre, x-, x+, y-, y+.
+int href_indicators(const double* prim5x4, double dx, double dy, double eps, double mu0,
+                    double kappa0, int signed_sum, double* lam3, double* lambda_b) {
+    auto P = [&](int k) { return PrimMoments{prim5x4[4 * k], prim5x4[4 * k + 1],
+                                             prim5x4[4 * k + 2], prim5x4[4 * k + 3]}; };
+    const DerivativeBundle d = spatial_derivatives(P(0), P(1), P(2), P(3), P(4), dx, dy);
+    TransportCoefficients tc;
+    tc.mu0 = mu0;
+    tc.kappa0 = kappa0;
+    const Eigenvalues lam = v_eps1_eigenvalues(d, P(0), eps, tc);
+    lam3[0] = lam.a; lam3[1] = lam.b; lam3[2] = lam.c;
+    *lambda_b = lambda_b_indicator(d, P(0), eps,
+                                   signed_sum ? LaplacianNorm::signed_sum : LaplacianNorm::squared_sum);
+    return 0;
+}
+
+int href_l1_distance(int n, double vmax, const double* f, double* out) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        *out = l1_distance_to_maxwellian(std::span<const double>(f, g.size()), g);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+// has_mask bit0 = eigenvalues, bit1 = lambda_B, bit2 = L1 distance present.
+int href_regime_update(int r, int has_mask, const double* lam3, double lambda_b, double l1,
+                       double eta0, double eta1, double delta0, int* out) {
+    try {
+        IndicatorSet ind;
+        if (has_mask & 1) ind.eigenvalues = Eigenvalues{lam3[0], lam3[1], lam3[2]};
+        if (has_mask & 2) ind.lambda_b = lambda_b;
+        if (has_mask & 4) ind.l1_distance = l1;
+        Thresholds th{eta0, eta1, delta0};
+        *out = regime_update(r, ind, th);
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_transport_rhs_periodic(int n, double vmax, const double* f, int nx, int ny, double dx,
+                                double dy, double eps_weno, double* out) {
+    const VelocityGrid g = make_velocity_grid(n, vmax);
+    const int64_t nb = g.size();
+    DistributionField in(nx * ny, int(nb)), res(nx * ny, int(nb));
+    for (int c = 0; c < nx * ny; ++c) {
+        auto b = in.ensure(c);
+        std::memcpy(b.data(), f + c * nb, nb * sizeof(double));
+    }
+    kinetic_transport_rhs_periodic(in, nx, ny, g, dx, dy, res, eps_weno);
+    for (int c = 0; c < nx * ny; ++c) std::memcpy(out + c * nb, res[c].data(), nb * sizeof(double));
+    return 0;
+}
+
+int href_esbgk_imex_step(int n, double vmax, double* f, int nx, int ny, double dx, double dy,
+                         double dt, const double* eps_cell, double beta, double nu_coeff,
+                         double eps_weno) {
+    try {
+        const VelocityGrid g = make_velocity_grid(n, vmax);
+        const int64_t nb = g.size();
+        DistributionField field(nx * ny, int(nb));
+        for (int c = 0; c < nx * ny; ++c)
+            std::memcpy(field.ensure(c).data(), f + c * nb, nb * sizeof(double));
+        EsbgkParams prm;
+        prm.beta = beta;
+        prm.nu_coeff = nu_coeff;
+        prm.eps_weno = eps_weno;
+        esbgk_imex_step(field, nx, ny, g, dx, dy, dt,
+                        std::span<const double>(eps_cell, size_t(nx) * ny), ImexTableau::pr222(),
+                        prm);
+        for (int c = 0; c < nx * ny; ++c) std::memcpy(f + c * nb, field[c].data(), nb * sizeof(double));
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+// src/boltzmann.cpp:47-110, restated call for call around the catching residual.
+int href_penalized_imex_step(void* p, double* f, int nx, int ny, double dx, double dy, double dt,
+                             const double* eps_cell, double pen_coeff, double eps_weno) {
+    const auto& h = *static_cast<RefKernel*>(p);
+    try {
+        const VelocityGrid& vgrid = h.vgrid;
+        const int cells = nx * ny;
+        const int nb = vgrid.size();
+        const ImexTableau tab = ImexTableau::pr222();
+        PenalizationRule rule;
+        rule.coeff = pen_coeff;
+        DistributionField fld(cells, nb), stage(cells, nb), q1(cells, nb), k1(cells, nb);
+        for (int c = 0; c < cells; ++c)
+            std::memcpy(fld.ensure(c).data(), f + int64_t(c) * nb, nb * sizeof(double));
+        std::vector<double> f_acc(nb), res(nb), q2(nb);
+        int first = 0;
+        for (int c = 0; c < cells; ++c) {
+            auto y = stage.ensure(c);
+            penalized_stage_solve(fld[c], tab.a_im[0][0] * dt, eps_cell[c], rule, vgrid, y);
+            auto kk = k1.ensure(c);
+            const double inv_a = 1.0 / tab.a_im[0][0];
+            for (int k = 0; k < nb; ++k) kk[k] = (y[k] - fld[c][k]) * inv_a;
+        }
+        kinetic_transport_rhs_periodic(stage, nx, ny, vgrid, dx, dy, q1, eps_weno);
+        for (int c = 0; c < cells; ++c) {
+            const int s = residual(h, stage[c], pen_coeff, res);
+            if (s && s != 4 && !first) first = s;
+            auto qc = q1[c];
+            const double inv_eps = 1.0 / eps_cell[c];
+            for (int k = 0; k < nb; ++k) qc[k] += res[k] * inv_eps;
+        }
+        for (int c = 0; c < cells; ++c) {
+            auto y = stage[c];
+            for (int k = 0; k < nb; ++k)
+                f_acc[k] = fld[c][k] + dt * tab.a_ex[1][0] * q1[c][k] + tab.a_im[1][0] * k1[c][k];
+            penalized_stage_solve(f_acc, tab.a_im[1][1] * dt, eps_cell[c], rule, vgrid, y);
+        }
+        std::array<const double*, 5> fx, fy;
+        auto wrap = [](int k, int n) { return (k % n + n) % n; };
+        const double inv_a2 = 1.0 / tab.a_im[1][1];
+        for (int c = 0; c < cells; ++c) {
+            const int i = c % nx, j = c / nx;
+            for (int pp = -2; pp <= 2; ++pp) {
+                fx[pp + 2] = stage[j * nx + wrap(i + pp, nx)].data();
+                fy[pp + 2] = stage[wrap(j + pp, ny) * nx + i].data();
+            }
+            kinetic_transport_rhs_cell(fx, fy, vgrid, dx, dy, eps_weno, q2.data());
+            const int s = residual(h, stage[c], pen_coeff, res);
+            if (s && s != 4 && !first) first = s;
+            const double inv_eps = 1.0 / eps_cell[c];
+            auto fc = fld[c];
+            for (int k = 0; k < nb; ++k) {
+                const double q2k = q2[k] + res[k] * inv_eps;
+                const double facc =
+                    fc[k] + dt * tab.a_ex[1][0] * q1[c][k] + tab.a_im[1][0] * k1[c][k];
+                const double k2 = (stage[c][k] - facc) * inv_a2;
+                fc[k] += dt * (tab.w_ex[0] * q1[c][k] + tab.w_ex[1] * q2k) +
+                         tab.w_im[0] * k1[c][k] + tab.w_im[1] * k2;
+            }
+        }
+        for (int c = 0; c < cells; ++c)
+            std::memcpy(f + int64_t(c) * nb, fld[c].data(), nb * sizeof(double));
+        return first;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+} // extern "C"

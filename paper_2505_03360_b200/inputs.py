@@ -1,0 +1,100 @@
+"""Seeded synthetic inputs with the shapes of BASELINE.json's configs.
+
+The reference ships no datasets or fixtures; every
+config's input is analytic.  These generators are the single source of the
+inputs used by the parity tests, the golden-vector script and bench.py.
+Master seed 2505033601, per-config stream = master XOR config id
+(SURVEY.md §8d "Synthetic inputs"); numpy PCG64 streams.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+MASTER_SEED = 2505033601
+VMAX = 8.0
+R_PHYS_MAX = 2.0 * VMAX / (3.0 + math.sqrt(2.0))  # aliasing bound, src/spectral.cpp:60
+
+
+def rng_for(config_id: int, salt: int = 0) -> np.random.Generator:
+    return np.random.default_rng(MASTER_SEED ^ config_id ^ (salt << 32))
+
+
+def nodes(n: int, vmax: float = VMAX) -> np.ndarray:
+    """Cell-centred velocity nodes v_k = -L + (k+1/2) dv (src/grid.cpp:18-33)."""
+    dv = 2.0 * vmax / n
+    return -vmax + (np.arange(n) + 0.5) * dv
+
+
+def maxwellian(n: int, rho: float, u, T: float, vmax: float = VMAX) -> np.ndarray:
+    v = nodes(n, vmax)
+    ex = np.exp(-((v - u[0]) ** 2) / (2 * T))
+    ey = np.exp(-((v - u[1]) ** 2) / (2 * T))
+    ez = np.exp(-((v - u[2]) ** 2) / (2 * T))
+    pref = rho / (2 * math.pi * T) ** 1.5
+    return (pref * ex[:, None, None] * ey[None, :, None] * ez[None, None, :]).ravel()
+
+
+def gaussian(n: int, rho: float, u, theta: np.ndarray, vmax: float = VMAX) -> np.ndarray:
+    v = nodes(n, vmax)
+    d = np.stack(np.meshgrid(v - u[0], v - u[1], v - u[2], indexing="ij"), axis=-1)
+    inv = np.linalg.inv(theta)
+    q = np.einsum("...i,ij,...j->...", d, inv, d)
+    pref = rho / math.sqrt((2 * math.pi) ** 3 * np.linalg.det(theta))
+    return (pref * np.exp(-0.5 * q)).ravel()
+
+
+def random_rotation(rng: np.random.Generator) -> np.ndarray:
+    q, r = np.linalg.qr(rng.normal(size=(3, 3)))
+    q = q * np.sign(np.diag(r))
+    if np.linalg.det(q) < 0:
+        q[:, 0] = -q[:, 0]
+    return q
+
+
+def config1_cells(ncells: int = 64, n: int = 16, seed_salt: int = 0) -> np.ndarray:
+    """Config 1: each cell a sum of two isotropic Maxwellians,
+    rho~U(0.5,1.5), u~U(-1,1)^3, T~U(0.5,2)."""
+    rng = rng_for(1, seed_salt)
+    out = np.empty((ncells, n ** 3))
+    for c in range(ncells):
+        f = np.zeros(n ** 3)
+        for _ in range(2):
+            rho = rng.uniform(0.5, 1.5)
+            u = rng.uniform(-1.0, 1.0, 3)
+            T = rng.uniform(0.5, 2.0)
+            f += maxwellian(n, rho, u, T)
+        out[c] = f
+    return out
+
+
+def config2_cells(ncells: int = 4096, n: int = 32, seed_salt: int = 0) -> np.ndarray:
+    """Config 2: 0.95 anisotropic Gaussian (rho~U(0.5,2), u~U(-.5,.5)^3,
+    Theta = R diag(U(0.5,2)^3) R^T) + 0.05 bimodal Maxwellian pair."""
+    rng = rng_for(2, seed_salt)
+    out = np.empty((ncells, n ** 3))
+    for c in range(ncells):
+        rho = rng.uniform(0.5, 2.0)
+        u = rng.uniform(-0.5, 0.5, 3)
+        lam = rng.uniform(0.5, 2.0, 3)
+        R = random_rotation(rng)
+        theta = R @ np.diag(lam) @ R.T
+        delta = rng.uniform(-1.0, 1.0, 3)
+        tbar = np.trace(theta) / 3.0
+        f = 0.95 * gaussian(n, rho, u, theta)
+        f += 0.05 * 0.5 * (maxwellian(n, rho, u + delta, tbar) + maxwellian(n, rho, u - delta, tbar))
+        out[c] = f
+    return out
+
+
+def config2_fast(ncells: int, n: int = 32, seed_salt: int = 0, distinct: int = 64) -> np.ndarray:
+    """Config-2 shaped batch built from `distinct` seeded cells tiled to
+    `ncells` (the bench's full 4096-cell batch without minutes of numpy
+    set-up).  Cell c is distinct cell c % distinct, plus a per-cell seeded
+    1e-3 relative amplitude scaling so no two cells are bitwise equal."""
+    base = config2_cells(distinct, n, seed_salt)
+    rng = rng_for(2, seed_salt + 1000)
+    idx = np.arange(ncells) % distinct
+    scale = 1.0 + 1e-3 * rng.uniform(-1.0, 1.0, ncells)
+    return base[idx] * scale[:, None]
