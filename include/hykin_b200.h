@@ -1,0 +1,124 @@
+/*
+ * hykin_b200.h — C-ABI of the B200-native fast-spectral collision path.
+ *
+ * Drop-in boundary for the data-parallel hot path of the reference solver
+ * (`hykin`, /root/reference/proj/core).  Each entry point names the
+ * reference interface it replaces (file:line, include/hykin = inc/).  The
+ * reference exposes C++ free functions taking std::span and throwing
+ * hykin::error subclasses; this ABI takes plain pointers + sizes and
+ * returns status codes that map 1:1 onto those exception classes
+ * (inc/errors.hpp:9-61).  INTEGRATION.md shows the C++ / ctypes bindings a
+ * maintainer adds on the reference side.
+ *
+ * Layout contract (replaces DistributionField, inc/fields.hpp:48-79): a
+ * field is ONE contiguous cell-major slab of doubles,
+ *     f[cell][k1][k2][k3],  cell = j*nx + i (inc/grid.hpp:30),
+ *     k index (k1*n + k2)*n + k3 (inc/grid.hpp:54), 64-bit offsets.
+ * `*_dev` pointers are CUDA device pointers; `*_host` pointers are host
+ * memory (pageable or pinned).  All device calls are ordered on the
+ * context's stream; only calls that return per-cell verdicts synchronise.
+ * fp64 throughout.  No CPU fallback: without a usable sm_100 device every
+ * call returns HK_CUDA.
+ */
+#ifndef HYKIN_B200_H
+#define HYKIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes == exception classes of inc/errors.hpp. */
+typedef enum {
+    HK_OK = 0,
+    HK_CONFIG = 1,                /* hykin::config_error */
+    HK_ALIASING = 2,              /* hykin::aliasing_config_error */
+    HK_DEGENERATE = 3,            /* hykin::degenerate_state_error */
+    HK_NUMERICAL_CONSISTENCY = 4, /* hykin::numerical_consistency_error */
+    HK_CONTRACT = 5,              /* hykin::contract_violation */
+    HK_CUDA = 6,                  /* device / runtime failure (no reference analogue) */
+    HK_NCCL = 7,                  /* collective failure (no reference analogue) */
+    HK_POSITIVITY = 8,            /* hykin::positivity_error */
+    HK_UNSUPPORTED = 9            /* size not implemented on this path */
+} hk_status;
+
+/* Per-cell verdict written by the collision kernels (device or host array). */
+typedef struct {
+    double max_re;    /* max_k |Re Q_k| */
+    double max_im;    /* max_k |Im Q_k| (exact path only; 0 on the fast path) */
+    double q_norm2;   /* sum_k (Re Q_k)^2 */
+    double nyq_bound; /* rigorous bound on ||dropped Nyquist term||_2 / ||Q||_2 (fast path) */
+    uint32_t flags;   /* HK_CELL_* bits */
+    uint32_t reserved;
+} hk_cell_status;
+
+#define HK_CELL_EXACT 1u            /* evaluated on the exact (full complex) path */
+#define HK_CELL_RESIDUE 2u          /* max|Im| > 1e-10 max|Re| (reference would throw, src/spectral.cpp:150) */
+#define HK_CELL_GUARD_REROUTED 4u   /* fast path rejected by the Nyquist guard, recomputed exactly */
+
+/* hk_collision_batch flags */
+#define HK_COLL_EXACT 1u  /* every cell on the exact path (complex ga, gb per direction) */
+#define HK_COLL_STRICT 2u /* exact + reference throw semantics: HK_NUMERICAL_CONSISTENCY, lowest cell */
+#define HK_COLL_NOGUARD 4u /* fast path without the Nyquist guard (benchmark/diagnostic only) */
+
+typedef struct hk_ctx_s* hk_ctx;
+typedef struct hk_kernel_s* hk_kernel;
+
+/* ---- context: one per (host thread, GPU) --------------------------------- */
+int hk_ctx_create(int device, hk_ctx* out);
+int hk_ctx_destroy(hk_ctx ctx);
+/* stream: a cudaStream_t (NULL = legacy default stream). */
+int hk_ctx_set_stream(hk_ctx ctx, void* stream);
+/* Last error message and failing cell index (-1 if none). */
+int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len);
+/* Number of this library's kernel launches since context creation. */
+int64_t hk_launch_count(hk_ctx ctx);
+
+/* ---- spectral kernel ------------------------------------------------------
+ * Replaces SpectralKernel precompute_kernel(const VelocityGrid&, int n, int a1,
+ * int a2, double r_phys)   (inc/spectral.hpp:49, src/spectral.cpp:53-112).
+ * Weight tables are evaluated on the device from the closed forms of the
+ * radial/planar transforms (they agree with the GK15 quadrature of
+ * src/quadrature.cpp to ~1e-14 relative).  Same validation and status:
+ * HK_CONFIG (a1,a2 < 1, n < 2, vmax <= 0, r_phys <= 0), HK_ALIASING
+ * (r_phys > 2 vmax/(3+sqrt 2)), HK_UNSUPPORTED (n not in {16, 32}). */
+int hk_kernel_create(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys,
+                     hk_kernel* out);
+/* Same, but takes the reference's own tables verbatim (SpectralKernel::alpha,
+ * alpha_prime [a1*a2][n^3], loss_diag [n^3], inc/spectral.hpp:25-27). */
+int hk_kernel_create_from_tables(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys,
+                                 const double* alpha_host, const double* alpha_prime_host,
+                                 const double* loss_diag_host, hk_kernel* out);
+int hk_kernel_destroy(hk_kernel k);
+/* out[0..5] = r, jacobian, weight, r_phys, distinct directions, a2 multiplicity of p=0 */
+int hk_kernel_info(hk_kernel k, double* out6);
+
+/* ---- collision operator ---------------------------------------------------
+ * Replaces void spectral_collision(std::span<const double> f, const
+ * SpectralKernel&, std::span<double> out)   (inc/spectral.hpp:56,
+ * src/spectral.cpp:114-154), batched over ncells cells.  q_dev receives
+ * Re Q per cell.  st_dev (nullable) receives one hk_cell_status per cell.
+ * Default: fast path (Hermitian-packed, one complex 3-D transform per
+ * direction) with a rigorous per-cell Nyquist guard that reroutes any cell
+ * whose dropped term could exceed 1e-11 relative L2 to the exact path.
+ * HK_COLL_STRICT returns HK_NUMERICAL_CONSISTENCY (hk_last_error gives the
+ * lowest failing cell) when any cell's residue exceeds 1e-10, after writing
+ * q_dev for every cell — the reference's throw-after-write behaviour. */
+int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_dev,
+                       int64_t ncells, uint32_t flags, hk_cell_status* st_dev);
+/* End-to-end variant over host buffers: H2D of f, collision, D2H of q (and
+ * st_host if non-NULL), synchronous.  This is the call the reference-facing
+ * C++ shim (include/hykin_b200.hpp) makes for spectral_collision. */
+int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host,
+                            int64_t ncells, uint32_t flags, hk_cell_status* st_host);
+
+/* ---- diagnostics ---------------------------------------------------------- */
+/* fp64 FMA peak of this device (DFMA microbenchmark), TFLOP/s. */
+double hk_measure_fp64_peak(hk_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,91 @@
+"""ctypes binding of the C-ABI in include/hykin_b200.h.
+
+The product path: every call here lands in paper_2505_03360_b200/lib/
+libhykin_b200.so (hand-written sm_100a CUDA).  There is no CPU fallback —
+if the library or a usable B200 is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libhykin_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "hykin_b200.h")
+
+HK_OK = 0
+HK_CONFIG = 1
+HK_ALIASING = 2
+HK_DEGENERATE = 3
+HK_NUMERICAL_CONSISTENCY = 4
+HK_CONTRACT = 5
+HK_CUDA = 6
+HK_NCCL = 7
+HK_POSITIVITY = 8
+HK_UNSUPPORTED = 9
+
+HK_CELL_EXACT = 1
+HK_CELL_RESIDUE = 2
+HK_CELL_GUARD_REROUTED = 4
+
+HK_COLL_EXACT = 1
+HK_COLL_STRICT = 2
+HK_COLL_NOGUARD = 4
+
+
+class CellStatus(C.Structure):
+    _fields_ = [
+        ("max_re", C.c_double),
+        ("max_im", C.c_double),
+        ("q_norm2", C.c_double),
+        ("nyq_bound", C.c_double),
+        ("flags", C.c_uint32),
+        ("reserved", C.c_uint32),
+    ]
+
+
+CELL_STATUS_BYTES = C.sizeof(CellStatus)  # 40
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libhykin_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `make -C paper_2505_03360_b200/csrc` "
+            "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, u32, dbl = C.c_void_p, C.c_int64, C.c_uint32, C.c_double
+    sig = {
+        "hk_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
+        "hk_ctx_destroy": (C.c_int, [vp]),
+        "hk_ctx_set_stream": (C.c_int, [vp, vp]),
+        "hk_last_error": (C.c_int, [vp, C.POINTER(i64), C.c_char_p, C.c_size_t]),
+        "hk_launch_count": (i64, [vp]),
+        "hk_kernel_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dbl, dbl, C.POINTER(vp)]),
+        "hk_kernel_create_from_tables": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dbl, dbl, vp, vp, vp,
+                                                   C.POINTER(vp)]),
+        "hk_kernel_destroy": (C.c_int, [vp]),
+        "hk_kernel_info": (C.c_int, [vp, C.POINTER(C.c_double)]),
+        "hk_collision_batch": (C.c_int, [vp, vp, vp, vp, i64, u32, vp]),
+        "hk_collision_batch_host": (C.c_int, [vp, vp, vp, vp, i64, u32, vp]),
+        "hk_measure_fp64_peak": (dbl, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols_from_header(path: str = HEADER) -> list[str]:
+    """Function names declared in include/hykin_b200.h."""
+    import re
+
+    text = open(path).read()
+    return sorted(set(re.findall(r"\b(hk_[a-z0-9_]+)\s*\(", text)))

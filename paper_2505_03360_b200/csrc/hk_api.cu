@@ -1,0 +1,271 @@
+// hk_api.cu — the C-ABI (include/hykin_b200.h): contexts, kernel objects,
+// dispatch.  No CPU fallback: every entry point fails with HK_CUDA when no
+// device is usable.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "hk_common.cuh"
+#include "hk_internal.h"
+
+namespace hk {
+
+int fail(hk_ctx ctx, int status, const std::string& msg, int64_t cell) {
+    if (ctx) {
+        ctx->err = msg;
+        ctx->err_cell = cell;
+    }
+    return status;
+}
+
+int check_cuda(hk_ctx ctx, cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return HK_OK;
+    return fail(ctx, HK_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int ensure_scratch(hk_ctx ctx, size_t bytes) {
+    if (bytes <= ctx->scratch_bytes) return HK_OK;
+    if (ctx->scratch) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(ctx->scratch);
+        ctx->scratch = nullptr;
+        ctx->scratch_bytes = 0;
+    }
+    int st = check_cuda(ctx, cudaMalloc(&ctx->scratch, bytes), "scratch alloc");
+    if (!st) ctx->scratch_bytes = bytes;
+    return st;
+}
+
+}  // namespace hk
+
+using namespace hk;
+
+extern "C" {
+
+int hk_ctx_create(int device, hk_ctx* out) {
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return HK_CUDA;
+    if (device < 0 || device >= ndev) return HK_CONFIG;
+    if (cudaSetDevice(device) != cudaSuccess) return HK_CUDA;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return HK_CUDA;
+    if (prop.major < 10) return HK_CUDA;  // sm_100a code only
+    auto* c = new hk_ctx_s;
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    *out = c;
+    return HK_OK;
+}
+
+int hk_ctx_destroy(hk_ctx ctx) {
+    if (!ctx) return HK_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    else cudaDeviceSynchronize();
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    delete ctx;
+    return HK_OK;
+}
+
+int hk_ctx_set_stream(hk_ctx ctx, void* stream) {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+    return HK_OK;
+}
+
+int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len) {
+    if (cell) *cell = ctx->err_cell;
+    if (msg && msg_len) {
+        std::strncpy(msg, ctx->err.c_str(), msg_len - 1);
+        msg[msg_len - 1] = 0;
+    }
+    return HK_OK;
+}
+
+int64_t hk_launch_count(hk_ctx ctx) { return ctx->launches; }
+
+static int kernel_common(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys,
+                         hk_kernel* out) {
+    *out = nullptr;
+    // Validation order of src/grid.cpp:19-22 and src/spectral.cpp:55-66.
+    if (n < 2) return fail(ctx, HK_CONFIG, "velocity grid needs at least 2 nodes per axis");
+    if (!(vmax > 0.0)) return fail(ctx, HK_CONFIG, "velocity cutoff must be positive");
+    if (a1 < 1 || a2 < 1) return fail(ctx, HK_CONFIG, "spherical quadrature sizes must be positive");
+    const double r_max = 2.0 * vmax / (3.0 + std::sqrt(2.0));
+    if (r_phys > r_max * (1.0 + 1e-12))
+        return fail(ctx, HK_ALIASING, "support radius exceeds the aliasing bound 2L/(3+sqrt(2))");
+    if (r_phys <= 0.0) return fail(ctx, HK_CONFIG, "support radius must be positive");
+    if (n != 16 && n != 32) return fail(ctx, HK_UNSUPPORTED, "device collision path supports n = 16, 32");
+    auto* k = new hk_kernel_s;
+    k->ctx = ctx;
+    k->n = n;
+    k->a1 = a1;
+    k->a2 = a2;
+    k->vmax = vmax;
+    k->r_phys = r_phys;
+    k->r = r_phys * M_PI / vmax;
+    const double s = vmax / M_PI;
+    k->jac = s * s * s * s;
+    k->weight = M_PI * M_PI / (a1 * a2);
+    k->md = (a1 - 1) * a2 + 1;
+    k->mult0 = a2;
+    *out = k;
+    return HK_OK;
+}
+
+static int finish_kernel(hk_ctx ctx, hk_kernel k, double* ra, double* rap, double* rl) {
+    int st = build_kernel_tables(ctx, k, ra, rap, rl);
+    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "kernel tables");
+    cudaFree(ra);
+    cudaFree(rap);
+    cudaFree(rl);
+    if (st) {
+        hk_kernel_destroy(k);
+        return st;
+    }
+    return HK_OK;
+}
+
+int hk_kernel_create(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys, hk_kernel* out) {
+    hk_kernel k;
+    int st = kernel_common(ctx, n, a1, a2, vmax, r_phys, &k);
+    if (st) return st;
+    cudaSetDevice(ctx->device);
+    const size_t total = size_t(n) * n * n, dirs = size_t(a1) * a2;
+    double *ra = nullptr, *rap = nullptr, *rl = nullptr;
+    if ((st = check_cuda(ctx, cudaMalloc(&ra, sizeof(double) * total * dirs), "alloc")) ||
+        (st = check_cuda(ctx, cudaMalloc(&rap, sizeof(double) * total * dirs), "alloc")) ||
+        (st = check_cuda(ctx, cudaMalloc(&rl, sizeof(double) * total), "alloc")) ||
+        (st = closed_form_raw_tables(ctx, k, ra, rap, rl))) {
+        cudaFree(ra);
+        cudaFree(rap);
+        cudaFree(rl);
+        hk_kernel_destroy(k);
+        return st;
+    }
+    st = finish_kernel(ctx, k, ra, rap, rl);
+    *out = st ? nullptr : k;
+    return st;
+}
+
+int hk_kernel_create_from_tables(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys,
+                                 const double* alpha_host, const double* alpha_prime_host,
+                                 const double* loss_diag_host, hk_kernel* out) {
+    hk_kernel k;
+    int st = kernel_common(ctx, n, a1, a2, vmax, r_phys, &k);
+    if (st) return st;
+    cudaSetDevice(ctx->device);
+    const size_t total = size_t(n) * n * n, dirs = size_t(a1) * a2;
+    double *ra = nullptr, *rap = nullptr, *rl = nullptr;
+    if ((st = check_cuda(ctx, cudaMalloc(&ra, sizeof(double) * total * dirs), "alloc")) ||
+        (st = check_cuda(ctx, cudaMalloc(&rap, sizeof(double) * total * dirs), "alloc")) ||
+        (st = check_cuda(ctx, cudaMalloc(&rl, sizeof(double) * total), "alloc")) ||
+        (st = check_cuda(ctx, cudaMemcpy(ra, alpha_host, sizeof(double) * total * dirs, cudaMemcpyHostToDevice), "H2D")) ||
+        (st = check_cuda(ctx, cudaMemcpy(rap, alpha_prime_host, sizeof(double) * total * dirs, cudaMemcpyHostToDevice), "H2D")) ||
+        (st = check_cuda(ctx, cudaMemcpy(rl, loss_diag_host, sizeof(double) * total, cudaMemcpyHostToDevice), "H2D"))) {
+        cudaFree(ra);
+        cudaFree(rap);
+        cudaFree(rl);
+        hk_kernel_destroy(k);
+        return st;
+    }
+    st = finish_kernel(ctx, k, ra, rap, rl);
+    *out = st ? nullptr : k;
+    return st;
+}
+
+int hk_kernel_destroy(hk_kernel k) {
+    if (!k) return HK_OK;
+    cudaFree(k->alpha);
+    cudaFree(k->alpha_p);
+    cudaFree(k->loss);
+    cudaFree(k->wfast);
+    cudaFree(k->abs_a);
+    cudaFree(k->abs_ap);
+    delete k;
+    return HK_OK;
+}
+
+int hk_kernel_info(hk_kernel k, double* out6) {
+    out6[0] = k->r;
+    out6[1] = k->jac;
+    out6[2] = k->weight;
+    out6[3] = k->r_phys;
+    out6[4] = k->md;
+    out6[5] = k->mult0;
+    return HK_OK;
+}
+
+static int strict_verdict(hk_ctx ctx, const hk_cell_status* st_host, int64_t ncells) {
+    for (int64_t c = 0; c < ncells; ++c)
+        if (st_host[c].flags & HK_CELL_RESIDUE) {
+            char buf[160];
+            std::snprintf(buf, sizeof buf,
+                          "spectral collision imaginary residue %g exceeds 1e-10 of max |Q| = %g",
+                          st_host[c].max_im, st_host[c].max_re);
+            return fail(ctx, HK_NUMERICAL_CONSISTENCY, buf, c);
+        }
+    return HK_OK;
+}
+
+int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_dev, int64_t ncells,
+                       uint32_t flags, hk_cell_status* st_dev) {
+    if (!ctx || !k) return HK_CONTRACT;
+    if (ncells < 0) return fail(ctx, HK_CONTRACT, "negative cell count");
+    cudaSetDevice(ctx->device);
+    ctx->err_cell = -1;
+    int st = collision_launch(ctx, k, f_dev, q_dev, ncells, flags, st_dev);
+    if (st) return st;
+    if (flags & HK_COLL_STRICT) {
+        // The verdict needs the per-cell residues on the host: synchronise.
+        hk_cell_status* dev = st_dev ? st_dev : static_cast<hk_cell_status*>(ctx->scratch);
+        hk_cell_status* h = new hk_cell_status[ncells > 0 ? ncells : 1];
+        st = check_cuda(ctx, cudaMemcpyAsync(h, dev, sizeof(hk_cell_status) * ncells, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
+        if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+        if (!st) st = strict_verdict(ctx, h, ncells);
+        delete[] h;
+        return st;
+    }
+    return check_cuda(ctx, cudaGetLastError(), "collision");
+}
+
+int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host,
+                            int64_t ncells, uint32_t flags, hk_cell_status* st_host) {
+    if (!ctx || !k) return HK_CONTRACT;
+    cudaSetDevice(ctx->device);
+    const size_t nb = size_t(k->n) * k->n * k->n;
+    const size_t bytes = sizeof(double) * nb * ncells;
+    // device buffers live after the scratch used by the collision launch: allocate separately
+    double *f_dev = nullptr, *q_dev = nullptr;
+    hk_cell_status* st_dev = nullptr;
+    int st;
+    if ((st = check_cuda(ctx, cudaMallocAsync(&f_dev, bytes, ctx->stream), "alloc f")) ||
+        (st = check_cuda(ctx, cudaMallocAsync(&q_dev, bytes, ctx->stream), "alloc q")) ||
+        (st = check_cuda(ctx, cudaMallocAsync(&st_dev, sizeof(hk_cell_status) * (ncells + 1), ctx->stream), "alloc st")))
+        return st;
+    st = check_cuda(ctx, cudaMemcpyAsync(f_dev, f_host, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D f");
+    const uint32_t dflags = (flags & HK_COLL_STRICT) ? ((flags & ~HK_COLL_STRICT) | HK_COLL_EXACT) : flags;
+    if (!st) st = hk_collision_batch(ctx, k, f_dev, q_dev, ncells, dflags, st_dev);
+    if (!st) st = check_cuda(ctx, cudaMemcpyAsync(q_host, q_dev, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H q");
+    hk_cell_status* sh = st_host;
+    std::unique_ptr<hk_cell_status[]> tmp;
+    if (!sh && (flags & HK_COLL_STRICT)) {
+        tmp.reset(new hk_cell_status[ncells > 0 ? ncells : 1]);
+        sh = tmp.get();
+    }
+    if (!st && sh)
+        st = check_cuda(ctx, cudaMemcpyAsync(sh, st_dev, sizeof(hk_cell_status) * ncells, cudaMemcpyDeviceToHost, ctx->stream), "D2H st");
+    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+    cudaFreeAsync(f_dev, ctx->stream);
+    cudaFreeAsync(q_dev, ctx->stream);
+    cudaFreeAsync(st_dev, ctx->stream);
+    if (!st && (flags & HK_COLL_STRICT)) st = strict_verdict(ctx, sh, ncells);
+    return st;
+}
+
+double hk_measure_fp64_peak(hk_ctx ctx) { return fp64_peak(ctx); }
+
+}  // extern "C"

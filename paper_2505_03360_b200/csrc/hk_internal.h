@@ -1,0 +1,66 @@
+// hk_internal.h — host-side objects behind the C-ABI handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+
+#include "../../include/hykin_b200.h"
+
+struct hk_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+    int64_t err_cell = -1;
+    std::string err;
+    int sm_count = 0;
+    // scratch (grown on demand, never shrunk)
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // pinned staging for the host entry points
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    std::map<int, int> max_clusters;  // key: kernel variant id
+};
+
+// Device-resident SpectralKernel (inc/spectral.hpp:15-33), re-laid out for
+// coalesced loads by the collision kernels: tables are [entry][i1][i3][i2]
+// with entry = distinct direction (the p = 0 row of src/spectral.cpp:83-90
+// repeats e = (0,0,1) a2 times and is stored once with multiplicity a2).
+struct hk_kernel_s {
+    hk_ctx ctx = nullptr;
+    int n = 0, a1 = 0, a2 = 0, md = 0;
+    double vmax = 0, r_phys = 0, r = 0, jac = 0, weight = 0, mult0 = 1;
+    double* alpha = nullptr;    // [md][n^3] exact radial weights
+    double* alpha_p = nullptr;  // [md][n^3] exact planar weights
+    double* loss = nullptr;     // [n^3] loss_diag (reference summation order)
+    double2* wfast = nullptr;   // [md+1][n^3] Hermitian-symmetrised (alpha_s, alpha'_s); entry md = (loss_s, 0)
+    double* abs_a = nullptr;    // [md][3][n][n] |antisymmetric alpha| on the Nyquist planes
+    double* abs_ap = nullptr;   // [md][3][n][n]
+    double absmax = 0;          // max over the abs tables (diagnostic)
+};
+
+namespace hk {
+
+// Sets ctx->err and returns the status.
+int fail(hk_ctx ctx, int status, const std::string& msg, int64_t cell = -1);
+int check_cuda(hk_ctx ctx, cudaError_t e, const char* what);
+// Ensures ctx->scratch holds >= bytes.
+int ensure_scratch(hk_ctx ctx, size_t bytes);
+
+// hk_weights.cu
+int build_kernel_tables(hk_ctx ctx, hk_kernel k, const double* raw_alpha_dev,
+                        const double* raw_alpha_p_dev, const double* raw_loss_dev);
+int closed_form_raw_tables(hk_ctx ctx, hk_kernel k, double* raw_alpha_dev,
+                           double* raw_alpha_p_dev, double* raw_loss_dev);
+
+// hk_collision.cu
+int collision_launch(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells,
+                     uint32_t flags, hk_cell_status* st);
+
+// hk_peak.cu
+double fp64_peak(hk_ctx ctx);
+
+}  // namespace hk

@@ -1,0 +1,122 @@
+"""GPU parity of the batched collision operator against the CPU oracle.
+
+Bar (BASELINE.json north_star): Q within 1e-10 relative L2 of the reference
+CPU path on the same seeded inputs.  The oracle is the C restatement pinned
+bitwise to the reference's own sources (tests/test_oracle_vs_ref.py)."""
+import numpy as np
+import pytest
+
+from paper_2505_03360_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def n16(oracle, hk):
+    n, a1, a2 = 16, 4, 8
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    ko = oracle.kernel(n, inputs.VMAX, a1, a2, inputs.R_PHYS_MAX, closed_form=False)
+    f = inputs.config1_cells(6, n)
+    q_ref, st_ref, res_ref = oracle.collision_batch(ko, f)
+    return dict(vg=vg, kern=kern, ko=ko, f=f, q_ref=q_ref, st_ref=st_ref, res_ref=res_ref)
+
+
+def test_n16_exact_matches_oracle(n16, hk):
+    import torch
+    f = torch.from_numpy(n16["f"]).cuda()
+    q, st = hk.spectral_collision(f, n16["kern"], exact=True, return_status=True)
+    q = q.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], n16["q_ref"][c]) < TOL, c
+    assert np.all(st["flags"] & 1)
+    # residue ratio reproduces the reference's verdict (src/spectral.cpp:150)
+    res = st["max_im"] / np.maximum(st["max_re"], 1e-300)
+    np.testing.assert_allclose(res, n16["res_ref"], rtol=1e-6)
+    assert np.array_equal((st["flags"] & 2) != 0, n16["st_ref"] == 4)
+
+
+def test_n16_default_path_reroutes_and_matches(n16, hk):
+    import torch
+    f = torch.from_numpy(n16["f"]).cuda()
+    q, st = hk.spectral_collision(f, n16["kern"], return_status=True)
+    q = q.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], n16["q_ref"][c]) < TOL, c
+    # at N=16 the Nyquist term matters: the guard must reroute
+    assert np.all(st["flags"] & 4)
+
+
+def test_n16_fast_noguard_is_not_exact(n16, hk):
+    import torch
+    f = torch.from_numpy(n16["f"]).cuda()
+    q = hk.spectral_collision(f, n16["kern"], guard=False).cpu().numpy()
+    errs = [rel_l2(q[c], n16["q_ref"][c]) for c in range(len(f))]
+    assert max(errs) > 1e-9  # proves the guard is load-bearing at N=16
+    assert max(errs) < 1e-3
+
+
+def test_n16_strict_raises_lowest_cell(n16, hk):
+    import torch
+    f = torch.from_numpy(n16["f"]).cuda()
+    with pytest.raises(hk.numerical_consistency_error) as ei:
+        hk.spectral_collision(f, n16["kern"], strict=True)
+    first = int(np.argmax(n16["st_ref"] == 4))
+    assert ei.value.cell == first
+
+
+def test_n16_reference_tables(n16, hk, oracle):
+    """Kernel built from the reference's GK15 tables (bitwise the reference's)."""
+    import torch
+    ko = n16["ko"]
+    kern = hk.precompute_kernel_from_tables(n16["vg"], 16, 4, 8, inputs.R_PHYS_MAX,
+                                            ko.alpha, ko.alpha_prime, ko.loss_diag)
+    f = torch.from_numpy(n16["f"]).cuda()
+    q = hk.spectral_collision(f, kern, exact=True).cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], n16["q_ref"][c]) < 1e-12, c
+
+
+@pytest.fixture(scope="module")
+def n32(oracle, hk):
+    n, a1, a2 = 32, 8, 8
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    ko = oracle.kernel(n, inputs.VMAX, a1, a2, inputs.R_PHYS_MAX, closed_form=True)
+    f = inputs.config2_cells(3, n)
+    q_ref, st_ref, res_ref = oracle.collision_batch(ko, f)
+    return dict(vg=vg, kern=kern, f=f, q_ref=q_ref, st_ref=st_ref, res_ref=res_ref)
+
+
+def test_n32_fast_matches_oracle(n32, hk):
+    import torch
+    f = torch.from_numpy(n32["f"]).cuda()
+    q, st = hk.spectral_collision(f, n32["kern"], return_status=True)
+    q = q.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], n32["q_ref"][c]) < TOL, c
+    assert np.all(st["nyq_bound"] < 1e-11)
+    assert not np.any(st["flags"] & 4)
+
+
+def test_n32_exact_matches_oracle(n32, hk):
+    import torch
+    f = torch.from_numpy(n32["f"]).cuda()
+    q, st = hk.spectral_collision(f, n32["kern"], exact=True, return_status=True)
+    q = q.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], n32["q_ref"][c]) < TOL, c
+    res = st["max_im"] / np.maximum(st["max_re"], 1e-300)
+    np.testing.assert_allclose(res, n32["res_ref"], rtol=1e-3, atol=1e-13)
+
+
+def test_n32_host_path(n32, hk):
+    q = hk.spectral_collision(np.ascontiguousarray(n32["f"]), n32["kern"])
+    for c in range(len(q)):
+        assert rel_l2(q[c], n32["q_ref"][c]) < TOL, c
