@@ -75,6 +75,11 @@ int hk_ctx_set_stream(hk_ctx ctx, void* stream);
 int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len);
 /* Number of this library's kernel launches since context creation. */
 int64_t hk_launch_count(hk_ctx ctx);
+/* CUDA-event timing of the library's kernels on the context stream (for the
+ * roofline in bench.py).  Enabling clears previous records.  tag 0 = main
+ * collision kernel, 1 = Nyquist guard, 2 = exact reroute. */
+int hk_ctx_set_timing(hk_ctx ctx, int on);
+int hk_ctx_timing_report(hk_ctx ctx, int tag, double* total_ms, int64_t* launches);
 
 /* ---- spectral kernel ------------------------------------------------------
  * Replaces SpectralKernel precompute_kernel(const VelocityGrid&, int n, int a1,

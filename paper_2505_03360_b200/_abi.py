@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libhykin_b200.so")
+LIB_PATH = os.environ.get("HK_LIB") or os.path.join(HERE, "lib", "libhykin_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "hykin_b200.h")
 
 HK_OK = 0
@@ -66,6 +66,8 @@ def lib() -> C.CDLL:
         "hk_ctx_set_stream": (C.c_int, [vp, vp]),
         "hk_last_error": (C.c_int, [vp, C.POINTER(i64), C.c_char_p, C.c_size_t]),
         "hk_launch_count": (i64, [vp]),
+        "hk_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+        "hk_ctx_timing_report": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(i64)]),
         "hk_kernel_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dbl, dbl, C.POINTER(vp)]),
         "hk_kernel_create_from_tables": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dbl, dbl, vp, vp, vp,
                                                    C.POINTER(vp)]),

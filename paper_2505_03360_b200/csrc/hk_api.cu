@@ -38,6 +38,20 @@ int ensure_scratch(hk_ctx ctx, size_t bytes) {
     return st;
 }
 
+void timing_begin(hk_ctx ctx, int tag) {
+    if (!ctx->timing) return;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, ctx->stream);
+    ctx->events.push_back({tag, {a, b}});
+}
+
+void timing_end(hk_ctx ctx) {
+    if (!ctx->timing || ctx->events.empty()) return;
+    cudaEventRecord(ctx->events.back().second.second, ctx->stream);
+}
+
 }  // namespace hk
 
 using namespace hk;
@@ -86,6 +100,40 @@ int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len) {
 }
 
 int64_t hk_launch_count(hk_ctx ctx) { return ctx->launches; }
+
+static void clear_events(hk_ctx ctx) {
+    for (auto& e : ctx->events) {
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    ctx->events.clear();
+}
+
+int hk_ctx_set_timing(hk_ctx ctx, int on) {
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    clear_events(ctx);
+    ctx->timing = on != 0;
+    return HK_OK;
+}
+
+int hk_ctx_timing_report(hk_ctx ctx, int tag, double* total_ms, int64_t* launches) {
+    cudaSetDevice(ctx->device);
+    double ms = 0.0;
+    int64_t n = 0;
+    for (auto& e : ctx->events) {
+        if (e.first != tag) continue;
+        cudaEventSynchronize(e.second.second);
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, e.second.first, e.second.second) == cudaSuccess) {
+            ms += t;
+            ++n;
+        }
+    }
+    *total_ms = ms;
+    *launches = n;
+    return HK_OK;
+}
 
 static int kernel_common(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys,
                          hk_kernel* out) {

@@ -27,11 +27,16 @@
 // Phase factors of src/fft.cpp:19-28 cancel between to_spectral and
 // to_nodal (|phase| = 1) and are not applied.
 #include <cstdio>
+#include <cstdlib>
 
 #include "hk_common.cuh"
 #include "hk_internal.h"
 
+
 namespace hk {
+
+// internal flag: route the FAST path through the 256-thread SMEM kernel
+constexpr uint32_t HK_COLL_LEGACY_FAST = 1u << 16;
 
 struct CollArgs {
     const double* f;
@@ -46,7 +51,9 @@ struct CollArgs {
     int md;
     double mult0, jac, w;
     hk_cell_status* st;
-    double* nyq;  // [cell][3][N][N] |F| on the Nyquist planes (FAST) or null
+    double* nyq;       // [cell][3][N][N] |F| on the Nyquist planes (FAST) or null
+    double2* xchg;     // [cluster][2 buffers][2 fields][C dest][P][N][N] L2 transpose scratch
+    unsigned* team_ctr;  // [teams] barrier counters (team kernel), zeroed per launch
 };
 
 template <int N, int C>
@@ -57,7 +64,8 @@ struct Geo {
     static constexpr int SLAB = P * PLANE;  // double2 per F slab / per received field
     static constexpr int NT = 256;
     static_assert(P * N == 128, "one pencil per thread per field");
-    static constexpr size_t SMEM = size_t(3 * SLAB) * sizeof(double2) + 8 * 3 * sizeof(double);
+    static constexpr size_t SMEM = size_t(3 * SLAB) * sizeof(double2) + 24 * sizeof(double);
+    static constexpr size_t XCHG_PER_CLUSTER = size_t(2) * 2 * C * P * N * N * sizeof(double2);
 };
 
 template <int N, int C, bool EXACT>
@@ -65,11 +73,13 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
     using G = Geo<N, C>;
     constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, SLAB = G::SLAB;
     constexpr int64_t NB = (int64_t)N * N * N;
+    constexpr int BLK = P * N * N;          // double2 per (dest rank, field) block
+    constexpr int64_t FIELD = (int64_t)C * BLK;  // double2 per field in the exchange buffer
     extern __shared__ __align__(16) double2 smem[];
     double2* Fs = smem;
     double2* Rv0 = smem + SLAB;
     double2* Rv1 = smem + 2 * SLAB;
-    double* red = reinterpret_cast<double*>(smem + 3 * SLAB);
+    double* red = reinterpret_cast<double*>(smem + 3 * SLAB);  // 24 doubles
 
     const unsigned r = cluster_rank();
     const unsigned cid = cluster_id_x();
@@ -78,12 +88,22 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
     const int phi = t >> 7;
     const int pp = t & 127;
     const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)cid * 2 * 2 * FIELD;  // this cluster's exchange buffers
+    unsigned buf = 0;  // alternates per exchange: no WAR barrier needed
 
     double2* RvMine = phi ? Rv1 : Rv0;
-
     const int n_entries = a.md + 1;  // distinct directions + loss
     const int rounds = EXACT ? n_entries : (n_entries + 1) / 2;
     const int loss_phi = EXACT ? 0 : ((n_entries - 1) & 1);
+
+    // Pull my block of field `fld` from the exchange buffer into padded SMEM rows.
+    auto pull = [&](double2* dstbase, const double2* src) {
+        const uint32_t d0 = smem_u32(dstbase);
+        for (int idx = t; idx < BLK; idx += 256) {
+            const int row = idx / N, col = idx % N;  // row = (plane, row-in-plane)
+            cp_async16(d0 + (row * ROW + col) * 16, src + idx);
+        }
+    };
 
     for (int64_t it = cid; it < count; it += ncl) {
         const int64_t cell = a.list ? a.list[it] : it;
@@ -106,23 +126,27 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
             for (int i = 0; i < N; ++i) row[i] = x[i];
         }
         __syncthreads();
-        if (t < 128) {  // forward over j1 (columns) -> owner of k1
-            const int j3l = pp / N, k2 = pp % N;
-            const double2* col = Rv0 + j3l * PLANE + k2;
-            double2 x[N];
+        {
+            double2* Xb = X + (int64_t)buf * 2 * FIELD;
+            if (t < 128) {  // forward over j1 (columns) -> block of the owner of k1: [k1l][k2][j3]
+                const int j3l = pp / N, k2 = pp % N;
+                const double2* col = Rv0 + j3l * PLANE + k2;
+                double2 x[N];
 #pragma unroll
-            for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
-            fft_reg<N, false>(x);
-            const int j3 = r * P + j3l;
+                for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
+                fft_reg<N, false>(x);
+                const int j3 = r * P + j3l;
 #pragma unroll
-            for (int dst = 0; dst < C; ++dst) {
-                double2* rb = dsmem_ptr(Fs + k2 * ROW + j3, dst);
-#pragma unroll
-                for (int kl = 0; kl < P; ++kl) rb[kl * PLANE] = x[dst * P + kl];
+                for (int k1 = 0; k1 < N; ++k1)
+                    st_cg16(Xb + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
             }
+            cluster_arrive();
+            cluster_wait();
+            pull(Fs, Xb + (int64_t)r * BLK);
+            cp_async_wait_all();
+            buf ^= 1;
         }
-        cluster_arrive();
-        cluster_wait();
+        __syncthreads();
         if (t < 128) {  // forward over k3 (rows of the slab), scale 1/N^3
             const int pl = pp / N, k2 = pp % N;
             double2* row = Fs + pl * PLANE + k2 * ROW;
@@ -154,21 +178,24 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
                 }
             }
         }
-        cluster_arrive();  // token: my Rv is free for round 0
 
         // ---------------- rounds over directions ----------------
-        double gacc[N];
+        // Gain accumulators: this thread owns nodes j1 in [phi N/2, (phi+1) N/2)
+        // of column (j3l, j2); FAST keeps Re only (N/2), EXACT complex (N).
+        constexpr int NG = EXACT ? N : N / 2;
+        double gacc[NG];
 #pragma unroll
-        for (int i = 0; i < N; ++i) gacc[i] = 0.0;
+        for (int i = 0; i < NG; ++i) gacc[i] = 0.0;
 
         for (int rd = 0; rd < rounds; ++rd) {
             const int e = EXACT ? rd : 2 * rd + phi;
             const bool valid = EXACT ? (rd < a.md || phi == 0) : (e < n_entries);
             const bool is_loss = (e == a.md);
-            // ---- phase A: X = F * weights, inverse FFT over i3 ----
+            double2* Xb = X + (int64_t)buf * 2 * FIELD + (int64_t)phi * FIELD;
+            // ---- phase A: X = F * weights, inverse FFT over i3, to L2 ----
             const int pl = pp / N, i2 = pp % N, i1 = r * P + pl;
-            double2 x[N];
             if (valid) {
+                double2 x[N];
                 const double2* frow = Fs + pl * PLANE + i2 * ROW;
                 if (EXACT) {
                     const double* wt = (is_loss ? a.loss : (phi ? a.alpha_p : a.alpha) + (int64_t)e * NB) +
@@ -189,18 +216,25 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
                     }
                 }
                 fft_reg<N, true>(x);
-            }
-            cluster_wait();  // every rank has finished reading its Rv (previous round)
-            if (valid) {
+                // block of the owner of j3: [j3l][i1][i2]
 #pragma unroll
-                for (int dst = 0; dst < C; ++dst) {
-                    double2* rb = dsmem_ptr(RvMine + i1 * ROW + i2, dst);
-#pragma unroll
-                    for (int jl = 0; jl < P; ++jl) rb[jl * PLANE] = x[dst * P + jl];
-                }
+                for (int j3 = 0; j3 < N; ++j3)
+                    st_cg16(Xb + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
             }
             cluster_arrive();
-            cluster_wait();  // my Rv now holds (all i1, all i2, my j3) of both fields
+            cluster_wait();  // every rank's phase A of this round is in L2
+            if (valid) {
+                // my half of the threads pulls my field's block
+                const uint32_t d0 = smem_u32(RvMine);
+                const double2* src = Xb + (int64_t)r * BLK;
+                for (int idx = pp; idx < BLK; idx += 128) {
+                    const int row = idx / N, col = idx % N;
+                    cp_async16(d0 + (row * ROW + col) * 16, src + idx);
+                }
+            }
+            cp_async_wait_all();
+            buf ^= 1;
+            __syncthreads();
 
             // ---- phase B: inverse FFT over i2 (rows), then i1 (columns) ----
             const int j3l = pp / N;
@@ -222,29 +256,46 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
                 for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
                 fft_reg<N, true>(y);
                 if (!EXACT && !is_loss) {
+                    // products of the partner's half go through my column slots
                     const double m = (e == 0) ? a.mult0 : 1.0;
+                    if (phi == 0) {  // register indices must stay compile-time
 #pragma unroll
-                    for (int j1 = 0; j1 < N; ++j1) gacc[j1] += m * (y[j1].x * y[j1].y);
+                        for (int h = 0; h < N / 2; ++h) {
+                            col[(N / 2 + h) * ROW].x = m * (y[N / 2 + h].x * y[N / 2 + h].y);
+                            gacc[h] += m * (y[h].x * y[h].y);
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < N / 2; ++h) {
+                            col[h * ROW].x = m * (y[h].x * y[h].y);
+                            gacc[h] += m * (y[N / 2 + h].x * y[N / 2 + h].y);
+                        }
+                    }
                 } else {
 #pragma unroll
                     for (int i = 0; i < N; ++i) col[i * ROW] = y[i];
                 }
             }
-            if (EXACT) {
-                __syncthreads();
-                if (rd < a.md) {  // gain += m * ga * gb on half the column per thread
-                    const double m = (rd == 0) ? a.mult0 : 1.0;
+            __syncthreads();
+            if (!EXACT) {
+                const int ep = 2 * rd + (1 - phi);  // partner's entry
+                if (ep < a.md) {
+                    const double2* pcol = (phi ? Rv0 : Rv1) + j3l * PLANE + j2;
 #pragma unroll
-                    for (int h = 0; h < N / 2; ++h) {
-                        const int j1 = phi * (N / 2) + h;
-                        const double2 ga = Rv0[j3l * PLANE + j1 * ROW + j2];
-                        const double2 gb = Rv1[j3l * PLANE + j1 * ROW + j2];
-                        gacc[2 * h] += m * (ga.x * gb.x - ga.y * gb.y);
-                        gacc[2 * h + 1] += m * (ga.x * gb.y + ga.y * gb.x);
-                    }
+                    for (int h = 0; h < N / 2; ++h) gacc[h] += pcol[(phi * (N / 2) + h) * ROW].x;
+                }
+            } else if (rd < a.md) {  // gain += m * ga * gb on half the column per thread
+                const double m = (rd == 0) ? a.mult0 : 1.0;
+#pragma unroll
+                for (int h = 0; h < N / 2; ++h) {
+                    const int j1 = phi * (N / 2) + h;
+                    const double2 ga = Rv0[j3l * PLANE + j1 * ROW + j2];
+                    const double2 gb = Rv1[j3l * PLANE + j1 * ROW + j2];
+                    gacc[2 * h] += m * (ga.x * gb.x - ga.y * gb.y);
+                    gacc[2 * h + 1] += m * (ga.x * gb.y + ga.y * gb.x);
                 }
             }
-            if (rd + 1 < rounds) cluster_arrive();  // my Rv may be overwritten
+            __syncthreads();  // Rv free for the next round's pull
         }
 
         // ---------------- epilogue: Q = jac (w gain - f loss) ----------------
@@ -255,7 +306,7 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
             if (!EXACT) {
                 double* Gd = reinterpret_cast<double*>(Free);
 #pragma unroll
-                for (int j1 = 0; j1 < N; ++j1) Gd[phi * N * N * P + (j1 * N + j2) * P + j3l] = gacc[j1];
+                for (int h = 0; h < N / 2; ++h) Gd[((phi * (N / 2) + h) * N + j2) * P + j3l] = gacc[h];
             } else {
 #pragma unroll
                 for (int h = 0; h < N / 2; ++h) {
@@ -271,8 +322,7 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
             const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
             double gre, gim;
             if (!EXACT) {
-                const double* Gd = reinterpret_cast<const double*>(Free);
-                gre = Gd[idx] + Gd[N * N * P + idx];
+                gre = reinterpret_cast<const double*>(Free)[idx];
                 gim = 0.0;
             } else {
                 const double2 g = Free[idx];
@@ -303,26 +353,285 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
         }
         __syncthreads();
         if (t == 0 && a.st) {
-            double m1 = 0, m2 = 0, s = 0;
+            double m1 = 0, m2 = 0, sum = 0;
             for (int w = 0; w < 8; ++w) {
                 m1 = fmax(m1, red[w]);
                 m2 = fmax(m2, red[8 + w]);
-                s += red[16 + w];
+                sum += red[16 + w];
             }
             hk_cell_status* sc = a.st + cell;
             atomic_max_nonneg(&sc->max_re, m1);
             atomic_max_nonneg(&sc->max_im, m2);
-            atomicAdd(&sc->q_norm2, s);
+            atomicAdd(&sc->q_norm2, sum);
             if (EXACT && r == 0) atomicOr(&sc->flags, HK_CELL_EXACT);
         }
-        cluster_arrive();
-        cluster_wait();  // end of cell: Fs / Rv of every rank reusable
+        __syncthreads();  // red / SMEM reusable by the next cell
     }
 }
 
-// Rigorous bound of the dropped Nyquist term of the FAST path, per cell:
-//   |Im ga_d(j)| <= A_d = sum_{k in S} |alpha_a,d(k)| |F(k)|,  likewise B_d,
-//   ||dQ||_2 <= jac w sum_d m_d A_d B_d N^{3/2}.
+// ---------------------------------------------------------------------------
+// FAST path, TMEM-resident spectrum: 128 threads per CTA, one field (= one
+// Hermitian-packed direction) per round, two CTAs (two cells) per SM so one
+// cell's barrier / L2 phases overlap the other's FFTs.  The cell's spectrum
+// slab F and the gain accumulators live in tensor memory (thread t <-> lane
+// t); shared memory holds only the exchange landing buffer.
+// ---------------------------------------------------------------------------
+template <int N, int C>
+struct GeoT {
+    static constexpr int P = N / C;
+    static constexpr int ROW = N + 1;
+    static constexpr int PLANE = N * ROW;
+    static constexpr int SLAB = P * PLANE;
+    static constexpr int NT = 128;
+    static_assert(P * N == NT, "one pencil per thread");
+    static constexpr uint32_t TM_COLS = 256;  // F: 4N cols (2N doubles), gain: 2N cols
+    static constexpr size_t SMEM = size_t(SLAB) * sizeof(double2) + 16 * sizeof(double) + 16;
+    static constexpr size_t XCHG_PER_CLUSTER = size_t(2) * C * P * N * N * sizeof(double2);
+};
+
+// Team barrier over the C CTAs of one cell (global counter, release/acquire
+// at GPU scope by one thread; the CTA barriers around it carry the other
+// threads' stores).  CTAs of a team are co-resident (cooperative launch).
+__device__ __forceinline__ void team_barrier(unsigned* ctr, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+template <int N, int C>
+__global__ void __launch_bounds__(128, 2) coll_fast_tmem_kernel(CollArgs a) {
+    using G = GeoT<N, C>;
+    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE;
+    constexpr int64_t NB = (int64_t)N * N * N;
+    constexpr int BLK = P * N * N;  // double2 per destination block
+    constexpr int64_t FIELD = (int64_t)C * BLK;
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rv = smem;
+    double* red = reinterpret_cast<double*>(smem + G::SLAB);  // 8 doubles
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 16);
+
+    const unsigned r = cluster_rank();
+    const unsigned cid = cluster_id_x();
+    const unsigned ncl = n_clusters_x();
+    const int t = threadIdx.x;
+    const int warp = t >> 5;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)cid * 2 * FIELD;
+    unsigned buf = 0;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * (warp & 3)) << 16);  // my lane, column 0
+    const uint32_t tmF = tm, tmG = tm + 4 * N;
+
+    const int n_entries = a.md + 1;
+    auto pull = [&](const double2* src) {
+        const uint32_t d0 = smem_u32(Rv);
+        for (int idx = t; idx < BLK; idx += 128) {
+            const int row = idx / N, col = idx % N;
+            cp_async16(d0 + (row * ROW + col) * 16, src + idx);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+    };
+
+    for (int64_t it = cid; it < count; it += ncl) {
+        const int64_t cell = a.list ? a.list[it] : it;
+        const double* fc = a.f + cell * NB;
+
+        // ---------------- prologue: F = FFT(f) / N^3 -> TMEM ----------------
+        for (int idx = t; idx < N * N * P; idx += 128) {
+            const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
+            Rv[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
+        }
+        __syncthreads();
+        {  // forward over j2 (rows (j3l, j1))
+            double2* row = Rv + (t / N) * PLANE + (t % N) * ROW;
+            double2 x[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) x[i] = row[i];
+            fft_reg<N, false>(x);
+#pragma unroll
+            for (int i = 0; i < N; ++i) row[i] = x[i];
+        }
+        __syncthreads();
+        {  // forward over j1 (columns (j3l, k2)) -> owner of k1
+            double2* Xb = X + (int64_t)buf * FIELD;
+            const int j3l = t / N, k2 = t % N;
+            const double2* col = Rv + j3l * PLANE + k2;
+            double2 x[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
+            fft_reg<N, false>(x);
+            const int j3 = r * P + j3l;
+#pragma unroll
+            for (int k1 = 0; k1 < N; ++k1)
+                st_cg16(Xb + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
+            cluster_arrive();
+            cluster_wait();
+            pull(Xb + (int64_t)r * BLK);  // rows (k1l, k2), columns k3
+            buf ^= 1;
+        }
+        {  // forward over k3, scale, F -> TMEM (+ Nyquist |F| for the guard)
+            const int pl = t / N, k2 = t % N, k1 = r * P + pl;
+            const double2* row = Rv + pl * PLANE + k2 * ROW;
+            double2 x[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) x[i] = row[i];
+            fft_reg<N, false>(x);
+            const double s = 1.0 / double(NB);
+#pragma unroll
+            for (int c = 0; c < N / 4; ++c) {
+                double v[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v[2 * i] = x[4 * c + i].x * s;
+                    v[2 * i + 1] = x[4 * c + i].y * s;
+                }
+                tmem_st16(tmF + 16 * c, v);
+            }
+            if (a.nyq) {
+                constexpr int H = N / 2;
+                double* ny = a.nyq + cell * 3 * N * N;
+                ny[2 * N * N + k1 * N + k2] = s * sqrt(x[H].x * x[H].x + x[H].y * x[H].y);
+                if (k2 == H) {
+#pragma unroll
+                    for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                }
+                if (k1 == H) {
+#pragma unroll
+                    for (int c = 0; c < N; ++c) ny[k2 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                }
+            }
+            const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+            for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
+            tmem_wait_st();
+        }
+
+        // ---------------- rounds: one field per round ----------------
+        for (int e = 0; e < n_entries; ++e) {
+            const bool is_loss = (e == a.md);
+            double2* Xb = X + (int64_t)buf * FIELD;
+            {  // phase A: X = F (alpha_s + i alpha'_s), inverse FFT over i3 -> L2
+                const int pl = t / N, i2 = t % N, i1 = r * P + pl;
+                const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + i2;
+                double2 x[N];
+#pragma unroll
+                for (int i3 = 0; i3 < N; ++i3) x[i3] = __ldg(wt + i3 * N);
+#pragma unroll
+                for (int c = 0; c < N / 4; ++c) {
+                    double v[8];
+                    tmem_ld16(tmF + 16 * c, v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const double2 w = x[4 * c + i];
+                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
+                    }
+                }
+                fft_reg<N, true>(x);
+#pragma unroll
+                for (int j3 = 0; j3 < N; ++j3)
+                    st_cg16(Xb + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
+            }
+            cluster_arrive();
+            cluster_wait();
+            pull(Xb + (int64_t)r * BLK);  // rows (j3l, i1), columns i2
+            buf ^= 1;
+            {  // phase B.1: inverse FFT over i2 (rows)
+                double2* row = Rv + (t / N) * PLANE + (t % N) * ROW;
+                double2 y[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) y[i] = row[i];
+                fft_reg<N, true>(y);
+#pragma unroll
+                for (int i = 0; i < N; ++i) row[i] = y[i];
+            }
+            __syncthreads();
+            {  // phase B.2: inverse FFT over i1 (columns), gain += m gs hs
+                const int j3l = t / N, j2 = t % N;
+                double2* col = Rv + j3l * PLANE + j2;
+                double2 y[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
+                fft_reg<N, true>(y);
+                if (!is_loss) {
+                    const double m = (e == 0) ? a.mult0 : 1.0;
+#pragma unroll
+                    for (int c = 0; c < N / 8; ++c) {
+                        double g[8];
+                        tmem_ld16(tmG + 16 * c, g);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) g[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
+                        tmem_st16(tmG + 16 * c, g);
+                    }
+                    tmem_wait_st();
+                } else {  // last round: (loss, w gain) into my column for the epilogue
+#pragma unroll
+                    for (int c = 0; c < N / 8; ++c) {
+                        double g[8];
+                        tmem_ld16(tmG + 16 * c, g);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) col[(8 * c + i) * ROW] = make_double2(y[8 * c + i].x, a.w * g[i]);
+                    }
+                }
+            }
+        }
+
+        // ---------------- epilogue: Q = jac (w gain - f loss) ----------------
+        __syncthreads();
+        double mre = 0.0, n2 = 0.0;
+        double* qc = a.q + cell * NB;
+        for (int idx = t; idx < N * N * P; idx += 128) {
+            const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
+            const double2 v = Rv[j3l * PLANE + j1 * ROW + j2];
+            const int64_t gi = ((int64_t)j1 * N + j2) * N + r * P + j3l;
+            const double qre = a.jac * (v.y - fc[gi] * v.x);
+            qc[gi] = qre;
+            mre = fmax(mre, fabs(qre));
+            n2 += qre * qre;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        }
+        if ((t & 31) == 0) {
+            red[warp] = mre;
+            red[4 + warp] = n2;
+        }
+        __syncthreads();
+        if (t == 0 && a.st) {
+            double m1 = 0, sum = 0;
+            for (int w = 0; w < 4; ++w) {
+                m1 = fmax(m1, red[w]);
+                sum += red[4 + w];
+            }
+            hk_cell_status* sc = a.st + cell;
+            atomic_max_nonneg(&sc->max_re, m1);
+            atomicAdd(&sc->q_norm2, sum);
+        }
+        __syncthreads();
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
+// Rigorous bound of the dropped Nyquist term of the FAST path, per cell.
+// With Y_d = alpha_a,d F and Y'_d = alpha'_a,d F supported on the Nyquist
+// set S:  |Im ga_d(j)| <= A_d = sum_S |Y_d|  and  ||Im gb_d||_2 = N^{3/2}
+// (sum_S |Y'_d|^2)^{1/2} (Parseval), so
+//   ||dQ||_2 <= jac w sum_d m_d N^{3/2} min(A_d ||Y'_d||_2, ||Y_d||_2 B_d).
 // Cells with bound / ||Q||_2 > tau are appended to the reroute list.
 __global__ void guard_kernel(int n, int md, double mult0, double jac, double w, double tau,
                              const double* __restrict__ nyq, const double* __restrict__ abs_a,
@@ -333,33 +642,39 @@ __global__ void guard_kernel(int n, int md, double mult0, double jac, double w, 
     if (cell >= ncells) return;
     const int nn3 = 3 * n * n;
     const double* F = nyq + cell * nn3;
-    __shared__ double sA[8], sB[8];
+    __shared__ double sred[4][8];
     double bound = 0.0;
     for (int e = 0; e < md; ++e) {
         const double* pa = abs_a + (int64_t)e * nn3;
         const double* pb = abs_ap + (int64_t)e * nn3;
-        double A = 0.0, B = 0.0;
+        double A = 0.0, B = 0.0, A2 = 0.0, B2 = 0.0;
         for (int i = threadIdx.x; i < nn3; i += blockDim.x) {
             const double fv = F[i];
-            A += __ldg(pa + i) * fv;
-            B += __ldg(pb + i) * fv;
+            const double ya = __ldg(pa + i) * fv, yb = __ldg(pb + i) * fv;
+            A += ya;
+            B += yb;
+            A2 += ya * ya;
+            B2 += yb * yb;
         }
         for (int o = 16; o > 0; o >>= 1) {
             A += __shfl_xor_sync(0xffffffffu, A, o);
             B += __shfl_xor_sync(0xffffffffu, B, o);
+            A2 += __shfl_xor_sync(0xffffffffu, A2, o);
+            B2 += __shfl_xor_sync(0xffffffffu, B2, o);
         }
         if ((threadIdx.x & 31) == 0) {
-            sA[threadIdx.x >> 5] = A;
-            sB[threadIdx.x >> 5] = B;
+            sred[0][threadIdx.x >> 5] = A;
+            sred[1][threadIdx.x >> 5] = B;
+            sred[2][threadIdx.x >> 5] = A2;
+            sred[3][threadIdx.x >> 5] = B2;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            double At = 0, Bt = 0;
-            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
-                At += sA[k];
-                Bt += sB[k];
-            }
-            bound += (e == 0 ? mult0 : 1.0) * At * Bt;
+            double t4[4] = {0, 0, 0, 0};
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k)
+                for (int q = 0; q < 4; ++q) t4[q] += sred[q][k];
+            const double b = fmin(t4[0] * sqrt(t4[3]), sqrt(t4[2]) * t4[1]);
+            bound += (e == 0 ? mult0 : 1.0) * b;
         }
         __syncthreads();
     }
@@ -391,7 +706,7 @@ __global__ void residue_kernel(int64_t ncells, hk_cell_status* st) {
 namespace {
 
 template <int N, int C, bool EXACT>
-int launch_variant(hk_ctx ctx, const CollArgs& args, int64_t max_cells) {
+int launch_variant(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) {
     using G = Geo<N, C>;
     auto kern = coll_kernel<N, C, EXACT>;
     const int key = N * 100 + C * 2 + (EXACT ? 1 : 0);
@@ -432,7 +747,64 @@ int launch_variant(hk_ctx ctx, const CollArgs& args, int64_t max_cells) {
     cfg.stream = ctx->stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    timing_begin(ctx, tag);
     st = check_cuda(ctx, cudaLaunchKernelEx(&cfg, kern, args), "collision kernel launch");
+    timing_end(ctx);
+    ctx->launches++;
+    return st;
+}
+
+template <int N, int C>
+int launch_fast_tmem(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) {
+    using G = GeoT<N, C>;
+    auto kern = coll_fast_tmem_kernel<N, C>;
+    const int key = N * 100 + C * 2 + 1000;
+    int st;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (!ctx->max_clusters.count(key)) {
+        if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
+                             "smem attribute")))
+            return st;
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cfg.gridDim = dim3(C * 256);
+        int ncl = 0, per_sm = 0;
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg), "max active clusters")))
+            return st;
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, G::SMEM), "occupancy")))
+            return st;
+        // The cluster query reports one CTA per SM for this kernel; the SMs
+        // host per_sm (= 2, TMEM-limited) co-resident clusters (measured: 30
+        // clusters of 8 on 120 SMs run in one wave, 32 do not).
+        {  // the occupancy API under-reports (1) for this kernel; 2 CTAs/SM fit by resources
+            cudaFuncAttributes fa;
+            if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && 2 * 128 * ((fa.numRegs + 7) & ~7) <= 65536 &&
+                2 * (G::SMEM + 1024) <= 233472)
+                per_sm = 2;
+        }
+        if (per_sm > 2) per_sm = 2;
+        if (ncl * C <= ctx->sm_count) ncl *= per_sm;
+        if (const char* m = getenv("HK_CLUSTERS")) ncl = atoi(m);  // experiment override
+        if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] fast tmem kernel: per_sm %d clusters %d\n", per_sm, ncl);
+        if (ncl < 1) return fail(ctx, HK_CUDA, "fast collision kernel cannot be resident");
+        ctx->max_clusters[key] = ncl;
+    }
+    int64_t ncl = ctx->max_clusters[key];
+    if (max_cells < ncl) ncl = max_cells;
+    if (ncl < 1) return HK_OK;
+    cfg.gridDim = dim3(unsigned(ncl * C));
+    cfg.stream = ctx->stream;
+    timing_begin(ctx, tag);
+    st = check_cuda(ctx, cudaLaunchKernelEx(&cfg, kern, args), "fast collision kernel launch");
+    timing_end(ctx);
     ctx->launches++;
     return st;
 }
@@ -447,8 +819,10 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     const size_t st_bytes = st ? 0 : sizeof(hk_cell_status) * ncells;
     const size_t nyq_bytes = guard ? sizeof(double) * nn3 * ncells : 0;
     const size_t list_bytes = guard ? sizeof(int64_t) * ncells : 0;
+    const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255) & ~size_t(255);
+    const size_t xchg_bytes = size_t(2 * ctx->sm_count / C + 1) * Geo<N, C>::XCHG_PER_CLUSTER + 4096;
     int s;
-    if ((s = ensure_scratch(ctx, st_bytes + nyq_bytes + list_bytes + 64))) return s;
+    if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
     char* base = static_cast<char*>(ctx->scratch);
     if (!st) st = reinterpret_cast<hk_cell_status*>(base);
     double* nyq = guard ? reinterpret_cast<double*>(base + st_bytes) : nullptr;
@@ -469,22 +843,30 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     a.jac = k->jac;
     a.w = k->weight;
     a.st = st;
+    a.xchg = reinterpret_cast<double2*>(base + xchg_off);
+    a.team_ctr = reinterpret_cast<unsigned*>(base + xchg_off + xchg_bytes - 4096);
     if (exact) {
-        if ((s = launch_variant<N, C, true>(ctx, a, ncells))) return s;
+        if ((s = launch_variant<N, C, true>(ctx, a, ncells, 0))) return s;
     } else {
         a.nyq = nyq;
-        if ((s = launch_variant<N, C, false>(ctx, a, ncells))) return s;
+        if (N == 32 && !(flags & HK_COLL_LEGACY_FAST)) {
+            if ((s = launch_fast_tmem<N, C>(ctx, a, ncells, 0))) return s;
+        } else {
+            if ((s = launch_variant<N, C, false>(ctx, a, ncells, 0))) return s;
+        }
         if (guard) {
             cudaMemsetAsync(count, 0, sizeof(int), ctx->stream);
+            timing_begin(ctx, 1);
             guard_kernel<<<unsigned(ncells), 256, 0, ctx->stream>>>(N, k->md, k->mult0, k->jac, k->weight, 1e-11, nyq,
                                                                   k->abs_a, k->abs_ap, ncells, st, list, count);
+            timing_end(ctx);
             ctx->launches++;
             if ((s = check_cuda(ctx, cudaGetLastError(), "guard kernel"))) return s;
             CollArgs b = a;
             b.nyq = nullptr;
             b.list = list;
             b.list_count = count;
-            if ((s = launch_variant<N, C, true>(ctx, b, ncells))) return s;
+            if ((s = launch_variant<N, C, true>(ctx, b, ncells, 2))) return s;
         }
     }
     {

@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <map>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/hykin_b200.h"
 
@@ -23,6 +25,9 @@ struct hk_ctx_s {
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
     std::map<int, int> max_clusters;  // key: kernel variant id
+    // optional CUDA-event timing of the collision kernels (tag -> event pairs)
+    bool timing = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
 };
 
 // Device-resident SpectralKernel (inc/spectral.hpp:15-33), re-laid out for
@@ -59,6 +64,10 @@ int closed_form_raw_tables(hk_ctx ctx, hk_kernel k, double* raw_alpha_dev,
 // hk_collision.cu
 int collision_launch(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells,
                      uint32_t flags, hk_cell_status* st);
+
+// Event-timing helpers (no-ops unless ctx->timing).
+void timing_begin(hk_ctx ctx, int tag);
+void timing_end(hk_ctx ctx);
 
 // hk_peak.cu
 double fp64_peak(hk_ctx ctx);

@@ -98,3 +98,48 @@ def config2_fast(ncells: int, n: int = 32, seed_salt: int = 0, distinct: int = 6
     idx = np.arange(ncells) % distinct
     scale = 1.0 + 1e-3 * rng.uniform(-1.0, 1.0, ncells)
     return base[idx] * scale[:, None]
+
+
+def config2_params(ncells: int, seed_salt: int = 0):
+    """The per-cell parameter draws of config2_cells, in the same RNG order."""
+    rng = rng_for(2, seed_salt)
+    rho = np.empty(ncells); u = np.empty((ncells, 3)); theta = np.empty((ncells, 3, 3))
+    delta = np.empty((ncells, 3))
+    for c in range(ncells):
+        rho[c] = rng.uniform(0.5, 2.0)
+        u[c] = rng.uniform(-0.5, 0.5, 3)
+        lam = rng.uniform(0.5, 2.0, 3)
+        R = random_rotation(rng)
+        theta[c] = R @ np.diag(lam) @ R.T
+        delta[c] = rng.uniform(-1.0, 1.0, 3)
+    return rho, u, theta, delta
+
+
+def config2_cells_torch(ncells: int, n: int = 32, device="cuda", seed_salt: int = 0, chunk: int = 512):
+    """config2_cells evaluated on the device (same draws, same formula), for
+    the bench's full 4096-cell batch.  Returns a [ncells, n^3] float64 tensor."""
+    import torch
+
+    rho, u, theta, delta = config2_params(ncells, seed_salt)
+    v = torch.as_tensor(nodes(n), dtype=torch.float64, device=device)
+    V = torch.stack(torch.meshgrid(v, v, v, indexing="ij"), dim=-1).reshape(-1, 3)  # [n^3, 3]
+    out = torch.empty((ncells, n ** 3), dtype=torch.float64, device=device)
+    inv = torch.as_tensor(np.linalg.inv(theta), device=device)
+    det = torch.as_tensor(np.linalg.det(theta), device=device)
+    rho_t = torch.as_tensor(rho, device=device)
+    u_t = torch.as_tensor(u, device=device)
+    d_t = torch.as_tensor(delta, device=device)
+    tbar = torch.as_tensor(np.trace(theta, axis1=1, axis2=2) / 3.0, device=device)
+    for s in range(0, ncells, chunk):
+        e = min(ncells, s + chunk)
+        D = V[None, :, :] - u_t[s:e, None, :]
+        q = torch.einsum("cki,cij,ckj->ck", D, inv[s:e], D)
+        g = rho_t[s:e, None] / torch.sqrt((2 * math.pi) ** 3 * det[s:e, None]) * torch.exp(-0.5 * q)
+
+        def mw(shift):
+            W = V[None, :, :] - (u_t[s:e, None, :] + shift)
+            T = tbar[s:e, None]
+            return rho_t[s:e, None] / (2 * math.pi * T) ** 1.5 * torch.exp(-(W * W).sum(-1) / (2 * T))
+
+        out[s:e] = 0.95 * g + 0.05 * 0.5 * (mw(d_t[s:e, None, :]) + mw(-d_t[s:e, None, :]))
+    return out
