@@ -54,6 +54,7 @@ struct CollArgs {
     double* nyq;       // [cell][3][N][N] |F| on the Nyquist planes (FAST) or null
     double2* xchg;     // [cluster][2 buffers][2 fields][C dest][P][N][N] L2 transpose scratch
     unsigned* team_ctr;  // [teams] barrier counters (team kernel), zeroed per launch
+    unsigned long long* prof;  // optional [4]: producer spin, consumer spin, producer total, consumer total (cycles)
 };
 
 template <int N, int C>
@@ -627,6 +628,310 @@ __global__ void __launch_bounds__(128, 2) coll_fast_tmem_kernel(CollArgs a) {
     if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
 }
 
+// ---------------------------------------------------------------------------
+// FAST path, warp-specialised and pipelined (the production kernel for N=32).
+// One CTA per SM, 256 threads: warps 0-3 PRODUCE (phase A: F * weights,
+// i3 transform, store to the L2 exchange slot), warps 4-7 CONSUME (pull the
+// slot, i2 and i1 transforms, gain).  A team of C CTAs (any SMs, cooperative
+// launch) shares a cell; producers run up to D exchanges ahead of consumers,
+// synchronised point-to-point by per-slot ready/done counters in global
+// memory, so barrier and L2 latency overlap the FFTs of the other role.
+// The spectrum slab F (written by consumers, read by producers) and the gain
+// accumulators live in TMEM; thread t of either role owns lane t % 128.
+// ---------------------------------------------------------------------------
+template <int N, int C>
+struct GeoP {
+    static constexpr int P = N / C;
+    static constexpr int ROW = N + 1;
+    static constexpr int PLANE = N * ROW;
+    static constexpr int SLAB = P * PLANE;
+    static constexpr int D = 4;  // exchange slots in flight per team
+    static_assert(P * N == 128, "one pencil per role thread");
+    static constexpr uint32_t TM_COLS = 256;
+    static constexpr size_t SMEM = size_t(3 * SLAB) * sizeof(double2) + 8 * sizeof(double) + 32;
+    static constexpr size_t XCHG_PER_TEAM = size_t(D) * C * P * N * N * sizeof(double2);
+};
+
+template <int N, int C>
+__global__ void __launch_bounds__(256, 1) coll_fast_pipe_kernel(CollArgs a) {
+    using G = GeoP<N, C>;
+    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
+    constexpr int64_t NB = (int64_t)N * N * N;
+    constexpr int BLK = P * N * N;
+    constexpr int64_t SLOT = (int64_t)C * BLK;
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rvb = smem;                // consumer landing buffers [2] (prefetch)
+    double2* Pw = smem + 2 * G::SLAB;   // producer work buffer (prologue)
+    double* red = reinterpret_cast<double*>(smem + 3 * G::SLAB);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 8);
+    uint64_t* fbar = reinterpret_cast<uint64_t*>(red + 10);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5;
+    const bool producer = t < 128;
+    const int u = t & 127;  // role-local thread index == TMEM lane
+    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)team * D * SLOT;
+    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
+    unsigned* done = ready + D;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    if (t == 0) {
+        mbar_init(smem_u32(fbar), 128);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t tmF = tm, tmG = tm + 4 * N;
+    const int n_entries = a.md + 1;
+    unsigned g = 0;      // exchange counter (identical sequence in both roles)
+    unsigned ncell = 0;  // cells processed (F-ready mbarrier parity)
+
+    if (producer) {
+        // ================================ PRODUCER ================================
+        long long spin_cyc = 0, t_start = clock64();
+        auto acquire_slot = [&](unsigned gg) {
+            if (u == 0) spin_cyc += spin_geq(done + gg % D, C * (gg / D));
+            named_bar(1, 128);
+        };
+        auto publish = [&](unsigned gg) {
+            named_bar(1, 128);
+            if (u == 0) signal_add(ready + gg % D);
+        };
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            // ---- prologue: 2-D forward transform of my j3 block, exchange ----
+            for (int idx = u; idx < N * N * P; idx += 128) {
+                const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
+                Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
+            }
+            named_bar(1, 128);
+            {
+                double2* row = Pw + (u / N) * PLANE + (u % N) * ROW;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = row[i];
+                fft_reg<N, false>(x);
+#pragma unroll
+                for (int i = 0; i < N; ++i) row[i] = x[i];
+            }
+            named_bar(1, 128);
+            {
+                const int j3l = u / N, k2 = u % N, j3 = r * P + j3l;
+                const double2* col = Pw + j3l * PLANE + k2;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
+                fft_reg<N, false>(x);
+                acquire_slot(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int k1 = 0; k1 < N; ++k1)
+                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
+                publish(g);
+                ++g;
+            }
+            // ---- wait until the consumers have put F(cell) into TMEM ----
+            mbar_wait_parity(smem_u32(fbar), ncell & 1);
+            tmem_fence_after();
+            // ---- phase A for every field ----
+            const int pl = u / N, i2 = u % N, i1 = r * P + pl;
+            for (int e = 0; e < n_entries; ++e) {
+                const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + i2;
+                double2 x[N];
+#pragma unroll
+                for (int i3 = 0; i3 < N; ++i3) x[i3] = __ldg(wt + i3 * N);
+#pragma unroll
+                for (int c = 0; c < N / 4; ++c) {
+                    double v[8];
+                    tmem_ld16(tmF + 16 * c, v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const double2 w = x[4 * c + i];
+                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
+                    }
+                }
+                fft_reg<N, true>(x);
+                acquire_slot(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int j3 = 0; j3 < N; ++j3)
+                    st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
+                publish(g);
+                ++g;
+            }
+        }
+        if (a.prof && u == 0) {
+            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
+        }
+    } else {
+        // ================================ CONSUMER ================================
+        // Exchange gg lands in Rvb[gg & 1]; the pull of gg+1 is issued before
+        // computing gg so its L2 latency overlaps the FFTs.
+        long long spin_cyc = 0, t_start = clock64();
+        auto issue = [&](unsigned gg) {
+            if (u == 0) spin_cyc += spin_geq(ready + gg % D, C * (gg / D + 1));
+            named_bar(2, 128);
+            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK;
+            const uint32_t d0 = smem_u32(Rvb + (gg & 1) * G::SLAB);
+            for (int idx = u; idx < BLK; idx += 128) cp_async16(d0 + ((idx / N) * ROW + (idx % N)) * 16, src + idx);
+            cp_async_commit();
+        };
+        auto complete = [&](unsigned gg) {  // only group gg is outstanding here
+            cp_async_wait_group0();
+            named_bar(2, 128);
+            if (u == 0) signal_add_relaxed(done + gg % D);  // slot reusable: data is in SMEM
+        };
+        if ((int64_t)team < count) issue(g);
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            // ---- prologue: last forward pass (k3), F -> TMEM ----
+            complete(g);
+            {
+                const double2* Rv = Rvb + (g & 1) * G::SLAB;
+                const int pl = u / N, k2 = u % N, k1 = r * P + pl;
+                const double2* row = Rv + pl * PLANE + k2 * ROW;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = row[i];
+                fft_reg<N, false>(x);
+                const double s = 1.0 / double(NB);
+#pragma unroll
+                for (int c = 0; c < N / 4; ++c) {
+                    double v[8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        v[2 * i] = x[4 * c + i].x * s;
+                        v[2 * i + 1] = x[4 * c + i].y * s;
+                    }
+                    tmem_st16(tmF + 16 * c, v);
+                }
+                if (a.nyq) {
+                    constexpr int H = N / 2;
+                    double* ny = a.nyq + cell * 3 * N * N;
+                    ny[2 * N * N + k1 * N + k2] = s * sqrt(x[H].x * x[H].x + x[H].y * x[H].y);
+                    if (k2 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                    }
+                    if (k1 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                    }
+                }
+                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
+                tmem_wait_st();
+                tmem_fence_before();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar)) : "memory");
+            }
+            named_bar(2, 128);  // all consumers done reading this buffer
+            issue(g + 1);  // field 0: only after F is published (producers need it)
+            ++g;
+            // ---- phase B for every field ----
+            for (int e = 0; e < n_entries; ++e) {
+                const bool is_loss = (e == a.md);
+                double2* Rv = Rvb + (g & 1) * G::SLAB;
+                complete(g);
+                const bool more = (e + 1 < n_entries) || (it + nteams < count);
+                if (more) issue(g + 1);
+                {  // inverse FFT over i2 (rows (j3l, i1))
+                    double2* row = Rv + (u / N) * PLANE + (u % N) * ROW;
+                    double2 y[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) y[i] = row[i];
+                    fft_reg<N, true>(y);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) row[i] = y[i];
+                }
+                named_bar(2, 128);
+                {  // inverse FFT over i1 (columns (j3l, j2)), gain += m gs hs
+                    const int j3l = u / N, j2 = u % N;
+                    double2* col = Rv + j3l * PLANE + j2;
+                    double2 y[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
+                    fft_reg<N, true>(y);
+                    if (!is_loss) {
+                        const double m = (e == 0) ? a.mult0 : 1.0;
+#pragma unroll
+                        for (int c = 0; c < N / 8; ++c) {
+                            double gv[8];
+                            tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) gv[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
+                            tmem_st16(tmG + 16 * c, gv);
+                        }
+                        tmem_wait_st();
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < N / 8; ++c) {
+                            double gv[8];
+                            tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) col[(8 * c + i) * ROW] = make_double2(y[8 * c + i].x, a.w * gv[i]);
+                        }
+                    }
+                }
+                named_bar(2, 128);  // reads of this buffer complete before it is refilled
+                if (!is_loss) ++g;
+            }
+            // ---- epilogue: Q = jac (w gain - f loss), loss field in Rvb[g & 1] ----
+            {
+                const double2* Rv = Rvb + (g & 1) * G::SLAB;
+                double mre = 0.0, n2 = 0.0;
+                double* qc = a.q + cell * NB;
+                for (int idx = u; idx < N * N * P; idx += 128) {
+                    const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
+                    const double2 v = Rv[j3l * PLANE + j1 * ROW + j2];
+                    const int64_t gi = ((int64_t)j1 * N + j2) * N + r * P + j3l;
+                    const double qre = a.jac * (v.y - fc[gi] * v.x);
+                    qc[gi] = qre;
+                    mre = fmax(mre, fabs(qre));
+                    n2 += qre * qre;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+                    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                }
+                if ((u & 31) == 0) {
+                    red[u >> 5] = mre;
+                    red[4 + (u >> 5)] = n2;
+                }
+                named_bar(2, 128);
+                if (u == 0 && a.st) {
+                    double m1 = 0, sum = 0;
+                    for (int w = 0; w < 4; ++w) {
+                        m1 = fmax(m1, red[w]);
+                        sum += red[4 + w];
+                    }
+                    hk_cell_status* sc = a.st + cell;
+                    atomic_max_nonneg(&sc->max_re, m1);
+                    atomicAdd(&sc->q_norm2, sum);
+                }
+                named_bar(2, 128);  // buffer / red reusable
+                ++g;
+            }
+        }
+        if (a.prof && u == 0) {
+            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
 // Rigorous bound of the dropped Nyquist term of the FAST path, per cell.
 // With Y_d = alpha_a,d F and Y'_d = alpha'_a,d F supported on the Nyquist
 // set S:  |Im ga_d(j)| <= A_d = sum_S |Y_d|  and  ||Im gb_d||_2 = N^{3/2}
@@ -810,6 +1115,57 @@ int launch_fast_tmem(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int ta
 }
 
 template <int N, int C>
+int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int tag) {
+    using G = GeoP<N, C>;
+    auto kern = coll_fast_pipe_kernel<N, C>;
+    const int key = N * 100 + C * 2 + 2000;
+    int st;
+    if (!ctx->max_clusters.count(key)) {
+        if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
+                             "smem attribute")))
+            return st;
+        int per_sm = 0;
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, G::SMEM), "occupancy")))
+            return st;
+        int teams = (per_sm >= 1 ? 1 : 0) * ctx->sm_count / C;  // one CTA per SM (TMEM, SMEM)
+        if (const char* m = getenv("HK_TEAMS")) teams = atoi(m);  // experiment override
+        if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] pipe kernel: per_sm %d teams %d\n", per_sm, teams);
+        if (teams < 1) return fail(ctx, HK_CUDA, "pipelined collision kernel cannot be resident");
+        ctx->max_clusters[key] = teams;
+    }
+    int64_t teams = ctx->max_clusters[key];
+    if (max_cells < teams) teams = max_cells;
+    if (teams < 1) return HK_OK;
+    CollArgs args = args_in;
+    if ((st = check_cuda(ctx, cudaMemsetAsync(args.team_ctr, 0, sizeof(unsigned) * 2 * G::D * teams, ctx->stream),
+                         "team counters")))
+        return st;
+    static unsigned long long* prof = nullptr;
+    const bool profiling = getenv("HK_PROF_SPIN") != nullptr;
+    if (profiling) {
+        if (!prof) cudaMalloc(&prof, 64);
+        cudaMemsetAsync(prof, 0, 64, ctx->stream);
+        args.prof = prof;
+    }
+    void* params[] = {&args};
+    timing_begin(ctx, tag);
+    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * C)), dim3(256), params,
+                                                     G::SMEM, ctx->stream),
+                    "pipelined collision kernel launch");
+    timing_end(ctx);
+    ctx->launches++;
+    if (profiling) {
+        unsigned long long h[4];
+        cudaMemcpyAsync(h, prof, 32, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        fprintf(stderr, "[hk prof] CTAs %lld: producer spin %.1f%% of %.3g cyc/CTA, consumer spin %.1f%% of %.3g cyc/CTA\n",
+                (long long)(teams * C), 100.0 * h[0] / (double)h[2], h[2] / double(teams * C), 100.0 * h[1] / (double)h[3],
+                h[3] / double(teams * C));
+    }
+    return st;
+}
+
+template <int N, int C>
 int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells, uint32_t flags,
              hk_cell_status* st) {
     const bool exact = (flags & (HK_COLL_EXACT | HK_COLL_STRICT)) != 0;
@@ -820,7 +1176,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     const size_t nyq_bytes = guard ? sizeof(double) * nn3 * ncells : 0;
     const size_t list_bytes = guard ? sizeof(int64_t) * ncells : 0;
     const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255) & ~size_t(255);
-    const size_t xchg_bytes = size_t(2 * ctx->sm_count / C + 1) * Geo<N, C>::XCHG_PER_CLUSTER + 4096;
+    const size_t xchg_bytes = size_t(2 * ctx->sm_count / C + 1) * Geo<N, C>::XCHG_PER_CLUSTER + 65536;
     int s;
     if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
     char* base = static_cast<char*>(ctx->scratch);
@@ -844,12 +1200,14 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     a.w = k->weight;
     a.st = st;
     a.xchg = reinterpret_cast<double2*>(base + xchg_off);
-    a.team_ctr = reinterpret_cast<unsigned*>(base + xchg_off + xchg_bytes - 4096);
+    a.team_ctr = reinterpret_cast<unsigned*>(base + xchg_off + xchg_bytes - 65536);
     if (exact) {
         if ((s = launch_variant<N, C, true>(ctx, a, ncells, 0))) return s;
     } else {
         a.nyq = nyq;
-        if (N == 32 && !(flags & HK_COLL_LEGACY_FAST)) {
+        if (N == 32 && !(flags & HK_COLL_LEGACY_FAST) && !getenv("HK_TMEM2")) {
+            if ((s = launch_fast_pipe<N, C>(ctx, a, ncells, 0))) return s;
+        } else if (N == 32 && !(flags & HK_COLL_LEGACY_FAST)) {
             if ((s = launch_fast_tmem<N, C>(ctx, a, ncells, 0))) return s;
         } else {
             if ((s = launch_variant<N, C, false>(ctx, a, ncells, 0))) return s;

@@ -201,6 +201,35 @@ __device__ __forceinline__ void st_cg16(double2* p, double2 v) {
     asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
+// Named barrier over `count` threads (role groups of a warp-specialised CTA).
+__device__ __forceinline__ void named_bar(unsigned id, unsigned count) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+// Spin until *p >= target (acquire, GPU scope).  Traps instead of hanging if
+// the producer never arrives (deadlock guard, ~2 s).
+__device__ __forceinline__ long long spin_geq(const unsigned* p, unsigned target) {
+    const long long t0 = clock64();
+    unsigned v;
+    for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+        if ((int)(v - target) >= 0) break;
+        if (clock64() - t0 > (1LL << 32)) __trap();
+        __nanosleep(32);
+    }
+    return clock64() - t0;
+}
+// WAR-only signal ("I have finished reading"): the reads it orders are
+// already complete (cp.async.wait_group), so no fence is issued.
+__device__ __forceinline__ void signal_add_relaxed(unsigned* p) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;\n" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void signal_add(unsigned* p) {
+    __threadfence();
+    atomicAdd(p, 1u);
+}
+
 // Non-negative double max via its ordered bit pattern.
 __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
     atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));

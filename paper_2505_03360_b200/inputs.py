@@ -143,3 +143,58 @@ def config2_cells_torch(ncells: int, n: int = 32, device="cuda", seed_salt: int 
 
         out[s:e] = 0.95 * g + 0.05 * 0.5 * (mw(d_t[s:e, None, :]) + mw(-d_t[s:e, None, :]))
     return out
+
+
+def _hermite(k: int, x):
+    """Probabilists' Hermite polynomials He_0..He_3."""
+    if k == 0:
+        return np.ones_like(x)
+    if k == 1:
+        return x
+    if k == 2:
+        return x * x - 1.0
+    return x * x * x - 3.0 * x
+
+
+HERMITE3 = [(a, b, 3 - a - b) for a in range(4) for b in range(4 - a)]  # the 10 (a,b,c), a+b+c=3
+
+
+def config3_fields(nx: int, ny: int, seed_salt: int = 0):
+    """Smooth seeded spatial fields of config 3 on a periodic [0,1)^2 grid:
+    rho = 1 + 0.2 sin, T = 1 + 0.2 cos, u = (0.1 sin, 0.1 cos, 0), and
+    eps_c in [0, 0.3] = rescaled sum of 4 random low-wavenumber sines."""
+    rng = rng_for(3, seed_salt)
+    x = (np.arange(nx) + 0.5) / nx
+    y = (np.arange(ny) + 0.5) / ny
+    X, Y = np.meshgrid(x, y, indexing="xy")  # [ny, nx], cell c = j*nx + i
+    ph = rng.uniform(0, 2 * np.pi, 4)
+    rho = 1.0 + 0.2 * np.sin(2 * np.pi * X + ph[0]) * np.cos(2 * np.pi * Y + ph[1])
+    T = 1.0 + 0.2 * np.cos(2 * np.pi * Y + ph[2]) * np.sin(2 * np.pi * X + ph[3])
+    ux = 0.1 * np.sin(2 * np.pi * (X + Y) + ph[1])
+    uy = 0.1 * np.cos(2 * np.pi * (X - Y) + ph[2])
+    e = np.zeros_like(X)
+    for _ in range(4):
+        kx, ky = rng.integers(1, 4, 2)
+        e += rng.uniform(0.5, 1.0) * np.sin(2 * np.pi * (kx * X + ky * Y) + rng.uniform(0, 2 * np.pi))
+    e = 0.3 * (e - e.min()) / max(e.max() - e.min(), 1e-300)
+    coef = rng.normal(size=len(HERMITE3))
+    coef /= np.linalg.norm(coef)
+    return dict(rho=rho.ravel(), T=T.ravel(), ux=ux.ravel(), uy=uy.ravel(), eps=e.ravel(), coef=coef)
+
+
+def config3_cells(nx: int, ny: int, n: int = 32, seed_salt: int = 0, cells=None):
+    """f = M(rho,u,T) (1 + eps_c P3(V)), V = (v-u)/sqrt(T), for the cells
+    listed (default: all nx*ny).  Returns ([ncells, n^3], fields)."""
+    fl = config3_fields(nx, ny, seed_salt)
+    idx = np.arange(nx * ny) if cells is None else np.asarray(cells)
+    v = nodes(n)
+    out = np.empty((len(idx), n ** 3))
+    for o, c in enumerate(idx):
+        rho, T, ux, uy, ep = fl["rho"][c], fl["T"][c], fl["ux"][c], fl["uy"][c], fl["eps"][c]
+        s = math.sqrt(T)
+        Vx, Vy, Vz = (v - ux) / s, (v - uy) / s, v / s
+        p3 = np.zeros((n, n, n))
+        for (a, b, cc), w in zip(HERMITE3, fl["coef"]):
+            p3 += w * _hermite(a, Vx)[:, None, None] * _hermite(b, Vy)[None, :, None] * _hermite(cc, Vz)[None, None, :]
+        out[o] = maxwellian(n, rho, (ux, uy, 0.0), T) * (1.0 + ep * p3.ravel())
+    return out, fl

@@ -1,0 +1,157 @@
+"""Pins the C restatement (oracle/hk_oracle.c) to the reference's own
+sources compiled here (oracle/_ref: unmodified src/*.cpp + FFTW/Eigen API
+shims).  CPU only; skipped where _ref was not built."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2505_03360_b200 import inputs
+
+VMAX = 8.0
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def k16(oracle, reflib):
+    ko = oracle.kernel(16, VMAX, 2, 4, inputs.R_PHYS_MAX, closed_form=False)
+    kr = reflib.kernel(16, VMAX, 2, 4, inputs.R_PHYS_MAX)
+    return ko, kr
+
+
+def test_precompute_tables_bitwise(k16):
+    ko, kr = k16
+    a, ap, ld, sc = kr.tables()
+    assert np.array_equal(a, ko.alpha) and np.array_equal(ap, ko.alpha_prime)
+    assert np.array_equal(ld, ko.loss_diag)
+    assert sc[0] == ko.r and sc[1] == ko.jacobian and sc[2] == ko.weight
+
+
+def test_closed_form_weights_match_quadrature(oracle, k16):
+    ko, _ = k16
+    kc = oracle.kernel(16, VMAX, 2, 4, inputs.R_PHYS_MAX, closed_form=True)
+    assert rel(kc.alpha, ko.alpha) < 1e-13 and rel(kc.alpha_prime, ko.alpha_prime) < 1e-13
+
+
+def test_collision_bitwise_and_throw_verdict(oracle, reflib, k16):
+    ko, kr = k16
+    f = inputs.config1_cells(3, 16)
+    qo, so, _ = oracle.collision_batch(ko, f)
+    qr, sr = reflib.collision_batch(kr, f)
+    assert np.array_equal(qo, qr)
+    assert np.array_equal(so, sr)  # both report the reference's numerical_consistency_error
+
+
+def test_precompute_errors(oracle, reflib):
+    for lib in (oracle, reflib):
+        assert lib.kernel(16, VMAX, 2, 2, inputs.R_PHYS_MAX * 1.01).status == 2  # aliasing
+        assert lib.kernel(16, VMAX, 0, 2, 1.0).status == 1                      # config
+        assert lib.kernel(16, VMAX, 2, 2, 0.0).status == 1
+
+
+def _cells3(n=8, nc=3):
+    f, _ = inputs.config3_cells(4, 4, n, cells=list(range(nc)))
+    return f
+
+
+def test_moments_family(oracle, reflib):
+    n = 8
+    for f in _cells3(n):
+        so, mo = oracle.moments(n, VMAX, f)
+        sr, mr = reflib.moments(n, VMAX, f)
+        assert so == sr == 0 and np.allclose(mo, mr, rtol=1e-14, atol=1e-16)
+        assert np.allclose(oracle.second_moment(n, VMAX, f), reflib.second_moment(n, VMAX, f), rtol=1e-14, atol=1e-16)
+        _, ao, bo, co = oracle.realizability(n, VMAX, f)
+        _, ar, br, cr = reflib.realizability(n, VMAX, f)
+        assert np.allclose(ao, ar, atol=1e-14) and np.allclose(bo, br, atol=1e-14) and abs(co - cr) < 1e-14
+        _, Mo = oracle.maxwellian(n, VMAX, mo)
+        _, Mr = reflib.maxwellian(n, VMAX, mr)
+        assert rel(Mo, Mr) < 1e-14
+        mom = np.array(mo[1:4]) * mo[0]
+        E = 0.5 * mo[0] * sum(x * x for x in mo[1:4]) + 1.5 * mo[0] * mo[4]
+        _, go = oracle.match_moments(n, VMAX, Mo, mo[0], mom, E)
+        _, gr = reflib.match_moments(n, VMAX, Mr, mr[0], mom, E)
+        assert rel(go, gr) < 1e-13
+        assert abs(oracle.l1_distance(n, VMAX, f)[1] - reflib.l1_distance(n, VMAX, f)[1]) < 1e-13
+
+
+def test_degenerate_moments(oracle, reflib):
+    z = np.zeros(8 ** 3)
+    assert oracle.moments(8, VMAX, z)[0] == 3 and reflib.moments(8, VMAX, z)[0] == 3
+
+
+def test_stage_solves(oracle, reflib):
+    n = 8
+    for f in _cells3(n):
+        po, s1 = oracle.penalized_stage_solve(n, VMAX, f, 0.3 * 1e-3, 1e-2)
+        pr, s2 = reflib.penalized_stage_solve(n, VMAX, f, 0.3 * 1e-3, 1e-2)
+        assert s1 == s2 == 0 and rel(po, pr) < 1e-13
+        eo, s1, fbo = oracle.esbgk_stage_solve(n, VMAX, f, 1e-3, 1e-2)
+        er, s2, fbr = reflib.esbgk_stage_solve(n, VMAX, f, 1e-3, 1e-2)
+        assert s1 == s2 == 0 and fbo == fbr and rel(eo, er) < 1e-13
+
+
+def test_esbgk_llt_fallback(oracle, reflib):
+    """beta = 5 with a weak relaxation makes Tc = -4 T I + 5 Theta indefinite for
+    a strongly anisotropic cell: both sides fall back to the Maxwellian
+    (src/moments.cpp:128-134)."""
+    n = 8
+    th = np.diag([0.2, 2.0, 2.0])
+    f = inputs.gaussian(n, 1.0, (0, 0, 0), th)
+    eo, _, fbo = oracle.esbgk_stage_solve(n, VMAX, f, 1e-6, 1e-2, beta=5.0)
+    er, _, fbr = reflib.esbgk_stage_solve(n, VMAX, f, 1e-6, 1e-2, beta=5.0)
+    assert fbo == fbr == 1 and rel(eo, er) < 1e-13
+
+
+def test_indicators_and_regime_truth_table(oracle, reflib):
+    rng = np.random.default_rng(7)
+    for _ in range(50):
+        prim = np.column_stack([rng.uniform(0.5, 2, 5), rng.uniform(-0.3, 0.3, 5), rng.uniform(-0.3, 0.3, 5),
+                                rng.uniform(0.5, 2, 5)])
+        _, lo, bo = oracle.indicators(prim, 0.01, 0.01, 1e-2)
+        lr, br = reflib.indicators(prim, 0.01, 0.01, 1e-2)
+        assert np.allclose(lo, lr, rtol=1e-14) and math.isclose(bo, br, rel_tol=1e-14)
+    # Algorithm 1 (src/regime.cpp:25-52): every branch incl. contract violations
+    lam_near, lam_far = [1.0, 1.0, 1.0], [1.0, 1.5, 1.0]
+    for r in (0, 1, 2, 3):
+        for lam in (None, lam_near, lam_far):
+            for lb in (None, 0.0, 1.0):
+                for l1 in (None, 0.0, 1.0):
+                    a = oracle.regime_update(r, lam, lb, l1, 1e-3, 1e-2, 1e-3)
+                    b = reflib.regime_update(r, lam, lb, l1, 1e-3, 1e-2, 1e-3)
+                    assert a[0] == b[0] and (a[0] != 0 or a[1] == b[1]), (r, lam, lb, l1, a, b)
+
+
+def test_transport_periodic(oracle, reflib):
+    n, nx, ny = 8, 5, 4
+    f, _ = inputs.config3_cells(nx, ny, n)
+    to = oracle.transport_rhs_periodic(f, nx, ny, n, VMAX, 0.1, 0.1)
+    tr = reflib.transport_rhs_periodic(f, nx, ny, n, VMAX, 0.1, 0.1)
+    assert np.array_equal(to, tr)
+    assert abs(to.sum()) < 1e-12 * np.abs(to).sum()  # globally conservative
+
+
+def test_penalized_residual(oracle, reflib, k16):
+    ko, kr = k16
+    f = inputs.config1_cells(2, 16)
+    for c in range(2):
+        ro, so, _ = oracle.penalized_residual(ko, f[c])
+        rr, sr = reflib.penalized_residual_batch(kr, f[c:c + 1])
+        assert so == sr[0] and rel(ro, rr[0]) < 1e-13
+
+
+def test_imex_steps(oracle, reflib):
+    n, nx, ny = 8, 4, 3
+    f, fl = inputs.config3_cells(nx, ny, n)
+    eps = np.full(nx * ny, 1e-2)
+    a, sa = oracle.esbgk_imex_step(f, nx, ny, n, VMAX, 0.1, 0.1, 1e-3, eps)
+    b, sb = reflib.esbgk_imex_step(f, nx, ny, n, VMAX, 0.1, 0.1, 1e-3, eps)
+    assert sa == sb == 0 and rel(a, b) < 1e-13
+    ko = oracle.kernel(n, VMAX, 2, 2, 2.0, closed_form=False)
+    kr = reflib.kernel(n, VMAX, 2, 2, 2.0)
+    a, sa = oracle.penalized_imex_step(ko, f, nx, ny, 0.1, 0.1, 1e-3, eps)
+    b, sb = reflib.penalized_imex_step(kr, f, nx, ny, 0.1, 0.1, 1e-3, eps)
+    assert sa == sb and rel(a, b) < 1e-13
