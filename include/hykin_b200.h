@@ -119,6 +119,61 @@ int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_d
 int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host,
                             int64_t ncells, uint32_t flags, hk_cell_status* st_host);
 
+
+/* ---- moments, relaxation stages, classifier, transport ----------------------
+ * Per-cell operators over a cell-major slab [ncells][n^3] (device pointers).
+ * Per-cell status arrays (int, nullable) receive HK_* codes; the reference
+ * would throw the corresponding exception for that cell. */
+
+/* moments_of (src/moments.cpp:21-53) -> mom[cell] = (rho, ux, uy, uz, T);
+ * second_moment (:55-81) -> sigma[cell] = (xx, xy, xz, yy, yz, zz);
+ * realizability_matrix (:269-312) -> real[cell] = (a_bar 3x3 row-major, b_bar[3], c_bar);
+ * l1_distance_to_maxwellian (src/indicators.cpp:89-98) -> l1[cell].  Each output nullable. */
+int hk_moments_batch(hk_ctx ctx, int n, double vmax, const double* f_dev, int64_t ncells, double* mom_dev,
+                     double* sigma_dev, double* real_dev, double* l1_dev, int* status_dev);
+/* maxwellian (src/moments.cpp:88-112) of mom[cell] = (rho, ux, uy, uz, T). */
+int hk_maxwellian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, int64_t ncells, double* out_dev,
+                        int* status_dev);
+/* esbgk_stage_solve (src/esbgk.cpp:9-45, inc/esbgk.hpp:36): per-cell Knudsen
+ * number eps_dev[cell] (or the scalar eps when eps_dev is NULL); nu = nu_coeff rho.
+ * info[cell] = status | (gaussian_fallback << 8); mom_dev (nullable) = moments of f*. */
+int hk_esbgk_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_dev, double* out_dev, int64_t ncells,
+                         double a, const double* eps_dev, double eps, double beta, double nu_coeff, int* info_dev,
+                         double* mom_dev);
+/* penalized_stage_solve (src/boltzmann.cpp:29-45, inc/boltzmann.hpp:36): rate pen_coeff rho. */
+int hk_penalized_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_dev, double* out_dev,
+                             int64_t ncells, double a, const double* eps_dev, double eps, double pen_coeff,
+                             int* info_dev, double* mom_dev);
+/* penalized_residual (src/boltzmann.cpp:9-27, inc/boltzmann.hpp:29): Q(f) + beta (f - M~),
+ * invariant moments projected out.  The collision part follows `flags` as
+ * hk_collision_batch (the throw-after-write residue verdict is reported in st_dev). */
+int hk_penalized_residual_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* out_dev, int64_t ncells,
+                                double pen_coeff, uint32_t flags, int* status_dev, hk_cell_status* st_dev);
+/* spatial_derivatives + v_eps1_eigenvalues + lambda_b_indicator + regime_update
+ * (src/indicators.cpp:14-87, src/regime.cpp:25-52) on a periodic nx x ny grid of
+ * kinetic cells, prim = prim_from_moments(mom) (src/coupling.cpp:33-35).
+ * r_in/r_out int8 layers {0,1,2}; ind[cell] = (lambda_a, lambda_b, lambda_c, lambda_B)
+ * (nullable); l1 may be NULL (HK_CONTRACT where Algorithm 1 needs it). */
+int hk_classify(hk_ctx ctx, int nx, int ny, double dx, double dy, const double* mom_dev, const double* eps_dev,
+                const double* l1_dev, const int8_t* r_in_dev, int8_t* r_out_dev, double* ind_dev, int* status_dev,
+                double eta0, double eta1, double delta0, double mu0, double kappa0, int signed_sum);
+/* kinetic_transport_rhs_periodic (src/transport.cpp:51-66): CWENO3 upwind.  x_halo = 0:
+ * periodic in x, input [ny][nx][n^3]; x_halo >= 2: input [ny][nx + 2 x_halo][n^3] carries
+ * ghost columns (x-slab of a partitioned grid), output [ny][nx][n^3].  Periodic in y. */
+int hk_transport_rhs(hk_ctx ctx, int n, double vmax, const double* f_dev, double* out_dev, int nx, int ny,
+                     int x_halo, double dx, double dy, double eps_weno);
+/* esbgk_imex_step (src/esbgk.cpp:47-99) / penalized_imex_step (src/boltzmann.cpp:47-110):
+ * one PR(2,2,2) step of a periodic all-kinetic field, in place.  work_dev: 6 nx ny n^3
+ * doubles or NULL (allocated from the stream-ordered pool). */
+int hk_esbgk_imex_step(hk_ctx ctx, int n, double vmax, double* f_dev, int nx, int ny, double dx, double dy, double dt,
+                       const double* eps_dev, double beta, double nu_coeff, double eps_weno, double* work_dev);
+int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int ny, double dx, double dy, double dt,
+                           const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
+                           double* work_dev);
+/* out = x + a y + b z (y, z nullable): the partitioner's halo-free elementwise updates. */
+int hk_axpby(hk_ctx ctx, int64_t count, double* out_dev, const double* x_dev, double a, const double* y_dev, double b,
+             const double* z_dev);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* fp64 FMA peak of this device (DFMA microbenchmark), TFLOP/s. */
 double hk_measure_fp64_peak(hk_ctx ctx);

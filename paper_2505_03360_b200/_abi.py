@@ -76,6 +76,18 @@ def lib() -> C.CDLL:
         "hk_collision_batch": (C.c_int, [vp, vp, vp, vp, i64, u32, vp]),
         "hk_collision_batch_host": (C.c_int, [vp, vp, vp, vp, i64, u32, vp]),
         "hk_measure_fp64_peak": (dbl, [vp]),
+        "hk_moments_batch": (C.c_int, [vp, C.c_int, dbl, vp, i64, vp, vp, vp, vp, vp]),
+        "hk_maxwellian_batch": (C.c_int, [vp, C.c_int, dbl, vp, i64, vp, vp]),
+        "hk_esbgk_stage_batch": (C.c_int, [vp, C.c_int, dbl, vp, vp, i64, dbl, vp, dbl, dbl, dbl, vp, vp]),
+        "hk_penalized_stage_batch": (C.c_int, [vp, C.c_int, dbl, vp, vp, i64, dbl, vp, dbl, dbl, vp, vp]),
+        "hk_penalized_residual_batch": (C.c_int, [vp, vp, vp, vp, i64, dbl, u32, vp, vp]),
+        "hk_classify": (C.c_int, [vp, C.c_int, C.c_int, dbl, dbl, vp, vp, vp, vp, vp, vp, vp, dbl, dbl, dbl, dbl,
+                                  dbl, C.c_int]),
+        "hk_transport_rhs": (C.c_int, [vp, C.c_int, dbl, vp, vp, C.c_int, C.c_int, C.c_int, dbl, dbl, dbl]),
+        "hk_esbgk_imex_step": (C.c_int, [vp, C.c_int, dbl, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, dbl, dbl, dbl,
+                                         vp]),
+        "hk_penalized_imex_step": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, dbl, dbl, u32, vp]),
+        "hk_axpby": (C.c_int, [vp, i64, vp, vp, dbl, vp, dbl, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -1,0 +1,572 @@
+// hk_cells.cu — per-cell moment / relaxation / classification kernels, sm_100a.
+//
+// One 256-thread CTA per cell (grid-strided over the batch); the cell's N^3
+// block is streamed from HBM with coalesced loads, reduced in registers +
+// warp shuffles, and the few scalar solves (3x3 Cholesky test, 5x5 complete-
+// pivoting LU) run on one thread.  These paths are HBM-bound (16 N^3 bytes
+// per cell-step); every pass after the first re-reads the block from L2.
+//
+// Reference functions (src/ = /root/reference/proj/core/src):
+//   moments_of             src/moments.cpp:21-53
+//   second_moment          src/moments.cpp:55-81
+//   maxwellian             src/moments.cpp:88-112
+//   anisotropic_gaussian   src/moments.cpp:120-157
+//   match_moments          src/moments.cpp:164-246
+//   remove_invariant_moments src/moments.cpp:192-267
+//   realizability_matrix   src/moments.cpp:269-312
+//   l1_distance_to_maxwellian src/indicators.cpp:89-98
+//   penalized_residual     src/boltzmann.cpp:9-27   (after the collision kernel)
+//   penalized_stage_solve  src/boltzmann.cpp:29-45
+//   esbgk_stage_solve      src/esbgk.cpp:9-45
+#include <cmath>
+
+#include "hk_cells.cuh"
+#include "hk_common.cuh"
+#include "hk_internal.h"
+
+namespace hk {
+
+namespace {
+
+constexpr int NT = 256;
+
+struct VGrid {
+    int n;
+    double vmax, dv, dvk;
+    __device__ double node(int k) const { return -vmax + (k + 0.5) * dv; }
+};
+
+__host__ VGrid make_vgrid(int n, double vmax) {
+    VGrid g;
+    g.n = n;
+    g.vmax = vmax;
+    g.dv = 2.0 * vmax / n;
+    g.dvk = g.dv * g.dv * g.dv;
+    return g;
+}
+
+// Block-wide sum of K doubles; result valid in every thread.
+template <int K>
+__device__ void block_sum(double (&v)[K], double* scratch /* [8][K] */) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) scratch[w * K + k] = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int ww = 0; ww < NT / 32; ++ww) s += scratch[ww * K + k];
+        v[k] = s;
+    }
+}
+
+// Eigen::FullPivLU<Matrix<double,5,5>> (src/moments.cpp:215-221), as
+// oracle/hk_oracle.c:hko_solve5.  Returns false when singular.
+__device__ bool solve5(const double a_in[25], const double rhs[5], double x[5]) {
+    double a[25];
+    int rp[5], cp[5];
+    for (int i = 0; i < 25; ++i) a[i] = a_in[i];
+    for (int i = 0; i < 5; ++i) rp[i] = cp[i] = i;
+    double maxpivot = 0.0;
+    int nonzero = 5;
+    for (int k = 0; k < 5; ++k) {
+        int bi = k, bj = k;
+        double big = -1.0;
+        for (int j = k; j < 5; ++j)
+            for (int i = k; i < 5; ++i) {
+                const double v = fabs(a[5 * i + j]);
+                if (v > big) { big = v; bi = i; bj = j; }
+            }
+        if (big == 0.0) { nonzero = k; break; }
+        if (big > maxpivot) maxpivot = big;
+        if (bi != k) {
+            for (int j = 0; j < 5; ++j) { const double t = a[5 * k + j]; a[5 * k + j] = a[5 * bi + j]; a[5 * bi + j] = t; }
+            const int t = rp[k]; rp[k] = rp[bi]; rp[bi] = t;
+        }
+        if (bj != k) {
+            for (int i = 0; i < 5; ++i) { const double t = a[5 * i + k]; a[5 * i + k] = a[5 * i + bj]; a[5 * i + bj] = t; }
+            const int t = cp[k]; cp[k] = cp[bj]; cp[bj] = t;
+        }
+        for (int i = k + 1; i < 5; ++i) {
+            a[5 * i + k] /= a[5 * k + k];
+            for (int j = k + 1; j < 5; ++j) a[5 * i + j] -= a[5 * i + k] * a[5 * k + j];
+        }
+    }
+    const double thr = 2.220446049250313e-16 * 5.0 * maxpivot;
+    int rank = 0;
+    for (int i = 0; i < nonzero; ++i) rank += fabs(a[5 * i + i]) > thr;
+    if (rank != 5) return false;
+    double y[5];
+    for (int i = 0; i < 5; ++i) y[i] = rhs[rp[i]];
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < i; ++j) y[i] -= a[5 * i + j] * y[j];
+    for (int i = 4; i >= 0; --i) {
+        for (int j = i + 1; j < 5; ++j) y[i] -= a[5 * i + j] * y[j];
+        y[i] /= a[5 * i + i];
+    }
+    for (int i = 0; i < 5; ++i) x[cp[i]] = y[i];
+    return true;
+}
+
+struct Mom {
+    double rho, ux, uy, uz, T;
+};
+
+// Pass 1 sums (k3-inner partials not reproduced; order differs by round-off):
+// s0, sx, sy, sz, s2, and the raw second moment xx, xy, xz, yy, yz, zz.
+__device__ void raw_sums(const double* __restrict__ f, const VGrid& g, double (&s)[11], double* scratch) {
+    const int n = g.n;
+    const int nb = n * n * n;
+#pragma unroll
+    for (int k = 0; k < 11; ++k) s[k] = 0.0;
+    for (int idx = threadIdx.x; idx < nb; idx += NT) {
+        const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+        const double vx = g.node(k1), vy = g.node(k2), vz = g.node(k3);
+        const double w = f[idx];
+        s[0] += w;
+        s[1] += vx * w;
+        s[2] += vy * w;
+        s[3] += vz * w;
+        s[4] += (vx * vx + vy * vy + vz * vz) * w;
+        s[5] += vx * vx * w;
+        s[6] += vx * vy * w;
+        s[7] += vx * vz * w;
+        s[8] += vy * vy * w;
+        s[9] += vy * vz * w;
+        s[10] += vz * vz * w;
+    }
+    block_sum<11>(s, scratch);
+}
+
+// moments_of (src/moments.cpp:44-52).  Returns HK_DEGENERATE on rho<=0 / T<=0.
+__device__ int moments_from_sums(const double (&s)[11], const VGrid& g, Mom& m) {
+    m.rho = s[0] * g.dvk;
+    m.ux = s[1] / s[0];
+    m.uy = s[2] / s[0];
+    m.uz = s[3] / s[0];
+    m.T = (s[4] / s[0] - (m.ux * m.ux + m.uy * m.uy + m.uz * m.uz)) / 3.0;
+    if (!(m.rho > 0.0)) return HK_DEGENERATE;
+    if (!(m.T > 0.0)) return HK_DEGENERATE;
+    return HK_OK;
+}
+
+__device__ double energy_of(const Mom& m) {
+    return 0.5 * m.rho * (m.ux * m.ux + m.uy * m.uy + m.uz * m.uz) + 1.5 * m.rho * m.T;
+}
+
+// Separable Maxwellian factors ex/ey/ez in shared memory (src/moments.cpp:93-102).
+__device__ double maxwell_factors(const Mom& m, const VGrid& g, double* ex, double* ey, double* ez) {
+    const double inv2T = 0.5 / m.T;
+    for (int k = threadIdx.x; k < g.n; k += NT) {
+        const double v = g.node(k);
+        ex[k] = exp(-(v - m.ux) * (v - m.ux) * inv2T);
+        ey[k] = exp(-(v - m.uy) * (v - m.uy) * inv2T);
+        ez[k] = exp(-(v - m.uz) * (v - m.uz) * inv2T);
+    }
+    __syncthreads();
+    return m.rho / pow(2.0 * M_PI * m.T, 1.5);
+}
+
+// Coupling matrix A_rc = sum phi_r psi_c w dvK of a weight given node-wise by
+// `wfun(idx, vx, vy, vz)` (src/moments.cpp:164-189).
+template <typename WF>
+__device__ void coupling(const VGrid& g, const double uc[3], WF wfun, double (&A)[25], double* scratch) {
+    const int n = g.n, nb = n * n * n;
+#pragma unroll
+    for (int i = 0; i < 25; ++i) A[i] = 0.0;
+    for (int idx = threadIdx.x; idx < nb; idx += NT) {
+        const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+        const double vx = g.node(k1), vy = g.node(k2), vz = g.node(k3);
+        const double w = wfun(idx, vx, vy, vz);
+        const double cx = vx - uc[0], cy = vy - uc[1], cz = vz - uc[2];
+        const double c2 = cx * cx + cy * cy + cz * cz;
+        const double v2 = vx * vx + vy * vy + vz * vz;
+        const double psi[5] = {1.0, cx, cy, cz, c2};
+        const double phi[5] = {1.0, vx, vy, vz, v2};
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+#pragma unroll
+            for (int c = 0; c < 5; ++c) A[5 * r + c] += phi[r] * psi[c] * w;
+    }
+    block_sum<25>(A, scratch);
+#pragma unroll
+    for (int i = 0; i < 25; ++i) A[i] *= g.dvk;
+}
+
+__device__ __forceinline__ double quad_factor(const double x[5], double vx, double vy, double vz, const double uc[3]) {
+    const double cx = vx - uc[0], cy = vy - uc[1], cz = vz - uc[2];
+    const double c2 = cx * cx + cy * cy + cz * cz;
+    return x[0] + x[1] * cx + x[2] * cy + x[3] * cz + x[4] * c2;
+}
+
+// ---------------------------------------------------------------------------
+// moments + second moment + realizability + L1 distance, one CTA per cell
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) moments_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
+                                                     double* __restrict__ mom, double* __restrict__ sigma,
+                                                     double* __restrict__ real, double* __restrict__ l1,
+                                                     int* __restrict__ status) {
+    __shared__ double scratch[8 * 25];
+    __shared__ double ex[128], ey[128], ez[128];
+    const int n = g.n, nb = n * n * n;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        const double* fc = f + cell * nb;
+        double s[11];
+        raw_sums(fc, g, s, scratch);
+        Mom m;
+        const int st = moments_from_sums(s, g, m);
+        if (threadIdx.x == 0) {
+            if (mom) {
+                double* o = mom + cell * 5;
+                o[0] = m.rho; o[1] = m.ux; o[2] = m.uy; o[3] = m.uz; o[4] = m.T;
+            }
+            if (sigma) {
+                double* o = sigma + cell * 6;
+                for (int k = 0; k < 6; ++k) o[k] = s[5 + k] * g.dvk;  // xx xy xz yy yz zz
+            }
+            if (status) status[cell] = st;
+        }
+        if (st != HK_OK || (!real && !l1)) continue;
+        // pass 2: realizability (src/moments.cpp:269-312) and L1 distance
+        const double pref = l1 ? maxwell_factors(m, g, ex, ey, ez) : 0.0;
+        const double ist = 1.0 / sqrt(m.T);
+        double r[11];
+#pragma unroll
+        for (int k = 0; k < 11; ++k) r[k] = 0.0;
+        for (int idx = threadIdx.x; idx < nb; idx += NT) {
+            const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+            const double Vx = (g.node(k1) - m.ux) * ist, Vy = (g.node(k2) - m.uy) * ist, Vz = (g.node(k3) - m.uz) * ist;
+            const double w = fc[idx];
+            const double V2 = Vx * Vx + Vy * Vy + Vz * Vz;
+            r[0] += Vx * Vx * w;
+            r[1] += Vx * Vy * w;
+            r[2] += Vx * Vz * w;
+            r[3] += Vy * Vy * w;
+            r[4] += Vy * Vz * w;
+            r[5] += Vz * Vz * w;
+            const double bw = 0.5 * (V2 - 5.0) * w;
+            r[6] += bw * Vx;
+            r[7] += bw * Vy;
+            r[8] += bw * Vz;
+            const double e = 0.5 * V2 - 2.5;
+            r[9] += e * e * w;
+            if (l1) r[10] += fabs(w - pref * ex[k1] * ey[k2] * ez[k3]);
+        }
+        block_sum<11>(r, scratch);
+        if (threadIdx.x == 0) {
+            if (real) {
+                const double sc = g.dvk / m.rho;
+                double s2[6];
+                for (int k = 0; k < 6; ++k) s2[k] = r[k] * sc;
+                const double tr3 = (s2[0] + s2[3] + s2[5]) / 3.0;
+                double* o = real + cell * 13;  // a_bar (3x3 row-major), b_bar, c_bar
+                o[0] = s2[0] - tr3; o[1] = s2[1]; o[2] = s2[2];
+                o[3] = s2[1]; o[4] = s2[3] - tr3; o[5] = s2[4];
+                o[6] = s2[2]; o[7] = s2[4]; o[8] = s2[5] - tr3;
+                o[9] = r[6] * sc; o[10] = r[7] * sc; o[11] = r[8] * sc;
+                o[12] = 0.4 * r[9] * sc;
+            }
+            if (l1) l1[cell] = r[10] * g.dvk;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Maxwellian of given moments (src/moments.cpp:88-112)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) maxwellian_kernel(const double* __restrict__ mom, int64_t ncells, VGrid g,
+                                                        double* __restrict__ out, int* __restrict__ status) {
+    __shared__ double ex[128], ey[128], ez[128];
+    const int n = g.n, nb = n * n * n;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        Mom m{mom[cell * 5], mom[cell * 5 + 1], mom[cell * 5 + 2], mom[cell * 5 + 3], mom[cell * 5 + 4]};
+        const bool ok = (m.rho > 0.0) && (m.T > 0.0);
+        if (threadIdx.x == 0 && status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
+        if (!ok) continue;
+        const double pref = maxwell_factors(m, g, ex, ey, ez);
+        double* o = out + cell * nb;
+        for (int idx = threadIdx.x; idx < nb; idx += NT) {
+            const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+            o[idx] = pref * ex[k1] * ey[k2] * ez[k3];
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Relaxation stages: f = (eps f* + A G~)/(eps + A), G~ the moment-matched
+// Maxwellian (penalized, src/boltzmann.cpp:29-45) or anisotropic Gaussian
+// (ES-BGK, src/esbgk.cpp:9-45).  Three passes: sums of f*, coupling matrix
+// of G (G recomputed, never stored), blend.
+// info[cell] = status | (gaussian_fallback << 8)
+// ---------------------------------------------------------------------------
+template <bool ESBGK>
+__global__ void __launch_bounds__(NT) stage_kernel(const double* __restrict__ fin, double* __restrict__ out,
+                                                   int64_t ncells, VGrid g, double a, const double* __restrict__ eps_cell,
+                                                   double eps_scalar, double beta, double coeff,
+                                                   int* __restrict__ info, double* __restrict__ mom_out) {
+    __shared__ double scratch[8 * 25];
+    __shared__ double ex[128], ey[128], ez[128];
+    __shared__ double par[16];  // [0..8] inverse Tc, [9] pref, [10] use_gauss, [11..15] x
+    const int n = g.n, nb = n * n * n;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        const double* fc = fin + cell * nb;
+        double* oc = out + cell * nb;
+        const double eps = eps_cell ? eps_cell[cell] : eps_scalar;
+        double s[11];
+        raw_sums(fc, g, s, scratch);
+        Mom m;
+        int st = moments_from_sums(s, g, m);
+        if (threadIdx.x == 0 && mom_out) {
+            double* o = mom_out + cell * 5;
+            o[0] = m.rho; o[1] = m.ux; o[2] = m.uy; o[3] = m.uz; o[4] = m.T;
+        }
+        const double A = ESBGK ? a * (coeff * m.rho) : a * (coeff * m.rho);  // nu = coeff rho | beta = coeff rho
+        if (st != HK_OK || !(A > 0.0)) {
+            if (threadIdx.x == 0 && info) info[cell] = st;
+            if (st == HK_OK)
+                for (int idx = threadIdx.x; idx < nb; idx += NT) oc[idx] = fc[idx];  // identity stage
+            __syncthreads();
+            continue;
+        }
+        int fallback = 0;
+        if (ESBGK && threadIdx.x == 0) {
+            // Sigma blend toward rho (T I + u u^T) (src/esbgk.cpp:24-33)
+            const double omb = 1.0 - beta;
+            const double u[3] = {m.ux, m.uy, m.uz};
+            const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+            double theta[9], tc[9];
+            const double denom = eps + omb * A, oa = omb * A;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) {
+                    const double sstar = s[5 + map[3 * i + j]] * g.dvk;
+                    const double siso = m.rho * ((i == j ? m.T : 0.0) + u[i] * u[j]);
+                    const double sstage = (eps * sstar + oa * siso) / denom;
+                    theta[3 * i + j] = sstage / m.rho - u[i] * u[j];
+                }
+            const double iso = (1.0 - beta) * m.T;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) tc[3 * i + j] = (i == j ? iso : 0.0) + beta * theta[3 * i + j];
+            // Eigen::LLT info (src/moments.cpp:128-134)
+            double l[9] = {0};
+            bool ok = true;
+            for (int k = 0; k < 3 && ok; ++k) {
+                double x = tc[3 * k + k];
+                for (int j = 0; j < k; ++j) x -= l[3 * k + j] * l[3 * k + j];
+                if (!(x > 0.0)) { ok = false; break; }
+                l[3 * k + k] = sqrt(x);
+                for (int i = k + 1; i < 3; ++i) {
+                    double y = tc[3 * i + k];
+                    for (int j = 0; j < k; ++j) y -= l[3 * i + j] * l[3 * k + j];
+                    l[3 * i + k] = y / l[3 * k + k];
+                }
+            }
+            if (ok) {
+                const double* q = tc;
+                const double c00 = q[4] * q[8] - q[5] * q[7], c01 = q[5] * q[6] - q[3] * q[8], c02 = q[3] * q[7] - q[4] * q[6];
+                const double det = q[0] * (q[4] * q[8] - q[5] * q[7]) - q[1] * (q[3] * q[8] - q[5] * q[6]) +
+                                   q[2] * (q[3] * q[7] - q[4] * q[6]);
+                const double dinv = q[0] * c00 + q[1] * c01 + q[2] * c02;
+                const double id = 1.0 / dinv;
+                par[0] = c00 * id; par[1] = (q[2] * q[7] - q[1] * q[8]) * id; par[2] = (q[1] * q[5] - q[2] * q[4]) * id;
+                par[3] = c01 * id; par[4] = (q[0] * q[8] - q[2] * q[6]) * id; par[5] = (q[2] * q[3] - q[0] * q[5]) * id;
+                par[6] = c02 * id; par[7] = (q[1] * q[6] - q[0] * q[7]) * id; par[8] = (q[0] * q[4] - q[1] * q[3]) * id;
+                par[9] = m.rho / sqrt(pow(2.0 * M_PI, 3) * det);
+                par[10] = 1.0;
+            } else {
+                par[10] = 0.0;  // fall back to the Maxwellian
+            }
+        }
+        __syncthreads();
+        const bool gauss = ESBGK && par[10] != 0.0;
+        if (ESBGK) fallback = gauss ? 0 : 1;
+        double pref = 0.0;
+        if (!gauss) pref = maxwell_factors(m, g, ex, ey, ez);
+        // equilibrium value at node idx, recomputed in passes 2 and 3
+        auto eq = [&](int idx, double vx, double vy, double vz) -> double {
+            const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+            if (!gauss) return pref * ex[k1] * ey[k2] * ez[k3];
+            const double dx = vx - m.ux, dy = vy - m.uy, dz = vz - m.uz;
+            const double qxy = par[0] * dx * dx + 2.0 * par[1] * dx * dy + par[4] * dy * dy;
+            const double lz = 2.0 * (par[2] * dx + par[5] * dy);
+            const double q = qxy + dz * (lz + par[8] * dz);
+            return par[9] * exp(-0.5 * q);
+        };
+        // match_moments(G, rho, rho u, E) (src/moments.cpp:225-246)
+        const double mom3[3] = {m.rho * m.ux, m.rho * m.uy, m.rho * m.uz};
+        const double uc[3] = {mom3[0] / m.rho, mom3[1] / m.rho, mom3[2] / m.rho};
+        double Amat[25];
+        coupling(g, uc, eq, Amat, scratch);
+        if (threadIdx.x == 0) {
+            const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
+            double x[5];
+            const bool ok = solve5(Amat, rhs, x);
+            for (int k = 0; k < 5; ++k) par[11 + k] = x[k];
+            st = ok ? HK_OK : HK_DEGENERATE;
+            if (info) info[cell] = st | (fallback << 8);
+            scratch[0] = st;
+        }
+        __syncthreads();
+        st = (int)scratch[0];
+        if (st == HK_OK) {
+            const double x[5] = {par[11], par[12], par[13], par[14], par[15]};
+            const double wf = eps / (eps + A), wg = A / (eps + A);
+            for (int idx = threadIdx.x; idx < nb; idx += NT) {
+                const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+                const double vx = g.node(k1), vy = g.node(k2), vz = g.node(k3);
+                const double G = eq(idx, vx, vy, vz) * quad_factor(x, vx, vy, vz, uc);
+                oc[idx] = wf * fc[idx] + wg * G;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// penalized_residual epilogue (src/boltzmann.cpp:14-26): q holds Q(f) on
+// entry and Q(f) + beta (f - M~) with the invariant moments removed on exit.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NT) residual_finish_kernel(const double* __restrict__ f, double* __restrict__ q,
+                                                             int64_t ncells, VGrid g, double pen_coeff,
+                                                             int* __restrict__ status) {
+    __shared__ double scratch[8 * 25];
+    __shared__ double ex[128], ey[128], ez[128];
+    __shared__ double par[12];
+    const int n = g.n, nb = n * n * n;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        const double* fc = f + cell * nb;
+        double* qc = q + cell * nb;
+        double s[11];
+        raw_sums(fc, g, s, scratch);
+        Mom m;
+        int st = moments_from_sums(s, g, m);
+        if (st != HK_OK) {
+            if (threadIdx.x == 0 && status) status[cell] = st;
+            __syncthreads();
+            continue;
+        }
+        const double beta = pen_coeff * m.rho;
+        const double pref = maxwell_factors(m, g, ex, ey, ez);
+        const double mom3[3] = {m.rho * m.ux, m.rho * m.uy, m.rho * m.uz};
+        const double uc[3] = {mom3[0] / m.rho, mom3[1] / m.rho, mom3[2] / m.rho};
+        auto maxw = [&](int idx, double, double, double) -> double {
+            const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+            return pref * ex[k1] * ey[k2] * ez[k3];
+        };
+        double Amat[25];
+        coupling(g, uc, maxw, Amat, scratch);
+        if (threadIdx.x == 0) {
+            const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
+            double x[5];
+            const bool ok = solve5(Amat, rhs, x);
+            for (int k = 0; k < 5; ++k) par[k] = x[k];
+            scratch[0] = ok ? HK_OK : HK_DEGENERATE;
+        }
+        __syncthreads();
+        st = (int)scratch[0];
+        __syncthreads();
+        if (st != HK_OK) {
+            if (threadIdx.x == 0 && status) status[cell] = st;
+            continue;
+        }
+        const double x[5] = {par[0], par[1], par[2], par[3], par[4]};
+        // out = Q + beta (f - M~); then remove_invariant_moments(out, M~, u)
+        // (src/moments.cpp:248-267) with uc = u.
+        const double u3[3] = {m.ux, m.uy, m.uz};
+        auto mt = [&](int idx, double vx, double vy, double vz) -> double {
+            return maxw(idx, vx, vy, vz) * quad_factor(x, vx, vy, vz, uc);
+        };
+        double B[25];
+        coupling(g, u3, mt, B, scratch);
+        double inv[5] = {0, 0, 0, 0, 0};
+        for (int idx = threadIdx.x; idx < nb; idx += NT) {
+            const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+            const double vx = g.node(k1), vy = g.node(k2), vz = g.node(k3);
+            const double o = qc[idx] + beta * (fc[idx] - mt(idx, vx, vy, vz));
+            qc[idx] = o;
+            inv[0] += o;
+            inv[1] += vx * o;
+            inv[2] += vy * o;
+            inv[3] += vz * o;
+            inv[4] += (vx * vx + vy * vy + vz * vz) * o;
+        }
+        block_sum<5>(inv, scratch);
+        if (threadIdx.x == 0) {
+            double rhs[5], y[5];
+            for (int k = 0; k < 5; ++k) rhs[k] = inv[k] * g.dvk;
+            const bool ok = solve5(B, rhs, y);
+            for (int k = 0; k < 5; ++k) par[5 + k] = y[k];
+            if (status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
+            scratch[0] = ok ? HK_OK : HK_DEGENERATE;
+        }
+        __syncthreads();
+        if ((int)scratch[0] == HK_OK) {
+            const double y[5] = {par[5], par[6], par[7], par[8], par[9]};
+            for (int idx = threadIdx.x; idx < nb; idx += NT) {
+                const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+                const double vx = g.node(k1), vy = g.node(k2), vz = g.node(k3);
+                qc[idx] -= quad_factor(y, vx, vy, vz, u3) * mt(idx, vx, vy, vz);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+int grid_for(hk_ctx ctx, int64_t ncells) {
+    const int64_t cap = int64_t(ctx->sm_count) * 8;
+    return int(ncells < cap ? ncells : cap);
+}
+
+}  // namespace
+
+int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncells, double* mom, double* sigma,
+                   double* real, double* l1, int* status) {
+    if (ncells <= 0) return HK_OK;
+    if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "moments: 2 <= n <= 128");
+    moments_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), mom, sigma, real, l1,
+                                                                  status);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "moments kernel");
+}
+
+int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status) {
+    if (ncells <= 0) return HK_OK;
+    if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "maxwellian: 2 <= n <= 128");
+    maxwellian_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(mom, ncells, make_vgrid(n, vmax), out, status);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "maxwellian kernel");
+}
+
+int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,
+                 const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out) {
+    if (ncells <= 0) return HK_OK;
+    if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "stage: 2 <= n <= 128");
+    const VGrid g = make_vgrid(n, vmax);
+    if (esbgk)
+        stage_kernel<true><<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(fin, out, ncells, g, a, eps_cell, eps_scalar,
+                                                                          beta, coeff, info, mom_out);
+    else
+        stage_kernel<false><<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(fin, out, ncells, g, a, eps_cell, eps_scalar,
+                                                                           beta, coeff, info, mom_out);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "stage kernel");
+}
+
+int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,
+                           int* status) {
+    if (ncells <= 0) return HK_OK;
+    residual_finish_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(f, q, ncells, make_vgrid(n, vmax), pen_coeff,
+                                                                          status);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "residual kernel");
+}
+
+}  // namespace hk

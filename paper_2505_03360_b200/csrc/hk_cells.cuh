@@ -1,0 +1,36 @@
+// hk_cells.cuh — launchers of the per-cell and field kernels (hk_cells.cu, hk_field.cu).
+#pragma once
+#include "hk_internal.h"
+
+namespace hk {
+
+int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncells, double* mom, double* sigma,
+                   double* real, double* l1, int* status);
+int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status);
+int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,
+                 const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out);
+int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,
+                           int* status);
+
+struct ClassifyParams {
+    int nx, ny;
+    double dx, dy, mu0, kappa0, eta0, eta1, delta0;
+    int signed_sum;
+};
+int classify_launch(hk_ctx ctx, const ClassifyParams& p, const double* mom, const double* eps_cell, const double* l1,
+                    const int8_t* r_in, int8_t* r_out, double* ind, int* status);
+
+struct TransportParams {
+    int n;
+    double vmax;
+    int nx, ny;      // output (interior) cells
+    int x_halo;      // 0: periodic in x; >= 2: input carries x_halo ghost columns per side
+    double dx, dy, eps_weno;
+};
+int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out);
+
+// out = x + a*y + b*z (elementwise, any of y/z nullable)
+int axpby_launch(hk_ctx ctx, int64_t count, double* out, const double* x, double a, const double* y, double b,
+                 const double* z);
+
+}  // namespace hk

@@ -1,0 +1,198 @@
+// hk_steps.cu — C-ABI entries for the per-cell / field operators and the
+// device-resident PR(2,2,2) IMEX steps (include/hykin_b200.h).
+//
+//   penalized_imex_step   src/boltzmann.cpp:47-110
+//   esbgk_imex_step       src/esbgk.cpp:47-99
+//   ImexTableau::pr222    inc/imex.hpp:23-34
+// All buffers stay in HBM; one step is a fixed sequence of stream-ordered
+// launches (CUDA-graph capturable).
+#include <cmath>
+
+#include "hk_cells.cuh"
+#include "hk_common.cuh"
+#include "hk_internal.h"
+
+namespace hk {
+
+namespace {
+
+struct PR222 {
+    double a_ex10, a_im00, a_im10, a_im11, w_ex0, w_ex1, w_im0, w_im1;
+};
+PR222 pr222() {
+    const double C = 1.0 / std::sqrt(2.0);
+    const double delta = 1.0 - 1.0 / (2.0 * C);
+    return {1.0, 1.0 - C, C - delta, delta, 0.5, 0.5, 0.5, 0.5};
+}
+
+// Fused elementwise IMEX combinations; e = per-cell Knudsen number.
+enum CombOp { K1 = 0, Q1 = 1, FACC = 2, FINAL = 3 };
+
+__global__ void combine_kernel(int op, int64_t count, int64_t nb, PR222 t, double dt, const double* __restrict__ e,
+                               double* __restrict__ o, const double* __restrict__ f, const double* __restrict__ y,
+                               const double* __restrict__ q1, const double* __restrict__ k1,
+                               const double* __restrict__ tr, const double* __restrict__ res) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const double inv_eps = res ? 1.0 / e[i / nb] : 0.0;
+        switch (op) {
+        case K1:  // k1 = (Y - f) / a11   (src/boltzmann.cpp:65-67)
+            o[i] = (y[i] - f[i]) * (1.0 / t.a_im00);
+            break;
+        case Q1:  // q1 = T(Y) + res(Y) / eps   (:69-76)
+            o[i] = res ? tr[i] + res[i] * inv_eps : tr[i];
+            break;
+        case FACC:  // f_acc = f + dt a_ex10 q1 + a_im10 k1   (:80-81)
+            o[i] = f[i] + dt * t.a_ex10 * q1[i] + t.a_im10 * k1[i];
+            break;
+        default: {  // final streaming combination (:99-108)
+            const double q2k = res ? tr[i] + res[i] * inv_eps : tr[i];
+            const double fc = o[i];
+            const double facc = fc + dt * t.a_ex10 * q1[i] + t.a_im10 * k1[i];
+            const double k2 = (y[i] - facc) * (1.0 / t.a_im11);
+            o[i] = fc + (dt * (t.w_ex0 * q1[i] + t.w_ex1 * q2k) + t.w_im0 * k1[i] + t.w_im1 * k2);
+        }
+        }
+    }
+}
+
+int combine(hk_ctx ctx, int op, int64_t count, int64_t nb, const PR222& t, double dt, const double* e, double* o,
+            const double* f, const double* y, const double* q1, const double* k1, const double* tr, const double* res) {
+    const int64_t blocks = (count + 255) / 256, cap = int64_t(ctx->sm_count) * 16;
+    combine_kernel<<<unsigned(blocks < cap ? blocks : cap), 256, 0, ctx->stream>>>(op, count, nb, t, dt, e, o, f, y, q1,
+                                                                                   k1, tr, res);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "combine kernel");
+}
+
+struct Work {
+    double *y, *q1, *k1, *tr, *res, *fa;
+};
+
+int get_work(hk_ctx ctx, double* user, int64_t count, Work& w, double** owned) {
+    *owned = nullptr;
+    double* base = user;
+    if (!base) {
+        int st = check_cuda(ctx, cudaMallocAsync(&base, sizeof(double) * count * 6, ctx->stream), "step work alloc");
+        if (st) return st;
+        *owned = base;
+    }
+    w = {base, base + count, base + 2 * count, base + 3 * count, base + 4 * count, base + 5 * count};
+    return HK_OK;
+}
+
+}  // namespace
+
+}  // namespace hk
+
+using namespace hk;
+
+extern "C" {
+
+int hk_moments_batch(hk_ctx ctx, int n, double vmax, const double* f_dev, int64_t ncells, double* mom_dev,
+                     double* sigma_dev, double* real_dev, double* l1_dev, int* status_dev) {
+    cudaSetDevice(ctx->device);
+    return moments_launch(ctx, n, vmax, f_dev, ncells, mom_dev, sigma_dev, real_dev, l1_dev, status_dev);
+}
+
+int hk_maxwellian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, int64_t ncells, double* out_dev,
+                        int* status_dev) {
+    cudaSetDevice(ctx->device);
+    return maxwellian_launch(ctx, n, vmax, mom_dev, ncells, out_dev, status_dev);
+}
+
+int hk_esbgk_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_dev, double* out_dev, int64_t ncells,
+                         double a, const double* eps_dev, double eps, double beta, double nu_coeff, int* info_dev,
+                         double* mom_dev) {
+    cudaSetDevice(ctx->device);
+    return stage_launch(ctx, true, n, vmax, f_star_dev, out_dev, ncells, a, eps_dev, eps, beta, nu_coeff, info_dev,
+                        mom_dev);
+}
+
+int hk_penalized_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_dev, double* out_dev,
+                             int64_t ncells, double a, const double* eps_dev, double eps, double pen_coeff,
+                             int* info_dev, double* mom_dev) {
+    cudaSetDevice(ctx->device);
+    return stage_launch(ctx, false, n, vmax, f_star_dev, out_dev, ncells, a, eps_dev, eps, 0.0, pen_coeff, info_dev,
+                        mom_dev);
+}
+
+int hk_penalized_residual_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* out_dev, int64_t ncells,
+                                double pen_coeff, uint32_t flags, int* status_dev, hk_cell_status* st_dev) {
+    cudaSetDevice(ctx->device);
+    int st = hk_collision_batch(ctx, k, f_dev, out_dev, ncells, flags & ~HK_COLL_STRICT, st_dev);
+    if (st) return st;
+    return residual_finish_launch(ctx, k->n, k->vmax, f_dev, out_dev, ncells, pen_coeff, status_dev);
+}
+
+int hk_classify(hk_ctx ctx, int nx, int ny, double dx, double dy, const double* mom_dev, const double* eps_dev,
+                const double* l1_dev, const int8_t* r_in_dev, int8_t* r_out_dev, double* ind_dev, int* status_dev,
+                double eta0, double eta1, double delta0, double mu0, double kappa0, int signed_sum) {
+    cudaSetDevice(ctx->device);
+    if (!(eta0 > 0.0) || !(eta1 > 0.0) || !(delta0 > 0.0))  // Thresholds::validate (src/indicators.cpp:9-12)
+        return fail(ctx, HK_CONFIG, "regime thresholds eta0, eta1, delta0 must be positive");
+    ClassifyParams p{nx, ny, dx, dy, mu0, kappa0, eta0, eta1, delta0, signed_sum};
+    return classify_launch(ctx, p, mom_dev, eps_dev, l1_dev, r_in_dev, r_out_dev, ind_dev, status_dev);
+}
+
+int hk_transport_rhs(hk_ctx ctx, int n, double vmax, const double* f_dev, double* out_dev, int nx, int ny,
+                     int x_halo, double dx, double dy, double eps_weno) {
+    cudaSetDevice(ctx->device);
+    TransportParams p{n, vmax, nx, ny, x_halo, dx, dy, eps_weno};
+    return transport_launch(ctx, p, f_dev, out_dev);
+}
+
+// Shared driver of both PR(2,2,2) steps on a periodic all-kinetic field.
+static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, double* f, int nx, int ny, double dx,
+                     double dy, double dt, const double* eps_dev, double beta, double coeff, double eps_weno,
+                     uint32_t flags, double* work_dev) {
+    cudaSetDevice(ctx->device);
+    const int64_t cells = (int64_t)nx * ny, nb = (int64_t)n * n * n, count = cells * nb;
+    const PR222 t = pr222();
+    Work w;
+    double* owned = nullptr;
+    int st = get_work(ctx, work_dev, count, w, &owned);
+    if (st) return st;
+    TransportParams tp{n, vmax, nx, ny, 0, dx, dy, eps_weno};
+    auto stage = [&](const double* fin, double a, double* out) {
+        return boltz ? stage_launch(ctx, false, n, vmax, fin, out, cells, a, eps_dev, 0.0, 0.0, coeff, nullptr, nullptr)
+                     : stage_launch(ctx, true, n, vmax, fin, out, cells, a, eps_dev, 0.0, beta, coeff, nullptr, nullptr);
+    };
+    auto residual = [&](const double* y, double* out) {
+        int s = hk_collision_batch(ctx, k, y, out, cells, flags & ~HK_COLL_STRICT, nullptr);
+        return s ? s : residual_finish_launch(ctx, n, vmax, y, out, cells, coeff, nullptr);
+    };
+    double* R = boltz ? w.res : nullptr;
+    if (!st) st = stage(f, t.a_im00 * dt, w.y);                                             // Y1
+    if (!st) st = combine(ctx, K1, count, nb, t, dt, eps_dev, w.k1, f, w.y, 0, 0, 0, 0);     // k1
+    if (!st) st = transport_launch(ctx, tp, w.y, w.tr);                                      // T(Y1)
+    if (!st && boltz) st = residual(w.y, w.res);                                             // res(Y1)
+    if (!st) st = combine(ctx, Q1, count, nb, t, dt, eps_dev, w.q1, 0, 0, 0, 0, w.tr, R);    // q1
+    if (!st) st = combine(ctx, FACC, count, nb, t, dt, eps_dev, w.fa, f, 0, w.q1, w.k1, 0, 0);  // f_acc
+    if (!st) st = stage(w.fa, t.a_im11 * dt, w.y);                                           // Y2
+    if (!st) st = transport_launch(ctx, tp, w.y, w.tr);                                      // T(Y2)
+    if (!st && boltz) st = residual(w.y, w.res);                                             // res(Y2)
+    if (!st) st = combine(ctx, FINAL, count, nb, t, dt, eps_dev, f, 0, w.y, w.q1, w.k1, w.tr, R);
+    if (owned) cudaFreeAsync(owned, ctx->stream);
+    return st;
+}
+
+int hk_esbgk_imex_step(hk_ctx ctx, int n, double vmax, double* f_dev, int nx, int ny, double dx, double dy, double dt,
+                       const double* eps_dev, double beta, double nu_coeff, double eps_weno, double* work_dev) {
+    return imex_step(ctx, nullptr, false, n, vmax, f_dev, nx, ny, dx, dy, dt, eps_dev, beta, nu_coeff, eps_weno, 0,
+                     work_dev);
+}
+
+int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int ny, double dx, double dy, double dt,
+                           const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
+                           double* work_dev) {
+    return imex_step(ctx, k, true, k->n, k->vmax, f_dev, nx, ny, dx, dy, dt, eps_dev, 0.0, pen_coeff, eps_weno, flags,
+                     work_dev);
+}
+
+int hk_axpby(hk_ctx ctx, int64_t count, double* out_dev, const double* x_dev, double a, const double* y_dev, double b,
+             const double* z_dev) {
+    cudaSetDevice(ctx->device);
+    return axpby_launch(ctx, count, out_dev, x_dev, a, y_dev, b, z_dev);
+}
+
+}  // extern "C"

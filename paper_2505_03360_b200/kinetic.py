@@ -1,0 +1,204 @@
+"""Per-cell kinetic operators and the PR(2,2,2) steps on the device.
+
+Python mirror of the reference's moments / ES-BGK / Boltzmann-layer /
+indicator / transport interfaces (inc/moments.hpp, inc/esbgk.hpp,
+inc/boltzmann.hpp, inc/indicators.hpp, inc/regime.hpp, inc/transport.hpp),
+batched over a cell-major slab ``[cells, n^3]`` of float64 CUDA tensors and
+executed by libhykin_b200.so.  Per-cell failures that the reference would
+throw are returned as status arrays (``status`` = HK_* code per cell) and,
+with ``check=True``, raised as the reference's exception class for the
+lowest failing cell.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _abi
+from . import default_context, degenerate_state_error, contract_violation, VelocityGrid, SpectralKernel
+
+_STATUS_EXC = {_abi.HK_DEGENERATE: degenerate_state_error, _abi.HK_CONTRACT: contract_violation}
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _check_cells(status, what):
+    bad = torch.nonzero(status & 0xFF).flatten()
+    if bad.numel():
+        c = int(bad[0])
+        code = int(status[c]) & 0xFF
+        raise _STATUS_EXC.get(code, RuntimeError)(f"{what}: cell {c} failed with status {code}")
+
+
+def _cells(f, n):
+    if not (f.is_cuda and f.dtype == torch.float64):
+        raise contract_violation("expected a float64 CUDA tensor")
+    f = f.contiguous()
+    nb = n ** 3
+    if f.numel() % nb:
+        raise contract_violation("not a whole number of velocity blocks")
+    return f, f.numel() // nb
+
+
+@dataclass
+class EsbgkParams:  # inc/esbgk.hpp:17-23
+    beta: float = -0.5
+    nu_coeff: float = 0.5 * math.pi
+    eps_weno: float = 1e-6
+
+
+@dataclass
+class PenalizationRule:  # inc/boltzmann.hpp:14-17
+    coeff: float = 2.0 * math.pi
+
+
+@dataclass
+class Thresholds:  # inc/indicators.hpp:49-55
+    eta0: float = 1e-3
+    eta1: float = 1e-2
+    delta0: float = 1e-3
+
+
+def moments_of(f, vgrid: VelocityGrid, *, sigma=False, realizability=False, l1=False, check=True, ctx=None):
+    """moments_of + second_moment + realizability_matrix + l1_distance_to_maxwellian,
+    batched.  Returns dict with 'moments' [cells,5] = (rho, ux, uy, uz, T) and the
+    requested extras ('sigma' [cells,6], 'realizability' [cells,13], 'l1' [cells])."""
+    ctx = ctx or default_context(f.device.index or 0)
+    f, nc = _cells(f, vgrid.nv)
+    dev = f.device
+    out = {"moments": torch.empty((nc, 5), dtype=torch.float64, device=dev),
+           "status": torch.empty(nc, dtype=torch.int32, device=dev)}
+    if sigma:
+        out["sigma"] = torch.empty((nc, 6), dtype=torch.float64, device=dev)
+    if realizability:
+        out["realizability"] = torch.empty((nc, 13), dtype=torch.float64, device=dev)
+    if l1:
+        out["l1"] = torch.empty(nc, dtype=torch.float64, device=dev)
+    ctx.check(ctx._lib.hk_moments_batch(ctx.h, vgrid.nv, vgrid.vmax, f.data_ptr(), nc, out["moments"].data_ptr(),
+                                        _ptr(out.get("sigma")), _ptr(out.get("realizability")), _ptr(out.get("l1")),
+                                        out["status"].data_ptr()))
+    if check:
+        _check_cells(out["status"], "moments_of")
+    return out
+
+
+def maxwellian(moments, vgrid: VelocityGrid, ctx=None):
+    """maxwellian (src/moments.cpp:88-112) for moments [cells,5]."""
+    ctx = ctx or default_context(moments.device.index or 0)
+    moments = moments.contiguous()
+    nc = moments.shape[0]
+    out = torch.empty((nc, vgrid.nv ** 3), dtype=torch.float64, device=moments.device)
+    st = torch.empty(nc, dtype=torch.int32, device=moments.device)
+    ctx.check(ctx._lib.hk_maxwellian_batch(ctx.h, vgrid.nv, vgrid.vmax, moments.data_ptr(), nc, out.data_ptr(),
+                                           st.data_ptr()))
+    _check_cells(st, "maxwellian")
+    return out
+
+
+def _eps_arg(eps, nc, dev):
+    if isinstance(eps, torch.Tensor):
+        e = eps.to(device=dev, dtype=torch.float64).contiguous()
+        assert e.numel() == nc
+        return e, 0.0
+    return None, float(eps)
+
+
+def esbgk_stage_solve(f_star, a: float, eps, params: EsbgkParams, vgrid: VelocityGrid, *, check=True, ctx=None):
+    """esbgk_stage_solve (src/esbgk.cpp:9-45), batched.  Returns (out, info) with
+    info = status | (gaussian_fallback << 8) per cell."""
+    ctx = ctx or default_context(f_star.device.index or 0)
+    f_star, nc = _cells(f_star, vgrid.nv)
+    e, es = _eps_arg(eps, nc, f_star.device)
+    out = torch.empty_like(f_star)
+    info = torch.empty(nc, dtype=torch.int32, device=f_star.device)
+    ctx.check(ctx._lib.hk_esbgk_stage_batch(ctx.h, vgrid.nv, vgrid.vmax, f_star.data_ptr(), out.data_ptr(), nc, a,
+                                            _ptr(e), es, params.beta, params.nu_coeff, info.data_ptr(), None))
+    if check:
+        _check_cells(info, "esbgk_stage_solve")
+    return out, info
+
+
+def penalized_stage_solve(f_star, a: float, eps, rule: PenalizationRule, vgrid: VelocityGrid, *, check=True,
+                          ctx=None):
+    """penalized_stage_solve (src/boltzmann.cpp:29-45), batched."""
+    ctx = ctx or default_context(f_star.device.index or 0)
+    f_star, nc = _cells(f_star, vgrid.nv)
+    e, es = _eps_arg(eps, nc, f_star.device)
+    out = torch.empty_like(f_star)
+    info = torch.empty(nc, dtype=torch.int32, device=f_star.device)
+    ctx.check(ctx._lib.hk_penalized_stage_batch(ctx.h, vgrid.nv, vgrid.vmax, f_star.data_ptr(), out.data_ptr(), nc, a,
+                                                _ptr(e), es, rule.coeff, info.data_ptr(), None))
+    if check:
+        _check_cells(info, "penalized_stage_solve")
+    return out, info
+
+
+def penalized_residual(f, kernel: SpectralKernel, vgrid: VelocityGrid, rule: PenalizationRule = PenalizationRule(),
+                       *, exact=False, check=True):
+    """penalized_residual (src/boltzmann.cpp:9-27), batched (collision incl.)."""
+    ctx = kernel.ctx
+    f, nc = _cells(f, vgrid.nv)
+    out = torch.empty_like(f)
+    st = torch.empty(nc, dtype=torch.int32, device=f.device)
+    flags = _abi.HK_COLL_EXACT if exact else 0
+    ctx.check(ctx._lib.hk_penalized_residual_batch(ctx.h, kernel.h, f.data_ptr(), out.data_ptr(), nc, rule.coeff,
+                                                   flags, st.data_ptr(), None))
+    if check:
+        _check_cells(st, "penalized_residual")
+    return out
+
+
+def classify(moments, nx: int, ny: int, dx: float, dy: float, eps_cell, r_in, th: Thresholds = Thresholds(),
+             l1=None, mu0=1.0, kappa0=1.0, signed_sum=False, ctx=None):
+    """Indicators + Algorithm 1 over a periodic grid of kinetic cells.
+    Returns (r_out int8 [cells], indicators [cells,4] = (la, lb, lc, lambda_B), status)."""
+    ctx = ctx or default_context(moments.device.index or 0)
+    dev = moments.device
+    nc = nx * ny
+    r_out = torch.empty(nc, dtype=torch.int8, device=dev)
+    ind = torch.empty((nc, 4), dtype=torch.float64, device=dev)
+    st = torch.empty(nc, dtype=torch.int32, device=dev)
+    e = eps_cell.to(device=dev, dtype=torch.float64).contiguous()
+    ctx.check(ctx._lib.hk_classify(ctx.h, nx, ny, dx, dy, moments.contiguous().data_ptr(), e.data_ptr(), _ptr(l1),
+                                   r_in.to(device=dev, dtype=torch.int8).contiguous().data_ptr(), r_out.data_ptr(),
+                                   ind.data_ptr(), st.data_ptr(), th.eta0, th.eta1, th.delta0, mu0, kappa0,
+                                   int(signed_sum)))
+    return r_out, ind, st
+
+
+def kinetic_transport_rhs_periodic(f, nx: int, ny: int, vgrid: VelocityGrid, dx: float, dy: float,
+                                   eps_weno: float = 1e-6, x_halo: int = 0, ctx=None):
+    """kinetic_transport_rhs_periodic (src/transport.cpp:51-66); with x_halo >= 2 the
+    input carries ghost columns (x-slab of a partitioned grid)."""
+    ctx = ctx or default_context(f.device.index or 0)
+    f = f.contiguous()
+    out = torch.empty((nx * ny, vgrid.nv ** 3), dtype=torch.float64, device=f.device)
+    ctx.check(ctx._lib.hk_transport_rhs(ctx.h, vgrid.nv, vgrid.vmax, f.data_ptr(), out.data_ptr(), nx, ny, x_halo, dx,
+                                        dy, eps_weno))
+    return out
+
+
+def esbgk_imex_step(f, nx, ny, vgrid: VelocityGrid, dx, dy, dt, eps_cell, params: EsbgkParams = EsbgkParams(),
+                    ctx=None):
+    """esbgk_imex_step (src/esbgk.cpp:47-99), in place on the device slab."""
+    ctx = ctx or default_context(f.device.index or 0)
+    assert f.is_contiguous()
+    e = eps_cell.to(device=f.device, dtype=torch.float64).contiguous()
+    ctx.check(ctx._lib.hk_esbgk_imex_step(ctx.h, vgrid.nv, vgrid.vmax, f.data_ptr(), nx, ny, dx, dy, dt, e.data_ptr(),
+                                          params.beta, params.nu_coeff, params.eps_weno, None))
+    return f
+
+
+def penalized_imex_step(f, nx, ny, kernel: SpectralKernel, dx, dy, dt, eps_cell,
+                        rule: PenalizationRule = PenalizationRule(), eps_weno: float = 1e-6, exact=False):
+    """penalized_imex_step (src/boltzmann.cpp:47-110), in place on the device slab."""
+    ctx = kernel.ctx
+    assert f.is_contiguous()
+    e = eps_cell.to(device=f.device, dtype=torch.float64).contiguous()
+    ctx.check(ctx._lib.hk_penalized_imex_step(ctx.h, kernel.h, f.data_ptr(), nx, ny, dx, dy, dt, e.data_ptr(),
+                                              rule.coeff, eps_weno, _abi.HK_COLL_EXACT if exact else 0, None))
+    return f
