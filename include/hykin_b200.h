@@ -170,6 +170,18 @@ int hk_esbgk_imex_step(hk_ctx ctx, int n, double vmax, double* f_dev, int nx, in
 int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int ny, double dx, double dy, double dt,
                            const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
                            double* work_dev);
+/* Transport of an x-slab [ny][nx][n^3] whose two ghost columns per side come from
+ * separate buffers left/right [ny][2][n^3] (filled by the NCCL halo exchange). */
+int hk_transport_rhs_slab(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_dev,
+                          const double* right_dev, double* out_dev, int nx, int ny, double dx, double dy,
+                          double eps_weno);
+/* Fused PR(2,2,2) combinations of src/boltzmann.cpp:60-109 (per-cell eps):
+ * op 0: out = (y - f)/a11;  op 1: out = tr + res/eps (res nullable);
+ * op 2: out = f + dt q1 + a21 k1;  op 3 (final, in place on out = f):
+ * f += dt (w q1 + w (tr + res/eps)) + w k1 + w (y - f_acc)/a22. */
+int hk_imex_combine(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, const double* eps_dev, double* out_dev,
+                    const double* f_dev, const double* y_dev, const double* q1_dev, const double* k1_dev,
+                    const double* tr_dev, const double* res_dev);
 /* out = x + a y + b z (y, z nullable): the partitioner's halo-free elementwise updates. */
 int hk_axpby(hk_ctx ctx, int64_t count, double* out_dev, const double* x_dev, double a, const double* y_dev, double b,
              const double* z_dev);

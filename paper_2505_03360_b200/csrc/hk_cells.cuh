@@ -27,7 +27,11 @@ struct TransportParams {
     int x_halo;      // 0: periodic in x; >= 2: input carries x_halo ghost columns per side
     double dx, dy, eps_weno;
 };
-int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out);
+int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh = nullptr,
+                     const double* rh = nullptr);
+int combine_launch(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, const double* eps, double* o,
+                   const double* f, const double* y, const double* q1, const double* k1, const double* tr,
+                   const double* res);
 
 // out = x + a*y + b*z (elementwise, any of y/z nullable)
 int axpby_launch(hk_ctx ctx, int64_t count, double* out, const double* x, double a, const double* y, double b,

@@ -119,12 +119,15 @@ __device__ __forceinline__ double upwind_flux_diff(double v, const double (&s)[5
 }
 
 // One thread per (cell, velocity node): 5-cell CWENO3 stencils in x and y.
+// x_halo == -2: columns -2,-1 come from `lh` [ny][2][nb], nx,nx+1 from `rh`.
 __global__ void __launch_bounds__(256) transport_kernel(TransportParams p, const double* __restrict__ f,
-                                                        double* __restrict__ out) {
+                                                        double* __restrict__ out, const double* __restrict__ lh,
+                                                        const double* __restrict__ rh) {
     const int n = p.n;
     const int64_t nb = (int64_t)n * n * n;
     const int64_t total = (int64_t)p.nx * p.ny * nb;
-    const int nxi = p.nx + 2 * p.x_halo;  // input row length (cells)
+    const int xh = p.x_halo > 0 ? p.x_halo : 0;
+    const int nxi = p.nx + 2 * xh;  // input row length (cells)
     const double dv = 2.0 * p.vmax / n;
     const double inv_dx = 1.0 / p.dx, inv_dy = 1.0 / p.dy;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -137,11 +140,17 @@ __global__ void __launch_bounds__(256) transport_kernel(TransportParams p, const
 #pragma unroll
         for (int q = -2; q <= 2; ++q) {
             int ii = i + q;
-            if (p.x_halo == 0) ii = (ii % p.nx + p.nx) % p.nx;
-            else ii += p.x_halo;
             const int jj = ((j + q) % p.ny + p.ny) % p.ny;
-            sx[q + 2] = f[((int64_t)j * nxi + ii) * nb + idx];
-            sy[q + 2] = f[((int64_t)jj * nxi + i + p.x_halo) * nb + idx];
+            if (p.x_halo < 0 && ii < 0)
+                sx[q + 2] = lh[((int64_t)j * 2 + (ii + 2)) * nb + idx];
+            else if (p.x_halo < 0 && ii >= p.nx)
+                sx[q + 2] = rh[((int64_t)j * 2 + (ii - p.nx)) * nb + idx];
+            else {
+                if (p.x_halo == 0) ii = (ii % p.nx + p.nx) % p.nx;
+                else ii += xh;
+                sx[q + 2] = f[((int64_t)j * nxi + ii) * nb + idx];
+            }
+            sy[q + 2] = f[((int64_t)jj * nxi + i + xh) * nb + idx];
         }
         out[t] = -upwind_flux_diff(vx, sx, p.eps_weno) * inv_dx - upwind_flux_diff(vy, sy, p.eps_weno) * inv_dy;
     }
@@ -169,13 +178,15 @@ int classify_launch(hk_ctx ctx, const ClassifyParams& p, const double* mom, cons
     return check_cuda(ctx, cudaGetLastError(), "classify kernel");
 }
 
-int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out) {
-    if (p.x_halo != 0 && p.x_halo < 2) return fail(ctx, HK_CONTRACT, "transport: x_halo must be 0 or >= 2");
+int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh,
+                     const double* rh) {
+    if (p.x_halo == 1 || p.x_halo < -2 || p.x_halo == -1 || (p.x_halo == -2 && (!lh || !rh)))
+        return fail(ctx, HK_CONTRACT, "transport: x_halo must be 0, -2 (separate halo buffers) or >= 2");
     const int64_t total = (int64_t)p.nx * p.ny * p.n * p.n * p.n;
     if (total <= 0) return HK_OK;
     const int64_t blocks = (total + 255) / 256;
     const int64_t cap = int64_t(ctx->sm_count) * 16;
-    transport_kernel<<<unsigned(blocks < cap ? blocks : cap), 256, 0, ctx->stream>>>(p, f, out);
+    transport_kernel<<<unsigned(blocks < cap ? blocks : cap), 256, 0, ctx->stream>>>(p, f, out, lh, rh);
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "transport kernel");
 }

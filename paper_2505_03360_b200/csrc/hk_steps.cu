@@ -82,6 +82,13 @@ int get_work(hk_ctx ctx, double* user, int64_t count, Work& w, double** owned) {
 
 }  // namespace
 
+int combine_launch(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, const double* eps, double* o,
+                   const double* f, const double* y, const double* q1, const double* k1, const double* tr,
+                   const double* res) {
+    if (op < 0 || op > 3) return fail(ctx, HK_CONTRACT, "combine: op in 0..3");
+    return combine(ctx, op, count, nb, pr222(), dt, eps, o, f, y, q1, k1, tr, res);
+}
+
 }  // namespace hk
 
 using namespace hk;
@@ -187,6 +194,21 @@ int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int n
                            double* work_dev) {
     return imex_step(ctx, k, true, k->n, k->vmax, f_dev, nx, ny, dx, dy, dt, eps_dev, 0.0, pen_coeff, eps_weno, flags,
                      work_dev);
+}
+
+int hk_transport_rhs_slab(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_dev,
+                          const double* right_dev, double* out_dev, int nx, int ny, double dx, double dy,
+                          double eps_weno) {
+    cudaSetDevice(ctx->device);
+    TransportParams p{n, vmax, nx, ny, -2, dx, dy, eps_weno};
+    return transport_launch(ctx, p, f_dev, out_dev, left_dev, right_dev);
+}
+
+int hk_imex_combine(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, const double* eps_dev, double* out_dev,
+                    const double* f_dev, const double* y_dev, const double* q1_dev, const double* k1_dev,
+                    const double* tr_dev, const double* res_dev) {
+    cudaSetDevice(ctx->device);
+    return combine_launch(ctx, op, count, nb, dt, eps_dev, out_dev, f_dev, y_dev, q1_dev, k1_dev, tr_dev, res_dev);
 }
 
 int hk_axpby(hk_ctx ctx, int64_t count, double* out_dev, const double* x_dev, double a, const double* y_dev, double b,

@@ -1,0 +1,76 @@
+"""x-slab partitioner host logic on CPU with the gloo backend (world 2 and 3):
+halo exchange == periodic neighbour columns, gather/scatter, all-reduces."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, nx, ny, nb, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_03360_b200.partition import XSlab, HALO, regime_counts, conservation_sums
+        g = torch.Generator().manual_seed(1234)
+        glob = torch.randn((ny * nx, nb), generator=g, dtype=torch.float64)
+        part = XSlab(nx, ny, world, rank)
+        loc = part.scatter(glob)
+        lh, rh = part.halo_buffers(nb, loc)
+        part.exchange(loc, lh, rh)
+        G = glob.view(ny, nx, nb)
+        li = [(part.i0 - HALO + k) % nx for k in range(HALO)]
+        ri = [(part.i0 + part.nxl + k) % nx for k in range(HALO)]
+        ok = torch.equal(lh, G[:, li]) and torch.equal(rh, G[:, ri])
+        ok = ok and torch.equal(part.gather(loc), glob)
+        # async variant
+        lh2, rh2 = part.halo_buffers(nb, loc)
+        works = part.exchange(loc, lh2, rh2, async_op=True)
+        for w in works:
+            if hasattr(w, "wait"):
+                w.wait()
+        ok = ok and torch.equal(lh2, lh) and torch.equal(rh2, rh)
+        # regime counts and conservation sums are global
+        r = (torch.arange(part.cells) + part.i0) % 3
+        counts = regime_counts(r)
+        mom = torch.ones((part.cells, 5), dtype=torch.float64)
+        sums = conservation_sums(mom)
+        ok = ok and counts.sum().item() == nx * ny and abs(sums[0].item() - nx * ny) < 1e-9
+        q.put((rank, ok, part.i0, part.nxl))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nx", [(2, 9), (3, 11)])
+def test_halo_exchange_gloo(world, nx):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, 4, 5, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok, _, _ in res), res
+    cols = sorted((i0, nxl) for _, _, i0, nxl in res)
+    assert sum(n for _, n in cols) == nx and all(cols[k][0] + cols[k][1] == cols[k + 1][0] for k in range(world - 1))
+
+
+def test_slab_bounds():
+    from paper_2505_03360_b200.partition import XSlab
+    with pytest.raises(ValueError):
+        XSlab(3, 4, 2, 0)
+    p = XSlab(512, 128, 8, 7)
+    assert p.nxl == 64 and p.i0 == 448 and p.left == 6 and p.right == 0
