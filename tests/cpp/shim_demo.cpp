@@ -1,0 +1,44 @@
+// Reference-style caller of the C++ shim: same call shapes as
+// hykin::precompute_kernel / hykin::spectral_collision.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "hykin_b200.hpp"
+
+namespace hk = hykin_b200;
+
+int main() {
+    const int n = 16;
+    const hk::VelocityGrid vg = hk::make_velocity_grid(n, 8.0);
+    const double r = 2.0 * 8.0 / (3.0 + std::sqrt(2.0));
+    const hk::SpectralKernel kern = hk::precompute_kernel(vg, n, 4, 8, r);
+    std::vector<double> f(vg.size()), q(vg.size()), qb(vg.size());
+    for (int k1 = 0; k1 < n; ++k1)
+        for (int k2 = 0; k2 < n; ++k2)
+            for (int k3 = 0; k3 < n; ++k3) {
+                const double vx = vg.node(k1), vy = vg.node(k2), vz = vg.node(k3);
+                f[vg.index(k1, k2, k3)] = std::exp(-0.5 * (vx * vx + vy * vy + vz * vz)) / std::pow(2 * M_PI, 1.5);
+            }
+    int threw = 0;
+    try {
+        hk::spectral_collision(f, kern, q);  // centred Maxwellian: the reference does not throw
+    } catch (const hk::numerical_consistency_error&) {
+        threw = 1;
+    }
+    hk::spectral_collision_batch(f, kern, qb);
+    double mx = 0, md = 0;
+    for (size_t i = 0; i < q.size(); ++i) {
+        mx = std::fmax(mx, std::fabs(f[i]));
+        md = std::fmax(md, std::fabs(q[i] - qb[i]));
+    }
+    double qmax = 0;
+    for (double v : q) qmax = std::fmax(qmax, std::fabs(v));
+    std::printf("{\"threw\": %d, \"Qmax_over_fmax\": %.3e, \"strict_vs_batch\": %.3e}\n", threw, qmax / mx, md / mx);
+    try {
+        hk::precompute_kernel(vg, n, 4, 8, 1.01 * r);
+        return 2;
+    } catch (const hk::aliasing_config_error&) {
+    }
+    return (threw == 0 && qmax / mx < 1e-3 && md / mx < 1e-12) ? 0 : 1;
+}
