@@ -6,6 +6,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <vector>
 
 #include "hk_common.cuh"
 #include "hk_internal.h"
@@ -81,6 +82,8 @@ int hk_ctx_destroy(hk_ctx ctx) {
     else cudaDeviceSynchronize();
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+    if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
     delete ctx;
     return HK_OK;
 }
@@ -283,30 +286,63 @@ int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_d
 int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host,
                             int64_t ncells, uint32_t flags, hk_cell_status* st_host) {
     if (!ctx || !k) return HK_CONTRACT;
+    if (ncells <= 0) return HK_OK;
     cudaSetDevice(ctx->device);
     const size_t nb = size_t(k->n) * k->n * k->n;
     const size_t bytes = sizeof(double) * nb * ncells;
-    // device buffers live after the scratch used by the collision launch: allocate separately
+    int st;
+    if (!ctx->s_in) {
+        if ((st = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking), "stream")) ||
+            (st = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking), "stream")))
+            return st;
+    }
     double *f_dev = nullptr, *q_dev = nullptr;
     hk_cell_status* st_dev = nullptr;
-    int st;
     if ((st = check_cuda(ctx, cudaMallocAsync(&f_dev, bytes, ctx->stream), "alloc f")) ||
         (st = check_cuda(ctx, cudaMallocAsync(&q_dev, bytes, ctx->stream), "alloc q")) ||
-        (st = check_cuda(ctx, cudaMallocAsync(&st_dev, sizeof(hk_cell_status) * (ncells + 1), ctx->stream), "alloc st")))
+        (st = check_cuda(ctx, cudaMallocAsync(&st_dev, sizeof(hk_cell_status) * ncells, ctx->stream), "alloc st")))
         return st;
-    st = check_cuda(ctx, cudaMemcpyAsync(f_dev, f_host, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D f");
     const uint32_t dflags = (flags & HK_COLL_STRICT) ? ((flags & ~HK_COLL_STRICT) | HK_COLL_EXACT) : flags;
-    if (!st) st = hk_collision_batch(ctx, k, f_dev, q_dev, ncells, dflags, st_dev);
-    if (!st) st = check_cuda(ctx, cudaMemcpyAsync(q_host, q_dev, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H q");
+    // Chunked pipeline: H2D(c+1) and D2H(c-1) overlap the collision of chunk c.
+    const int64_t chunk = ncells >= 2048 ? (ncells + 7) / 8 : ncells;
+    cudaEvent_t ready_alloc;
+    cudaEventCreateWithFlags(&ready_alloc, cudaEventDisableTiming);
+    cudaEventRecord(ready_alloc, ctx->stream);
+    cudaStreamWaitEvent(ctx->s_in, ready_alloc, 0);
+    cudaStreamWaitEvent(ctx->s_out, ready_alloc, 0);
+    std::vector<cudaEvent_t> evs;
+    for (int64_t c0 = 0; c0 < ncells && !st; c0 += chunk) {
+        const int64_t nc = (ncells - c0) < chunk ? (ncells - c0) : chunk;
+        cudaEvent_t in_done, comp_done;
+        cudaEventCreateWithFlags(&in_done, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&comp_done, cudaEventDisableTiming);
+        evs.push_back(in_done);
+        evs.push_back(comp_done);
+        st = check_cuda(ctx, cudaMemcpyAsync(f_dev + c0 * nb, f_host + c0 * nb, sizeof(double) * nb * nc,
+                                             cudaMemcpyHostToDevice, ctx->s_in), "H2D f");
+        cudaEventRecord(in_done, ctx->s_in);
+        cudaStreamWaitEvent(ctx->stream, in_done, 0);
+        if (!st) st = hk_collision_batch(ctx, k, f_dev + c0 * nb, q_dev + c0 * nb, nc, dflags, st_dev + c0);
+        cudaEventRecord(comp_done, ctx->stream);
+        cudaStreamWaitEvent(ctx->s_out, comp_done, 0);
+        if (!st)
+            st = check_cuda(ctx, cudaMemcpyAsync(q_host + c0 * nb, q_dev + c0 * nb, sizeof(double) * nb * nc,
+                                                 cudaMemcpyDeviceToHost, ctx->s_out), "D2H q");
+    }
     hk_cell_status* sh = st_host;
     std::unique_ptr<hk_cell_status[]> tmp;
     if (!sh && (flags & HK_COLL_STRICT)) {
-        tmp.reset(new hk_cell_status[ncells > 0 ? ncells : 1]);
+        tmp.reset(new hk_cell_status[ncells]);
         sh = tmp.get();
     }
     if (!st && sh)
-        st = check_cuda(ctx, cudaMemcpyAsync(sh, st_dev, sizeof(hk_cell_status) * ncells, cudaMemcpyDeviceToHost, ctx->stream), "D2H st");
-    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+        st = check_cuda(ctx, cudaMemcpyAsync(sh, st_dev, sizeof(hk_cell_status) * ncells, cudaMemcpyDeviceToHost,
+                                             ctx->stream), "D2H st");
+    int s2 = check_cuda(ctx, cudaStreamSynchronize(ctx->s_out), "sync");
+    int s3 = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+    if (!st) st = s2 ? s2 : s3;
+    for (auto e : evs) cudaEventDestroy(e);
+    cudaEventDestroy(ready_alloc);
     cudaFreeAsync(f_dev, ctx->stream);
     cudaFreeAsync(q_dev, ctx->stream);
     cudaFreeAsync(st_dev, ctx->stream);

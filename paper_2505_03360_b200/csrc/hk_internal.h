@@ -25,6 +25,8 @@ struct hk_ctx_s {
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
     std::map<int, int> max_clusters;  // key: kernel variant id
+    // copy streams of the host (e2e) entry point: H2D / D2H overlap compute
+    cudaStream_t s_in = nullptr, s_out = nullptr;
     // optional CUDA-event timing of the collision kernels (tag -> event pairs)
     bool timing = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
