@@ -932,6 +932,279 @@ __global__ void __launch_bounds__(256, 1) coll_fast_pipe_kernel(CollArgs a) {
     if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
 }
 
+// ---------------------------------------------------------------------------
+// FAST path, warp-autonomous pipeline (production kernel for N = 32).
+// Same team / slot / TMEM organisation as coll_fast_pipe_kernel, but every
+// warp is its own pipeline over ONE plane: producer warp p handles the 32
+// pencils (i1 = rP + p, i2 = lane), consumer warp c the j3 plane c; the only
+// CTA-wide barrier left is the cooperative f load of the prologue.  Next-round
+// weights are prefetched with cp.async into the producer warp's shared-memory
+// plane, so the L2 latency of the tables overlaps the current round.
+// Slot counters count warps: 8 CTAs x 4 warps = 32 arrivals per use.
+// ---------------------------------------------------------------------------
+template <int N, int C>
+__global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
+    using G = GeoP<N, C>;
+    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
+    static_assert(P == 4 && N == 32, "one plane per warp: N = 32, P = 4");
+    constexpr int64_t NB = (int64_t)N * N * N;
+    constexpr int BLK = P * N * N;
+    constexpr int64_t SLOT = (int64_t)C * BLK;
+    constexpr unsigned ARR = C * P;  // arrivals per slot use
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rvb = smem;               // consumer landing [2][P planes][N][ROW]
+    double2* Pw = smem + 2 * G::SLAB;  // producer: prologue block / per-warp weight planes
+    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * G::SLAB);  // [P]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int pw = warp & 3;  // plane of this warp (either role)
+    const bool producer = t < 128;
+    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)team * D * SLOT;
+    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
+    unsigned* done = ready + D;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    if (t < P) mbar_init(smem_u32(fbar + t), 32);
+    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * pw) << 16);
+    const uint32_t tmF = tm, tmG = tm + 4 * N;
+    const int n_entries = a.md + 1;
+    unsigned g = 0, ncell = 0;
+
+    if (producer) {
+        // ================================ PRODUCER WARP ================================
+        const int i1 = r * P + pw, i2 = lane;
+        double2* wbuf = Pw + pw * PLANE;  // [i3][lane] weights of the next round
+        const uint32_t wbuf_s = smem_u32(wbuf);
+        auto issue_w = [&](int e) {
+            const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + i2;
+#pragma unroll
+            for (int i3 = 0; i3 < N; ++i3) cp_async16(wbuf_s + (i3 * 32 + lane) * 16, wt + i3 * N);
+            cp_async_commit();
+        };
+        auto acquire = [&](unsigned gg) {
+            if (lane == 0) spin_geq(done + gg % D, ARR * (gg / D));
+            __syncwarp();
+        };
+        auto publish = [&](unsigned gg) {
+            __syncwarp();
+            if (lane == 0) signal_add(ready + gg % D);
+        };
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            // ---- prologue: f block (cooperative), 2-D forward transform of plane j3l = pw ----
+            named_bar(1, 128);  // every producer warp is done with its weight plane
+            for (int idx = t; idx < N * N * P; idx += 128) {
+                const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
+                Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
+            }
+            named_bar(1, 128);
+            {
+                double2* row = Pw + pw * PLANE + lane * ROW;  // (j3l = pw, j1 = lane)
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = row[i];
+                fft_reg<N, false>(x);
+#pragma unroll
+                for (int i = 0; i < N; ++i) row[i] = x[i];
+            }
+            __syncwarp();
+            {
+                const int j3 = r * P + pw, k2 = lane;
+                const double2* col = Pw + pw * PLANE + k2;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
+                fft_reg<N, false>(x);
+                __syncwarp();  // plane reads done: the weight prefetch may overwrite it
+                issue_w(0);
+                acquire(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int k1 = 0; k1 < N; ++k1)
+                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
+                publish(g);
+                ++g;
+            }
+            mbar_wait_parity(smem_u32(fbar + pw), ncell & 1);  // consumers put F(plane) in TMEM
+            tmem_fence_after();
+            // ---- phase A for every field ----
+            for (int e = 0; e < n_entries; ++e) {
+                cp_async_wait_all();
+                __syncwarp();
+                double2 x[N];
+#pragma unroll
+                for (int i3 = 0; i3 < N; ++i3) x[i3] = wbuf[i3 * 32 + lane];
+                __syncwarp();
+                if (e + 1 < n_entries) issue_w(e + 1);
+#pragma unroll
+                for (int c = 0; c < N / 4; ++c) {
+                    double v[8];
+                    tmem_ld16(tmF + 16 * c, v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const double2 w = x[4 * c + i];
+                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
+                    }
+                }
+                fft_reg<N, true>(x);
+                acquire(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int j3 = 0; j3 < N; ++j3)
+                    st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
+                publish(g);
+                ++g;
+            }
+        }
+    } else {
+        // ================================ CONSUMER WARP ================================
+        const int pl = pw;  // my plane: k1l (prologue) / j3l (rounds)
+        auto issue = [&](unsigned gg) {
+            if (lane == 0) spin_geq(ready + gg % D, ARR * (gg / D + 1));
+            __syncwarp();
+            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + pl * N * N;
+            const uint32_t d0 = smem_u32(Rvb + (gg & 1) * G::SLAB + pl * PLANE);
+#pragma unroll 8
+            for (int k = 0; k < N; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
+            cp_async_commit();
+        };
+        auto complete = [&](unsigned gg) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (lane == 0) signal_add_relaxed(done + gg % D);
+        };
+        if ((int64_t)team < count) issue(g);
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            // ---- prologue: forward over k3 of rows (k1l = pl, k2 = lane), F -> TMEM ----
+            complete(g);
+            {
+                const double2* row = Rvb + (g & 1) * G::SLAB + pl * PLANE + lane * ROW;
+                const int k1 = r * P + pl, k2 = lane;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = row[i];
+                fft_reg<N, false>(x);
+                const double s = 1.0 / double(NB);
+#pragma unroll
+                for (int c = 0; c < N / 4; ++c) {
+                    double v[8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        v[2 * i] = x[4 * c + i].x * s;
+                        v[2 * i + 1] = x[4 * c + i].y * s;
+                    }
+                    tmem_st16(tmF + 16 * c, v);
+                }
+                if (a.nyq) {
+                    constexpr int H = N / 2;
+                    double* ny = a.nyq + cell * 3 * N * N;
+                    ny[2 * N * N + k1 * N + k2] = s * sqrt(x[H].x * x[H].x + x[H].y * x[H].y);
+                    if (k2 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                    }
+                    if (k1 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                    }
+                }
+                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
+                tmem_wait_st();
+                tmem_fence_before();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pl)) : "memory");
+            }
+            __syncwarp();
+            issue(g + 1);  // field 0 (needs F, published above)
+            ++g;
+            // ---- phase B for every field ----
+            for (int e = 0; e < n_entries; ++e) {
+                const bool is_loss = (e == a.md);
+                double2* Rv = Rvb + (g & 1) * G::SLAB + pl * PLANE;
+                complete(g);
+                const bool more = (e + 1 < n_entries) || (it + nteams < count);
+                if (more) issue(g + 1);
+                {  // inverse FFT over i2: row i1 = lane of my j3 plane
+                    double2* row = Rv + lane * ROW;
+                    double2 y[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) y[i] = row[i];
+                    fft_reg<N, true>(y);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) row[i] = y[i];
+                }
+                __syncwarp();
+                double2 y[N];
+                {  // inverse FFT over i1: column j2 = lane
+                    const double2* col = Rv + lane;
+#pragma unroll
+                    for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
+                    fft_reg<N, true>(y);
+                }
+                __syncwarp();  // reads of this buffer complete before it is refilled
+                if (!is_loss) {
+                    const double m = (e == 0) ? a.mult0 : 1.0;
+#pragma unroll
+                    for (int c = 0; c < N / 8; ++c) {
+                        double gv[8];
+                        tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) gv[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
+                        tmem_st16(tmG + 16 * c, gv);
+                    }
+                    tmem_wait_st();
+                    ++g;
+                } else {
+                    // ---- epilogue: Q = jac (w gain - f loss) for nodes (j1, j2 = lane, j3 = rP + pl) ----
+                    double* qc = a.q + cell * NB;
+                    double mre = 0.0, n2 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < N / 8; ++c) {
+                        double gv[8];
+                        tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int j1 = 8 * c + i;
+                            const int64_t gi = ((int64_t)j1 * N + lane) * N + r * P + pl;
+                            const double qre = a.jac * (a.w * gv[i] - fc[gi] * y[j1].x);
+                            qc[gi] = qre;
+                            mre = fmax(mre, fabs(qre));
+                            n2 += qre * qre;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+                        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                    }
+                    if (lane == 0 && a.st) {
+                        hk_cell_status* sc = a.st + cell;
+                        atomic_max_nonneg(&sc->max_re, mre);
+                        atomicAdd(&sc->q_norm2, n2);
+                    }
+                    ++g;
+                }
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
 // Rigorous bound of the dropped Nyquist term of the FAST path, per cell.
 // With Y_d = alpha_a,d F and Y'_d = alpha'_a,d F supported on the Nyquist
 // set S:  |Im ga_d(j)| <= A_d = sum_S |Y_d|  and  ||Im gb_d||_2 = N^{3/2}
@@ -1117,8 +1390,9 @@ int launch_fast_tmem(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int ta
 template <int N, int C>
 int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int tag) {
     using G = GeoP<N, C>;
-    auto kern = coll_fast_pipe_kernel<N, C>;
-    const int key = N * 100 + C * 2 + 2000;
+    const bool warp_mode = !getenv("HK_PIPE_CTA");  // default: warp-autonomous kernel
+    auto kern = warp_mode ? coll_fast_warp_kernel<N, C> : coll_fast_pipe_kernel<N, C>;
+    const int key = N * 100 + C * 2 + 2000 + (warp_mode ? 1 : 0);
     int st;
     if (!ctx->max_clusters.count(key)) {
         if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
@@ -1205,11 +1479,17 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
         if ((s = launch_variant<N, C, true>(ctx, a, ncells, 0))) return s;
     } else {
         a.nyq = nyq;
-        if (N == 32 && !(flags & HK_COLL_LEGACY_FAST) && !getenv("HK_TMEM2")) {
-            if ((s = launch_fast_pipe<N, C>(ctx, a, ncells, 0))) return s;
-        } else if (N == 32 && !(flags & HK_COLL_LEGACY_FAST)) {
-            if ((s = launch_fast_tmem<N, C>(ctx, a, ncells, 0))) return s;
-        } else {
+        bool done = false;
+        if constexpr (N == 32 && C == 8) {
+            if (!(flags & HK_COLL_LEGACY_FAST) && !getenv("HK_TMEM2")) {
+                if ((s = launch_fast_pipe<N, C>(ctx, a, ncells, 0))) return s;
+                done = true;
+            } else if (!(flags & HK_COLL_LEGACY_FAST)) {
+                if ((s = launch_fast_tmem<N, C>(ctx, a, ncells, 0))) return s;
+                done = true;
+            }
+        }
+        if (!done) {
             if ((s = launch_variant<N, C, false>(ctx, a, ncells, 0))) return s;
         }
         if (guard) {
