@@ -210,12 +210,15 @@ __device__ __forceinline__ void named_bar(unsigned id, unsigned count) {
 __device__ __forceinline__ long long spin_geq(const unsigned* p, unsigned target) {
     const long long t0 = clock64();
     unsigned v;
+    // Poll with relaxed loads (no L1 invalidation per iteration), then one
+    // acquire load once the target is reached.
     for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
         if ((int)(v - target) >= 0) break;
         if (clock64() - t0 > (1LL << 32)) __trap();
-        __nanosleep(32);
+        __nanosleep(20);
     }
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return clock64() - t0;
 }
 // WAR-only signal ("I have finished reading"): the reads it orders are
@@ -225,9 +228,9 @@ __device__ __forceinline__ void signal_add_relaxed(unsigned* p) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+// RAW signal ("my stores are visible"): release at GPU scope.
 __device__ __forceinline__ void signal_add(unsigned* p) {
-    __threadfence();
-    atomicAdd(p, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(p) : "memory");
 }
 
 // Non-negative double max via its ordered bit pattern.
