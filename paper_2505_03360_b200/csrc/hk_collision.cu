@@ -645,7 +645,10 @@ struct GeoP {
     static constexpr int ROW = N + 1;
     static constexpr int PLANE = N * ROW;
     static constexpr int SLAB = P * PLANE;
-    static constexpr int D = 4;  // exchange slots in flight per team
+#ifndef HK_SLOTS
+#define HK_SLOTS 4
+#endif
+    static constexpr int D = HK_SLOTS;  // exchange slots in flight per team
     static_assert(P * N == 128, "one pencil per role thread");
     static constexpr uint32_t TM_COLS = 256;
     static constexpr size_t SMEM = size_t(3 * SLAB) * sizeof(double2) + 8 * sizeof(double) + 32;
@@ -1205,6 +1208,300 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
     if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
 }
 
+// ---------------------------------------------------------------------------
+// FAST path, split-pencil warp pipeline (production kernel for N = 32).
+// As coll_fast_warp_kernel, but every 32-point pencil is shared by the lane
+// pair (l, l ^ 16) (fftx2_dit / fftx2_dif), so a thread holds 16 complex
+// values and the CTA runs 16 warps (8 producers, 8 consumers; two warps per
+// plane) at <= 128 registers: twice the latency hiding of the 8-warp kernel.
+// Distributions: F in TMEM is parity split (output of the forward DIF),
+// phase A runs the inverse DIT (parity in, index halves out); the consumer
+// row pass uses DIF, the column pass DIT (gain nodes = index halves).
+// ---------------------------------------------------------------------------
+template <int N, int C>
+__global__ void __launch_bounds__(512, 1) coll_fast_x2_kernel(CollArgs a) {
+    using G = GeoP<N, C>;
+    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
+    static_assert(P == 4 && N == 32, "N = 32, P = 4");
+    constexpr int64_t NB = (int64_t)N * N * N;
+    constexpr int BLK = P * N * N;
+    constexpr int64_t SLOT = (int64_t)C * BLK;
+    constexpr unsigned ARR = C * 2 * P;  // warps per role per team: 8 CTAs x 8
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rvb = smem;               // consumer landing [2][P][N][ROW]
+    double2* Pw = smem + 2 * G::SLAB;  // producer prologue block / weight buffers
+    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * G::SLAB);  // [P]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const bool producer = t < 256;
+    const int rw = warp & 7;          // role-local warp
+    const int pl = rw >> 1, hp = rw & 1;
+    const int pp = 16 * hp + (lane & 15);  // pencil (row / column) index within the plane
+    const int h = lane >> 4;               // half of the pencil
+    const int pg = pl >> 1;                // TMEM column group (planes pl, pl+2 share lanes)
+    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)team * D * SLOT;
+    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
+    unsigned* done = ready + D;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    if (t < P) mbar_init(smem_u32(fbar + t), 64);
+    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t tmF = tm + 64 * pg, tmG = tm + 128 + 32 * pg;
+    const int n_entries = a.md + 1;
+    unsigned g = 0, ncell = 0;
+
+    if (producer) {
+        // ================================ PRODUCERS ================================
+        const int i1 = r * P + pl, i2 = pp;
+        double2* wbuf = Pw + pl * PLANE + hp * (N * 16);  // [i3][16 pencils]
+        const uint32_t wbuf_s = smem_u32(wbuf);
+        auto issue_w = [&](int e) {  // my 16 pencils' weights: lanes 0-15 even i3, 16-31 odd
+            const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + 16 * hp + (lane & 15);
+#pragma unroll
+            for (int m = 0; m < 16; ++m) {
+                const int i3 = 2 * m + h;
+                cp_async16(wbuf_s + (i3 * 16 + (lane & 15)) * 16, wt + i3 * N);
+            }
+            cp_async_commit();
+        };
+        auto acquire = [&](unsigned gg) {
+            if (lane == 0) spin_geq(done + gg % D, ARR * (gg / D));
+            __syncwarp();
+        };
+        auto publish = [&](unsigned gg) {
+            __syncwarp();
+            if (lane == 0) signal_add(ready + gg % D);
+        };
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            named_bar(1, 256);  // all producer warps are done with Pw
+            for (int idx = t; idx < N * N * P; idx += 256) {
+                const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
+                Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
+            }
+            named_bar(1, 256);
+            {  // forward over j2: row (j3l = pl, j1 = pp); DIF, written back parity split
+                double2* row = Pw + pl * PLANE + pp * ROW;
+                double2 v[16];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    v[j] = row[8 * h + j];
+                    v[8 + j] = row[16 + 8 * h + j];
+                }
+                fftx2_dif<false>(v, h);
+#pragma unroll
+                for (int m = 0; m < 16; ++m) row[2 * m + h] = v[m];
+            }
+            named_bar(1, 256);  // columns need every row of the plane
+            {  // forward over j1: column (j3l = pl, k2 = pp) -> exchange, k1 = 2m + h
+                const int j3 = r * P + pl, k2 = pp;
+                const double2* col = Pw + pl * PLANE + k2;
+                double2 v[16];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    v[j] = col[(8 * h + j) * ROW];
+                    v[8 + j] = col[(16 + 8 * h + j) * ROW];
+                }
+                fftx2_dif<false>(v, h);
+                named_bar(1, 256);  // Pw reads done: weight prefetch may overwrite it
+                issue_w(0);
+                acquire(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int m = 0; m < 16; ++m) {
+                    const int k1 = 2 * m + h;
+                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, v[m]);
+                }
+                publish(g);
+                ++g;
+            }
+            mbar_wait_parity(smem_u32(fbar + pl), ncell & 1);
+            tmem_fence_after();
+            for (int e = 0; e < n_entries; ++e) {
+                cp_async_wait_all();
+                __syncwarp();
+                double2 x[16];
+#pragma unroll
+                for (int m = 0; m < 16; ++m) x[m] = wbuf[(2 * m + h) * 16 + (lane & 15)];
+                __syncwarp();
+                if (e + 1 < n_entries) issue_w(e + 1);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {  // F[2m + h], m = 4c..4c+3
+                    double v[8];
+                    tmem_ld16(tmF + 16 * c, v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const double2 w = x[4 * c + i];
+                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
+                    }
+                }
+                fftx2_dit<true>(x, h);  // x[j] = Y[8h + j], x[8 + j] = Y[16 + 8h + j]
+                acquire(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int j3a = 8 * h + j, j3b = 16 + 8 * h + j;
+                    st_cg16(Xs + (int64_t)(j3a / P) * BLK + ((j3a % P) * N + i1) * N + i2, x[j]);
+                    st_cg16(Xs + (int64_t)(j3b / P) * BLK + ((j3b % P) * N + i1) * N + i2, x[8 + j]);
+                }
+                publish(g);
+                ++g;
+            }
+        }
+    } else {
+        // ================================ CONSUMERS ================================
+        const unsigned pair_bar = 2 + pl;  // the two warps of my plane
+        auto issue = [&](unsigned gg) {     // my half plane: rows [16 hp, 16 hp + 16)
+            if (lane == 0) spin_geq(ready + gg % D, ARR * (gg / D + 1));
+            __syncwarp();
+            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + pl * N * N + 16 * hp * N;
+            const uint32_t d0 = smem_u32(Rvb + (gg & 1) * G::SLAB + pl * PLANE + 16 * hp * ROW);
+#pragma unroll 8
+            for (int k = 0; k < 16; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
+            cp_async_commit();
+        };
+        auto complete = [&](unsigned gg) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (lane == 0) signal_add_relaxed(done + gg % D);
+        };
+        if ((int64_t)team < count) issue(g);
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            complete(g);
+            {  // forward over k3 of row (k1l = pl, k2 = pp): DIF -> F[2m + h] -> TMEM
+                const double2* row = Rvb + (g & 1) * G::SLAB + pl * PLANE + pp * ROW;
+                const int k1 = r * P + pl, k2 = pp;
+                double2 v[16];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    v[j] = row[8 * h + j];
+                    v[8 + j] = row[16 + 8 * h + j];
+                }
+                fftx2_dif<false>(v, h);
+                const double s = 1.0 / double(NB);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    double w8[8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        w8[2 * i] = v[4 * c + i].x * s;
+                        w8[2 * i + 1] = v[4 * c + i].y * s;
+                    }
+                    tmem_st16(tmF + 16 * c, w8);
+                }
+                if (a.nyq) {
+                    constexpr int H = N / 2;
+                    double* ny = a.nyq + cell * 3 * N * N;
+                    if (h == 0) ny[2 * N * N + k1 * N + k2] = s * sqrt(v[8].x * v[8].x + v[8].y * v[8].y);  // k3 = 16
+                    if (k2 == H) {
+#pragma unroll
+                        for (int m = 0; m < 16; ++m)
+                            ny[1 * N * N + k1 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                    }
+                    if (k1 == H) {
+#pragma unroll
+                        for (int m = 0; m < 16; ++m) ny[k2 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                    }
+                }
+                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                tmem_st16(tmG, z);
+                tmem_st16(tmG + 16, z);
+                tmem_wait_st();
+                tmem_fence_before();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pl)) : "memory");
+            }
+            named_bar(pair_bar, 64);  // both halves done with this buffer
+            issue(g + 1);
+            ++g;
+            for (int e = 0; e < n_entries; ++e) {
+                const bool is_loss = (e == a.md);
+                double2* Rv = Rvb + (g & 1) * G::SLAB + pl * PLANE;
+                complete(g);
+                const bool more = (e + 1 < n_entries) || (it + nteams < count);
+                if (more) issue(g + 1);
+                {  // inverse over i2: row i1 = pp (DIF, in place, parity split)
+                    double2* row = Rv + pp * ROW;
+                    double2 v[16];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        v[j] = row[8 * h + j];
+                        v[8 + j] = row[16 + 8 * h + j];
+                    }
+                    fftx2_dif<true>(v, h);
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) row[2 * m + h] = v[m];
+                }
+                named_bar(pair_bar, 64);  // columns need both halves' rows
+                double2 y[16];
+                {  // inverse over i1: column j2 = pp (DIT): y[j] = node j1 = 8h + j, y[8+j] = 16 + 8h + j
+                    const double2* col = Rv + pp;
+#pragma unroll
+                    for (int m = 0; m < 16; ++m) y[m] = col[(2 * m + h) * ROW];
+                    fftx2_dit<true>(y, h);
+                }
+                named_bar(pair_bar, 64);  // buffer free for the pull two exchanges ahead
+                if (!is_loss) {
+                    const double m = (e == 0) ? a.mult0 : 1.0;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        double gv[8];
+                        tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) gv[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
+                        tmem_st16(tmG + 16 * c, gv);
+                    }
+                    tmem_wait_st();
+                    ++g;
+                } else {
+                    double* qc = a.q + cell * NB;
+                    double mre = 0.0, n2 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        double gv[8];
+                        tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int jj = 8 * c + i;
+                            const int j1 = (jj < 8) ? 8 * h + jj : 16 + 8 * h + (jj - 8);
+                            const int64_t gi = ((int64_t)j1 * N + pp) * N + r * P + pl;
+                            const double qre = a.jac * (a.w * gv[i] - fc[gi] * y[jj].x);
+                            qc[gi] = qre;
+                            mre = fmax(mre, fabs(qre));
+                            n2 += qre * qre;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+                        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                    }
+                    if (lane == 0 && a.st) {
+                        hk_cell_status* sc = a.st + cell;
+                        atomic_max_nonneg(&sc->max_re, mre);
+                        atomicAdd(&sc->q_norm2, n2);
+                    }
+                    ++g;
+                }
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
 // Rigorous bound of the dropped Nyquist term of the FAST path, per cell.
 // With Y_d = alpha_a,d F and Y'_d = alpha'_a,d F supported on the Nyquist
 // set S:  |Im ga_d(j)| <= A_d = sum_S |Y_d|  and  ||Im gb_d||_2 = N^{3/2}
@@ -1390,16 +1687,20 @@ int launch_fast_tmem(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int ta
 template <int N, int C>
 int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int tag) {
     using G = GeoP<N, C>;
-    const bool warp_mode = !getenv("HK_PIPE_CTA");  // default: warp-autonomous kernel
-    auto kern = warp_mode ? coll_fast_warp_kernel<N, C> : coll_fast_pipe_kernel<N, C>;
-    const int key = N * 100 + C * 2 + 2000 + (warp_mode ? 1 : 0);
+    // default: warp-autonomous 8-warp kernel; HK_FAST_KERNEL=x2|cta selects the split-pencil
+    // 16-warp variant (measured slower: +70% instructions) or the CTA-synchronous one
+    const char* kv = getenv("HK_FAST_KERNEL");
+    const int variant = !kv ? 1 : (kv[0] == 'x' ? 2 : (kv[0] == 'c' ? 0 : 1));
+    auto kern = variant == 2 ? coll_fast_x2_kernel<N, C> : (variant == 1 ? coll_fast_warp_kernel<N, C> : coll_fast_pipe_kernel<N, C>);
+    const int nthreads = variant == 2 ? 512 : 256;
+    const int key = N * 100 + C * 2 + 2000 + variant;
     int st;
     if (!ctx->max_clusters.count(key)) {
         if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
                              "smem attribute")))
             return st;
         int per_sm = 0;
-        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, G::SMEM), "occupancy")))
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, G::SMEM), "occupancy")))
             return st;
         int teams = (per_sm >= 1 ? 1 : 0) * ctx->sm_count / C;  // one CTA per SM (TMEM, SMEM)
         if (const char* m = getenv("HK_TEAMS")) teams = atoi(m);  // experiment override
@@ -1423,7 +1724,7 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     }
     void* params[] = {&args};
     timing_begin(ctx, tag);
-    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * C)), dim3(256), params,
+    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * C)), dim3(nthreads), params,
                                                      G::SMEM, ctx->stream),
                     "pipelined collision kernel launch");
     timing_end(ctx);
