@@ -198,3 +198,39 @@ def config3_cells(nx: int, ny: int, n: int = 32, seed_salt: int = 0, cells=None)
             p3 += w * _hermite(a, Vx)[:, None, None] * _hermite(b, Vy)[None, :, None] * _hermite(cc, Vz)[None, None, :]
         out[o] = maxwellian(n, rho, (ux, uy, 0.0), T) * (1.0 + ep * p3.ravel())
     return out, fl
+
+
+def config3_cells_torch(nx: int, ny: int, n: int = 32, device="cuda", seed_salt: int = 0, chunk: int = 1024):
+    """config3_cells evaluated on the device (same fields and formula)."""
+    import torch
+
+    fl = config3_fields(nx, ny, seed_salt)
+    ncells = nx * ny
+    v = torch.as_tensor(nodes(n), dtype=torch.float64, device=device)
+    out = torch.empty((ncells, n ** 3), dtype=torch.float64, device=device)
+    par = {k: torch.as_tensor(fl[k], dtype=torch.float64, device=device) for k in ("rho", "T", "ux", "uy", "eps")}
+    coef = [float(c) for c in fl["coef"]]
+
+    def he(k, x):
+        if k == 0:
+            return torch.ones_like(x)
+        if k == 1:
+            return x
+        if k == 2:
+            return x * x - 1.0
+        return x * x * x - 3.0 * x
+
+    for s in range(0, ncells, chunk):
+        e = min(ncells, s + chunk)
+        rho, T, ux, uy, ep = (par[k][s:e, None] for k in ("rho", "T", "ux", "uy", "eps"))
+        sT = torch.sqrt(T)
+        Vx, Vy, Vz = (v[None, :] - ux) / sT, (v[None, :] - uy) / sT, v[None, :] / sT  # [c, n]
+        p3 = torch.zeros((e - s, n, n, n), dtype=torch.float64, device=device)
+        for (a, b, c), w in zip(HERMITE3, coef):
+            p3 += w * he(a, Vx)[:, :, None, None] * he(b, Vy)[:, None, :, None] * he(c, Vz)[:, None, None, :]
+        ex = torch.exp(-(v[None, :] - ux) ** 2 / (2 * T))
+        ey = torch.exp(-(v[None, :] - uy) ** 2 / (2 * T))
+        ez = torch.exp(-(v[None, :]) ** 2 / (2 * T))
+        M = (rho / (2 * math.pi * T) ** 1.5)[:, :, None, None] * ex[:, :, None, None] * ey[:, None, :, None] * ez[:, None, None, :]
+        out[s:e] = (M * (1.0 + ep[:, :, None, None] * p3)).reshape(e - s, -1)
+    return out, fl

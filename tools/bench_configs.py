@@ -1,0 +1,113 @@
+"""Measures the non-headline BASELINE configs on one B200 (JSON lines).
+
+config 1: 64 homogeneous cells, 16^3, M = 4x8 (hard spheres; the reference has
+          no 3-D Maxwell-molecule kernel), Q + forward Euler f + 0.01 Q.
+config 3: 256 x 256 cells, 32^3: moments + realizability + L1 (classifier
+          inputs), Algorithm-1 classification, ES-BGK stage (a = dt = 1e-3,
+          eps = 1e-2, beta = -1/2, nu = pi/2 rho).  HBM-bound: achieved GB/s on
+          algorithmic bytes (f read once per kernel, stage output written once).
+Times are CUDA events on the launching stream, warm, median of `--iters`.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_2505_03360_b200 as hk
+from paper_2505_03360_b200 import inputs, kinetic
+
+HBM = 6537.0  # GB/s, MEASURED_PEAKS.json
+
+
+def timed(fn, iters):
+    ts = []
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    for _ in range(iters):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def config1(iters):
+    n, a1, a2, cells = 16, 4, 8, 64
+    ctx = hk.default_context()
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    k = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    f = torch.from_numpy(inputs.config1_cells(cells, n)).cuda()
+    q = torch.empty_like(f)
+    f1 = torch.empty_like(f)
+
+    def step():
+        hk.spectral_collision(f, k, out=q)
+        ctx._lib.hk_axpby(ctx.h, f.numel(), f1.data_ptr(), f.data_ptr(), 0.01, q.data_ptr(), 0.0, None)
+
+    ms = timed(step, iters)
+    md = (a1 - 1) * a2 + 1
+    W = (2 * md + 2) * 5 * n ** 3 * math.log2(n ** 3) + (12 * md + 10) * n ** 3
+    peak = ctx.fp64_peak_tflops()
+    ach = W * cells / (ms * 1e-3) / 1e12
+    return {"config": "config1: 64 cells, 16^3, M=4x8, hard spheres, Q + forward Euler dt=0.01",
+            "path": "fast kernel + Nyquist guard (every 16^3 cell rerouted to the exact kernel)",
+            "ms_per_step": ms, "cell_updates_per_s": cells / (ms * 1e-3),
+            "roofline": {"bound": "fp64", "achieved_tflops": ach, "peak_tflops": peak, "frac": ach / peak,
+                         "note": "64 cells on 148 SMs: fill-limited (32 clusters of 2 CTAs)"}}
+
+
+def config3(iters, nx=256, ny=256):
+    n = 32
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    f, fl = inputs.config3_cells_torch(nx, ny, n)
+    cells = nx * ny
+    eps = torch.full((cells,), 1e-2, dtype=torch.float64, device="cuda")
+    r_in = torch.ones(cells, dtype=torch.int8, device="cuda")
+    th = kinetic.Thresholds(eta0=1e-3, eta1=1e-2, delta0=1e-3)
+    res = {}
+
+    def mom():
+        res["m"] = kinetic.moments_of(f, vg, realizability=True, l1=True, check=False)
+
+    def cls():
+        res["c"] = kinetic.classify(res["m"]["moments"], nx, ny, 1.0 / nx, 1.0 / ny, eps, r_in, th, l1=res["m"]["l1"])
+
+    def es():
+        res["e"] = kinetic.esbgk_stage_solve(f, 1e-3, eps, kinetic.EsbgkParams(), vg, check=False)
+
+    t_m = timed(mom, iters)
+    t_c = timed(cls, iters)
+    t_e = timed(es, iters)
+    del res["e"]
+    b_read = cells * n ** 3 * 8
+    layers = [int((res["c"][0] == k).sum()) for k in range(3)]
+    out = {"config": "config3: 256x256 cells, 32^3, classify + ES-BGK stage (a=dt=1e-3, eps=1e-2, Pr=2/3)",
+           "ms": {"moments_realizability_l1": t_m, "classify": t_c, "esbgk_stage": t_e},
+           "ms_per_step": t_m + t_c + t_e, "cell_steps_per_s": cells / ((t_m + t_c + t_e) * 1e-3),
+           "layers_after_classify": layers,
+           "roofline": {"bound": "hbm", "peak_gbs": HBM,
+                        "moments_gbs": b_read / (t_m * 1e-3) / 1e9, "moments_frac": b_read / (t_m * 1e-3) / 1e9 / HBM,
+                        "esbgk_gbs": 2 * b_read / (t_e * 1e-3) / 1e9, "esbgk_frac": 2 * b_read / (t_e * 1e-3) / 1e9 / HBM,
+                        "note": "algorithmic bytes: f read once (moments), f read + stage written (ES-BGK); the "
+                                "kernels re-read f (realizability/L1 pass, Gaussian coupling pass) from L2/HBM"}}
+    return out
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--configs", default="1,3")
+    ap.add_argument("--nx", type=int, default=256)
+    args = ap.parse_args()
+    for c in args.configs.split(","):
+        r = config1(args.iters) if c == "1" else config3(args.iters, args.nx, args.nx)
+        print(json.dumps(r), flush=True)
