@@ -1,6 +1,8 @@
 // hk_api.cu — the C-ABI (include/hykin_b200.h): contexts, kernel objects,
 // dispatch.  No CPU fallback: every entry point fails with HK_CUDA when no
 // device is usable.
+#include <cuda.h>
+
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -83,6 +85,7 @@ int hk_ctx_destroy(hk_ctx ctx) {
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
+    if (ctx->sio_flags) cudaFree(ctx->sio_flags);
     if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
     delete ctx;
     return HK_OK;
@@ -283,6 +286,120 @@ int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_d
     return check_cuda(ctx, cudaGetLastError(), "collision");
 }
 
+// Streamed variant of the host entry point (N = 32 fast path): ONE persistent
+// collision launch consumes f chunk by chunk as the H2D stream lands it
+// (device flag written by cuStreamWriteValue32 after each chunk's copy) and
+// publishes finished chunks through per-chunk counters that the D2H stream
+// waits on (cuStreamWaitValue32), so PCIe traffic in both directions overlaps
+// the whole computation.  Cells the Nyquist guard reroutes are fetched again
+// after the exact kernel.  Returns HK_UNSUPPORTED (nothing enqueued) when the
+// kernel cannot stream (caller falls back to chunked launches).
+static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host, int64_t ncells,
+                                   uint32_t flags, hk_cell_status* st_host) {
+    const size_t nb = size_t(k->n) * k->n * k->n;
+    const size_t bytes = sizeof(double) * nb * ncells;
+    const int64_t chunk = ncells >= 1024 ? (ncells + 15) / 16 : ncells;
+    const int64_t nch = (ncells + chunk - 1) / chunk;
+    double *f_dev = nullptr, *q_dev = nullptr;
+    hk_cell_status* st_dev = nullptr;
+    unsigned* flags_dev = nullptr;  // [nch] in_ready, [nch] out_done
+    int st;
+    if ((st = check_cuda(ctx, cudaMallocAsync(&f_dev, bytes, ctx->stream), "alloc f")) ||
+        (st = check_cuda(ctx, cudaMallocAsync(&q_dev, bytes, ctx->stream), "alloc q")) ||
+        (st = check_cuda(ctx, cudaMallocAsync(&st_dev, sizeof(hk_cell_status) * ncells, ctx->stream), "alloc st")))
+        return st;
+    if (ctx->sio_flags_n < 2 * nch) {
+        cudaStreamSynchronize(ctx->stream);
+        if (ctx->sio_flags) cudaFree(ctx->sio_flags);
+        ctx->sio_flags = nullptr;
+        ctx->sio_flags_n = 0;
+        if ((st = check_cuda(ctx, cudaMalloc(&ctx->sio_flags, sizeof(unsigned) * 2 * nch), "alloc flags"))) return st;
+        ctx->sio_flags_n = 2 * nch;
+    }
+    flags_dev = ctx->sio_flags;
+    cudaMemsetAsync(flags_dev, 0, sizeof(unsigned) * 2 * nch, ctx->stream);
+    cudaEvent_t e0;
+    cudaEventCreateWithFlags(&e0, cudaEventDisableTiming);
+    cudaEventRecord(e0, ctx->stream);
+    cudaStreamWaitEvent(ctx->s_in, e0, 0);
+    cudaStreamWaitEvent(ctx->s_out, e0, 0);
+    // Enqueue the copy streams first (H2D + ready flags, waits + D2H): nothing
+    // is launched until the stream memory operations are known to work.
+    const unsigned per_cell = 8u * 4u;  // consumer warps per cell (C x P of coll_fast_warp_kernel)
+    {
+        CUresult r0 = cuStreamWriteValue32((CUstream)ctx->s_in, (CUdeviceptr)flags_dev, 0, 0);
+        CUresult r1 = cuStreamWaitValue32((CUstream)ctx->s_out, (CUdeviceptr)flags_dev, 0, CU_STREAM_WAIT_VALUE_GEQ);
+        if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) {
+            if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] stream memory ops unavailable (%d, %d)\n", (int)r0, (int)r1);
+            cudaStreamSynchronize(ctx->s_in);
+            cudaStreamSynchronize(ctx->s_out);
+            cudaEventDestroy(e0);
+            cudaFreeAsync(f_dev, ctx->stream);
+            cudaFreeAsync(q_dev, ctx->stream);
+            cudaFreeAsync(st_dev, ctx->stream);
+            return HK_UNSUPPORTED;  // stream memory operations unavailable: chunked path
+        }
+    }
+    for (int64_t c = 0; c < nch && !st; ++c) {
+        const int64_t c0 = c * chunk, nc = (ncells - c0) < chunk ? (ncells - c0) : chunk;
+        st = check_cuda(ctx, cudaMemcpyAsync(f_dev + c0 * nb, f_host + c0 * nb, sizeof(double) * nb * nc,
+                                             cudaMemcpyHostToDevice, ctx->s_in), "H2D f");
+        CUresult r;
+        if (!st && (r = cuStreamWriteValue32((CUstream)ctx->s_in, (CUdeviceptr)(flags_dev + c), 1, 0)) != CUDA_SUCCESS)
+            st = fail(ctx, HK_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
+        if (!st && (r = cuStreamWaitValue32((CUstream)ctx->s_out, (CUdeviceptr)(flags_dev + nch + c),
+                                            unsigned(nc) * per_cell, CU_STREAM_WAIT_VALUE_GEQ)) != CUDA_SUCCESS)
+            st = fail(ctx, HK_CUDA, "cuStreamWaitValue32 failed: " + std::to_string((int)r));
+        if (!st)
+            st = check_cuda(ctx, cudaMemcpyAsync(q_host + c0 * nb, q_dev + c0 * nb, sizeof(double) * nb * nc,
+                                                 cudaMemcpyDeviceToHost, ctx->s_out), "D2H q");
+    }
+    if (!st) {
+        ctx->sio_in_ready = flags_dev;
+        ctx->sio_out_done = flags_dev + nch;
+        ctx->sio_chunk = chunk;
+        ctx->sio_used = false;
+        st = hk_collision_batch(ctx, k, f_dev, q_dev, ncells, flags, st_dev);
+        const bool streamed = ctx->sio_used;
+        ctx->sio_in_ready = nullptr;
+        ctx->sio_out_done = nullptr;
+        ctx->sio_used = false;
+        if (!st && !streamed) {
+            // kernel variant without streamed I/O: release the waiting D2H stream by
+            // completing the counters, then let the caller redo the batch chunked.
+            for (int64_t c = 0; c < nch; ++c)
+                cuStreamWriteValue32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
+            st = HK_UNSUPPORTED;
+        }
+    }
+    // rerouted cells: their exact Q overwrote q_dev after the streamed copy
+    int count = 0;
+    std::vector<int64_t> list;
+    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+    if (!st && ctx->last_count) {
+        st = check_cuda(ctx, cudaMemcpy(&count, ctx->last_count, sizeof(int), cudaMemcpyDeviceToHost), "D2H count");
+        if (!st && count > 0) {
+            list.resize(count);
+            st = check_cuda(ctx, cudaMemcpy(list.data(), ctx->last_list, sizeof(int64_t) * count, cudaMemcpyDeviceToHost),
+                            "D2H list");
+        }
+    }
+    for (int i = 0; i < count && !st; ++i)
+        st = check_cuda(ctx, cudaMemcpyAsync(q_host + list[i] * nb, q_dev + list[i] * nb, sizeof(double) * nb,
+                                             cudaMemcpyDeviceToHost, ctx->s_out), "D2H rerouted");
+    if (!st && st_host)
+        st = check_cuda(ctx, cudaMemcpyAsync(st_host, st_dev, sizeof(hk_cell_status) * ncells, cudaMemcpyDeviceToHost,
+                                             ctx->s_out), "D2H st");
+    const int s1 = check_cuda(ctx, cudaStreamSynchronize(ctx->s_out), "sync out");
+    const int s2 = check_cuda(ctx, cudaStreamSynchronize(ctx->s_in), "sync in");
+    if (!st) st = s1 ? s1 : s2;
+    cudaEventDestroy(e0);
+    cudaFreeAsync(f_dev, ctx->stream);
+    cudaFreeAsync(q_dev, ctx->stream);
+    cudaFreeAsync(st_dev, ctx->stream);
+    return st;
+}
+
 int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host,
                             int64_t ncells, uint32_t flags, hk_cell_status* st_host) {
     if (!ctx || !k) return HK_CONTRACT;
@@ -295,6 +412,11 @@ int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, doubl
         if ((st = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_in, cudaStreamNonBlocking), "stream")) ||
             (st = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking), "stream")))
             return st;
+    }
+    if (k->n == 32 && !(flags & (HK_COLL_EXACT | HK_COLL_STRICT)) && ncells >= 256 && !getenv("HK_NO_STREAMED_IO")) {
+        st = collision_host_streamed(ctx, k, f_host, q_host, ncells, flags, st_host);
+        if (st != HK_UNSUPPORTED) return st;
+        cudaStreamSynchronize(ctx->stream);
     }
     double *f_dev = nullptr, *q_dev = nullptr;
     hk_cell_status* st_dev = nullptr;

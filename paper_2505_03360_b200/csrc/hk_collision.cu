@@ -55,6 +55,12 @@ struct CollArgs {
     double2* xchg;     // [cluster][2 buffers][2 fields][C dest][P][N][N] L2 transpose scratch
     unsigned* team_ctr;  // [teams] barrier counters (team kernel), zeroed per launch
     unsigned long long* prof;  // optional [4]: producer spin, consumer spin, producer total, consumer total (cycles)
+    // streamed host I/O (warp kernel): chunk c of `chunk` cells may be read once
+    // in_ready[c] >= 1 (set by the H2D stream); out_done[c] counts finished
+    // consumer-warp epilogues (the D2H stream waits for chunk * C * P).
+    const unsigned* in_ready;
+    unsigned* out_done;
+    int64_t chunk;
 };
 
 template <int N, int C>
@@ -1004,6 +1010,7 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
             const int64_t cell = a.list ? a.list[it] : it;
             const double* fc = a.f + cell * NB;
             // ---- prologue: f block (cooperative), 2-D forward transform of plane j3l = pw ----
+            if (a.in_ready && t == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);  // host chunk has landed
             named_bar(1, 128);  // every producer warp is done with its weight plane
             for (int idx = t; idx < N * N * P; idx += 128) {
                 const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
@@ -1197,6 +1204,8 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                         atomic_max_nonneg(&sc->max_re, mre);
                         atomicAdd(&sc->q_norm2, n2);
                     }
+                    __syncwarp();
+                    if (lane == 0 && a.out_done) signal_add(a.out_done + cell / a.chunk);  // q rows visible
                     ++g;
                 }
             }
@@ -1712,6 +1721,12 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     if (max_cells < teams) teams = max_cells;
     if (teams < 1) return HK_OK;
     CollArgs args = args_in;
+    if (variant == 1 && ctx->sio_in_ready) {  // streamed host I/O (warp kernel only)
+        args.in_ready = ctx->sio_in_ready;
+        args.out_done = ctx->sio_out_done;
+        args.chunk = ctx->sio_chunk;
+        ctx->sio_used = true;
+    }
     if ((st = check_cuda(ctx, cudaMemsetAsync(args.team_ctr, 0, sizeof(unsigned) * 2 * G::D * teams, ctx->stream),
                          "team counters")))
         return st;
@@ -1775,6 +1790,8 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     a.w = k->weight;
     a.st = st;
     a.xchg = reinterpret_cast<double2*>(base + xchg_off);
+    ctx->last_list = list;
+    ctx->last_count = guard ? count : nullptr;
     a.team_ctr = reinterpret_cast<unsigned*>(base + xchg_off + xchg_bytes - 65536);
     if (exact) {
         if ((s = launch_variant<N, C, true>(ctx, a, ncells, 0))) return s;

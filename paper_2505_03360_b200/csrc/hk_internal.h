@@ -27,6 +27,16 @@ struct hk_ctx_s {
     std::map<int, int> max_clusters;  // key: kernel variant id
     // copy streams of the host (e2e) entry point: H2D / D2H overlap compute
     cudaStream_t s_in = nullptr, s_out = nullptr;
+    // streamed-I/O flags for the next collision launch (host entry point), and
+    // the guard's reroute list / count of the last launch (device pointers)
+    const unsigned* sio_in_ready = nullptr;
+    unsigned* sio_out_done = nullptr;
+    int64_t sio_chunk = 0;
+    bool sio_used = false;  // set by the launcher when the kernel honoured the flags
+    unsigned* sio_flags = nullptr;  // cudaMalloc'd (stream memory ops reject pool memory)
+    int64_t sio_flags_n = 0;
+    int64_t* last_list = nullptr;
+    int* last_count = nullptr;
     // optional CUDA-event timing of the collision kernels (tag -> event pairs)
     bool timing = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;

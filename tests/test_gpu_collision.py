@@ -120,3 +120,20 @@ def test_n32_host_path(n32, hk):
     q = hk.spectral_collision(np.ascontiguousarray(n32["f"]), n32["kern"])
     for c in range(len(q)):
         assert rel_l2(q[c], n32["q_ref"][c]) < TOL, c
+
+
+def test_n32_streamed_host_path_matches_device_path(hk):
+    """The e2e entry point (one persistent launch fed chunk by chunk from pinned
+    host memory, results streamed back) gives the device path's Q bitwise,
+    including the cells the Nyquist guard reroutes."""
+    import torch
+    vg = hk.make_velocity_grid(32, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, 32, 8, 8, inputs.R_PHYS_MAX)
+    f = inputs.config2_cells_torch(1100, 32, device="cuda")
+    q_dev, st_dev = hk.spectral_collision(f, kern, return_status=True)
+    fh = f.cpu().pin_memory()
+    qh = torch.empty_like(fh).pin_memory()
+    q_host, st_host = hk.spectral_collision(fh.numpy(), kern, out=qh.numpy(), return_status=True)
+    assert np.array_equal(q_host, q_dev.cpu().numpy())
+    assert np.array_equal(st_host["flags"], st_dev["flags"])
+    assert (st_host["flags"] & 4).sum() > 0  # some cells rerouted: the re-fetch path ran
