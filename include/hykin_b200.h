@@ -107,7 +107,7 @@ int hk_kernel_info(hk_kernel k, double* out6);
  * Re Q per cell.  st_dev (nullable) receives one hk_cell_status per cell.
  * Default: fast path (Hermitian-packed, one complex 3-D transform per
  * direction) with a rigorous per-cell Nyquist guard that reroutes any cell
- * whose dropped term could exceed 1e-11 relative L2 to the exact path.
+ * whose dropped term could exceed 5e-11 relative L2 to the exact path.
  * HK_COLL_STRICT returns HK_NUMERICAL_CONSISTENCY (hk_last_error gives the
  * lowest failing cell) when any cell's residue exceeds 1e-10, after writing
  * q_dev for every cell — the reference's throw-after-write behaviour. */
