@@ -186,6 +186,27 @@ int hk_imex_combine(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, co
 int hk_axpby(hk_ctx ctx, int64_t count, double* out_dev, const double* x_dev, double a, const double* y_dev, double b,
              const double* z_dev);
 
+/* ---- multi-GPU: NCCL communicator of a context ------------
+ * One process per GPU.  Rank 0 calls hk_comm_unique_id, the host side ships
+ * the 128 opaque bytes to every rank (MPI / torch.distributed / a file), and
+ * each rank calls hk_ctx_comm_init on its context.  NCCL is loaded at run
+ * time (libnccl.so.2); HK_NCCL if it is absent or a collective fails. */
+#define HK_COMM_ID_BYTES 128
+int hk_comm_unique_id(void* id_out /* HK_COMM_ID_BYTES */);
+int hk_ctx_comm_init(hk_ctx ctx, int nranks, int rank, const void* id /* HK_COMM_ID_BYTES */);
+int hk_ctx_comm_info(hk_ctx ctx, int* nranks, int* rank);
+/* x-slab halo exchange before a transport sweep (kinetic_transport_rhs_periodic's
+ * neighbour reads, src/transport.cpp:51-66, across ranks).  f: [ny][nx_local][n^3];
+ * left <- last two columns of rank-1, right <- first two columns of rank+1
+ * (periodic over ranks), each [ny][2][n^3] — the layout hk_transport_rhs_slab reads. */
+int hk_halo_exchange(hk_ctx ctx, int n, const double* f_dev, int64_t nx_local, int64_t ny, double* left_dev,
+                     double* right_dev);
+/* In-place all-reduce of `count` doubles over the context's ranks: regime counts,
+ * conservation sums (HK_REDUCE_SUM), CFL / residual maxima (HK_REDUCE_MAX). */
+#define HK_REDUCE_SUM 0
+#define HK_REDUCE_MAX 1
+int hk_allreduce_scalars(hk_ctx ctx, double* buf_dev, int64_t count, int op);
+
 /* ---- diagnostics ---------------------------------------------------------- */
 /* fp64 FMA peak of this device (DFMA microbenchmark), TFLOP/s. */
 double hk_measure_fp64_peak(hk_ctx ctx);

@@ -117,6 +117,33 @@ class Context:
     def fp64_peak_tflops(self) -> float:
         return float(self._lib.hk_measure_fp64_peak(self.h))
 
+    # ---- native NCCL communicator (hk_comm.cu) ----
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """128 opaque bytes (ncclGetUniqueId) that rank 0 ships to every rank."""
+        buf = C.create_string_buffer(_abi.HK_COMM_ID_BYTES)
+        st = _abi.lib().hk_comm_unique_id(buf)
+        if st:
+            raise device_error(f"hk_comm_unique_id failed with status {st} (libnccl.so.2 missing?)")
+        return buf.raw
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        if len(uid) != _abi.HK_COMM_ID_BYTES:
+            raise contract_violation("communicator id must be 128 bytes")
+        self.check(self._lib.hk_ctx_comm_init(self.h, nranks, rank, C.c_char_p(uid)))
+
+    def halo_exchange(self, f, n: int, nx_local: int, ny: int, left, right):
+        """x-slab halos over the context's communicator: f [ny][nx_local][n^3],
+        left/right [ny][2][n^3] (torch CUDA tensors, fp64, contiguous)."""
+        self.check(self._lib.hk_halo_exchange(self.h, n, C.c_void_p(f.data_ptr()), nx_local, ny,
+                                              C.c_void_p(left.data_ptr()), C.c_void_p(right.data_ptr())))
+
+    def allreduce_(self, buf, op: str = "sum"):
+        """In-place all-reduce of a CUDA fp64 tensor over the context's ranks."""
+        code = {"sum": _abi.HK_REDUCE_SUM, "max": _abi.HK_REDUCE_MAX}[op]
+        self.check(self._lib.hk_allreduce_scalars(self.h, C.c_void_p(buf.data_ptr()), buf.numel(), code))
+        return buf
+
     def __del__(self):
         if getattr(self, "h", None):
             try:

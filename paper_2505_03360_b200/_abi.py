@@ -24,6 +24,10 @@ HK_NCCL = 7
 HK_POSITIVITY = 8
 HK_UNSUPPORTED = 9
 
+HK_COMM_ID_BYTES = 128
+HK_REDUCE_SUM = 0
+HK_REDUCE_MAX = 1
+
 HK_CELL_EXACT = 1
 HK_CELL_RESIDUE = 2
 HK_CELL_GUARD_REROUTED = 4
@@ -90,6 +94,11 @@ def lib() -> C.CDLL:
         "hk_axpby": (C.c_int, [vp, i64, vp, vp, dbl, vp, dbl, vp]),
         "hk_transport_rhs_slab": (C.c_int, [vp, C.c_int, dbl, vp, vp, vp, vp, C.c_int, C.c_int, dbl, dbl, dbl]),
         "hk_imex_combine": (C.c_int, [vp, C.c_int, i64, i64, dbl, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "hk_comm_unique_id": (C.c_int, [vp]),
+        "hk_ctx_comm_init": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+        "hk_ctx_comm_info": (C.c_int, [vp, vp, vp]),
+        "hk_halo_exchange": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp]),
+        "hk_allreduce_scalars": (C.c_int, [vp, vp, i64, C.c_int]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

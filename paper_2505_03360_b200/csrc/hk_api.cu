@@ -82,6 +82,7 @@ int hk_ctx_destroy(hk_ctx ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
+    comm_destroy(ctx);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
@@ -152,7 +153,7 @@ static int kernel_common(hk_ctx ctx, int n, int a1, int a2, double vmax, double 
     if (r_phys > r_max * (1.0 + 1e-12))
         return fail(ctx, HK_ALIASING, "support radius exceeds the aliasing bound 2L/(3+sqrt(2))");
     if (r_phys <= 0.0) return fail(ctx, HK_CONFIG, "support radius must be positive");
-    if (n != 16 && n != 32) return fail(ctx, HK_UNSUPPORTED, "device collision path supports n = 16, 32");
+    if (n != 16 && n != 32 && n != 64) return fail(ctx, HK_UNSUPPORTED, "device collision path supports n = 16, 32, 64");
     auto* k = new hk_kernel_s;
     k->ctx = ctx;
     k->n = n;
@@ -294,8 +295,29 @@ int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_d
 // the whole computation.  Cells the Nyquist guard reroutes are fetched again
 // after the exact kernel.  Returns HK_UNSUPPORTED (nothing enqueued) when the
 // kernel cannot stream (caller falls back to chunked launches).
+// Stream memory operations come from the driver API; they are resolved at
+// run time through the runtime's entry-point query so that the library does
+// not link libcuda (it must load on hosts without a driver: CPU test suite).
+using PfnStreamValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PfnStreamValue32 p_write_value32 = nullptr, p_wait_value32 = nullptr;
+static bool stream_memops_available() {
+    static int state = -1;
+    if (state < 0) {
+        void *w = nullptr, *v = nullptr;
+        cudaDriverEntryPointQueryResult qw, qv;
+        const bool ok = cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &qw) == cudaSuccess &&
+                        cudaGetDriverEntryPoint("cuStreamWaitValue32", &v, cudaEnableDefault, &qv) == cudaSuccess &&
+                        qw == cudaDriverEntryPointSuccess && qv == cudaDriverEntryPointSuccess && w && v;
+        p_write_value32 = reinterpret_cast<PfnStreamValue32>(w);
+        p_wait_value32 = reinterpret_cast<PfnStreamValue32>(v);
+        state = ok ? 1 : 0;
+    }
+    return state == 1;
+}
+
 static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host, int64_t ncells,
                                    uint32_t flags, hk_cell_status* st_host) {
+    if (!stream_memops_available()) return HK_UNSUPPORTED;
     const size_t nb = size_t(k->n) * k->n * k->n;
     const size_t bytes = sizeof(double) * nb * ncells;
     const int64_t chunk = ncells >= 1024 ? (ncells + 15) / 16 : ncells;
@@ -327,8 +349,8 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
     // is launched until the stream memory operations are known to work.
     const unsigned per_cell = 8u * 4u;  // consumer warps per cell (C x P of coll_fast_warp_kernel)
     {
-        CUresult r0 = cuStreamWriteValue32((CUstream)ctx->s_in, (CUdeviceptr)flags_dev, 0, 0);
-        CUresult r1 = cuStreamWaitValue32((CUstream)ctx->s_out, (CUdeviceptr)flags_dev, 0, CU_STREAM_WAIT_VALUE_GEQ);
+        CUresult r0 = p_write_value32((CUstream)ctx->s_in, (CUdeviceptr)flags_dev, 0, 0);
+        CUresult r1 = p_wait_value32((CUstream)ctx->s_out, (CUdeviceptr)flags_dev, 0, CU_STREAM_WAIT_VALUE_GEQ);
         if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) {
             if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] stream memory ops unavailable (%d, %d)\n", (int)r0, (int)r1);
             cudaStreamSynchronize(ctx->s_in);
@@ -345,9 +367,9 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
         st = check_cuda(ctx, cudaMemcpyAsync(f_dev + c0 * nb, f_host + c0 * nb, sizeof(double) * nb * nc,
                                              cudaMemcpyHostToDevice, ctx->s_in), "H2D f");
         CUresult r;
-        if (!st && (r = cuStreamWriteValue32((CUstream)ctx->s_in, (CUdeviceptr)(flags_dev + c), 1, 0)) != CUDA_SUCCESS)
+        if (!st && (r = p_write_value32((CUstream)ctx->s_in, (CUdeviceptr)(flags_dev + c), 1, 0)) != CUDA_SUCCESS)
             st = fail(ctx, HK_CUDA, "cuStreamWriteValue32 failed: " + std::to_string((int)r));
-        if (!st && (r = cuStreamWaitValue32((CUstream)ctx->s_out, (CUdeviceptr)(flags_dev + nch + c),
+        if (!st && (r = p_wait_value32((CUstream)ctx->s_out, (CUdeviceptr)(flags_dev + nch + c),
                                             unsigned(nc) * per_cell, CU_STREAM_WAIT_VALUE_GEQ)) != CUDA_SUCCESS)
             st = fail(ctx, HK_CUDA, "cuStreamWaitValue32 failed: " + std::to_string((int)r));
         if (!st)
@@ -368,7 +390,7 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
             // kernel variant without streamed I/O: release the waiting D2H stream by
             // completing the counters, then let the caller redo the batch chunked.
             for (int64_t c = 0; c < nch; ++c)
-                cuStreamWriteValue32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
+                p_write_value32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
             st = HK_UNSUPPORTED;
         }
     }

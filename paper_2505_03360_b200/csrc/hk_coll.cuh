@@ -1,0 +1,44 @@
+// hk_coll.cuh — arguments shared by the collision kernels (hk_collision.cu,
+// hk_coll64.cu) and the N = 64 launcher.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "hk_internal.h"
+
+namespace hk {
+
+struct CollArgs {
+    const double* f;
+    double* q;
+    int64_t ncells;
+    const int64_t* list;    // optional cell list (rerouted cells)
+    const int* list_count;  // device count for `list`
+    const double* alpha;
+    const double* alpha_p;
+    const double* loss;
+    const double2* wfast;
+    int md;
+    double mult0, jac, w;
+    hk_cell_status* st;
+    double* nyq;       // [cell][3][N][N] |F| on the Nyquist planes (FAST) or null
+    double2* xchg;     // [cluster][2 buffers][2 fields][C dest][P][N][N] L2 transpose scratch
+    unsigned* team_ctr;  // [teams] barrier counters (team kernel), zeroed per launch
+    unsigned long long* prof;  // optional [4]: producer spin, consumer spin, producer total, consumer total (cycles)
+    // streamed host I/O (warp kernel): chunk c of `chunk` cells may be read once
+    // in_ready[c] >= 1 (set by the H2D stream); out_done[c] counts finished
+    // consumer-warp epilogues (the D2H stream waits for chunk * C * P).
+    const unsigned* in_ready;
+    unsigned* out_done;
+    int64_t chunk;
+};
+
+// hk_coll64.cu: N = 64 team kernel (C = 32 CTAs per cell, cooperative launch).
+// Bytes of exchange scratch per launch, and the launcher (exact = two complex
+// transforms per direction, reference arithmetic; else the Hermitian-packed
+// fast path that writes |F| on the Nyquist planes to args.nyq for the guard).
+size_t coll64_xchg_bytes(hk_ctx ctx);
+int launch_coll64(hk_ctx ctx, const CollArgs& args, bool exact, int64_t max_cells, int tag);
+
+}  // namespace hk

@@ -1,0 +1,494 @@
+// hk_coll64.cu — collision operator at N = 64 (config 5), sm_100a.
+//
+// Same operator as hk_collision.cu (spectral_collision, src/spectral.cpp:114-154;
+// FftWorkspace3d, src/fft.cpp:49-81), re-partitioned for a 64^3 cell whose
+// spectrum (4 MiB complex) no longer fits one SM:
+//
+//   * a TEAM of C = 32 CTAs (one per SM, cooperative launch, 4 teams = 128
+//     SMs) evaluates one cell at a time; CTA r owns P = 2 planes: i1 planes
+//     rP..rP+1 of the spectrum (producer side) and j3 planes of the nodal
+//     fields (consumer side);
+//   * F for the CTA's two i1 planes lives in TMEM (256 of 512 columns), the
+//     gain accumulators of its two j3 planes in the rest;
+//   * every 64-point pencil is split over the lane pair (l, l ^ 16): a thread
+//     holds 32 complex values (fftxh_dit / fftxh_dif), so one warp covers 16
+//     pencils and four warps a whole plane;
+//   * warps 0-3 produce (weights x F, inverse FFT over i3, 16-byte st.cg into
+//     an L2 exchange slot), warps 4-7 consume one j3 plane at a time (cp.async
+//     pull, double-buffered; inverse FFT over i2, then i1; product; gain);
+//     producers and consumers of a team synchronise with per-slot ready/done
+//     counters in global memory (release / relaxed-poll acquire, D slots).
+//
+// FAST (default): one Hermitian-packed transform per distinct direction,
+// IFFT(F (alpha_s + i alpha'_s)) = gs + i hs, gain += m gs hs; the dropped
+// Nyquist term is bounded per cell by guard_kernel and failing cells are
+// recomputed by EXACT.  EXACT: the reference's arithmetic, two complex
+// transforms per direction (alpha F, alpha' F) and a complex gain; the ga
+// field is parked in its landing buffer until gb arrives.
+#include <cstdio>
+#include <cstdlib>
+
+#include "hk_coll.cuh"
+#include "hk_common.cuh"
+
+namespace hk {
+
+struct Geo64 {
+    static constexpr int N = 64, C = 32, P = 2, M = 32, Q = 16;
+    static constexpr int ROW = N + 1;           // padded SMEM row (conflict-free columns)
+    static constexpr int PLANE = N * ROW;       // double2 per landing plane
+    static constexpr int D = 4;                 // exchange slots per team
+    static constexpr int64_t NB = (int64_t)N * N * N;
+    static constexpr int BLK = P * N * N;       // double2 per destination CTA per field
+    static constexpr int64_t SLOT = (int64_t)C * BLK;
+    static constexpr unsigned ARR = C * 4;      // warp arrivals per slot use (each role)
+    static constexpr uint32_t TM_COLS = 512;
+    static constexpr size_t SMEM = size_t(3 * PLANE) * sizeof(double2) + 64;
+    static constexpr size_t XCHG_PER_TEAM = size_t(D) * SLOT * sizeof(double2);
+};
+
+template <bool EXACT>
+__global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
+    using G = Geo64;
+    constexpr int N = G::N, C = G::C, P = G::P, M = G::M, Q = G::Q, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
+    constexpr int64_t NB = G::NB;
+    constexpr int BLK = G::BLK;
+    constexpr int64_t SLOT = G::SLOT;
+    constexpr unsigned ARR = G::ARR;
+    constexpr int GCOLS = EXACT ? 128 : 64;  // TMEM columns of gain per plane
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rvb = smem;              // consumer landing planes [2][N][ROW]
+    double2* Pw = smem + 2 * PLANE;   // producer: prologue plane / weight staging
+    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * PLANE);  // [P] F-plane ready
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int rw = warp & 3;                 // role-local warp == TMEM lane quarter
+    const int pp = 16 * rw + (lane & 15);    // pencil (row / column) within a plane
+    const int h = lane >> 4;                 // half of the pencil
+    const int u = t & 127;
+    const bool producer = t < 128;
+    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)team * D * SLOT;
+    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
+    unsigned* done = ready + D;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    if (t < P) mbar_init(smem_u32(fbar + t), 128);
+    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * rw) << 16);
+    const uint32_t tmF = tm, tmG = tm + 256;  // F plane pl: +128 pl; gain plane pl: +GCOLS pl
+    const int nfields = EXACT ? 2 * a.md + 1 : a.md + 1;
+    unsigned g = 0, ncell = 0;
+
+    if (producer) {
+        // ================================ PRODUCERS ================================
+        // Weight staging: thread-private slots [m][u] (interleaved: conflict-free).
+        const uint32_t wb_s = smem_u32(Pw);
+        auto issue_w = [&](int fi, int pl) {
+            const int i1 = r * P + pl;
+            if constexpr (!EXACT) {
+                const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N + pp;
+#pragma unroll
+                for (int m = 0; m < M; ++m) cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N);
+            } else {
+                const double* base = (fi == 2 * a.md) ? a.loss : ((fi & 1) ? a.alpha_p : a.alpha) + (int64_t)(fi >> 1) * NB;
+                const double* wt = base + (int64_t)i1 * N * N + pp;
+#pragma unroll
+                for (int m = 0; m < M; ++m) cp_async8(wb_s + (m * 128 + u) * 8, wt + (2 * m + h) * N);
+            }
+            cp_async_commit();
+        };
+        auto acquire = [&](unsigned gg) {
+            if (lane == 0) spin_geq(done + gg % D, ARR * (gg / D));
+            __syncwarp();
+        };
+        auto publish = [&](unsigned gg) {
+            __syncwarp();
+            if (lane == 0) signal_add(ready + gg % D);
+        };
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            // ---- prologue: per j3 plane, 2-D forward transform (j2 then j1) -> owner of k1 ----
+            for (int pl = 0; pl < P; ++pl) {
+                const int j3 = r * P + pl;
+                named_bar(1, 128);  // Pw free
+                for (int idx = u; idx < N * N; idx += 128)
+                    Pw[(idx / N) * ROW + (idx % N)] = make_double2(fc[(int64_t)idx * N + j3], 0.0);
+                named_bar(1, 128);
+                {  // rows j1 = pp over j2 (DIF), back in natural order
+                    double2* row = Pw + pp * ROW;
+                    double2 v[M];
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        v[j] = row[h * Q + j];
+                        v[Q + j] = row[M + h * Q + j];
+                    }
+                    fftxh_dif<M, false>(v, h);
+                    __syncwarp();
+#pragma unroll
+                    for (int m = 0; m < M; ++m) row[2 * m + h] = v[m];
+                }
+                named_bar(1, 128);  // columns need every row
+                {  // columns k2 = pp over j1 (DIT): v[j] = K1 index hQ + j, v[Q + j] = M + hQ + j
+                    const double2* col = Pw + pp;
+                    double2 v[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) v[m] = col[(2 * m + h) * ROW];
+                    fftxh_dit<M, false>(v, h);
+                    if (pl == 0) acquire(g);
+                    double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        const int ka = h * Q + j, kb = M + h * Q + j;
+                        st_cg16(Xs + (int64_t)(ka / P) * BLK + ((ka % P) * N + pp) * N + j3, v[j]);
+                        st_cg16(Xs + (int64_t)(kb / P) * BLK + ((kb % P) * N + pp) * N + j3, v[Q + j]);
+                    }
+                }
+            }
+            publish(g);
+            ++g;
+            named_bar(1, 128);  // prologue reads of Pw done: weight staging may overwrite it
+            issue_w(0, 0);
+            // ---- phase A: X = F * weights, inverse FFT over i3, -> owner of j3 ----
+            for (int fi = 0; fi < nfields; ++fi) {
+#pragma unroll 1
+                for (int pl = 0; pl < P; ++pl) {
+                    if (fi == 0) {
+                        mbar_wait_parity(smem_u32(fbar + pl), ncell & 1);  // consumers put F(plane) in TMEM
+                        tmem_fence_after();
+                    }
+                    cp_async_wait_all();
+                    __syncwarp();
+                    double2 x[M];
+                    if constexpr (!EXACT) {
+                        const double2* wb = Pw;
+#pragma unroll
+                        for (int m = 0; m < M; ++m) x[m] = wb[m * 128 + u];
+                    } else {
+                        const double* wb = reinterpret_cast<const double*>(Pw);
+#pragma unroll
+                        for (int m = 0; m < M; ++m) x[m] = make_double2(wb[m * 128 + u], 0.0);
+                    }
+                    __syncwarp();
+                    if (pl + 1 < P)
+                        issue_w(fi, pl + 1);
+                    else if (fi + 1 < nfields)
+                        issue_w(fi + 1, 0);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {  // F[2m + h], m = 4c .. 4c + 3
+                        double v[8];
+                        tmem_ld16(tmF + 128 * pl + 16 * c, v);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const double2 w = x[4 * c + i];
+                            if constexpr (!EXACT)
+                                x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
+                            else
+                                x[4 * c + i] = make_double2(v[2 * i] * w.x, v[2 * i + 1] * w.x);
+                        }
+                    }
+                    fftxh_dit<M, true>(x, h);  // x[j] = Y[hQ + j], x[Q + j] = Y[M + hQ + j]
+                    if (pl == 0) acquire(g);
+                    double2* Xs = X + (int64_t)(g % D) * SLOT;
+                    const int i1 = r * P + pl;
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        const int ja = h * Q + j, jb = M + h * Q + j;
+                        st_cg16(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j]);
+                        st_cg16(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j]);
+                    }
+                }
+                publish(g);
+                ++g;
+            }
+        }
+    } else {
+        // ================================ CONSUMERS ================================
+        // Units: (field, plane) pulls in a fixed order per cell; unit k lands in
+        // Rvb[k & 1] (units per cell is even).  Field 0 is the prologue.
+        const int upc = 2 * (1 + nfields);
+        auto unit_of = [&](int k, int& fi, int& pl) {
+            if (k < 2) {
+                fi = 0;
+                pl = k;
+                return;
+            }
+            const int j = k - 2;
+            if (EXACT && j < 4 * a.md) {  // (ga, p0) (gb, p0) (ga, p1) (gb, p1) per direction
+                fi = 1 + 2 * (j >> 2) + (j & 1);
+                pl = (j >> 1) & 1;
+            } else {
+                const int jj = EXACT ? j - 4 * a.md : j;
+                fi = (EXACT ? 1 + 2 * a.md : 1) + (jj >> 1);
+                pl = jj & 1;
+            }
+        };
+        auto issue = [&](unsigned gs, int pl, int buf) {  // my 16 rows of (slot gs, plane pl)
+            if (lane == 0) spin_geq(ready + gs % D, ARR * (gs / D + 1));
+            __syncwarp();
+            const double2* src = X + (int64_t)(gs % D) * SLOT + (int64_t)r * BLK + (int64_t)pl * N * N + 16 * rw * N;
+            const uint32_t d0 = smem_u32(Rvb + buf * PLANE + 16 * rw * ROW);
+#pragma unroll 4
+            for (int k = 0; k < 16; ++k) {
+                cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
+                cp_async16(d0 + (k * ROW + 32 + lane) * 16, src + k * N + 32 + lane);
+            }
+            cp_async_commit();
+        };
+        auto complete = [&](unsigned gs, int pl) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (pl == P - 1 && lane == 0) signal_add_relaxed(done + gs % D);  // last pull of this slot
+            named_bar(2, 128);  // every warp's rows have landed; previous unit fully consumed
+        };
+        if ((int64_t)team < count) issue(0, 0, 0);
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            const unsigned gb = ncell * (1 + nfields);
+            const bool more_cells = it + nteams < count;
+            double mre = 0.0, mim = 0.0, n2 = 0.0;
+#pragma unroll 1
+            for (int k = 0; k < upc; ++k) {
+                int fi, pl;
+                unit_of(k, fi, pl);
+                const unsigned gs = gb + fi;
+                const int buf = k & 1;
+                double2* Rv = Rvb + buf * PLANE;
+                complete(gs, pl);
+                const bool has_next = (k + 1 < upc) || more_cells;
+                unsigned gs2 = gb + 1 + nfields;
+                int pl2 = 0;
+                if (k + 1 < upc) {
+                    int f2;
+                    unit_of(k + 1, f2, pl2);
+                    gs2 = gb + f2;
+                }
+                // Deferred successor: after the last prologue plane (the first field
+                // needs F in TMEM) and, EXACT, after a gb unit (the other buffer holds ga).
+                const bool defer = (fi == 0 && pl == P - 1) || (EXACT && fi >= 1 && fi <= 2 * a.md && ((fi - 1) & 1));
+                if (has_next && !defer) issue(gs2, pl2, buf ^ 1);
+                if (fi == 0) {
+                    // ---- prologue: forward over k3 of rows (k1 = rP + pl, k2 = pp) -> F (TMEM) ----
+                    const double2* row = Rv + pp * ROW;
+                    const int k1 = r * P + pl, k2 = pp;
+                    double2 v[M];
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        v[j] = row[h * Q + j];
+                        v[Q + j] = row[M + h * Q + j];
+                    }
+                    fftxh_dif<M, false>(v, h);  // v[m] = F[k3 = 2m + h] (unscaled)
+                    const double s = 1.0 / double(NB);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        double w8[8];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            w8[2 * i] = v[4 * c + i].x * s;
+                            w8[2 * i + 1] = v[4 * c + i].y * s;
+                        }
+                        tmem_st16(tmF + 128 * pl + 16 * c, w8);
+                    }
+                    if (!EXACT && a.nyq) {
+                        constexpr int H = N / 2;
+                        double* ny = a.nyq + cell * 3 * N * N;
+                        if (h == 0) ny[2 * N * N + k1 * N + k2] = s * sqrt(v[H / 2].x * v[H / 2].x + v[H / 2].y * v[H / 2].y);
+                        if (k2 == H) {
+#pragma unroll
+                            for (int m = 0; m < M; ++m)
+                                ny[1 * N * N + k1 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                        }
+                        if (k1 == H) {
+#pragma unroll
+                            for (int m = 0; m < M; ++m) ny[k2 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                        }
+                    }
+                    const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                    for (int c = 0; c < GCOLS / 16; ++c) tmem_st16(tmG + GCOLS * pl + 16 * c, z);
+                    tmem_wait_st();
+                    tmem_fence_before();
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pl)) : "memory");
+                } else {
+                    // ---- field: inverse over i2 (rows i1 = pp), then i1 (columns j2 = pp) ----
+                    {
+                        double2* row = Rv + pp * ROW;
+                        double2 v[M];
+#pragma unroll
+                        for (int j = 0; j < Q; ++j) {
+                            v[j] = row[h * Q + j];
+                            v[Q + j] = row[M + h * Q + j];
+                        }
+                        fftxh_dif<M, true>(v, h);
+                        __syncwarp();
+#pragma unroll
+                        for (int m = 0; m < M; ++m) row[2 * m + h] = v[m];
+                    }
+                    named_bar(2, 128);  // columns need every row
+                    double2 y[M];       // y[j] = node j1 = hQ + j, y[Q + j] = node M + hQ + j
+                    double2* col = Rv + pp;
+#pragma unroll
+                    for (int m = 0; m < M; ++m) y[m] = col[(2 * m + h) * ROW];
+                    fftxh_dit<M, true>(y, h);
+                    const bool is_loss = EXACT ? (fi == 1 + 2 * a.md) : (fi == 1 + a.md);
+                    const int j3 = r * P + pl;
+                    if (!is_loss) {
+                        if constexpr (!EXACT) {
+                            const double mu = (fi == 1) ? a.mult0 : 1.0;
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                double gv[8];
+                                tmem_ld16(tmG + GCOLS * pl + 16 * c, gv);
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) gv[i] += mu * (y[8 * c + i].x * y[8 * c + i].y);
+                                tmem_st16(tmG + GCOLS * pl + 16 * c, gv);
+                            }
+                            tmem_wait_st();
+                        } else if (!((fi - 1) & 1)) {  // ga: park it in place for the gb unit
+                            __syncwarp();
+#pragma unroll
+                            for (int j = 0; j < Q; ++j) {
+                                col[(h * Q + j) * ROW] = y[j];
+                                col[(M + h * Q + j) * ROW] = y[Q + j];
+                            }
+                        } else {  // gb: gain += m ga gb (complex), ga in the other buffer
+                            const double mu = (fi == 2) ? a.mult0 : 1.0;
+                            const double2* gcol = Rvb + (buf ^ 1) * PLANE + pp;
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {  // nodes jj = 4c .. 4c + 3
+                                double gv[8];
+                                tmem_ld16(tmG + GCOLS * pl + 16 * c, gv);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const int jj = 4 * c + i;
+                                    const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
+                                    const double2 ga = gcol[j1 * ROW], gbv = y[jj];
+                                    gv[2 * i] += mu * (ga.x * gbv.x - ga.y * gbv.y);
+                                    gv[2 * i + 1] += mu * (ga.x * gbv.y + ga.y * gbv.x);
+                                }
+                                tmem_st16(tmG + GCOLS * pl + 16 * c, gv);
+                            }
+                            tmem_wait_st();
+                        }
+                    } else {
+                        // ---- epilogue for plane pl: Q = jac (w gain - f loss) at (j1, pp, j3) ----
+                        double* qc = a.q + cell * NB;
+                        if constexpr (!EXACT) {
+#pragma unroll
+                            for (int c = 0; c < 4; ++c) {
+                                double gv[8];
+                                tmem_ld16(tmG + GCOLS * pl + 16 * c, gv);
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    const int jj = 8 * c + i;
+                                    const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
+                                    const int64_t gi = ((int64_t)j1 * N + pp) * N + j3;
+                                    const double qre = a.jac * (a.w * gv[i] - fc[gi] * y[jj].x);
+                                    qc[gi] = qre;
+                                    mre = fmax(mre, fabs(qre));
+                                    n2 += qre * qre;
+                                }
+                            }
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) {
+                                double gv[8];
+                                tmem_ld16(tmG + GCOLS * pl + 16 * c, gv);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const int jj = 4 * c + i;
+                                    const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
+                                    const int64_t gi = ((int64_t)j1 * N + pp) * N + j3;
+                                    const double fv = fc[gi];
+                                    const double qre = a.jac * (a.w * gv[2 * i] - fv * y[jj].x);
+                                    const double qim = a.jac * (a.w * gv[2 * i + 1] - fv * y[jj].y);
+                                    qc[gi] = qre;
+                                    mre = fmax(mre, fabs(qre));
+                                    mim = fmax(mim, fabs(qim));
+                                    n2 += qre * qre;
+                                }
+                            }
+                        }
+                        if (pl == P - 1) {
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) {
+                                mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+                                mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
+                                n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                            }
+                            if (lane == 0 && a.st) {
+                                hk_cell_status* sc = a.st + cell;
+                                atomic_max_nonneg(&sc->max_re, mre);
+                                atomicAdd(&sc->q_norm2, n2);
+                                if (EXACT) {
+                                    atomic_max_nonneg(&sc->max_im, mim);
+                                    if (r == 0 && rw == 0) atomicOr(&sc->flags, HK_CELL_EXACT);
+                                }
+                            }
+                        }
+                    }
+                }
+                if (has_next && defer) {
+                    named_bar(2, 128);  // every warp is done with the other buffer
+                    issue(gs2, pl2, buf ^ 1);
+                }
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
+size_t coll64_xchg_bytes(hk_ctx ctx) {
+    const int teams = ctx->sm_count / Geo64::C;
+    return size_t(teams > 0 ? teams : 1) * Geo64::XCHG_PER_TEAM;
+}
+
+int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_cells, int tag) {
+    using G = Geo64;
+    auto kern = exact ? coll64_kernel<true> : coll64_kernel<false>;
+    const int key = 6400 + (exact ? 1 : 0);
+    int st;
+    if (!ctx->max_clusters.count(key)) {
+        if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
+                             "smem attribute")))
+            return st;
+        int per_sm = 0;
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, G::SMEM), "occupancy")))
+            return st;
+        int teams = per_sm >= 1 ? ctx->sm_count / G::C : 0;
+        if (const char* m = getenv("HK_TEAMS64")) teams = atoi(m);  // experiment override (<= sm_count / C)
+        if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] coll64 kernel (exact %d): per_sm %d teams %d\n", exact, per_sm, teams);
+        if (teams < 1) return fail(ctx, HK_CUDA, "N = 64 collision kernel cannot be resident");
+        ctx->max_clusters[key] = teams;
+    }
+    int64_t teams = ctx->max_clusters[key];
+    if (max_cells < teams) teams = max_cells;
+    if (teams < 1) return HK_OK;
+    CollArgs args = args_in;
+    args.in_ready = nullptr;
+    args.out_done = nullptr;
+    if ((st = check_cuda(ctx, cudaMemsetAsync(args.team_ctr, 0, sizeof(unsigned) * 2 * G::D * teams, ctx->stream),
+                         "team counters")))
+        return st;
+    void* params[] = {&args};
+    timing_begin(ctx, tag);
+    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * G::C)), dim3(256), params,
+                                                     G::SMEM, ctx->stream),
+                    "N = 64 collision kernel launch");
+    timing_end(ctx);
+    ctx->launches++;
+    return st;
+}
+
+}  // namespace hk

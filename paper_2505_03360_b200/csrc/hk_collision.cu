@@ -31,6 +31,7 @@
 
 #include "hk_common.cuh"
 #include "hk_internal.h"
+#include "hk_coll.cuh"
 
 
 namespace hk {
@@ -43,31 +44,6 @@ constexpr double kGuardTau = 5e-11;
 
 // internal flag: route the FAST path through the 256-thread SMEM kernel
 constexpr uint32_t HK_COLL_LEGACY_FAST = 1u << 16;
-
-struct CollArgs {
-    const double* f;
-    double* q;
-    int64_t ncells;
-    const int64_t* list;    // optional cell list (rerouted cells)
-    const int* list_count;  // device count for `list`
-    const double* alpha;
-    const double* alpha_p;
-    const double* loss;
-    const double2* wfast;
-    int md;
-    double mult0, jac, w;
-    hk_cell_status* st;
-    double* nyq;       // [cell][3][N][N] |F| on the Nyquist planes (FAST) or null
-    double2* xchg;     // [cluster][2 buffers][2 fields][C dest][P][N][N] L2 transpose scratch
-    unsigned* team_ctr;  // [teams] barrier counters (team kernel), zeroed per launch
-    unsigned long long* prof;  // optional [4]: producer spin, consumer spin, producer total, consumer total (cycles)
-    // streamed host I/O (warp kernel): chunk c of `chunk` cells may be read once
-    // in_ready[c] >= 1 (set by the H2D stream); out_done[c] counts finished
-    // consumer-warp epilogues (the D2H stream waits for chunk * C * P).
-    const unsigned* in_ready;
-    unsigned* out_done;
-    int64_t chunk;
-};
 
 template <int N, int C>
 struct Geo {
@@ -1790,7 +1766,11 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     const size_t nyq_bytes = guard ? sizeof(double) * nn3 * ncells : 0;
     const size_t list_bytes = guard ? sizeof(int64_t) * ncells : 0;
     const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255) & ~size_t(255);
-    const size_t xchg_bytes = size_t(2 * ctx->sm_count / C + 1) * Geo<N, C>::XCHG_PER_CLUSTER + 65536;
+    size_t xchg_bytes;
+    if constexpr (N == 64)
+        xchg_bytes = coll64_xchg_bytes(ctx) + 65536;
+    else
+        xchg_bytes = size_t(2 * ctx->sm_count / C + 1) * Geo<N, C>::XCHG_PER_CLUSTER + 65536;
     int s;
     if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
     char* base = static_cast<char*>(ctx->scratch);
@@ -1817,11 +1797,22 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     ctx->last_list = list;
     ctx->last_count = guard ? count : nullptr;
     a.team_ctr = reinterpret_cast<unsigned*>(base + xchg_off + xchg_bytes - 65536);
+    // exact collision launch (reference arithmetic) for a cell list or the batch
+    auto launch_exact = [&](const CollArgs& x, int tag) -> int {
+        if constexpr (N == 64)
+            return launch_coll64(ctx, x, true, ncells, tag);
+        else
+            return launch_variant<N, C, true>(ctx, x, ncells, tag);
+    };
     if (exact) {
-        if ((s = launch_variant<N, C, true>(ctx, a, ncells, 0))) return s;
+        if ((s = launch_exact(a, 0))) return s;
     } else {
         a.nyq = nyq;
         bool done = false;
+        if constexpr (N == 64) {
+            if ((s = launch_coll64(ctx, a, false, ncells, 0))) return s;
+            done = true;
+        }
         if constexpr (N == 32 && C == 8) {
             if (!(flags & HK_COLL_LEGACY_FAST) && !getenv("HK_TMEM2")) {
                 if ((s = launch_fast_pipe<N, C>(ctx, a, ncells, 0))) return s;
@@ -1831,8 +1822,10 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
                 done = true;
             }
         }
-        if (!done) {
-            if ((s = launch_variant<N, C, false>(ctx, a, ncells, 0))) return s;
+        if constexpr (N != 64) {
+            if (!done) {
+                if ((s = launch_variant<N, C, false>(ctx, a, ncells, 0))) return s;
+            }
         }
         if (guard) {
             cudaMemsetAsync(count, 0, sizeof(int), ctx->stream);
@@ -1851,7 +1844,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
             b.nyq = nullptr;
             b.list = list;
             b.list_count = count;
-            if ((s = launch_variant<N, C, true>(ctx, b, ncells, 2))) return s;
+            if ((s = launch_exact(b, 2))) return s;
         }
     }
     {
@@ -1872,8 +1865,10 @@ int collision_launch(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_
         return run_size<16, 2>(ctx, k, f, q, ncells, flags, st);
     case 32:
         return run_size<32, 8>(ctx, k, f, q, ncells, flags, st);
+    case 64:
+        return run_size<64, 32>(ctx, k, f, q, ncells, flags, st);
     default:
-        return fail(ctx, HK_UNSUPPORTED, "collision path implemented for n = 16, 32");
+        return fail(ctx, HK_UNSUPPORTED, "collision path implemented for n = 16, 32, 64");
     }
 }
 

@@ -196,6 +196,10 @@ __device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* gsrc) 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// 8-byte variant (cp.async.ca: sizes below 16 B go through L1).
+__device__ __forceinline__ void cp_async8(uint32_t smem_dst, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_dst), "l"(gsrc) : "memory");
+}
 // L2-only 16-byte store (skip L1: the consumer is another SM).
 __device__ __forceinline__ void st_cg16(double2* p, double2 v) {
     asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
@@ -363,6 +367,54 @@ __device__ __forceinline__ void fftx2_dif(double2 (&v)[16], int h) {
         v[8 + j] = h ? b[j] : r;
     }
     fft_reg<16, INV>(v);  // v[m] = X[2m + h]
+}
+
+// Generic split-pencil transforms of length L = 2M over the lane pair
+// (l, l ^ 16); each thread holds M values (M = 32 for the N = 64 kernels:
+// 64 data registers pairs instead of 128).  Same contracts as fftx2_*, with
+// 8 -> M/2 and 16 -> M:
+//   fftxh_dit: in  v[m] = x[2m + h]                 out v[j] = X[hM/2 + j], v[M/2 + j] = X[M + hM/2 + j]
+//   fftxh_dif: in  v[j] = x[hM/2 + j], v[M/2 + j] = x[M + hM/2 + j]    out v[m] = X[2m + h]
+template <int M, bool INV>
+__device__ __forceinline__ void fftxh_dit(double2 (&v)[M], int h) {
+    constexpr int L = 2 * M, Q = M / 2;
+    static_assert(64 % L == 0, "twiddle table covers L | 64");
+    fft_reg<M, INV>(v);  // E[k] (h = 0) or O[k] (h = 1)
+    if (h) {
+#pragma unroll
+        for (int k = 1; k < M; ++k) {
+            double2 w = c_tw64[k * (64 / L)];  // e^{-2 pi i k / L}
+            if (INV) w.y = -w.y;
+            v[k] = cmul(v[k], w);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        const double2 send = h ? v[j] : v[Q + j];  // h=0 sends E[Q+j], h=1 sends T[j]
+        const double2 r = shfl_xor16(send);
+        const double2 a = h ? r : v[j];            // E[hQ + j]
+        const double2 b = h ? v[Q + j] : r;        // T[hQ + j]
+        v[j] = cadd(a, b);                         // X[hQ + j]
+        v[Q + j] = csub(a, b);                     // X[M + hQ + j]
+    }
+}
+
+template <int M, bool INV>
+__device__ __forceinline__ void fftxh_dif(double2 (&v)[M], int h) {
+    constexpr int L = 2 * M, Q = M / 2;
+    static_assert(64 % L == 0, "twiddle table covers L | 64");
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+        const double2 a = cadd(v[j], v[Q + j]);  // n = hQ + j
+        double2 w = h ? c_tw64[(Q + j) * (64 / L)] : c_tw64[j * (64 / L)];
+        if (INV) w.y = -w.y;
+        const double2 b = cmul(csub(v[j], v[Q + j]), w);
+        const double2 send = h ? a : b;  // h=0 sends b (n = j), h=1 sends a (n = Q + j)
+        const double2 r = shfl_xor16(send);
+        v[j] = h ? r : a;       // h=0: a[j];        h=1: b[j] (from h=0)
+        v[Q + j] = h ? b : r;   // h=0: a[Q+j] (h=1); h=1: own b[Q+j]
+    }
+    fft_reg<M, INV>(v);  // v[m] = X[2m + h]
 }
 
 }  // namespace hk

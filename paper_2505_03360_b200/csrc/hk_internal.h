@@ -37,6 +37,9 @@ struct hk_ctx_s {
     int64_t sio_flags_n = 0;
     int64_t* last_list = nullptr;
     int* last_count = nullptr;
+    // NCCL communicator (hk_comm.cu; ncclComm_t, loaded at run time)
+    void* comm = nullptr;
+    int nranks = 1, rank = 0;
     // optional CUDA-event timing of the collision kernels (tag -> event pairs)
     bool timing = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> events;
@@ -83,5 +86,8 @@ void timing_end(hk_ctx ctx);
 
 // hk_peak.cu
 double fp64_peak(hk_ctx ctx);
+
+// hk_comm.cu
+void comm_destroy(hk_ctx ctx);
 
 }  // namespace hk

@@ -234,3 +234,40 @@ def config3_cells_torch(nx: int, ny: int, n: int = 32, device="cuda", seed_salt:
         M = (rho / (2 * math.pi * T) ** 1.5)[:, :, None, None] * ex[:, :, None, None] * ey[:, None, :, None] * ez[:, None, None, :]
         out[s:e] = (M * (1.0 + ep[:, :, None, None] * p3)).reshape(e - s, -1)
     return out, fl
+
+
+# ---------------------------------------------------------------------------
+# Config 5: 512 x 128 normal shock, N = 64, all cells Boltzmann.
+# Upstream rho = 1, T = 1, u_x = 3 sqrt(5/3); Rankine-Hugoniot downstream for
+# gamma = 5/3 (rho = 3, u_x = sqrt(5/3), T = 11/3).  The profile is the
+# Mott-Smith bimodal form f = (1 - th) M_up + th M_down with
+# th = (1 + tanh((x - 0.5) / (4 dx))) / 2, times (1 + 0.01 U(-1, 1)) density
+# noise per cell: non-equilibrium inside the interface, Maxwellian outside.
+# ---------------------------------------------------------------------------
+C5_UP = (1.0, (3.0 * math.sqrt(5.0 / 3.0), 0.0, 0.0), 1.0)
+C5_DOWN = (3.0, (math.sqrt(5.0 / 3.0), 0.0, 0.0), 11.0 / 3.0)
+
+
+def config5_theta(nx: int = 512) -> np.ndarray:
+    dx = 1.0 / nx
+    x = (np.arange(nx) + 0.5) * dx
+    return 0.5 * (1.0 + np.tanh((x - 0.5) / (4.0 * dx)))
+
+
+def config5_cells(ncells: int, n: int = 64, nx: int = 512, ny: int = 128, seed_salt: int = 0,
+                  columns=None) -> np.ndarray:
+    """`ncells` cells of the config-5 field.  By default cell c sits in the
+    (c mod 16)-th x-column nearest the interface (the non-equilibrium part of
+    the shock); `columns` selects the x-columns explicitly (cycled)."""
+    rng = rng_for(5, seed_salt)
+    th = config5_theta(nx)
+    if columns is None:
+        columns = np.argsort(np.abs(np.arange(nx) + 0.5 - nx / 2), kind="stable")[:16]
+    mu = maxwellian(n, *C5_UP)
+    md = maxwellian(n, *C5_DOWN)
+    out = np.empty((ncells, n ** 3))
+    for c in range(ncells):
+        i = columns[c % len(columns)]
+        noise = 1.0 + 0.01 * rng.uniform(-1.0, 1.0)
+        out[c] = noise * ((1.0 - th[i]) * mu + th[i] * md)
+    return out

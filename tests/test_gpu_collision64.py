@@ -1,0 +1,88 @@
+"""GPU parity of the N = 64 collision kernel (config 5, hk_coll64.cu).
+
+Oracle parity at a small quadrature (a1 x a2 = 2 x 4, so the CPU oracle runs
+in seconds at 64^3), and FAST-vs-EXACT self-consistency at config 5's
+8 x 8 quadrature.  Bar: 1e-10 relative L2 (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+from paper_2505_03360_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+N = 64
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def small(oracle, hk):
+    a1, a2 = 2, 4
+    vg = hk.make_velocity_grid(N, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, N, a1, a2, inputs.R_PHYS_MAX)
+    ko = oracle.kernel(N, inputs.VMAX, a1, a2, inputs.R_PHYS_MAX, closed_form=True)
+    f = inputs.config5_cells(3, N)
+    q_ref, st_ref, res_ref = oracle.collision_batch(ko, f)
+    return dict(kern=kern, f=f, q_ref=q_ref, st_ref=st_ref, res_ref=res_ref)
+
+
+def test_n64_exact_matches_oracle(small, hk):
+    import torch
+    f = torch.from_numpy(small["f"]).cuda()
+    q, st = hk.spectral_collision(f, small["kern"], exact=True, return_status=True)
+    q = q.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], small["q_ref"][c]) < TOL, c
+    assert np.all(st["flags"] & 1)
+    res = st["max_im"] / np.maximum(st["max_re"], 1e-300)
+    np.testing.assert_allclose(res, small["res_ref"], rtol=1e-5, atol=1e-15)
+
+
+def test_n64_default_path_matches_oracle(small, hk):
+    import torch
+    f = torch.from_numpy(small["f"]).cuda()
+    q, st = hk.spectral_collision(f, small["kern"], return_status=True)
+    q = q.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], small["q_ref"][c]) < TOL, c
+    assert np.all(st["nyq_bound"] >= 0)
+
+
+def test_n64_host_entry_point(small, hk):
+    q = hk.spectral_collision(small["f"], small["kern"])
+    for c in range(len(small["f"])):
+        assert rel_l2(q[c], small["q_ref"][c]) < TOL, c
+
+
+@pytest.fixture(scope="module")
+def cfg5(hk):
+    vg = hk.make_velocity_grid(N, inputs.VMAX)
+    return hk.precompute_kernel(vg, N, 8, 8, inputs.R_PHYS_MAX)
+
+
+def test_n64_cfg5_fast_equals_exact(cfg5, hk):
+    """8 x 8 quadrature, more cells than teams (several cells per team, the
+    guard's reroute list): the default path agrees with the exact kernel."""
+    import torch
+    f = torch.from_numpy(inputs.config5_cells(9, N)).cuda()
+    qe, ste = hk.spectral_collision(f, cfg5, exact=True, return_status=True)
+    qf, stf = hk.spectral_collision(f, cfg5, return_status=True)
+    qn = hk.spectral_collision(f, cfg5, guard=False)
+    qe, qf, qn = qe.cpu().numpy(), qf.cpu().numpy(), qn.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(qf[c], qe[c]) < TOL, c
+        # the unguarded fast path differs from exact only by the bounded Nyquist term
+        assert rel_l2(qn[c], qe[c]) <= 1.01 * stf["nyq_bound"][c] + 1e-13, c
+    assert np.all(ste["flags"] & 1)
+
+
+def test_n64_cfg5_mass_conservation(cfg5, hk):
+    """The k = 0 mode of Q vanishes: mass is conserved to round-off."""
+    import torch
+    fh = inputs.config5_cells(2, N)
+    q = hk.spectral_collision(torch.from_numpy(fh).cuda(), cfg5).cpu().numpy()
+    for c in range(2):
+        assert abs(q[c].sum()) < 1e-10 * np.abs(q[c]).sum()

@@ -9,7 +9,7 @@ tail -3 gpurun_out/gpu_tests_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 ARGS="--steps 2 --warmup 3 --e2e-steps 1 --no-cpu-baseline"
 timeout 600 python bench.py $ARGS > gpurun_out/plain_launch_$TAG.log 2>&1 && \
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:hk:: --csv --log-file gpurun_out/launches_$TAG.csv \
   python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
 timeout 300 python tools/profile_collision.py --cells 1024 --iters 1 > gpurun_out/plain_prof_$TAG.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:coll_fast -c 1 -o gpurun_out/coll_fast_$TAG \

@@ -20,6 +20,9 @@ vg = hk.make_velocity_grid(args.n, 8.0)
 kern = hk.precompute_kernel(vg, args.n, args.a1, args.a2, inputs.R_PHYS_MAX, ctx=ctx)
 if args.n == 32:
     f = inputs.config2_cells_torch(args.cells, 32, device="cuda")
+elif args.n == 64:
+    base = torch.from_numpy(inputs.config5_cells(min(args.cells, 16), 64)).cuda()
+    f = base.repeat((args.cells + len(base) - 1) // len(base), 1)[: args.cells].contiguous()
 else:
     f = torch.from_numpy(inputs.config1_cells(args.cells, args.n)).cuda()
 q = torch.empty_like(f)
