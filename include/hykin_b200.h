@@ -52,6 +52,7 @@ typedef struct {
     double nyq_bound; /* rigorous bound on ||dropped Nyquist term||_2 / ||Q||_2 (fast path) */
     uint32_t flags;   /* HK_CELL_* bits */
     uint32_t reserved;
+    double loss_norm2; /* sum_k (jac f_k L_k)^2, the loss term's scale (fast path; the guard's round-off floor) */
 } hk_cell_status;
 
 #define HK_CELL_EXACT 1u            /* evaluated on the exact (full complex) path */

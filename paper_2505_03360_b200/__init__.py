@@ -249,7 +249,8 @@ def precompute_kernel_from_tables(vgrid: VelocityGrid, n: int, a1: int, a2: int,
 
 def _status_array_np(ncells: int) -> np.ndarray:
     return np.zeros(ncells, dtype=np.dtype([("max_re", "f8"), ("max_im", "f8"), ("q_norm2", "f8"),
-                                            ("nyq_bound", "f8"), ("flags", "u4"), ("reserved", "u4")]))
+                                            ("nyq_bound", "f8"), ("flags", "u4"), ("reserved", "u4"),
+                                            ("loss_norm2", "f8")]))
 
 
 def spectral_collision(f, kernel: SpectralKernel, out=None, *, exact: bool = False,

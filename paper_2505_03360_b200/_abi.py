@@ -45,6 +45,7 @@ class CellStatus(C.Structure):
         ("nyq_bound", C.c_double),
         ("flags", C.c_uint32),
         ("reserved", C.c_uint32),
+        ("loss_norm2", C.c_double),
     ]
 
 

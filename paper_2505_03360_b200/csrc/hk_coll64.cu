@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
             const double* fc = a.f + cell * NB;
             const unsigned gb = ncell * (1 + nfields);
             const bool more_cells = it + nteams < count;
-            double mre = 0.0, mim = 0.0, n2 = 0.0;
+            double mre = 0.0, mim = 0.0, n2 = 0.0, l2 = 0.0;
 #pragma unroll 1
             for (int k = 0; k < upc; ++k) {
                 int fi, pl;
@@ -391,10 +391,12 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                                     const int jj = 8 * c + i;
                                     const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
                                     const int64_t gi = ((int64_t)j1 * N + pp) * N + j3;
-                                    const double qre = a.jac * (a.w * gv[i] - fc[gi] * y[jj].x);
+                                    const double lt = fc[gi] * y[jj].x;
+                                    const double qre = a.jac * (a.w * gv[i] - lt);
                                     qc[gi] = qre;
                                     mre = fmax(mre, fabs(qre));
                                     n2 += qre * qre;
+                                    l2 += lt * lt;
                                 }
                             }
                         } else {
@@ -423,11 +425,13 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                                 mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
                                 mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
                                 n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                                if (!EXACT) l2 += __shfl_xor_sync(0xffffffffu, l2, o);
                             }
                             if (lane == 0 && a.st) {
                                 hk_cell_status* sc = a.st + cell;
                                 atomic_max_nonneg(&sc->max_re, mre);
                                 atomicAdd(&sc->q_norm2, n2);
+                                if (!EXACT) atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
                                 if (EXACT) {
                                     atomic_max_nonneg(&sc->max_im, mim);
                                     if (r == 0 && rw == 0) atomicOr(&sc->flags, HK_CELL_EXACT);

@@ -41,6 +41,11 @@ namespace hk {
 // bound is rigorous, so 5e-11 keeps every fast-path cell inside it with 2x
 // margin (measured bound/actual ratio on config 2: 10-20x).
 constexpr double kGuardTau = 5e-11;
+// Near equilibrium ||Q|| collapses to round-off of the gain - loss difference;
+// the exact path itself is only accurate to ~1e-15 ||jac f L||.  A fast-path
+// cell whose bound is below tau * kGuardFloor * ||jac f L|| (= 1e-15 ||jac f L||)
+// is as accurate as the exact path would be and is not rerouted.
+constexpr double kGuardFloor = 2e-5;
 
 // internal flag: route the FAST path through the 256-thread SMEM kernel
 constexpr uint32_t HK_COLL_LEGACY_FAST = 1u << 16;
@@ -53,7 +58,7 @@ struct Geo {
     static constexpr int SLAB = P * PLANE;  // double2 per F slab / per received field
     static constexpr int NT = 256;
     static_assert(P * N == 128, "one pencil per thread per field");
-    static constexpr size_t SMEM = size_t(3 * SLAB) * sizeof(double2) + 24 * sizeof(double);
+    static constexpr size_t SMEM = size_t(3 * SLAB) * sizeof(double2) + 32 * sizeof(double);
     static constexpr size_t XCHG_PER_CLUSTER = size_t(2) * 2 * C * P * N * N * sizeof(double2);
 };
 
@@ -68,7 +73,7 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
     double2* Fs = smem;
     double2* Rv0 = smem + SLAB;
     double2* Rv1 = smem + 2 * SLAB;
-    double* red = reinterpret_cast<double*>(smem + 3 * SLAB);  // 24 doubles
+    double* red = reinterpret_cast<double*>(smem + 3 * SLAB);  // 32 doubles
 
     const unsigned r = cluster_rank();
     const unsigned cid = cluster_id_x();
@@ -305,7 +310,7 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
             }
         }
         __syncthreads();
-        double mre = 0.0, mim = 0.0, n2 = 0.0;
+        double mre = 0.0, mim = 0.0, n2 = 0.0, l2 = 0.0;
         double* qc = a.q + cell * NB;
         for (int idx = t; idx < N * N * P; idx += 256) {
             const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
@@ -326,6 +331,7 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
             mre = fmax(mre, fabs(qre));
             n2 += qre * qre;
             if (EXACT) mim = fmax(mim, fabs(a.jac * (a.w * gim - fv * L.y)));
+            else l2 += (fv * L.x) * (fv * L.x);
         }
         // block reduction -> global atomics into the cell's verdict
 #pragma unroll
@@ -333,25 +339,29 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
             mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
             mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
             n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+            l2 += __shfl_xor_sync(0xffffffffu, l2, o);
         }
         const int warp = t >> 5, lane = t & 31;
         if (lane == 0) {
             red[warp] = mre;
             red[8 + warp] = mim;
             red[16 + warp] = n2;
+            red[24 + warp] = l2;
         }
         __syncthreads();
         if (t == 0 && a.st) {
-            double m1 = 0, m2 = 0, sum = 0;
+            double m1 = 0, m2 = 0, sum = 0, lsum = 0;
             for (int w = 0; w < 8; ++w) {
                 m1 = fmax(m1, red[w]);
                 m2 = fmax(m2, red[8 + w]);
                 sum += red[16 + w];
+                lsum += red[24 + w];
             }
             hk_cell_status* sc = a.st + cell;
             atomic_max_nonneg(&sc->max_re, m1);
             atomic_max_nonneg(&sc->max_im, m2);
             atomicAdd(&sc->q_norm2, sum);
+            if (!EXACT) atomicAdd(&sc->loss_norm2, a.jac * a.jac * lsum);
             if (EXACT && r == 0) atomicOr(&sc->flags, HK_CELL_EXACT);
         }
         __syncthreads();  // red / SMEM reusable by the next cell
@@ -1161,7 +1171,7 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                 } else {
                     // ---- epilogue: Q = jac (w gain - f loss) for nodes (j1, j2 = lane, j3 = rP + pl) ----
                     double* qc = a.q + cell * NB;
-                    double mre = 0.0, n2 = 0.0;
+                    double mre = 0.0, n2 = 0.0, l2 = 0.0;
 #pragma unroll
                     for (int c = 0; c < N / 8; ++c) {
                         double gv[8];
@@ -1170,21 +1180,25 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                         for (int i = 0; i < 8; ++i) {
                             const int j1 = 8 * c + i;
                             const int64_t gi = ((int64_t)j1 * N + lane) * N + r * P + pl;
-                            const double qre = a.jac * (a.w * gv[i] - fc[gi] * y[j1].x);
+                            const double lt = fc[gi] * y[j1].x;
+                            const double qre = a.jac * (a.w * gv[i] - lt);
                             qc[gi] = qre;
                             mre = fmax(mre, fabs(qre));
                             n2 += qre * qre;
+                            l2 += lt * lt;
                         }
                     }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) {
                         mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
                         n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                        l2 += __shfl_xor_sync(0xffffffffu, l2, o);
                     }
                     if (lane == 0 && a.st) {
                         hk_cell_status* sc = a.st + cell;
                         atomic_max_nonneg(&sc->max_re, mre);
                         atomicAdd(&sc->q_norm2, n2);
+                        atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
                     }
                     __syncwarp();
                     if (lane == 0 && a.out_done) signal_add(a.out_done + cell / a.chunk);  // q rows visible
@@ -1568,7 +1582,10 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
         const double abs_bound = jac * w * bound[threadIdx.x] * pow(double(n), 1.5);
         const double rel = qn > 0.0 ? abs_bound / qn : (abs_bound > 0.0 ? INFINITY : 0.0);
         sc->nyq_bound = rel;
-        if (!(rel <= tau)) {
+        // reroute unless the bound is within tau of ||Q|| or below the exact
+        // path's own round-off floor (kGuardFloor ||jac f L||: near-equilibrium cells)
+        const double scale = fmax(qn, kGuardFloor * sqrt(sc->loss_norm2));
+        if (!(abs_bound <= tau * scale)) {
             const int slot = atomicAdd(count, 1);
             list[slot] = cell;
             sc->max_re = 0.0;

@@ -271,3 +271,23 @@ def config5_cells(ncells: int, n: int = 64, nx: int = 512, ny: int = 128, seed_s
         noise = 1.0 + 0.01 * rng.uniform(-1.0, 1.0)
         out[c] = noise * ((1.0 - th[i]) * mu + th[i] * md)
     return out
+
+
+def config5_slab_torch(i0: int = 224, nxl: int = 64, ny: int = 128, n: int = 64, nx: int = 512, device="cuda",
+                       seed_salt: int = 0):
+    """The x-slab [ny][nxl][n^3] of the config-5 field starting at column i0
+    (one GPU's share in the 8-GPU weak-scaling layout), built on the device:
+    f = noise (1 - th) M_up + noise th M_down per cell."""
+    import torch
+    th = config5_theta(nx)[i0:i0 + nxl]
+    rng = rng_for(5, seed_salt + 1)
+    noise = 1.0 + 0.01 * rng.uniform(-1.0, 1.0, (ny, nxl))
+    a = torch.from_numpy((noise * (1.0 - th)[None, :]).reshape(-1)).to(device)
+    b = torch.from_numpy((noise * th[None, :]).reshape(-1)).to(device)
+    mu = torch.from_numpy(maxwellian(n, *C5_UP)).to(device)
+    md = torch.from_numpy(maxwellian(n, *C5_DOWN)).to(device)
+    f = torch.empty((ny * nxl, n ** 3), dtype=torch.float64, device=device)
+    for c0 in range(0, ny * nxl, 512):
+        c1 = min(c0 + 512, ny * nxl)
+        torch.addcmul(torch.outer(b[c0:c1], md), a[c0:c1, None], mu[None, :], out=f[c0:c1])
+    return f

@@ -86,3 +86,20 @@ def test_n64_cfg5_mass_conservation(cfg5, hk):
     q = hk.spectral_collision(torch.from_numpy(fh).cuda(), cfg5).cpu().numpy()
     for c in range(2):
         assert abs(q[c].sum()) < 1e-10 * np.abs(q[c]).sum()
+
+
+def test_n64_equilibrium_cells(cfg5, hk):
+    """Upstream / downstream Maxwellian cells (the truncated domain leaves
+    ||Q|| ~ 1e-5 ||jac f L||): the default path agrees with the exact kernel to
+    1e-10 ||Q||, or to the exact path's own round-off floor (1e-14 ||jac f L||)."""
+    import torch
+    fh = inputs.config5_cells(4, N, columns=[0, 1, 510, 511])
+    f = torch.from_numpy(fh).cuda()
+    qf, st = hk.spectral_collision(f, cfg5, return_status=True)
+    qe = hk.spectral_collision(f, cfg5, exact=True)
+    qf, qe = qf.cpu().numpy(), qe.cpu().numpy()
+    for c in range(4):
+        scale = np.sqrt(st["loss_norm2"][c])
+        assert scale > 0
+        gap = np.linalg.norm(qf[c] - qe[c])
+        assert gap <= max(TOL * np.linalg.norm(qe[c]), 1e-14 * scale), c

@@ -102,12 +102,60 @@ def config3(iters, nx=256, ny=256):
     return out
 
 
+def config5(iters, steps=True):
+    """Config 5, one GPU's x-slab (64 x 128 cells, N = 64, M = 8 x 8): Q over
+    the slab (fast path + guard) and, with `steps`, one PR(2,2,2) IMEX step of
+    the slab (periodic in x within the slab: the 1-GPU share of the weak-
+    scaling layout; 2 Q evaluations per cell-step)."""
+    n, a1, a2, nxl, ny = 64, 8, 8, 64, 128
+    ctx = hk.default_context()
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    k = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    f = inputs.config5_slab_torch(224, nxl, ny, n)
+    cells = nxl * ny
+    q = torch.empty_like(f)
+    res = {}
+
+    def coll():
+        res["st"] = hk.spectral_collision(f, k, out=q, return_status=True)[1]
+
+    ms_q = timed(coll, iters)
+    md = (a1 - 1) * a2 + 1
+    W = (2 * md + 2) * 5 * n ** 3 * math.log2(n ** 3) + (12 * md + 10) * n ** 3
+    peak = ctx.fp64_peak_tflops()
+    ach = W * cells / (ms_q * 1e-3) / 1e12
+    out = {"config": "config5 slab: 64 x 128 cells (1 of 8 x-slabs of 512 x 128), N=64, M=8x8, hard spheres",
+           "collision": {"ms": ms_q, "cell_updates_per_s": cells / (ms_q * 1e-3),
+                         "rerouted": int(((res["st"]["flags"] & 4) != 0).sum()),
+                         "roofline": {"bound": "fp64", "achieved_tflops": ach, "peak_tflops": peak, "frac": ach / peak,
+                                      "algorithmic_flop_per_update": W}}}
+    if steps:
+        del q
+        torch.cuda.empty_cache()
+        dx = 1.0 / 512
+        eps = torch.full((cells,), 1e-2, dtype=torch.float64, device="cuda")
+
+        def step():
+            kinetic.penalized_imex_step(f, nxl, ny, k, dx, 1.0 / ny, 0.1 * dx, eps)
+
+        ms_s = timed(step, max(1, iters // 2))
+        out["imex_step"] = {"ms": ms_s, "cell_updates_per_s": 2 * cells / (ms_s * 1e-3),
+                            "note": "PR(2,2,2): 2 Q + 2 transports + stage solves per cell-step; dt = 0.1 dx, eps = 1e-2"}
+    return out
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--configs", default="1,3")
     ap.add_argument("--nx", type=int, default=256)
+    ap.add_argument("--no-steps", action="store_true")
     args = ap.parse_args()
     for c in args.configs.split(","):
-        r = config1(args.iters) if c == "1" else config3(args.iters, args.nx, args.nx)
+        if c == "1":
+            r = config1(args.iters)
+        elif c == "5":
+            r = config5(args.iters, steps=not args.no_steps)
+        else:
+            r = config3(args.iters, args.nx, args.nx)
         print(json.dumps(r), flush=True)

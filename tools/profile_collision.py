@@ -24,6 +24,8 @@ vg = hk.make_velocity_grid(args.n, 8.0)
 kern = hk.precompute_kernel(vg, args.n, args.a1, args.a2, inputs.R_PHYS_MAX)
 if args.n == 32:
     f = inputs.config2_cells_torch(args.cells, 32, device="cuda")
+elif args.n == 64:
+    f = torch.from_numpy(inputs.config5_cells(args.cells, 64)).cuda()
 else:
     f = torch.from_numpy(inputs.config1_cells(args.cells, args.n)).cuda()
 q = torch.empty_like(f)
