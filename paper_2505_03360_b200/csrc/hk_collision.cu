@@ -943,7 +943,15 @@ __global__ void __launch_bounds__(256, 1) coll_fast_pipe_kernel(CollArgs a) {
 // plane, so the L2 latency of the tables overlaps the current round.
 // Slot counters count warps: 8 CTAs x 4 warps = 32 arrivals per use.
 // ---------------------------------------------------------------------------
-template <int N, int C>
+// DEFER (off by default, HK_FAST_KERNEL=d): a producer warp publishes field e
+// only after computing field e+1, so the release fence finds the stores long
+// completed — measured 10 % slower: the consumers already wait on `ready`
+// (17.5 % of cycles vs 12 % producer spin on `done`, HK_PROF_SPIN), so the
+// team is latency-coupled and later publication costs more than the fence.
+// (Also measured and removed: moving every other field's i2 transform from
+// the consumers to the producers to balance the 2:1 transform count: 27 %
+// slower, the producers became the late side.)
+template <int N, int C, bool DEFER>
 __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
     using G = GeoP<N, C>;
     constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
@@ -990,18 +998,26 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
             for (int i3 = 0; i3 < N; ++i3) cp_async16(wbuf_s + (i3 * 32 + lane) * 16, wt + i3 * N);
             cp_async_commit();
         };
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
         auto acquire = [&](unsigned gg) {
-            if (lane == 0) spin_geq(done + gg % D, ARR * (gg / D));
+            if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR * (gg / D));
             __syncwarp();
         };
         auto publish = [&](unsigned gg) {
             __syncwarp();
             if (lane == 0) signal_add(ready + gg % D);
         };
+        unsigned pend = ~0u;  // DEFER: field stored but not yet published
+        auto flush = [&]() {
+            if (pend != ~0u) publish(pend);
+            pend = ~0u;
+        };
         for (int64_t it = team; it < count; it += nteams, ++ncell) {
             const int64_t cell = a.list ? a.list[it] : it;
             const double* fc = a.f + cell * NB;
             // ---- prologue: f block (cooperative), 2-D forward transform of plane j3l = pw ----
+            flush();  // previous cell's loss field
             if (a.in_ready && t == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);  // host chunk has landed
             named_bar(1, 128);  // every producer warp is done with its weight plane
             for (int idx = t; idx < N * N * P; idx += 128) {
@@ -1058,26 +1074,48 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                     }
                 }
                 fft_reg<N, true>(x);
+                if (DEFER) flush();  // field e-1: its stores completed during this FFT
                 acquire(g);
                 double2* Xs = X + (int64_t)(g % D) * SLOT;
 #pragma unroll
                 for (int j3 = 0; j3 < N; ++j3)
                     st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
-                publish(g);
+                if (DEFER)
+                    pend = g;
+                else
+                    publish(g);
                 ++g;
             }
+        }
+        flush();
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
         }
     } else {
         // ================================ CONSUMER WARP ================================
         const int pl = pw;  // my plane: k1l (prologue) / j3l (rounds)
-        auto issue = [&](unsigned gg) {
-            if (lane == 0) spin_geq(ready + gg % D, ARR * (gg / D + 1));
-            __syncwarp();
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
+        auto pull = [&](unsigned gg) {
             const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + pl * N * N;
             const uint32_t d0 = smem_u32(Rvb + (gg & 1) * G::SLAB + pl * PLANE);
 #pragma unroll 8
             for (int k = 0; k < N; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
             cp_async_commit();
+        };
+        auto issue = [&](unsigned gg) {  // wait until every producer warp published gg, then pull
+            if (lane == 0) spin_cyc += spin_geq(ready + gg % D, ARR * (gg / D + 1));
+            __syncwarp();
+            pull(gg);
+        };
+        auto try_issue = [&](unsigned gg) -> bool {  // pull gg if it is already published
+            unsigned v = 0;
+            if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ready + gg % D) : "memory");
+            v = __shfl_sync(0xffffffffu, v, 0);
+            if ((int)(v - ARR * (gg / D + 1)) < 0) return false;
+            pull(gg);
+            return true;
         };
         auto complete = [&](unsigned gg) {
             cp_async_wait_all();
@@ -1137,7 +1175,9 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                 double2* Rv = Rvb + (g & 1) * G::SLAB + pl * PLANE;
                 complete(g);
                 const bool more = (e + 1 < n_entries) || (it + nteams < count);
-                if (more) issue(g + 1);
+                // prefetch g+1 if it is published; otherwise transform g first
+                // instead of idling on the counter (second chance after the rows)
+                bool pending = more && !try_issue(g + 1);
                 {  // inverse FFT over i2: row i1 = lane of my j3 plane
                     double2* row = Rv + lane * ROW;
                     double2 y[N];
@@ -1148,6 +1188,7 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                     for (int i = 0; i < N; ++i) row[i] = y[i];
                 }
                 __syncwarp();
+                if (pending) pending = !try_issue(g + 1);
                 double2 y[N];
                 {  // inverse FFT over i1: column j2 = lane
                     const double2* col = Rv + lane;
@@ -1156,6 +1197,7 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                     fft_reg<N, true>(y);
                 }
                 __syncwarp();  // reads of this buffer complete before it is refilled
+                if (pending) issue(g + 1);
                 if (!is_loss) {
                     const double m = (e == 0) ? a.mult0 : 1.0;
 #pragma unroll
@@ -1205,6 +1247,10 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                     ++g;
                 }
             }
+        }
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
         }
     }
     tmem_fence_before();
@@ -1716,8 +1762,13 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     // default: warp-autonomous 8-warp kernel; HK_FAST_KERNEL=x2|cta selects the split-pencil
     // 16-warp variant (measured slower: +70% instructions) or the CTA-synchronous one
     const char* kv = getenv("HK_FAST_KERNEL");
-    const int variant = !kv ? 1 : (kv[0] == 'x' ? 2 : (kv[0] == 'c' ? 0 : 1));
-    auto kern = variant == 2 ? coll_fast_x2_kernel<N, C> : (variant == 1 ? coll_fast_warp_kernel<N, C> : coll_fast_pipe_kernel<N, C>);
+    // variant 1: warp kernel (default), 3: warp kernel with deferred publish
+    // (measured 10 % slower), 2: x2, 0: CTA pipeline
+    const int variant = !kv ? 1 : (kv[0] == 'x' ? 2 : (kv[0] == 'c' ? 0 : (kv[0] == 'd' ? 3 : 1)));
+    auto kern = variant == 2 ? coll_fast_x2_kernel<N, C>
+              : variant == 1 ? coll_fast_warp_kernel<N, C, false>
+              : variant == 3 ? coll_fast_warp_kernel<N, C, true>
+                             : coll_fast_pipe_kernel<N, C>;
     const int nthreads = variant == 2 ? 512 : 256;
     const int key = N * 100 + C * 2 + 2000 + variant;
     int st;
@@ -1738,7 +1789,7 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     if (max_cells < teams) teams = max_cells;
     if (teams < 1) return HK_OK;
     CollArgs args = args_in;
-    if (variant == 1 && ctx->sio_in_ready) {  // streamed host I/O (warp kernel only)
+    if ((variant == 1 || variant == 3) && ctx->sio_in_ready) {  // streamed host I/O (warp kernels only)
         args.in_ready = ctx->sio_in_ready;
         args.out_done = ctx->sio_out_done;
         args.chunk = ctx->sio_chunk;
