@@ -22,7 +22,7 @@ struct CollArgs {
     int md;
     double mult0, jac, w;
     hk_cell_status* st;
-    double* nyq;       // [cell][3][N][N] |F| on the Nyquist planes (FAST) or null
+    double2* nyq;      // [cell][3][N][N] F on the Nyquist planes (FAST: guard + correction) or null
     double2* xchg;     // [cluster][2 buffers][2 fields][C dest][P][N][N] L2 transpose scratch
     unsigned* team_ctr;  // [teams] barrier counters (team kernel), zeroed per launch
     unsigned long long* prof;  // optional [4]: producer spin, consumer spin, producer total, consumer total (cycles)
@@ -40,5 +40,11 @@ struct CollArgs {
 // fast path that writes |F| on the Nyquist planes to args.nyq for the guard).
 size_t coll64_xchg_bytes(hk_ctx ctx);
 int launch_coll64(hk_ctx ctx, const CollArgs& args, bool exact, int64_t max_cells, int tag);
+
+// hk_nyqfix.cu: exact Nyquist correction of the fast result for the cells on a
+// device list (the guard's reroute list).
+int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int64_t max_cells, const double2* nyqF,
+                   const double* ta, const double* tap, int md, double mult0, double jac, double w, double* q,
+                   hk_cell_status* st);
 
 }  // namespace hk

@@ -299,16 +299,16 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                     }
                     if (!EXACT && a.nyq) {
                         constexpr int H = N / 2;
-                        double* ny = a.nyq + cell * 3 * N * N;
-                        if (h == 0) ny[2 * N * N + k1 * N + k2] = s * sqrt(v[H / 2].x * v[H / 2].x + v[H / 2].y * v[H / 2].y);
+                        double2* ny = a.nyq + cell * 3 * N * N;
+                        if (h == 0) ny[2 * N * N + k1 * N + k2] = make_double2(s * v[H / 2].x, s * v[H / 2].y);
                         if (k2 == H) {
 #pragma unroll
                             for (int m = 0; m < M; ++m)
-                                ny[1 * N * N + k1 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                                ny[1 * N * N + k1 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
                         }
                         if (k1 == H) {
 #pragma unroll
-                            for (int m = 0; m < M; ++m) ny[k2 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                            for (int m = 0; m < M; ++m) ny[k2 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
                         }
                     }
                     const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -153,23 +153,18 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
             for (int i = 0; i < N; ++i) row[i] = make_double2(x[i].x * s, x[i].y * s);
         }
         __syncthreads();
-        if (!EXACT && a.nyq) {  // |F| on the three Nyquist planes for the guard
-            double* ny = a.nyq + cell * 3 * N * N;
+        if (!EXACT && a.nyq) {  // F on the three Nyquist planes (guard + correction)
+            double2* ny = a.nyq + cell * 3 * N * N;
             constexpr int H = N / 2;
             for (int idx = t; idx < P * N; idx += 256) {
                 const int pl = idx / N, c = idx % N;
                 const int k1 = r * P + pl;
-                const double2 v1 = Fs[pl * PLANE + H * ROW + c];  // (k1, H, k3=c)
-                ny[1 * N * N + k1 * N + c] = sqrt(v1.x * v1.x + v1.y * v1.y);
-                const double2 v2 = Fs[pl * PLANE + c * ROW + H];  // (k1, k2=c, H)
-                ny[2 * N * N + k1 * N + c] = sqrt(v2.x * v2.x + v2.y * v2.y);
+                ny[1 * N * N + k1 * N + c] = Fs[pl * PLANE + H * ROW + c];  // (k1, H, k3=c)
+                ny[2 * N * N + k1 * N + c] = Fs[pl * PLANE + c * ROW + H];  // (k1, k2=c, H)
             }
             if (H / P == (int)r) {
                 const int pl = H % P;
-                for (int idx = t; idx < N * N; idx += 256) {
-                    const double2 v = Fs[pl * PLANE + (idx / N) * ROW + (idx % N)];
-                    ny[idx] = sqrt(v.x * v.x + v.y * v.y);
-                }
+                for (int idx = t; idx < N * N; idx += 256) ny[idx] = Fs[pl * PLANE + (idx / N) * ROW + (idx % N)];
             }
         }
 
@@ -499,15 +494,15 @@ __global__ void __launch_bounds__(128, 2) coll_fast_tmem_kernel(CollArgs a) {
             }
             if (a.nyq) {
                 constexpr int H = N / 2;
-                double* ny = a.nyq + cell * 3 * N * N;
-                ny[2 * N * N + k1 * N + k2] = s * sqrt(x[H].x * x[H].x + x[H].y * x[H].y);
+                double2* ny = a.nyq + cell * 3 * N * N;
+                ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
                 if (k2 == H) {
 #pragma unroll
-                    for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                    for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
                 }
                 if (k1 == H) {
 #pragma unroll
-                    for (int c = 0; c < N; ++c) ny[k2 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                    for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
                 }
             }
             const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -815,15 +810,15 @@ __global__ void __launch_bounds__(256, 1) coll_fast_pipe_kernel(CollArgs a) {
                 }
                 if (a.nyq) {
                     constexpr int H = N / 2;
-                    double* ny = a.nyq + cell * 3 * N * N;
-                    ny[2 * N * N + k1 * N + k2] = s * sqrt(x[H].x * x[H].x + x[H].y * x[H].y);
+                    double2* ny = a.nyq + cell * 3 * N * N;
+                    ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
                     if (k2 == H) {
 #pragma unroll
-                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
                     }
                     if (k1 == H) {
 #pragma unroll
-                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
                     }
                 }
                 const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1148,15 +1143,15 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                 }
                 if (a.nyq) {
                     constexpr int H = N / 2;
-                    double* ny = a.nyq + cell * 3 * N * N;
-                    ny[2 * N * N + k1 * N + k2] = s * sqrt(x[H].x * x[H].x + x[H].y * x[H].y);
+                    double2* ny = a.nyq + cell * 3 * N * N;
+                    ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
                     if (k2 == H) {
 #pragma unroll
-                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
                     }
                     if (k1 == H) {
 #pragma unroll
-                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = s * sqrt(x[c].x * x[c].x + x[c].y * x[c].y);
+                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
                     }
                 }
                 const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1453,16 +1448,16 @@ __global__ void __launch_bounds__(512, 1) coll_fast_x2_kernel(CollArgs a) {
                 }
                 if (a.nyq) {
                     constexpr int H = N / 2;
-                    double* ny = a.nyq + cell * 3 * N * N;
-                    if (h == 0) ny[2 * N * N + k1 * N + k2] = s * sqrt(v[8].x * v[8].x + v[8].y * v[8].y);  // k3 = 16
+                    double2* ny = a.nyq + cell * 3 * N * N;
+                    if (h == 0) ny[2 * N * N + k1 * N + k2] = make_double2(s * v[8].x, s * v[8].y);  // k3 = 16
                     if (k2 == H) {
 #pragma unroll
                         for (int m = 0; m < 16; ++m)
-                            ny[1 * N * N + k1 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                            ny[1 * N * N + k1 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
                     }
                     if (k1 == H) {
 #pragma unroll
-                        for (int m = 0; m < 16; ++m) ny[k2 * N + 2 * m + h] = s * sqrt(v[m].x * v[m].x + v[m].y * v[m].y);
+                        for (int m = 0; m < 16; ++m) ny[k2 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
                     }
                 }
                 const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1563,7 +1558,7 @@ __global__ void __launch_bounds__(512, 1) coll_fast_x2_kernel(CollArgs a) {
 // memory once per block (K-chunks of KC), so they are read once per GC cells.
 constexpr int GC = 16, KC = 64, KS = KC + 1;  // KS: padded row stride (bank-conflict free)
 __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0, double jac, double w, double tau,
-                                                    const double* __restrict__ nyq, const double* __restrict__ abs_a,
+                                                    const double2* __restrict__ nyq, const double* __restrict__ abs_a,
                                                     const double* __restrict__ abs_ap, int64_t ncells,
                                                     hk_cell_status* __restrict__ st, int64_t* __restrict__ list,
                                                     int* __restrict__ count) {
@@ -1583,13 +1578,18 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
         __syncthreads();
         for (int i = threadIdx.x; i < GC * KC; i += blockDim.x) {
             const int c = i / KC, k = i % KC;
-            sF[i] = (c0 + c < ncells && k0 + k < nn3) ? nyq[(c0 + c) * nn3 + k0 + k] : 0.0;
+            double v = 0.0;
+            if (c0 + c < ncells && k0 + k < nn3) {
+                const double2 z = nyq[(c0 + c) * nn3 + k0 + k];
+                v = sqrt(z.x * z.x + z.y * z.y);
+            }
+            sF[i] = v;
         }
         for (int i = threadIdx.x; i < md * KC; i += blockDim.x) {
             const int e = i / KC, k = i % KC;
             const bool ok = k0 + k < nn3;
-            sA[e * KS + k] = ok ? __ldg(abs_a + (int64_t)e * nn3 + k0 + k) : 0.0;
-            sB[e * KS + k] = ok ? __ldg(abs_ap + (int64_t)e * nn3 + k0 + k) : 0.0;
+            sA[e * KS + k] = ok ? fabs(__ldg(abs_a + (int64_t)e * nn3 + k0 + k)) : 0.0;  // signed tables
+            sB[e * KS + k] = ok ? fabs(__ldg(abs_ap + (int64_t)e * nn3 + k0 + k)) : 0.0;
         }
         __syncthreads();
 #pragma unroll
@@ -1831,7 +1831,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     const int64_t nn3 = 3LL * N * N;
     // scratch: [nyq |F| planes][reroute list][count]
     const size_t st_bytes = st ? 0 : sizeof(hk_cell_status) * ncells;
-    const size_t nyq_bytes = guard ? sizeof(double) * nn3 * ncells : 0;
+    const size_t nyq_bytes = guard ? sizeof(double2) * nn3 * ncells : 0;
     const size_t list_bytes = guard ? sizeof(int64_t) * ncells : 0;
     const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255) & ~size_t(255);
     size_t xchg_bytes;
@@ -1843,7 +1843,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
     char* base = static_cast<char*>(ctx->scratch);
     if (!st) st = reinterpret_cast<hk_cell_status*>(base);
-    double* nyq = guard ? reinterpret_cast<double*>(base + st_bytes) : nullptr;
+    double2* nyq = guard ? reinterpret_cast<double2*>(base + st_bytes) : nullptr;
     int64_t* list = guard ? reinterpret_cast<int64_t*>(base + st_bytes + nyq_bytes) : nullptr;
     int* count = reinterpret_cast<int*>(base + st_bytes + nyq_bytes + list_bytes);
     cudaMemsetAsync(st, 0, sizeof(hk_cell_status) * ncells, ctx->stream);
@@ -1908,11 +1908,19 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
             timing_end(ctx);
             ctx->launches++;
             if ((s = check_cuda(ctx, cudaGetLastError(), "guard kernel"))) return s;
-            CollArgs b = a;
-            b.nyq = nullptr;
-            b.list = list;
-            b.list_count = count;
-            if ((s = launch_exact(b, 2))) return s;
+            if (getenv("HK_GUARD_EXACT")) {  // comparison path: recompute the listed cells exactly
+                CollArgs b = a;
+                b.nyq = nullptr;
+                b.list = list;
+                b.list_count = count;
+                if ((s = launch_exact(b, 2))) return s;
+            } else {  // add the exact Nyquist term to the listed cells (hk_nyqfix.cu)
+                timing_begin(ctx, 2);
+                s = launch_nyq_fix(ctx, N, list, count, ncells, nyq, k->abs_a, k->abs_ap, k->md, k->mult0, k->jac,
+                                   k->weight, q, st);
+                timing_end(ctx);
+                if (s) return s;
+            }
         }
     }
     {

@@ -37,6 +37,9 @@ struct hk_ctx_s {
     int64_t sio_flags_n = 0;
     int64_t* last_list = nullptr;
     int* last_count = nullptr;
+    // Nyquist-correction plane scratch (hk_nyqfix.cu)
+    void* fix_scratch = nullptr;
+    size_t fix_bytes = 0;
     // NCCL communicator (hk_comm.cu; ncclComm_t, loaded at run time)
     void* comm = nullptr;
     int nranks = 1, rank = 0;
@@ -57,8 +60,8 @@ struct hk_kernel_s {
     double* alpha_p = nullptr;  // [md][n^3] exact planar weights
     double* loss = nullptr;     // [n^3] loss_diag (reference summation order)
     double2* wfast = nullptr;   // [md+1][n^3] Hermitian-symmetrised (alpha_s, alpha'_s); entry md = (loss_s, 0)
-    double* abs_a = nullptr;    // [md][3][n][n] |antisymmetric alpha| on the Nyquist planes
-    double* abs_ap = nullptr;   // [md][3][n][n]
+    double* abs_a = nullptr;    // [md][3][n][n] antisymmetric alpha on the Nyquist planes (signed)
+    double* abs_ap = nullptr;   // [md][3][n][n] antisymmetric alpha' (signed)
     double absmax = 0;          // max over the abs tables (diagnostic)
 };
 

@@ -1,0 +1,260 @@
+// hk_nyqfix.cu — exact Nyquist correction of fast-path cells.
+//
+// The FAST collision kernels return Q_fast = jac (w sum_d m_d gs_d hs_d - f L)
+// with gs + i hs = IFFT(F (alpha_s + i alpha'_s)).  The exact operator of
+// spectral_collision (src/spectral.cpp:114-154) has Re(ga gb) = gs hs - ga_i hb_i,
+// where ga_i = IFFT(alpha_a F) / i and hb_i = IFFT(alpha'_a F) / i come from the
+// antisymmetric parts of the weights, which live on the three Nyquist sets only
+// (S1: k1 = H;  S2: k2 = H, k1 != H;  S3: k3 = H, k1, k2 != H;  H = N/2).  A
+// Nyquist set is a plane, so its 3-D inverse transform is a 2-D transform times
+// a sign along the normal axis:
+//     ga_i(j) = (-1)^j1 A1(j2, j3) + (-1)^j2 A2(j1, j3) + (-1)^j3 A3(j1, j2),
+// with one complex 2-D transform per plane giving both A and B (hb_i) because
+// each restricted input is anti-Hermitian:  IFFT2(Y_a + i Y_b) = -B + i A.
+// Two kernels add  -jac w sum_d m_d ga_i,d hb_i,d  to Q for the cells on the
+// guard's list, turning their fast result into the exact one (real part) at a
+// few per cent of the cost of re-running the exact collision kernel:
+//   nyq_planes_kernel: per (cell, direction) the three packed 2-D transforms
+//                      (SMEM, in place) -> scratch [cell][d][3][N][N];
+//   nyq_apply_kernel:  per (cell, slab of T j1-planes) the correction of every
+//                      node accumulated over all directions in registers, then
+//                      one read-modify-write of Q.
+// The list is processed in chunks sized to bound the scratch (~2 GiB).
+#include <cstdio>
+#include <cstdlib>
+
+#include "hk_coll.cuh"
+#include "hk_common.cuh"
+
+namespace hk {
+
+template <int N>
+struct GeoFix {
+    static constexpr int ROW = N + 1;
+    static constexpr int PLANE = N * ROW;                          // double2, padded plane
+    static constexpr int NN = N * N;
+    static constexpr size_t SMEM1 = size_t(3) * PLANE * sizeof(double2);
+    static constexpr int T = N >= 64 ? 4 : (N >= 32 ? 8 : 16);    // j1 planes per apply work item
+    static constexpr int MP = NN / 256;                            // (j2, j3) pairs per thread
+    static constexpr int STAGE = NN + 2 * T * N;                   // double2 per direction in SMEM
+    static constexpr size_t SMEM2 = size_t(2) * STAGE * sizeof(double2) + 64 * sizeof(double);
+};
+
+// Inverse 1-D transforms of `npen` pencils in shared memory, in place, natural
+// order: pencil p starts at base + (p / ppg) gstride + (p % ppg) pstride, its
+// elements are estride apart.
+template <int N>
+__device__ __forceinline__ void smem_fft_pass(double2* base, int npen, int pstride, int estride, int ppg = 1 << 30,
+                                              int gstride = 0) {
+    auto at = [&](int p) { return base + (size_t)(p / ppg) * gstride + (size_t)(p % ppg) * pstride; };
+    if constexpr (N <= 32) {
+        for (int p = threadIdx.x; p < npen; p += blockDim.x) {
+            double2* x0 = at(p);
+            double2 v[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) v[i] = x0[i * estride];
+            fft_reg<N, true>(v);
+#pragma unroll
+            for (int i = 0; i < N; ++i) x0[i * estride] = v[i];
+        }
+    } else {  // N = 64: one pencil per lane pair (l, l ^ 16)
+        constexpr int M = N / 2, Q = M / 2;
+        const int lane = threadIdx.x & 31, h = lane >> 4;
+        const int slot0 = (threadIdx.x >> 5) * 16 + (lane & 15);
+        const int slots = blockDim.x / 2;
+        for (int pb = 0; pb < npen; pb += slots) {  // uniform trip count: the pair shuffles
+            const int p = pb + slot0;
+            const bool on = p < npen;
+            double2* x0 = at(on ? p : 0);
+            double2 v[M];
+#pragma unroll
+            for (int j = 0; j < Q; ++j) {
+                v[j] = on ? x0[(h * Q + j) * estride] : make_double2(0.0, 0.0);
+                v[Q + j] = on ? x0[(M + h * Q + j) * estride] : make_double2(0.0, 0.0);
+            }
+            fftxh_dif<M, true>(v, h);
+            __syncwarp();
+            if (on) {
+#pragma unroll
+                for (int m = 0; m < M; ++m) x0[(2 * m + h) * estride] = v[m];
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Phase 1: Z_p = IFFT2((alpha_a + i alpha'_a) F |_{S_p}) = -B_p + i A_p for every
+// (listed cell, direction) of the chunk -> planes[w][3][N][N], w = local cell * md + d.
+template <int N>
+__global__ void __launch_bounds__(256) nyq_planes_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
+                                                         int64_t chunk0, int64_t chunk_n, const double2* __restrict__ nyqF,
+                                                         const double* __restrict__ ta, const double* __restrict__ tap,
+                                                         int md, double2* __restrict__ planes) {
+    using G = GeoFix<N>;
+    constexpr int ROW = G::ROW, PLANE = G::PLANE, NN = G::NN;
+    extern __shared__ __align__(16) double2 sm[];
+    const int t = threadIdx.x;
+    int64_t avail = (int64_t)*count - chunk0;
+    if (avail > chunk_n) avail = chunk_n;
+    for (int64_t wi = blockIdx.x; wi < avail * md; wi += gridDim.x) {
+        const int64_t it = chunk0 + wi / md;
+        const int d = (int)(wi % md);
+        const int64_t cell = list[it];
+        const double2* Fc = nyqF + cell * 3 * NN;
+        __syncthreads();  // previous item's planes written out
+        for (int i = t; i < 3 * NN; i += blockDim.x) {
+            const int64_t toff = (int64_t)d * 3 * NN + i;
+            const double a = __ldg(ta + toff), b = __ldg(tap + toff);
+            const double2 F = Fc[i];
+            sm[(i / NN) * PLANE + ((i % NN) / N) * ROW + (i % N)] = make_double2(a * F.x - b * F.y, a * F.y + b * F.x);
+        }
+        __syncthreads();
+        smem_fft_pass<N>(sm, 3 * N, ROW, 1);             // rows of the three planes
+        __syncthreads();
+        smem_fft_pass<N>(sm, 3 * N, 1, ROW, N, PLANE);   // columns
+        __syncthreads();
+        double2* out = planes + wi * 3 * NN;
+        for (int i = t; i < 3 * NN; i += blockDim.x) out[i] = sm[(i / NN) * PLANE + ((i % NN) / N) * ROW + (i % N)];
+    }
+}
+
+// Phase 2: per (listed cell, j1 slab) accumulate -sum_d m_d ga_i hb_i over all
+// directions in registers (thread: MP (j2, j3) pairs x T planes), then Q += jac w acc.
+template <int N>
+__global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
+                                                           int64_t chunk0, int64_t chunk_n,
+                                                           const double2* __restrict__ planes, int md, double mult0,
+                                                           double jac, double w, double* __restrict__ q,
+                                                           hk_cell_status* __restrict__ st) {
+    using G = GeoFix<N>;
+    constexpr int NN = G::NN, T = G::T, MP = G::MP, STAGE = G::STAGE, SLABS = N / T;
+    constexpr int64_t NB = (int64_t)N * N * N;
+    extern __shared__ __align__(16) double2 sm[];
+    double* red = reinterpret_cast<double*>(sm + 2 * STAGE);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int64_t avail = (int64_t)*count - chunk0;
+    if (avail > chunk_n) avail = chunk_n;
+    for (int64_t wi = blockIdx.x; wi < avail * SLABS; wi += gridDim.x) {
+        const int64_t lc = wi / SLABS;
+        const int slab = (int)(wi % SLABS), j1_0 = slab * T;
+        const int64_t cell = list[chunk0 + lc];
+        const double2* pc = planes + lc * md * 3 * NN;
+        // stage direction d: plane 0 (full), rows j1_0.. of planes 1 and 2
+        auto stage = [&](int d, int buf) {
+            const double2* src = pc + (int64_t)d * 3 * NN;
+            const uint32_t dst = smem_u32(sm + buf * STAGE);
+            for (int i = t; i < STAGE; i += blockDim.x) {
+                const double2* g = i < NN ? src + i
+                                 : (i < NN + T * N ? src + NN + j1_0 * N + (i - NN)
+                                                   : src + 2 * NN + j1_0 * N + (i - NN - T * N));
+                cp_async16(dst + i * 16, g);
+            }
+            cp_async_commit();
+        };
+        double acc[MP * T];
+#pragma unroll
+        for (int k = 0; k < MP * T; ++k) acc[k] = 0.0;
+        __syncthreads();  // previous item done with both buffers
+        stage(0, 0);
+        for (int d = 0; d < md; ++d) {
+            cp_async_wait_all();
+            __syncthreads();  // direction d landed for every thread; buffer d+1 free
+            if (d + 1 < md) stage(d + 1, (d + 1) & 1);
+            const double2* P0 = sm + (d & 1) * STAGE;
+            const double2* P1 = P0 + NN;
+            const double2* P2 = P1 + T * N;
+            const double mu = (d == 0) ? mult0 : 1.0;
+#pragma unroll
+            for (int m = 0; m < MP; ++m) {
+                const int p = t + 256 * m, j2 = p / N, j3 = p % N;
+                const double2 z0 = P0[p];
+                const double s2 = (j2 & 1) ? -1.0 : 1.0, s3 = (j3 & 1) ? -1.0 : 1.0;
+#pragma unroll
+                for (int tt = 0; tt < T; ++tt) {
+                    const double s1 = ((j1_0 + tt) & 1) ? -1.0 : 1.0;
+                    const double2 z1 = P1[tt * N + j3], z2 = P2[tt * N + j2];
+                    const double A = s1 * z0.y + s2 * z1.y + s3 * z2.y;
+                    const double B = s1 * z0.x + s2 * z1.x + s3 * z2.x;  // = -hb_i
+                    acc[m * T + tt] += mu * (A * B);                     // = -m ga_i hb_i
+                }
+            }
+        }
+        double mre = 0.0, n2 = 0.0;
+        double* qc = q + cell * NB;
+#pragma unroll
+        for (int m = 0; m < MP; ++m) {
+            const int p = t + 256 * m;
+#pragma unroll
+            for (int tt = 0; tt < T; ++tt) {
+                const int64_t gi = (int64_t)(j1_0 + tt) * NN + p;
+                const double qv = qc[gi] + jac * w * acc[m * T + tt];
+                qc[gi] = qv;
+                mre = fmax(mre, fabs(qv));
+                n2 += qv * qv;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        }
+        if (lane == 0) {
+            red[warp] = mre;
+            red[32 + warp] = n2;
+        }
+        __syncthreads();
+        if (t == 0) {  // the guard cleared max_re / q_norm2 of listed cells
+            double m1 = 0.0, s = 0.0;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+                m1 = fmax(m1, red[k]);
+                s += red[32 + k];
+            }
+            atomic_max_nonneg(&st[cell].max_re, m1);
+            atomicAdd(&st[cell].q_norm2, s);
+        }
+    }
+}
+
+int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int64_t max_cells, const double2* nyqF,
+                   const double* ta, const double* tap, int md, double mult0, double jac, double w, double* q,
+                   hk_cell_status* st) {
+    if (max_cells < 1) return HK_OK;
+    const size_t per_cell = size_t(md) * 3 * n * n * sizeof(double2);
+    int64_t chunk = int64_t((size_t(2) << 30) / per_cell);
+    if (chunk < 1) chunk = 1;
+    if (chunk > max_cells) chunk = max_cells;
+    const size_t need = per_cell * chunk;
+    if (need > ctx->fix_bytes) {
+        if (ctx->fix_scratch) {
+            cudaStreamSynchronize(ctx->stream);
+            cudaFree(ctx->fix_scratch);
+            ctx->fix_scratch = nullptr;
+            ctx->fix_bytes = 0;
+        }
+        int s = check_cuda(ctx, cudaMalloc(&ctx->fix_scratch, need), "nyq_fix scratch");
+        if (s) return s;
+        ctx->fix_bytes = need;
+    }
+    double2* planes = static_cast<double2*>(ctx->fix_scratch);
+    auto run = [&](auto k1, size_t smem1, int per_sm1, auto k2, size_t smem2) -> int {
+        int s;
+        if ((s = check_cuda(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem")) ||
+            (s = check_cuda(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), "smem")))
+            return s;
+        for (int64_t c0 = 0; c0 < max_cells; c0 += chunk) {
+            k1<<<unsigned(ctx->sm_count * per_sm1), 256, smem1, ctx->stream>>>(list, count, c0, chunk, nyqF, ta, tap, md, planes);
+            k2<<<unsigned(ctx->sm_count), 256, smem2, ctx->stream>>>(list, count, c0, chunk, planes, md, mult0, jac, w, q, st);
+            ctx->launches += 2;
+            if ((s = check_cuda(ctx, cudaGetLastError(), "nyq_fix kernels"))) return s;
+        }
+        return HK_OK;
+    };
+    switch (n) {
+    case 16: return run(nyq_planes_kernel<16>, GeoFix<16>::SMEM1, 8, nyq_apply_kernel<16>, GeoFix<16>::SMEM2);
+    case 32: return run(nyq_planes_kernel<32>, GeoFix<32>::SMEM1, 4, nyq_apply_kernel<32>, GeoFix<32>::SMEM2);
+    case 64: return run(nyq_planes_kernel<64>, GeoFix<64>::SMEM1, 1, nyq_apply_kernel<64>, GeoFix<64>::SMEM2);
+    default: return fail(ctx, HK_UNSUPPORTED, "nyq_fix: n = 16, 32, 64");
+    }
+}
+
+}  // namespace hk

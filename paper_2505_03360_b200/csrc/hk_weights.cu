@@ -11,7 +11,8 @@
 //     own tables uploaded verbatim) build the device layouts:
 //        exact  alpha / alpha_p / loss   [entry][i1][i3][i2]
 //        fast   (alpha_s, alpha'_s)      Hermitian-symmetrised, entry md = (loss_s, 0)
-//        guard  |alpha_a|, |alpha'_a|    on the three Nyquist planes.
+//        nyquist alpha_a, alpha'_a  antisymmetric parts on the three Nyquist planes
+//                                   (signed: the guard takes |.|, the correction kernel the values).
 #include <cmath>
 
 #include "hk_common.cuh"
@@ -91,7 +92,7 @@ __global__ void layout_kernel(int n, int a2, int md, const double* __restrict__ 
         alpha[(int64_t)e * total + dev] = a;
         alpha_p[(int64_t)e * total + dev] = ap;
         wfast[(int64_t)e * total + dev] = make_double2(0.5 * (a + am), 0.5 * (ap + apm));
-        const double aa = 0.5 * fabs(a - am), aap = 0.5 * fabs(ap - apm);
+        const double aa = 0.5 * (a - am), aap = 0.5 * (ap - apm);  // signed antisymmetric parts
         double* pa = abs_a + (int64_t)e * 3 * nn;
         double* pap = abs_ap + (int64_t)e * 3 * nn;
         // Nyquist planes, each S point counted once (plane 0, then 1, then 2).

@@ -137,3 +137,23 @@ def test_n32_streamed_host_path_matches_device_path(hk):
     assert np.array_equal(q_host, q_dev.cpu().numpy())
     assert np.array_equal(st_host["flags"], st_dev["flags"])
     assert (st_host["flags"] & 4).sum() > 0  # some cells rerouted: the re-fetch path ran
+
+
+def test_n32_nyquist_correction_equals_exact(hk):
+    """Cells whose spectrum reaches the Nyquist planes (config-5 shock cells on
+    the 32^3 grid: the truncated downstream Maxwellian) fail the guard; their
+    fast result plus the exact Nyquist correction (hk_nyqfix.cu) must equal the
+    exact kernel's Q to round-off."""
+    import torch
+    vg = hk.make_velocity_grid(32, inputs.VMAX)
+    k = hk.precompute_kernel(vg, 32, 8, 8, inputs.R_PHYS_MAX)
+    f = torch.from_numpy(inputs.config5_cells(48, 32, columns=list(range(240, 272)) + [400, 450, 500, 511])).cuda()
+    qd, st = hk.spectral_collision(f, k, return_status=True)
+    qe = hk.spectral_collision(f, k, exact=True)
+    qd, qe = qd.cpu().numpy(), qe.cpu().numpy()
+    fixed = (st["flags"] & 4) != 0
+    assert fixed.sum() >= 4  # the correction path ran
+    for c in range(len(qd)):
+        assert rel_l2(qd[c], qe[c]) < 1e-12 if fixed[c] else rel_l2(qd[c], qe[c]) < TOL, c
+    # the corrected cells' verdicts describe the corrected Q
+    np.testing.assert_allclose(st["q_norm2"][fixed], (qd[fixed] ** 2).sum(1), rtol=1e-12)
