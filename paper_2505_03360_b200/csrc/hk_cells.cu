@@ -19,6 +19,7 @@
 //   penalized_stage_solve  src/boltzmann.cpp:29-45
 //   esbgk_stage_solve      src/esbgk.cpp:9-45
 #include <cmath>
+#include <cstdlib>
 
 #include "hk_cells.cuh"
 #include "hk_common.cuh"
@@ -603,6 +604,8 @@ __device__ double maxwell_factors_w(const Mom& m, const VGrid& g, double* ex, do
 // Coupling matrix from the 14 weighted monomial moments of w (degree <= 4)
 // instead of 25 direct products: A = sum phi psi^T w with psi affine in
 // (1, v, |v|^2) (src/moments.cpp:164-189 evaluates the same sums directly).
+__device__ void coupling_from_monomials(const double (&M)[14], const double uc[3], double dvk, double (&A)[25]);
+
 template <typename WF>
 __device__ void coupling_w(const VGrid& g, int lg, const double uc[3], WF wfun, double (&A)[25]) {
     double M[14];  // M0, M1[3], M2[xx xy xz yy yz zz], M3[3] (= sum v^2 v_i w), M4
@@ -625,6 +628,11 @@ __device__ void coupling_w(const VGrid& g, int lg, const double uc[3], WF wfun, 
         }
     });
     warp_sum<14>(M);
+    coupling_from_monomials(M, uc, g.dvk, A);
+}
+
+// A_rc = sum phi_r psi_c w dvK from the 14 weighted monomial moments of w.
+__device__ void coupling_from_monomials(const double (&M)[14], const double uc[3], double dvk, double (&A)[25]) {
     const double M0 = M[0];
     const double M1[3] = {M[1], M[2], M[3]};
     const double M2[3][3] = {{M[4], M[5], M[6]}, {M[5], M[7], M[8]}, {M[6], M[8], M[9]}};
@@ -647,7 +655,7 @@ __device__ void coupling_w(const VGrid& g, int lg, const double uc[3], WF wfun, 
     for (int i = 0; i < 3; ++i) A[21 + i] = M3[i] - uc[i] * Mv2;
     A[24] = M4 - 2.0 * ucM3 + U2 * Mv2;
 #pragma unroll
-    for (int i = 0; i < 25; ++i) A[i] *= g.dvk;
+    for (int i = 0; i < 25; ++i) A[i] *= dvk;
 }
 
 __global__ void __launch_bounds__(32 * WPB, HK_MOM_MINB) moments_warp_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
@@ -940,6 +948,440 @@ __global__ void __launch_bounds__(32 * WPB, HK_STAGE_MINB) residual_finish_warp_
     }
 }
 
+// ---------------------------------------------------------------------------
+// moments + second moment + realizability + L1, one 512-thread CTA per cell,
+// one CTA per SM (grid = SM count): the 148 blocks in flight (37 MB at N = 32)
+// stay in L2, so the L1 pass re-reads the block from L2, not HBM.
+// Realizability from ONE pass of raw monomial moments up to degree 4
+// (S, S_i, S_ij, R_i = sum |v|^2 v_i f, Q4 = sum |v|^4 f) via the central-
+// moment identities (c = v - u):
+//   C_ij          = S_ij - u_i u_j S
+//   sum |c|^2 c_i = R_i - u_i P - 2 (S2 u)_i + 2 u_i |u|^2 S,   P = tr S2
+//   sum |c|^4     = Q4 + 4 u.S2.u - 4 u.R + 2 |u|^2 P - 3 |u|^4 S
+// (src/moments.cpp:269-312 sums the same quantities over V = c / sqrt(T)
+// directly; the identities are exact, cancellation costs ~|u|^4 / T^2 ulps).
+// ---------------------------------------------------------------------------
+template <int MT, int MINB>
+__global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
+                                                            int lg, double* __restrict__ mom, double* __restrict__ sigma,
+                                                            double* __restrict__ real, double* __restrict__ l1,
+                                                            int* __restrict__ status) {
+    __shared__ double red[MT / 32][16];
+    __shared__ double tabs[3][128];
+    __shared__ double bc[8];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = g.n, nb = n * n * n, npairs = nb >> 1;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        const double* fc = f + cell * nb;
+        double M[14];  // S, Sx, Sy, Sz, Sxx, Sxy, Sxz, Syy, Syz, Szz, Rx, Ry, Rz, Q4
+#pragma unroll
+        for (int k = 0; k < 14; ++k) M[k] = 0.0;
+#pragma unroll 4
+        for (int p = t; p < npairs; p += MT) {
+            const int idx = 2 * p;
+            const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
+            const double vx = g.node(k1), vy = g.node(k2), z0 = g.node(k3), z1 = g.node(k3 + 1);
+            const double2 w = ldg2(fc + idx);
+            const double zz0 = z0 * z0, zz1 = z1 * z1;
+            const double m0 = w.x + w.y, m1 = z0 * w.x + z1 * w.y, m2 = zz0 * w.x + zz1 * w.y;
+            const double m3 = zz0 * (z0 * w.x) + zz1 * (z1 * w.y), m4 = zz0 * (zz0 * w.x) + zz1 * (zz1 * w.y);
+            const double xx = vx * vx, yy = vy * vy, r2 = xx + yy;
+            M[0] += m0;
+            M[1] += vx * m0;
+            M[2] += vy * m0;
+            M[3] += m1;
+            M[4] += xx * m0;
+            M[5] += vx * (vy * m0);
+            M[6] += vx * m1;
+            M[7] += yy * m0;
+            M[8] += vy * m1;
+            M[9] += m2;
+            const double a = r2 * m0 + m2;
+            M[10] += vx * a;
+            M[11] += vy * a;
+            M[12] += r2 * m1 + m3;
+            M[13] += r2 * (r2 * m0 + 2.0 * m2) + m4;
+        }
+#pragma unroll
+        for (int k = 0; k < 14; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) M[k] += __shfl_xor_sync(0xffffffffu, M[k], o);
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 14; ++k) red[warp][k] = M[k];
+        __syncthreads();
+        if (t == 0) {
+            double S[14];
+            for (int k = 0; k < 14; ++k) {
+                double v = 0.0;
+                for (int w2 = 0; w2 < MT / 32; ++w2) v += red[w2][k];
+                S[k] = v;
+            }
+            const double s11[11] = {S[0], S[1], S[2], S[3], S[4] + S[7] + S[9], S[4], S[5], S[6], S[7], S[8], S[9]};
+            Mom m;
+            const int st = moments_from_sums(s11, g, m);
+            if (mom) {
+                double* o = mom + cell * 5;
+                o[0] = m.rho; o[1] = m.ux; o[2] = m.uy; o[3] = m.uz; o[4] = m.T;
+            }
+            if (sigma)
+                for (int k = 0; k < 6; ++k) sigma[cell * 6 + k] = s11[5 + k] * g.dvk;
+            if (status) status[cell] = st;
+            if (st == HK_OK && real) {
+                const double u[3] = {m.ux, m.uy, m.uz};
+                const double S2[3][3] = {{S[4], S[5], S[6]}, {S[5], S[7], S[8]}, {S[6], S[8], S[9]}};
+                const double R[3] = {S[10], S[11], S[12]};
+                const double S0 = S[0], P = S[4] + S[7] + S[9];
+                const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+                double C[3][3], c3[3], S2u[3];
+                for (int i = 0; i < 3; ++i) {
+                    S2u[i] = S2[i][0] * u[0] + S2[i][1] * u[1] + S2[i][2] * u[2];
+                    for (int j = 0; j < 3; ++j) C[i][j] = S2[i][j] - u[i] * u[j] * S0;
+                    c3[i] = R[i] - u[i] * P - 2.0 * S2u[i] + 2.0 * u[i] * uu * S0;
+                }
+                const double uS2u = u[0] * S2u[0] + u[1] * S2u[1] + u[2] * S2u[2];
+                const double uR = u[0] * R[0] + u[1] * R[1] + u[2] * R[2];
+                const double c4 = S[13] + 4.0 * uS2u - 4.0 * uR + 2.0 * uu * P - 3.0 * uu * uu * S0;
+                const double c2 = C[0][0] + C[1][1] + C[2][2];
+                const double T = m.T, iS = 1.0 / S0;
+                double s2[3][3];
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) s2[i][j] = C[i][j] / T * iS;
+                const double tr3 = (s2[0][0] + s2[1][1] + s2[2][2]) / 3.0;
+                double* o = real + cell * 13;
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) o[3 * i + j] = s2[i][j] - (i == j ? tr3 : 0.0);
+                const double it32 = 1.0 / (T * sqrt(T));
+                for (int i = 0; i < 3; ++i) o[9 + i] = 0.5 * c3[i] * it32 * iS;  // sum (|V|^2 - 5)/2 V_i f / S
+                // C = 0.4 sum (|V|^2/2 - 5/2)^2 f / S = 0.4 (|V|^4/4 - 5/2 |V|^2 + 25/4) averaged
+                o[12] = 0.4 * (0.25 * c4 / (T * T) - 2.5 * c2 / T + 6.25 * S0) * iS;
+            }
+            bc[0] = st;
+            bc[1] = m.rho; bc[2] = m.ux; bc[3] = m.uy; bc[4] = m.uz; bc[5] = m.T;
+        }
+        __syncthreads();
+        if (l1 && bc[0] == 0.0) {
+            Mom m{bc[1], bc[2], bc[3], bc[4], bc[5]};
+            const double inv2T = 0.5 / m.T;
+            for (int k = t; k < n; k += MT) {
+                const double v = g.node(k);
+                tabs[0][k] = exp(-(v - m.ux) * (v - m.ux) * inv2T);
+                tabs[1][k] = exp(-(v - m.uy) * (v - m.uy) * inv2T);
+                tabs[2][k] = exp(-(v - m.uz) * (v - m.uz) * inv2T);
+            }
+            const double pref = m.rho / pow(2.0 * M_PI * m.T, 1.5);
+            __syncthreads();
+            double acc = 0.0;
+#pragma unroll 4
+            for (int p = t; p < npairs; p += MT) {
+                const int idx = 2 * p;
+                const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
+                const double2 w = ldg2(fc + idx);
+                const double pxy = pref * tabs[0][k1] * tabs[1][k2];
+                acc += fabs(w.x - pxy * tabs[2][k3]) + fabs(w.y - pxy * tabs[2][k3 + 1]);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) red[warp][15] = acc;
+            __syncthreads();
+            if (t == 0) {
+                double v = 0.0;
+                for (int w2 = 0; w2 < MT / 32; ++w2) v += red[w2][15];
+                l1[cell] = v * g.dvk;
+            }
+        }
+        __syncthreads();  // red / tabs / bc reused by the next cell
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Stage solves (penalized / ES-BGK), one 256-thread CTA per cell, 3 CTAs per
+// SM (the cells in flight stay in L2 between the first and last pass).  A
+// thread owns groups of 4 consecutive k3 nodes of one (k1, k2) pencil.  The
+// equilibrium is evaluated WITHOUT a per-node exp: for the Gaussian
+//   exp(-1/2 d^T S d) = P(k1,k2) R(k1,k2)^k3 Z(k3),
+//   P = pref exp(-Q12/2 - L dz0),  R = exp(-L dv),  Z = exp(-S33 dz^2 / 2),
+//   L = S13 dx + S23 dy  (dz = dz0 + k3 dv on the uniform grid),
+// with P, R per pencil and Z per k3 in shared memory (N^2 + N exps per cell
+// instead of 2 N^3) and R^k3 by a branch-free square-and-multiply; cells whose
+// exponent ranges could overflow take the direct exp.  The Maxwellian is the
+// separable special case (R = 1).  Same passes as stage_kernel:
+// raw sums -> Sigma / LLT / inverse -> coupling matrix (14 monomial moments of
+// the equilibrium) -> FullPivLU solve -> blended output.
+// ---------------------------------------------------------------------------
+template <bool ESBGK, int MT, int MINB>
+__global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __restrict__ fin, double* __restrict__ out,
+                                                             int64_t ncells, VGrid g, int lg, double a,
+                                                             const double* __restrict__ eps_cell, double eps_scalar,
+                                                             double beta, double coeff, int* __restrict__ info,
+                                                             double* __restrict__ mom_out) {
+    extern __shared__ double dsm[];
+    const int n = g.n, nb = n * n * n, ngroups = nb >> 2;
+    double* Ptab = dsm;            // [n*n]
+    double* Rtab = Ptab + n * n;   // [n*n]
+    double* Ztab = Rtab + n * n;   // [n]
+    double* red = Ztab + n;        // [MT/32][16]
+    double* par = red + (MT / 32) * 16;  // [32]
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    auto block_reduce = [&](double* v, int K) {  // sum of K values over the CTA -> par[16..16+K) (K <= 14)
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        if (lane == 0)
+            for (int k = 0; k < K; ++k) red[warp * 16 + k] = v[k];
+        __syncthreads();
+        if (t < K) {
+            double s = 0.0;
+            for (int w2 = 0; w2 < MT / 32; ++w2) s += red[w2 * 16 + t];
+            par[16 + t] = s;
+        }
+        __syncthreads();
+    };
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        const double* fc = fin + cell * nb;
+        double* oc = out + cell * nb;
+        const double eps = eps_cell ? eps_cell[cell] : eps_scalar;
+        // ---- pass 1: raw sums ----
+        {
+            double s[11];
+#pragma unroll
+            for (int k = 0; k < 11; ++k) s[k] = 0.0;
+#pragma unroll 2
+            for (int q = t; q < ngroups; q += MT) {
+                const int idx = 4 * q;
+                const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
+                const double vx = g.node(k1), vy = g.node(k2);
+                const double2 wa = ldg2(fc + idx), wb = ldg2(fc + idx + 2);
+                const double w[4] = {wa.x, wa.y, wb.x, wb.y};
+                double c0 = 0, cz = 0, czz = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double z = g.node(k3 + j);
+                    c0 += w[j];
+                    cz += z * w[j];
+                    czz += z * (z * w[j]);
+                }
+                s[0] += c0;
+                s[1] += vx * c0;
+                s[2] += vy * c0;
+                s[3] += cz;
+                s[4] += (vx * vx + vy * vy) * c0 + czz;
+                s[5] += vx * (vx * c0);
+                s[6] += vx * (vy * c0);
+                s[7] += vx * cz;
+                s[8] += vy * (vy * c0);
+                s[9] += vy * cz;
+                s[10] += czz;
+            }
+            block_reduce(s, 11);
+        }
+        double s11[11];
+#pragma unroll
+        for (int k = 0; k < 11; ++k) s11[k] = par[16 + k];
+        Mom m;
+        int st = moments_from_sums(s11, g, m);
+        if (t == 0 && mom_out) {
+            double* o = mom_out + cell * 5;
+            o[0] = m.rho; o[1] = m.ux; o[2] = m.uy; o[3] = m.uz; o[4] = m.T;
+        }
+        const double A = a * (coeff * m.rho);  // a nu (nu = coeff rho) | a beta_pen (beta = coeff rho)
+        if (st != HK_OK || !(A > 0.0)) {
+            if (t == 0 && info) info[cell] = st;
+            if (st == HK_OK)
+                for (int q = t; q < ngroups; q += MT) {
+                    const int idx = 4 * q;
+                    *reinterpret_cast<double2*>(oc + idx) = ldg2(fc + idx);
+                    *reinterpret_cast<double2*>(oc + idx + 2) = ldg2(fc + idx + 2);
+                }
+            __syncthreads();
+            continue;
+        }
+        // ---- ES-BGK tensor (src/esbgk.cpp:24-33) + LLT test + inverse, thread 0 ----
+        if (t == 0) {
+            par[0] = 0.0;  // use_gauss
+            if (ESBGK) {
+                const double omb = 1.0 - beta;
+                const double u[3] = {m.ux, m.uy, m.uz};
+                const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+                double tc[9];
+                const double denom = eps + omb * A, oa = omb * A;
+                const double iso = (1.0 - beta) * m.T;
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) {
+                        const double sstar = s11[5 + map[3 * i + j]] * g.dvk;
+                        const double siso = m.rho * ((i == j ? m.T : 0.0) + u[i] * u[j]);
+                        const double theta = (eps * sstar + oa * siso) / denom / m.rho - u[i] * u[j];
+                        tc[3 * i + j] = (i == j ? iso : 0.0) + beta * theta;
+                    }
+                double l[9] = {0};
+                bool ok = true;
+                for (int k = 0; k < 3 && ok; ++k) {
+                    double x = tc[3 * k + k];
+                    for (int j = 0; j < k; ++j) x -= l[3 * k + j] * l[3 * k + j];
+                    if (!(x > 0.0)) { ok = false; break; }
+                    l[3 * k + k] = sqrt(x);
+                    for (int i = k + 1; i < 3; ++i) {
+                        double y = tc[3 * i + k];
+                        for (int j = 0; j < k; ++j) y -= l[3 * i + j] * l[3 * k + j];
+                        l[3 * i + k] = y / l[3 * k + k];
+                    }
+                }
+                if (ok) {
+                    const double* q = tc;
+                    const double c00 = q[4] * q[8] - q[5] * q[7], c01 = q[5] * q[6] - q[3] * q[8], c02 = q[3] * q[7] - q[4] * q[6];
+                    const double det = q[0] * (q[4] * q[8] - q[5] * q[7]) - q[1] * (q[3] * q[8] - q[5] * q[6]) +
+                                       q[2] * (q[3] * q[7] - q[4] * q[6]);
+                    const double id = 1.0 / (q[0] * c00 + q[1] * c01 + q[2] * c02);
+                    par[1] = c00 * id; par[2] = (q[2] * q[7] - q[1] * q[8]) * id; par[3] = (q[1] * q[5] - q[2] * q[4]) * id;
+                    par[4] = (q[0] * q[8] - q[2] * q[6]) * id; par[5] = (q[2] * q[3] - q[0] * q[5]) * id;
+                    par[6] = (q[0] * q[4] - q[1] * q[3]) * id;  // S11 S12 S13 S22 S23 S33
+                    par[7] = m.rho / sqrt(pow(2.0 * M_PI, 3) * det);
+                    par[0] = 1.0;
+                }
+            }
+            par[8] = 0.0;  // direct-exp flag (set below if a table factor could overflow)
+        }
+        __syncthreads();
+        const bool gauss = par[0] != 0.0;
+        const int fallback = (ESBGK && !gauss) ? 1 : 0;
+        const double S11 = par[1], S12 = par[2], S13 = par[3], S22 = par[4], S23 = par[5], S33 = par[6], gpref = par[7];
+        // ---- equilibrium tables ----
+        {
+            const double dz0 = g.node(0) - m.uz, dv = g.dv;
+            if (gauss) {
+                for (int k = t; k < n; k += MT) {
+                    const double dz = g.node(k) - m.uz;
+                    Ztab[k] = exp(-0.5 * S33 * dz * dz);
+                }
+                for (int pidx = t; pidx < n * n; pidx += MT) {
+                    const double dx = g.node(pidx >> lg) - m.ux, dy = g.node(pidx & (n - 1)) - m.uy;
+                    const double L = S13 * dx + S23 * dy;
+                    const double eP = -0.5 * (S11 * dx * dx + 2.0 * S12 * dx * dy + S22 * dy * dy) - L * dz0;
+                    const double eR = -L * dv;
+                    if (!(fabs(eP) < 600.0 && fabs(eR) * (n - 1) < 600.0 && fabs(eP + eR * (n - 1)) < 600.0))
+                        par[8] = 1.0;  // benign race: every writer stores 1
+                    Ptab[pidx] = gpref * exp(eP);
+                    Rtab[pidx] = exp(eR);
+                }
+            } else {  // Maxwellian: separable (src/moments.cpp:93-102)
+                const double inv2T = 0.5 / m.T, mpref = m.rho / pow(2.0 * M_PI * m.T, 1.5);
+                for (int k = t; k < n; k += MT) {
+                    const double dz = g.node(k) - m.uz;
+                    Ztab[k] = exp(-dz * dz * inv2T);
+                }
+                for (int pidx = t; pidx < n * n; pidx += MT) {
+                    const double dx = g.node(pidx >> lg) - m.ux, dy = g.node(pidx & (n - 1)) - m.uy;
+                    Ptab[pidx] = mpref * exp(-dx * dx * inv2T) * exp(-dy * dy * inv2T);
+                    Rtab[pidx] = 1.0;
+                }
+            }
+        }
+        __syncthreads();
+        const bool direct = par[8] != 0.0;
+        // equilibrium at the 4 nodes of group idx (k1, k2 fixed, k3 .. k3+3)
+        auto eq4 = [&](int k1, int k2, int k3, double (&e)[4]) {
+            if (!direct) {
+                const int pidx = (k1 << lg) | k2;
+                const double P = Ptab[pidx], R = Rtab[pidx];
+                double rk = 1.0, r = R;
+#pragma unroll
+                for (int b = 0; b < 7; ++b) {  // R^k3, k3 < 128
+                    if (b < lg) {
+                        rk = ((k3 >> b) & 1) ? rk * r : rk;
+                        r *= r;
+                    }
+                }
+                double v = P * rk;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    e[j] = v * Ztab[k3 + j];
+                    v *= R;
+                }
+            } else {
+                const double dx = g.node(k1) - m.ux, dy = g.node(k2) - m.uy;
+                const double qxy = S11 * dx * dx + 2.0 * S12 * dx * dy + S22 * dy * dy, lz = 2.0 * (S13 * dx + S23 * dy);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double dz = g.node(k3 + j) - m.uz;
+                    e[j] = gpref * exp(-0.5 * (qxy + dz * (lz + S33 * dz)));
+                }
+            }
+        };
+        // ---- pass 2: coupling matrix of the equilibrium (14 monomial moments) ----
+        const double mom3[3] = {m.rho * m.ux, m.rho * m.uy, m.rho * m.uz};
+        const double uc[3] = {mom3[0] / m.rho, mom3[1] / m.rho, mom3[2] / m.rho};
+        {
+            double M[14];
+#pragma unroll
+            for (int k = 0; k < 14; ++k) M[k] = 0.0;
+            for (int q = t; q < ngroups; q += MT) {
+                const int idx = 4 * q;
+                const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
+                const double vx = g.node(k1), vy = g.node(k2);
+                double e[4];
+                eq4(k1, k2, k3, e);
+                double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double z = g.node(k3 + j), zz = z * z;
+                    m0 += e[j];
+                    m1 += z * e[j];
+                    m2 += zz * e[j];
+                    m3 += zz * (z * e[j]);
+                    m4 += zz * (zz * e[j]);
+                }
+                const double xx = vx * vx, yy = vy * vy, r2 = xx + yy;
+                M[0] += m0;
+                M[1] += vx * m0; M[2] += vy * m0; M[3] += m1;
+                M[4] += xx * m0; M[5] += vx * (vy * m0); M[6] += vx * m1;
+                M[7] += yy * m0; M[8] += vy * m1; M[9] += m2;
+                const double aa = r2 * m0 + m2;
+                M[10] += vx * aa; M[11] += vy * aa; M[12] += r2 * m1 + m3;
+                M[13] += r2 * (r2 * m0 + 2.0 * m2) + m4;
+            }
+            block_reduce(M, 14);
+        }
+        if (t == 0) {
+            double Mm[14], Amat[25];
+            for (int k = 0; k < 14; ++k) Mm[k] = par[16 + k];
+            coupling_from_monomials(Mm, uc, g.dvk, Amat);
+            const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
+            double x[5];
+            const bool ok = solve5(Amat, rhs, x);
+            for (int k = 0; k < 5; ++k) par[9 + k] = x[k];
+            st = ok ? HK_OK : HK_DEGENERATE;
+            if (info) info[cell] = st | (fallback << 8);
+            par[14] = st;
+        }
+        __syncthreads();
+        if ((int)par[14] == HK_OK) {
+            const double x[5] = {par[9], par[10], par[11], par[12], par[13]};
+            const double wf = eps / (eps + A), wg = A / (eps + A);
+            // ---- pass 3: out = wf f + wg G (x0 + x.c + x4 |c|^2) ----
+            for (int q = t; q < ngroups; q += MT) {
+                const int idx = 4 * q;
+                const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
+                const double vx = g.node(k1), vy = g.node(k2);
+                double e[4];
+                eq4(k1, k2, k3, e);
+                const double2 fa = ldg2(fc + idx), fb = ldg2(fc + idx + 2);
+                const double fv[4] = {fa.x, fa.y, fb.x, fb.y};
+                const double cx = vx - uc[0], cy = vy - uc[1];
+                const double pxy = x[0] + x[1] * cx + x[2] * cy + x[4] * (cx * cx + cy * cy);
+                double o[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const double cz = g.node(k3 + j) - uc[2];
+                    o[j] = wf * fv[j] + wg * (e[j] * (pxy + cz * (x[3] + x[4] * cz)));
+                }
+                *reinterpret_cast<double2*>(oc + idx) = make_double2(o[0], o[1]);
+                *reinterpret_cast<double2*>(oc + idx + 2) = make_double2(o[2], o[3]);
+            }
+        }
+        __syncthreads();  // tables / par reused by the next cell
+    }
+}
+
 bool warp_path(int n) { return n >= 4 && n <= 64 && (n & (n - 1)) == 0; }
 int log2i(int n) {
     int l = 0;
@@ -962,7 +1404,18 @@ int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncel
                    double* real, double* l1, int* status) {
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "moments: 2 <= n <= 128");
-    if (warp_path(n))
+    static const int mom_var = getenv("HK_MOM_VAR") ? atoi(getenv("HK_MOM_VAR")) : 3;  // CTAs per SM x 256 threads
+    if (warp_path(n) && n >= 8 && mom_var > 0) {
+        const int64_t cap = int64_t(ctx->sm_count) * (mom_var == 1 ? 1 : mom_var);
+        const int grid = int(ncells < cap ? ncells : cap);
+        const VGrid g = make_vgrid(n, vmax);
+        if (mom_var == 1)
+            moments_cta_kernel<512, 1><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status);
+        else if (mom_var <= 3)
+            moments_cta_kernel<256, 3><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status);
+        else
+            moments_cta_kernel<256, 4><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status);
+    } else if (warp_path(n))
         moments_warp_kernel<<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), log2i(n),
                                                                                   mom, sigma, real, l1, status);
     else
@@ -985,7 +1438,18 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "stage: 2 <= n <= 128");
     const VGrid g = make_vgrid(n, vmax);
-    if (warp_path(n)) {
+    static const bool stage_warp = getenv("HK_STAGE_WARP") != nullptr;
+    if (warp_path(n) && n >= 8 && !stage_warp) {
+        static const int sv = getenv("HK_STAGE_VAR") ? atoi(getenv("HK_STAGE_VAR")) : 3;  // CTAs per SM
+        const int64_t cap = int64_t(ctx->sm_count) * sv;
+        const int grid = int(ncells < cap ? ncells : cap);
+        const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32);
+        auto kern = sv >= 3 ? (esbgk ? stage_cta_kernel<true, 256, 3> : stage_cta_kernel<false, 256, 3>)
+                            : (esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>);
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 256, smem, ctx->stream>>>(fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info,
+                                               mom_out);
+    } else if (warp_path(n)) {
         if (esbgk)
             stage_warp_kernel<true><<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(
                 fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info, mom_out);

@@ -154,6 +154,9 @@ def test_n32_nyquist_correction_equals_exact(hk):
     fixed = (st["flags"] & 4) != 0
     assert fixed.sum() >= 4  # the correction path ran
     for c in range(len(qd)):
-        assert rel_l2(qd[c], qe[c]) < 1e-12 if fixed[c] else rel_l2(qd[c], qe[c]) < TOL, c
+        gap = np.linalg.norm(qd[c] - qe[c])
+        # round-off of either path: 1e-12 of ||Q||, or 1e-14 of the loss term for near-equilibrium cells
+        floor = max(1e-12 * np.linalg.norm(qe[c]), 1e-14 * np.sqrt(st["loss_norm2"][c]))
+        assert gap <= (floor if fixed[c] else max(TOL * np.linalg.norm(qe[c]), floor)), c
     # the corrected cells' verdicts describe the corrected Q
     np.testing.assert_allclose(st["q_norm2"][fixed], (qd[fixed] ** 2).sum(1), rtol=1e-12)
