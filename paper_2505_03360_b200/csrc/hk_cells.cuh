@@ -29,6 +29,9 @@ struct TransportParams {
 };
 int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh = nullptr,
                      const double* rh = nullptr);
+// hk_transport.cu: y-marching transport (n a power of two, n^3 % 32 == 0, ny >= 3)
+int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
+                           const double* rh);
 int combine_launch(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, const double* eps, double* o,
                    const double* f, const double* y, const double* q1, const double* k1, const double* tr,
                    const double* res);

@@ -8,6 +8,7 @@
 //   prim_from_moments     src/coupling.cpp:33-35
 //   kinetic_transport_rhs src/transport.cpp:12-66, cweno3 src/euler.cpp:10-40
 #include <cmath>
+#include <cstdlib>
 
 #include "hk_cells.cuh"
 #include "hk_common.cuh"
@@ -184,6 +185,13 @@ int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, doub
         return fail(ctx, HK_CONTRACT, "transport: x_halo must be 0, -2 (separate halo buffers) or >= 2");
     const int64_t total = (int64_t)p.nx * p.ny * p.n * p.n * p.n;
     if (total <= 0) return HK_OK;
+    const int64_t nb = (int64_t)p.n * p.n * p.n;
+    static const bool old_path = getenv("HK_TRANSPORT_NODE") != nullptr;
+    if (!old_path && (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3) {
+        int lg = 0;
+        while ((1 << lg) < p.n) ++lg;
+        return transport_march_launch(ctx, p, lg, f, out, lh, rh);
+    }
     const int64_t blocks = (total + 255) / 256;
     const int64_t cap = int64_t(ctx->sm_count) * 16;
     transport_kernel<<<unsigned(blocks < cap ? blocks : cap), 256, 0, ctx->stream>>>(p, f, out, lh, rh);

@@ -37,6 +37,9 @@ struct hk_ctx_s {
     int64_t sio_flags_n = 0;
     int64_t* last_list = nullptr;
     int* last_count = nullptr;
+    // work fields of the device-resident IMEX steps (hk_steps.cu)
+    void* step_work = nullptr;
+    size_t step_bytes = 0;
     // Nyquist-correction plane scratch (hk_nyqfix.cu)
     void* fix_scratch = nullptr;
     size_t fix_bytes = 0;

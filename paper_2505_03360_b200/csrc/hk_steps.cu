@@ -68,13 +68,25 @@ struct Work {
     double *y, *q1, *k1, *tr, *res, *fa;
 };
 
+// Work fields of a step: the caller's buffer, else a context-owned one kept
+// across steps (grow-only; re-allocating ~100 GB per step costs seconds).
 int get_work(hk_ctx ctx, double* user, int64_t count, Work& w, double** owned) {
     *owned = nullptr;
     double* base = user;
     if (!base) {
-        int st = check_cuda(ctx, cudaMallocAsync(&base, sizeof(double) * count * 6, ctx->stream), "step work alloc");
-        if (st) return st;
-        *owned = base;
+        const size_t need = sizeof(double) * count * 6;
+        if (need > ctx->step_bytes) {
+            if (ctx->step_work) {
+                cudaStreamSynchronize(ctx->stream);
+                cudaFree(ctx->step_work);
+                ctx->step_work = nullptr;
+                ctx->step_bytes = 0;
+            }
+            int st = check_cuda(ctx, cudaMalloc(&ctx->step_work, need), "step work alloc");
+            if (st) return st;
+            ctx->step_bytes = need;
+        }
+        base = static_cast<double*>(ctx->step_work);
     }
     w = {base, base + count, base + 2 * count, base + 3 * count, base + 4 * count, base + 5 * count};
     return HK_OK;

@@ -1,0 +1,122 @@
+// hk_transport.cu — CWENO3 upwind kinetic transport sweep, y-marching
+// (kinetic_transport_rhs_cell / _periodic, src/transport.cpp:12-66; cweno3,
+// src/euler.cpp:10-40).  Compiled with FMA contraction (hk_field.cu, which
+// keeps the per-node kernel and the classifier bitwise to the reference, is
+// not); results agree with the reference to ~1e-15 relative.
+#include "hk_cells.cuh"
+#include "hk_common.cuh"
+
+namespace hk {
+
+namespace {
+
+// Face values of the CWENO3 reconstruction (src/euler.cpp:10-40) with the
+// three nonlinear weights normalised through ONE reciprocal:
+//   a_k = c_k / D_k^2  ->  w_k = c_k P_k / sum_m c_m P_m,  P_k = prod_{m != k} D_m^2
+// (same values as the reference's three divisions up to rounding).
+__device__ __forceinline__ void cweno3_faces(double um, double uc, double up, double eps, double& left, double& right) {
+    const double sl = uc - um, sr = up - uc;
+    const double b = 0.5 * (up - um);
+    const double c = up - 2.0 * uc + um;
+    const double dl = (eps + sl * sl), dr = (eps + sr * sr), dc = (eps + ((13.0 / 3.0) * c * c + b * b));
+    const double l2 = dl * dl, r2 = dr * dr, c2 = dc * dc;
+    const double pl = 0.25 * (c2 * r2), pc = 0.5 * (l2 * r2), pr = 0.25 * (l2 * c2);
+    const double inv = 1.0 / (pl + pc + pr);
+    const double al = pl * inv, ac = pc * inv, ar = pr * inv;
+    const double pc_a = uc - c / 12.0;
+    const double c0 = al * uc + ar * uc + ac * pc_a;
+    const double c1 = al * sl + ar * sr + ac * b;
+    const double cc = ac * c;
+    left = c0 - 0.5 * c1 + 0.25 * cc;
+    right = c0 + 0.5 * c1 + 0.25 * cc;
+}
+
+// Transport sweep, y-marching (replaces the per-node kernel above for the
+// production path).  Thread (lane, ty) owns velocity node idx = 32 chunk +
+// lane of column i = IW group + ty and marches j = 0 .. ny-1: the y stencil
+// is a 5-value sliding window in registers (one new load per step) and the
+// upwind face computed at step j is the minus face of step j+1, so a step
+// costs one y reconstruction instead of two; the x neighbours are read by the
+// neighbouring column threads of the same CTA (L1 hits).  HBM traffic ~ one
+// read and one write of the field.
+constexpr int TIW = 8;  // columns per CTA
+__global__ void __launch_bounds__(32 * TIW) transport_march_kernel(TransportParams p, int lg, const double* __restrict__ f,
+                                                                   double* __restrict__ out, const double* __restrict__ lh,
+                                                                   const double* __restrict__ rh) {
+    const int n = p.n;
+    const int64_t nb = (int64_t)n * n * n;
+    const int lane = threadIdx.x, ty = threadIdx.y;
+    const int i = blockIdx.y * TIW + ty;
+    if (i >= p.nx) return;
+    const int64_t idx = (int64_t)blockIdx.x * 32 + lane;
+    const int k1 = (int)(idx >> (2 * lg)), k2 = (int)((idx >> lg) & (n - 1));
+    const double dv = 2.0 * p.vmax / n;
+    const double vx = -p.vmax + (k1 + 0.5) * dv, vy = -p.vmax + (k2 + 0.5) * dv;
+    const double inv_dx = 1.0 / p.dx, inv_dy = 1.0 / p.dy, eps = p.eps_weno;
+    const int xh = p.x_halo > 0 ? p.x_halo : 0;
+    const int nxi = p.nx + 2 * xh;
+    const int ny = p.ny;
+    auto at = [&](int ii, int jj) -> double {  // f at interior column ii (may be -2..nx+1), row jj (periodic)
+        jj = jj < 0 ? jj + ny : (jj >= ny ? jj - ny : jj);
+        if (p.x_halo < 0) {
+            if (ii < 0) return __ldg(lh + ((int64_t)jj * 2 + (ii + 2)) * nb + idx);
+            if (ii >= p.nx) return __ldg(rh + ((int64_t)jj * 2 + (ii - p.nx)) * nb + idx);
+        } else if (p.x_halo == 0) {
+            ii = ii < 0 ? ii + p.nx : (ii >= p.nx ? ii - p.nx : ii);
+        }
+        return __ldg(f + ((int64_t)jj * nxi + ii + xh) * nb + idx);
+    };
+    // y window w[0..4] = f(i, j-2 .. j+2); upwind y face of the previous step
+    double w0 = at(i, -2), w1 = at(i, -1), w2 = at(i, 0), w3 = at(i, 1), w4 = at(i, 2);
+    const bool ypos = vy > 0.0, xpos = vx > 0.0;
+    double fy_prev;
+    {
+        double l, r;
+        if (ypos) {  // right face of cell j-1 = cweno3(w0, w1, w2).right
+            cweno3_faces(w0, w1, w2, eps, l, r);
+            fy_prev = r;
+        } else {     // left face of cell j = cweno3(w1, w2, w3).left
+            cweno3_faces(w1, w2, w3, eps, l, r);
+            fy_prev = l;
+        }
+    }
+    for (int j = 0; j < ny; ++j) {
+        if (j > 0) {
+            w0 = w1; w1 = w2; w2 = w3; w3 = w4;
+            w4 = at(i, j + 2);
+        }
+        double fy_next, l, r;
+        if (ypos) {  // right face of cell j
+            cweno3_faces(w1, w2, w3, eps, l, r);
+            fy_next = r;
+        } else {     // left face of cell j+1
+            cweno3_faces(w2, w3, w4, eps, l, r);
+            fy_next = l;
+        }
+        const double xm2 = at(i - 2, j), xm1 = at(i - 1, j), xp1 = at(i + 1, j), xp2 = at(i + 2, j);
+        double fxp, fxm;
+        if (xpos) {
+            cweno3_faces(xm1, w2, xp1, eps, l, fxp);
+            cweno3_faces(xm2, xm1, w2, eps, l, fxm);
+        } else {
+            cweno3_faces(w2, xp1, xp2, eps, fxp, r);
+            cweno3_faces(xm1, w2, xp1, eps, fxm, r);
+        }
+        const double fx = vx * (fxp - fxm), fy = vy * (fy_next - fy_prev);
+        out[((int64_t)j * p.nx + i) * nb + idx] = -fx * inv_dx - fy * inv_dy;
+        fy_prev = fy_next;
+    }
+}
+
+}  // namespace
+
+int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
+                           const double* rh) {
+    const int64_t nb = (int64_t)p.n * p.n * p.n;
+    const dim3 grid(unsigned(nb / 32), unsigned((p.nx + TIW - 1) / TIW));
+    transport_march_kernel<<<grid, dim3(32, TIW), 0, ctx->stream>>>(p, lg, f, out, lh, rh);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "transport kernel");
+}
+
+}  // namespace hk

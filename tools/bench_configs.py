@@ -84,19 +84,33 @@ def config3(iters, nx=256, ny=256):
     def es():
         res["e"] = kinetic.esbgk_stage_solve(f, 1e-3, eps, kinetic.EsbgkParams(), vg, check=False)
 
+    def tr():
+        res["t"] = kinetic.kinetic_transport_rhs_periodic(f, nx, ny, vg, 1.0 / nx, 1.0 / ny)
+
     t_m = timed(mom, iters)
     t_c = timed(cls, iters)
     t_e = timed(es, iters)
     del res["e"]
+    t_t = timed(tr, iters)
+    del res["t"]
+    torch.cuda.empty_cache()
+
+    def step():  # one ES-BGK PR(2,2,2) step of the whole field (src/esbgk.cpp:47-99), in place
+        kinetic.esbgk_imex_step(f, nx, ny, vg, 1.0 / nx, 1.0 / ny, 1e-3, eps)
+
+    t_s = timed(step, max(1, iters // 2))
     b_read = cells * n ** 3 * 8
     layers = [int((res["c"][0] == k).sum()) for k in range(3)]
     out = {"config": "config3: 256x256 cells, 32^3, classify + ES-BGK stage (a=dt=1e-3, eps=1e-2, Pr=2/3)",
-           "ms": {"moments_realizability_l1": t_m, "classify": t_c, "esbgk_stage": t_e},
+           "ms": {"moments_realizability_l1": t_m, "classify": t_c, "esbgk_stage": t_e, "transport_rhs": t_t,
+                  "esbgk_imex_step": t_s},
            "ms_per_step": t_m + t_c + t_e, "cell_steps_per_s": cells / ((t_m + t_c + t_e) * 1e-3),
            "layers_after_classify": layers,
            "roofline": {"bound": "hbm", "peak_gbs": HBM,
                         "moments_gbs": b_read / (t_m * 1e-3) / 1e9, "moments_frac": b_read / (t_m * 1e-3) / 1e9 / HBM,
                         "esbgk_gbs": 2 * b_read / (t_e * 1e-3) / 1e9, "esbgk_frac": 2 * b_read / (t_e * 1e-3) / 1e9 / HBM,
+                        "transport_gbs": 2 * b_read / (t_t * 1e-3) / 1e9,
+                        "transport_frac": 2 * b_read / (t_t * 1e-3) / 1e9 / HBM,
                         "note": "algorithmic bytes: f read once (moments), f read + stage written (ES-BGK); the "
                                 "kernels re-read f (realizability/L1 pass, Gaussian coupling pass) from L2/HBM"}}
     return out
