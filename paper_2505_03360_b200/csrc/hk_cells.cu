@@ -18,6 +18,7 @@
 //   penalized_residual     src/boltzmann.cpp:9-27   (after the collision kernel)
 //   penalized_stage_solve  src/boltzmann.cpp:29-45
 //   esbgk_stage_solve      src/esbgk.cpp:9-45
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 
@@ -1114,7 +1115,8 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                                                              int64_t ncells, VGrid g, int lg, double a,
                                                              const double* __restrict__ eps_cell, double eps_scalar,
                                                              double beta, double coeff, int* __restrict__ info,
-                                                             double* __restrict__ mom_out) {
+                                                             double* __restrict__ mom_out, double* __restrict__ k1_out,
+                                                             double k1_scale) {
     extern __shared__ double dsm[];
     const int n = g.n, nb = n * n * n, ngroups = nb >> 2;
     double* Ptab = dsm;            // [n*n]
@@ -1192,6 +1194,10 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                     const int idx = 4 * q;
                     *reinterpret_cast<double2*>(oc + idx) = ldg2(fc + idx);
                     *reinterpret_cast<double2*>(oc + idx + 2) = ldg2(fc + idx + 2);
+                    if (k1_out) {  // identity stage: k1 = 0
+                        *reinterpret_cast<double2*>(k1_out + cell * nb + idx) = make_double2(0.0, 0.0);
+                        *reinterpret_cast<double2*>(k1_out + cell * nb + idx + 2) = make_double2(0.0, 0.0);
+                    }
                 }
             __syncthreads();
             continue;
@@ -1376,10 +1382,21 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 }
                 *reinterpret_cast<double2*>(oc + idx) = make_double2(o[0], o[1]);
                 *reinterpret_cast<double2*>(oc + idx + 2) = make_double2(o[2], o[3]);
+                if (k1_out) {  // fused K1 of the IMEX step: k1 = (Y - f) / a11
+                    double* kc = k1_out + cell * nb + idx;
+                    *reinterpret_cast<double2*>(kc) = make_double2((o[0] - fv[0]) * k1_scale, (o[1] - fv[1]) * k1_scale);
+                    *reinterpret_cast<double2*>(kc + 2) = make_double2((o[2] - fv[2]) * k1_scale, (o[3] - fv[3]) * k1_scale);
+                }
             }
         }
         __syncthreads();  // tables / par reused by the next cell
     }
+}
+
+__global__ void k1_kernel(int64_t count, double* __restrict__ k1, const double* __restrict__ y,
+                          const double* __restrict__ f, double scale) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        k1[i] = (y[i] - f[i]) * scale;
 }
 
 bool warp_path(int n) { return n >= 4 && n <= 64 && (n & (n - 1)) == 0; }
@@ -1434,7 +1451,8 @@ int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t
 }
 
 int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,
-                 const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out) {
+                 const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out,
+                 double* k1_out, double k1_scale) {
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "stage: 2 <= n <= 128");
     const VGrid g = make_vgrid(n, vmax);
@@ -1448,7 +1466,9 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
                             : (esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>);
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, 256, smem, ctx->stream>>>(fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info,
-                                               mom_out);
+                                               mom_out, k1_out, k1_scale);
+        ctx->launches++;
+        return check_cuda(ctx, cudaGetLastError(), "stage kernel");
     } else if (warp_path(n)) {
         if (esbgk)
             stage_warp_kernel<true><<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(
@@ -1463,7 +1483,15 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
         stage_kernel<false><<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(fin, out, ncells, g, a, eps_cell, eps_scalar,
                                                                            beta, coeff, info, mom_out);
     ctx->launches++;
-    return check_cuda(ctx, cudaGetLastError(), "stage kernel");
+    int st = check_cuda(ctx, cudaGetLastError(), "stage kernel");
+    if (!st && k1_out) {  // these kernels do not fuse K1
+        const int64_t count = ncells * (int64_t)n * n * n;
+        k1_kernel<<<unsigned(std::min<int64_t>((count + 255) / 256, int64_t(ctx->sm_count) * 16)), 256, 0, ctx->stream>>>(
+            count, k1_out, out, fin, k1_scale);
+        ctx->launches++;
+        st = check_cuda(ctx, cudaGetLastError(), "k1 kernel");
+    }
+    return st;
 }
 
 int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,

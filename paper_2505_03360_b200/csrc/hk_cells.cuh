@@ -8,7 +8,8 @@ int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncel
                    double* real, double* l1, int* status);
 int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status);
 int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,
-                 const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out);
+                 const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out,
+                 double* k1_out = nullptr, double k1_scale = 0.0);
 int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,
                            int* status);
 
@@ -27,11 +28,28 @@ struct TransportParams {
     int x_halo;      // 0: periodic in x; >= 2: input carries x_halo ghost columns per side
     double dx, dy, eps_weno;
 };
+
+// Final PR(2,2,2) combination fused into the second transport of a step
+// (src/boltzmann.cpp:99-108, src/esbgk.cpp:90-97): with T = T(Y2) computed in
+// place,  q2 = T + res/eps,  f_acc = f + dt a_ex10 q1 + a_im10 k1,
+// k2 = (Y2 - f_acc)/a_im11,  f += dt (w0 q1 + w1 q2) + w0 k1 + w1 k2.
+struct FinalCombine {
+    double* f;               // in/out
+    const double* q1;
+    const double* k1;
+    const double* res;       // nullable (ES-BGK)
+    const double* eps;       // per cell
+    double dt, a_ex10, a_im10, a_im11, w_ex0, w_ex1, w_im0, w_im1;
+};
 int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh = nullptr,
                      const double* rh = nullptr);
 // hk_transport.cu: y-marching transport (n a power of two, n^3 % 32 == 0, ny >= 3)
 int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
-                           const double* rh);
+                           const double* rh, const FinalCombine* fin = nullptr);
+// PR(2,2,2) second transport + final combination (x periodic); false if the
+// marching kernel does not apply (caller runs transport + combine instead).
+bool transport_final_supported(const TransportParams& p);
+int transport_final_launch(hk_ctx ctx, const TransportParams& p, const double* y2, const FinalCombine& fc);
 int combine_launch(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, const double* eps, double* o,
                    const double* f, const double* y, const double* q1, const double* k1, const double* tr,
                    const double* res);

@@ -172,25 +172,34 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
     int st = get_work(ctx, work_dev, count, w, &owned);
     if (st) return st;
     TransportParams tp{n, vmax, nx, ny, 0, dx, dy, eps_weno};
-    auto stage = [&](const double* fin, double a, double* out) {
-        return boltz ? stage_launch(ctx, false, n, vmax, fin, out, cells, a, eps_dev, 0.0, 0.0, coeff, nullptr, nullptr)
-                     : stage_launch(ctx, true, n, vmax, fin, out, cells, a, eps_dev, 0.0, beta, coeff, nullptr, nullptr);
+    auto stage = [&](const double* fin, double a, double* out, double* k1) {
+        return boltz ? stage_launch(ctx, false, n, vmax, fin, out, cells, a, eps_dev, 0.0, 0.0, coeff, nullptr, nullptr,
+                                    k1, 1.0 / t.a_im00)
+                     : stage_launch(ctx, true, n, vmax, fin, out, cells, a, eps_dev, 0.0, beta, coeff, nullptr, nullptr,
+                                    k1, 1.0 / t.a_im00);
     };
     auto residual = [&](const double* y, double* out) {
         int s = hk_collision_batch(ctx, k, y, out, cells, flags & ~HK_COLL_STRICT, nullptr);
         return s ? s : residual_finish_launch(ctx, n, vmax, y, out, cells, coeff, nullptr);
     };
     double* R = boltz ? w.res : nullptr;
-    if (!st) st = stage(f, t.a_im00 * dt, w.y);                                             // Y1
-    if (!st) st = combine(ctx, K1, count, nb, t, dt, eps_dev, w.k1, f, w.y, 0, 0, 0, 0);     // k1
-    if (!st) st = transport_launch(ctx, tp, w.y, w.tr);                                      // T(Y1)
-    if (!st && boltz) st = residual(w.y, w.res);                                             // res(Y1)
-    if (!st) st = combine(ctx, Q1, count, nb, t, dt, eps_dev, w.q1, 0, 0, 0, 0, w.tr, R);    // q1
+    // Stage 1 (k1 fused into the stage kernel), explicit q1; ES-BGK has no
+    // residual, so T(Y1) is q1 itself.
+    if (!st) st = stage(f, t.a_im00 * dt, w.y, w.k1);                                      // Y1, k1
+    if (!st) st = transport_launch(ctx, tp, w.y, boltz ? w.tr : w.q1);                     // T(Y1)
+    if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y1)
+    if (!st && boltz) st = combine(ctx, Q1, count, nb, t, dt, eps_dev, w.q1, 0, 0, 0, 0, w.tr, R);  // q1
     if (!st) st = combine(ctx, FACC, count, nb, t, dt, eps_dev, w.fa, f, 0, w.q1, w.k1, 0, 0);  // f_acc
-    if (!st) st = stage(w.fa, t.a_im11 * dt, w.y);                                           // Y2
-    if (!st) st = transport_launch(ctx, tp, w.y, w.tr);                                      // T(Y2)
-    if (!st && boltz) st = residual(w.y, w.res);                                             // res(Y2)
-    if (!st) st = combine(ctx, FINAL, count, nb, t, dt, eps_dev, f, 0, w.y, w.q1, w.k1, w.tr, R);
+    if (!st) st = stage(w.fa, t.a_im11 * dt, w.y, nullptr);                                // Y2
+    if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y2)
+    if (!st && transport_final_supported(tp)) {  // T(Y2) + final combination, one kernel
+        const FinalCombine fc{f, w.q1, w.k1, R, eps_dev, dt, t.a_ex10, t.a_im10, t.a_im11, t.w_ex0, t.w_ex1, t.w_im0,
+                              t.w_im1};
+        st = transport_final_launch(ctx, tp, w.y, fc);
+    } else {
+        if (!st) st = transport_launch(ctx, tp, w.y, w.tr);                                // T(Y2)
+        if (!st) st = combine(ctx, FINAL, count, nb, t, dt, eps_dev, f, 0, w.y, w.q1, w.k1, w.tr, R);
+    }
     if (owned) cudaFreeAsync(owned, ctx->stream);
     return st;
 }

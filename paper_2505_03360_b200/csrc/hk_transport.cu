@@ -3,6 +3,8 @@
 // src/euler.cpp:10-40).  Compiled with FMA contraction (hk_field.cu, which
 // keeps the per-node kernel and the classifier bitwise to the reference, is
 // not); results agree with the reference to ~1e-15 relative.
+#include <cstdlib>
+
 #include "hk_cells.cuh"
 #include "hk_common.cuh"
 
@@ -40,9 +42,10 @@ __device__ __forceinline__ void cweno3_faces(double um, double uc, double up, do
 // neighbouring column threads of the same CTA (L1 hits).  HBM traffic ~ one
 // read and one write of the field.
 constexpr int TIW = 8;  // columns per CTA
+template <bool FINAL>
 __global__ void __launch_bounds__(32 * TIW) transport_march_kernel(TransportParams p, int lg, const double* __restrict__ f,
                                                                    double* __restrict__ out, const double* __restrict__ lh,
-                                                                   const double* __restrict__ rh) {
+                                                                   const double* __restrict__ rh, FinalCombine fc) {
     const int n = p.n;
     const int64_t nb = (int64_t)n * n * n;
     const int lane = threadIdx.x, ty = threadIdx.y;
@@ -80,11 +83,26 @@ __global__ void __launch_bounds__(32 * TIW) transport_march_kernel(TransportPara
             fy_prev = l;
         }
     }
+    // Per-row loads are issued one row ahead (software pipelining): the
+    // marching loop is otherwise latency-bound on them.
+    auto row_loads = [&](int jj, double& nw4, double (&nx4)[4], double (&nf)[3]) {
+        nw4 = at(i, jj + 2);
+        nx4[0] = at(i - 2, jj); nx4[1] = at(i - 1, jj); nx4[2] = at(i + 1, jj); nx4[3] = at(i + 2, jj);
+        if constexpr (FINAL) {
+            const int64_t o = ((int64_t)jj * p.nx + i) * nb + idx;
+            nf[0] = fc.f[o]; nf[1] = __ldg(fc.q1 + o); nf[2] = __ldg(fc.k1 + o);
+        }
+    };
+    double cx4[4], cf[3] = {0, 0, 0}, cw4;
+    row_loads(0, cw4, cx4, cf);
     for (int j = 0; j < ny; ++j) {
         if (j > 0) {
             w0 = w1; w1 = w2; w2 = w3; w3 = w4;
-            w4 = at(i, j + 2);
+            w4 = cw4;
         }
+        const double xm2 = cx4[0], xm1 = cx4[1], xp1 = cx4[2], xp2 = cx4[3];
+        const double fv = cf[0], q1 = cf[1], k1 = cf[2];
+        if (j + 1 < ny) row_loads(j + 1, cw4, cx4, cf);
         double fy_next, l, r;
         if (ypos) {  // right face of cell j
             cweno3_faces(w1, w2, w3, eps, l, r);
@@ -93,7 +111,6 @@ __global__ void __launch_bounds__(32 * TIW) transport_march_kernel(TransportPara
             cweno3_faces(w2, w3, w4, eps, l, r);
             fy_next = l;
         }
-        const double xm2 = at(i - 2, j), xm1 = at(i - 1, j), xp1 = at(i + 1, j), xp2 = at(i + 2, j);
         double fxp, fxm;
         if (xpos) {
             cweno3_faces(xm1, w2, xp1, eps, l, fxp);
@@ -103,7 +120,18 @@ __global__ void __launch_bounds__(32 * TIW) transport_march_kernel(TransportPara
             cweno3_faces(xm1, w2, xp1, eps, fxm, r);
         }
         const double fx = vx * (fxp - fxm), fy = vy * (fy_next - fy_prev);
-        out[((int64_t)j * p.nx + i) * nb + idx] = -fx * inv_dx - fy * inv_dy;
+        const double tr = -fx * inv_dx - fy * inv_dy;
+        const int64_t o = ((int64_t)j * p.nx + i) * nb + idx;
+        if constexpr (!FINAL) {
+            out[o] = tr;
+            (void)fv; (void)q1; (void)k1;
+        } else {  // f += dt (w0 q1 + w1 q2) + w0 k1 + w1 k2 at this node (Y2 = w2)
+            const int64_t cell = (int64_t)j * p.nx + i;
+            const double q2 = fc.res ? tr + fc.res[o] / fc.eps[cell] : tr;
+            const double facc = fv + fc.dt * fc.a_ex10 * q1 + fc.a_im10 * k1;
+            const double k2 = (w2 - facc) * (1.0 / fc.a_im11);
+            fc.f[o] = fv + (fc.dt * (fc.w_ex0 * q1 + fc.w_ex1 * q2) + fc.w_im0 * k1 + fc.w_im1 * k2);
+        }
         fy_prev = fy_next;
     }
 }
@@ -111,12 +139,26 @@ __global__ void __launch_bounds__(32 * TIW) transport_march_kernel(TransportPara
 }  // namespace
 
 int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
-                           const double* rh) {
+                           const double* rh, const FinalCombine* fin) {
     const int64_t nb = (int64_t)p.n * p.n * p.n;
     const dim3 grid(unsigned(nb / 32), unsigned((p.nx + TIW - 1) / TIW));
-    transport_march_kernel<<<grid, dim3(32, TIW), 0, ctx->stream>>>(p, lg, f, out, lh, rh);
+    if (fin)
+        transport_march_kernel<true><<<grid, dim3(32, TIW), 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+    else
+        transport_march_kernel<false><<<grid, dim3(32, TIW), 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "transport kernel");
+}
+
+bool transport_final_supported(const TransportParams& p) {
+    const int64_t nb = (int64_t)p.n * p.n * p.n;
+    return (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3 && p.x_halo == 0 && !getenv("HK_TRANSPORT_NODE");
+}
+
+int transport_final_launch(hk_ctx ctx, const TransportParams& p, const double* y2, const FinalCombine& fc) {
+    int lg = 0;
+    while ((1 << lg) < p.n) ++lg;
+    return transport_march_launch(ctx, p, lg, y2, nullptr, nullptr, nullptr, &fc);
 }
 
 }  // namespace hk
