@@ -6,7 +6,7 @@ cell in the Boltzmann regime, hard spheres, N = 32^3 velocity grid on
 [-8,8]^3, M = 64 directions (a1 x a2 = 8 x 8), r_phys = 2L/(3+sqrt 2), fp64.
 One STEP = one evaluation of Q(f) for every cell of the batch (4096 cell
 updates) through the library's public entry point hk_collision_batch
-(default path: Hermitian-packed fast path + Nyquist guard + exact reroute).
+(default path: Hermitian-packed fast path + Nyquist guard + exact Nyquist correction of the listed cells).
 The 1 GiB input slab exceeds the 126 MB L2, so no flush is needed.
 
 Multi-GPU (torchrun): weak scaling, each rank owns its own 64x64-cell batch
@@ -303,14 +303,15 @@ def run_gpu(args):
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "cells_per_gpu": ncells, "n": N, "a1": A1, "a2": A2,
-                           "path": "fast (Hermitian-packed) + Nyquist guard + exact reroute",
+                           "path": "fast (Hermitian-packed) + Nyquist guard + exact Nyquist correction of listed cells",
                            "cells_rerouted_last_step": rerouted,
                            "l2": "inputs (1 GiB per GPU) larger than the 126 MB L2; no flush"},
                 "clocks": clk.summary(),
                 "gpu_launches": launches,
                 "e2e": {"value": e2e_value, "unit": UNIT,
                         "h2d_bytes_per_step": int(fh.numel() * 8),
-                        "d2h_bytes_per_step": int(qh.numel() * 8 + ncells * 40),
+                        # Q, plus the guard-listed cells fetched again after their correction
+                        "d2h_bytes_per_step": int(qh.numel() * 8 + rerouted * N ** 3 * 8 + 4 + 8 * rerouted),
                         "steps": args.e2e_steps, "api": "hk_collision_batch_host (pinned)"},
                 "roofline": roof,
                 "cpu_baseline": cb}
