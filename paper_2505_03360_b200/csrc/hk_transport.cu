@@ -42,8 +42,11 @@ __device__ __forceinline__ void cweno3_faces(double um, double uc, double up, do
 // neighbouring column threads of the same CTA (L1 hits).  HBM traffic ~ one
 // read and one write of the field.
 constexpr int TIW = 8;  // columns per CTA
+#ifndef HK_TR_MINB
+#define HK_TR_MINB 2
+#endif
 template <bool FINAL>
-__global__ void __launch_bounds__(32 * TIW) transport_march_kernel(TransportParams p, int lg, const double* __restrict__ f,
+__global__ void __launch_bounds__(32 * TIW, HK_TR_MINB) transport_march_kernel(TransportParams p, int lg, const double* __restrict__ f,
                                                                    double* __restrict__ out, const double* __restrict__ lh,
                                                                    const double* __restrict__ rh, FinalCombine fc) {
     const int n = p.n;
