@@ -230,9 +230,7 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                 pl = jj & 1;
             }
         };
-        auto issue = [&](unsigned gs, int pl, int buf) {  // my 16 rows of (slot gs, plane pl)
-            if (lane == 0) spin_geq(ready + gs % D, ARR * (gs / D + 1));
-            __syncwarp();
+        auto pull = [&](unsigned gs, int pl, int buf) {  // my 16 rows of (slot gs, plane pl)
             const double2* src = X + (int64_t)(gs % D) * SLOT + (int64_t)r * BLK + (int64_t)pl * N * N + 16 * rw * N;
             const uint32_t d0 = smem_u32(Rvb + buf * PLANE + 16 * rw * ROW);
 #pragma unroll 4
@@ -241,6 +239,19 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                 cp_async16(d0 + (k * ROW + 32 + lane) * 16, src + k * N + 32 + lane);
             }
             cp_async_commit();
+        };
+        auto issue = [&](unsigned gs, int pl, int buf) {
+            if (lane == 0) spin_geq(ready + gs % D, ARR * (gs / D + 1));
+            __syncwarp();
+            pull(gs, pl, buf);
+        };
+        auto try_issue = [&](unsigned gs, int pl, int buf) -> bool {  // pull only if already published
+            unsigned v = 0;
+            if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ready + gs % D) : "memory");
+            v = __shfl_sync(0xffffffffu, v, 0);
+            if ((int)(v - ARR * (gs / D + 1)) < 0) return false;
+            pull(gs, pl, buf);
+            return true;
         };
         auto complete = [&](unsigned gs, int pl) {
             cp_async_wait_all();
@@ -274,7 +285,8 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                 // Deferred successor: after the last prologue plane (the first field
                 // needs F in TMEM) and, EXACT, after a gb unit (the other buffer holds ga).
                 const bool defer = (fi == 0 && pl == P - 1) || (EXACT && fi >= 1 && fi <= 2 * a.md && ((fi - 1) & 1));
-                if (has_next && !defer) issue(gs2, pl2, buf ^ 1);
+                // successor pull: now if published, else retried between the passes
+                bool pending = has_next && !defer && !try_issue(gs2, pl2, buf ^ 1);
                 if (fi == 0) {
                     // ---- prologue: forward over k3 of rows (k1 = rP + pl, k2 = pp) -> F (TMEM) ----
                     const double2* row = Rv + pp * ROW;
@@ -317,6 +329,7 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                     tmem_wait_st();
                     tmem_fence_before();
                     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pl)) : "memory");
+                    if (pending) issue(gs2, pl2, buf ^ 1);
                 } else {
                     // ---- field: inverse over i2 (rows i1 = pp), then i1 (columns j2 = pp) ----
                     {
@@ -332,12 +345,14 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
 #pragma unroll
                         for (int m = 0; m < M; ++m) row[2 * m + h] = v[m];
                     }
+                    if (pending) pending = !try_issue(gs2, pl2, buf ^ 1);
                     named_bar(2, 128);  // columns need every row
                     double2 y[M];       // y[j] = node j1 = hQ + j, y[Q + j] = node M + hQ + j
                     double2* col = Rv + pp;
 #pragma unroll
                     for (int m = 0; m < M; ++m) y[m] = col[(2 * m + h) * ROW];
                     fftxh_dit<M, true>(y, h);
+                    if (pending) issue(gs2, pl2, buf ^ 1);
                     const bool is_loss = EXACT ? (fi == 1 + 2 * a.md) : (fi == 1 + a.md);
                     const int j3 = r * P + pl;
                     if (!is_loss) {
