@@ -57,7 +57,7 @@ typedef struct {
 
 #define HK_CELL_EXACT 1u            /* evaluated on the exact (full complex) path */
 #define HK_CELL_RESIDUE 2u          /* max|Im| > 1e-10 max|Re| (reference would throw, src/spectral.cpp:150) */
-#define HK_CELL_GUARD_REROUTED 4u   /* fast path rejected by the Nyquist guard, recomputed exactly */
+#define HK_CELL_GUARD_REROUTED 4u   /* listed by the Nyquist guard; its exact Nyquist term was added (hk_nyqfix) */
 
 /* hk_collision_batch flags */
 #define HK_COLL_EXACT 1u  /* every cell on the exact path (complex ga, gb per direction) */
@@ -78,7 +78,7 @@ int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len);
 int64_t hk_launch_count(hk_ctx ctx);
 /* CUDA-event timing of the library's kernels on the context stream (for the
  * roofline in bench.py).  Enabling clears previous records.  tag 0 = main
- * collision kernel, 1 = Nyquist guard, 2 = exact reroute. */
+ * collision kernel, 1 = Nyquist guard, 2 = Nyquist correction of the listed cells. */
 int hk_ctx_set_timing(hk_ctx ctx, int on);
 int hk_ctx_timing_report(hk_ctx ctx, int tag, double* total_ms, int64_t* launches);
 
@@ -89,7 +89,7 @@ int hk_ctx_timing_report(hk_ctx ctx, int tag, double* total_ms, int64_t* launche
  * radial/planar transforms (they agree with the GK15 quadrature of
  * src/quadrature.cpp to ~1e-14 relative).  Same validation and status:
  * HK_CONFIG (a1,a2 < 1, n < 2, vmax <= 0, r_phys <= 0), HK_ALIASING
- * (r_phys > 2 vmax/(3+sqrt 2)), HK_UNSUPPORTED (n not in {16, 32}). */
+ * (r_phys > 2 vmax/(3+sqrt 2)), HK_UNSUPPORTED (n not in {16, 32, 64}). */
 int hk_kernel_create(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys,
                      hk_kernel* out);
 /* Same, but takes the reference's own tables verbatim (SpectralKernel::alpha,
@@ -107,8 +107,11 @@ int hk_kernel_info(hk_kernel k, double* out6);
  * src/spectral.cpp:114-154), batched over ncells cells.  q_dev receives
  * Re Q per cell.  st_dev (nullable) receives one hk_cell_status per cell.
  * Default: fast path (Hermitian-packed, one complex 3-D transform per
- * direction) with a rigorous per-cell Nyquist guard that reroutes any cell
- * whose dropped term could exceed 5e-11 relative L2 to the exact path.
+ * direction) with a rigorous per-cell Nyquist guard: any cell whose dropped
+ * term could exceed 5e-11 of max(||Q||_2, 2e-5 ||jac f L||_2) gets that term
+ * computed exactly and added (Re Q then equals the exact path's).
+ * HK_COLL_EXACT: the reference's arithmetic (two complex transforms per
+ * direction) for every cell; HK_COLL_NOGUARD: fast path only.
  * HK_COLL_STRICT returns HK_NUMERICAL_CONSISTENCY (hk_last_error gives the
  * lowest failing cell) when any cell's residue exceeds 1e-10, after writing
  * q_dev for every cell — the reference's throw-after-write behaviour. */
