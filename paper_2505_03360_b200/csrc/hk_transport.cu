@@ -139,11 +139,160 @@ __global__ void __launch_bounds__(32 * TIW, HK_TR_MINB) transport_march_kernel(T
     }
 }
 
+// Lane-per-column variant: lane l of a warp owns column i = 28 b - 2 + l for
+// NPT consecutive velocity nodes and marches down the rows like the kernel
+// above.  The x neighbours' centre values come from the neighbouring lanes
+// (shuffles, no loads), and the x minus face of lane l is lane l-1's plus
+// face, so a row costs ONE x and ONE y reconstruction per node (2 instead of
+// 3); lanes 0, 1, 30, 31 are halo columns (no output).
+constexpr int TL_OUT = 28;
+template <bool FINAL, int NPT>
+__global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p, int lg, const double* __restrict__ f,
+                                                              double* __restrict__ out, const double* __restrict__ lh,
+                                                              const double* __restrict__ rh, FinalCombine fc) {
+    static_assert(NPT == 2, "double2 node pairs");
+    const int n = p.n;
+    const int64_t nb = (int64_t)n * n * n;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t grp = (int64_t)blockIdx.y * (blockDim.x >> 5) + w;
+    if (grp * NPT >= nb) return;  // warp-uniform
+    const int64_t idx = grp * NPT;
+    const int k1 = (int)(idx >> (2 * lg)), k2 = (int)((idx >> lg) & (n - 1)), k3 = (int)(idx & (n - 1));
+    const int i = blockIdx.x * TL_OUT - 2 + lane;
+    const bool outlane = lane >= 2 && lane < 2 + TL_OUT && i < p.nx;
+    const double dv = 2.0 * p.vmax / n;
+    const double vx = -p.vmax + (k1 + 0.5) * dv, vy = -p.vmax + (k2 + 0.5) * dv;
+    const double inv_dx = 1.0 / p.dx, inv_dy = 1.0 / p.dy, eps = p.eps_weno;
+    const int xh = p.x_halo > 0 ? p.x_halo : 0;
+    const int nxi = p.nx + 2 * xh;
+    const int ny = p.ny;
+    // this lane's column source: interior (periodic wrap), halo buffer, or ghost column
+    const double* colbase;
+    int64_t rowstride;
+    {
+        int ii = i;
+        if (p.x_halo < 0) {
+            ii = ii < -2 ? -2 : (ii > p.nx + 1 ? p.nx + 1 : ii);  // lanes past the halo are never used
+            if (ii < 0) { colbase = lh + (int64_t)(ii + 2) * nb; rowstride = 2 * nb; }
+            else if (ii >= p.nx) { colbase = rh + (int64_t)(ii - p.nx) * nb; rowstride = 2 * nb; }
+            else { colbase = f + (int64_t)ii * nb; rowstride = (int64_t)nxi * nb; }
+        } else if (p.x_halo == 0) {
+            ii = ((ii % p.nx) + p.nx) % p.nx;
+            colbase = f + (int64_t)ii * nb;
+            rowstride = (int64_t)nxi * nb;
+        } else {
+            ii = ii < -xh ? -xh : (ii > p.nx + xh - 1 ? p.nx + xh - 1 : ii);
+            colbase = f + (int64_t)(ii + xh) * nb;
+            rowstride = (int64_t)nxi * nb;
+        }
+        colbase += idx;
+    }
+    auto ld = [&](int jj) -> double2 {
+        jj = jj < 0 ? jj + ny : (jj >= ny ? jj - ny : jj);
+        return __ldg(reinterpret_cast<const double2*>(colbase + (int64_t)jj * rowstride));
+    };
+    auto sh_up = [&](double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); };
+    auto sh_dn = [&](double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); };
+    double2 w0 = ld(-2), w1 = ld(-1), w2 = ld(0), w3 = ld(1), w4 = ld(2);
+    const bool ypos = vy > 0.0, xpos = vx > 0.0;
+    auto yface = [&](double a, double b, double c, double d, double e) -> double {  // new upwind y face
+        double l, r;
+        if (ypos) { cweno3_faces(b, c, d, eps, l, r); return r; }
+        cweno3_faces(c, d, e, eps, l, r);
+        return l;
+    };
+    double fyp[2];
+    {
+        double l, r;
+        if (ypos) {
+            cweno3_faces(w0.x, w1.x, w2.x, eps, l, r); fyp[0] = r;
+            cweno3_faces(w0.y, w1.y, w2.y, eps, l, r); fyp[1] = r;
+        } else {
+            cweno3_faces(w1.x, w2.x, w3.x, eps, l, r); fyp[0] = l;
+            cweno3_faces(w1.y, w2.y, w3.y, eps, l, r); fyp[1] = l;
+        }
+    }
+    double2 nw4 = make_double2(0, 0), nf0 = nw4, nf1 = nw4, nf2 = nw4;
+    auto fin_loads = [&](int jj, double2& a, double2& b, double2& c) {
+        const int64_t o = ((int64_t)jj * p.nx + i) * nb + idx;
+        a = *reinterpret_cast<const double2*>(fc.f + o);
+        b = __ldg(reinterpret_cast<const double2*>(fc.q1 + o));
+        c = __ldg(reinterpret_cast<const double2*>(fc.k1 + o));
+    };
+    if (FINAL && outlane) fin_loads(0, nf0, nf1, nf2);
+    for (int j = 0; j < ny; ++j) {
+        if (j > 0) {
+            w0 = w1; w1 = w2; w2 = w3; w3 = w4;
+            w4 = nw4;
+        }
+        const double2 cf = nf0, cq = nf1, ck = nf2;
+        if (j + 1 < ny) {
+            nw4 = ld(j + 3);  // row j+3 = w4 of row j+1
+            if (FINAL && outlane) fin_loads(j + 1, nf0, nf1, nf2);
+        }
+        const double c[2] = {w2.x, w2.y};
+        double fy[2], fx[2];
+        fy[0] = yface(w0.x, w1.x, w2.x, w3.x, w4.x);
+        fy[1] = yface(w0.y, w1.y, w2.y, w3.y, w4.y);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const double cp1 = sh_dn(c[q], 1);
+            double plus, l, r;
+            if (xpos) {  // right face of cell i
+                const double cm1 = sh_up(c[q], 1);
+                cweno3_faces(cm1, c[q], cp1, eps, l, r);
+                plus = r;
+            } else {     // left face of cell i+1
+                const double cp2 = sh_dn(c[q], 2);
+                cweno3_faces(c[q], cp1, cp2, eps, l, r);
+                plus = l;
+            }
+            const double minus = sh_up(plus, 1);
+            fx[q] = vx * (plus - minus);
+        }
+        if (outlane) {
+            const int64_t o = ((int64_t)j * p.nx + i) * nb + idx;
+            double tr[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) tr[q] = -fx[q] * inv_dx - vy * (fy[q] - fyp[q]) * inv_dy;
+            if constexpr (!FINAL) {
+                *reinterpret_cast<double2*>(out + o) = make_double2(tr[0], tr[1]);
+            } else {
+                const int64_t cell = (int64_t)j * p.nx + i;
+                const double ie = fc.res ? 1.0 / fc.eps[cell] : 0.0;
+                const double fv[2] = {cf.x, cf.y}, q1[2] = {cq.x, cq.y}, k1v[2] = {ck.x, ck.y}, y2[2] = {w2.x, w2.y};
+                double o2[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double q2 = fc.res ? tr[q] + fc.res[o + q] * ie : tr[q];
+                    const double facc = fv[q] + fc.dt * fc.a_ex10 * q1[q] + fc.a_im10 * k1v[q];
+                    const double k2 = (y2[q] - facc) * (1.0 / fc.a_im11);
+                    o2[q] = fv[q] + (fc.dt * (fc.w_ex0 * q1[q] + fc.w_ex1 * q2) + fc.w_im0 * k1v[q] + fc.w_im1 * k2);
+                }
+                *reinterpret_cast<double2*>(fc.f + o) = make_double2(o2[0], o2[1]);
+            }
+        }
+        fyp[0] = fy[0];
+        fyp[1] = fy[1];
+    }
+    (void)k3;
+}
+
 }  // namespace
 
 int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
                            const double* rh, const FinalCombine* fin) {
     const int64_t nb = (int64_t)p.n * p.n * p.n;
+    static const bool lanes = !getenv("HK_TRANSPORT_MARCH");
+    if (lanes) {  // lane-per-column kernel (default)
+        const dim3 grid(unsigned((p.nx + TL_OUT - 1) / TL_OUT), unsigned((nb / 2 + 3) / 4));
+        if (fin)
+            transport_lanes_kernel<true, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+        else
+            transport_lanes_kernel<false, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+        ctx->launches++;
+        return check_cuda(ctx, cudaGetLastError(), "transport kernel");
+    }
     const dim3 grid(unsigned(nb / 32), unsigned((p.nx + TIW - 1) / TIW));
     if (fin)
         transport_march_kernel<true><<<grid, dim3(32, TIW), 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
