@@ -164,36 +164,46 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                         mbar_wait_parity(smem_u32(fbar + pl), ncell & 1);  // consumers put F(plane) in TMEM
                         tmem_fence_after();
                     }
-                    cp_async_wait_all();
-                    __syncwarp();
+                    // F of this half-pencil (32 complex = 128 TMEM columns): four x32
+                    // loads and ONE wait, overlapping the weight reads
                     double2 x[M];
+                    {
+                        uint32_t r0[32], r1[32], r2[32], r3[32];
+                        tmem_ld32_nowait(tmF + 128 * pl, r0);
+                        tmem_ld32_nowait(tmF + 128 * pl + 32, r1);
+                        tmem_ld32_nowait(tmF + 128 * pl + 64, r2);
+                        tmem_ld32_nowait(tmF + 128 * pl + 96, r3);
+                        cp_async_wait_all();
+                        __syncwarp();
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
+                            x[8 + m] = make_double2(tmem_pair(r1[4 * m], r1[4 * m + 1]), tmem_pair(r1[4 * m + 2], r1[4 * m + 3]));
+                            x[16 + m] = make_double2(tmem_pair(r2[4 * m], r2[4 * m + 1]), tmem_pair(r2[4 * m + 2], r2[4 * m + 3]));
+                            x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
+                        }
+                    }
                     if constexpr (!EXACT) {
                         const double2* wb = Pw;
 #pragma unroll
-                        for (int m = 0; m < M; ++m) x[m] = wb[m * 128 + u];
+                        for (int m = 0; m < M; ++m) {
+                            const double2 w = wb[m * 128 + u], v = x[m];
+                            x[m] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+                        }
                     } else {
                         const double* wb = reinterpret_cast<const double*>(Pw);
 #pragma unroll
-                        for (int m = 0; m < M; ++m) x[m] = make_double2(wb[m * 128 + u], 0.0);
+                        for (int m = 0; m < M; ++m) {
+                            const double w = wb[m * 128 + u];
+                            x[m] = make_double2(x[m].x * w, x[m].y * w);
+                        }
                     }
                     __syncwarp();
                     if (pl + 1 < P)
                         issue_w(fi, pl + 1);
                     else if (fi + 1 < nfields)
                         issue_w(fi + 1, 0);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {  // F[2m + h], m = 4c .. 4c + 3
-                        double v[8];
-                        tmem_ld16(tmF + 128 * pl + 16 * c, v);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const double2 w = x[4 * c + i];
-                            if constexpr (!EXACT)
-                                x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
-                            else
-                                x[4 * c + i] = make_double2(v[2 * i] * w.x, v[2 * i + 1] * w.x);
-                        }
-                    }
                     fftxh_dit<M, true>(x, h);  // x[j] = Y[hQ + j], x[Q + j] = Y[M + hQ + j]
                     if (pl == 0) acquire(g);
                     double2* Xs = X + (int64_t)(g % D) * SLOT;
@@ -358,12 +368,19 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                     if (!is_loss) {
                         if constexpr (!EXACT) {
                             const double mu = (fi == 1) ? a.mult0 : 1.0;
+                            uint32_t g0[32], g1[32];  // 32 gain accumulators: two x32 loads, one wait
+                            tmem_ld32_nowait(tmG + GCOLS * pl, g0);
+                            tmem_ld32_nowait(tmG + GCOLS * pl + 32, g1);
+                            tmem_wait_ld();
 #pragma unroll
                             for (int c = 0; c < 4; ++c) {
                                 double gv[8];
-                                tmem_ld16(tmG + GCOLS * pl + 16 * c, gv);
 #pragma unroll
-                                for (int i = 0; i < 8; ++i) gv[i] += mu * (y[8 * c + i].x * y[8 * c + i].y);
+                                for (int i = 0; i < 8; ++i) {
+                                    const int k = 16 * (c & 1) + 2 * i;
+                                    const double old = (c < 2) ? tmem_pair(g0[k], g0[k + 1]) : tmem_pair(g1[k], g1[k + 1]);
+                                    gv[i] = old + mu * (y[8 * c + i].x * y[8 * c + i].y);
+                                }
                                 tmem_st16(tmG + GCOLS * pl + 16 * c, gv);
                             }
                             tmem_wait_st();

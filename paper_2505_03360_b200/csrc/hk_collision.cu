@@ -1051,23 +1051,33 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
             tmem_fence_after();
             // ---- phase A for every field ----
             for (int e = 0; e < n_entries; ++e) {
-                cp_async_wait_all();
-                __syncwarp();
+                // F (this pencil's 32 complex = 128 TMEM columns): four x32 loads, ONE wait,
+                // issued before the weights are read so the TMEM latency overlaps them
                 double2 x[N];
+                {
+                    uint32_t r0[32], r1[32], r2[32], r3[32];
+                    tmem_ld32_nowait(tmF, r0);
+                    tmem_ld32_nowait(tmF + 32, r1);
+                    tmem_ld32_nowait(tmF + 64, r2);
+                    tmem_ld32_nowait(tmF + 96, r3);
+                    cp_async_wait_all();
+                    __syncwarp();
+                    tmem_wait_ld();
 #pragma unroll
-                for (int i3 = 0; i3 < N; ++i3) x[i3] = wbuf[i3 * 32 + lane];
-                __syncwarp();
-                if (e + 1 < n_entries) issue_w(e + 1);
-#pragma unroll
-                for (int c = 0; c < N / 4; ++c) {
-                    double v[8];
-                    tmem_ld16(tmF + 16 * c, v);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const double2 w = x[4 * c + i];
-                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
+                    for (int m = 0; m < 8; ++m) {
+                        x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
+                        x[8 + m] = make_double2(tmem_pair(r1[4 * m], r1[4 * m + 1]), tmem_pair(r1[4 * m + 2], r1[4 * m + 3]));
+                        x[16 + m] = make_double2(tmem_pair(r2[4 * m], r2[4 * m + 1]), tmem_pair(r2[4 * m + 2], r2[4 * m + 3]));
+                        x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
                     }
                 }
+#pragma unroll
+                for (int i3 = 0; i3 < N; ++i3) {
+                    const double2 w = wbuf[i3 * 32 + lane], v = x[i3];
+                    x[i3] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+                }
+                __syncwarp();
+                if (e + 1 < n_entries) issue_w(e + 1);
                 fft_reg<N, true>(x);
                 if (DEFER) flush();  // field e-1: its stores completed during this FFT
                 acquire(g);
@@ -1195,12 +1205,19 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
                 if (pending) issue(g + 1);
                 if (!is_loss) {
                     const double m = (e == 0) ? a.mult0 : 1.0;
+                    uint32_t g0[32], g1[32];  // the 32 gain accumulators: two x32 loads, one wait
+                    tmem_ld32_nowait(tmG, g0);
+                    tmem_ld32_nowait(tmG + 32, g1);
+                    tmem_wait_ld();
 #pragma unroll
                     for (int c = 0; c < N / 8; ++c) {
                         double gv[8];
-                        tmem_ld16(tmG + 16 * c, gv);
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) gv[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
+                        for (int i = 0; i < 8; ++i) {
+                            const int k = 16 * (c & 1) + 2 * i;
+                            const double old = (c < 2) ? tmem_pair(g0[k], g0[k + 1]) : tmem_pair(g1[k], g1[k + 1]);
+                            gv[i] = old + m * (y[8 * c + i].x * y[8 * c + i].y);
+                        }
                         tmem_st16(tmG + 16 * c, gv);
                     }
                     tmem_wait_st();
