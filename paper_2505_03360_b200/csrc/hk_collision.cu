@@ -639,7 +639,7 @@ struct GeoP {
     static constexpr int PLANE = N * ROW;
     static constexpr int SLAB = P * PLANE;
 #ifndef HK_SLOTS
-#define HK_SLOTS 4
+#define HK_SLOTS 3  // measured: D = 2 60.8 ms, 3 51.9, 4 52.6, 5 52.9 (config 2, no guard)
 #endif
     static constexpr int D = HK_SLOTS;  // exchange slots in flight per team
     static_assert(P * N == 128, "one pencil per role thread");
