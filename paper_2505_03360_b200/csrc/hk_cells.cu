@@ -962,6 +962,10 @@ __global__ void __launch_bounds__(32 * WPB, HK_STAGE_MINB) residual_finish_warp_
 // (src/moments.cpp:269-312 sums the same quantities over V = c / sqrt(T)
 // directly; the identities are exact, cancellation costs ~|u|^4 / T^2 ulps).
 // ---------------------------------------------------------------------------
+#ifndef HK_MOM_UNROLL
+#define HK_MOM_UNROLL 8  // loads in flight per thread: 2 -> 7.4 ms, 4 -> 6.0, 8 -> 5.8 (config 3)
+#endif
+constexpr int kMomUnroll = HK_MOM_UNROLL;
 template <int MT, int MINB>
 __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
                                                             int lg, double* __restrict__ mom, double* __restrict__ sigma,
@@ -977,7 +981,7 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
         double M[14];  // S, Sx, Sy, Sz, Sxx, Sxy, Sxz, Syy, Syz, Szz, Rx, Ry, Rz, Q4
 #pragma unroll
         for (int k = 0; k < 14; ++k) M[k] = 0.0;
-#pragma unroll 4
+#pragma unroll kMomUnroll
         for (int p = t; p < npairs; p += MT) {
             const int idx = 2 * p;
             const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
@@ -1073,7 +1077,7 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
             const double pref = m.rho / pow(2.0 * M_PI * m.T, 1.5);
             __syncthreads();
             double acc = 0.0;
-#pragma unroll 4
+#pragma unroll kMomUnroll
             for (int p = t; p < npairs; p += MT) {
                 const int idx = 2 * p;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
