@@ -1114,6 +1114,16 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
 // raw sums -> Sigma / LLT / inverse -> coupling matrix (14 monomial moments of
 // the equilibrium) -> FullPivLU solve -> blended output.
 // ---------------------------------------------------------------------------
+#ifndef HK_STAGE_U1
+#define HK_STAGE_U1 8  // pass-1 loads in flight: 2 -> 15.4 ms, 4 -> 14.7, 8 -> 14.3 (config 3 ES-BGK stage)
+#endif
+#ifndef HK_STAGE_U2
+#define HK_STAGE_U2 1
+#endif
+#ifndef HK_STAGE_U3
+#define HK_STAGE_U3 1
+#endif
+constexpr int kStageU1 = HK_STAGE_U1, kStageU2 = HK_STAGE_U2, kStageU3 = HK_STAGE_U3;
 template <bool ESBGK, int MT, int MINB>
 __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __restrict__ fin, double* __restrict__ out,
                                                              int64_t ncells, VGrid g, int lg, double a,
@@ -1152,7 +1162,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             double s[11];
 #pragma unroll
             for (int k = 0; k < 11; ++k) s[k] = 0.0;
-#pragma unroll 2
+#pragma unroll kStageU1
             for (int q = t; q < ngroups; q += MT) {
                 const int idx = 4 * q;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
@@ -1324,6 +1334,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             double M[14];
 #pragma unroll
             for (int k = 0; k < 14; ++k) M[k] = 0.0;
+#pragma unroll kStageU2
             for (int q = t; q < ngroups; q += MT) {
                 const int idx = 4 * q;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
@@ -1368,6 +1379,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             const double x[5] = {par[9], par[10], par[11], par[12], par[13]};
             const double wf = eps / (eps + A), wg = A / (eps + A);
             // ---- pass 3: out = wf f + wg G (x0 + x.c + x4 |c|^2) ----
+#pragma unroll kStageU3
             for (int q = t; q < ngroups; q += MT) {
                 const int idx = 4 * q;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
