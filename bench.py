@@ -281,7 +281,7 @@ def run_gpu(args):
     roof = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if peak > 0 else None,
             "traffic": (traffic * ncells / cells_per) if (traffic and cells_per) else None,
-            "kernel": "coll_fast_warp_kernel<32,8>", "kernel_ms": k_ms,
+            "kernel": "coll_fast_w12_kernel<32,4>", "kernel_ms": k_ms,
             "kernel_share_of_step": (kms.value / args.steps) / ms_per_step if ms_per_step else None,
             "guard_ms": gms.value / max(gn.value, 1), "reroute_ms": rms.value / max(rn.value, 1),
             "peak_source": "live DFMA microbenchmark (hk_measure_fp64_peak); fp64 not in MEASURED_PEAKS.json",

@@ -349,7 +349,7 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
     cudaStreamWaitEvent(ctx->s_out, e0, 0);
     // Enqueue the copy streams first (H2D + ready flags, waits + D2H): nothing
     // is launched until the stream memory operations are known to work.
-    const unsigned per_cell = 8u * 4u;  // consumer warps per cell (C x P of coll_fast_warp_kernel)
+    const unsigned per_cell = 8u * 4u;  // consumer plane epilogues per cell (= N planes of j3, every warp kernel)
     {
         CUresult r0 = p_write_value32((CUstream)ctx->s_in, (CUdeviceptr)flags_dev, 0, 0);
         CUresult r1 = p_wait_value32((CUstream)ctx->s_out, (CUdeviceptr)flags_dev, 0, CU_STREAM_WAIT_VALUE_GEQ);

@@ -1272,6 +1272,674 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// FAST path, warp-autonomous pipeline with TWO planes per warp: a team of
+// C = 4 CTAs (P = 8 planes each), so 37 teams cover all 148 SMs (vs 18 x 8 =
+// 144), each publish / release fence covers two planes of stores, and a slot
+// waits for 16 warp arrivals instead of 32.  Otherwise the structure of
+// coll_fast_warp_kernel: producer warp pw owns i1 planes pw and pw + 4,
+// consumer warp pw owns j3 planes pw and pw + 4; a field is two units
+// (pp = 0, 1) for each warp.  TMEM (512 columns): F of plane pw + 4 pp at
+// 128 pp, gain at 256 + 64 pp.
+// ---------------------------------------------------------------------------
+template <int N, int C>
+struct GeoW {
+    static constexpr int P = N / C;   // planes per CTA
+    static constexpr int PPW = P / 4; // planes per warp
+    static constexpr int ROW = N + 1, PLANE = N * ROW;
+    static constexpr int D = HK_SLOTS;
+    static constexpr uint32_t TM_COLS = 512;
+    // landing [2][4 warps][PLANE] + producer staging [4 warps][PLANE]
+    static constexpr size_t SMEM = size_t(12 * PLANE) * sizeof(double2) + 2 * P * sizeof(uint64_t) + 32;
+};
+
+template <int N, int C>
+__global__ void __launch_bounds__(256, 1) coll_fast_wide_kernel(CollArgs a) {
+    using G = GeoW<N, C>;
+    constexpr int P = G::P, PPW = G::PPW, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
+    static_assert(N == 32 && PPW == 2, "N = 32, two planes per warp");
+    constexpr int64_t NB = (int64_t)N * N * N;
+    constexpr int BLK = P * N * N;
+    constexpr int64_t SLOT = (int64_t)C * BLK;
+    constexpr unsigned ARR = C * 4;  // warp arrivals per slot use (each role)
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rvb = smem;                // consumer landing [2][4][PLANE]
+    double2* Pw = smem + 8 * PLANE;     // producer staging [4][PLANE]
+    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 12 * PLANE);  // [P]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int pw = warp & 3;
+    const bool producer = t < 128;
+    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)team * D * SLOT;
+    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
+    unsigned* done = ready + D;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    if (t < P) mbar_init(smem_u32(fbar + t), 32);
+    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * pw) << 16);
+    const int n_entries = a.md + 1;
+    unsigned g = 0, ncell = 0;
+
+    if (producer) {
+        // ================================ PRODUCER WARP ================================
+        double2* wbuf = Pw + pw * PLANE;  // weights of the next unit [i3][lane] / transposes
+        const uint32_t wbuf_s = smem_u32(wbuf);
+        auto issue_w = [&](int e, int pp) {
+            const int i1 = r * P + pw + 4 * pp;
+            const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + lane;
+#pragma unroll
+            for (int i3 = 0; i3 < N; ++i3) cp_async16(wbuf_s + (i3 * 32 + lane) * 16, wt + i3 * N);
+            cp_async_commit();
+        };
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
+        auto acquire = [&](unsigned gg) {
+            if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR * (gg / D));
+            __syncwarp();
+        };
+        auto publish = [&](unsigned gg) {
+            __syncwarp();
+            if (lane == 0) signal_add(ready + gg % D);
+        };
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            if (a.in_ready && t == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);  // host chunk has landed
+            // ---- prologue: 2-D forward transforms of j3 planes 4 pp + (0..3) ----
+#pragma unroll 1
+            for (int pp = 0; pp < PPW; ++pp) {
+                named_bar(1, 128);  // every producer warp is done with its staging plane
+                for (int idx = t; idx < N * N * 4; idx += 128) {
+                    const int j3l = idx % 4, j2 = (idx / 4) % N, j1 = idx / (4 * N);
+                    Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + 4 * pp + j3l], 0.0);
+                }
+                named_bar(1, 128);
+                {
+                    double2* row = wbuf + lane * ROW;  // (j3l = pw, j1 = lane)
+                    double2 x[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) x[i] = row[i];
+                    fft_reg<N, false>(x);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) row[i] = x[i];
+                }
+                __syncwarp();
+                const int j3 = r * P + 4 * pp + pw, k2 = lane;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = wbuf[k2 + i * ROW];
+                fft_reg<N, false>(x);
+                if (pp == 0) acquire(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int k1 = 0; k1 < N; ++k1)
+                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
+            }
+            publish(g);
+            ++g;
+            __syncwarp();  // my staging plane is free: first weights
+            issue_w(0, 0);
+            // ---- phase A: per field, the two i1 planes of this warp ----
+            for (int e = 0; e < n_entries; ++e) {
+#pragma unroll 1
+                for (int pp = 0; pp < PPW; ++pp) {
+                    if (e == 0) {
+                        mbar_wait_parity(smem_u32(fbar + pw + 4 * pp), ncell & 1);  // F(plane) in TMEM
+                        tmem_fence_after();
+                    }
+                    const uint32_t tmF = tm + 128 * pp;
+                    double2 x[N];
+                    {
+                        uint32_t r0[32], r1[32], r2[32], r3[32];
+                        tmem_ld32_nowait(tmF, r0);
+                        tmem_ld32_nowait(tmF + 32, r1);
+                        tmem_ld32_nowait(tmF + 64, r2);
+                        tmem_ld32_nowait(tmF + 96, r3);
+                        cp_async_wait_all();
+                        __syncwarp();
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
+                            x[8 + m] = make_double2(tmem_pair(r1[4 * m], r1[4 * m + 1]), tmem_pair(r1[4 * m + 2], r1[4 * m + 3]));
+                            x[16 + m] = make_double2(tmem_pair(r2[4 * m], r2[4 * m + 1]), tmem_pair(r2[4 * m + 2], r2[4 * m + 3]));
+                            x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
+                        }
+                    }
+#pragma unroll
+                    for (int i3 = 0; i3 < N; ++i3) {
+                        const double2 w = wbuf[i3 * 32 + lane], v = x[i3];
+                        x[i3] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+                    }
+                    __syncwarp();
+                    if (pp + 1 < PPW)
+                        issue_w(e, pp + 1);
+                    else if (e + 1 < n_entries)
+                        issue_w(e + 1, 0);
+                    fft_reg<N, true>(x);
+                    if (pp == 0) acquire(g);
+                    double2* Xs = X + (int64_t)(g % D) * SLOT;
+                    const int i1 = r * P + pw + 4 * pp;
+#pragma unroll
+                    for (int j3 = 0; j3 < N; ++j3)
+                        st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + lane, x[j3]);
+                }
+                publish(g);  // one release fence for both planes
+                ++g;
+            }
+        }
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
+        }
+    } else {
+        // ================================ CONSUMER WARP ================================
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
+        // unit u = 2 (slot index) + pp lands in Rvb[u & 1][pw]
+        auto pull = [&](unsigned gg, int pp, int buf) {
+            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + (pw + 4 * pp) * N * N;
+            const uint32_t d0 = smem_u32(Rvb + (buf * 4 + pw) * PLANE);
+#pragma unroll 8
+            for (int k = 0; k < N; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
+            cp_async_commit();
+        };
+        auto issue = [&](unsigned gg, int pp, int buf) {
+            if (lane == 0) spin_cyc += spin_geq(ready + gg % D, ARR * (gg / D + 1));
+            __syncwarp();
+            pull(gg, pp, buf);
+        };
+        auto try_issue = [&](unsigned gg, int pp, int buf) -> bool {
+            unsigned v = 0;
+            if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ready + gg % D) : "memory");
+            v = __shfl_sync(0xffffffffu, v, 0);
+            if ((int)(v - ARR * (gg / D + 1)) < 0) return false;
+            pull(gg, pp, buf);
+            return true;
+        };
+        auto complete = [&](unsigned gg, int pp) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (pp == PPW - 1 && lane == 0) signal_add_relaxed(done + gg % D);  // last pull of this slot
+        };
+        unsigned u = 0;  // unit counter (buffer parity)
+        if ((int64_t)team < count) issue(g, 0, 0);
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            const bool more_cells = it + nteams < count;
+            // ---- prologue units: forward over k3 of rows (k1l = pw + 4 pp, k2 = lane), F -> TMEM ----
+#pragma unroll 1
+            for (int pp = 0; pp < PPW; ++pp, ++u) {
+                complete(g, pp);
+                const double2* row = Rvb + ((u & 1) * 4 + pw) * PLANE + lane * ROW;
+                const int k1 = r * P + pw + 4 * pp, k2 = lane;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = row[i];
+                __syncwarp();
+                if (pp + 1 < PPW) issue(g, pp + 1, (u + 1) & 1);  // same slot, already published
+                fft_reg<N, false>(x);
+                const double s = 1.0 / double(NB);
+                const uint32_t tmF = tm + 128 * pp, tmG = tm + 256 + 64 * pp;
+#pragma unroll
+                for (int c = 0; c < N / 4; ++c) {
+                    double v[8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        v[2 * i] = x[4 * c + i].x * s;
+                        v[2 * i + 1] = x[4 * c + i].y * s;
+                    }
+                    tmem_st16(tmF + 16 * c, v);
+                }
+                if (a.nyq) {
+                    constexpr int H = N / 2;
+                    double2* ny = a.nyq + cell * 3 * N * N;
+                    ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
+                    if (k2 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
+                    }
+                    if (k1 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
+                    }
+                }
+                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
+                tmem_wait_st();
+                tmem_fence_before();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pw + 4 * pp)) : "memory");
+            }
+            __syncwarp();
+            issue(g + 1, 0, u & 1);  // field 0 (needs F of both planes, published above)
+            ++g;
+            // ---- fields ----
+            for (int e = 0; e < n_entries; ++e) {
+                const bool is_loss = (e == a.md);
+#pragma unroll 1
+                for (int pp = 0; pp < PPW; ++pp, ++u) {
+                    double2* Rv = Rvb + ((u & 1) * 4 + pw) * PLANE;
+                    complete(g, pp);
+                    const bool last = pp + 1 == PPW;
+                    const bool more = !last || (e + 1 < n_entries) || more_cells;
+                    const unsigned g2 = last ? g + 1 : g;
+                    const int pp2 = last ? 0 : pp + 1;
+                    bool pending = more && !try_issue(g2, pp2, (u + 1) & 1);
+                    {  // inverse FFT over i2: row i1 = lane of j3 plane pw + 4 pp
+                        double2* row = Rv + lane * ROW;
+                        double2 y[N];
+#pragma unroll
+                        for (int i = 0; i < N; ++i) y[i] = row[i];
+                        fft_reg<N, true>(y);
+#pragma unroll
+                        for (int i = 0; i < N; ++i) row[i] = y[i];
+                    }
+                    __syncwarp();
+                    if (pending) pending = !try_issue(g2, pp2, (u + 1) & 1);
+                    double2 y[N];
+                    {  // inverse FFT over i1: column j2 = lane
+                        const double2* col = Rv + lane;
+#pragma unroll
+                        for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
+                        fft_reg<N, true>(y);
+                    }
+                    __syncwarp();
+                    if (pending) issue(g2, pp2, (u + 1) & 1);
+                    const uint32_t tmG = tm + 256 + 64 * pp;
+                    if (!is_loss) {
+                        const double m = (e == 0) ? a.mult0 : 1.0;
+                        uint32_t g0[32], g1[32];
+                        tmem_ld32_nowait(tmG, g0);
+                        tmem_ld32_nowait(tmG + 32, g1);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int c = 0; c < N / 8; ++c) {
+                            double gv[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const int k = 16 * (c & 1) + 2 * i;
+                                const double old = (c < 2) ? tmem_pair(g0[k], g0[k + 1]) : tmem_pair(g1[k], g1[k + 1]);
+                                gv[i] = old + m * (y[8 * c + i].x * y[8 * c + i].y);
+                            }
+                            tmem_st16(tmG + 16 * c, gv);
+                        }
+                        tmem_wait_st();
+                    } else {
+                        // ---- epilogue for plane j3 = rP + pw + 4 pp ----
+                        const int j3 = r * P + pw + 4 * pp;
+                        double* qc = a.q + cell * NB;
+                        double mre = 0.0, n2 = 0.0, l2 = 0.0;
+#pragma unroll
+                        for (int c = 0; c < N / 8; ++c) {
+                            double gv[8];
+                            tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const int j1 = 8 * c + i;
+                                const int64_t gi = ((int64_t)j1 * N + lane) * N + j3;
+                                const double lt = fc[gi] * y[j1].x;
+                                const double qre = a.jac * (a.w * gv[i] - lt);
+                                qc[gi] = qre;
+                                mre = fmax(mre, fabs(qre));
+                                n2 += qre * qre;
+                                l2 += lt * lt;
+                            }
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+                            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                            l2 += __shfl_xor_sync(0xffffffffu, l2, o);
+                        }
+                        if (lane == 0 && a.st) {
+                            hk_cell_status* sc = a.st + cell;
+                            atomic_max_nonneg(&sc->max_re, mre);
+                            atomicAdd(&sc->q_norm2, n2);
+                            atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
+                        }
+                        __syncwarp();
+                        if (lane == 0 && a.out_done) signal_add(a.out_done + cell / a.chunk);  // q rows visible
+                    }
+                }
+                ++g;
+            }
+        }
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
+// 12-warp variant: 4 producer warps (two i1 planes each) and 8 consumer warps
+// (one j3 plane each, single landing buffer): per scheduler one producer and
+// two consumers, matching the 1 : 2 transform count of the two roles; the
+// consumers hide each other's pull latency instead of double buffering.
+// <= 168 registers per thread (384 threads).
+template <int N, int C>
+__global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
+    using G = GeoW<N, C>;
+    constexpr int P = G::P, PPW = G::PPW, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
+    static_assert(N == 32 && PPW == 2, "N = 32, two planes per warp");
+    constexpr int64_t NB = (int64_t)N * N * N;
+    constexpr int BLK = P * N * N;
+    constexpr int64_t SLOT = (int64_t)C * BLK;
+    constexpr unsigned ARR = C * 4;     // producer warp arrivals per slot (ready)
+    constexpr unsigned ARR_C = C * 8;   // consumer warp arrivals per slot (done)
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rvb = smem;                // consumer landing [8 consumer warps][PLANE]
+    double2* Pw = smem + 8 * PLANE;     // producer staging [4][PLANE]
+    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 12 * PLANE);  // [P]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int pw = warp & 3;
+    const bool producer = t < 128;
+    const int cw = warp - 4;  // consumer warp = j3 / k1 plane (0..7)
+    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)team * D * SLOT;
+    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
+    unsigned* done = ready + D;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    if (t < P) mbar_init(smem_u32(fbar + t), 32);
+    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * pw) << 16);  // lanes of warp % 4 (both roles)
+    const int n_entries = a.md + 1;
+    unsigned g = 0, ncell = 0;
+
+    if (producer) {
+        // ================================ PRODUCER WARP ================================
+        double2* wbuf = Pw + pw * PLANE;  // weights of the next unit [i3][lane] / transposes
+        const uint32_t wbuf_s = smem_u32(wbuf);
+        auto issue_w = [&](int e, int pp) {
+            const int i1 = r * P + pw + 4 * pp;
+            const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + lane;
+#pragma unroll
+            for (int i3 = 0; i3 < N; ++i3) cp_async16(wbuf_s + (i3 * 32 + lane) * 16, wt + i3 * N);
+            cp_async_commit();
+        };
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
+        auto acquire = [&](unsigned gg) {
+            if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR_C * (gg / D));
+            __syncwarp();
+        };
+        auto publish = [&](unsigned gg) {
+            __syncwarp();
+            if (lane == 0) signal_add(ready + gg % D);
+        };
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            if (a.in_ready && t == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);  // host chunk has landed
+            // ---- prologue: 2-D forward transforms of j3 planes 4 pp + (0..3) ----
+#pragma unroll 1
+            for (int pp = 0; pp < PPW; ++pp) {
+                named_bar(1, 128);  // every producer warp is done with its staging plane
+                for (int idx = t; idx < N * N * 4; idx += 128) {
+                    const int j3l = idx % 4, j2 = (idx / 4) % N, j1 = idx / (4 * N);
+                    Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + 4 * pp + j3l], 0.0);
+                }
+                named_bar(1, 128);
+                {
+                    double2* row = wbuf + lane * ROW;  // (j3l = pw, j1 = lane)
+                    double2 x[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) x[i] = row[i];
+                    fft_reg<N, false>(x);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) row[i] = x[i];
+                }
+                __syncwarp();
+                const int j3 = r * P + 4 * pp + pw, k2 = lane;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = wbuf[k2 + i * ROW];
+                fft_reg<N, false>(x);
+                if (pp == 0) acquire(g);
+                double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                for (int k1 = 0; k1 < N; ++k1)
+                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
+            }
+            publish(g);
+            ++g;
+            __syncwarp();  // my staging plane is free: first weights
+            issue_w(0, 0);
+            // ---- phase A: per field, the two i1 planes of this warp ----
+            for (int e = 0; e < n_entries; ++e) {
+#pragma unroll 1
+                for (int pp = 0; pp < PPW; ++pp) {
+                    if (e == 0) {
+                        mbar_wait_parity(smem_u32(fbar + pw + 4 * pp), ncell & 1);  // F(plane) in TMEM
+                        tmem_fence_after();
+                    }
+                    const uint32_t tmF = tm + 128 * pp;
+                    double2 x[N];
+                    {
+                        uint32_t r0[32], r1[32], r2[32], r3[32];
+                        tmem_ld32_nowait(tmF, r0);
+                        tmem_ld32_nowait(tmF + 32, r1);
+                        tmem_ld32_nowait(tmF + 64, r2);
+                        tmem_ld32_nowait(tmF + 96, r3);
+                        cp_async_wait_all();
+                        __syncwarp();
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
+                            x[8 + m] = make_double2(tmem_pair(r1[4 * m], r1[4 * m + 1]), tmem_pair(r1[4 * m + 2], r1[4 * m + 3]));
+                            x[16 + m] = make_double2(tmem_pair(r2[4 * m], r2[4 * m + 1]), tmem_pair(r2[4 * m + 2], r2[4 * m + 3]));
+                            x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
+                        }
+                    }
+#pragma unroll
+                    for (int i3 = 0; i3 < N; ++i3) {
+                        const double2 w = wbuf[i3 * 32 + lane], v = x[i3];
+                        x[i3] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+                    }
+                    __syncwarp();
+                    if (pp + 1 < PPW)
+                        issue_w(e, pp + 1);
+                    else if (e + 1 < n_entries)
+                        issue_w(e + 1, 0);
+                    fft_reg<N, true>(x);
+                    if (pp == 0) acquire(g);
+                    double2* Xs = X + (int64_t)(g % D) * SLOT;
+                    const int i1 = r * P + pw + 4 * pp;
+#pragma unroll
+                    for (int j3 = 0; j3 < N; ++j3)
+                        st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + lane, x[j3]);
+                }
+                publish(g);  // one release fence for both planes
+                ++g;
+            }
+        }
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
+        }
+    } else {
+        // ================================ CONSUMER WARP ================================
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
+        double2* Rv = Rvb + cw * PLANE;  // single landing buffer of my plane
+        const uint32_t tmF = tm + 128 * (cw >> 2), tmG = tm + 256 + 64 * (cw >> 2);
+        auto pull = [&](unsigned gg) {
+            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + cw * N * N;
+            const uint32_t d0 = smem_u32(Rv);
+#pragma unroll 8
+            for (int k = 0; k < N; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
+            cp_async_commit();
+        };
+        auto issue = [&](unsigned gg) {
+            if (lane == 0) spin_cyc += spin_geq(ready + gg % D, ARR * (gg / D + 1));
+            __syncwarp();
+            pull(gg);
+        };
+        auto complete = [&](unsigned gg) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (lane == 0) signal_add_relaxed(done + gg % D);
+        };
+        if ((int64_t)team < count) issue(g);
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            const bool more_cells = it + nteams < count;
+            // ---- prologue: forward over k3 of rows (k1l = cw, k2 = lane), F -> TMEM ----
+            complete(g);
+            {
+                const double2* row = Rv + lane * ROW;
+                const int k1 = r * P + cw, k2 = lane;
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = row[i];
+                fft_reg<N, false>(x);
+                const double s = 1.0 / double(NB);
+#pragma unroll
+                for (int c = 0; c < N / 4; ++c) {
+                    double v[8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        v[2 * i] = x[4 * c + i].x * s;
+                        v[2 * i + 1] = x[4 * c + i].y * s;
+                    }
+                    tmem_st16(tmF + 16 * c, v);
+                }
+                if (a.nyq) {
+                    constexpr int H = N / 2;
+                    double2* ny = a.nyq + cell * 3 * N * N;
+                    ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
+                    if (k2 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
+                    }
+                    if (k1 == H) {
+#pragma unroll
+                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
+                    }
+                }
+                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
+                tmem_wait_st();
+                tmem_fence_before();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + cw)) : "memory");
+            }
+            __syncwarp();
+            issue(g + 1);  // field 0 (needs F, published above)
+            ++g;
+            for (int e = 0; e < n_entries; ++e) {
+                const bool is_loss = (e == a.md);
+                complete(g);
+                const bool more = (e + 1 < n_entries) || more_cells;
+                {  // inverse FFT over i2: row i1 = lane of j3 plane cw
+                    double2* row = Rv + lane * ROW;
+                    double2 y[N];
+#pragma unroll
+                    for (int i = 0; i < N; ++i) y[i] = row[i];
+                    fft_reg<N, true>(y);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) row[i] = y[i];
+                }
+                __syncwarp();
+                double2 y[N];
+                {  // inverse FFT over i1: column j2 = lane
+                    const double2* col = Rv + lane;
+#pragma unroll
+                    for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
+                }
+                __syncwarp();  // buffer free: the next field's pull overlaps this transform
+                if (more) issue(g + 1);
+                fft_reg<N, true>(y);
+                if (!is_loss) {
+                    const double m = (e == 0) ? a.mult0 : 1.0;
+                    uint32_t g0[32], g1[32];
+                    tmem_ld32_nowait(tmG, g0);
+                    tmem_ld32_nowait(tmG + 32, g1);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < N / 8; ++c) {
+                        double gv[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int k = 16 * (c & 1) + 2 * i;
+                            const double old = (c < 2) ? tmem_pair(g0[k], g0[k + 1]) : tmem_pair(g1[k], g1[k + 1]);
+                            gv[i] = old + m * (y[8 * c + i].x * y[8 * c + i].y);
+                        }
+                        tmem_st16(tmG + 16 * c, gv);
+                    }
+                    tmem_wait_st();
+                } else {
+                    const int j3 = r * P + cw;
+                    double* qc = a.q + cell * NB;
+                    double mre = 0.0, n2 = 0.0, l2 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < N / 8; ++c) {
+                        double gv[8];
+                        tmem_ld16(tmG + 16 * c, gv);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int j1 = 8 * c + i;
+                            const int64_t gi = ((int64_t)j1 * N + lane) * N + j3;
+                            const double lt = fc[gi] * y[j1].x;
+                            const double qre = a.jac * (a.w * gv[i] - lt);
+                            qc[gi] = qre;
+                            mre = fmax(mre, fabs(qre));
+                            n2 += qre * qre;
+                            l2 += lt * lt;
+                        }
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+                        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                        l2 += __shfl_xor_sync(0xffffffffu, l2, o);
+                    }
+                    if (lane == 0 && a.st) {
+                        hk_cell_status* sc = a.st + cell;
+                        atomic_max_nonneg(&sc->max_re, mre);
+                        atomicAdd(&sc->q_norm2, n2);
+                        atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
+                    }
+                    __syncwarp();
+                    if (lane == 0 && a.out_done) signal_add(a.out_done + cell / a.chunk);  // q rows visible
+                }
+                ++g;
+            }
+        }
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
+// ---------------------------------------------------------------------------
 // FAST path, split-pencil warp pipeline (production kernel for N = 32).
 // As coll_fast_warp_kernel, but every 32-point pencil is shared by the lane
 // pair (l, l ^ 16) (fftx2_dit / fftx2_dif), so a thread holds 16 complex
@@ -1781,22 +2449,30 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     const char* kv = getenv("HK_FAST_KERNEL");
     // variant 1: warp kernel (default), 3: warp kernel with deferred publish
     // (measured 10 % slower), 2: x2, 0: CTA pipeline
-    const int variant = !kv ? 1 : (kv[0] == 'x' ? 2 : (kv[0] == 'c' ? 0 : (kv[0] == 'd' ? 3 : 1)));
+    // 4: two planes per warp, teams of 4 CTAs (coll_fast_wide_kernel)
+    // default 5 (12 warps, measured 49.0 ms vs 52.0 ms for the 8-warp kernel); HK_FAST_KERNEL=8 for variant 1
+    const int variant = !kv ? 5
+                      : (kv[0] == 'x' ? 2 : (kv[0] == 'c' ? 0 : (kv[0] == 'd' ? 3 : (kv[0] == 'w' ? 4 : (kv[0] == '8' ? 1 : 5)))));
+    constexpr int CW = 4;  // team size of the wide kernel
     auto kern = variant == 2 ? coll_fast_x2_kernel<N, C>
               : variant == 1 ? coll_fast_warp_kernel<N, C, false>
               : variant == 3 ? coll_fast_warp_kernel<N, C, true>
+              : variant == 4 ? coll_fast_wide_kernel<N, CW>
+              : variant == 5 ? coll_fast_w12_kernel<N, CW>
                              : coll_fast_pipe_kernel<N, C>;
-    const int nthreads = variant == 2 ? 512 : 256;
+    const int nthreads = variant == 2 ? 512 : (variant == 5 ? 384 : 256);
+    const int TC = (variant == 4 || variant == 5) ? CW : C;  // CTAs per team
+    const size_t smem = (variant == 4 || variant == 5) ? GeoW<N, CW>::SMEM : G::SMEM;
     const int key = N * 100 + C * 2 + 2000 + variant;
     int st;
     if (!ctx->max_clusters.count(key)) {
-        if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
+        if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                              "smem attribute")))
             return st;
         int per_sm = 0;
-        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, G::SMEM), "occupancy")))
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, smem), "occupancy")))
             return st;
-        int teams = (per_sm >= 1 ? 1 : 0) * ctx->sm_count / C;  // one CTA per SM (TMEM, SMEM)
+        int teams = (per_sm >= 1 ? 1 : 0) * ctx->sm_count / TC;  // one CTA per SM (TMEM, SMEM)
         if (const char* m = getenv("HK_TEAMS")) teams = atoi(m);  // experiment override
         if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] pipe kernel: per_sm %d teams %d\n", per_sm, teams);
         if (teams < 1) return fail(ctx, HK_CUDA, "pipelined collision kernel cannot be resident");
@@ -1806,7 +2482,7 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     if (max_cells < teams) teams = max_cells;
     if (teams < 1) return HK_OK;
     CollArgs args = args_in;
-    if ((variant == 1 || variant == 3) && ctx->sio_in_ready) {  // streamed host I/O (warp kernels only)
+    if ((variant == 1 || variant == 3 || variant == 4 || variant == 5) && ctx->sio_in_ready) {  // streamed host I/O (warp kernels only)
         args.in_ready = ctx->sio_in_ready;
         args.out_done = ctx->sio_out_done;
         args.chunk = ctx->sio_chunk;
@@ -1824,8 +2500,8 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     }
     void* params[] = {&args};
     timing_begin(ctx, tag);
-    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * C)), dim3(nthreads), params,
-                                                     G::SMEM, ctx->stream),
+    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * TC)), dim3(nthreads), params,
+                                                     smem, ctx->stream),
                     "pipelined collision kernel launch");
     timing_end(ctx);
     ctx->launches++;
@@ -1834,8 +2510,8 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
         cudaMemcpyAsync(h, prof, 32, cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         fprintf(stderr, "[hk prof] CTAs %lld: producer spin %.1f%% of %.3g cyc/CTA, consumer spin %.1f%% of %.3g cyc/CTA\n",
-                (long long)(teams * C), 100.0 * h[0] / (double)h[2], h[2] / double(teams * C), 100.0 * h[1] / (double)h[3],
-                h[3] / double(teams * C));
+                (long long)(teams * TC), 100.0 * h[0] / (double)h[2], h[2] / double(teams * TC), 100.0 * h[1] / (double)h[3],
+                h[3] / double(teams * TC));
     }
     return st;
 }
