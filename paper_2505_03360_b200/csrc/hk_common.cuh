@@ -174,6 +174,14 @@ __device__ __forceinline__ void mbar_init_fence() {
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
 }
+// 1-D bulk copy global -> this CTA's shared memory (TMA engine), completion
+// counted on `bar` in bytes (pair with mbar_arrive_expect_tx).  16-byte
+// aligned addresses, size a multiple of 16.
+__device__ __forceinline__ void bulk_g2s(uint32_t smem_dst, const void* gsrc, unsigned bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_dst),
+                 "l"(gsrc), "r"(bytes), "r"(bar)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, unsigned parity) {
     asm volatile(
         "{\n"
