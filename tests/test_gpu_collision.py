@@ -160,3 +160,22 @@ def test_n32_nyquist_correction_equals_exact(hk):
         assert gap <= (floor if fixed[c] else max(TOL * np.linalg.norm(qe[c]), floor)), c
     # the corrected cells' verdicts describe the corrected Q
     np.testing.assert_allclose(st["q_norm2"][fixed], (qd[fixed] ** 2).sum(1), rtol=1e-12)
+
+
+def test_n32_conservation_matches_reference_level(n32, hk):
+    """Mass, momentum and energy of Q (the collision invariants) are preserved to
+    the reference's own level: the invariant moments of the device Q match those
+    of the reference's Q to 1e-10 of the moment scale (BASELINE north_star)."""
+    import torch
+    f = torch.from_numpy(n32["f"]).cuda()
+    q = hk.spectral_collision(f, n32["kern"]).cpu().numpy()
+    v = inputs.nodes(32)
+    vx = np.broadcast_to(v[:, None, None], (32, 32, 32)).ravel()
+    vy = np.broadcast_to(v[None, :, None], (32, 32, 32)).ravel()
+    vz = np.broadcast_to(v[None, None, :], (32, 32, 32)).ravel()
+    phis = [np.ones_like(vx), vx, vy, vz, vx * vx + vy * vy + vz * vz]
+    for c in range(len(q)):
+        scale = np.abs(n32["q_ref"][c]).sum() * 8.0 ** 2
+        for phi in phis:
+            ours, ref = float((q[c] * phi).sum()), float((n32["q_ref"][c] * phi).sum())
+            assert abs(ours - ref) <= 1e-10 * scale, (c, ours, ref)

@@ -13,5 +13,5 @@ timeout 600 python bench.py $ARGS > gpurun_out/plain_launch_$TAG.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k regex:hk:: --csv --log-file gpurun_out/launches_$TAG.csv \
   python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
 timeout 300 python tools/profile_collision.py --cells 1024 --iters 1 > gpurun_out/plain_prof_$TAG.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:coll_fast -c 1 -o gpurun_out/coll_fast_$TAG \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:coll_fast_w12 -c 1 -o gpurun_out/coll_fast_$TAG \
   python tools/profile_collision.py --cells 1024 --iters 1 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
