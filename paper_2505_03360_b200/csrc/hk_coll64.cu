@@ -485,6 +485,347 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
     if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
 }
 
+// FAST path with 12 warps: warps 0-3 produce exactly as in coll64_kernel,
+// warps 4-11 are two consumer groups of four, group k owning j3 plane k
+// (single landing buffer each), so both planes of a field are consumed
+// concurrently: one producer and two consumers per scheduler, matching the
+// 1 : 2 transform count of the roles (as coll_fast_w12_kernel at N = 32).
+__global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
+    constexpr bool EXACT = false;
+    using G = Geo64;
+    constexpr int N = G::N, C = G::C, P = G::P, M = G::M, Q = G::Q, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
+    constexpr int64_t NB = G::NB;
+    constexpr int BLK = G::BLK;
+    constexpr int64_t SLOT = G::SLOT;
+    constexpr unsigned ARR = G::ARR;          // producer warp arrivals per slot (ready)
+    constexpr unsigned ARR_C = 2 * G::ARR;    // consumer warp arrivals per slot (done)
+    constexpr int GCOLS = EXACT ? 128 : 64;  // TMEM columns of gain per plane
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Rvb = smem;              // consumer landing planes [group][N][ROW]
+    double2* Pw = smem + 2 * PLANE;   // producer: prologue plane / weight staging
+    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * PLANE);  // [P] F-plane ready
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+
+    const int t = threadIdx.x;
+    const int warp = t >> 5, lane = t & 31;
+    const int rw = warp & 3;                 // role-local warp == TMEM lane quarter
+    const int pp = 16 * rw + (lane & 15);    // pencil (row / column) within a plane
+    const int h = lane >> 4;                 // half of the pencil
+    const int u = t & 127;
+    const bool producer = t < 128;
+    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)team * D * SLOT;
+    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
+    unsigned* done = ready + D;
+
+    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
+    if (t < P) mbar_init(smem_u32(fbar + t), 128);
+    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tm = *tslot + ((uint32_t)(32 * rw) << 16);
+    const uint32_t tmF = tm, tmG = tm + 256;  // F plane pl: +128 pl; gain plane pl: +GCOLS pl
+    const int nfields = EXACT ? 2 * a.md + 1 : a.md + 1;
+    unsigned g = 0, ncell = 0;
+
+    if (producer) {
+        // ================================ PRODUCERS ================================
+        // Weight staging: thread-private slots [m][u] (interleaved: conflict-free).
+        const uint32_t wb_s = smem_u32(Pw);
+        auto issue_w = [&](int fi, int pl) {
+            const int i1 = r * P + pl;
+            if constexpr (!EXACT) {
+                const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N + pp;
+#pragma unroll
+                for (int m = 0; m < M; ++m) cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N);
+            } else {
+                const double* base = (fi == 2 * a.md) ? a.loss : ((fi & 1) ? a.alpha_p : a.alpha) + (int64_t)(fi >> 1) * NB;
+                const double* wt = base + (int64_t)i1 * N * N + pp;
+#pragma unroll
+                for (int m = 0; m < M; ++m) cp_async8(wb_s + (m * 128 + u) * 8, wt + (2 * m + h) * N);
+            }
+            cp_async_commit();
+        };
+        auto acquire = [&](unsigned gg) {
+            if (lane == 0) spin_geq(done + gg % D, ARR_C * (gg / D));
+            __syncwarp();
+        };
+        auto publish = [&](unsigned gg) {
+            __syncwarp();
+            if (lane == 0) signal_add(ready + gg % D);
+        };
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            // ---- prologue: per j3 plane, 2-D forward transform (j2 then j1) -> owner of k1 ----
+            for (int pl = 0; pl < P; ++pl) {
+                const int j3 = r * P + pl;
+                named_bar(1, 128);  // Pw free
+                for (int idx = u; idx < N * N; idx += 128)
+                    Pw[(idx / N) * ROW + (idx % N)] = make_double2(fc[(int64_t)idx * N + j3], 0.0);
+                named_bar(1, 128);
+                {  // rows j1 = pp over j2 (DIF), back in natural order
+                    double2* row = Pw + pp * ROW;
+                    double2 v[M];
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        v[j] = row[h * Q + j];
+                        v[Q + j] = row[M + h * Q + j];
+                    }
+                    fftxh_dif<M, false>(v, h);
+                    __syncwarp();
+#pragma unroll
+                    for (int m = 0; m < M; ++m) row[2 * m + h] = v[m];
+                }
+                named_bar(1, 128);  // columns need every row
+                {  // columns k2 = pp over j1 (DIT): v[j] = K1 index hQ + j, v[Q + j] = M + hQ + j
+                    const double2* col = Pw + pp;
+                    double2 v[M];
+#pragma unroll
+                    for (int m = 0; m < M; ++m) v[m] = col[(2 * m + h) * ROW];
+                    fftxh_dit<M, false>(v, h);
+                    if (pl == 0) acquire(g);
+                    double2* Xs = X + (int64_t)(g % D) * SLOT;
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        const int ka = h * Q + j, kb = M + h * Q + j;
+                        st_cg16(Xs + (int64_t)(ka / P) * BLK + ((ka % P) * N + pp) * N + j3, v[j]);
+                        st_cg16(Xs + (int64_t)(kb / P) * BLK + ((kb % P) * N + pp) * N + j3, v[Q + j]);
+                    }
+                }
+            }
+            publish(g);
+            ++g;
+            named_bar(1, 128);  // prologue reads of Pw done: weight staging may overwrite it
+            issue_w(0, 0);
+            // ---- phase A: X = F * weights, inverse FFT over i3, -> owner of j3 ----
+            for (int fi = 0; fi < nfields; ++fi) {
+#pragma unroll 1
+                for (int pl = 0; pl < P; ++pl) {
+                    if (fi == 0) {
+                        mbar_wait_parity(smem_u32(fbar + pl), ncell & 1);  // consumers put F(plane) in TMEM
+                        tmem_fence_after();
+                    }
+                    // F of this half-pencil (32 complex = 128 TMEM columns): four x32
+                    // loads and ONE wait, overlapping the weight reads
+                    double2 x[M];
+                    {
+                        uint32_t r0[32], r1[32], r2[32], r3[32];
+                        tmem_ld32_nowait(tmF + 128 * pl, r0);
+                        tmem_ld32_nowait(tmF + 128 * pl + 32, r1);
+                        tmem_ld32_nowait(tmF + 128 * pl + 64, r2);
+                        tmem_ld32_nowait(tmF + 128 * pl + 96, r3);
+                        cp_async_wait_all();
+                        __syncwarp();
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) {
+                            x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
+                            x[8 + m] = make_double2(tmem_pair(r1[4 * m], r1[4 * m + 1]), tmem_pair(r1[4 * m + 2], r1[4 * m + 3]));
+                            x[16 + m] = make_double2(tmem_pair(r2[4 * m], r2[4 * m + 1]), tmem_pair(r2[4 * m + 2], r2[4 * m + 3]));
+                            x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
+                        }
+                    }
+                    if constexpr (!EXACT) {
+                        const double2* wb = Pw;
+#pragma unroll
+                        for (int m = 0; m < M; ++m) {
+                            const double2 w = wb[m * 128 + u], v = x[m];
+                            x[m] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+                        }
+                    } else {
+                        const double* wb = reinterpret_cast<const double*>(Pw);
+#pragma unroll
+                        for (int m = 0; m < M; ++m) {
+                            const double w = wb[m * 128 + u];
+                            x[m] = make_double2(x[m].x * w, x[m].y * w);
+                        }
+                    }
+                    __syncwarp();
+                    if (pl + 1 < P)
+                        issue_w(fi, pl + 1);
+                    else if (fi + 1 < nfields)
+                        issue_w(fi + 1, 0);
+                    fftxh_dit<M, true>(x, h);  // x[j] = Y[hQ + j], x[Q + j] = Y[M + hQ + j]
+                    if (pl == 0) acquire(g);
+                    double2* Xs = X + (int64_t)(g % D) * SLOT;
+                    const int i1 = r * P + pl;
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        const int ja = h * Q + j, jb = M + h * Q + j;
+                        st_cg16(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j]);
+                        st_cg16(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j]);
+                    }
+                }
+                publish(g);
+                ++g;
+            }
+        }
+    } else {
+        // ============================ CONSUMER GROUPS ============================
+        const int grp = (warp - 4) >> 2;   // = my j3 / k1 plane (P = 2)
+        const unsigned bar = 2 + grp;      // named barrier of my group (128 threads)
+        double2* Rv = Rvb + grp * PLANE;
+        auto pull = [&](unsigned gs) {     // my 16 rows of plane grp of slot gs
+            const double2* src = X + (int64_t)(gs % D) * SLOT + (int64_t)r * BLK + (int64_t)grp * N * N + 16 * rw * N;
+            const uint32_t d0 = smem_u32(Rv + 16 * rw * ROW);
+#pragma unroll 4
+            for (int k = 0; k < 16; ++k) {
+                cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
+                cp_async16(d0 + (k * ROW + 32 + lane) * 16, src + k * N + 32 + lane);
+            }
+            cp_async_commit();
+        };
+        auto issue = [&](unsigned gs) {
+            if (lane == 0) spin_geq(ready + gs % D, ARR * (gs / D + 1));
+            __syncwarp();
+            pull(gs);
+        };
+        auto complete = [&](unsigned gs) {
+            cp_async_wait_all();
+            __syncwarp();
+            if (lane == 0) signal_add_relaxed(done + gs % D);
+            named_bar(bar, 128);  // every warp's rows of my plane have landed
+        };
+        if ((int64_t)team < count) issue(0);
+        for (int64_t it = team; it < count; it += nteams, ++ncell) {
+            const int64_t cell = a.list ? a.list[it] : it;
+            const double* fc = a.f + cell * NB;
+            const unsigned gb = ncell * (1 + nfields);
+            const bool more_cells = it + nteams < count;
+            // ---- prologue: forward over k3 of rows (k1 = rP + grp, k2 = pp), F -> TMEM ----
+            complete(gb);
+            {
+                const double2* row = Rv + pp * ROW;
+                const int k1 = r * P + grp, k2 = pp;
+                double2 v[M];
+#pragma unroll
+                for (int j = 0; j < Q; ++j) {
+                    v[j] = row[h * Q + j];
+                    v[Q + j] = row[M + h * Q + j];
+                }
+                fftxh_dif<M, false>(v, h);  // v[m] = F[k3 = 2m + h] (unscaled)
+                const double s = 1.0 / double(NB);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    double w8[8];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        w8[2 * i] = v[4 * c + i].x * s;
+                        w8[2 * i + 1] = v[4 * c + i].y * s;
+                    }
+                    tmem_st16(tmF + 128 * grp + 16 * c, w8);
+                }
+                if (a.nyq) {
+                    constexpr int H = N / 2;
+                    double2* ny = a.nyq + cell * 3 * N * N;
+                    if (h == 0) ny[2 * N * N + k1 * N + k2] = make_double2(s * v[H / 2].x, s * v[H / 2].y);
+                    if (k2 == H) {
+#pragma unroll
+                        for (int m = 0; m < M; ++m)
+                            ny[1 * N * N + k1 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
+                    }
+                    if (k1 == H) {
+#pragma unroll
+                        for (int m = 0; m < M; ++m) ny[k2 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
+                    }
+                }
+                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+                for (int c = 0; c < GCOLS / 16; ++c) tmem_st16(tmG + GCOLS * grp + 16 * c, z);
+                tmem_wait_st();
+                tmem_fence_before();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + grp)) : "memory");
+            }
+            named_bar(bar, 128);  // my group's reads of the buffer are done
+            issue(gb + 1);        // field 1 (needs F of both planes: the other group publishes its own)
+            double mre = 0.0, n2 = 0.0, l2 = 0.0;
+            for (int fi = 1; fi <= nfields; ++fi) {
+                const unsigned gs = gb + fi;
+                complete(gs);
+                {  // rows i1 = pp over i2 (DIF), back in natural order
+                    double2* row = Rv + pp * ROW;
+                    double2 v[M];
+#pragma unroll
+                    for (int j = 0; j < Q; ++j) {
+                        v[j] = row[h * Q + j];
+                        v[Q + j] = row[M + h * Q + j];
+                    }
+                    fftxh_dif<M, true>(v, h);
+                    __syncwarp();
+#pragma unroll
+                    for (int m = 0; m < M; ++m) row[2 * m + h] = v[m];
+                }
+                named_bar(bar, 128);  // columns need every row
+                double2 y[M];
+                const double2* col = Rv + pp;
+#pragma unroll
+                for (int m = 0; m < M; ++m) y[m] = col[(2 * m + h) * ROW];
+                named_bar(bar, 128);  // buffer free: the next field's pull overlaps the transform
+                if (fi < nfields || more_cells) issue(gs + 1);
+                fftxh_dit<M, true>(y, h);  // y[j] = node hQ + j, y[Q + j] = node M + hQ + j
+                const int j3 = r * P + grp;
+                if (fi < nfields) {
+                    const double mu = (fi == 1) ? a.mult0 : 1.0;
+                    uint32_t g0[32], g1[32];
+                    tmem_ld32_nowait(tmG + GCOLS * grp, g0);
+                    tmem_ld32_nowait(tmG + GCOLS * grp + 32, g1);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        double gv[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int k = 16 * (c & 1) + 2 * i;
+                            const double old = (c < 2) ? tmem_pair(g0[k], g0[k + 1]) : tmem_pair(g1[k], g1[k + 1]);
+                            gv[i] = old + mu * (y[8 * c + i].x * y[8 * c + i].y);
+                        }
+                        tmem_st16(tmG + GCOLS * grp + 16 * c, gv);
+                    }
+                    tmem_wait_st();
+                } else {  // loss field: Q = jac (w gain - f loss) at (j1, pp, j3)
+                    double* qc = a.q + cell * NB;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        double gv[8];
+                        tmem_ld16(tmG + GCOLS * grp + 16 * c, gv);
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const int jj = 8 * c + i;
+                            const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
+                            const int64_t gi = ((int64_t)j1 * N + pp) * N + j3;
+                            const double lt = fc[gi] * y[jj].x;
+                            const double qre = a.jac * (a.w * gv[i] - lt);
+                            qc[gi] = qre;
+                            mre = fmax(mre, fabs(qre));
+                            n2 += qre * qre;
+                            l2 += lt * lt;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+                n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+                l2 += __shfl_xor_sync(0xffffffffu, l2, o);
+            }
+            if (lane == 0 && a.st) {
+                hk_cell_status* sc = a.st + cell;
+                atomic_max_nonneg(&sc->max_re, mre);
+                atomicAdd(&sc->q_norm2, n2);
+                atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
+            }
+        }
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
+}
+
 size_t coll64_xchg_bytes(hk_ctx ctx) {
     const int teams = ctx->sm_count / Geo64::C;
     return size_t(teams > 0 ? teams : 1) * Geo64::XCHG_PER_TEAM;
@@ -492,15 +833,18 @@ size_t coll64_xchg_bytes(hk_ctx ctx) {
 
 int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_cells, int tag) {
     using G = Geo64;
-    auto kern = exact ? coll64_kernel<true> : coll64_kernel<false>;
-    const int key = 6400 + (exact ? 1 : 0);
+    static const bool eight = getenv("HK_C64_8W") != nullptr;  // 8-warp FAST kernel for comparison
+    const bool w12 = !exact && !eight;
+    auto kern = exact ? coll64_kernel<true> : (w12 ? coll64_w12_kernel : coll64_kernel<false>);
+    const int nthreads = w12 ? 384 : 256;
+    const int key = 6400 + (exact ? 1 : 0) + (w12 ? 2 : 0);
     int st;
     if (!ctx->max_clusters.count(key)) {
         if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
                              "smem attribute")))
             return st;
         int per_sm = 0;
-        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, G::SMEM), "occupancy")))
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, G::SMEM), "occupancy")))
             return st;
         int teams = per_sm >= 1 ? ctx->sm_count / G::C : 0;
         if (const char* m = getenv("HK_TEAMS64")) teams = atoi(m);  // experiment override (<= sm_count / C)
@@ -519,7 +863,7 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
         return st;
     void* params[] = {&args};
     timing_begin(ctx, tag);
-    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * G::C)), dim3(256), params,
+    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * G::C)), dim3(nthreads), params,
                                                      G::SMEM, ctx->stream),
                     "N = 64 collision kernel launch");
     timing_end(ctx);
