@@ -190,6 +190,31 @@ int hk_imex_combine(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, co
 int hk_axpby(hk_ctx ctx, int64_t count, double* out_dev, const double* x_dev, double a, const double* y_dev, double b,
              const double* z_dev);
 
+/* ---- Layer 0 (compressible Euler) and layer transitions (SURVEY §8f "next") --
+ * Conserved fields are [cell][4] = (rho, rho ux, rho uy, E), cell = j*nx + i,
+ * periodic torus, xi = heat ratio.  Bitwise the reference's arithmetic.
+ * HK_POSITIVITY (lowest failing cell in hk_last_error) where the reference
+ * throws positivity_error; these calls synchronise to report it. */
+/* euler_rhs_periodic (src/euler.cpp:159-170): out = -dF/dx - dG/dy (CWENO3 + local LF). */
+int hk_euler_rhs_periodic(hk_ctx ctx, const double* u_dev, int nx, int ny, double dx, double dy, double xi,
+                          double eps_weno, double* out_dev);
+/* tvd_rk2_step_periodic (src/euler.cpp:172-181), in place; work_dev: 8 nx ny doubles or NULL. */
+int hk_euler_tvd_rk2_step(hk_ctx ctx, double* u_dev, int nx, int ny, double dx, double dy, double dt, double xi,
+                          double eps_weno, double* work_dev);
+/* convert_on_transition 0 -> 1 (src/regime.cpp:62-65): f = maxwellian(moments_from_conserved(u)). */
+int hk_conserved_to_maxwellian(hk_ctx ctx, int n, double vmax, const double* u_dev, int64_t ncells, double heat_ratio,
+                               double* f_dev);
+/* convert_on_transition 1 -> 0 (src/regime.cpp:66-70): u = conserved_from_moments(moments_of(f));
+ * HK_DEGENERATE as moments_of. */
+int hk_distribution_to_conserved(hk_ctx ctx, int n, double vmax, const double* f_dev, int64_t ncells,
+                                 double heat_ratio, double* u_dev);
+/* Dynamic packing of a regime's cells into a dense batch and back (nb doubles per
+ * cell, nb even): dst[k] = src[idx[k]] / dst[idx[k]] = src[k]. */
+int hk_gather_cells(hk_ctx ctx, int64_t nb, const double* src_dev, const int64_t* idx_dev, int64_t count,
+                    double* dst_dev);
+int hk_scatter_cells(hk_ctx ctx, int64_t nb, const double* src_dev, const int64_t* idx_dev, int64_t count,
+                     double* dst_dev);
+
 /* ---- multi-GPU: NCCL communicator of a context ------------
  * One process per GPU.  Rank 0 calls hk_comm_unique_id, the host side ships
  * the 128 opaque bytes to every rank (MPI / torch.distributed / a file), and

@@ -1201,3 +1201,152 @@ void hko_transport_rhs_periodic(const double* f, int nx, int ny, int n, double v
             hko_transport_rhs_cell(fx, fy, n, vmax, dx, dy, eps_weno, out + (j * nx + i) * nb);
         }
 }
+
+
+/* ===================================================================== */
+/* Layer-0 Euler (src/euler.cpp:54-189), statement order kept            */
+/* ===================================================================== */
+typedef struct { double rho, ux, uy, p; } HkoPrim;
+
+static int hko_to_primitive(const double* u, double xi, HkoPrim* q) {  /* :66-82 */
+    if (!(u[0] > 0.0)) return HKO_POSITIVITY;
+    const double p = (xi - 1.0) * (u[3] - 0.5 * (u[1] * u[1] + u[2] * u[2]) / u[0]);
+    if (!(p > 0.0)) return HKO_POSITIVITY;
+    q->rho = u[0];
+    q->p = p;
+    q->ux = u[1] / u[0];
+    q->uy = u[2] / u[0];
+    return 0;
+}
+
+static void hko_to_conserved(const HkoPrim* p, double xi, double u[4]) {  /* :84-91 */
+    u[0] = p->rho;
+    u[1] = p->rho * p->ux;
+    u[2] = p->rho * p->uy;
+    u[3] = p->p / (xi - 1.0) + 0.5 * p->rho * (p->ux * p->ux + p->uy * p->uy);
+}
+
+static int hko_euler_flux(const double u[4], int axis, double xi, double f[4]) {  /* :95-108 */
+    if (!(u[0] > 0.0)) return HKO_POSITIVITY;
+    const double p = (xi - 1.0) * (u[3] - 0.5 * (u[1] * u[1] + u[2] * u[2]) / u[0]);
+    if (!(p > 0.0)) return HKO_POSITIVITY;
+    const double un = (axis == 0 ? u[1] : u[2]) / u[0];
+    f[0] = u[0] * un;
+    f[1] = u[1] * un;
+    f[2] = u[2] * un;
+    if (axis == 0) f[1] += p;
+    else f[2] += p;
+    f[3] = un * (u[3] + p);
+    return 0;
+}
+
+static int hko_face_flux(const HkoPrim* q0, const HkoPrim* q1, const HkoPrim* q2, const HkoPrim* q3,
+                         int axis, double xi, double eps, double out[4]) {  /* :124-141 */
+    HkoPrim l, r;
+    double dum;
+    hko_cweno3(q0->rho, q1->rho, q2->rho, eps, &dum, &l.rho);
+    hko_cweno3(q0->ux, q1->ux, q2->ux, eps, &dum, &l.ux);
+    hko_cweno3(q0->uy, q1->uy, q2->uy, eps, &dum, &l.uy);
+    hko_cweno3(q0->p, q1->p, q2->p, eps, &dum, &l.p);
+    hko_cweno3(q1->rho, q2->rho, q3->rho, eps, &r.rho, &dum);
+    hko_cweno3(q1->ux, q2->ux, q3->ux, eps, &r.ux, &dum);
+    hko_cweno3(q1->uy, q2->uy, q3->uy, eps, &r.uy, &dum);
+    hko_cweno3(q1->p, q2->p, q3->p, eps, &r.p, &dum);
+    if (!(l.rho > 0.0) || !(l.p > 0.0) || !(r.rho > 0.0) || !(r.p > 0.0)) return HKO_POSITIVITY;
+    /* max_wave_speed (:110-114) */
+    const double ul = axis == 0 ? l.ux : l.uy, ur = axis == 0 ? r.ux : r.uy;
+    const double cl = sqrt(xi * l.p / l.rho), cr = sqrt(xi * r.p / r.rho);
+    const double a = fmax(fabs(ul) + cl, fabs(ur) + cr);
+    double uL[4], uR[4], fl[4], fr[4];
+    hko_to_conserved(&l, xi, uL);
+    hko_to_conserved(&r, xi, uR);
+    /* lax_friedrichs_flux (:116-121): 0.5 (fl + fr) - (0.5 a)(ur - ul) */
+    int s = hko_euler_flux(uL, axis, xi, fl);
+    if (s) return s;
+    s = hko_euler_flux(uR, axis, xi, fr);
+    if (s) return s;
+    for (int k = 0; k < 4; ++k) out[k] = 0.5 * (fl[k] + fr[k]) - (0.5 * a) * (uR[k] - uL[k]);
+    return 0;
+}
+
+int hko_euler_rhs_periodic(const double* u, int nx, int ny, double dx, double dy, double xi,
+                           double eps_weno, double* out, long* bad_cell) {
+    const long cells = (long)nx * ny;
+    HkoPrim* q = malloc(sizeof(HkoPrim) * cells);
+    int first = 0;
+    if (bad_cell) *bad_cell = -1;
+    for (long c = 0; c < cells; ++c) {
+        const int s = hko_to_primitive(u + 4 * c, xi, q + c);
+        if (s && !first) {
+            first = s;
+            if (bad_cell) *bad_cell = c;
+        }
+    }
+    if (first) {
+        free(q);
+        return first;
+    }
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            const HkoPrim* px[5];
+            const HkoPrim* py[5];
+            for (int k = -2; k <= 2; ++k) {
+                px[k + 2] = q + (long)j * nx + wrapi(i + k, nx);
+                py[k + 2] = q + (long)wrapi(j + k, ny) * nx + i;
+            }
+            double fxp[4], fxm[4], fyp[4], fym[4];
+            int s = hko_face_flux(px[1], px[2], px[3], px[4], 0, xi, eps_weno, fxp);
+            if (!s) s = hko_face_flux(px[0], px[1], px[2], px[3], 0, xi, eps_weno, fxm);
+            if (!s) s = hko_face_flux(py[1], py[2], py[3], py[4], 1, xi, eps_weno, fyp);
+            if (!s) s = hko_face_flux(py[0], py[1], py[2], py[3], 1, xi, eps_weno, fym);
+            const long c = (long)j * nx + i;
+            if (s) {
+                if (!first) {
+                    first = s;
+                    if (bad_cell) *bad_cell = c;
+                }
+                continue;
+            }
+            for (int k = 0; k < 4; ++k) out[4 * c + k] = -(fxp[k] - fxm[k]) / dx - (fyp[k] - fym[k]) / dy;
+        }
+    free(q);
+    return first;
+}
+
+int hko_tvd_rk2_step_periodic(double* u, int nx, int ny, double dx, double dy, double dt,
+                              double xi, double eps_weno, long* bad_cell) {
+    const long n4 = 4L * nx * ny;
+    double* l1 = malloc(sizeof(double) * n4);
+    double* u1 = malloc(sizeof(double) * n4);
+    int s = hko_euler_rhs_periodic(u, nx, ny, dx, dy, xi, eps_weno, l1, bad_cell);
+    if (!s) {
+        for (long i = 0; i < n4; ++i) u1[i] = u[i] + dt * l1[i];
+        s = hko_euler_rhs_periodic(u1, nx, ny, dx, dy, xi, eps_weno, l1, bad_cell);
+        if (!s)
+            for (long i = 0; i < n4; ++i) u[i] = 0.5 * u[i] + 0.5 * u1[i] + (0.5 * dt) * l1[i];
+    }
+    free(l1);
+    free(u1);
+    return s;
+}
+
+int hko_moments_from_conserved(const double u[4], double heat_ratio, double mom5[5]) {
+    if (!(u[0] > 0.0)) return HKO_POSITIVITY;
+    const double p = (heat_ratio - 1.0) * (u[3] - 0.5 * (u[1] * u[1] + u[2] * u[2]) / u[0]);
+    if (!(p > 0.0)) return HKO_POSITIVITY;
+    mom5[0] = u[0];
+    mom5[1] = u[1] / u[0];
+    mom5[2] = u[2] / u[0];
+    mom5[3] = 0.0;
+    mom5[4] = p / u[0];
+    return 0;
+}
+
+void hko_conserved_from_moments(const double mom5[5], double heat_ratio, double u[4]) {
+    const double rho = mom5[0];
+    u[0] = rho;
+    u[1] = rho * mom5[1];
+    u[2] = rho * mom5[2];
+    const double u2 = mom5[1] * mom5[1] + mom5[2] * mom5[2] + mom5[3] * mom5[3];
+    u[3] = rho * mom5[4] / (heat_ratio - 1.0) + 0.5 * rho * u2;
+}

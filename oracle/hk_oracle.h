@@ -152,6 +152,18 @@ void hko_transport_rhs_cell(const double* const fx[5], const double* const fy[5]
 void hko_transport_rhs_periodic(const double* f, int nx, int ny, int n, double vmax, double dx,
                                 double dy, double eps_weno, double* out);
 
+/* ---------------- Layer-0 Euler (src/euler.cpp:67-189) ---------------- */
+/* u, out: [cell][4] = (rho, mx, my, E), cell = j*nx + i, periodic torus.
+ * Returns HKO_POSITIVITY (and *bad_cell) on a non-positive density / pressure
+ * of a cell state or of a reconstructed face state, as the reference throws. */
+int hko_euler_rhs_periodic(const double* u, int nx, int ny, double dx, double dy, double xi,
+                           double eps_weno, double* out, long* bad_cell);        /* :159-170 */
+int hko_tvd_rk2_step_periodic(double* u, int nx, int ny, double dx, double dy, double dt,
+                              double xi, double eps_weno, long* bad_cell);      /* :172-181 */
+/* Transitions (src/coupling.cpp:7-22, src/regime.cpp:54-72) */
+int hko_moments_from_conserved(const double u[4], double heat_ratio, double mom5[5]);
+void hko_conserved_from_moments(const double mom5[5], double heat_ratio, double u[4]);
+
 #ifdef __cplusplus
 }
 #endif

@@ -232,6 +232,34 @@ class Oracle:
                                             C.c_double(dy), C.c_double(eps_weno), _ptr(out))
         return out
 
+    # ---- Layer-0 Euler (src/euler.cpp:159-181), transitions (src/coupling.cpp:7-22) ----
+    def euler_rhs_periodic(self, u, nx, ny, dx, dy, xi=5.0 / 3.0, eps_weno=1e-6):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros_like(u)
+        bad = C.c_long(-1)
+        st = self.lib.hko_euler_rhs_periodic(_ptr(u), nx, ny, C.c_double(dx), C.c_double(dy), C.c_double(xi),
+                                             C.c_double(eps_weno), _ptr(out), C.byref(bad))
+        return st, out, bad.value
+
+    def tvd_rk2_step_periodic(self, u, nx, ny, dx, dy, dt, xi=5.0 / 3.0, eps_weno=1e-6):
+        u = np.ascontiguousarray(u, dtype=np.float64).copy()
+        bad = C.c_long(-1)
+        st = self.lib.hko_tvd_rk2_step_periodic(_ptr(u), nx, ny, C.c_double(dx), C.c_double(dy), C.c_double(dt),
+                                                C.c_double(xi), C.c_double(eps_weno), C.byref(bad))
+        return st, u
+
+    def moments_from_conserved(self, u4, heat_ratio=5.0 / 3.0):
+        u4 = np.ascontiguousarray(u4, dtype=np.float64)
+        m = np.zeros(5)
+        st = self.lib.hko_moments_from_conserved(_ptr(u4), C.c_double(heat_ratio), _ptr(m))
+        return st, m
+
+    def conserved_from_moments(self, mom5, heat_ratio=5.0 / 3.0):
+        mom5 = np.ascontiguousarray(mom5, dtype=np.float64)
+        u = np.zeros(4)
+        self.lib.hko_conserved_from_moments(_ptr(mom5), C.c_double(heat_ratio), _ptr(u))
+        return u
+
     def penalized_imex_step(self, k: OracleKernel, f, nx, ny, dx, dy, dt, eps_cell,
                             pen_coeff=2 * np.pi, eps_weno=1e-6):
         f = np.ascontiguousarray(f, dtype=np.float64).copy()
@@ -396,6 +424,32 @@ class RefLib:
         self.lib.href_transport_rhs_periodic(n, C.c_double(vmax), _ptr(f), nx, ny, C.c_double(dx),
                                              C.c_double(dy), C.c_double(eps_weno), _ptr(out))
         return out
+
+    # ---- Layer-0 Euler and transitions, the reference's own code ----
+    def euler_rhs_periodic(self, u, nx, ny, dx, dy, xi=5.0 / 3.0, eps_weno=1e-6):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros_like(u)
+        st = self.lib.href_euler_rhs_periodic(_ptr(u), nx, ny, C.c_double(dx), C.c_double(dy), C.c_double(xi),
+                                              C.c_double(eps_weno), _ptr(out))
+        return st, out
+
+    def tvd_rk2_step_periodic(self, u, nx, ny, dx, dy, dt, xi=5.0 / 3.0, eps_weno=1e-6):
+        u = np.ascontiguousarray(u, dtype=np.float64).copy()
+        st = self.lib.href_tvd_rk2_step_periodic(_ptr(u), nx, ny, C.c_double(dx), C.c_double(dy), C.c_double(dt),
+                                                 C.c_double(xi), C.c_double(eps_weno))
+        return st, u
+
+    def moments_from_conserved(self, u4, heat_ratio=5.0 / 3.0):
+        u4 = np.ascontiguousarray(u4, dtype=np.float64)
+        m = np.zeros(5)
+        st = self.lib.href_moments_from_conserved(_ptr(u4), C.c_double(heat_ratio), _ptr(m))
+        return st, m
+
+    def conserved_from_moments(self, mom5, heat_ratio=5.0 / 3.0):
+        mom5 = np.ascontiguousarray(mom5, dtype=np.float64)
+        u = np.zeros(4)
+        self.lib.href_conserved_from_moments(_ptr(mom5), C.c_double(heat_ratio), _ptr(u))
+        return u
 
     def penalized_imex_step(self, k: RefKernel, f, nx, ny, dx, dy, dt, eps_cell,
                             pen_coeff=2 * np.pi, eps_weno=1e-6):

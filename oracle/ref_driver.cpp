@@ -22,6 +22,8 @@
 #include <vector>
 
 #include "hykin/boltzmann.hpp"
+#include "hykin/coupling.hpp"
+#include "hykin/euler.hpp"
 #include "hykin/errors.hpp"
 #include "hykin/esbgk.hpp"
 #include "hykin/indicators.hpp"
@@ -429,6 +431,66 @@ int href_penalized_imex_step(void* p, double* f, int nx, int ny, double dx, doub
     } catch (...) {
         return status_of(std::current_exception());
     }
+}
+
+// ---- Layer-0 Euler (src/euler.cpp:159-181) and transitions (src/coupling.cpp:7-22) ----
+static ConservedField to_field(const double* u, int cells) {
+    ConservedField f(cells);
+    for (int c = 0; c < cells; ++c)
+        for (int k = 0; k < 4; ++k) f[c][k] = u[4 * c + k];
+    return f;
+}
+
+int href_euler_rhs_periodic(const double* u, int nx, int ny, double dx, double dy, double xi,
+                            double eps_weno, double* out) {
+    try {
+        EulerScheme s;
+        s.xi = xi;
+        s.eps_weno = eps_weno;
+        const ConservedField r = euler_rhs_periodic(to_field(u, nx * ny), nx, ny, dx, dy, s);
+        for (int c = 0; c < nx * ny; ++c)
+            for (int k = 0; k < 4; ++k) out[4 * c + k] = r[c][k];
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_tvd_rk2_step_periodic(double* u, int nx, int ny, double dx, double dy, double dt, double xi,
+                               double eps_weno) {
+    try {
+        EulerScheme s;
+        s.xi = xi;
+        s.eps_weno = eps_weno;
+        ConservedField f = to_field(u, nx * ny);
+        tvd_rk2_step_periodic(f, nx, ny, dx, dy, dt, s);
+        for (int c = 0; c < nx * ny; ++c)
+            for (int k = 0; k < 4; ++k) u[4 * c + k] = f[c][k];
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+int href_moments_from_conserved(const double* u, double heat_ratio, double* mom5) {
+    try {
+        ConservedState c;
+        for (int k = 0; k < 4; ++k) c[k] = u[k];
+        const Moments m = moments_from_conserved(c, heat_ratio);
+        mom5[0] = m.rho; mom5[1] = m.u.x(); mom5[2] = m.u.y(); mom5[3] = m.u.z(); mom5[4] = m.T;
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+void href_conserved_from_moments(const double* mom5, double heat_ratio, double* u) {
+    Moments m;
+    m.rho = mom5[0];
+    m.u = Eigen::Vector3d(mom5[1], mom5[2], mom5[3]);
+    m.T = mom5[4];
+    const ConservedState c = conserved_from_moments(m, heat_ratio);
+    for (int k = 0; k < 4; ++k) u[k] = c[k];
 }
 
 } // extern "C"

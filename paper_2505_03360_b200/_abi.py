@@ -95,6 +95,12 @@ def lib() -> C.CDLL:
         "hk_axpby": (C.c_int, [vp, i64, vp, vp, dbl, vp, dbl, vp]),
         "hk_transport_rhs_slab": (C.c_int, [vp, C.c_int, dbl, vp, vp, vp, vp, C.c_int, C.c_int, dbl, dbl, dbl]),
         "hk_imex_combine": (C.c_int, [vp, C.c_int, i64, i64, dbl, vp, vp, vp, vp, vp, vp, vp, vp]),
+        "hk_euler_rhs_periodic": (C.c_int, [vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, dbl, vp]),
+        "hk_euler_tvd_rk2_step": (C.c_int, [vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, dbl, dbl, vp]),
+        "hk_conserved_to_maxwellian": (C.c_int, [vp, C.c_int, dbl, vp, i64, dbl, vp]),
+        "hk_distribution_to_conserved": (C.c_int, [vp, C.c_int, dbl, vp, i64, dbl, vp]),
+        "hk_gather_cells": (C.c_int, [vp, i64, vp, vp, i64, vp]),
+        "hk_scatter_cells": (C.c_int, [vp, i64, vp, vp, i64, vp]),
         "hk_comm_unique_id": (C.c_int, [vp]),
         "hk_ctx_comm_init": (C.c_int, [vp, C.c_int, C.c_int, vp]),
         "hk_ctx_comm_info": (C.c_int, [vp, vp, vp]),

@@ -37,6 +37,8 @@ struct hk_ctx_s {
     int64_t sio_flags_n = 0;
     int64_t* last_list = nullptr;
     int* last_count = nullptr;
+    // lowest failing cell of the Euler / transition kernels (hk_euler.cu)
+    void* bad_flag = nullptr;
     // work fields of the device-resident IMEX steps (hk_steps.cu)
     void* step_work = nullptr;
     size_t step_bytes = 0;

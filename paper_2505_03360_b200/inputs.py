@@ -291,3 +291,35 @@ def config5_slab_torch(i0: int = 224, nxl: int = 64, ny: int = 128, n: int = 64,
         c1 = min(c0 + 512, ny * nxl)
         torch.addcmul(torch.outer(b[c0:c1], md), a[c0:c1, None], mu[None, :], out=f[c0:c1])
     return f
+
+
+# ---------------------------------------------------------------------------
+# Layer-0 states (config 4: quadrant Riemann problem, SURVEY §8d), seeded.
+# ---------------------------------------------------------------------------
+def config4_conserved(nx: int = 200, ny: int = 200, xi: float = 5.0 / 3.0, seed_salt: int = 0,
+                      smooth: bool = True) -> np.ndarray:
+    """[nx*ny, 4] conserved (rho, rho ux, rho uy, E) of config 4's quadrants
+    (rho {1, .125, .5, .25}, T {1, .8, 1, .5}, p = rho T, u = 0); with
+    `smooth` the quadrant edges are tanh-smoothed over 2 cells and a 1 %
+    seeded velocity perturbation is added (so every flux term is active)."""
+    rng = rng_for(4, seed_salt)
+    x = (np.arange(nx) + 0.5) / nx
+    y = (np.arange(ny) + 0.5) / ny
+    X, Y = np.meshgrid(x, y)  # [ny, nx]
+    rq = np.array([1.0, 0.125, 0.5, 0.25])
+    tq = np.array([1.0, 0.8, 1.0, 0.5])
+    if smooth:
+        w = 2.0 / nx
+        sx = 0.5 * (1 + np.tanh((X - 0.5) / w))
+        sy = 0.5 * (1 + np.tanh((Y - 0.5) / w))
+    else:
+        sx = (X > 0.5).astype(float)
+        sy = (Y > 0.5).astype(float)
+    wts = [(1 - sx) * (1 - sy), sx * (1 - sy), (1 - sx) * sy, sx * sy]
+    rho = sum(wq * r for wq, r in zip(wts, rq))
+    T = sum(wq * t for wq, t in zip(wts, tq))
+    ux = 0.01 * rng.uniform(-1, 1, rho.shape)
+    uy = 0.01 * rng.uniform(-1, 1, rho.shape)
+    p = rho * T
+    E = p / (xi - 1.0) + 0.5 * rho * (ux * ux + uy * uy)
+    return np.stack([rho, rho * ux, rho * uy, E], -1).reshape(nx * ny, 4)

@@ -202,3 +202,63 @@ def penalized_imex_step(f, nx, ny, kernel: SpectralKernel, dx, dy, dt, eps_cell,
     ctx.check(ctx._lib.hk_penalized_imex_step(ctx.h, kernel.h, f.data_ptr(), nx, ny, dx, dy, dt, e.data_ptr(),
                                               rule.coeff, eps_weno, _abi.HK_COLL_EXACT if exact else 0, None))
     return f
+
+
+# ---------------------------------------------------------------------------
+# Layer 0 (compressible Euler) and layer transitions (SURVEY §8f "next")
+# ---------------------------------------------------------------------------
+def euler_rhs_periodic(u, nx: int, ny: int, dx: float, dy: float, xi: float = 5.0 / 3.0, eps_weno: float = 1e-6,
+                       ctx=None):
+    """euler_rhs_periodic (src/euler.cpp:159-170): u [nx*ny, 4] conserved -> rhs."""
+    ctx = ctx or default_context(u.device.index or 0)
+    u = u.contiguous()
+    out = torch.empty_like(u)
+    ctx.check(ctx._lib.hk_euler_rhs_periodic(ctx.h, u.data_ptr(), nx, ny, dx, dy, xi, eps_weno, out.data_ptr()))
+    return out
+
+
+def tvd_rk2_step_periodic(u, nx: int, ny: int, dx: float, dy: float, dt: float, xi: float = 5.0 / 3.0,
+                          eps_weno: float = 1e-6, ctx=None):
+    """tvd_rk2_step_periodic (src/euler.cpp:172-181), in place on the device field."""
+    ctx = ctx or default_context(u.device.index or 0)
+    assert u.is_contiguous()
+    ctx.check(ctx._lib.hk_euler_tvd_rk2_step(ctx.h, u.data_ptr(), nx, ny, dx, dy, dt, xi, eps_weno, None))
+    return u
+
+
+def conserved_to_maxwellian(u, vgrid: VelocityGrid, heat_ratio: float = 5.0 / 3.0, ctx=None):
+    """Layer 0 -> 1 (src/regime.cpp:62-65): Maxwellian of each cell's hydro state."""
+    ctx = ctx or default_context(u.device.index or 0)
+    u = u.contiguous()
+    nc = u.shape[0]
+    f = torch.empty((nc, vgrid.nv ** 3), dtype=torch.float64, device=u.device)
+    ctx.check(ctx._lib.hk_conserved_to_maxwellian(ctx.h, vgrid.nv, vgrid.vmax, u.data_ptr(), nc, heat_ratio, f.data_ptr()))
+    return f
+
+
+def distribution_to_conserved(f, vgrid: VelocityGrid, heat_ratio: float = 5.0 / 3.0, ctx=None):
+    """Layer 1 -> 0 (src/regime.cpp:66-70): hydro state of each cell's moments."""
+    ctx = ctx or default_context(f.device.index or 0)
+    f, nc = _cells(f, vgrid.nv)
+    u = torch.empty((nc, 4), dtype=torch.float64, device=f.device)
+    ctx.check(ctx._lib.hk_distribution_to_conserved(ctx.h, vgrid.nv, vgrid.vmax, f.data_ptr(), nc, heat_ratio,
+                                                    u.data_ptr()))
+    return u
+
+
+def gather_cells(src, idx, ctx=None):
+    """Dense batch of the cells `idx` (int64 device tensor) of a cell-major slab."""
+    ctx = ctx or default_context(src.device.index or 0)
+    idx = idx.to(device=src.device, dtype=torch.int64).contiguous()
+    dst = torch.empty((idx.numel(), src.shape[1]), dtype=src.dtype, device=src.device)
+    ctx.check(ctx._lib.hk_gather_cells(ctx.h, src.shape[1], src.data_ptr(), idx.data_ptr(), idx.numel(), dst.data_ptr()))
+    return dst
+
+
+def scatter_cells(src, idx, dst, ctx=None):
+    """dst[idx[k]] = src[k] (the inverse of gather_cells), in place on `dst`."""
+    ctx = ctx or default_context(src.device.index or 0)
+    idx = idx.to(device=src.device, dtype=torch.int64).contiguous()
+    ctx.check(ctx._lib.hk_scatter_cells(ctx.h, src.shape[1], src.contiguous().data_ptr(), idx.data_ptr(), idx.numel(),
+                                        dst.data_ptr()))
+    return dst
