@@ -17,6 +17,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
+import numpy as np
 import torch
 
 import paper_2505_03360_b200 as hk
@@ -116,6 +117,48 @@ def config3(iters, nx=256, ny=256):
     return out
 
 
+def config4(iters):
+    """Config 4 pieces on one GPU: the layer-0 Euler TVD-RK2 step on the
+    200 x 200 quadrant field, and Q (N = 32, M = 4 x 8) for the ~19 % band
+    cells (eps = 0.1 within 0.025 of x = 0.5, y = 0.5 and the periodic wrap
+    lines) gathered into a dense batch, the Boltzmann part of a hybrid step."""
+    nx = ny = 200
+    ud = torch.from_numpy(inputs.config4_conserved(nx, ny)).cuda()
+    dx = 1.0 / nx
+
+    def eul():
+        kinetic.tvd_rk2_step_periodic(ud, nx, ny, dx, dx, 0.1 * dx)
+
+    t_e = timed(eul, iters)
+    x = (np.arange(nx) + 0.5) * dx
+    near = lambda z: (np.abs(z - 0.5) < 0.025) | (z < 0.025) | (z > 1 - 0.025)
+    X, Y = np.meshgrid(x, x)
+    band = np.flatnonzero((near(X) | near(Y)).ravel())
+    n, a1, a2 = 32, 4, 8
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    k = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    f = kinetic.conserved_to_maxwellian(ud, vg)  # layer 0 -> 1 for every cell
+    f += 0.05 * torch.roll(f, 1, 0)  # non-equilibrium band content
+    idx = torch.from_numpy(band).cuda()
+    res = {}
+
+    def coll():
+        g = kinetic.gather_cells(f, idx)
+        res["q"] = hk.spectral_collision(g, k)
+        kinetic.scatter_cells(res["q"], idx, f)
+
+    t_q = timed(coll, iters)
+    md = (a1 - 1) * a2 + 1
+    W = (2 * md + 2) * 5 * n ** 3 * math.log2(n ** 3) + (12 * md + 10) * n ** 3
+    ach = W * len(band) / (t_q * 1e-3) / 1e12
+    return {"config": "config4: 200x200 quadrant Riemann problem; Euler layer on all cells, Boltzmann Q (N=32, M=4x8) "
+                      "on the eps band", "band_cells": int(len(band)), "ms": {"euler_tvd_rk2_step": t_e,
+                                                                               "band_collision_gather_scatter": t_q},
+            "euler_cell_steps_per_s": nx * ny / (t_e * 1e-3), "band_cell_updates_per_s": len(band) / (t_q * 1e-3),
+            "roofline": {"bound": "fp64", "collision_achieved_tflops": ach,
+                         "collision_frac": ach / hk.default_context().fp64_peak_tflops()}}
+
+
 def config5(iters, steps=True):
     """Config 5, one GPU's x-slab (64 x 128 cells, N = 64, M = 8 x 8): Q over
     the slab (fast path + guard) and, with `steps`, one PR(2,2,2) IMEX step of
@@ -168,6 +211,8 @@ if __name__ == "__main__":
     for c in args.configs.split(","):
         if c == "1":
             r = config1(args.iters)
+        elif c == "4":
+            r = config4(args.iters)
         elif c == "5":
             r = config5(args.iters, steps=not args.no_steps)
         else:
