@@ -230,6 +230,20 @@ int hk_ctx_comm_info(hk_ctx ctx, int* nranks, int* rank);
  * (periodic over ranks), each [ny][2][n^3] — the layout hk_transport_rhs_slab reads. */
 int hk_halo_exchange(hk_ctx ctx, int n, const double* f_dev, int64_t nx_local, int64_t ny, double* left_dev,
                      double* right_dev);
+/* Halo-free variant over NVLink / NVSwitch peer memory: the transport kernel
+ * reads the two ghost columns straight from the neighbour ranks' slabs
+ * ([ny][left_nx][n^3], last two columns; [ny][right_nx][n^3], first two),
+ * mapped into this process with hk_ipc_open.  No exchange step; the caller
+ * orders the neighbours' writes before the call (stream sync + barrier). */
+int hk_transport_rhs_peer(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_slab_dev,
+                          int left_nx, const double* right_slab_dev, int right_nx, double* out_dev, int nx, int ny,
+                          double dx, double dy, double eps_weno);
+/* CUDA IPC of a device buffer (64-byte handle): export on the owner, open on a
+ * peer; the opened pointer is the allocation base, add *offset_out (nullable). */
+#define HK_IPC_HANDLE_BYTES 64
+int hk_ipc_handle(hk_ctx ctx, const void* dev_ptr, void* handle_out /* HK_IPC_HANDLE_BYTES */, int64_t* offset_out);
+int hk_ipc_open(hk_ctx ctx, const void* handle, void** dev_ptr_out);
+int hk_ipc_close(hk_ctx ctx, void* dev_ptr);
 /* In-place all-reduce of `count` doubles over the context's ranks: regime counts,
  * conservation sums (HK_REDUCE_SUM), CFL / residual maxima (HK_REDUCE_MAX). */
 #define HK_REDUCE_SUM 0

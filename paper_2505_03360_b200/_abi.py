@@ -25,6 +25,7 @@ HK_POSITIVITY = 8
 HK_UNSUPPORTED = 9
 
 HK_COMM_ID_BYTES = 128
+HK_IPC_HANDLE_BYTES = 64
 HK_REDUCE_SUM = 0
 HK_REDUCE_MAX = 1
 
@@ -101,6 +102,11 @@ def lib() -> C.CDLL:
         "hk_distribution_to_conserved": (C.c_int, [vp, C.c_int, dbl, vp, i64, dbl, vp]),
         "hk_gather_cells": (C.c_int, [vp, i64, vp, vp, i64, vp]),
         "hk_scatter_cells": (C.c_int, [vp, i64, vp, vp, i64, vp]),
+        "hk_transport_rhs_peer": (C.c_int, [vp, C.c_int, dbl, vp, vp, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int,
+                                            dbl, dbl, dbl]),
+        "hk_ipc_handle": (C.c_int, [vp, vp, vp, C.POINTER(C.c_int64)]),
+        "hk_ipc_open": (C.c_int, [vp, vp, C.POINTER(C.c_void_p)]),
+        "hk_ipc_close": (C.c_int, [vp, vp]),
         "hk_comm_unique_id": (C.c_int, [vp]),
         "hk_ctx_comm_init": (C.c_int, [vp, C.c_int, C.c_int, vp]),
         "hk_ctx_comm_info": (C.c_int, [vp, vp, vp]),

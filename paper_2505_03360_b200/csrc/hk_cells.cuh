@@ -25,8 +25,13 @@ struct TransportParams {
     int n;
     double vmax;
     int nx, ny;      // output (interior) cells
-    int x_halo;      // 0: periodic in x; >= 2: input carries x_halo ghost columns per side
+    int x_halo;      // 0: periodic in x; >= 2: input carries x_halo ghost columns per side;
+                     // -2: ghost columns come from the lh / rh slabs below
     double dx, dy, eps_weno;
+    // x_halo == -2: lh / rh are [ny][lnx][n^3] / [ny][rnx][n^3] slabs whose LAST two /
+    // FIRST two columns are the ghosts: 2 for separate halo buffers, the neighbour's
+    // nx when lh / rh point straight at the neighbour rank's slab (NVLink peer memory)
+    int lnx = 2, rnx = 2;
 };
 
 // Final PR(2,2,2) combination fused into the second transport of a step

@@ -12,6 +12,7 @@
 // slab f [ny][nx_local][n^3]; left halo = the left neighbour's last two
 // columns, right halo = the right neighbour's first two, [ny][2][n^3] each,
 // periodic over ranks (rank +- 1 mod nranks; one rank wraps onto itself).
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -140,6 +141,49 @@ int hk_allreduce_scalars(hk_ctx ctx, double* buf_dev, int64_t count, int op) {
                       nccl().AllReduce(buf_dev, buf_dev, (size_t)count, ncclFloat64, op == HK_REDUCE_SUM ? ncclSum : ncclMax,
                                        static_cast<ncclComm_t>(ctx->comm), ctx->stream),
                       "ncclAllReduce");
+}
+
+// ---- CUDA IPC: another rank's device buffer mapped into this process ----
+// A handle names the whole allocation; a pointer inside a sub-allocating pool
+// (PyTorch's caching allocator) also needs its offset from the allocation base
+// (driver cuMemGetAddressRange, resolved through the runtime's entry points).
+int hk_ipc_handle(hk_ctx ctx, const void* dev_ptr, void* handle_out, int64_t* offset_out) {
+    if (!dev_ptr || !handle_out) return fail(ctx, HK_CONTRACT, "hk_ipc_handle: null pointer");
+    cudaSetDevice(ctx->device);
+    cudaIpcMemHandle_t h;
+    int st = check_cuda(ctx, cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)), "cudaIpcGetMemHandle");
+    if (st) return st;
+    std::memcpy(handle_out, &h, sizeof h);
+    if (offset_out) {
+        using Pfn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static Pfn range = nullptr;
+        if (!range) {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess || !fn)
+                return fail(ctx, HK_CUDA, "cuMemGetAddressRange unavailable");
+            range = reinterpret_cast<Pfn>(fn);
+        }
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (range(&base, &size, (CUdeviceptr)dev_ptr) != CUDA_SUCCESS) return fail(ctx, HK_CUDA, "cuMemGetAddressRange");
+        *offset_out = (int64_t)((CUdeviceptr)dev_ptr - base);
+    }
+    return HK_OK;
+}
+
+int hk_ipc_open(hk_ctx ctx, const void* handle, void** dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return fail(ctx, HK_CONTRACT, "hk_ipc_open: null pointer");
+    cudaSetDevice(ctx->device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    return check_cuda(ctx, cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int hk_ipc_close(hk_ctx ctx, void* dev_ptr) {
+    cudaSetDevice(ctx->device);
+    return check_cuda(ctx, cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
 }
 
 int hk_ctx_comm_info(hk_ctx ctx, int* nranks, int* rank) {

@@ -143,9 +143,9 @@ __global__ void __launch_bounds__(256) transport_kernel(TransportParams p, const
             int ii = i + q;
             const int jj = ((j + q) % p.ny + p.ny) % p.ny;
             if (p.x_halo < 0 && ii < 0)
-                sx[q + 2] = lh[((int64_t)j * 2 + (ii + 2)) * nb + idx];
+                sx[q + 2] = lh[((int64_t)j * p.lnx + (p.lnx + ii)) * nb + idx];
             else if (p.x_halo < 0 && ii >= p.nx)
-                sx[q + 2] = rh[((int64_t)j * 2 + (ii - p.nx)) * nb + idx];
+                sx[q + 2] = rh[((int64_t)j * p.rnx + (ii - p.nx)) * nb + idx];
             else {
                 if (p.x_halo == 0) ii = (ii % p.nx + p.nx) % p.nx;
                 else ii += xh;

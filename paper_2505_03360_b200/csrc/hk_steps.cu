@@ -217,6 +217,18 @@ int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int n
                      work_dev);
 }
 
+int hk_transport_rhs_peer(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_slab_dev,
+                          int left_nx, const double* right_slab_dev, int right_nx, double* out_dev, int nx, int ny,
+                          double dx, double dy, double eps_weno) {
+    if (left_nx < 2 || right_nx < 2 || !left_slab_dev || !right_slab_dev)
+        return fail(ctx, HK_CONTRACT, "transport_rhs_peer: neighbour slabs need >= 2 columns");
+    cudaSetDevice(ctx->device);
+    TransportParams p{n, vmax, nx, ny, -2, dx, dy, eps_weno};
+    p.lnx = left_nx;
+    p.rnx = right_nx;
+    return transport_launch(ctx, p, f_dev, out_dev, left_slab_dev, right_slab_dev);
+}
+
 int hk_transport_rhs_slab(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_dev,
                           const double* right_dev, double* out_dev, int nx, int ny, double dx, double dy,
                           double eps_weno) {

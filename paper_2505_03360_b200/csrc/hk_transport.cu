@@ -65,8 +65,8 @@ __global__ void __launch_bounds__(32 * TIW, HK_TR_MINB) transport_march_kernel(T
     auto at = [&](int ii, int jj) -> double {  // f at interior column ii (may be -2..nx+1), row jj (periodic)
         jj = jj < 0 ? jj + ny : (jj >= ny ? jj - ny : jj);
         if (p.x_halo < 0) {
-            if (ii < 0) return __ldg(lh + ((int64_t)jj * 2 + (ii + 2)) * nb + idx);
-            if (ii >= p.nx) return __ldg(rh + ((int64_t)jj * 2 + (ii - p.nx)) * nb + idx);
+            if (ii < 0) return __ldg(lh + ((int64_t)jj * p.lnx + (p.lnx + ii)) * nb + idx);
+            if (ii >= p.nx) return __ldg(rh + ((int64_t)jj * p.rnx + (ii - p.nx)) * nb + idx);
         } else if (p.x_halo == 0) {
             ii = ii < 0 ? ii + p.nx : (ii >= p.nx ? ii - p.nx : ii);
         }
@@ -173,8 +173,8 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
         int ii = i;
         if (p.x_halo < 0) {
             ii = ii < -2 ? -2 : (ii > p.nx + 1 ? p.nx + 1 : ii);  // lanes past the halo are never used
-            if (ii < 0) { colbase = lh + (int64_t)(ii + 2) * nb; rowstride = 2 * nb; }
-            else if (ii >= p.nx) { colbase = rh + (int64_t)(ii - p.nx) * nb; rowstride = 2 * nb; }
+            if (ii < 0) { colbase = lh + (int64_t)(p.lnx + ii) * nb; rowstride = (int64_t)p.lnx * nb; }
+            else if (ii >= p.nx) { colbase = rh + (int64_t)(ii - p.nx) * nb; rowstride = (int64_t)p.rnx * nb; }
             else { colbase = f + (int64_t)ii * nb; rowstride = (int64_t)nxi * nb; }
         } else if (p.x_halo == 0) {
             ii = ((ii % p.nx) + p.nx) % p.nx;

@@ -195,3 +195,65 @@ def penalized_imex_step_slab(part: XSlab, f: torch.Tensor, kernel, dx: float, dy
     transport(y, tr)
     comb(3, f, yv=y, qv=q1, kv=k1, tv=tr, rv=res)
     return f
+
+
+class PeerHalo:
+    """x-slab transport over NVLink / NVSwitch peer memory: the neighbours'
+    slabs are mapped into this process once (CUDA IPC), and the transport
+    kernel reads their two ghost columns directly (hk_transport_rhs_peer): no
+    exchange step and no halo buffers.  `refresh()` orders the neighbours'
+    writes before the read (stream sync + barrier); call it before every
+    transport of a field the neighbours just wrote, and again before they
+    overwrite it (`done()`).  One rank maps its own slab (periodic wrap)."""
+
+    def __init__(self, part: XSlab, slab: torch.Tensor, ctx, group=None):
+        import ctypes as C
+        from . import _abi
+        self.part, self.slab, self.ctx, self.group = part, slab, ctx, group
+        lib = ctx._lib
+        handle = C.create_string_buffer(_abi.HK_IPC_HANDLE_BYTES)
+        off = C.c_int64(0)
+        ctx.check(lib.hk_ipc_handle(ctx.h, C.c_void_p(slab.data_ptr()), handle, C.byref(off)))
+        mine = (handle.raw, off.value, part.nxl)
+        if part.world == 1:
+            infos = [mine]
+        else:
+            infos = [None] * part.world
+            dist.all_gather_object(infos, mine, group=group)
+        self._opened = []
+
+        def ptr_of(rank):
+            if rank == part.rank:
+                return slab.data_ptr(), part.nxl
+            h, o, nxl = infos[rank]
+            base = C.c_void_p()
+            ctx.check(lib.hk_ipc_open(ctx.h, C.c_char_p(h), C.byref(base)))
+            self._opened.append(base)
+            return base.value + o, nxl
+
+        self.left_ptr, self.left_nx = ptr_of(part.left)
+        if part.right == part.left:
+            self.right_ptr, self.right_nx = self.left_ptr, self.left_nx
+        else:
+            self.right_ptr, self.right_nx = ptr_of(part.right)
+
+    def refresh(self):
+        torch.cuda.current_stream().synchronize()
+        if self.part.world > 1:
+            dist.barrier(group=self.group)
+
+    done = refresh
+
+    def transport(self, out: torch.Tensor, vgrid, dx: float, dy: float, eps_weno: float = 1e-6):
+        import ctypes as C
+        p = self.part
+        self.ctx.check(self.ctx._lib.hk_transport_rhs_peer(
+            self.ctx.h, vgrid.nv, C.c_double(vgrid.vmax), C.c_void_p(self.slab.data_ptr()),
+            C.c_void_p(self.left_ptr), self.left_nx, C.c_void_p(self.right_ptr), self.right_nx,
+            C.c_void_p(out.data_ptr()), p.nxl, p.ny, C.c_double(dx), C.c_double(dy), C.c_double(eps_weno)))
+        return out
+
+    def close(self):
+        for b in self._opened:
+            self.ctx._lib.hk_ipc_close(self.ctx.h, b)
+        self._opened = []
