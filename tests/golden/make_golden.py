@@ -22,8 +22,23 @@ from paper_2505_03360_b200 import inputs  # noqa: E402
 VMAX = 8.0
 
 
+def euler(R):
+    """Layer-0 Euler (src/euler.cpp:159-181) on config 4's smoothed quadrants."""
+    nx, ny = 24, 20
+    u = inputs.config4_conserved(nx, ny)
+    st, rhs = R.euler_rhs_periodic(u, nx, ny, 1.0 / nx, 1.0 / ny)
+    st2, u1 = R.tvd_rk2_step_periodic(u, nx, ny, 1.0 / nx, 1.0 / ny, 2e-3)
+    assert st == st2 == 0
+    np.savez_compressed(os.path.join(HERE, "euler_cfg4.npz"), u=u, rhs=rhs, step=u1, nx=nx, ny=ny, dt=2e-3,
+                        xi=5.0 / 3.0, eps_weno=1e-6)
+
+
 def main():
     R = RefLib()
+    if "--only-euler" in sys.argv:
+        euler(R)
+        return
+    euler(R)
     # config 1 shapes: 16^3, M = 4 x 8, R = 2L/(3+sqrt2), hard spheres
     k = R.kernel(16, VMAX, 4, 8, inputs.R_PHYS_MAX)
     f = inputs.config1_cells(4, 16)

@@ -67,3 +67,14 @@ def test_regime_truth_table(oracle):
         assert st == row["status"], row
         if st == 0:
             assert out == row["out"], row
+
+
+def test_euler_cfg4(oracle):
+    """Layer-0 Euler residual and TVD-RK2 step, bitwise the reference's."""
+    g = load("euler_cfg4.npz")
+    nx, ny = int(g["nx"]), int(g["ny"])
+    st, rhs, _ = oracle.euler_rhs_periodic(g["u"], nx, ny, 1.0 / nx, 1.0 / ny, float(g["xi"]), float(g["eps_weno"]))
+    assert st == 0 and np.array_equal(rhs, g["rhs"])
+    st, u1 = oracle.tvd_rk2_step_periodic(g["u"], nx, ny, 1.0 / nx, 1.0 / ny, float(g["dt"]), float(g["xi"]),
+                                          float(g["eps_weno"]))
+    assert st == 0 and np.array_equal(u1, g["step"])

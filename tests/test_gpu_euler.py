@@ -87,3 +87,17 @@ def test_gather_scatter_cells(hk):
     dst = torch.zeros_like(src)
     kinetic.scatter_cells(g[:3], idx[:3], dst)
     assert torch.equal(dst[idx[:3]], src[idx[:3]]) and not dst[0].any()
+
+
+def test_euler_against_golden_fixture(hk):
+    """The device Euler layer against the reference-generated fixture (no oracle)."""
+    import os
+    import torch
+    from paper_2505_03360_b200 import kinetic
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "euler_cfg4.npz"))
+    nx, ny = int(g["nx"]), int(g["ny"])
+    ud = torch.from_numpy(g["u"]).cuda()
+    rhs = kinetic.euler_rhs_periodic(ud, nx, ny, 1.0 / nx, 1.0 / ny).cpu().numpy()
+    assert np.array_equal(rhs, g["rhs"])
+    kinetic.tvd_rk2_step_periodic(ud, nx, ny, 1.0 / nx, 1.0 / ny, float(g["dt"]))
+    assert np.array_equal(ud.cpu().numpy(), g["step"])
