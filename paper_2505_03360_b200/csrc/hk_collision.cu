@@ -364,264 +364,6 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// FAST path, TMEM-resident spectrum: 128 threads per CTA, one field (= one
-// Hermitian-packed direction) per round, two CTAs (two cells) per SM so one
-// cell's barrier / L2 phases overlap the other's FFTs.  The cell's spectrum
-// slab F and the gain accumulators live in tensor memory (thread t <-> lane
-// t); shared memory holds only the exchange landing buffer.
-// ---------------------------------------------------------------------------
-template <int N, int C>
-struct GeoT {
-    static constexpr int P = N / C;
-    static constexpr int ROW = N + 1;
-    static constexpr int PLANE = N * ROW;
-    static constexpr int SLAB = P * PLANE;
-    static constexpr int NT = 128;
-    static_assert(P * N == NT, "one pencil per thread");
-    static constexpr uint32_t TM_COLS = 256;  // F: 4N cols (2N doubles), gain: 2N cols
-    static constexpr size_t SMEM = size_t(SLAB) * sizeof(double2) + 16 * sizeof(double) + 16;
-    static constexpr size_t XCHG_PER_CLUSTER = size_t(2) * C * P * N * N * sizeof(double2);
-};
-
-// Team barrier over the C CTAs of one cell (global counter, release/acquire
-// at GPU scope by one thread; the CTA barriers around it carry the other
-// threads' stores).  CTAs of a team are co-resident (cooperative launch).
-__device__ __forceinline__ void team_barrier(unsigned* ctr, unsigned target) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
-        unsigned v;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ctr) : "memory");
-        } while (v < target);
-    }
-    __syncthreads();
-}
-
-template <int N, int C>
-__global__ void __launch_bounds__(128, 2) coll_fast_tmem_kernel(CollArgs a) {
-    using G = GeoT<N, C>;
-    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE;
-    constexpr int64_t NB = (int64_t)N * N * N;
-    constexpr int BLK = P * N * N;  // double2 per destination block
-    constexpr int64_t FIELD = (int64_t)C * BLK;
-    extern __shared__ __align__(16) double2 smem[];
-    double2* Rv = smem;
-    double* red = reinterpret_cast<double*>(smem + G::SLAB);  // 8 doubles
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 16);
-
-    const unsigned r = cluster_rank();
-    const unsigned cid = cluster_id_x();
-    const unsigned ncl = n_clusters_x();
-    const int t = threadIdx.x;
-    const int warp = t >> 5;
-    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
-    double2* X = a.xchg + (int64_t)cid * 2 * FIELD;
-    unsigned buf = 0;
-
-    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t tm = *tslot + ((uint32_t)(32 * (warp & 3)) << 16);  // my lane, column 0
-    const uint32_t tmF = tm, tmG = tm + 4 * N;
-
-    const int n_entries = a.md + 1;
-    auto pull = [&](const double2* src) {
-        const uint32_t d0 = smem_u32(Rv);
-        for (int idx = t; idx < BLK; idx += 128) {
-            const int row = idx / N, col = idx % N;
-            cp_async16(d0 + (row * ROW + col) * 16, src + idx);
-        }
-        cp_async_wait_all();
-        __syncthreads();
-    };
-
-    for (int64_t it = cid; it < count; it += ncl) {
-        const int64_t cell = a.list ? a.list[it] : it;
-        const double* fc = a.f + cell * NB;
-
-        // ---------------- prologue: F = FFT(f) / N^3 -> TMEM ----------------
-        for (int idx = t; idx < N * N * P; idx += 128) {
-            const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
-            Rv[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
-        }
-        __syncthreads();
-        {  // forward over j2 (rows (j3l, j1))
-            double2* row = Rv + (t / N) * PLANE + (t % N) * ROW;
-            double2 x[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) x[i] = row[i];
-            fft_reg<N, false>(x);
-#pragma unroll
-            for (int i = 0; i < N; ++i) row[i] = x[i];
-        }
-        __syncthreads();
-        {  // forward over j1 (columns (j3l, k2)) -> owner of k1
-            double2* Xb = X + (int64_t)buf * FIELD;
-            const int j3l = t / N, k2 = t % N;
-            const double2* col = Rv + j3l * PLANE + k2;
-            double2 x[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
-            fft_reg<N, false>(x);
-            const int j3 = r * P + j3l;
-#pragma unroll
-            for (int k1 = 0; k1 < N; ++k1)
-                st_cg16(Xb + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
-            cluster_arrive();
-            cluster_wait();
-            pull(Xb + (int64_t)r * BLK);  // rows (k1l, k2), columns k3
-            buf ^= 1;
-        }
-        {  // forward over k3, scale, F -> TMEM (+ Nyquist |F| for the guard)
-            const int pl = t / N, k2 = t % N, k1 = r * P + pl;
-            const double2* row = Rv + pl * PLANE + k2 * ROW;
-            double2 x[N];
-#pragma unroll
-            for (int i = 0; i < N; ++i) x[i] = row[i];
-            fft_reg<N, false>(x);
-            const double s = 1.0 / double(NB);
-#pragma unroll
-            for (int c = 0; c < N / 4; ++c) {
-                double v[8];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    v[2 * i] = x[4 * c + i].x * s;
-                    v[2 * i + 1] = x[4 * c + i].y * s;
-                }
-                tmem_st16(tmF + 16 * c, v);
-            }
-            if (a.nyq) {
-                constexpr int H = N / 2;
-                double2* ny = a.nyq + cell * 3 * N * N;
-                ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
-                if (k2 == H) {
-#pragma unroll
-                    for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                }
-                if (k1 == H) {
-#pragma unroll
-                    for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                }
-            }
-            const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-            for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
-            tmem_wait_st();
-        }
-
-        // ---------------- rounds: one field per round ----------------
-        for (int e = 0; e < n_entries; ++e) {
-            const bool is_loss = (e == a.md);
-            double2* Xb = X + (int64_t)buf * FIELD;
-            {  // phase A: X = F (alpha_s + i alpha'_s), inverse FFT over i3 -> L2
-                const int pl = t / N, i2 = t % N, i1 = r * P + pl;
-                const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + i2;
-                double2 x[N];
-#pragma unroll
-                for (int i3 = 0; i3 < N; ++i3) x[i3] = __ldg(wt + i3 * N);
-#pragma unroll
-                for (int c = 0; c < N / 4; ++c) {
-                    double v[8];
-                    tmem_ld16(tmF + 16 * c, v);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const double2 w = x[4 * c + i];
-                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
-                    }
-                }
-                fft_reg<N, true>(x);
-#pragma unroll
-                for (int j3 = 0; j3 < N; ++j3)
-                    st_cg16(Xb + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
-            }
-            cluster_arrive();
-            cluster_wait();
-            pull(Xb + (int64_t)r * BLK);  // rows (j3l, i1), columns i2
-            buf ^= 1;
-            {  // phase B.1: inverse FFT over i2 (rows)
-                double2* row = Rv + (t / N) * PLANE + (t % N) * ROW;
-                double2 y[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) y[i] = row[i];
-                fft_reg<N, true>(y);
-#pragma unroll
-                for (int i = 0; i < N; ++i) row[i] = y[i];
-            }
-            __syncthreads();
-            {  // phase B.2: inverse FFT over i1 (columns), gain += m gs hs
-                const int j3l = t / N, j2 = t % N;
-                double2* col = Rv + j3l * PLANE + j2;
-                double2 y[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
-                fft_reg<N, true>(y);
-                if (!is_loss) {
-                    const double m = (e == 0) ? a.mult0 : 1.0;
-#pragma unroll
-                    for (int c = 0; c < N / 8; ++c) {
-                        double g[8];
-                        tmem_ld16(tmG + 16 * c, g);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) g[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
-                        tmem_st16(tmG + 16 * c, g);
-                    }
-                    tmem_wait_st();
-                } else {  // last round: (loss, w gain) into my column for the epilogue
-#pragma unroll
-                    for (int c = 0; c < N / 8; ++c) {
-                        double g[8];
-                        tmem_ld16(tmG + 16 * c, g);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) col[(8 * c + i) * ROW] = make_double2(y[8 * c + i].x, a.w * g[i]);
-                    }
-                }
-            }
-        }
-
-        // ---------------- epilogue: Q = jac (w gain - f loss) ----------------
-        __syncthreads();
-        double mre = 0.0, n2 = 0.0;
-        double* qc = a.q + cell * NB;
-        for (int idx = t; idx < N * N * P; idx += 128) {
-            const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
-            const double2 v = Rv[j3l * PLANE + j1 * ROW + j2];
-            const int64_t gi = ((int64_t)j1 * N + j2) * N + r * P + j3l;
-            const double qre = a.jac * (v.y - fc[gi] * v.x);
-            qc[gi] = qre;
-            mre = fmax(mre, fabs(qre));
-            n2 += qre * qre;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
-            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-        }
-        if ((t & 31) == 0) {
-            red[warp] = mre;
-            red[4 + warp] = n2;
-        }
-        __syncthreads();
-        if (t == 0 && a.st) {
-            double m1 = 0, sum = 0;
-            for (int w = 0; w < 4; ++w) {
-                m1 = fmax(m1, red[w]);
-                sum += red[4 + w];
-            }
-            hk_cell_status* sc = a.st + cell;
-            atomic_max_nonneg(&sc->max_re, m1);
-            atomicAdd(&sc->q_norm2, sum);
-        }
-        __syncthreads();
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
-}
-
-// ---------------------------------------------------------------------------
 // FAST path, warp-specialised and pipelined (the production kernel for N=32).
 // One CTA per SM, 256 threads: warps 0-3 PRODUCE (phase A: F * weights,
 // i3 transform, store to the L2 exchange slot), warps 4-7 CONSUME (pull the
@@ -648,289 +390,9 @@ struct GeoP {
     static constexpr size_t XCHG_PER_TEAM = size_t(D) * C * P * N * N * sizeof(double2);
 };
 
-template <int N, int C>
-__global__ void __launch_bounds__(256, 1) coll_fast_pipe_kernel(CollArgs a) {
-    using G = GeoP<N, C>;
-    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
-    constexpr int64_t NB = (int64_t)N * N * N;
-    constexpr int BLK = P * N * N;
-    constexpr int64_t SLOT = (int64_t)C * BLK;
-    extern __shared__ __align__(16) double2 smem[];
-    double2* Rvb = smem;                // consumer landing buffers [2] (prefetch)
-    double2* Pw = smem + 2 * G::SLAB;   // producer work buffer (prologue)
-    double* red = reinterpret_cast<double*>(smem + 3 * G::SLAB);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 8);
-    uint64_t* fbar = reinterpret_cast<uint64_t*>(red + 10);
-
-    const int t = threadIdx.x;
-    const int warp = t >> 5;
-    const bool producer = t < 128;
-    const int u = t & 127;  // role-local thread index == TMEM lane
-    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
-    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
-    double2* X = a.xchg + (int64_t)team * D * SLOT;
-    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
-    unsigned* done = ready + D;
-
-    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
-    if (t == 0) {
-        mbar_init(smem_u32(fbar), 128);
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t tm = *tslot + ((uint32_t)(32 * (warp & 3)) << 16);
-    const uint32_t tmF = tm, tmG = tm + 4 * N;
-    const int n_entries = a.md + 1;
-    unsigned g = 0;      // exchange counter (identical sequence in both roles)
-    unsigned ncell = 0;  // cells processed (F-ready mbarrier parity)
-
-    if (producer) {
-        // ================================ PRODUCER ================================
-        long long spin_cyc = 0, t_start = clock64();
-        auto acquire_slot = [&](unsigned gg) {
-            if (u == 0) spin_cyc += spin_geq(done + gg % D, C * (gg / D));
-            named_bar(1, 128);
-        };
-        auto publish = [&](unsigned gg) {
-            named_bar(1, 128);
-            if (u == 0) signal_add(ready + gg % D);
-        };
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            // ---- prologue: 2-D forward transform of my j3 block, exchange ----
-            for (int idx = u; idx < N * N * P; idx += 128) {
-                const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
-                Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
-            }
-            named_bar(1, 128);
-            {
-                double2* row = Pw + (u / N) * PLANE + (u % N) * ROW;
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = row[i];
-                fft_reg<N, false>(x);
-#pragma unroll
-                for (int i = 0; i < N; ++i) row[i] = x[i];
-            }
-            named_bar(1, 128);
-            {
-                const int j3l = u / N, k2 = u % N, j3 = r * P + j3l;
-                const double2* col = Pw + j3l * PLANE + k2;
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
-                fft_reg<N, false>(x);
-                acquire_slot(g);
-                double2* Xs = X + (int64_t)(g % D) * SLOT;
-#pragma unroll
-                for (int k1 = 0; k1 < N; ++k1)
-                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
-                publish(g);
-                ++g;
-            }
-            // ---- wait until the consumers have put F(cell) into TMEM ----
-            mbar_wait_parity(smem_u32(fbar), ncell & 1);
-            tmem_fence_after();
-            // ---- phase A for every field ----
-            const int pl = u / N, i2 = u % N, i1 = r * P + pl;
-            for (int e = 0; e < n_entries; ++e) {
-                const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + i2;
-                double2 x[N];
-#pragma unroll
-                for (int i3 = 0; i3 < N; ++i3) x[i3] = __ldg(wt + i3 * N);
-#pragma unroll
-                for (int c = 0; c < N / 4; ++c) {
-                    double v[8];
-                    tmem_ld16(tmF + 16 * c, v);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const double2 w = x[4 * c + i];
-                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
-                    }
-                }
-                fft_reg<N, true>(x);
-                acquire_slot(g);
-                double2* Xs = X + (int64_t)(g % D) * SLOT;
-#pragma unroll
-                for (int j3 = 0; j3 < N; ++j3)
-                    st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
-                publish(g);
-                ++g;
-            }
-        }
-        if (a.prof && u == 0) {
-            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
-            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
-        }
-    } else {
-        // ================================ CONSUMER ================================
-        // Exchange gg lands in Rvb[gg & 1]; the pull of gg+1 is issued before
-        // computing gg so its L2 latency overlaps the FFTs.
-        long long spin_cyc = 0, t_start = clock64();
-        auto issue = [&](unsigned gg) {
-            if (u == 0) spin_cyc += spin_geq(ready + gg % D, C * (gg / D + 1));
-            named_bar(2, 128);
-            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK;
-            const uint32_t d0 = smem_u32(Rvb + (gg & 1) * G::SLAB);
-            for (int idx = u; idx < BLK; idx += 128) cp_async16(d0 + ((idx / N) * ROW + (idx % N)) * 16, src + idx);
-            cp_async_commit();
-        };
-        auto complete = [&](unsigned gg) {  // only group gg is outstanding here
-            cp_async_wait_group0();
-            named_bar(2, 128);
-            if (u == 0) signal_add_relaxed(done + gg % D);  // slot reusable: data is in SMEM
-        };
-        if ((int64_t)team < count) issue(g);
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            // ---- prologue: last forward pass (k3), F -> TMEM ----
-            complete(g);
-            {
-                const double2* Rv = Rvb + (g & 1) * G::SLAB;
-                const int pl = u / N, k2 = u % N, k1 = r * P + pl;
-                const double2* row = Rv + pl * PLANE + k2 * ROW;
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = row[i];
-                fft_reg<N, false>(x);
-                const double s = 1.0 / double(NB);
-#pragma unroll
-                for (int c = 0; c < N / 4; ++c) {
-                    double v[8];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        v[2 * i] = x[4 * c + i].x * s;
-                        v[2 * i + 1] = x[4 * c + i].y * s;
-                    }
-                    tmem_st16(tmF + 16 * c, v);
-                }
-                if (a.nyq) {
-                    constexpr int H = N / 2;
-                    double2* ny = a.nyq + cell * 3 * N * N;
-                    ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
-                    if (k2 == H) {
-#pragma unroll
-                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                    }
-                    if (k1 == H) {
-#pragma unroll
-                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                    }
-                }
-                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-                for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
-                tmem_wait_st();
-                tmem_fence_before();
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar)) : "memory");
-            }
-            named_bar(2, 128);  // all consumers done reading this buffer
-            issue(g + 1);  // field 0: only after F is published (producers need it)
-            ++g;
-            // ---- phase B for every field ----
-            for (int e = 0; e < n_entries; ++e) {
-                const bool is_loss = (e == a.md);
-                double2* Rv = Rvb + (g & 1) * G::SLAB;
-                complete(g);
-                const bool more = (e + 1 < n_entries) || (it + nteams < count);
-                if (more) issue(g + 1);
-                {  // inverse FFT over i2 (rows (j3l, i1))
-                    double2* row = Rv + (u / N) * PLANE + (u % N) * ROW;
-                    double2 y[N];
-#pragma unroll
-                    for (int i = 0; i < N; ++i) y[i] = row[i];
-                    fft_reg<N, true>(y);
-#pragma unroll
-                    for (int i = 0; i < N; ++i) row[i] = y[i];
-                }
-                named_bar(2, 128);
-                {  // inverse FFT over i1 (columns (j3l, j2)), gain += m gs hs
-                    const int j3l = u / N, j2 = u % N;
-                    double2* col = Rv + j3l * PLANE + j2;
-                    double2 y[N];
-#pragma unroll
-                    for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
-                    fft_reg<N, true>(y);
-                    if (!is_loss) {
-                        const double m = (e == 0) ? a.mult0 : 1.0;
-#pragma unroll
-                        for (int c = 0; c < N / 8; ++c) {
-                            double gv[8];
-                            tmem_ld16(tmG + 16 * c, gv);
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) gv[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
-                            tmem_st16(tmG + 16 * c, gv);
-                        }
-                        tmem_wait_st();
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < N / 8; ++c) {
-                            double gv[8];
-                            tmem_ld16(tmG + 16 * c, gv);
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) col[(8 * c + i) * ROW] = make_double2(y[8 * c + i].x, a.w * gv[i]);
-                        }
-                    }
-                }
-                named_bar(2, 128);  // reads of this buffer complete before it is refilled
-                if (!is_loss) ++g;
-            }
-            // ---- epilogue: Q = jac (w gain - f loss), loss field in Rvb[g & 1] ----
-            {
-                const double2* Rv = Rvb + (g & 1) * G::SLAB;
-                double mre = 0.0, n2 = 0.0;
-                double* qc = a.q + cell * NB;
-                for (int idx = u; idx < N * N * P; idx += 128) {
-                    const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
-                    const double2 v = Rv[j3l * PLANE + j1 * ROW + j2];
-                    const int64_t gi = ((int64_t)j1 * N + j2) * N + r * P + j3l;
-                    const double qre = a.jac * (v.y - fc[gi] * v.x);
-                    qc[gi] = qre;
-                    mre = fmax(mre, fabs(qre));
-                    n2 += qre * qre;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
-                    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-                }
-                if ((u & 31) == 0) {
-                    red[u >> 5] = mre;
-                    red[4 + (u >> 5)] = n2;
-                }
-                named_bar(2, 128);
-                if (u == 0 && a.st) {
-                    double m1 = 0, sum = 0;
-                    for (int w = 0; w < 4; ++w) {
-                        m1 = fmax(m1, red[w]);
-                        sum += red[4 + w];
-                    }
-                    hk_cell_status* sc = a.st + cell;
-                    atomic_max_nonneg(&sc->max_re, m1);
-                    atomicAdd(&sc->q_norm2, sum);
-                }
-                named_bar(2, 128);  // buffer / red reusable
-                ++g;
-            }
-        }
-        if (a.prof && u == 0) {
-            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
-            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
-        }
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
-}
-
 // ---------------------------------------------------------------------------
 // FAST path, warp-autonomous pipeline (production kernel for N = 32).
-// Same team / slot / TMEM organisation as coll_fast_pipe_kernel, but every
+// Teams of C CTAs exchanging through L2 slots, F and gain in TMEM; every
 // warp is its own pipeline over ONE plane: producer warp p handles the 32
 // pencils (i1 = rP + p, i2 = lane), consumer warp c the j3 plane c; the only
 // CTA-wide barrier left is the cooperative f load of the prologue.  Next-round
@@ -1292,338 +754,6 @@ struct GeoW {
     static constexpr size_t SMEM = size_t(12 * PLANE) * sizeof(double2) + 2 * P * sizeof(uint64_t) + 32;
 };
 
-template <int N, int C>
-__global__ void __launch_bounds__(256, 1) coll_fast_wide_kernel(CollArgs a) {
-    using G = GeoW<N, C>;
-    constexpr int P = G::P, PPW = G::PPW, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
-    static_assert(N == 32 && PPW == 2, "N = 32, two planes per warp");
-    constexpr int64_t NB = (int64_t)N * N * N;
-    constexpr int BLK = P * N * N;
-    constexpr int64_t SLOT = (int64_t)C * BLK;
-    constexpr unsigned ARR = C * 4;  // warp arrivals per slot use (each role)
-    extern __shared__ __align__(16) double2 smem[];
-    double2* Rvb = smem;                // consumer landing [2][4][PLANE]
-    double2* Pw = smem + 8 * PLANE;     // producer staging [4][PLANE]
-    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 12 * PLANE);  // [P]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
-
-    const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
-    const int pw = warp & 3;
-    const bool producer = t < 128;
-    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
-    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
-    double2* X = a.xchg + (int64_t)team * D * SLOT;
-    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
-    unsigned* done = ready + D;
-
-    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
-    if (t < P) mbar_init(smem_u32(fbar + t), 32);
-    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t tm = *tslot + ((uint32_t)(32 * pw) << 16);
-    const int n_entries = a.md + 1;
-    unsigned g = 0, ncell = 0;
-
-    if (producer) {
-        // ================================ PRODUCER WARP ================================
-        double2* wbuf = Pw + pw * PLANE;  // weights of the next unit [i3][lane] / transposes
-        const uint32_t wbuf_s = smem_u32(wbuf);
-        auto issue_w = [&](int e, int pp) {
-            const int i1 = r * P + pw + 4 * pp;
-            const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + lane;
-#pragma unroll
-            for (int i3 = 0; i3 < N; ++i3) cp_async16(wbuf_s + (i3 * 32 + lane) * 16, wt + i3 * N);
-            cp_async_commit();
-        };
-        long long spin_cyc = 0;
-        const long long t_start = clock64();
-        auto acquire = [&](unsigned gg) {
-            if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR * (gg / D));
-            __syncwarp();
-        };
-        auto publish = [&](unsigned gg) {
-            __syncwarp();
-            if (lane == 0) signal_add(ready + gg % D);
-        };
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            if (a.in_ready && t == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);  // host chunk has landed
-            // ---- prologue: 2-D forward transforms of j3 planes 4 pp + (0..3) ----
-#pragma unroll 1
-            for (int pp = 0; pp < PPW; ++pp) {
-                named_bar(1, 128);  // every producer warp is done with its staging plane
-                for (int idx = t; idx < N * N * 4; idx += 128) {
-                    const int j3l = idx % 4, j2 = (idx / 4) % N, j1 = idx / (4 * N);
-                    Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + 4 * pp + j3l], 0.0);
-                }
-                named_bar(1, 128);
-                {
-                    double2* row = wbuf + lane * ROW;  // (j3l = pw, j1 = lane)
-                    double2 x[N];
-#pragma unroll
-                    for (int i = 0; i < N; ++i) x[i] = row[i];
-                    fft_reg<N, false>(x);
-#pragma unroll
-                    for (int i = 0; i < N; ++i) row[i] = x[i];
-                }
-                __syncwarp();
-                const int j3 = r * P + 4 * pp + pw, k2 = lane;
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = wbuf[k2 + i * ROW];
-                fft_reg<N, false>(x);
-                if (pp == 0) acquire(g);
-                double2* Xs = X + (int64_t)(g % D) * SLOT;
-#pragma unroll
-                for (int k1 = 0; k1 < N; ++k1)
-                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
-            }
-            publish(g);
-            ++g;
-            __syncwarp();  // my staging plane is free: first weights
-            issue_w(0, 0);
-            // ---- phase A: per field, the two i1 planes of this warp ----
-            for (int e = 0; e < n_entries; ++e) {
-#pragma unroll 1
-                for (int pp = 0; pp < PPW; ++pp) {
-                    if (e == 0) {
-                        mbar_wait_parity(smem_u32(fbar + pw + 4 * pp), ncell & 1);  // F(plane) in TMEM
-                        tmem_fence_after();
-                    }
-                    const uint32_t tmF = tm + 128 * pp;
-                    double2 x[N];
-                    {
-                        uint32_t r0[32], r1[32], r2[32], r3[32];
-                        tmem_ld32_nowait(tmF, r0);
-                        tmem_ld32_nowait(tmF + 32, r1);
-                        tmem_ld32_nowait(tmF + 64, r2);
-                        tmem_ld32_nowait(tmF + 96, r3);
-                        cp_async_wait_all();
-                        __syncwarp();
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int m = 0; m < 8; ++m) {
-                            x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
-                            x[8 + m] = make_double2(tmem_pair(r1[4 * m], r1[4 * m + 1]), tmem_pair(r1[4 * m + 2], r1[4 * m + 3]));
-                            x[16 + m] = make_double2(tmem_pair(r2[4 * m], r2[4 * m + 1]), tmem_pair(r2[4 * m + 2], r2[4 * m + 3]));
-                            x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
-                        }
-                    }
-#pragma unroll
-                    for (int i3 = 0; i3 < N; ++i3) {
-                        const double2 w = wbuf[i3 * 32 + lane], v = x[i3];
-                        x[i3] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
-                    }
-                    __syncwarp();
-                    if (pp + 1 < PPW)
-                        issue_w(e, pp + 1);
-                    else if (e + 1 < n_entries)
-                        issue_w(e + 1, 0);
-                    fft_reg<N, true>(x);
-                    if (pp == 0) acquire(g);
-                    double2* Xs = X + (int64_t)(g % D) * SLOT;
-                    const int i1 = r * P + pw + 4 * pp;
-#pragma unroll
-                    for (int j3 = 0; j3 < N; ++j3)
-                        st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + lane, x[j3]);
-                }
-                publish(g);  // one release fence for both planes
-                ++g;
-            }
-        }
-        if (a.prof && lane == 0) {
-            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
-            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
-        }
-    } else {
-        // ================================ CONSUMER WARP ================================
-        long long spin_cyc = 0;
-        const long long t_start = clock64();
-        // unit u = 2 (slot index) + pp lands in Rvb[u & 1][pw]
-        auto pull = [&](unsigned gg, int pp, int buf) {
-            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + (pw + 4 * pp) * N * N;
-            const uint32_t d0 = smem_u32(Rvb + (buf * 4 + pw) * PLANE);
-#pragma unroll 8
-            for (int k = 0; k < N; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
-            cp_async_commit();
-        };
-        auto issue = [&](unsigned gg, int pp, int buf) {
-            if (lane == 0) spin_cyc += spin_geq(ready + gg % D, ARR * (gg / D + 1));
-            __syncwarp();
-            pull(gg, pp, buf);
-        };
-        auto try_issue = [&](unsigned gg, int pp, int buf) -> bool {
-            unsigned v = 0;
-            if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ready + gg % D) : "memory");
-            v = __shfl_sync(0xffffffffu, v, 0);
-            if ((int)(v - ARR * (gg / D + 1)) < 0) return false;
-            pull(gg, pp, buf);
-            return true;
-        };
-        auto complete = [&](unsigned gg, int pp) {
-            cp_async_wait_all();
-            __syncwarp();
-            if (pp == PPW - 1 && lane == 0) signal_add_relaxed(done + gg % D);  // last pull of this slot
-        };
-        unsigned u = 0;  // unit counter (buffer parity)
-        if ((int64_t)team < count) issue(g, 0, 0);
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            const bool more_cells = it + nteams < count;
-            // ---- prologue units: forward over k3 of rows (k1l = pw + 4 pp, k2 = lane), F -> TMEM ----
-#pragma unroll 1
-            for (int pp = 0; pp < PPW; ++pp, ++u) {
-                complete(g, pp);
-                const double2* row = Rvb + ((u & 1) * 4 + pw) * PLANE + lane * ROW;
-                const int k1 = r * P + pw + 4 * pp, k2 = lane;
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = row[i];
-                __syncwarp();
-                if (pp + 1 < PPW) issue(g, pp + 1, (u + 1) & 1);  // same slot, already published
-                fft_reg<N, false>(x);
-                const double s = 1.0 / double(NB);
-                const uint32_t tmF = tm + 128 * pp, tmG = tm + 256 + 64 * pp;
-#pragma unroll
-                for (int c = 0; c < N / 4; ++c) {
-                    double v[8];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        v[2 * i] = x[4 * c + i].x * s;
-                        v[2 * i + 1] = x[4 * c + i].y * s;
-                    }
-                    tmem_st16(tmF + 16 * c, v);
-                }
-                if (a.nyq) {
-                    constexpr int H = N / 2;
-                    double2* ny = a.nyq + cell * 3 * N * N;
-                    ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
-                    if (k2 == H) {
-#pragma unroll
-                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                    }
-                    if (k1 == H) {
-#pragma unroll
-                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                    }
-                }
-                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-                for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
-                tmem_wait_st();
-                tmem_fence_before();
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pw + 4 * pp)) : "memory");
-            }
-            __syncwarp();
-            issue(g + 1, 0, u & 1);  // field 0 (needs F of both planes, published above)
-            ++g;
-            // ---- fields ----
-            for (int e = 0; e < n_entries; ++e) {
-                const bool is_loss = (e == a.md);
-#pragma unroll 1
-                for (int pp = 0; pp < PPW; ++pp, ++u) {
-                    double2* Rv = Rvb + ((u & 1) * 4 + pw) * PLANE;
-                    complete(g, pp);
-                    const bool last = pp + 1 == PPW;
-                    const bool more = !last || (e + 1 < n_entries) || more_cells;
-                    const unsigned g2 = last ? g + 1 : g;
-                    const int pp2 = last ? 0 : pp + 1;
-                    bool pending = more && !try_issue(g2, pp2, (u + 1) & 1);
-                    {  // inverse FFT over i2: row i1 = lane of j3 plane pw + 4 pp
-                        double2* row = Rv + lane * ROW;
-                        double2 y[N];
-#pragma unroll
-                        for (int i = 0; i < N; ++i) y[i] = row[i];
-                        fft_reg<N, true>(y);
-#pragma unroll
-                        for (int i = 0; i < N; ++i) row[i] = y[i];
-                    }
-                    __syncwarp();
-                    if (pending) pending = !try_issue(g2, pp2, (u + 1) & 1);
-                    double2 y[N];
-                    {  // inverse FFT over i1: column j2 = lane
-                        const double2* col = Rv + lane;
-#pragma unroll
-                        for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
-                        fft_reg<N, true>(y);
-                    }
-                    __syncwarp();
-                    if (pending) issue(g2, pp2, (u + 1) & 1);
-                    const uint32_t tmG = tm + 256 + 64 * pp;
-                    if (!is_loss) {
-                        const double m = (e == 0) ? a.mult0 : 1.0;
-                        uint32_t g0[32], g1[32];
-                        tmem_ld32_nowait(tmG, g0);
-                        tmem_ld32_nowait(tmG + 32, g1);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int c = 0; c < N / 8; ++c) {
-                            double gv[8];
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const int k = 16 * (c & 1) + 2 * i;
-                                const double old = (c < 2) ? tmem_pair(g0[k], g0[k + 1]) : tmem_pair(g1[k], g1[k + 1]);
-                                gv[i] = old + m * (y[8 * c + i].x * y[8 * c + i].y);
-                            }
-                            tmem_st16(tmG + 16 * c, gv);
-                        }
-                        tmem_wait_st();
-                    } else {
-                        // ---- epilogue for plane j3 = rP + pw + 4 pp ----
-                        const int j3 = r * P + pw + 4 * pp;
-                        double* qc = a.q + cell * NB;
-                        double mre = 0.0, n2 = 0.0, l2 = 0.0;
-#pragma unroll
-                        for (int c = 0; c < N / 8; ++c) {
-                            double gv[8];
-                            tmem_ld16(tmG + 16 * c, gv);
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const int j1 = 8 * c + i;
-                                const int64_t gi = ((int64_t)j1 * N + lane) * N + j3;
-                                const double lt = fc[gi] * y[j1].x;
-                                const double qre = a.jac * (a.w * gv[i] - lt);
-                                qc[gi] = qre;
-                                mre = fmax(mre, fabs(qre));
-                                n2 += qre * qre;
-                                l2 += lt * lt;
-                            }
-                        }
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
-                            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-                            l2 += __shfl_xor_sync(0xffffffffu, l2, o);
-                        }
-                        if (lane == 0 && a.st) {
-                            hk_cell_status* sc = a.st + cell;
-                            atomic_max_nonneg(&sc->max_re, mre);
-                            atomicAdd(&sc->q_norm2, n2);
-                            atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
-                        }
-                        __syncwarp();
-                        if (lane == 0 && a.out_done) signal_add(a.out_done + cell / a.chunk);  // q rows visible
-                    }
-                }
-                ++g;
-            }
-        }
-        if (a.prof && lane == 0) {
-            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
-            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
-        }
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
-}
-
 // 12-warp variant: 4 producer warps (two i1 planes each) and 8 consumer warps
 // (one j3 plane each, single landing buffer): per scheduler one producer and
 // two consumers, matching the 1 : 2 transform count of the two roles; the
@@ -1939,300 +1069,6 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
     if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
 }
 
-// ---------------------------------------------------------------------------
-// FAST path, split-pencil warp pipeline (production kernel for N = 32).
-// As coll_fast_warp_kernel, but every 32-point pencil is shared by the lane
-// pair (l, l ^ 16) (fftx2_dit / fftx2_dif), so a thread holds 16 complex
-// values and the CTA runs 16 warps (8 producers, 8 consumers; two warps per
-// plane) at <= 128 registers: twice the latency hiding of the 8-warp kernel.
-// Distributions: F in TMEM is parity split (output of the forward DIF),
-// phase A runs the inverse DIT (parity in, index halves out); the consumer
-// row pass uses DIF, the column pass DIT (gain nodes = index halves).
-// ---------------------------------------------------------------------------
-template <int N, int C>
-__global__ void __launch_bounds__(512, 1) coll_fast_x2_kernel(CollArgs a) {
-    using G = GeoP<N, C>;
-    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
-    static_assert(P == 4 && N == 32, "N = 32, P = 4");
-    constexpr int64_t NB = (int64_t)N * N * N;
-    constexpr int BLK = P * N * N;
-    constexpr int64_t SLOT = (int64_t)C * BLK;
-    constexpr unsigned ARR = C * 2 * P;  // warps per role per team: 8 CTAs x 8
-    extern __shared__ __align__(16) double2 smem[];
-    double2* Rvb = smem;               // consumer landing [2][P][N][ROW]
-    double2* Pw = smem + 2 * G::SLAB;  // producer prologue block / weight buffers
-    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * G::SLAB);  // [P]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
-
-    const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
-    const bool producer = t < 256;
-    const int rw = warp & 7;          // role-local warp
-    const int pl = rw >> 1, hp = rw & 1;
-    const int pp = 16 * hp + (lane & 15);  // pencil (row / column) index within the plane
-    const int h = lane >> 4;               // half of the pencil
-    const int pg = pl >> 1;                // TMEM column group (planes pl, pl+2 share lanes)
-    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
-    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
-    double2* X = a.xchg + (int64_t)team * D * SLOT;
-    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
-    unsigned* done = ready + D;
-
-    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
-    if (t < P) mbar_init(smem_u32(fbar + t), 64);
-    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t tm = *tslot + ((uint32_t)(32 * (warp & 3)) << 16);
-    const uint32_t tmF = tm + 64 * pg, tmG = tm + 128 + 32 * pg;
-    const int n_entries = a.md + 1;
-    unsigned g = 0, ncell = 0;
-
-    if (producer) {
-        // ================================ PRODUCERS ================================
-        const int i1 = r * P + pl, i2 = pp;
-        double2* wbuf = Pw + pl * PLANE + hp * (N * 16);  // [i3][16 pencils]
-        const uint32_t wbuf_s = smem_u32(wbuf);
-        auto issue_w = [&](int e) {  // my 16 pencils' weights: lanes 0-15 even i3, 16-31 odd
-            const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + 16 * hp + (lane & 15);
-#pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const int i3 = 2 * m + h;
-                cp_async16(wbuf_s + (i3 * 16 + (lane & 15)) * 16, wt + i3 * N);
-            }
-            cp_async_commit();
-        };
-        auto acquire = [&](unsigned gg) {
-            if (lane == 0) spin_geq(done + gg % D, ARR * (gg / D));
-            __syncwarp();
-        };
-        auto publish = [&](unsigned gg) {
-            __syncwarp();
-            if (lane == 0) signal_add(ready + gg % D);
-        };
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            named_bar(1, 256);  // all producer warps are done with Pw
-            for (int idx = t; idx < N * N * P; idx += 256) {
-                const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
-                Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
-            }
-            named_bar(1, 256);
-            {  // forward over j2: row (j3l = pl, j1 = pp); DIF, written back parity split
-                double2* row = Pw + pl * PLANE + pp * ROW;
-                double2 v[16];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    v[j] = row[8 * h + j];
-                    v[8 + j] = row[16 + 8 * h + j];
-                }
-                fftx2_dif<false>(v, h);
-#pragma unroll
-                for (int m = 0; m < 16; ++m) row[2 * m + h] = v[m];
-            }
-            named_bar(1, 256);  // columns need every row of the plane
-            {  // forward over j1: column (j3l = pl, k2 = pp) -> exchange, k1 = 2m + h
-                const int j3 = r * P + pl, k2 = pp;
-                const double2* col = Pw + pl * PLANE + k2;
-                double2 v[16];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    v[j] = col[(8 * h + j) * ROW];
-                    v[8 + j] = col[(16 + 8 * h + j) * ROW];
-                }
-                fftx2_dif<false>(v, h);
-                named_bar(1, 256);  // Pw reads done: weight prefetch may overwrite it
-                issue_w(0);
-                acquire(g);
-                double2* Xs = X + (int64_t)(g % D) * SLOT;
-#pragma unroll
-                for (int m = 0; m < 16; ++m) {
-                    const int k1 = 2 * m + h;
-                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, v[m]);
-                }
-                publish(g);
-                ++g;
-            }
-            mbar_wait_parity(smem_u32(fbar + pl), ncell & 1);
-            tmem_fence_after();
-            for (int e = 0; e < n_entries; ++e) {
-                cp_async_wait_all();
-                __syncwarp();
-                double2 x[16];
-#pragma unroll
-                for (int m = 0; m < 16; ++m) x[m] = wbuf[(2 * m + h) * 16 + (lane & 15)];
-                __syncwarp();
-                if (e + 1 < n_entries) issue_w(e + 1);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {  // F[2m + h], m = 4c..4c+3
-                    double v[8];
-                    tmem_ld16(tmF + 16 * c, v);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const double2 w = x[4 * c + i];
-                        x[4 * c + i] = make_double2(v[2 * i] * w.x - v[2 * i + 1] * w.y, v[2 * i] * w.y + v[2 * i + 1] * w.x);
-                    }
-                }
-                fftx2_dit<true>(x, h);  // x[j] = Y[8h + j], x[8 + j] = Y[16 + 8h + j]
-                acquire(g);
-                double2* Xs = X + (int64_t)(g % D) * SLOT;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int j3a = 8 * h + j, j3b = 16 + 8 * h + j;
-                    st_cg16(Xs + (int64_t)(j3a / P) * BLK + ((j3a % P) * N + i1) * N + i2, x[j]);
-                    st_cg16(Xs + (int64_t)(j3b / P) * BLK + ((j3b % P) * N + i1) * N + i2, x[8 + j]);
-                }
-                publish(g);
-                ++g;
-            }
-        }
-    } else {
-        // ================================ CONSUMERS ================================
-        const unsigned pair_bar = 2 + pl;  // the two warps of my plane
-        auto issue = [&](unsigned gg) {     // my half plane: rows [16 hp, 16 hp + 16)
-            if (lane == 0) spin_geq(ready + gg % D, ARR * (gg / D + 1));
-            __syncwarp();
-            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + pl * N * N + 16 * hp * N;
-            const uint32_t d0 = smem_u32(Rvb + (gg & 1) * G::SLAB + pl * PLANE + 16 * hp * ROW);
-#pragma unroll 8
-            for (int k = 0; k < 16; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
-            cp_async_commit();
-        };
-        auto complete = [&](unsigned gg) {
-            cp_async_wait_all();
-            __syncwarp();
-            if (lane == 0) signal_add_relaxed(done + gg % D);
-        };
-        if ((int64_t)team < count) issue(g);
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            complete(g);
-            {  // forward over k3 of row (k1l = pl, k2 = pp): DIF -> F[2m + h] -> TMEM
-                const double2* row = Rvb + (g & 1) * G::SLAB + pl * PLANE + pp * ROW;
-                const int k1 = r * P + pl, k2 = pp;
-                double2 v[16];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    v[j] = row[8 * h + j];
-                    v[8 + j] = row[16 + 8 * h + j];
-                }
-                fftx2_dif<false>(v, h);
-                const double s = 1.0 / double(NB);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    double w8[8];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        w8[2 * i] = v[4 * c + i].x * s;
-                        w8[2 * i + 1] = v[4 * c + i].y * s;
-                    }
-                    tmem_st16(tmF + 16 * c, w8);
-                }
-                if (a.nyq) {
-                    constexpr int H = N / 2;
-                    double2* ny = a.nyq + cell * 3 * N * N;
-                    if (h == 0) ny[2 * N * N + k1 * N + k2] = make_double2(s * v[8].x, s * v[8].y);  // k3 = 16
-                    if (k2 == H) {
-#pragma unroll
-                        for (int m = 0; m < 16; ++m)
-                            ny[1 * N * N + k1 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
-                    }
-                    if (k1 == H) {
-#pragma unroll
-                        for (int m = 0; m < 16; ++m) ny[k2 * N + 2 * m + h] = make_double2(s * v[m].x, s * v[m].y);
-                    }
-                }
-                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                tmem_st16(tmG, z);
-                tmem_st16(tmG + 16, z);
-                tmem_wait_st();
-                tmem_fence_before();
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pl)) : "memory");
-            }
-            named_bar(pair_bar, 64);  // both halves done with this buffer
-            issue(g + 1);
-            ++g;
-            for (int e = 0; e < n_entries; ++e) {
-                const bool is_loss = (e == a.md);
-                double2* Rv = Rvb + (g & 1) * G::SLAB + pl * PLANE;
-                complete(g);
-                const bool more = (e + 1 < n_entries) || (it + nteams < count);
-                if (more) issue(g + 1);
-                {  // inverse over i2: row i1 = pp (DIF, in place, parity split)
-                    double2* row = Rv + pp * ROW;
-                    double2 v[16];
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        v[j] = row[8 * h + j];
-                        v[8 + j] = row[16 + 8 * h + j];
-                    }
-                    fftx2_dif<true>(v, h);
-#pragma unroll
-                    for (int m = 0; m < 16; ++m) row[2 * m + h] = v[m];
-                }
-                named_bar(pair_bar, 64);  // columns need both halves' rows
-                double2 y[16];
-                {  // inverse over i1: column j2 = pp (DIT): y[j] = node j1 = 8h + j, y[8+j] = 16 + 8h + j
-                    const double2* col = Rv + pp;
-#pragma unroll
-                    for (int m = 0; m < 16; ++m) y[m] = col[(2 * m + h) * ROW];
-                    fftx2_dit<true>(y, h);
-                }
-                named_bar(pair_bar, 64);  // buffer free for the pull two exchanges ahead
-                if (!is_loss) {
-                    const double m = (e == 0) ? a.mult0 : 1.0;
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        double gv[8];
-                        tmem_ld16(tmG + 16 * c, gv);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) gv[i] += m * (y[8 * c + i].x * y[8 * c + i].y);
-                        tmem_st16(tmG + 16 * c, gv);
-                    }
-                    tmem_wait_st();
-                    ++g;
-                } else {
-                    double* qc = a.q + cell * NB;
-                    double mre = 0.0, n2 = 0.0;
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        double gv[8];
-                        tmem_ld16(tmG + 16 * c, gv);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int jj = 8 * c + i;
-                            const int j1 = (jj < 8) ? 8 * h + jj : 16 + 8 * h + (jj - 8);
-                            const int64_t gi = ((int64_t)j1 * N + pp) * N + r * P + pl;
-                            const double qre = a.jac * (a.w * gv[i] - fc[gi] * y[jj].x);
-                            qc[gi] = qre;
-                            mre = fmax(mre, fabs(qre));
-                            n2 += qre * qre;
-                        }
-                    }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
-                        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-                    }
-                    if (lane == 0 && a.st) {
-                        hk_cell_status* sc = a.st + cell;
-                        atomic_max_nonneg(&sc->max_re, mre);
-                        atomicAdd(&sc->q_norm2, n2);
-                    }
-                    ++g;
-                }
-            }
-        }
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
-}
-
 // Rigorous bound of the dropped Nyquist term of the FAST path, per cell.
 // With Y_d = alpha_a,d F and Y'_d = alpha'_a,d F supported on the Nyquist
 // set S:  |Im ga_d(j)| <= A_d = sum_S |Y_d|  and  ||Im gb_d||_2 = N^{3/2}
@@ -2387,82 +1223,22 @@ int launch_variant(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag)
 }
 
 template <int N, int C>
-int launch_fast_tmem(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) {
-    using G = GeoT<N, C>;
-    auto kern = coll_fast_tmem_kernel<N, C>;
-    const int key = N * 100 + C * 2 + 1000;
-    int st;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = G::SMEM;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (!ctx->max_clusters.count(key)) {
-        if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
-                             "smem attribute")))
-            return st;
-        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        cfg.gridDim = dim3(C * 256);
-        int ncl = 0, per_sm = 0;
-        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg), "max active clusters")))
-            return st;
-        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, G::SMEM), "occupancy")))
-            return st;
-        // The cluster query reports one CTA per SM for this kernel; the SMs
-        // host per_sm (= 2, TMEM-limited) co-resident clusters (measured: 30
-        // clusters of 8 on 120 SMs run in one wave, 32 do not).
-        {  // the occupancy API under-reports (1) for this kernel; 2 CTAs/SM fit by resources
-            cudaFuncAttributes fa;
-            if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && 2 * 128 * ((fa.numRegs + 7) & ~7) <= 65536 &&
-                2 * (G::SMEM + 1024) <= 233472)
-                per_sm = 2;
-        }
-        if (per_sm > 2) per_sm = 2;
-        if (ncl * C <= ctx->sm_count) ncl *= per_sm;
-        if (const char* m = getenv("HK_CLUSTERS")) ncl = atoi(m);  // experiment override
-        if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] fast tmem kernel: per_sm %d clusters %d\n", per_sm, ncl);
-        if (ncl < 1) return fail(ctx, HK_CUDA, "fast collision kernel cannot be resident");
-        ctx->max_clusters[key] = ncl;
-    }
-    int64_t ncl = ctx->max_clusters[key];
-    if (max_cells < ncl) ncl = max_cells;
-    if (ncl < 1) return HK_OK;
-    cfg.gridDim = dim3(unsigned(ncl * C));
-    cfg.stream = ctx->stream;
-    timing_begin(ctx, tag);
-    st = check_cuda(ctx, cudaLaunchKernelEx(&cfg, kern, args), "fast collision kernel launch");
-    timing_end(ctx);
-    ctx->launches++;
-    return st;
-}
-
-template <int N, int C>
 int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int tag) {
     using G = GeoP<N, C>;
-    // default: warp-autonomous 8-warp kernel; HK_FAST_KERNEL=x2|cta selects the split-pencil
-    // 16-warp variant (measured slower: +70% instructions) or the CTA-synchronous one
+    // Default: the 12-warp kernel (teams of 4 on all SMs).  HK_FAST_KERNEL=8
+    // selects the 8-warp kernel (teams of 8, 144 SMs; 52.0 vs 49.0 ms at
+    // config 2), =d the 8-warp kernel with deferred publish (+10 %).  Measured
+    // and removed: CTA-synchronous pipeline, 2-CTA/SM TMEM cluster, split
+    // pencils over lane pairs, two planes per warp with 4 + 4 warps.
     const char* kv = getenv("HK_FAST_KERNEL");
-    // variant 1: warp kernel (default), 3: warp kernel with deferred publish
-    // (measured 10 % slower), 2: x2, 0: CTA pipeline
-    // 4: two planes per warp, teams of 4 CTAs (coll_fast_wide_kernel)
-    // default 5 (12 warps, measured 49.0 ms vs 52.0 ms for the 8-warp kernel); HK_FAST_KERNEL=8 for variant 1
-    const int variant = !kv ? 5
-                      : (kv[0] == 'x' ? 2 : (kv[0] == 'c' ? 0 : (kv[0] == 'd' ? 3 : (kv[0] == 'w' ? 4 : (kv[0] == '8' ? 1 : 5)))));
-    constexpr int CW = 4;  // team size of the wide kernel
-    auto kern = variant == 2 ? coll_fast_x2_kernel<N, C>
-              : variant == 1 ? coll_fast_warp_kernel<N, C, false>
+    const int variant = !kv ? 5 : (kv[0] == '8' ? 1 : (kv[0] == 'd' ? 3 : 5));
+    constexpr int CW = 4;  // team size of the 12-warp kernel
+    auto kern = variant == 1 ? coll_fast_warp_kernel<N, C, false>
               : variant == 3 ? coll_fast_warp_kernel<N, C, true>
-              : variant == 4 ? coll_fast_wide_kernel<N, CW>
-              : variant == 5 ? coll_fast_w12_kernel<N, CW>
-                             : coll_fast_pipe_kernel<N, C>;
-    const int nthreads = variant == 2 ? 512 : (variant == 5 ? 384 : 256);
-    const int TC = (variant == 4 || variant == 5) ? CW : C;  // CTAs per team
-    const size_t smem = (variant == 4 || variant == 5) ? GeoW<N, CW>::SMEM : G::SMEM;
+                             : coll_fast_w12_kernel<N, CW>;
+    const int nthreads = variant == 5 ? 384 : 256;
+    const int TC = variant == 5 ? CW : C;  // CTAs per team
+    const size_t smem = variant == 5 ? GeoW<N, CW>::SMEM : G::SMEM;
     const int key = N * 100 + C * 2 + 2000 + variant;
     int st;
     if (!ctx->max_clusters.count(key)) {
@@ -2482,7 +1258,7 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     if (max_cells < teams) teams = max_cells;
     if (teams < 1) return HK_OK;
     CollArgs args = args_in;
-    if ((variant == 1 || variant == 3 || variant == 4 || variant == 5) && ctx->sio_in_ready) {  // streamed host I/O (warp kernels only)
+    if (ctx->sio_in_ready) {  // streamed host I/O (every warp kernel)  // streamed host I/O (warp kernels only)
         args.in_ready = ctx->sio_in_ready;
         args.out_done = ctx->sio_out_done;
         args.chunk = ctx->sio_chunk;
@@ -2575,11 +1351,8 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
             done = true;
         }
         if constexpr (N == 32 && C == 8) {
-            if (!(flags & HK_COLL_LEGACY_FAST) && !getenv("HK_TMEM2")) {
+            if (!(flags & HK_COLL_LEGACY_FAST)) {
                 if ((s = launch_fast_pipe<N, C>(ctx, a, ncells, 0))) return s;
-                done = true;
-            } else if (!(flags & HK_COLL_LEGACY_FAST)) {
-                if ((s = launch_fast_tmem<N, C>(ctx, a, ncells, 0))) return s;
                 done = true;
             }
         }

@@ -320,76 +320,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const double (&v)[8]) 
 }  // namespace hk
 
 // ---------------------------------------------------------------------------
-// Split-pencil 32-point transforms: one pencil over the lane pair (l, l ^ 16),
-// h = (lane >> 4) & 1 selects the half.  Halving the per-thread pencil
-// (64 instead of 128 data registers) doubles the warps an SM can hold.
-//   fftx2_dit: input x[2m + h] (m = 0..15, parity split)  -> output v[j] = X[8h + j],
-//              v[8 + j] = X[16 + 8h + j]                   (index halves)
-//   fftx2_dif: input v[j] = x[8h + j], v[8 + j] = x[16 + 8h + j] (index halves)
-//              -> output v[m] = X[2m + h]                  (parity split)
-// Unnormalised, forward = e^{-2 pi i}, INV = e^{+2 pi i}, like fft_reg.
+// Split-pencil transforms: one pencil over the lane pair (l, l ^ 16), h = (lane
+// >> 4) & 1 selects the half.  Unnormalised, forward = e^{-2 pi i}, INV =
+// e^{+2 pi i}, like fft_reg.
 // ---------------------------------------------------------------------------
 namespace hk {
 
 __device__ __forceinline__ double2 shfl_xor16(double2 v) {
     return make_double2(__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16));
-}
-
-template <bool INV>
-__device__ __forceinline__ void fftx2_dit(double2 (&v)[16], int h) {
-    fft_reg<16, INV>(v);  // E[k] (h = 0) or O[k] (h = 1)
-    if (h) {
-#pragma unroll
-        for (int k = 1; k < 16; ++k) {
-            double2 w = c_tw64[2 * k];  // e^{-2 pi i k / 32}
-            if (INV) w.y = -w.y;
-            v[k] = cmul(v[k], w);      // T[k] = w^k O[k]
-        }
-    }
-    double2 lo[8], hi[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const double2 send = h ? v[j] : v[8 + j];  // h=0 sends E[8+j], h=1 sends T[j]
-        const double2 r = shfl_xor16(send);
-        const double2 a = h ? r : v[j];            // E[8h + j]
-        const double2 b = h ? v[8 + j] : r;        // T[8h + j]
-        lo[j] = cadd(a, b);                        // X[8h + j]
-        hi[j] = csub(a, b);                        // X[16 + 8h + j]
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        v[j] = lo[j];
-        v[8 + j] = hi[j];
-    }
-}
-
-template <bool INV>
-__device__ __forceinline__ void fftx2_dif(double2 (&v)[16], int h) {
-    // first DIF stage on my n in [8h, 8h+8): a[n] = x[n] + x[n+16], b[n] = (x[n] - x[n+16]) w^n
-    double2 a[8], b[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        a[j] = cadd(v[j], v[8 + j]);
-        b[j] = csub(v[j], v[8 + j]);
-    }
-    // twiddle w^n, n = 8h + j
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        double2 w0 = c_tw64[2 * j], w1 = c_tw64[2 * (8 + j)];
-        double2 w = h ? w1 : w0;
-        if (INV) w.y = -w.y;
-        b[j] = cmul(b[j], w);
-    }
-    // h = 0 collects a[0..15] (even outputs), h = 1 collects b[0..15] (odd outputs)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const double2 send = h ? a[j] : b[j];  // h=0 sends b[j] (n=j), h=1 sends a[8+j]
-        const double2 r = shfl_xor16(send);
-        // h = 0: own a[j] (n = j), receives a[8+j];  h = 1: own b[8+j], receives b[j]
-        v[j] = h ? r : a[j];
-        v[8 + j] = h ? b[j] : r;
-    }
-    fft_reg<16, INV>(v);  // v[m] = X[2m + h]
 }
 
 // Generic split-pencil transforms of length L = 2M over the lane pair
