@@ -257,3 +257,67 @@ class PeerHalo:
         for b in self._opened:
             self.ctx._lib.hk_ipc_close(self.ctx.h, b)
         self._opened = []
+
+
+# ---------------------------------------------------------------------------
+# Dynamic load balancing of Boltzmann (layer-2) cells across ranks (SURVEY §8f
+# "next" #3): x-slabs are imbalanced when layer-2 cells cluster at an
+# interface.  Every rank lists its layer-2 cells; a deterministic plan (from
+# the all-gathered counts) moves the excess of over-loaded ranks to
+# under-loaded ones with one all-to-all of f blocks, each rank evaluates the
+# operator on a dense batch, and a second all-to-all returns the results to
+# the owners.  Per-cell operators are independent and deterministic, so the
+# result is bitwise the owner's local evaluation.
+# ---------------------------------------------------------------------------
+def balance_plan(counts):
+    """counts[r] = layer-2 cells on rank r -> send[r][s] = cells r ships to s.
+    Targets differ by at most one; ranks keep their own cells first; surplus
+    goes to deficits in rank order (identical on every rank)."""
+    world = len(counts)
+    total = sum(counts)
+    target = [total // world + (1 if r < total % world else 0) for r in range(world)]
+    send = [[0] * world for _ in range(world)]
+    surplus = [max(0, counts[r] - target[r]) for r in range(world)]
+    deficit = [max(0, target[r] - counts[r]) for r in range(world)]
+    s = 0
+    for r in range(world):
+        while surplus[r] > 0:
+            while deficit[s] == 0:
+                s += 1
+            m = min(surplus[r], deficit[s])
+            send[r][s] += m
+            surplus[r] -= m
+            deficit[s] -= m
+    return send
+
+
+def balanced_apply(local: torch.Tensor, cells: torch.Tensor, fn, group=None):
+    """out[cells] = fn(local[cells]) with the work of all ranks' `cells` spread
+    evenly: `local` [n_local, nb] (this rank's slab), `cells` int64 indices
+    into it, `fn` a per-cell batch operator ([m, nb] -> [m, nb], e.g.
+    spectral_collision).  Returns (out rows for `cells`, plan)."""
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    if world == 1:
+        return fn(local[cells]), [[len(cells)]]
+    rank = dist.get_rank(group)
+    counts = [None] * world
+    dist.all_gather_object(counts, int(len(cells)), group=group)
+    send = balance_plan(counts)
+    keep = counts[rank] - sum(send[rank])
+    # rows shipped: the tail of my list, in destination-rank order
+    out_split = [send[rank][s] for s in range(world)]
+    in_split = [send[s][rank] for s in range(world)]
+    nb = local.shape[1]
+    if local.is_cuda:
+        from .kinetic import gather_cells
+        batch = gather_cells(local, cells)
+    else:
+        batch = local[cells]
+    ship = batch[keep:].contiguous()
+    recv = torch.empty((sum(in_split), nb), dtype=local.dtype, device=local.device)
+    dist.all_to_all_single(recv, ship, in_split, out_split, group=group)
+    work = torch.cat([batch[:keep], recv]) if recv.numel() else batch[:keep]
+    res = fn(work)
+    back = torch.empty((sum(out_split), nb), dtype=local.dtype, device=local.device)
+    dist.all_to_all_single(back, res[keep:].contiguous(), out_split, in_split, group=group)
+    return torch.cat([res[:keep], back]), send
