@@ -1090,11 +1090,15 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
     double* bound = sB + md * KS;     // [GC]
     const int64_t c0 = (int64_t)blockIdx.x * GC;
     const int nn3 = 3 * n * n;
-    const int npair = GC * md;        // (cell, direction) pairs, <= 256 * PPT
-    constexpr int PPT = 8;
-    double acc[PPT][4];
+    // Register tile per thread: 4 cells x up to 2 directions (e = el, el + 64),
+    // so one SMEM read of a table value serves 4 cells (the cell values are
+    // warp-wide broadcasts).
+    const int el = threadIdx.x & 63, cg = threadIdx.x >> 6;  // direction lane, cell group (4 x 4 cells)
+    double acc[2][4][4];
 #pragma unroll
-    for (int p = 0; p < PPT; ++p) acc[p][0] = acc[p][1] = acc[p][2] = acc[p][3] = 0.0;
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[m][c][0] = acc[m][c][1] = acc[m][c][2] = acc[m][c][3] = 0.0;
     for (int k0 = 0; k0 < nn3; k0 += KC) {
         __syncthreads();
         for (int i = threadIdx.x; i < GC * KC; i += blockDim.x) {
@@ -1114,19 +1118,24 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
         }
         __syncthreads();
 #pragma unroll
-        for (int p = 0; p < PPT; ++p) {
-            const int pr = threadIdx.x + 256 * p;
-            if (pr >= npair) break;
-            const int c = pr / md, e = pr % md;
-            const double* fF = sF + c * KC;
+        for (int m = 0; m < 2; ++m) {
+            const int e = el + 64 * m;
+            if (e >= md) continue;
             const double* fa = sA + e * KS;
             const double* fb = sB + e * KS;
+            const double* fF = sF + 4 * cg * KC;
+#pragma unroll 4
             for (int k = 0; k < KC; ++k) {
-                const double ya = fa[k] * fF[k], yb = fb[k] * fF[k];
-                acc[p][0] += ya;
-                acc[p][1] += yb;
-                acc[p][2] += ya * ya;
-                acc[p][3] += yb * yb;
+                const double a = fa[k], b = fb[k];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double F = fF[c * KC + k];
+                    const double ya = a * F, yb = b * F;
+                    acc[m][c][0] += ya;
+                    acc[m][c][1] += yb;
+                    acc[m][c][2] += ya * ya;
+                    acc[m][c][3] += yb * yb;
+                }
             }
         }
     }
@@ -1134,12 +1143,14 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
     if (threadIdx.x < GC) bound[threadIdx.x] = 0.0;
     __syncthreads();
 #pragma unroll
-    for (int p = 0; p < PPT; ++p) {
-        const int pr = threadIdx.x + 256 * p;
-        if (pr >= npair) break;
-        const int c = pr / md, e = pr % md;
-        const double b = fmin(acc[p][0] * sqrt(acc[p][3]), sqrt(acc[p][2]) * acc[p][1]);
-        atomicAdd(bound + c, (e == 0 ? mult0 : 1.0) * b);
+    for (int m = 0; m < 2; ++m) {
+        const int e = el + 64 * m;
+        if (e >= md) continue;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const double b = fmin(acc[m][c][0] * sqrt(acc[m][c][3]), sqrt(acc[m][c][2]) * acc[m][c][1]);
+            atomicAdd(bound + 4 * cg + c, (e == 0 ? mult0 : 1.0) * b);
+        }
     }
     __syncthreads();
     if (threadIdx.x < GC && c0 + threadIdx.x < ncells) {
@@ -1366,7 +1377,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
             timing_begin(ctx, 1);
             {
                 const size_t gsmem = sizeof(double) * (GC * KC + 2 * k->md * KS + GC);
-                if (k->md * GC > 256 * 8) return fail(ctx, HK_UNSUPPORTED, "guard: too many directions");
+                if (k->md > 128) return fail(ctx, HK_UNSUPPORTED, "guard: at most 128 distinct directions");
                 cudaFuncSetAttribute(guard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
                 guard_kernel<<<unsigned((ncells + GC - 1) / GC), 256, gsmem, ctx->stream>>>(
                     N, k->md, k->mult0, k->jac, k->weight, kGuardTau, nyq, k->abs_a, k->abs_ap, ncells, st, list, count);
