@@ -41,7 +41,8 @@ typedef enum {
     HK_CUDA = 6,                  /* device / runtime failure (no reference analogue) */
     HK_NCCL = 7,                  /* collective failure (no reference analogue) */
     HK_POSITIVITY = 8,            /* hykin::positivity_error */
-    HK_UNSUPPORTED = 9            /* size not implemented on this path */
+    HK_UNSUPPORTED = 9,           /* size not implemented on this path */
+    HK_SCENARIO_END = 10          /* hykin::scenario_end_error */
 } hk_status;
 
 /* Per-cell verdict written by the collision kernels (device or host array). */
@@ -214,6 +215,44 @@ int hk_gather_cells(hk_ctx ctx, int64_t nb, const double* src_dev, const int64_t
                     double* dst_dev);
 int hk_scatter_cells(hk_ctx ctx, int64_t nb, const double* src_dev, const int64_t* idx_dev, int64_t count,
                      double* dst_dev);
+
+/* ---- embedded obstacles (SURVEY §8f "next" #4) --------------------------------
+ * ObstacleSpec (inc/hykin/obstacle.hpp:9-34): geometry in cell indices; shape
+ * HK_OBSTACLE_NONE / _RECTANGLE (half extents) / _DISK (radius); the fixed
+ * interior state (rho, pressure, ux, uy); a per-step displacement. */
+#define HK_OBSTACLE_NONE 0
+#define HK_OBSTACLE_RECTANGLE 1
+#define HK_OBSTACLE_DISK 2
+typedef struct {
+    int shape, center_i, center_j, half_i, half_j, radius;
+    double rho, pressure, ux, uy;
+    int move_di, move_dj;
+} hk_obstacle_spec;
+/* Cell kinds (enum class CellKind, inc/hykin/grid.hpp:63). */
+#define HK_CELL_INTERIOR 0
+#define HK_CELL_OBSTACLE 1
+#define HK_CELL_FORCED_RING 2
+#define HK_CELL_GHOST 3
+/* classify_cells (src/grid.cpp:74-110): kind_dev [ny*nx] uint8, cell = j*nx + i;
+ * 4-cell ghost frame, footprint, 2-cell forced-kinetic ring.  HK_CONFIG (first
+ * offending cell in row-major order in hk_last_error) when the footprint or
+ * the ring reaches the ghost frame.  Synchronises. */
+int hk_classify_cells(hk_ctx ctx, int64_t nx, int64_t ny, const hk_obstacle_spec* spec, uint8_t* kind_dev);
+/* apply_obstacle (src/coupling.cpp:95-147), once per time step.  spec (host)
+ * is moved in place; r_dev [cells] int8 regimes, kind_dev [cells] the previous
+ * classification (updated), hydro_dev [cells][4] conserved states, f_dev
+ * [cells][n^3] the dense distribution field: blocks of newly covered cells are
+ * left untouched (the reference releases them), vacated cells get the fixed
+ * state's Maxwellian, ring cells leaving layer 0 the Maxwellian of their hydro
+ * state.  covered/vacated (nullable host ints) count the transitions.
+ * Errors follow the reference's throw points: HK_CONFIG (static obstacle
+ * touching the ghost frame) and HK_SCENARIO_END (moving one leaving the
+ * domain) before any cell is touched; HK_POSITIVITY / HK_DEGENERATE at the
+ * first failing cell, earlier cells updated as the reference's loop leaves
+ * them.  Synchronises (one 16-byte read-back). */
+int hk_apply_obstacle(hk_ctx ctx, int n, double vmax, hk_obstacle_spec* spec, int64_t nx, int64_t ny, int8_t* r_dev,
+                      uint8_t* kind_dev, double* hydro_dev, double* f_dev, double heat_ratio, int* covered,
+                      int* vacated);
 
 /* ---- multi-GPU: NCCL communicator of a context ------------
  * One process per GPU.  Rank 0 calls hk_comm_unique_id, the host side ships

@@ -1350,3 +1350,100 @@ void hko_conserved_from_moments(const double mom5[5], double heat_ratio, double 
     const double u2 = mom5[1] * mom5[1] + mom5[2] * mom5[2] + mom5[3] * mom5[3];
     u[3] = rho * mom5[4] / (heat_ratio - 1.0) + 0.5 * rho * u2;
 }
+
+
+/* ===================================================================== */
+/* Obstacles (src/grid.cpp:56-110, src/coupling.cpp:95-147)              */
+/* ===================================================================== */
+#define HKO_GHOST 4
+static int hko_in_ghost(int nx, int ny, int i, int j) {
+    return i < HKO_GHOST || i >= nx - HKO_GHOST || j < HKO_GHOST || j >= ny - HKO_GHOST;
+}
+
+static int hko_in_footprint(const hko_obstacle* s, int i, int j) {  /* src/grid.cpp:56-71 */
+    if (s->shape == 1) return abs(i - s->center_i) <= s->half_i && abs(j - s->center_j) <= s->half_j;
+    if (s->shape == 2) {
+        const double di = i - s->center_i, dj = j - s->center_j;
+        return di * di + dj * dj <= (double)s->radius * s->radius;
+    }
+    return 0;
+}
+
+int hko_classify_cells(int nx, int ny, const hko_obstacle* s, unsigned char* kind, long* bad_cell) {
+    if (bad_cell) *bad_cell = -1;
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) kind[(long)j * nx + i] = hko_in_ghost(nx, ny, i, j) ? 3 : 0;
+    if (s->shape == 0) return 0;
+    const int ring = 2;
+    for (int j = 0; j < ny; ++j)
+        for (int i = 0; i < nx; ++i) {
+            const long c = (long)j * nx + i;
+            if (hko_in_footprint(s, i, j)) {
+                if (kind[c] == 3) { if (bad_cell) *bad_cell = c; return HKO_CONFIG; }
+                kind[c] = 1;
+                continue;
+            }
+            int near = 0;
+            for (int dj = -ring; dj <= ring && !near; ++dj)
+                for (int di = -ring; di <= ring && !near; ++di) near = hko_in_footprint(s, i + di, j + dj);
+            if (near) {
+                if (kind[c] == 3) { if (bad_cell) *bad_cell = c; return HKO_CONFIG; }
+                kind[c] = 2;
+            }
+        }
+    return 0;
+}
+
+int hko_apply_obstacle(int nx, int ny, int n, double vmax, hko_obstacle* s, signed char* r, unsigned char* kind,
+                       double* hydro, double* f, double heat_ratio, int* covered, int* vacated) {
+    *covered = 0;
+    *vacated = 0;
+    if (s->shape == 0) return 0;
+    const int moving = s->move_di != 0 || s->move_dj != 0;
+    s->center_i += s->move_di;
+    s->center_j += s->move_dj;
+    const long cells = (long)nx * ny, nb = (long)n * n * n;
+    unsigned char* nk = malloc(cells);
+    const int st = hko_classify_cells(nx, ny, s, nk, NULL);
+    if (st) {
+        free(nk);
+        return moving ? HKO_SCENARIO_END : st;
+    }
+    /* obstacle_moments / obstacle_state (src/coupling.cpp:39-53) */
+    hko_moments fm;
+    fm.rho = s->rho;
+    fm.u[0] = s->ux; fm.u[1] = s->uy; fm.u[2] = 0.0;
+    fm.T = s->pressure / s->rho;
+    const double mom5[5] = {fm.rho, fm.u[0], fm.u[1], fm.u[2], fm.T};
+    double fixed[4];
+    hko_conserved_from_moments(mom5, heat_ratio, fixed);
+    int first = 0;
+    for (long c = 0; c < cells; ++c) {
+        const unsigned char before = kind[c], after = nk[c];
+        if (after == 1) {
+            if (before != 1) ++*covered;
+            for (int k = 0; k < 4; ++k) hydro[4 * c + k] = fixed[k];
+            r[c] = 2;
+        } else if (before == 1) {
+            ++*vacated;
+            r[c] = 2;
+            for (int k = 0; k < 4; ++k) hydro[4 * c + k] = fixed[k];
+            const int s3 = hko_maxwellian(&fm, n, vmax, f + c * nb);
+            if (s3) { first = s3; break; }  /* degenerate fixed state: throws after r, hydro */
+        }
+        if (after == 2 && r[c] != 2) {
+            if (r[c] == 0) {
+                double m5[5];
+                const int s2 = hko_moments_from_conserved(hydro + 4 * c, heat_ratio, m5);
+                if (s2) { first = s2; break; }  /* the reference throws mid-loop */
+                hko_moments m;
+                m.rho = m5[0]; m.u[0] = m5[1]; m.u[1] = m5[2]; m.u[2] = m5[3]; m.T = m5[4];
+                hko_maxwellian(&m, n, vmax, f + c * nb);
+            }
+            r[c] = 2;
+        }
+        kind[c] = after;
+    }
+    free(nk);
+    return first;
+}

@@ -38,7 +38,8 @@ enum {
     HKO_DEGENERATE = 3,            /* degenerate_state_error */
     HKO_NUMERICAL_CONSISTENCY = 4, /* numerical_consistency_error */
     HKO_CONTRACT = 5,              /* contract_violation */
-    HKO_POSITIVITY = 8             /* positivity_error */
+    HKO_POSITIVITY = 8,            /* positivity_error */
+    HKO_SCENARIO_END = 10          /* scenario_end_error */
 };
 
 /* ---------------- FFT (stand-in for FFTW3 C2C, src/fft.cpp:35-40) ---------------- */
@@ -163,6 +164,20 @@ int hko_tvd_rk2_step_periodic(double* u, int nx, int ny, double dx, double dy, d
 /* Transitions (src/coupling.cpp:7-22, src/regime.cpp:54-72) */
 int hko_moments_from_conserved(const double u[4], double heat_ratio, double mom5[5]);
 void hko_conserved_from_moments(const double mom5[5], double heat_ratio, double u[4]);
+
+/* ---------------- obstacles (src/grid.cpp:56-110, src/coupling.cpp:95-147) ---------------- */
+typedef struct {
+    int shape; /* 0 none, 1 rectangle, 2 disk (ObstacleSpec::Shape) */
+    int center_i, center_j, half_i, half_j, radius;
+    double rho, pressure, ux, uy;
+    int move_di, move_dj;
+} hko_obstacle;
+/* kind: 0 interior, 1 obstacle, 2 forced_ring, 3 ghost (CellKind); ghost frame depth 4. */
+int hko_classify_cells(int nx, int ny, const hko_obstacle* s, unsigned char* kind, long* bad_cell);
+/* Dense f [cells][n^3]: released (covered) blocks are left untouched. Returns
+ * HKO_CONFIG / HKO_SCENARIO_END / HKO_POSITIVITY like the reference throws. */
+int hko_apply_obstacle(int nx, int ny, int n, double vmax, hko_obstacle* s, signed char* r, unsigned char* kind,
+                       double* hydro, double* f, double heat_ratio, int* covered, int* vacated);
 
 #ifdef __cplusplus
 }

@@ -50,6 +50,18 @@ class _Moments(C.Structure):
     _fields_ = [("rho", C.c_double), ("u", C.c_double * 3), ("T", C.c_double)]
 
 
+class Obstacle(C.Structure):
+    """hko_obstacle / ObstacleSpec (inc/hykin/obstacle.hpp); shape 0 none, 1 rectangle, 2 disk."""
+    _fields_ = [("shape", C.c_int), ("center_i", C.c_int), ("center_j", C.c_int), ("half_i", C.c_int),
+                ("half_j", C.c_int), ("radius", C.c_int), ("rho", C.c_double), ("pressure", C.c_double),
+                ("ux", C.c_double), ("uy", C.c_double), ("move_di", C.c_int), ("move_dj", C.c_int)]
+
+    def copy(self):
+        o = Obstacle()
+        C.pointer(o)[0] = self
+        return o
+
+
 def build(quiet: bool = True) -> None:
     """Builds liboracle.so (and _ref when /root/reference is present)."""
     import subprocess
@@ -260,6 +272,26 @@ class Oracle:
         self.lib.hko_conserved_from_moments(_ptr(mom5), C.c_double(heat_ratio), _ptr(u))
         return u
 
+    # --- obstacles (src/grid.cpp:56-110, src/coupling.cpp:95-147) -----------
+    def classify_cells(self, nx, ny, spec):
+        kind = np.zeros(nx * ny, dtype=np.uint8)
+        bad = C.c_long(-1)
+        st = self.lib.hko_classify_cells(nx, ny, C.byref(spec), kind.ctypes.data_as(C.c_void_p), C.byref(bad))
+        return st, kind, bad.value
+
+    def apply_obstacle(self, nx, ny, n, vmax, spec, r, kind, hydro, f, heat_ratio=5.0 / 3.0):
+        """In-place on copies; returns (status, spec, r, kind, hydro, f, covered, vacated)."""
+        spec = spec.copy()
+        r = np.ascontiguousarray(r, dtype=np.int8).copy()
+        kind = np.ascontiguousarray(kind, dtype=np.uint8).copy()
+        hydro = np.ascontiguousarray(hydro, dtype=np.float64).copy()
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        cov, vac = C.c_int(0), C.c_int(0)
+        st = self.lib.hko_apply_obstacle(nx, ny, n, C.c_double(vmax), C.byref(spec), r.ctypes.data_as(C.c_void_p),
+                                         kind.ctypes.data_as(C.c_void_p), _ptr(hydro), _ptr(f),
+                                         C.c_double(heat_ratio), C.byref(cov), C.byref(vac))
+        return st, spec, r, kind, hydro, f, cov.value, vac.value
+
     def penalized_imex_step(self, k: OracleKernel, f, nx, ny, dx, dy, dt, eps_cell,
                             pen_coeff=2 * np.pi, eps_weno=1e-6):
         f = np.ascontiguousarray(f, dtype=np.float64).copy()
@@ -450,6 +482,27 @@ class RefLib:
         u = np.zeros(4)
         self.lib.href_conserved_from_moments(_ptr(mom5), C.c_double(heat_ratio), _ptr(u))
         return u
+
+    # --- obstacles ------------------------------------------------------------
+    def classify_cells(self, nx, ny, spec):
+        kind = np.zeros(nx * ny, dtype=np.uint8)
+        st = self.lib.href_classify_cells(nx, ny, C.byref(spec), kind.ctypes.data_as(C.c_void_p))
+        return st, kind
+
+    def apply_obstacle(self, nx, ny, n, vmax, spec, r, kind, hydro, f, has, heat_ratio=5.0 / 3.0):
+        """`has` marks the cells owning a distribution block (DistributionField::has)."""
+        spec = spec.copy()
+        r = np.ascontiguousarray(r, dtype=np.int8).copy()
+        kind = np.ascontiguousarray(kind, dtype=np.uint8).copy()
+        hydro = np.ascontiguousarray(hydro, dtype=np.float64).copy()
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        has = np.ascontiguousarray(has, dtype=np.uint8).copy()
+        cov, vac = C.c_int(0), C.c_int(0)
+        st = self.lib.href_apply_obstacle(nx, ny, n, C.c_double(vmax), C.byref(spec), r.ctypes.data_as(C.c_void_p),
+                                          kind.ctypes.data_as(C.c_void_p), _ptr(hydro), _ptr(f),
+                                          has.ctypes.data_as(C.c_void_p), C.c_double(heat_ratio), C.byref(cov),
+                                          C.byref(vac))
+        return st, spec, r, kind, hydro, f, has, cov.value, vac.value
 
     def penalized_imex_step(self, k: RefKernel, f, nx, ny, dx, dy, dt, eps_cell,
                             pen_coeff=2 * np.pi, eps_weno=1e-6):

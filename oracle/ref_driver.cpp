@@ -24,6 +24,8 @@
 #include "hykin/boltzmann.hpp"
 #include "hykin/coupling.hpp"
 #include "hykin/euler.hpp"
+#include "hykin/grid.hpp"
+#include "hykin/obstacle.hpp"
 #include "hykin/errors.hpp"
 #include "hykin/esbgk.hpp"
 #include "hykin/indicators.hpp"
@@ -52,6 +54,8 @@ int status_of(const std::exception_ptr& e) {
         return 5;
     } catch (const positivity_error&) {
         return 8;
+    } catch (const scenario_end_error&) {
+        return 10;
     } catch (...) {
         return 99;
     }
@@ -491,6 +495,73 @@ void href_conserved_from_moments(const double* mom5, double heat_ratio, double* 
     m.T = mom5[4];
     const ConservedState c = conserved_from_moments(m, heat_ratio);
     for (int k = 0; k < 4; ++k) u[k] = c[k];
+}
+
+// ---- obstacles (src/grid.cpp:56-110, src/coupling.cpp:95-147) ----
+struct HrefObstacle {
+    int shape, center_i, center_j, half_i, half_j, radius;
+    double rho, pressure, ux, uy;
+    int move_di, move_dj;
+};
+static ObstacleSpec to_spec(const HrefObstacle& h) {
+    ObstacleSpec o;
+    o.shape = h.shape == 1 ? ObstacleSpec::Shape::rectangle : (h.shape == 2 ? ObstacleSpec::Shape::disk : ObstacleSpec::Shape::none);
+    o.center_i = h.center_i; o.center_j = h.center_j; o.half_i = h.half_i; o.half_j = h.half_j; o.radius = h.radius;
+    o.rho = h.rho; o.pressure = h.pressure; o.ux = h.ux; o.uy = h.uy; o.move_di = h.move_di; o.move_dj = h.move_dj;
+    return o;
+}
+
+int href_classify_cells(int nx, int ny, const HrefObstacle* spec, unsigned char* kind) {
+    try {
+        SpatialGrid g;
+        g.nx = nx;
+        g.ny = ny;
+        const std::vector<CellKind> k = classify_cells(g, to_spec(*spec));
+        for (int c = 0; c < nx * ny; ++c) kind[c] = (unsigned char)k[c];
+        return 0;
+    } catch (...) {
+        return status_of(std::current_exception());
+    }
+}
+
+// Dense f [cells][n^3] in/out; `has` [cells] in/out marks the cells that own a block.
+int href_apply_obstacle(int nx, int ny, int n, double vmax, HrefObstacle* spec, signed char* r, unsigned char* kind,
+                        double* hydro, double* f, unsigned char* has, double heat_ratio, int* covered, int* vacated) {
+    SpatialGrid g;
+    g.nx = nx;
+    g.ny = ny;
+    const VelocityGrid vg = make_velocity_grid(n, vmax);
+    const int cells = nx * ny;
+    const int64_t nb = vg.size();
+    ObstacleSpec o = to_spec(*spec);
+    RegimeMap reg;
+    reg.nx = nx;
+    reg.ny = ny;
+    reg.r.assign(r, r + cells);
+    reg.kind.resize(cells);
+    for (int c = 0; c < cells; ++c) reg.kind[c] = (CellKind)kind[c];
+    ConservedField hy = to_field(hydro, cells);
+    DistributionField df(cells, int(nb));
+    for (int c = 0; c < cells; ++c)
+        if (has[c]) std::memcpy(df.ensure(c).data(), f + c * nb, nb * sizeof(double));
+    int st = 0;
+    try {
+        const ObstacleApplyResult res = apply_obstacle(g, vg, o, reg, hy, df, heat_ratio);
+        *covered = res.covered;
+        *vacated = res.vacated;
+    } catch (...) {
+        st = status_of(std::current_exception());
+    }
+    spec->center_i = o.center_i;
+    spec->center_j = o.center_j;
+    for (int c = 0; c < cells; ++c) {
+        r[c] = reg.r[c];
+        kind[c] = (unsigned char)reg.kind[c];
+        for (int k = 0; k < 4; ++k) hydro[4 * c + k] = hy[c][k];
+        has[c] = df.has(c) ? 1 : 0;
+        if (df.has(c)) std::memcpy(f + c * nb, df[c].data(), nb * sizeof(double));
+    }
+    return st;
 }
 
 } // extern "C"

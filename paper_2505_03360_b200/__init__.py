@@ -25,7 +25,7 @@ from . import _abi
 
 __all__ = [
     "error", "config_error", "aliasing_config_error", "degenerate_state_error",
-    "positivity_error", "contract_violation", "numerical_consistency_error",
+    "positivity_error", "contract_violation", "numerical_consistency_error", "scenario_end_error",
     "VelocityGrid", "make_velocity_grid", "SpectralKernel", "precompute_kernel",
     "precompute_kernel_from_tables", "spectral_collision", "Context", "default_context",
 ]
@@ -62,6 +62,10 @@ class numerical_consistency_error(error):
         self.cell = cell
 
 
+class scenario_end_error(error):
+    """A moving obstacle left the domain (src/coupling.cpp:113-118)."""
+
+
 class device_error(error):
     """CUDA failure (no reference analogue; the reference is CPU-only)."""
 
@@ -76,6 +80,7 @@ _STATUS_EXC = {
     _abi.HK_NCCL: device_error,
     _abi.HK_POSITIVITY: positivity_error,
     _abi.HK_UNSUPPORTED: config_error,
+    _abi.HK_SCENARIO_END: scenario_end_error,
 }
 
 

@@ -23,6 +23,7 @@ HK_CUDA = 6
 HK_NCCL = 7
 HK_POSITIVITY = 8
 HK_UNSUPPORTED = 9
+HK_SCENARIO_END = 10
 
 HK_COMM_ID_BYTES = 128
 HK_IPC_HANDLE_BYTES = 64
@@ -51,6 +52,26 @@ class CellStatus(C.Structure):
 
 
 CELL_STATUS_BYTES = C.sizeof(CellStatus)  # 40
+
+HK_OBSTACLE_NONE, HK_OBSTACLE_RECTANGLE, HK_OBSTACLE_DISK = 0, 1, 2
+HK_CELL_INTERIOR, HK_CELL_OBSTACLE, HK_CELL_FORCED_RING, HK_CELL_GHOST = 0, 1, 2, 3
+
+
+class ObstacleSpec(C.Structure):
+    """hk_obstacle_spec == ObstacleSpec (inc/hykin/obstacle.hpp:9-34)."""
+    _fields_ = [("shape", C.c_int), ("center_i", C.c_int), ("center_j", C.c_int), ("half_i", C.c_int),
+                ("half_j", C.c_int), ("radius", C.c_int), ("rho", C.c_double), ("pressure", C.c_double),
+                ("ux", C.c_double), ("uy", C.c_double), ("move_di", C.c_int), ("move_dj", C.c_int)]
+
+    def __init__(self, shape=HK_OBSTACLE_NONE, center_i=0, center_j=0, half_i=0, half_j=0, radius=0, rho=1.0,
+                 pressure=1.0, ux=0.0, uy=0.0, move_di=0, move_dj=0):
+        super().__init__(shape, center_i, center_j, half_i, half_j, radius, rho, pressure, ux, uy, move_di, move_dj)
+
+    def enabled(self) -> bool:
+        return self.shape != HK_OBSTACLE_NONE
+
+    def temperature(self) -> float:
+        return self.pressure / self.rho
 
 _lib = None
 
@@ -112,6 +133,9 @@ def lib() -> C.CDLL:
         "hk_ctx_comm_info": (C.c_int, [vp, vp, vp]),
         "hk_halo_exchange": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp]),
         "hk_allreduce_scalars": (C.c_int, [vp, vp, i64, C.c_int]),
+        "hk_classify_cells": (C.c_int, [vp, i64, i64, C.POINTER(ObstacleSpec), vp]),
+        "hk_apply_obstacle": (C.c_int, [vp, C.c_int, dbl, C.POINTER(ObstacleSpec), i64, i64, vp, vp, vp, vp, dbl,
+                                        C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -284,17 +284,22 @@ __global__ void __launch_bounds__(NT) moments_kernel(const double* __restrict__ 
 // ---------------------------------------------------------------------------
 // Maxwellian of given moments (src/moments.cpp:88-112)
 // ---------------------------------------------------------------------------
+// dst_idx (optional): cell k is written to block dst_idx[k]; count_dev
+// (optional): the list length lives on the device (at most ncells).
 __global__ void __launch_bounds__(NT) maxwellian_kernel(const double* __restrict__ mom, int64_t ncells, VGrid g,
-                                                        double* __restrict__ out, int* __restrict__ status) {
+                                                        double* __restrict__ out, int* __restrict__ status,
+                                                        const int64_t* __restrict__ dst_idx,
+                                                        const int* __restrict__ count_dev) {
     __shared__ double ex[128], ey[128], ez[128];
     const int n = g.n, nb = n * n * n;
+    if (count_dev) ncells = min(ncells, (int64_t)*count_dev);
     for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
         Mom m{mom[cell * 5], mom[cell * 5 + 1], mom[cell * 5 + 2], mom[cell * 5 + 3], mom[cell * 5 + 4]};
         const bool ok = (m.rho > 0.0) && (m.T > 0.0);
         if (threadIdx.x == 0 && status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
         if (!ok) continue;
         const double pref = maxwell_factors(m, g, ex, ey, ez);
-        double* o = out + cell * nb;
+        double* o = out + (dst_idx ? dst_idx[cell] : cell) * nb;
         for (int idx = threadIdx.x; idx < nb; idx += NT) {
             const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
             o[idx] = pref * ex[k1] * ey[k2] * ez[k3];
@@ -1458,10 +1463,12 @@ int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncel
     return check_cuda(ctx, cudaGetLastError(), "moments kernel");
 }
 
-int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status) {
+int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status,
+                      const int64_t* dst_idx, const int* count_dev) {
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "maxwellian: 2 <= n <= 128");
-    maxwellian_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(mom, ncells, make_vgrid(n, vmax), out, status);
+    maxwellian_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(mom, ncells, make_vgrid(n, vmax), out, status,
+                                                                     dst_idx, count_dev);
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "maxwellian kernel");
 }

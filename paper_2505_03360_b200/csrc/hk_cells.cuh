@@ -6,7 +6,8 @@ namespace hk {
 
 int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncells, double* mom, double* sigma,
                    double* real, double* l1, int* status);
-int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status);
+int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status,
+                      const int64_t* dst_idx = nullptr, const int* count_dev = nullptr);
 int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,
                  const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out,
                  double* k1_out = nullptr, double k1_scale = 0.0);

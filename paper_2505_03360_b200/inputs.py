@@ -323,3 +323,27 @@ def config4_conserved(nx: int = 200, ny: int = 200, xi: float = 5.0 / 3.0, seed_
     p = rho * T
     E = p / (xi - 1.0) + 0.5 * rho * (ux * ux + uy * uy)
     return np.stack([rho, rho * ux, rho * uy, E], -1).reshape(nx * ny, 4)
+
+
+def obstacle_fields(kind: np.ndarray, n: int, seed_salt: int = 0, bad_cells=()):
+    """Pre-update state around an embedded obstacle (src/coupling.cpp:95-147):
+    given the previous classification `kind` (0 interior, 1 obstacle, 2 ring, 3 ghost),
+    returns (r int8, hydro [cells,4], f [cells,n^3], has uint8).  Interior cells get
+    a random regime in {0,1,2}; ring and obstacle cells are Layer 2; obstacle cells
+    own no block (released); every cell with r != 0 owns one.  `bad_cells` get a
+    negative pressure (the reference's moments_from_conserved throws there)."""
+    rng = rng_for(6, seed_salt)
+    cells = kind.size
+    r = np.where(kind == 0, rng.integers(0, 3, cells), 0).astype(np.int8)
+    r[(kind == 1) | (kind == 2)] = 2
+    rho = rng.uniform(0.5, 2.0, cells)
+    u = rng.uniform(-0.3, 0.3, (cells, 2))
+    p = rng.uniform(0.5, 1.5, cells)
+    p[list(bad_cells)] = -0.2
+    hydro = np.empty((cells, 4))
+    hydro[:, 0] = rho
+    hydro[:, 1:3] = rho[:, None] * u
+    hydro[:, 3] = p / (5.0 / 3.0 - 1.0) + 0.5 * rho * (u ** 2).sum(1)
+    has = ((r != 0) & (kind != 1)).astype(np.uint8)
+    f = np.where(has[:, None] != 0, rng.uniform(0.0, 1e-2, (cells, n ** 3)), 0.0)
+    return r, hydro, f, has

@@ -11,7 +11,9 @@ lowest failing cell.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
+from typing import NamedTuple
 from dataclasses import dataclass
 
 import torch
@@ -262,3 +264,37 @@ def scatter_cells(src, idx, dst, ctx=None):
     ctx.check(ctx._lib.hk_scatter_cells(ctx.h, src.shape[1], src.contiguous().data_ptr(), idx.data_ptr(), idx.numel(),
                                         dst.data_ptr()))
     return dst
+
+
+# ---- embedded obstacles (src/grid.cpp:56-110, src/coupling.cpp:95-147) -------
+ObstacleSpec = _abi.ObstacleSpec
+
+
+class ObstacleApplyResult(NamedTuple):  # inc/hykin/coupling.hpp:53-56
+    covered: int
+    vacated: int
+
+
+def classify_cells(nx: int, ny: int, spec: ObstacleSpec, device=0, ctx=None):
+    """CellKind per cell (uint8 device tensor [ny*nx]): 0 interior, 1 obstacle,
+    2 forced ring, 3 ghost.  config_error when the obstacle or its ring
+    reaches the 4-cell ghost frame."""
+    ctx = ctx or default_context(device)
+    kind = torch.empty(nx * ny, dtype=torch.uint8, device=f"cuda:{ctx.device}")
+    ctx.check(ctx._lib.hk_classify_cells(ctx.h, nx, ny, C.byref(spec), kind.data_ptr()))
+    return kind
+
+
+def apply_obstacle(nx: int, ny: int, vgrid: VelocityGrid, spec: ObstacleSpec, r, kind, hydro, f,
+                   heat_ratio: float = 5.0 / 3.0, ctx=None) -> ObstacleApplyResult:
+    """One step of the obstacle update, in place: `spec` moves, r (int8), kind
+    (uint8), hydro [cells,4] and the dense field f [cells,n^3] (device tensors)
+    follow the reference; blocks of newly covered cells are left as they are."""
+    for t, dt in ((r, torch.int8), (kind, torch.uint8), (hydro, torch.float64), (f, torch.float64)):
+        assert t.is_cuda and t.dtype == dt and t.is_contiguous(), "device tensors of the documented dtypes"
+    ctx = ctx or default_context(f.device.index or 0)
+    cov, vac = C.c_int(0), C.c_int(0)
+    ctx.check(ctx._lib.hk_apply_obstacle(ctx.h, vgrid.nv, vgrid.vmax, C.byref(spec), nx, ny, r.data_ptr(),
+                                         kind.data_ptr(), hydro.data_ptr(), f.data_ptr(), heat_ratio, C.byref(cov),
+                                         C.byref(vac)))
+    return ObstacleApplyResult(cov.value, vac.value)

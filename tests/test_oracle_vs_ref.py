@@ -182,3 +182,84 @@ def test_transitions_bitwise(oracle, reflib):
         assert so == sr == 0 and np.array_equal(mo, mr)
         assert np.array_equal(oracle.conserved_from_moments(mo), reflib.conserved_from_moments(mr))
     assert oracle.moments_from_conserved([-1.0, 0, 0, 1.0])[0] == reflib.moments_from_conserved([-1.0, 0, 0, 1.0])[0] == 8
+
+
+def _spec(oracle_mod, shape, ci, cj, hi=0, hj=0, rad=0, mdi=0, mdj=0):
+    s = oracle_mod.Obstacle()
+    s.shape, s.center_i, s.center_j, s.half_i, s.half_j, s.radius = shape, ci, cj, hi, hj, rad
+    s.rho, s.pressure, s.ux, s.uy, s.move_di, s.move_dj = 1.3, 0.9, 0.2, -0.1, mdi, mdj
+    return s
+
+
+def test_obstacle_classify_bitwise(oracle, reflib):
+    """classify_cells (src/grid.cpp:74-110): ghost frame, footprint, 2-cell ring,
+    and the config_error when either touches the ghost frame."""
+    import oracle.oracle as om
+    for nx, ny, spec in ((24, 20, _spec(om, 1, 10, 9, 2, 1)), (24, 24, _spec(om, 2, 12, 12, rad=3)),
+                         (30, 22, _spec(om, 0, 0, 0)), (24, 24, _spec(om, 2, 14, 12, rad=4)),
+                         (24, 24, _spec(om, 1, 7, 12, 0, 0)), (24, 24, _spec(om, 1, 3, 12, 1, 1))):
+        st_o, k_o, bad = oracle.classify_cells(nx, ny, spec)
+        st_r, k_r = reflib.classify_cells(nx, ny, spec)
+        assert st_o == st_r, (spec.center_i, spec.radius)
+        if st_o == 0:
+            assert np.array_equal(k_o, k_r)
+        else:
+            assert st_o == 1 and bad >= 0
+
+
+def test_obstacle_apply_bitwise(oracle, reflib):
+    """apply_obstacle (src/coupling.cpp:95-147) over a moving disk until it leaves
+    the domain (scenario_end_error), a static rectangle, and a forced-ring cell
+    whose state throws mid-loop: r, kind, hydro, the surviving blocks, the
+    moved spec and the covered/vacated counts all bitwise."""
+    import oracle.oracle as om
+    n, nx, ny = 8, 24, 22
+    cases = [(_spec(om, 2, 9, 11, rad=2, mdi=1, mdj=0), 12, ()), (_spec(om, 1, 11, 10, 2, 1), 1, ()),
+             (_spec(om, 1, 11, 10, 2, 1, mdi=1, mdj=1), 2, None)]
+    for spec, steps, bad in cases:
+        _, kind, _ = oracle.classify_cells(nx, ny, spec)
+        if bad is None:  # an interior r=0 cell of the next ring with a negative pressure
+            nxt = spec.copy(); nxt.center_i += 1; nxt.center_j += 1
+            _, k2, _ = oracle.classify_cells(nx, ny, nxt)
+            bad = [int(np.flatnonzero((k2 == 2) & (kind == 0))[3])]
+        r, hydro, f, has = inputs.obstacle_fields(kind, n, seed_salt=steps, bad_cells=bad)
+        if bad:
+            r[bad] = 0; has[bad] = 0; f[bad] = 0.0
+        so = sr = spec
+        ko = kr = kind
+        ro, rr, ho, hr, fo, fr, hs = r, r, hydro, hydro, f, f, has
+        for step in range(steps):
+            st_o, so, ro, ko, ho, fo, co, vo = oracle.apply_obstacle(nx, ny, n, VMAX, so, ro, ko, ho, fo)
+            st_r, sr, rr, kr, hr, fr, hs, cr, vr = reflib.apply_obstacle(nx, ny, n, VMAX, sr, rr, kr, hr, fr, hs)
+            assert st_o == st_r, step
+            assert (so.center_i, so.center_j) == (sr.center_i, sr.center_j)
+            assert np.array_equal(ro, rr) and np.array_equal(ko, kr) and np.array_equal(ho, hr)
+            live = hs != 0
+            assert np.array_equal(fo[live], fr[live])
+            if st_o:
+                break
+            assert (co, vo) == (cr, vr)
+        else:
+            assert not (spec.move_di or spec.move_dj), "moving obstacle should have hit the ghost frame"
+        if spec.move_di and bad == ():
+            assert st_o == 10
+        if bad:
+            assert st_o == 8  # positivity_error from moments_from_conserved
+
+
+def test_obstacle_degenerate_fixed_state(oracle, reflib):
+    """A moving obstacle whose fixed state has T <= 0: maxwellian throws
+    degenerate_state_error at the first vacated cell, after its r and hydro
+    were overwritten (src/coupling.cpp:130-136)."""
+    import oracle.oracle as om
+    n, nx, ny = 8, 24, 22
+    spec = _spec(om, 1, 10, 10, 1, 1, mdi=1)
+    spec.pressure = -0.5
+    _, kind, _ = oracle.classify_cells(nx, ny, spec)
+    r, hydro, f, has = inputs.obstacle_fields(kind, n, seed_salt=3)
+    st_o, so, ro, ko, ho, fo, _, _ = oracle.apply_obstacle(nx, ny, n, VMAX, spec, r, kind, hydro, f)
+    st_r, sr, rr, kr, hr, fr, hs, _, _ = reflib.apply_obstacle(nx, ny, n, VMAX, spec, r, kind, hydro, f, has)
+    assert st_o == st_r == 3
+    assert np.array_equal(ro, rr) and np.array_equal(ko, kr) and np.array_equal(ho, hr)
+    live = (hs != 0) & (has != 0)  # the failing vacated cell had no block before (ensure() made one)
+    assert np.array_equal(fo[live], fr[live])
