@@ -254,6 +254,31 @@ int hk_apply_obstacle(hk_ctx ctx, int n, double vmax, hk_obstacle_spec* spec, in
                       uint8_t* kind_dev, double* hydro_dev, double* f_dev, double heat_ratio, int* covered,
                       int* vacated);
 
+/* ---- cross-layer stencil synthesis (src/coupling.cpp:57-93; SURVEY §8f "next" #1) --
+ * What a stencil at a cell sees in the hybrid field: ghost cells read the
+ * closest interior cell (src/grid.cpp:12-16); obstacle cells the fixed state of
+ * spec (required when any kind is HK_CELL_OBSTACLE, else nullable); layer-0
+ * cells (r == 0) their conserved state; kinetic cells their moments / stored
+ * block.  Grids carry the reference's 4-cell ghost frame (nx, ny >= 9).
+ * Both calls synchronise once to report the reference's exception. */
+/* synthesize_hydro_state for every cell: out_dev [cells][4].  HK_DEGENERATE
+ * (lowest cell) when moments_of of a referenced kinetic block throws. */
+int hk_synthesize_hydro(hk_ctx ctx, int n, double vmax, int64_t nx, int64_t ny, const hk_obstacle_spec* spec,
+                        const int8_t* r_dev, const uint8_t* kind_dev, const double* hydro_dev, const double* f_dev,
+                        double heat_ratio, double* out_dev);
+/* synthesize_distribution.  List mode (idx_dev != NULL): out_dev[k] = the block
+ * seen at cell idx_dev[k], k < count.  Stencil mode (idx_dev == NULL, count and
+ * out_dev ignored): in place in the dense field f_dev, every cell that is not
+ * kinetic (ghost, obstacle or layer 0) but lies on the transport stencil
+ * (+-2 cells along x or y) of a kinetic interior cell gets the synthesized
+ * block, so a kinetic transport sweep over f_dev reads exactly the reference's
+ * neighbours; *filled (nullable) = blocks written.  HK_POSITIVITY /
+ * HK_DEGENERATE (lowest list entry / cell, nothing written) as the reference. */
+int hk_synthesize_distributions(hk_ctx ctx, int n, double vmax, int64_t nx, int64_t ny, const hk_obstacle_spec* spec,
+                                const int8_t* r_dev, const uint8_t* kind_dev, const double* hydro_dev, double* f_dev,
+                                double heat_ratio, const int64_t* idx_dev, int64_t count, double* out_dev,
+                                int64_t* filled);
+
 /* ---- multi-GPU: NCCL communicator of a context ------------
  * One process per GPU.  Rank 0 calls hk_comm_unique_id, the host side ships
  * the 128 opaque bytes to every rank (MPI / torch.distributed / a file), and

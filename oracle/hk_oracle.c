@@ -1447,3 +1447,65 @@ int hko_apply_obstacle(int nx, int ny, int n, double vmax, hko_obstacle* s, sign
     free(nk);
     return first;
 }
+
+/* ===================================================================== */
+/* Cross-layer stencil synthesis (src/coupling.cpp:57-93)                */
+/* ===================================================================== */
+static long hko_clamped(int nx, int ny, int i, int j) { /* SpatialGrid::clamp_interior, src/grid.cpp:12-16 */
+    if (hko_in_ghost(nx, ny, i, j)) {
+        const int ilo = HKO_GHOST, ihi = nx - HKO_GHOST - 1, jlo = HKO_GHOST, jhi = ny - HKO_GHOST - 1;
+        i = i < ilo ? ilo : (i > ihi ? ihi : i);
+        j = j < jlo ? jlo : (j > jhi ? jhi : j);
+    }
+    return (long)j * nx + i;
+}
+
+static hko_moments hko_fixed_moments(const hko_obstacle* s) { /* obstacle_moments, src/coupling.cpp:47-53 */
+    hko_moments m;
+    m.rho = s->rho;
+    m.u[0] = s->ux; m.u[1] = s->uy; m.u[2] = 0.0;
+    m.T = s->pressure / s->rho;
+    return m;
+}
+
+int hko_synthesize_hydro_state(int nx, int ny, int n, double vmax, const hko_obstacle* s, const signed char* r,
+                               const unsigned char* kind, const double* hydro, const double* f, double heat_ratio,
+                               int i, int j, double out[4]) {
+    const long c = hko_clamped(nx, ny, i, j);
+    if (kind[c] == 1) { /* obstacle_state */
+        const hko_moments m = hko_fixed_moments(s);
+        const double m5[5] = {m.rho, m.u[0], m.u[1], m.u[2], m.T};
+        hko_conserved_from_moments(m5, heat_ratio, out);
+        return 0;
+    }
+    if (r[c] == 0) {
+        for (int k = 0; k < 4; ++k) out[k] = hydro[4 * c + k];
+        return 0;
+    }
+    hko_moments m;
+    const int st = hko_moments_of(n, vmax, f + c * (long)n * n * n, &m);
+    if (st) return st;
+    const double m5[5] = {m.rho, m.u[0], m.u[1], m.u[2], m.T};
+    hko_conserved_from_moments(m5, heat_ratio, out);
+    return 0;
+}
+
+int hko_synthesize_distribution(int nx, int ny, int n, double vmax, const hko_obstacle* s, const signed char* r,
+                                const unsigned char* kind, const double* hydro, const double* f, double heat_ratio,
+                                int i, int j, double* out) {
+    const long c = hko_clamped(nx, ny, i, j), nb = (long)n * n * n;
+    if (kind[c] == 1) {
+        const hko_moments m = hko_fixed_moments(s);
+        return hko_maxwellian(&m, n, vmax, out);
+    }
+    if (r[c] == 0) {
+        double m5[5];
+        const int st = hko_moments_from_conserved(hydro + 4 * c, heat_ratio, m5);
+        if (st) return st;
+        hko_moments m;
+        m.rho = m5[0]; m.u[0] = m5[1]; m.u[1] = m5[2]; m.u[2] = m5[3]; m.T = m5[4];
+        return hko_maxwellian(&m, n, vmax, out);
+    }
+    memcpy(out, f + c * nb, sizeof(double) * nb);
+    return 0;
+}

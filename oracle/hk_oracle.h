@@ -178,6 +178,15 @@ int hko_classify_cells(int nx, int ny, const hko_obstacle* s, unsigned char* kin
  * HKO_CONFIG / HKO_SCENARIO_END / HKO_POSITIVITY like the reference throws. */
 int hko_apply_obstacle(int nx, int ny, int n, double vmax, hko_obstacle* s, signed char* r, unsigned char* kind,
                        double* hydro, double* f, double heat_ratio, int* covered, int* vacated);
+/* Cross-layer stencil synthesis (src/coupling.cpp:57-93) at cell (i, j) of an
+ * nx x ny grid: ghost cells read their clamped interior cell (src/grid.cpp:12-16).
+ * hydro [cells][4], f dense [cells][n^3]; s may be NULL when no cell is an obstacle. */
+int hko_synthesize_hydro_state(int nx, int ny, int n, double vmax, const hko_obstacle* s, const signed char* r,
+                               const unsigned char* kind, const double* hydro, const double* f, double heat_ratio,
+                               int i, int j, double out[4]);
+int hko_synthesize_distribution(int nx, int ny, int n, double vmax, const hko_obstacle* s, const signed char* r,
+                                const unsigned char* kind, const double* hydro, const double* f, double heat_ratio,
+                                int i, int j, double* out);
 
 #ifdef __cplusplus
 }

@@ -292,6 +292,26 @@ class Oracle:
                                          C.c_double(heat_ratio), C.byref(cov), C.byref(vac))
         return st, spec, r, kind, hydro, f, cov.value, vac.value
 
+    def synthesize(self, which, nx, ny, n, vmax, spec, r, kind, hydro, f, cells, heat_ratio=5.0 / 3.0):
+        """synthesize_hydro_state (which 0, -> [k,4]) / synthesize_distribution (which 1,
+        -> [k,n^3]) at the (i, j) pairs `cells`; returns (first failing status, out)."""
+        r = np.ascontiguousarray(r, dtype=np.int8)
+        kind = np.ascontiguousarray(kind, dtype=np.uint8)
+        hydro = np.ascontiguousarray(hydro, dtype=np.float64)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        width = 4 if which == 0 else n ** 3
+        out = np.zeros((len(cells), width))
+        fn = self.lib.hko_synthesize_hydro_state if which == 0 else self.lib.hko_synthesize_distribution
+        sp = C.byref(spec) if spec is not None else None
+        for k, (i, j) in enumerate(cells):
+            row = np.zeros(width)
+            st = fn(nx, ny, n, C.c_double(vmax), sp, r.ctypes.data_as(C.c_void_p), kind.ctypes.data_as(C.c_void_p),
+                    _ptr(hydro), _ptr(f), C.c_double(heat_ratio), int(i), int(j), _ptr(row))
+            if st:
+                return st, out
+            out[k] = row
+        return 0, out
+
     def penalized_imex_step(self, k: OracleKernel, f, nx, ny, dx, dy, dt, eps_cell,
                             pen_coeff=2 * np.pi, eps_weno=1e-6):
         f = np.ascontiguousarray(f, dtype=np.float64).copy()
@@ -503,6 +523,21 @@ class RefLib:
                                           has.ctypes.data_as(C.c_void_p), C.c_double(heat_ratio), C.byref(cov),
                                           C.byref(vac))
         return st, spec, r, kind, hydro, f, has, cov.value, vac.value
+
+    def synthesize(self, which, nx, ny, n, vmax, spec, r, kind, hydro, f, has, cells, heat_ratio=5.0 / 3.0):
+        r = np.ascontiguousarray(r, dtype=np.int8)
+        kind = np.ascontiguousarray(kind, dtype=np.uint8)
+        hydro = np.ascontiguousarray(hydro, dtype=np.float64)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        has = np.ascontiguousarray(has, dtype=np.uint8)
+        ij = np.ascontiguousarray(np.asarray(cells, dtype=np.int32).reshape(-1, 2))
+        ii, jj = np.ascontiguousarray(ij[:, 0]), np.ascontiguousarray(ij[:, 1])
+        out = np.zeros((len(ij), 4 if which == 0 else n ** 3))
+        st = self.lib.href_synthesize(which, nx, ny, n, C.c_double(vmax), C.byref(spec) if spec is not None else None,
+                                      r.ctypes.data_as(C.c_void_p), kind.ctypes.data_as(C.c_void_p), _ptr(hydro),
+                                      _ptr(f), has.ctypes.data_as(C.c_void_p), C.c_double(heat_ratio), _ptr(ii),
+                                      _ptr(jj), len(ij), _ptr(out))
+        return st, out
 
     def penalized_imex_step(self, k: RefKernel, f, nx, ny, dx, dy, dt, eps_cell,
                             pen_coeff=2 * np.pi, eps_weno=1e-6):

@@ -564,4 +564,54 @@ int href_apply_obstacle(int nx, int ny, int n, double vmax, HrefObstacle* spec, 
     return st;
 }
 
+// ---- cross-layer stencil synthesis (src/coupling.cpp:57-93), for cells (ii[k], jj[k]) ----
+int href_synthesize(int which, int nx, int ny, int n, double vmax, const HrefObstacle* spec, const signed char* r,
+                    const unsigned char* kind, const double* hydro, const double* f, const unsigned char* has,
+                    double heat_ratio, const int* ii, const int* jj, int count, double* out) {
+    SpatialGrid g;
+    g.nx = nx;
+    g.ny = ny;
+    const VelocityGrid vg = make_velocity_grid(n, vmax);
+    const int cells = nx * ny;
+    const int64_t nb = vg.size();
+    ObstacleSpec o;
+    if (spec) o = to_spec(*spec);
+    RegimeMap reg;
+    reg.nx = nx;
+    reg.ny = ny;
+    reg.r.assign(r, r + cells);
+    reg.kind.resize(cells);
+    for (int c = 0; c < cells; ++c) reg.kind[c] = (CellKind)kind[c];
+    ConservedField hy = to_field(hydro, cells);
+    DistributionField df(cells, int(nb));
+    for (int c = 0; c < cells; ++c)
+        if (has[c]) std::memcpy(df.ensure(c).data(), f + c * nb, nb * sizeof(double));
+    StageView v;
+    v.grid = &g;
+    v.vgrid = &vg;
+    v.regime = &reg;
+    v.hydro = &hy;
+    v.f = &df;
+    v.obstacle = spec ? &o : nullptr;
+    v.heat_ratio = heat_ratio;
+    std::vector<double> scratch;
+    for (int k = 0; k < count; ++k) {
+        try {
+            if (which == 0) {
+                const ConservedState u = synthesize_hydro_state(v, ii[k], jj[k]);
+                out[4 * k + 0] = u.rho;
+                out[4 * k + 1] = u.mx;
+                out[4 * k + 2] = u.my;
+                out[4 * k + 3] = u.E;
+            } else {
+                const double* p = synthesize_distribution(v, ii[k], jj[k], scratch);
+                std::memcpy(out + k * nb, p, nb * sizeof(double));
+            }
+        } catch (...) {
+            return status_of(std::current_exception());
+        }
+    }
+    return 0;
+}
+
 } // extern "C"

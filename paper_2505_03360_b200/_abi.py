@@ -134,6 +134,10 @@ def lib() -> C.CDLL:
         "hk_halo_exchange": (C.c_int, [vp, C.c_int, vp, i64, i64, vp, vp]),
         "hk_allreduce_scalars": (C.c_int, [vp, vp, i64, C.c_int]),
         "hk_classify_cells": (C.c_int, [vp, i64, i64, C.POINTER(ObstacleSpec), vp]),
+        "hk_synthesize_hydro": (C.c_int, [vp, C.c_int, dbl, i64, i64, C.POINTER(ObstacleSpec), vp, vp, vp, vp, dbl,
+                                          vp]),
+        "hk_synthesize_distributions": (C.c_int, [vp, C.c_int, dbl, i64, i64, C.POINTER(ObstacleSpec), vp, vp, vp, vp,
+                                                  dbl, vp, i64, vp, C.POINTER(C.c_int64)]),
         "hk_apply_obstacle": (C.c_int, [vp, C.c_int, dbl, C.POINTER(ObstacleSpec), i64, i64, vp, vp, vp, vp, dbl,
                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     }

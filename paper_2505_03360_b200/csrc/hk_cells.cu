@@ -214,12 +214,14 @@ __device__ __forceinline__ double quad_factor(const double x[5], double vx, doub
 __global__ void __launch_bounds__(NT) moments_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
                                                      double* __restrict__ mom, double* __restrict__ sigma,
                                                      double* __restrict__ real, double* __restrict__ l1,
-                                                     int* __restrict__ status) {
+                                                     int* __restrict__ status, const int64_t* __restrict__ src_idx,
+                                                     const int* __restrict__ count_dev) {
     __shared__ double scratch[8 * 25];
     __shared__ double ex[128], ey[128], ez[128];
     const int n = g.n, nb = n * n * n;
+    if (count_dev) ncells = min(ncells, (int64_t)*count_dev);
     for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
-        const double* fc = f + cell * nb;
+        const double* fc = f + (src_idx ? src_idx[cell] : cell) * nb;
         double s[11];
         raw_sums(fc, g, s, scratch);
         Mom m;
@@ -667,14 +669,17 @@ __device__ void coupling_from_monomials(const double (&M)[14], const double uc[3
 __global__ void __launch_bounds__(32 * WPB, HK_MOM_MINB) moments_warp_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
                                                               int lg, double* __restrict__ mom,
                                                               double* __restrict__ sigma, double* __restrict__ real,
-                                                              double* __restrict__ l1, int* __restrict__ status) {
+                                                              double* __restrict__ l1, int* __restrict__ status,
+                                                              const int64_t* __restrict__ src_idx,
+                                                              const int* __restrict__ count_dev) {
     __shared__ double tab[WPB][3][64];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* ex = tab[wid][0];
     double* ey = tab[wid][1];
     double* ez = tab[wid][2];
+    if (count_dev) ncells = min(ncells, (int64_t)*count_dev);
     for (int64_t cell = (int64_t)blockIdx.x * WPB + wid; cell < ncells; cell += (int64_t)gridDim.x * WPB) {
-        const double* fc = f + cell * g.n * g.n * g.n;
+        const double* fc = f + (src_idx ? src_idx[cell] : cell) * g.n * g.n * g.n;
         double s[11];
         raw_sums_w(fc, g, lg, s);
         Mom m;
@@ -975,14 +980,16 @@ template <int MT, int MINB>
 __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
                                                             int lg, double* __restrict__ mom, double* __restrict__ sigma,
                                                             double* __restrict__ real, double* __restrict__ l1,
-                                                            int* __restrict__ status) {
+                                                            int* __restrict__ status, const int64_t* __restrict__ src_idx,
+                                                     const int* __restrict__ count_dev) {
     __shared__ double red[MT / 32][16];
     __shared__ double tabs[3][128];
     __shared__ double bc[8];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = g.n, nb = n * n * n, npairs = nb >> 1;
+    if (count_dev) ncells = min(ncells, (int64_t)*count_dev);
     for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
-        const double* fc = f + cell * nb;
+        const double* fc = f + (src_idx ? src_idx[cell] : cell) * nb;
         double M[14];  // S, Sx, Sy, Sz, Sxx, Sxy, Sxz, Syy, Syz, Szz, Rx, Ry, Rz, Q4
 #pragma unroll
         for (int k = 0; k < 14; ++k) M[k] = 0.0;
@@ -1439,7 +1446,8 @@ int grid_for(hk_ctx ctx, int64_t ncells) {
 }  // namespace
 
 int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncells, double* mom, double* sigma,
-                   double* real, double* l1, int* status) {
+                   double* real, double* l1, int* status, const int64_t* src_idx,
+                   const int* count_dev) {
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "moments: 2 <= n <= 128");
     static const int mom_var = getenv("HK_MOM_VAR") ? atoi(getenv("HK_MOM_VAR")) : 3;  // CTAs per SM x 256 threads
@@ -1448,17 +1456,17 @@ int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncel
         const int grid = int(ncells < cap ? ncells : cap);
         const VGrid g = make_vgrid(n, vmax);
         if (mom_var == 1)
-            moments_cta_kernel<512, 1><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status);
+            moments_cta_kernel<512, 1><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev);
         else if (mom_var <= 3)
-            moments_cta_kernel<256, 3><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status);
+            moments_cta_kernel<256, 3><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev);
         else
-            moments_cta_kernel<256, 4><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status);
+            moments_cta_kernel<256, 4><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev);
     } else if (warp_path(n))
         moments_warp_kernel<<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), log2i(n),
-                                                                                  mom, sigma, real, l1, status);
+                                                                                  mom, sigma, real, l1, status, src_idx, count_dev);
     else
         moments_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), mom, sigma, real,
-                                                                      l1, status);
+                                                                      l1, status, src_idx, count_dev);
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "moments kernel");
 }

@@ -5,7 +5,8 @@
 namespace hk {
 
 int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncells, double* mom, double* sigma,
-                   double* real, double* l1, int* status);
+                   double* real, double* l1, int* status, const int64_t* src_idx = nullptr,
+                   const int* count_dev = nullptr);
 int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t ncells, double* out, int* status,
                       const int64_t* dst_idx = nullptr, const int* count_dev = nullptr);
 int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,

@@ -298,3 +298,43 @@ def apply_obstacle(nx: int, ny: int, vgrid: VelocityGrid, spec: ObstacleSpec, r,
                                          kind.data_ptr(), hydro.data_ptr(), f.data_ptr(), heat_ratio, C.byref(cov),
                                          C.byref(vac)))
     return ObstacleApplyResult(cov.value, vac.value)
+
+
+# ---- cross-layer stencil synthesis (src/coupling.cpp:57-93) ------------------
+def _stage_view_args(r, kind, hydro, f):
+    for t, dt in ((r, torch.int8), (kind, torch.uint8), (hydro, torch.float64), (f, torch.float64)):
+        assert t.is_cuda and t.dtype == dt and t.is_contiguous(), "device tensors of the documented dtypes"
+
+
+def synthesize_hydro_state(nx: int, ny: int, vgrid: VelocityGrid, r, kind, hydro, f, spec: ObstacleSpec = None,
+                           heat_ratio: float = 5.0 / 3.0, ctx=None):
+    """The conserved state a stencil sees at every cell ([cells, 4] device tensor)."""
+    _stage_view_args(r, kind, hydro, f)
+    ctx = ctx or default_context(f.device.index or 0)
+    out = torch.empty((nx * ny, 4), dtype=torch.float64, device=f.device)
+    ctx.check(ctx._lib.hk_synthesize_hydro(ctx.h, vgrid.nv, vgrid.vmax, nx, ny,
+                                           C.byref(spec) if spec is not None else None, r.data_ptr(), kind.data_ptr(),
+                                           hydro.data_ptr(), f.data_ptr(), heat_ratio, out.data_ptr()))
+    return out
+
+
+def synthesize_distribution(nx: int, ny: int, vgrid: VelocityGrid, r, kind, hydro, f, cells=None,
+                            spec: ObstacleSpec = None, heat_ratio: float = 5.0 / 3.0, ctx=None):
+    """cells (int64 tensor of cell indices): the blocks a stencil sees there,
+    [len(cells), n^3].  cells None: fills the transport-stencil halo of the
+    kinetic cells in place in f and returns the number of blocks written."""
+    _stage_view_args(r, kind, hydro, f)
+    ctx = ctx or default_context(f.device.index or 0)
+    sp = C.byref(spec) if spec is not None else None
+    filled = C.c_int64(0)
+    if cells is None:
+        ctx.check(ctx._lib.hk_synthesize_distributions(ctx.h, vgrid.nv, vgrid.vmax, nx, ny, sp, r.data_ptr(),
+                                                       kind.data_ptr(), hydro.data_ptr(), f.data_ptr(), heat_ratio,
+                                                       None, 0, None, C.byref(filled)))
+        return filled.value
+    idx = cells.to(device=f.device, dtype=torch.int64).contiguous()
+    out = torch.empty((idx.numel(), vgrid.nv ** 3), dtype=torch.float64, device=f.device)
+    ctx.check(ctx._lib.hk_synthesize_distributions(ctx.h, vgrid.nv, vgrid.vmax, nx, ny, sp, r.data_ptr(),
+                                                   kind.data_ptr(), hydro.data_ptr(), f.data_ptr(), heat_ratio,
+                                                   idx.data_ptr(), idx.numel(), out.data_ptr(), C.byref(filled)))
+    return out

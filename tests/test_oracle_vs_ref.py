@@ -263,3 +263,48 @@ def test_obstacle_degenerate_fixed_state(oracle, reflib):
     assert np.array_equal(ro, rr) and np.array_equal(ko, kr) and np.array_equal(ho, hr)
     live = (hs != 0) & (has != 0)  # the failing vacated cell had no block before (ensure() made one)
     assert np.array_equal(fo[live], fr[live])
+
+
+def _synth_state(oracle, om, nx=20, ny=18, n=8, seed=5, bad=()):
+    """A mixed field: ghost frame, an obstacle with its ring, random regimes."""
+    spec = _spec(om, 2, 9, 9, rad=2)
+    _, kind, _ = oracle.classify_cells(nx, ny, spec)
+    r, hydro, f, has = inputs.obstacle_fields(kind, n, seed_salt=seed, bad_cells=bad)
+    # kinetic blocks with a physical moment structure (moments_of must succeed)
+    rng = np.random.default_rng(seed)
+    for c in np.flatnonzero(has):
+        f[c] = inputs.maxwellian(n, rng.uniform(0.5, 2), rng.uniform(-0.3, 0.3, 3), rng.uniform(0.6, 1.5))
+    cells = [(i, j) for j in range(ny) for i in range(nx)]
+    return spec, kind, r, hydro, f, has, cells
+
+
+def test_stencil_synthesis_bitwise(oracle, reflib):
+    """synthesize_hydro_state / synthesize_distribution (src/coupling.cpp:57-93)
+    at every cell of a mixed field, ghost frame included."""
+    import oracle.oracle as om
+    nx, ny, n = 20, 18, 8
+    spec, kind, r, hydro, f, has, cells = _synth_state(oracle, om, nx, ny, n)
+    for which in (0, 1):
+        st_o, out_o = oracle.synthesize(which, nx, ny, n, VMAX, spec, r, kind, hydro, f, cells)
+        st_r, out_r = reflib.synthesize(which, nx, ny, n, VMAX, spec, r, kind, hydro, f, has, cells)
+        assert st_o == st_r == 0
+        assert np.array_equal(out_o, out_r), which
+
+
+def test_stencil_synthesis_errors(oracle, reflib):
+    """A layer-0 cell with negative pressure: positivity_error from the
+    distribution synthesis; a kinetic block with rho <= 0: degenerate_state_error
+    from the hydro synthesis."""
+    import oracle.oracle as om
+    nx, ny, n = 20, 18, 8
+    spec, kind, r, hydro, f, has, cells = _synth_state(oracle, om, nx, ny, n)
+    c0 = int(np.flatnonzero((r == 0) & (kind == 0))[0])
+    hydro = hydro.copy(); hydro[c0, 3] = -1.0
+    ij = [(c0 % nx, c0 // nx)]
+    assert oracle.synthesize(1, nx, ny, n, VMAX, spec, r, kind, hydro, f, ij)[0] == 8
+    assert reflib.synthesize(1, nx, ny, n, VMAX, spec, r, kind, hydro, f, has, ij)[0] == 8
+    c1 = int(np.flatnonzero((r != 0) & (kind == 0))[0])
+    f = f.copy(); f[c1] = -f[c1]
+    ij = [(c1 % nx, c1 // nx)]
+    assert oracle.synthesize(0, nx, ny, n, VMAX, spec, r, kind, hydro, f, ij)[0] == 3
+    assert reflib.synthesize(0, nx, ny, n, VMAX, spec, r, kind, hydro, f, has, ij)[0] == 3
