@@ -743,6 +743,15 @@ __global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
 // (pp = 0, 1) for each warp.  TMEM (512 columns): F of plane pw + 4 pp at
 // 128 pp, gain at 256 + 64 pp.
 // ---------------------------------------------------------------------------
+#ifndef HK_FFT_FMA
+#define HK_FFT_FMA 1  // FMA butterflies (fft_fma) in the 12-warp kernel
+#endif
+template <int N, bool INV>
+__device__ __forceinline__ void fft_w(double2 (&x)[N]) {
+    if constexpr (HK_FFT_FMA) fft_fma<N, INV>(x);
+    else fft_reg<N, INV>(x);
+}
+
 template <int N, int C>
 struct GeoW {
     static constexpr int P = N / C;   // planes per CTA
@@ -835,7 +844,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                     double2 x[N];
 #pragma unroll
                     for (int i = 0; i < N; ++i) x[i] = row[i];
-                    fft_reg<N, false>(x);
+                    fft_w<N, false>(x);
 #pragma unroll
                     for (int i = 0; i < N; ++i) row[i] = x[i];
                 }
@@ -844,7 +853,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                 double2 x[N];
 #pragma unroll
                 for (int i = 0; i < N; ++i) x[i] = wbuf[k2 + i * ROW];
-                fft_reg<N, false>(x);
+                fft_w<N, false>(x);
                 if (pp == 0) acquire(g);
                 double2* Xs = X + (int64_t)(g % D) * SLOT;
 #pragma unroll
@@ -892,7 +901,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                         issue_w(e, pp + 1);
                     else if (e + 1 < n_entries)
                         issue_w(e + 1, 0);
-                    fft_reg<N, true>(x);
+                    fft_w<N, true>(x);
                     if (pp == 0) acquire(g);
                     double2* Xs = X + (int64_t)(g % D) * SLOT;
                     const int i1 = r * P + pw + 4 * pp;
@@ -944,7 +953,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                 double2 x[N];
 #pragma unroll
                 for (int i = 0; i < N; ++i) x[i] = row[i];
-                fft_reg<N, false>(x);
+                fft_w<N, false>(x);
                 const double s = 1.0 / double(NB);
 #pragma unroll
                 for (int c = 0; c < N / 4; ++c) {
@@ -988,7 +997,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                     double2 y[N];
 #pragma unroll
                     for (int i = 0; i < N; ++i) y[i] = row[i];
-                    fft_reg<N, true>(y);
+                    fft_w<N, true>(y);
 #pragma unroll
                     for (int i = 0; i < N; ++i) row[i] = y[i];
                 }
@@ -1001,7 +1010,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                 }
                 __syncwarp();  // buffer free: the next field's pull overlaps this transform
                 if (more) issue(g + 1);
-                fft_reg<N, true>(y);
+                fft_w<N, true>(y);
                 if (!is_loss) {
                     const double m = (e == 0) ? a.mult0 : 1.0;
                     uint32_t g0[32], g1[32];

@@ -105,6 +105,51 @@ __device__ __forceinline__ void fft_reg(double2 (&x)[N]) {
     for (int i = 0; i < N; ++i) x[i] = y[i];
 }
 
+// Same transform, radix-2 decimation in time with FMA butterflies: the
+// twiddled butterfly (a + w b, a - w b) is o0 = fma(w, b, a) in 4 DFMA and
+// o1 = 2a - o0 in 2 DFMA (6 fp64 instructions instead of 4 DADD + 2 DMUL +
+// 2 DFMA); trivial twiddles (1, -+i) stay 4 DADD.  456 -> 388 fp64
+// instructions per 32-point pencil.  Bit-reversed renaming on input.
+template <int N, int LEN, bool INV>
+__device__ __forceinline__ void fft_fma_stage(double2 (&y)[N]) {
+    constexpr int HALF = LEN / 2;
+#pragma unroll
+    for (int i = 0; i < N; i += LEN) {
+#pragma unroll
+        for (int j = 0; j < HALF; ++j) {
+            const int k = j * (N / LEN);
+            const double2 a = y[i + j], b = y[i + j + HALF];
+            if (k == 0) {
+                y[i + j] = cadd(a, b);
+                y[i + j + HALF] = csub(a, b);
+            } else if (4 * k == N) {  // w = -i (forward) / +i (inverse)
+                const double2 t = INV ? make_double2(-b.y, b.x) : make_double2(b.y, -b.x);
+                y[i + j] = cadd(a, t);
+                y[i + j + HALF] = csub(a, t);
+            } else {
+                // constant-bank twiddle operands; the conjugate (INV) flips register signs only
+                const double2 w = c_tw64[k * (64 / N)];
+                const double by = INV ? b.y : -b.y, bx = INV ? -b.x : b.x;
+                const double2 o0 = make_double2(__fma_rn(w.x, b.x, __fma_rn(w.y, by, a.x)),
+                                                __fma_rn(w.x, b.y, __fma_rn(w.y, bx, a.y)));
+                y[i + j] = o0;
+                y[i + j + HALF] = make_double2(__fma_rn(2.0, a.x, -o0.x), __fma_rn(2.0, a.y, -o0.y));
+            }
+        }
+    }
+    if constexpr (LEN < N) fft_fma_stage<N, 2 * LEN, INV>(y);
+}
+
+template <int N, bool INV>
+__device__ __forceinline__ void fft_fma(double2 (&x)[N]) {
+    double2 y[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) y[i] = x[bitrev<N>(i)];
+    fft_fma_stage<N, 2, INV>(y);
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = y[i];
+}
+
 // Cluster barrier split into arrive (release) / wait (acquire) so that
 // independent work can run between the two (PTX barrier.cluster).
 __device__ __forceinline__ void cluster_arrive() {
