@@ -976,7 +976,7 @@ __global__ void __launch_bounds__(32 * WPB, HK_STAGE_MINB) residual_finish_warp_
 #define HK_MOM_UNROLL 8  // loads in flight per thread: 2 -> 7.4 ms, 4 -> 6.0, 8 -> 5.8 (config 3)
 #endif
 constexpr int kMomUnroll = HK_MOM_UNROLL;
-template <int MT, int MINB>
+template <int MT, int MINB, int UNR = kMomUnroll>
 __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
                                                             int lg, double* __restrict__ mom, double* __restrict__ sigma,
                                                             double* __restrict__ real, double* __restrict__ l1,
@@ -984,40 +984,62 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
                                                      const int* __restrict__ count_dev) {
     __shared__ double red[MT / 32][16];
     __shared__ double tabs[3][128];
+    __shared__ double2 xpow[128][2];  // (vx, vx^2), (vx^3, vx^4) per k1
     __shared__ double bc[8];
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int n = g.n, nb = n * n * n, npairs = nb >> 1;
+    const int n = g.n, nb = n * n * n;
     if (count_dev) ncells = min(ncells, (int64_t)*count_dev);
+    for (int k = t; k < n; k += MT) {
+        const double v = g.node(k), v2 = v * v;
+        xpow[k][0] = make_double2(v, v2);
+        xpow[k][1] = make_double2(v2 * v, v2 * v2);
+    }
+    __syncthreads();
     for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
         const double* fc = f + (src_idx ? src_idx[cell] : cell) * nb;
         double M[14];  // S, Sx, Sy, Sz, Sxx, Sxy, Sxz, Syy, Syz, Szz, Rx, Ry, Rz, Q4
 #pragma unroll
         for (int k = 0; k < 14; ++k) M[k] = 0.0;
-#pragma unroll kMomUnroll
-        for (int p = t; p < npairs; p += MT) {
-            const int idx = 2 * p;
-            const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
-            const double vx = g.node(k1), vy = g.node(k2), z0 = g.node(k3), z1 = g.node(k3 + 1);
-            const double2 w = ldg2(fc + idx);
-            const double zz0 = z0 * z0, zz1 = z1 * z1;
-            const double m0 = w.x + w.y, m1 = z0 * w.x + z1 * w.y, m2 = zz0 * w.x + zz1 * w.y;
-            const double m3 = zz0 * (z0 * w.x) + zz1 * (z1 * w.y), m4 = zz0 * (zz0 * w.x) + zz1 * (zz1 * w.y);
-            const double xx = vx * vx, yy = vy * vy, r2 = xx + yy;
-            M[0] += m0;
-            M[1] += vx * m0;
-            M[2] += vy * m0;
-            M[3] += m1;
-            M[4] += xx * m0;
-            M[5] += vx * (vy * m0);
-            M[6] += vx * m1;
-            M[7] += yy * m0;
-            M[8] += vy * m1;
-            M[9] += m2;
-            const double a = r2 * m0 + m2;
-            M[10] += vx * a;
-            M[11] += vy * a;
-            M[12] += r2 * m1 + m3;
-            M[13] += r2 * (r2 * m0 + 2.0 * m2) + m4;
+        // Column form: a thread owns the k1-columns of two adjacent (k2, k3)
+        // nodes and accumulates A_a = sum_k1 vx^a f (a <= 4: 5 fp64 per node,
+        // vx powers from shared memory); the 14 moments follow per column from
+        // A_a and the column's (vy, vz) (src/moments.cpp:21-86 sums the same
+        // monomials; only the summation order differs).
+        for (int cp = t; cp < (n << lg) / 2; cp += MT) {
+            const int col = 2 * cp, k2 = col >> lg, k3 = col & (n - 1);
+            const double* fcol = fc + col;
+            double A0[5] = {0, 0, 0, 0, 0}, A1[5] = {0, 0, 0, 0, 0};
+#pragma unroll UNR
+            for (int k1 = 0; k1 < n; ++k1) {
+                const double2 w = ldg2(fcol + ((int64_t)k1 << (2 * lg)));
+                const double2 p12 = xpow[k1][0], p34 = xpow[k1][1];
+                A0[0] += w.x; A1[0] += w.y;
+                A0[1] += p12.x * w.x; A1[1] += p12.x * w.y;
+                A0[2] += p12.y * w.x; A1[2] += p12.y * w.y;
+                A0[3] += p34.x * w.x; A1[3] += p34.x * w.y;
+                A0[4] += p34.y * w.x; A1[4] += p34.y * w.y;
+            }
+            const double vy = g.node(k2), yy = vy * vy;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double* A = h ? A1 : A0;
+                const double vz = g.node(k3 + h), rho2 = yy + vz * vz;
+                M[0] += A[0];
+                M[1] += A[1];
+                M[2] += vy * A[0];
+                M[3] += vz * A[0];
+                M[4] += A[2];
+                M[5] += vy * A[1];
+                M[6] += vz * A[1];
+                M[7] += yy * A[0];
+                M[8] += vy * (vz * A[0]);
+                M[9] += vz * (vz * A[0]);
+                const double b = A[2] + rho2 * A[0];
+                M[10] += A[3] + rho2 * A[1];
+                M[11] += vy * b;
+                M[12] += vz * b;
+                M[13] += A[4] + rho2 * (2.0 * A[2] + rho2 * A[0]);
+            }
         }
 #pragma unroll
         for (int k = 0; k < 14; ++k)
@@ -1089,13 +1111,16 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
             const double pref = m.rho / pow(2.0 * M_PI * m.T, 1.5);
             __syncthreads();
             double acc = 0.0;
-#pragma unroll kMomUnroll
-            for (int p = t; p < npairs; p += MT) {
-                const int idx = 2 * p;
-                const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
-                const double2 w = ldg2(fc + idx);
-                const double pxy = pref * tabs[0][k1] * tabs[1][k2];
-                acc += fabs(w.x - pxy * tabs[2][k3]) + fabs(w.y - pxy * tabs[2][k3 + 1]);
+            for (int cp = t; cp < (n << lg) / 2; cp += MT) {  // same column form
+                const int col = 2 * cp, k2 = col >> lg, k3 = col & (n - 1);
+                const double* fcol = fc + col;
+                const double py0 = pref * tabs[1][k2] * tabs[2][k3], py1 = pref * tabs[1][k2] * tabs[2][k3 + 1];
+#pragma unroll UNR
+                for (int k1 = 0; k1 < n; ++k1) {
+                    const double2 w = ldg2(fcol + ((int64_t)k1 << (2 * lg)));
+                    const double ex = tabs[0][k1];
+                    acc += fabs(w.x - py0 * ex) + fabs(w.y - py1 * ex);
+                }
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -1126,6 +1151,24 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
 // raw sums -> Sigma / LLT / inverse -> coupling matrix (14 monomial moments of
 // the equilibrium) -> FullPivLU solve -> blended output.
 // ---------------------------------------------------------------------------
+// 14 monomial moments (S, S_i, S_ij, R_i, Q4) of a pencil from its k3 sums m_c = sum z^c e
+__device__ __forceinline__ void acc14(double (&M)[14], double vx, double vy, double m0, double m1, double m2, double m3,
+                                      double m4) {
+    const double xx = vx * vx, yy = vy * vy, r2 = xx + yy;
+    M[0] += m0;
+    M[1] += vx * m0; M[2] += vy * m0; M[3] += m1;
+    M[4] += xx * m0; M[5] += vx * (vy * m0); M[6] += vx * m1;
+    M[7] += yy * m0; M[8] += vy * m1; M[9] += m2;
+    const double aa = r2 * m0 + m2;
+    M[10] += vx * aa; M[11] += vy * aa; M[12] += r2 * m1 + m3;
+    M[13] += r2 * (r2 * m0 + 2.0 * m2) + m4;
+}
+
+// Bank swizzle of the pass-3 (Z, ZQ) table: the 8 threads of a pencil read
+// entries 4 s + j (s = 0..7) at once; slot = k ^ ((k >> 3) & 3) in the low
+// three bits puts them in 8 distinct 16-byte bank groups.
+__device__ __forceinline__ int zq_slot(int k) { return (k & ~7) | ((k & 7) ^ ((k >> 3) & 3)); }
+
 #ifndef HK_STAGE_U1
 #define HK_STAGE_U1 8  // pass-1 loads in flight: 2 -> 15.4 ms, 4 -> 14.7, 8 -> 14.3 (config 3 ES-BGK stage)
 #endif
@@ -1150,6 +1193,9 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
     double* Ztab = Rtab + n * n;   // [n]
     double* red = Ztab + n;        // [MT/32][16]
     double* par = red + (MT / 32) * 16;  // [32]
+    double2* xpow = reinterpret_cast<double2*>(par + 32);  // [n] (vx, vx^2)
+    double* Htab = par + 32 + 2 * n;   // [n][6]: z^c Z(k3), c <= 4 (pass-2 Horner coefficients)
+    double2* ZQ = reinterpret_cast<double2*>(Htab + 6 * n);  // [n]: (Z, Z Q) of pass 3
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     auto block_reduce = [&](double* v, int K) {  // sum of K values over the CTA -> par[16..16+K) (K <= 14)
         for (int k = 0; k < K; ++k)
@@ -1165,41 +1211,49 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
         }
         __syncthreads();
     };
+    for (int k = t; k < n; k += MT) {
+        const double v = g.node(k);
+        xpow[k] = make_double2(v, v * v);
+    }
+    __syncthreads();
     for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
         const double* fc = fin + cell * nb;
         double* oc = out + cell * nb;
         const double eps = eps_cell ? eps_cell[cell] : eps_scalar;
-        // ---- pass 1: raw sums ----
+        // ---- pass 1: raw sums, column form (moments_cta_kernel): a thread owns the
+        // k1-columns of two adjacent (k2, k3) nodes, A_a = sum_k1 vx^a f (a <= 2) ----
         {
             double s[11];
 #pragma unroll
             for (int k = 0; k < 11; ++k) s[k] = 0.0;
+            for (int cp = t; cp < (n << lg) / 2; cp += MT) {
+                const int col = 2 * cp, k2 = col >> lg, k3 = col & (n - 1);
+                const double* fcol = fc + col;
+                double A[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll kStageU1
-            for (int q = t; q < ngroups; q += MT) {
-                const int idx = 4 * q;
-                const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
-                const double vx = g.node(k1), vy = g.node(k2);
-                const double2 wa = ldg2(fc + idx), wb = ldg2(fc + idx + 2);
-                const double w[4] = {wa.x, wa.y, wb.x, wb.y};
-                double c0 = 0, cz = 0, czz = 0;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const double z = g.node(k3 + j);
-                    c0 += w[j];
-                    cz += z * w[j];
-                    czz += z * (z * w[j]);
+                for (int k1 = 0; k1 < n; ++k1) {
+                    const double2 w = ldg2(fcol + ((int64_t)k1 << (2 * lg)));
+                    const double2 p = xpow[k1];
+                    A[0][0] += w.x; A[1][0] += w.y;
+                    A[0][1] += p.x * w.x; A[1][1] += p.x * w.y;
+                    A[0][2] += p.y * w.x; A[1][2] += p.y * w.y;
                 }
-                s[0] += c0;
-                s[1] += vx * c0;
-                s[2] += vy * c0;
-                s[3] += cz;
-                s[4] += (vx * vx + vy * vy) * c0 + czz;
-                s[5] += vx * (vx * c0);
-                s[6] += vx * (vy * c0);
-                s[7] += vx * cz;
-                s[8] += vy * (vy * c0);
-                s[9] += vy * cz;
-                s[10] += czz;
+                const double vy = g.node(k2);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double vz = g.node(k3 + h);
+                    s[0] += A[h][0];
+                    s[1] += A[h][1];
+                    s[2] += vy * A[h][0];
+                    s[3] += vz * A[h][0];
+                    s[4] += A[h][2] + (vy * vy + vz * vz) * A[h][0];
+                    s[5] += A[h][2];
+                    s[6] += vy * A[h][1];
+                    s[7] += vz * A[h][1];
+                    s[8] += vy * (vy * A[h][0]);
+                    s[9] += vy * (vz * A[h][0]);
+                    s[10] += vz * (vz * A[h][0]);
+                }
             }
             block_reduce(s, 11);
         }
@@ -1278,12 +1332,18 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
         const int fallback = (ESBGK && !gauss) ? 1 : 0;
         const double S11 = par[1], S12 = par[2], S13 = par[3], S22 = par[4], S23 = par[5], S33 = par[6], gpref = par[7];
         // ---- equilibrium tables ----
+        auto hcoef = [&](int k) {  // Horner coefficients z^c Z(k) of pass 2
+            const double z = g.node(k), Z = Ztab[k];
+            double* h = Htab + 6 * k;
+            h[0] = Z; h[1] = z * Z; h[2] = z * (z * Z); h[3] = z * (z * (z * Z)); h[4] = z * (z * (z * (z * Z)));
+        };
         {
             const double dz0 = g.node(0) - m.uz, dv = g.dv;
             if (gauss) {
                 for (int k = t; k < n; k += MT) {
                     const double dz = g.node(k) - m.uz;
                     Ztab[k] = exp(-0.5 * S33 * dz * dz);
+                    hcoef(k);
                 }
                 for (int pidx = t; pidx < n * n; pidx += MT) {
                     const double dx = g.node(pidx >> lg) - m.ux, dy = g.node(pidx & (n - 1)) - m.uy;
@@ -1300,6 +1360,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 for (int k = t; k < n; k += MT) {
                     const double dz = g.node(k) - m.uz;
                     Ztab[k] = exp(-dz * dz * inv2T);
+                    hcoef(k);
                 }
                 for (int pidx = t; pidx < n * n; pidx += MT) {
                     const double dx = g.node(pidx >> lg) - m.ux, dy = g.node(pidx & (n - 1)) - m.uy;
@@ -1346,11 +1407,49 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             double M[14];
 #pragma unroll
             for (int k = 0; k < 14; ++k) M[k] = 0.0;
+            if (!direct) {
+                // Per pencil, sum_k3 z^c e = P sum_k3 (z^c Z)(k3) R^k3: five polynomials in R by
+                // Horner (5 FMA per node), PB pencils per thread sharing the coefficient loads.
+                constexpr int PB = MINB >= 3 ? 2 : 4;  // register budget
+                const int np = n << lg;
+                for (int pb = t; pb < np; pb += PB * MT) {
+                    double R4[PB], h[PB][5];
+#pragma unroll
+                    for (int u = 0; u < PB; ++u) {
+                        const int pidx = pb + u * MT;
+                        R4[u] = pidx < np ? Rtab[pidx] : 0.0;
+#pragma unroll
+                        for (int c = 0; c < 5; ++c) h[u][c] = 0.0;
+                    }
+#pragma unroll 4
+                    for (int k3 = n - 1; k3 >= 0; --k3) {
+                        const double2 a01 = *reinterpret_cast<const double2*>(Htab + 6 * k3);
+                        const double2 a23 = *reinterpret_cast<const double2*>(Htab + 6 * k3 + 2);
+                        const double a4 = Htab[6 * k3 + 4];
+#pragma unroll
+                        for (int u = 0; u < PB; ++u) {
+                            h[u][0] = fma(h[u][0], R4[u], a01.x);
+                            h[u][1] = fma(h[u][1], R4[u], a01.y);
+                            h[u][2] = fma(h[u][2], R4[u], a23.x);
+                            h[u][3] = fma(h[u][3], R4[u], a23.y);
+                            h[u][4] = fma(h[u][4], R4[u], a4);
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < PB; ++u) {
+                        const int pidx = pb + u * MT;
+                        if (pidx < np) {
+                            const double P = Ptab[pidx];
+                            acc14(M, g.node(pidx >> lg), g.node(pidx & (n - 1)), P * h[u][0], P * h[u][1], P * h[u][2],
+                                  P * h[u][3], P * h[u][4]);
+                        }
+                    }
+                }
+            } else
 #pragma unroll kStageU2
             for (int q = t; q < ngroups; q += MT) {
                 const int idx = 4 * q;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
-                const double vx = g.node(k1), vy = g.node(k2);
                 double e[4];
                 eq4(k1, k2, k3, e);
                 double m0 = 0, m1 = 0, m2 = 0, m3 = 0, m4 = 0;
@@ -1363,14 +1462,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                     m3 += zz * (z * e[j]);
                     m4 += zz * (zz * e[j]);
                 }
-                const double xx = vx * vx, yy = vy * vy, r2 = xx + yy;
-                M[0] += m0;
-                M[1] += vx * m0; M[2] += vy * m0; M[3] += m1;
-                M[4] += xx * m0; M[5] += vx * (vy * m0); M[6] += vx * m1;
-                M[7] += yy * m0; M[8] += vy * m1; M[9] += m2;
-                const double aa = r2 * m0 + m2;
-                M[10] += vx * aa; M[11] += vy * aa; M[12] += r2 * m1 + m3;
-                M[13] += r2 * (r2 * m0 + 2.0 * m2) + m4;
+                acc14(M, g.node(k1), g.node(k2), m0, m1, m2, m3, m4);
             }
             block_reduce(M, 14);
         }
@@ -1390,23 +1482,50 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
         if ((int)par[14] == HK_OK) {
             const double x[5] = {par[9], par[10], par[11], par[12], par[13]};
             const double wf = eps / (eps + A), wg = A / (eps + A);
+            if (!direct) {  // (Z, Z Q) per k3, Q = cz (x3 + x4 cz)
+                for (int k = t; k < n; k += MT) {
+                    const double cz = g.node(k) - uc[2], Z = Ztab[k];
+                    ZQ[zq_slot(k)] = make_double2(Z, Z * (cz * (x[3] + x[4] * cz)));
+                }
+                __syncthreads();
+            }
             // ---- pass 3: out = wf f + wg G (x0 + x.c + x4 |c|^2) ----
 #pragma unroll kStageU3
             for (int q = t; q < ngroups; q += MT) {
                 const int idx = 4 * q;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
                 const double vx = g.node(k1), vy = g.node(k2);
-                double e[4];
-                eq4(k1, k2, k3, e);
                 const double2 fa = ldg2(fc + idx), fb = ldg2(fc + idx + 2);
                 const double fv[4] = {fa.x, fa.y, fb.x, fb.y};
                 const double cx = vx - uc[0], cy = vy - uc[1];
                 const double pxy = x[0] + x[1] * cx + x[2] * cy + x[4] * (cx * cx + cy * cy);
                 double o[4];
+                if (!direct) {  // wg e (pxy + Q) = (wg P R^k3) (Z pxy + Z Q)
+                    const int pidx = (k1 << lg) | k2;
+                    const double R = Rtab[pidx];
+                    double rk = 1.0, r = R;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const double cz = g.node(k3 + j) - uc[2];
-                    o[j] = wf * fv[j] + wg * (e[j] * (pxy + cz * (x[3] + x[4] * cz)));
+                    for (int b = 0; b < 7; ++b) {  // R^k3, k3 < 128
+                        if (b < lg) {
+                            rk = ((k3 >> b) & 1) ? rk * r : rk;
+                            r *= r;
+                        }
+                    }
+                    double v = (wg * Ptab[pidx]) * rk;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double2 zq = ZQ[zq_slot(k3 + j)];
+                        o[j] = fma(wf, fv[j], v * fma(zq.x, pxy, zq.y));
+                        v *= R;
+                    }
+                } else {
+                    double e[4];
+                    eq4(k1, k2, k3, e);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const double cz = g.node(k3 + j) - uc[2];
+                        o[j] = wf * fv[j] + wg * (e[j] * (pxy + cz * (x[3] + x[4] * cz)));
+                    }
                 }
                 *reinterpret_cast<double2*>(oc + idx) = make_double2(o[0], o[1]);
                 *reinterpret_cast<double2*>(oc + idx + 2) = make_double2(o[2], o[3]);
@@ -1450,17 +1569,20 @@ int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncel
                    const int* count_dev) {
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "moments: 2 <= n <= 128");
-    static const int mom_var = getenv("HK_MOM_VAR") ? atoi(getenv("HK_MOM_VAR")) : 3;  // CTAs per SM x 256 threads
+    static const int mom_var = getenv("HK_MOM_VAR") ? atoi(getenv("HK_MOM_VAR")) : 2;  // variant: CTA size x CTAs per SM x loads in flight (3.99 ms at config 3; 3 -> 4.72)
     if (warp_path(n) && n >= 8 && mom_var > 0) {
-        const int64_t cap = int64_t(ctx->sm_count) * (mom_var == 1 ? 1 : mom_var);
+        static const int per_sm[7] = {3, 1, 2, 3, 4, 6, 2};
+        const int64_t cap = int64_t(ctx->sm_count) * per_sm[mom_var <= 6 ? mom_var : 3];
         const int grid = int(ncells < cap ? ncells : cap);
         const VGrid g = make_vgrid(n, vmax);
-        if (mom_var == 1)
-            moments_cta_kernel<512, 1><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev);
-        else if (mom_var <= 3)
-            moments_cta_kernel<256, 3><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev);
-        else
-            moments_cta_kernel<256, 4><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev);
+        switch (mom_var) {  // CTA size, CTAs per SM, loads in flight per thread
+        case 1: moments_cta_kernel<512, 1, 16><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
+        case 2: moments_cta_kernel<256, 2, 16><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
+        case 4: moments_cta_kernel<256, 4, 8><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
+        case 5: moments_cta_kernel<128, 6, 8><<<grid, 128, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
+        case 6: moments_cta_kernel<512, 2, 8><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
+        default: moments_cta_kernel<256, 3, 8><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
+        }
     } else if (warp_path(n))
         moments_warp_kernel<<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), log2i(n),
                                                                                   mom, sigma, real, l1, status, src_idx, count_dev);
@@ -1489,10 +1611,10 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
     const VGrid g = make_vgrid(n, vmax);
     static const bool stage_warp = getenv("HK_STAGE_WARP") != nullptr;
     if (warp_path(n) && n >= 8 && !stage_warp) {
-        static const int sv = getenv("HK_STAGE_VAR") ? atoi(getenv("HK_STAGE_VAR")) : 3;  // CTAs per SM
+        static const int sv = getenv("HK_STAGE_VAR") ? atoi(getenv("HK_STAGE_VAR")) : 2;  // CTAs per SM (2: 12.5 ms, 3: 12.8 at config 3)
         const int64_t cap = int64_t(ctx->sm_count) * sv;
         const int grid = int(ncells < cap ? ncells : cap);
-        const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32);
+        const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32 + 2 * n + 6 * n + 2 * n);
         auto kern = sv >= 3 ? (esbgk ? stage_cta_kernel<true, 256, 3> : stage_cta_kernel<false, 256, 3>)
                             : (esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>);
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

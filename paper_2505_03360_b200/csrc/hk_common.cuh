@@ -371,6 +371,10 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const double (&v)[8]) 
 // ---------------------------------------------------------------------------
 namespace hk {
 
+#ifndef HK_FFTXH_INNER
+#define HK_FFTXH_INNER fft_fma  // per-half transform of the split pencils (fft_reg: DIF, no FMA butterflies)
+#endif
+
 __device__ __forceinline__ double2 shfl_xor16(double2 v) {
     return make_double2(__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16));
 }
@@ -385,7 +389,7 @@ template <int M, bool INV>
 __device__ __forceinline__ void fftxh_dit(double2 (&v)[M], int h) {
     constexpr int L = 2 * M, Q = M / 2;
     static_assert(64 % L == 0, "twiddle table covers L | 64");
-    fft_reg<M, INV>(v);  // E[k] (h = 0) or O[k] (h = 1)
+    HK_FFTXH_INNER<M, INV>(v);  // E[k] (h = 0) or O[k] (h = 1)
     if (h) {
 #pragma unroll
         for (int k = 1; k < M; ++k) {
@@ -420,7 +424,7 @@ __device__ __forceinline__ void fftxh_dif(double2 (&v)[M], int h) {
         v[j] = h ? r : a;       // h=0: a[j];        h=1: b[j] (from h=0)
         v[Q + j] = h ? b : r;   // h=0: a[Q+j] (h=1); h=1: own b[Q+j]
     }
-    fft_reg<M, INV>(v);  // v[m] = X[2m + h]
+    HK_FFTXH_INNER<M, INV>(v);  // v[m] = X[2m + h]
 }
 
 }  // namespace hk
