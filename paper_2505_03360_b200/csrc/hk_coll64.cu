@@ -548,8 +548,10 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
             }
             cp_async_commit();
         };
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
         auto acquire = [&](unsigned gg) {
-            if (lane == 0) spin_geq(done + gg % D, ARR_C * (gg / D));
+            if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR_C * (gg / D));
             __syncwarp();
         };
         auto publish = [&](unsigned gg) {
@@ -663,6 +665,10 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                 ++g;
             }
         }
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
+        }
     } else {
         // ============================ CONSUMER GROUPS ============================
         const int grp = (warp - 4) >> 2;   // = my j3 / k1 plane (P = 2)
@@ -678,8 +684,10 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
             }
             cp_async_commit();
         };
+        long long spin_cyc = 0;
+        const long long t_start = clock64();
         auto issue = [&](unsigned gs) {
-            if (lane == 0) spin_geq(ready + gs % D, ARR * (gs / D + 1));
+            if (lane == 0) spin_cyc += spin_geq(ready + gs % D, ARR * (gs / D + 1));
             __syncwarp();
             pull(gs);
         };
@@ -819,6 +827,10 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                 atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
             }
         }
+        if (a.prof && lane == 0) {
+            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
+            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
+        }
     }
     tmem_fence_before();
     __syncthreads();
@@ -861,6 +873,13 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
     if ((st = check_cuda(ctx, cudaMemsetAsync(args.team_ctr, 0, sizeof(unsigned) * 2 * G::D * teams, ctx->stream),
                          "team counters")))
         return st;
+    static unsigned long long* prof = nullptr;
+    const bool profiling = w12 && getenv("HK_PROF_SPIN") != nullptr;
+    if (profiling) {
+        if (!prof) cudaMalloc(&prof, 64);
+        cudaMemsetAsync(prof, 0, 64, ctx->stream);
+        args.prof = prof;
+    }
     void* params[] = {&args};
     timing_begin(ctx, tag);
     st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * G::C)), dim3(nthreads), params,
@@ -868,6 +887,13 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
                     "N = 64 collision kernel launch");
     timing_end(ctx);
     ctx->launches++;
+    if (profiling) {
+        unsigned long long h[4];
+        cudaMemcpyAsync(h, prof, 32, cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        fprintf(stderr, "[hk prof] coll64 CTAs %lld: producer spin %.1f%%, consumer spin %.1f%%\n", (long long)(teams * G::C),
+                100.0 * h[0] / (double)h[2], 100.0 * h[1] / (double)h[3]);
+    }
     return st;
 }
 

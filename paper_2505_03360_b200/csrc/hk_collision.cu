@@ -752,6 +752,16 @@ __device__ __forceinline__ void fft_w(double2 (&x)[N]) {
     else fft_reg<N, INV>(x);
 }
 
+#ifndef HK_PROD_PHASES
+#define HK_PROD_PHASES 0  // producer phase timers (HK_PROF_SPIN report), profiling builds only
+#endif
+#if HK_PROD_PHASES
+#define HK_PH_T(v) long long v = clock64()
+#define HK_PH_ADD(k, v) do { const long long _t = clock64(); ph[k] += _t - v; v = _t; } while (0)
+#else
+#define HK_PH_T(v) do {} while (0)
+#define HK_PH_ADD(k, v) do {} while (0)
+#endif
 template <int N, int C>
 struct GeoW {
     static constexpr int P = N / C;   // planes per CTA
@@ -818,6 +828,9 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
         };
         long long spin_cyc = 0;
         const long long t_start = clock64();
+#if HK_PROD_PHASES
+        long long ph[6] = {0, 0, 0, 0, 0, 0};
+#endif
         auto acquire = [&](unsigned gg) {
             if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR_C * (gg / D));
             __syncwarp();
@@ -868,6 +881,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
             for (int e = 0; e < n_entries; ++e) {
 #pragma unroll 1
                 for (int pp = 0; pp < PPW; ++pp) {
+                    HK_PH_T(tA);
                     if (e == 0) {
                         mbar_wait_parity(smem_u32(fbar + pw + 4 * pp), ncell & 1);  // F(plane) in TMEM
                         tmem_fence_after();
@@ -883,6 +897,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                         cp_async_wait_all();
                         __syncwarp();
                         tmem_wait_ld();
+                        HK_PH_ADD(0, tA);
 #pragma unroll
                         for (int m = 0; m < 8; ++m) {
                             x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
@@ -901,21 +916,30 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                         issue_w(e, pp + 1);
                     else if (e + 1 < n_entries)
                         issue_w(e + 1, 0);
+                    HK_PH_ADD(1, tA);
                     fft_w<N, true>(x);
+                    HK_PH_ADD(2, tA);
                     if (pp == 0) acquire(g);
+                    HK_PH_ADD(3, tA);
                     double2* Xs = X + (int64_t)(g % D) * SLOT;
                     const int i1 = r * P + pw + 4 * pp;
 #pragma unroll
                     for (int j3 = 0; j3 < N; ++j3)
                         st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + lane, x[j3]);
+                    HK_PH_ADD(4, tA);
                 }
+                HK_PH_T(tP);
                 publish(g);  // one release fence for both planes
+                HK_PH_ADD(5, tP);
                 ++g;
             }
         }
         if (a.prof && lane == 0) {
             atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
             atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
+#if HK_PROD_PHASES
+            for (int k = 0; k < 6; ++k) atomicAdd(&a.prof[8 + k], (unsigned long long)ph[k]);
+#endif
         }
     } else {
         // ================================ CONSUMER WARP ================================
@@ -1290,8 +1314,8 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     static unsigned long long* prof = nullptr;
     const bool profiling = getenv("HK_PROF_SPIN") != nullptr;
     if (profiling) {
-        if (!prof) cudaMalloc(&prof, 64);
-        cudaMemsetAsync(prof, 0, 64, ctx->stream);
+        if (!prof) cudaMalloc(&prof, 256);
+        cudaMemsetAsync(prof, 0, 256, ctx->stream);
         args.prof = prof;
     }
     void* params[] = {&args};
@@ -1302,9 +1326,13 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     timing_end(ctx);
     ctx->launches++;
     if (profiling) {
-        unsigned long long h[4];
-        cudaMemcpyAsync(h, prof, 32, cudaMemcpyDeviceToHost, ctx->stream);
+        unsigned long long h[16];
+        cudaMemcpyAsync(h, prof, 128, cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
+        if (h[8] + h[9] + h[10])
+            fprintf(stderr, "[hk prof] producer phases (%% of producer time): tmem+wait %.1f, mul+issue %.1f, fft %.1f, acquire %.1f, "
+                    "stores %.1f, publish %.1f\n", 100.0 * h[8] / h[2], 100.0 * h[9] / h[2], 100.0 * h[10] / h[2],
+                    100.0 * h[11] / h[2], 100.0 * h[12] / h[2], 100.0 * h[13] / h[2]);
         fprintf(stderr, "[hk prof] CTAs %lld: producer spin %.1f%% of %.3g cyc/CTA, consumer spin %.1f%% of %.3g cyc/CTA\n",
                 (long long)(teams * TC), 100.0 * h[0] / (double)h[2], h[2] / double(teams * TC), 100.0 * h[1] / (double)h[3],
                 h[3] / double(teams * TC));

@@ -262,6 +262,11 @@ __device__ __forceinline__ void st_cg16(double2* p, double2 v) {
 __device__ __forceinline__ void named_bar(unsigned id, unsigned count) {
     asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
 }
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 // Spin until *p >= target (acquire, GPU scope).  Traps instead of hanging if
 // the producer never arrives (deadlock guard, ~2 s).
 __device__ __forceinline__ long long spin_geq(const unsigned* p, unsigned target) {
