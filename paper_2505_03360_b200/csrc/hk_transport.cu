@@ -16,6 +16,18 @@ namespace {
 // three nonlinear weights normalised through ONE reciprocal:
 //   a_k = c_k / D_k^2  ->  w_k = c_k P_k / sum_m c_m P_m,  P_k = prod_{m != k} D_m^2
 // (same values as the reference's three divisions up to rounding).
+// 1/x for the normalisation of the nonlinear weights (x >= eps^2 (...) > 0,
+// never denormal): the MUFU seed refined by two Newton steps (~1 ulp), without
+// the IEEE division's slow-path branch.
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
 __device__ __forceinline__ void cweno3_faces(double um, double uc, double up, double eps, double& left, double& right) {
     const double sl = uc - um, sr = up - uc;
     const double b = 0.5 * (up - um);
@@ -23,9 +35,9 @@ __device__ __forceinline__ void cweno3_faces(double um, double uc, double up, do
     const double dl = (eps + sl * sl), dr = (eps + sr * sr), dc = (eps + ((13.0 / 3.0) * c * c + b * b));
     const double l2 = dl * dl, r2 = dr * dr, c2 = dc * dc;
     const double pl = 0.25 * (c2 * r2), pc = 0.5 * (l2 * r2), pr = 0.25 * (l2 * c2);
-    const double inv = 1.0 / (pl + pc + pr);
+    const double inv = rcp_nr(pl + pc + pr);
     const double al = pl * inv, ac = pc * inv, ar = pr * inv;
-    const double pc_a = uc - c / 12.0;
+    const double pc_a = uc - c * (1.0 / 12.0);
     const double c0 = al * uc + ar * uc + ac * pc_a;
     const double c1 = al * sl + ar * sr + ac * b;
     const double cc = ac * c;
