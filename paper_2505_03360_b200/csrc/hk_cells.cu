@@ -1611,15 +1611,20 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
     const VGrid g = make_vgrid(n, vmax);
     static const bool stage_warp = getenv("HK_STAGE_WARP") != nullptr;
     if (warp_path(n) && n >= 8 && !stage_warp) {
-        static const int sv = getenv("HK_STAGE_VAR") ? atoi(getenv("HK_STAGE_VAR")) : 2;  // CTAs per SM (2: 12.5 ms, 3: 12.8 at config 3)
+        static const int sv = getenv("HK_STAGE_VAR") ? atoi(getenv("HK_STAGE_VAR")) : 5;  // config 3: 2 -> 12.5 ms, 3 -> 12.8, 4 -> 12.2, 5 -> 11.7, 6 -> 11.6
         const int64_t cap = int64_t(ctx->sm_count) * sv;
         const int grid = int(ncells < cap ? ncells : cap);
         const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32 + 2 * n + 6 * n + 2 * n);
-        auto kern = sv >= 3 ? (esbgk ? stage_cta_kernel<true, 256, 3> : stage_cta_kernel<false, 256, 3>)
-                            : (esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>);
+        // sv: CTAs per SM; 2, 3 -> 256-thread CTAs, 4..6 -> 128-thread CTAs
+        auto kern = sv == 3   ? (esbgk ? stage_cta_kernel<true, 256, 3> : stage_cta_kernel<false, 256, 3>)
+                    : sv == 4 ? (esbgk ? stage_cta_kernel<true, 128, 4> : stage_cta_kernel<false, 128, 4>)
+                    : sv == 5 ? (esbgk ? stage_cta_kernel<true, 128, 5> : stage_cta_kernel<false, 128, 5>)
+                    : sv == 6 ? (esbgk ? stage_cta_kernel<true, 128, 6> : stage_cta_kernel<false, 128, 6>)
+                              : (esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>);
+        const int mt = (sv >= 4 && sv <= 6) ? 128 : 256;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, 256, smem, ctx->stream>>>(fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info,
-                                               mom_out, k1_out, k1_scale);
+        kern<<<grid, mt, smem, ctx->stream>>>(fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info,
+                                              mom_out, k1_out, k1_scale);
         ctx->launches++;
         return check_cuda(ctx, cudaGetLastError(), "stage kernel");
     } else if (warp_path(n)) {
