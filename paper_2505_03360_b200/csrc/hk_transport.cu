@@ -45,6 +45,26 @@ __device__ __forceinline__ void cweno3_faces(double um, double uc, double up, do
     right = c0 + 0.5 * c1 + 0.25 * cc;
 }
 
+// One face only (the upwind one), the same CWENO3 value in fewer operations:
+// with the weights summing to one, c0 = uc - a_c c / 12, so
+//   right = uc + (1/S) [ (p_l s_l + p_r s_r) / 2 + p_c (b / 2 + c / 6) ]
+//   left  = uc + (1/S) [-(p_l s_l + p_r s_r) / 2 + p_c (c / 6 - b / 2) ]
+// with p = 4 x (the weights' numerators above) and S their sum (~31 instead
+// of ~45 fp64 operations per face).
+template <bool RIGHT>
+__device__ __forceinline__ double cweno3_face(double um, double uc, double up, double eps) {
+    const double sl = uc - um, sr = up - uc;
+    const double b = 0.5 * (up - um);
+    const double c = sr - sl;  // up - 2 uc + um
+    const double dl = fma(sl, sl, eps), dr = fma(sr, sr, eps), dc = fma((13.0 / 3.0) * c, c, fma(b, b, eps));
+    const double l2 = dl * dl, r2 = dr * dr, c2 = dc * dc;
+    const double pl = c2 * r2, pr = l2 * c2, pc = (l2 + l2) * r2;
+    const double inv = rcp_nr(pl + pc + pr);
+    const double side = 0.5 * fma(pl, sl, pr * sr);
+    const double mid = RIGHT ? fma(c, 1.0 / 6.0, 0.5 * b) : fma(c, 1.0 / 6.0, -0.5 * b);
+    return fma(inv, RIGHT ? fma(pc, mid, side) : fma(pc, mid, -side), uc);
+}
+
 // Transport sweep, y-marching (replaces the per-node kernel above for the
 // production path).  Thread (lane, ty) owns velocity node idx = 32 chunk +
 // lane of column i = IW group + ty and marches j = 0 .. ny-1: the y stencil
@@ -208,21 +228,15 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
     double2 w0 = ld(-2), w1 = ld(-1), w2 = ld(0), w3 = ld(1), w4 = ld(2);
     const bool ypos = vy > 0.0, xpos = vx > 0.0;
     auto yface = [&](double a, double b, double c, double d, double e) -> double {  // new upwind y face
-        double l, r;
-        if (ypos) { cweno3_faces(b, c, d, eps, l, r); return r; }
-        cweno3_faces(c, d, e, eps, l, r);
-        return l;
+        return ypos ? cweno3_face<true>(b, c, d, eps) : cweno3_face<false>(c, d, e, eps);
     };
     double fyp[2];
-    {
-        double l, r;
-        if (ypos) {
-            cweno3_faces(w0.x, w1.x, w2.x, eps, l, r); fyp[0] = r;
-            cweno3_faces(w0.y, w1.y, w2.y, eps, l, r); fyp[1] = r;
-        } else {
-            cweno3_faces(w1.x, w2.x, w3.x, eps, l, r); fyp[0] = l;
-            cweno3_faces(w1.y, w2.y, w3.y, eps, l, r); fyp[1] = l;
-        }
+    if (ypos) {
+        fyp[0] = cweno3_face<true>(w0.x, w1.x, w2.x, eps);
+        fyp[1] = cweno3_face<true>(w0.y, w1.y, w2.y, eps);
+    } else {
+        fyp[0] = cweno3_face<false>(w1.x, w2.x, w3.x, eps);
+        fyp[1] = cweno3_face<false>(w1.y, w2.y, w3.y, eps);
     }
     double2 nw4 = make_double2(0, 0), nf0 = nw4, nf1 = nw4, nf2 = nw4;
     auto fin_loads = [&](int jj, double2& a, double2& b, double2& c) {
@@ -249,15 +263,13 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const double cp1 = sh_dn(c[q], 1);
-            double plus, l, r;
+            double plus;
             if (xpos) {  // right face of cell i
                 const double cm1 = sh_up(c[q], 1);
-                cweno3_faces(cm1, c[q], cp1, eps, l, r);
-                plus = r;
+                plus = cweno3_face<true>(cm1, c[q], cp1, eps);
             } else {     // left face of cell i+1
                 const double cp2 = sh_dn(c[q], 2);
-                cweno3_faces(c[q], cp1, cp2, eps, l, r);
-                plus = l;
+                plus = cweno3_face<false>(c[q], cp1, cp2, eps);
             }
             const double minus = sh_up(plus, 1);
             fx[q] = vx * (plus - minus);
