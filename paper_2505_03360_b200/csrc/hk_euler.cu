@@ -224,8 +224,20 @@ int hk_euler_tvd_rk2_step(hk_ctx ctx, double* u_dev, int nx, int ny, double dx, 
     cudaSetDevice(ctx->device);
     const int64_t n4 = 4LL * nx * ny;
     double* w = work_dev;
-    if (!w && cudaMallocAsync(&w, sizeof(double) * 2 * n4, ctx->stream) != cudaSuccess)
-        return fail(ctx, HK_CUDA, "euler step work alloc");
+    if (!w) {  // the context's step workspace (kept across calls: no per-step allocation)
+        const size_t need = sizeof(double) * 2 * n4;
+        if (need > ctx->step_bytes) {
+            if (ctx->step_work) {
+                cudaStreamSynchronize(ctx->stream);
+                cudaFree(ctx->step_work);
+                ctx->step_work = nullptr;
+                ctx->step_bytes = 0;
+            }
+            if (cudaMalloc(&ctx->step_work, need) != cudaSuccess) return fail(ctx, HK_CUDA, "euler step work alloc");
+            ctx->step_bytes = need;
+        }
+        w = static_cast<double*>(ctx->step_work);
+    }
     double *l = w, *u1 = w + n4;
     unsigned long long* bad = bad_slot(ctx);
     cudaMemsetAsync(bad, 0xff, sizeof *bad, ctx->stream);
@@ -241,7 +253,6 @@ int hk_euler_tvd_rk2_step(hk_ctx ctx, double* u_dev, int nx, int ny, double dx, 
         ctx->launches++;
         st = check_cuda(ctx, cudaGetLastError(), "euler step");
     }
-    if (!work_dev) cudaFreeAsync(w, ctx->stream);
     return st;
 }
 

@@ -5,4 +5,4 @@ set -u
 mkdir -p gpurun_out
 TAG=${1:-r01}
 bash tools/profile_round.sh $TAG
-timeout 900 python tools/bench_configs.py --configs 1,3,5 --iters 3 > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err; echo "configs rc=$?"
+timeout 900 python tools/bench_configs.py --configs 1,3,4,5 --iters 3 > gpurun_out/configs_$TAG.jsonl 2> gpurun_out/configs_$TAG.err; echo "configs rc=$?"
