@@ -71,49 +71,106 @@ __device__ void block_sum(double (&v)[K], double* scratch /* [8][K] */) {
 
 // Eigen::FullPivLU<Matrix<double,5,5>> (src/moments.cpp:215-221), as
 // oracle/hk_oracle.c:hko_solve5.  Returns false when singular.
-__device__ bool solve5(const double a_in[25], const double rhs[5], double x[5]) {
-    double a[25];
+// Register-resident form: every index is a compile-time constant after
+// unrolling; the data-dependent pivot row / column swaps are selects (no
+// local memory).  Same pivot order (first maximum in column-major scan), same
+// operations per element as the scalar algorithm.
+__device__ __forceinline__ bool solve5(const double a_in[25], const double rhs[5], double x[5]) {
+    double a[5][5];
     int rp[5], cp[5];
-    for (int i = 0; i < 25; ++i) a[i] = a_in[i];
-    for (int i = 0; i < 5; ++i) rp[i] = cp[i] = i;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+#pragma unroll
+        for (int j = 0; j < 5; ++j) a[i][j] = a_in[5 * i + j];
+        rp[i] = cp[i] = i;
+    }
     double maxpivot = 0.0;
     int nonzero = 5;
+    bool live = true;
+#pragma unroll
     for (int k = 0; k < 5; ++k) {
         int bi = k, bj = k;
         double big = -1.0;
+#pragma unroll
         for (int j = k; j < 5; ++j)
+#pragma unroll
             for (int i = k; i < 5; ++i) {
-                const double v = fabs(a[5 * i + j]);
-                if (v > big) { big = v; bi = i; bj = j; }
+                const double v = fabs(a[i][j]);
+                const bool gt = v > big;
+                big = gt ? v : big;
+                bi = gt ? i : bi;
+                bj = gt ? j : bj;
             }
-        if (big == 0.0) { nonzero = k; break; }
-        if (big > maxpivot) maxpivot = big;
-        if (bi != k) {
-            for (int j = 0; j < 5; ++j) { const double t = a[5 * k + j]; a[5 * k + j] = a[5 * bi + j]; a[5 * bi + j] = t; }
-            const int t = rp[k]; rp[k] = rp[bi]; rp[bi] = t;
+        if (live && big == 0.0) {
+            nonzero = k;
+            live = false;
         }
-        if (bj != k) {
-            for (int i = 0; i < 5; ++i) { const double t = a[5 * i + k]; a[5 * i + k] = a[5 * i + bj]; a[5 * i + bj] = t; }
-            const int t = cp[k]; cp[k] = cp[bj]; cp[bj] = t;
-        }
-        for (int i = k + 1; i < 5; ++i) {
-            a[5 * i + k] /= a[5 * k + k];
-            for (int j = k + 1; j < 5; ++j) a[5 * i + j] -= a[5 * i + k] * a[5 * k + j];
+        if (live) {
+            if (big > maxpivot) maxpivot = big;
+#pragma unroll
+            for (int r = k + 1; r < 5; ++r) {  // rows k <-> bi
+                const bool sw = bi == r;
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    const double t = a[k][j];
+                    a[k][j] = sw ? a[r][j] : t;
+                    a[r][j] = sw ? t : a[r][j];
+                }
+                const int ti = rp[k];
+                rp[k] = sw ? rp[r] : ti;
+                rp[r] = sw ? ti : rp[r];
+            }
+#pragma unroll
+            for (int c = k + 1; c < 5; ++c) {  // columns k <-> bj
+                const bool sw = bj == c;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const double t = a[i][k];
+                    a[i][k] = sw ? a[i][c] : t;
+                    a[i][c] = sw ? t : a[i][c];
+                }
+                const int ti = cp[k];
+                cp[k] = sw ? cp[c] : ti;
+                cp[c] = sw ? ti : cp[c];
+            }
+#pragma unroll
+            for (int i = k + 1; i < 5; ++i) {
+                a[i][k] /= a[k][k];
+#pragma unroll
+                for (int j = k + 1; j < 5; ++j) a[i][j] -= a[i][k] * a[k][j];
+            }
         }
     }
     const double thr = 2.220446049250313e-16 * 5.0 * maxpivot;
     int rank = 0;
-    for (int i = 0; i < nonzero; ++i) rank += fabs(a[5 * i + i]) > thr;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) rank += (i < nonzero && fabs(a[i][i]) > thr) ? 1 : 0;
     if (rank != 5) return false;
     double y[5];
-    for (int i = 0; i < 5; ++i) y[i] = rhs[rp[i]];
-    for (int i = 0; i < 5; ++i)
-        for (int j = 0; j < i; ++j) y[i] -= a[5 * i + j] * y[j];
-    for (int i = 4; i >= 0; --i) {
-        for (int j = i + 1; j < 5; ++j) y[i] -= a[5 * i + j] * y[j];
-        y[i] /= a[5 * i + i];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        double v = rhs[0];
+#pragma unroll
+        for (int r = 1; r < 5; ++r) v = rp[i] == r ? rhs[r] : v;
+        y[i] = v;
     }
-    for (int i = 0; i < 5; ++i) x[cp[i]] = y[i];
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int j = 0; j < i; ++j) y[i] -= a[i][j] * y[j];
+#pragma unroll
+    for (int i = 4; i >= 0; --i) {
+#pragma unroll
+        for (int j = i + 1; j < 5; ++j) y[i] -= a[i][j] * y[j];
+        y[i] /= a[i][i];
+    }
+#pragma unroll
+    for (int o = 0; o < 5; ++o) {
+        double v = 0.0;
+#pragma unroll
+        for (int i = 0; i < 5; ++i) v = cp[i] == o ? y[i] : v;
+        x[o] = v;
+    }
     return true;
 }
 
@@ -1179,6 +1236,12 @@ __device__ __forceinline__ int zq_slot(int k) { return (k & ~7) | ((k & 7) ^ ((k
 #define HK_STAGE_U3 1
 #endif
 constexpr int kStageU1 = HK_STAGE_U1, kStageU2 = HK_STAGE_U2, kStageU3 = HK_STAGE_U3;
+#ifndef HK_STAGE_PROF
+#define HK_STAGE_PROF 0  // per-phase clocks of thread 0 (profiling builds)
+#endif
+#if HK_STAGE_PROF
+__device__ unsigned long long g_stage_prof[5];
+#endif
 template <bool ESBGK, int MT, int MINB>
 __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __restrict__ fin, double* __restrict__ out,
                                                              int64_t ncells, VGrid g, int lg, double a,
@@ -1216,6 +1279,12 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
         xpow[k] = make_double2(v, v * v);
     }
     __syncthreads();
+#if HK_STAGE_PROF
+    long long sp[5] = {0, 0, 0, 0, 0}, st0 = clock64();
+#define SP_MARK(k) do { if (t == 0) { const long long _c = clock64(); sp[k] += _c - st0; st0 = _c; } } while (0)
+#else
+#define SP_MARK(k) do {} while (0)
+#endif
     for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
         const double* fc = fin + cell * nb;
         double* oc = out + cell * nb;
@@ -1282,6 +1351,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             __syncthreads();
             continue;
         }
+        SP_MARK(0);
         // ---- ES-BGK tensor (src/esbgk.cpp:24-33) + LLT test + inverse, thread 0 ----
         if (t == 0) {
             par[0] = 0.0;  // use_gauss
@@ -1400,6 +1470,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 }
             }
         };
+        SP_MARK(1);
         // ---- pass 2: coupling matrix of the equilibrium (14 monomial moments) ----
         const double mom3[3] = {m.rho * m.ux, m.rho * m.uy, m.rho * m.uz};
         const double uc[3] = {mom3[0] / m.rho, mom3[1] / m.rho, mom3[2] / m.rho};
@@ -1466,6 +1537,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             }
             block_reduce(M, 14);
         }
+        SP_MARK(2);
         if (t == 0) {
             double Mm[14], Amat[25];
             for (int k = 0; k < 14; ++k) Mm[k] = par[16 + k];
@@ -1479,6 +1551,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             par[14] = st;
         }
         __syncthreads();
+        SP_MARK(3);
         if ((int)par[14] == HK_OK) {
             const double x[5] = {par[9], par[10], par[11], par[12], par[13]};
             const double wf = eps / (eps + A), wg = A / (eps + A);
@@ -1537,7 +1610,13 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             }
         }
         __syncthreads();  // tables / par reused by the next cell
+        SP_MARK(4);
     }
+#if HK_STAGE_PROF
+    if (t == 0)
+        for (int q = 0; q < 5; ++q) atomicAdd(&g_stage_prof[q], (unsigned long long)sp[q]);
+#endif
+#undef SP_MARK
 }
 
 __global__ void k1_kernel(int64_t count, double* __restrict__ k1, const double* __restrict__ y,
@@ -1625,6 +1704,18 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, mt, smem, ctx->stream>>>(fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info,
                                               mom_out, k1_out, k1_scale);
+#if HK_STAGE_PROF
+        {
+            unsigned long long h[5];
+            cudaStreamSynchronize(ctx->stream);
+            cudaMemcpyFromSymbol(h, g_stage_prof, sizeof h);
+            const double tot = double(h[0] + h[1] + h[2] + h[3] + h[4]);
+            fprintf(stderr, "[hk stage prof] pass1 %.1f%% tail1+tables %.1f%% pass2 %.1f%% solve %.1f%% pass3 %.1f%%\n",
+                    100 * h[0] / tot, 100 * h[1] / tot, 100 * h[2] / tot, 100 * h[3] / tot, 100 * h[4] / tot);
+            const unsigned long long z[5] = {0, 0, 0, 0, 0};
+            cudaMemcpyToSymbol(g_stage_prof, z, sizeof z);
+        }
+#endif
         ctx->launches++;
         return check_cuda(ctx, cudaGetLastError(), "stage kernel");
     } else if (warp_path(n)) {
