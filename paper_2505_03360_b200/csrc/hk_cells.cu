@@ -1087,6 +1087,7 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
         xpow[k][1] = make_double2(v2 * v, v2 * v2);
     }
     __syncthreads();
+    const uint64_t pol_last = l2_evict_last(), pol_first = l2_evict_first();
     for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
         const double* fc = f + (src_idx ? src_idx[cell] : cell) * nb;
         double M[14];  // S, Sx, Sy, Sz, Sxx, Sxy, Sxz, Syy, Syz, Szz, Rx, Ry, Rz, Q4
@@ -1103,7 +1104,7 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
             double A0[5] = {0, 0, 0, 0, 0}, A1[5] = {0, 0, 0, 0, 0};
 #pragma unroll UNR
             for (int k1 = 0; k1 < n; ++k1) {
-                const double2 w = ldg2(fcol + ((int64_t)k1 << (2 * lg)));
+                const double2 w = ldg2_hint(fcol + ((int64_t)k1 << (2 * lg)), l1 ? pol_last : pol_first);
                 const double2 p12 = xpow[k1][0], p34 = xpow[k1][1];
                 A0[0] += w.x; A1[0] += w.y;
                 A0[1] += p12.x * w.x; A1[1] += p12.x * w.y;
@@ -1209,7 +1210,7 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
                 const double py0 = pref * tabs[1][k2] * tabs[2][k3], py1 = pref * tabs[1][k2] * tabs[2][k3 + 1];
 #pragma unroll UNR
                 for (int k1 = 0; k1 < n; ++k1) {
-                    const double2 w = ldg2(fcol + ((int64_t)k1 << (2 * lg)));
+                    const double2 w = ldg2_hint(fcol + ((int64_t)k1 << (2 * lg)), pol_first);
                     const double ex = tabs[0][k1];
                     acc += fabs(w.x - py0 * ex) + fabs(w.y - py1 * ex);
                 }
