@@ -171,15 +171,25 @@ __global__ void moments_to_conserved_kernel(const double* __restrict__ mom, int6
     u[4 * c + 3] = rho * m[4] / (hr - 1.0) + 0.5 * rho * u2;
 }
 
-// dst[k] = src[idx[k]] (gather, dir 0) or dst[idx[k]] = src[k] (scatter, dir 1), nb doubles per cell
-__global__ void cells_copy_kernel(int dir, int64_t nb, const int64_t* __restrict__ idx, int64_t count,
-                                  const double* __restrict__ src, double* __restrict__ dst) {
-    for (int64_t k = blockIdx.y; k < count; k += gridDim.y) {
+// dst[k] = src[idx[k]] (gather, dir 0) or dst[idx[k]] = src[k] (scatter, dir 1), nb doubles per cell.
+// One 256-thread CTA per cell block (grid-strided over the list), 8 16-byte loads in flight per thread.
+__global__ void __launch_bounds__(256) cells_copy_kernel(int dir, int64_t nb, const int64_t* __restrict__ idx,
+                                                         int64_t count, const double* __restrict__ src,
+                                                         double* __restrict__ dst) {
+    const int64_t n2 = nb / 2;
+    for (int64_t k = blockIdx.x; k < count; k += gridDim.x) {
         const int64_t s = dir == 0 ? idx[k] : k, d = dir == 0 ? k : idx[k];
         const double2* sp = reinterpret_cast<const double2*>(src + s * nb);
         double2* dp = reinterpret_cast<double2*>(dst + d * nb);
-        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nb / 2; e += (int64_t)gridDim.x * blockDim.x)
-            dp[e] = sp[e];
+        int64_t e = threadIdx.x;
+        for (; e + 7 * 256 < n2; e += 8 * 256) {
+            double2 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcs(sp + e + u * 256);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) __stcs(dp + e + u * 256, v[u]);
+        }
+        for (; e < n2; e += 256) __stcs(dp + e, __ldcs(sp + e));
     }
 }
 
@@ -305,7 +315,7 @@ int hk_gather_cells(hk_ctx ctx, int64_t nb, const double* src_dev, const int64_t
     if (count <= 0) return HK_OK;
     if (nb % 2) return fail(ctx, HK_CONTRACT, "gather: cell size must be even");
     cudaSetDevice(ctx->device);
-    const dim3 grid(unsigned(std::min<int64_t>((nb / 2 + 255) / 256, 64)), unsigned(std::min<int64_t>(count, 65535)));
+    const unsigned grid = unsigned(std::min<int64_t>(count, int64_t(ctx->sm_count) * 8));
     cells_copy_kernel<<<grid, 256, 0, ctx->stream>>>(0, nb, idx_dev, count, src_dev, dst_dev);
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "gather");
@@ -315,7 +325,7 @@ int hk_scatter_cells(hk_ctx ctx, int64_t nb, const double* src_dev, const int64_
     if (count <= 0) return HK_OK;
     if (nb % 2) return fail(ctx, HK_CONTRACT, "scatter: cell size must be even");
     cudaSetDevice(ctx->device);
-    const dim3 grid(unsigned(std::min<int64_t>((nb / 2 + 255) / 256, 64)), unsigned(std::min<int64_t>(count, 65535)));
+    const unsigned grid = unsigned(std::min<int64_t>(count, int64_t(ctx->sm_count) * 8));
     cells_copy_kernel<<<grid, 256, 0, ctx->stream>>>(1, nb, idx_dev, count, src_dev, dst_dev);
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "scatter");
