@@ -279,6 +279,45 @@ int hk_synthesize_distributions(hk_ctx ctx, int n, double vmax, int64_t nx, int6
                                 double heat_ratio, const int64_t* idx_dev, int64_t count, double* out_dev,
                                 int64_t* filled);
 
+/* ---- hybrid time step (SURVEY §8f "next" #1: the Algorithm-1 driver) --------
+ * The reference ships the per-cell pieces (regime_update src/regime.cpp:25-52,
+ * convert_on_transition :54-72, synthesize_* src/coupling.cpp:57-93) but not
+ * the step driver (simulation.cpp is absent; SPEC.md harness run_scenario,
+ * PAPER.md Algorithm 1 and its stencil-synthesis paragraphs).  The step below
+ * is the restatement of that loop the oracle (hko_hybrid_step) pins, on a
+ * periodic nx x ny torus without obstacles (BASELINE config 4):
+ *   1. indicator pass at t^n: hydro view = U (layer 0) or moments_of(f)
+ *      (kinetic), L1 distance of the kinetic cells, regime_update per cell
+ *      (skipped when update_regimes == 0: the given r is kept);
+ *   2. convert_on_transition: 0->1 f = maxwellian(U); 1->0 U = moments(f);
+ *   3. layer 0: TVD-RK2 of the hydro view on the whole torus (kinetic cells
+ *      enter the Euler stencil through their moments), kept on r == 0 cells;
+ *   4. layers 1 and 2: one PR(2,2,2) step of the kinetic cells (ES-BGK stage
+ *      solves on r == 1, penalized stage solves + penalized residual on
+ *      r == 2), the transport stencil reading the Maxwellian of the t^n hydro
+ *      state on the layer-0 cells within +-2 cells of a kinetic cell (frozen
+ *      over the step).
+ * r_dev [cells] int8 (in/out), hydro_dev [cells][4] conserved (authoritative
+ * on layer 0), f_dev [cells][n^3] dense (authoritative on kinetic cells; the
+ * layer-0 halo blocks are overwritten), eps_dev [cells].  counts (host,
+ * nullable, 6 entries): cells in layers 0/1/2 after the step, transitions
+ * 0->1 and 1->0, halo blocks synthesized.  Errors: HK_POSITIVITY /
+ * HK_DEGENERATE with the lowest failing cell.  Synchronises 2-3 times. */
+typedef struct {
+    double eta0, eta1, delta0;  /* Thresholds (inc/indicators.hpp:49-55) */
+    double mu0, kappa0;         /* mu = mu0 sqrt(T), kappa = kappa0 sqrt(T) */
+    int signed_sum;             /* LaplacianNorm::signed_sum */
+    int update_regimes;         /* 1: Algorithm 1 each step; 0: r_dev kept */
+    double heat_ratio;          /* 5/3 */
+    double esbgk_beta;          /* -1/2 (Pr = 2/3) */
+    double nu_coeff;            /* ES-BGK nu = nu_coeff rho (pi/2) */
+    double pen_coeff;           /* penalization beta = pen_coeff rho (2 pi) */
+    double eps_weno;            /* 1e-6 */
+    uint32_t coll_flags;        /* hk_collision_batch flags of the residuals */
+} hk_hybrid_params;
+int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx, double dy, double dt, const double* eps_dev,
+                   int8_t* r_dev, double* hydro_dev, double* f_dev, const hk_hybrid_params* params, int64_t* counts);
+
 /* ---- multi-GPU: NCCL communicator of a context ------------
  * One process per GPU.  Rank 0 calls hk_comm_unique_id, the host side ships
  * the 128 opaque bytes to every rank (MPI / torch.distributed / a file), and

@@ -1509,3 +1509,173 @@ int hko_synthesize_distribution(int nx, int ny, int n, double vmax, const hko_ob
     memcpy(out, f + c * nb, sizeof(double) * nb);
     return 0;
 }
+
+/* ===================================================================== */
+/* Hybrid time step (restatement: SPEC.md harness run_scenario, PAPER.md  */
+/* Algorithm 1 + the stencil-synthesis paragraphs after it)               */
+/* ===================================================================== */
+
+static int hyb_kinetic_at(const signed char* r, int nx, int ny, long i, long j) {
+    return r[wrapi(j, ny) * nx + wrapi(i, nx)] != 0;
+}
+
+int hko_hybrid_step(int nx, int ny, const hko_kernel* k, double dx, double dy, double dt, const double* eps,
+                    signed char* r, double* hydro, double* f, const hko_hybrid_params* p, long counts[6]) {
+    const int n = k->n;
+    const double vmax = k->vmax, hr = p->heat_ratio;
+    const long cells = (long)nx * ny, nb = (long)n * n * n;
+    const pr222 t = tableau_pr222();
+    double* mom = (double*)malloc(sizeof(double) * 5 * cells);
+    double* W = (double*)malloc(sizeof(double) * 4 * cells);
+    signed char* rn = (signed char*)malloc(cells);
+    int st = HKO_OK;
+    long n01 = 0, n10 = 0, nhalo = 0, nl[3] = {0, 0, 0};
+    /* 1. indicator pass at t^n: the hydro view of every cell */
+    for (long c = 0; c < cells && !st; ++c) {
+        if (r[c] == 0) {
+            st = hko_moments_from_conserved(hydro + 4 * c, hr, mom + 5 * c);
+        } else {
+            hko_moments m;
+            st = hko_moments_of(n, vmax, f + c * nb, &m);
+            mom[5 * c] = m.rho;
+            mom[5 * c + 1] = m.u[0];
+            mom[5 * c + 2] = m.u[1];
+            mom[5 * c + 3] = m.u[2];
+            mom[5 * c + 4] = m.T;
+        }
+    }
+    for (long c = 0; c < cells && !st; ++c) {
+        int out = r[c];
+        if (p->update_regimes) { /* indicators on prim_from_moments (src/coupling.cpp:33-35) */
+            const long i = c % nx, j = c / nx;
+            double pc[4], xm[4], xp[4], ym[4], yp[4], d[11], lam[3], l1 = 0.0;
+            const long nbr[5] = {c, j * nx + wrapi(i - 1, nx), j * nx + wrapi(i + 1, nx), wrapi(j - 1, ny) * nx + i,
+                                 wrapi(j + 1, ny) * nx + i};
+            double* q[5] = {pc, xm, xp, ym, yp};
+            for (int e = 0; e < 5; ++e) {
+                const double* m = mom + 5 * nbr[e];
+                q[e][0] = m[0]; q[e][1] = m[1]; q[e][2] = m[2]; q[e][3] = m[4];
+            }
+            hko_spatial_derivatives(pc, xm, xp, ym, yp, dx, dy, d);
+            hko_v_eps1_eigenvalues(d, pc, eps[c], p->mu0, p->kappa0, lam);
+            const double lb = hko_lambda_b(d, pc, eps[c], p->signed_sum);
+            if (r[c] == 1) st = hko_l1_distance(f + c * nb, n, vmax, &l1);
+            if (!st) st = hko_regime_update(r[c], lam, &lb, r[c] == 1 ? &l1 : NULL, p->eta0, p->eta1, p->delta0, &out);
+        }
+        rn[c] = (signed char)out;
+    }
+    /* 2. convert_on_transition (src/regime.cpp:54-72); W = hydro view fed to layer 0 */
+    for (long c = 0; c < cells && !st; ++c) {
+        if (r[c] == 0) {
+            memcpy(W + 4 * c, hydro + 4 * c, sizeof(double) * 4);
+            if (rn[c] != 0) ++n01;
+        } else {
+            hko_conserved_from_moments(mom + 5 * c, hr, W + 4 * c);
+            if (rn[c] == 0) {
+                memcpy(hydro + 4 * c, W + 4 * c, sizeof(double) * 4);
+                ++n10;
+            }
+        }
+        ++nl[(int)rn[c]];
+    }
+    /* Maxwellians of the 0 -> 1 cells and of the layer-0 transport halo */
+    for (long c = 0; c < cells && !st; ++c) {
+        int mw = r[c] == 0 && rn[c] != 0;
+        if (rn[c] == 0) {
+            const long i = c % nx, j = c / nx;
+            for (int dd = 1; dd <= 2 && !mw; ++dd)
+                mw = hyb_kinetic_at(rn, nx, ny, i - dd, j) || hyb_kinetic_at(rn, nx, ny, i + dd, j) ||
+                     hyb_kinetic_at(rn, nx, ny, i, j - dd) || hyb_kinetic_at(rn, nx, ny, i, j + dd);
+            nhalo += mw;
+        }
+        if (mw) {
+            double m5[5];
+            st = hko_moments_from_conserved(hydro + 4 * c, hr, m5);
+            if (!st) {
+                const hko_moments m = {m5[0], {m5[1], m5[2], m5[3]}, m5[4]};
+                st = hko_maxwellian(&m, n, vmax, f + c * nb);
+            }
+        }
+    }
+    /* 3. layer 0 */
+    if (!st && nl[0]) {
+        long bad = -1;
+        st = hko_tvd_rk2_step_periodic(W, nx, ny, dx, dy, dt, hr, p->eps_weno, &bad);
+        for (long c = 0; c < cells && !st; ++c)
+            if (rn[c] == 0) memcpy(hydro + 4 * c, W + 4 * c, sizeof(double) * 4);
+    }
+    /* 4. kinetic cells: PR(2,2,2) (src/boltzmann.cpp:47-110, src/esbgk.cpp:47-99) */
+    if (!st && nl[1] + nl[2]) {
+        double* Y = (double*)malloc(sizeof(double) * cells * nb);
+        double* q1 = (double*)malloc(sizeof(double) * cells * nb);
+        double* k1 = (double*)malloc(sizeof(double) * cells * nb);
+        double* fa = (double*)malloc(sizeof(double) * nb);
+        double* res = (double*)malloc(sizeof(double) * nb);
+        double* q2 = (double*)malloc(sizeof(double) * nb);
+        memcpy(Y, f, sizeof(double) * cells * nb); /* halo cells keep their Maxwellian */
+#define STAGE(fin, a, out) (rn[c] == 1 ? hko_esbgk_stage_solve(fin, a, eps[c], p->esbgk_beta, p->nu_coeff, n, vmax, out, NULL, NULL) \
+                                       : hko_penalized_stage_solve(fin, a, eps[c], p->pen_coeff, n, vmax, out, NULL))
+#define NOTE(x) do { int s_ = (x); if (s_ && s_ != HKO_NUMERICAL_CONSISTENCY && !st) st = s_; } while (0)
+        const double inv_a = 1.0 / t.a_im00, inv_a2 = 1.0 / t.a_im11;
+        for (long c = 0; c < cells; ++c) {
+            if (!rn[c]) continue;
+            NOTE(STAGE(f + c * nb, t.a_im00 * dt, Y + c * nb));
+            for (long i = 0; i < nb; ++i) k1[c * nb + i] = (Y[c * nb + i] - f[c * nb + i]) * inv_a;
+        }
+        for (long c = 0; c < cells; ++c) { /* q1 = T(Y1) + res(Y1) / eps */
+            if (!rn[c]) continue;
+            const long i = c % nx, j = c / nx;
+            const double* fx[5];
+            const double* fy[5];
+            for (int pp = -2; pp <= 2; ++pp) {
+                fx[pp + 2] = Y + (j * nx + wrapi(i + pp, nx)) * nb;
+                fy[pp + 2] = Y + (wrapi(j + pp, ny) * nx + i) * nb;
+            }
+            hko_transport_rhs_cell(fx, fy, n, vmax, dx, dy, p->eps_weno, q1 + c * nb);
+            if (rn[c] == 2) {
+                NOTE(hko_penalized_residual(k, Y + c * nb, p->pen_coeff, res, NULL));
+                const double inv_eps = 1.0 / eps[c];
+                for (long kk = 0; kk < nb; ++kk) q1[c * nb + kk] += res[kk] * inv_eps;
+            }
+        }
+        for (long c = 0; c < cells; ++c) { /* Y2 */
+            if (!rn[c]) continue;
+            for (long i = 0; i < nb; ++i) fa[i] = f[c * nb + i] + dt * t.a_ex10 * q1[c * nb + i] + t.a_im10 * k1[c * nb + i];
+            NOTE(STAGE(fa, t.a_im11 * dt, Y + c * nb));
+        }
+        double* fnew = (double*)malloc(sizeof(double) * cells * nb);
+        for (long c = 0; c < cells; ++c) { /* final combination */
+            if (!rn[c]) continue;
+            const long i = c % nx, j = c / nx;
+            const double* fx[5];
+            const double* fy[5];
+            for (int pp = -2; pp <= 2; ++pp) {
+                fx[pp + 2] = Y + (j * nx + wrapi(i + pp, nx)) * nb;
+                fy[pp + 2] = Y + (wrapi(j + pp, ny) * nx + i) * nb;
+            }
+            hko_transport_rhs_cell(fx, fy, n, vmax, dx, dy, p->eps_weno, q2);
+            if (rn[c] == 2) NOTE(hko_penalized_residual(k, Y + c * nb, p->pen_coeff, res, NULL));
+            const double inv_eps = 1.0 / eps[c];
+            const double* fc = f + c * nb;
+            for (long kk = 0; kk < nb; ++kk) {
+                const double q2k = rn[c] == 2 ? q2[kk] + res[kk] * inv_eps : q2[kk];
+                const double facc = fc[kk] + dt * t.a_ex10 * q1[c * nb + kk] + t.a_im10 * k1[c * nb + kk];
+                const double k2 = (Y[c * nb + kk] - facc) * inv_a2;
+                fnew[c * nb + kk] = fc[kk] + (dt * (t.w_ex0 * q1[c * nb + kk] + t.w_ex1 * q2k) +
+                                              t.w_im0 * k1[c * nb + kk] + t.w_im1 * k2);
+            }
+        }
+        for (long c = 0; c < cells; ++c)
+            if (rn[c]) memcpy(f + c * nb, fnew + c * nb, sizeof(double) * nb);
+#undef STAGE
+#undef NOTE
+        free(fnew); free(Y); free(q1); free(k1); free(fa); free(res); free(q2);
+    }
+    if (!st) memcpy(r, rn, cells);
+    if (counts) {
+        counts[0] = nl[0]; counts[1] = nl[1]; counts[2] = nl[2];
+        counts[3] = n01; counts[4] = n10; counts[5] = nhalo;
+    }
+    free(mom); free(W); free(rn);
+    return st;
+}

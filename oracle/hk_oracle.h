@@ -188,6 +188,26 @@ int hko_synthesize_distribution(int nx, int ny, int n, double vmax, const hko_ob
                                 const unsigned char* kind, const double* hydro, const double* f, double heat_ratio,
                                 int i, int j, double* out);
 
+/* ---------------- hybrid time step (restatement; the reference's driver is absent) ----------------
+ * One step of the hybrid scheme on a periodic nx x ny torus without obstacles,
+ * as SPEC.md harness run_scenario and PAPER.md Algorithm 1 describe it and as
+ * include/hykin_b200.h:hk_hybrid_step states it: indicator pass at t^n
+ * (hydro view = U on layer 0, moments_of(f) on kinetic cells), regime_update
+ * (src/regime.cpp:25-52), convert_on_transition (:54-72), layer 0 = TVD-RK2
+ * of the hydro view (src/euler.cpp:172-181) kept on r == 0, kinetic cells = one
+ * PR(2,2,2) step (ES-BGK on r == 1, penalized Boltzmann on r == 2) whose
+ * transport stencil reads the frozen Maxwellian of the t^n hydro state on the
+ * layer-0 cells within +-2 cells (synthesize_distribution, src/coupling.cpp:72-93).
+ * counts (nullable): n0, n1, n2 after the step, transitions 0->1, 1->0, halo
+ * blocks.  Returns the first failure (HKO_POSITIVITY / HKO_DEGENERATE). */
+typedef struct {
+    double eta0, eta1, delta0, mu0, kappa0;
+    int signed_sum, update_regimes;
+    double heat_ratio, esbgk_beta, nu_coeff, pen_coeff, eps_weno;
+} hko_hybrid_params;
+int hko_hybrid_step(int nx, int ny, const hko_kernel* k, double dx, double dy, double dt, const double* eps,
+                    signed char* r, double* hydro, double* f, const hko_hybrid_params* p, long counts[6]);
+
 #ifdef __cplusplus
 }
 #endif

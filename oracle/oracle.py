@@ -331,6 +331,30 @@ class Oracle:
                                           C.c_double(eps_weno), 1)
         return f, st
 
+    def hybrid_step(self, k: OracleKernel, nx, ny, dx, dy, dt, eps_cell, r, hydro, f, params):
+        """hko_hybrid_step on copies; params = paper_2505_03360_b200.HybridParams-like object
+        with the hko_hybrid_params fields.  Returns (status, r, hydro, f, counts[6])."""
+        r = np.ascontiguousarray(r, dtype=np.int8).copy()
+        hydro = np.ascontiguousarray(hydro, dtype=np.float64).copy()
+        f = np.ascontiguousarray(f, dtype=np.float64).copy()
+        e = np.ascontiguousarray(eps_cell, dtype=np.float64)
+        hp = HkoHybridParams(params.eta0, params.eta1, params.delta0, params.mu0, params.kappa0,
+                             int(params.signed_sum), int(params.update_regimes), params.heat_ratio,
+                             params.esbgk_beta, params.nu_coeff, params.pen_coeff, params.eps_weno)
+        counts = np.zeros(6, dtype=np.int64)
+        st = self.lib.hko_hybrid_step(nx, ny, k.ref, C.c_double(dx), C.c_double(dy), C.c_double(dt), _ptr(e),
+                                      r.ctypes.data_as(C.c_void_p), _ptr(hydro), _ptr(f), C.byref(hp),
+                                      counts.ctypes.data_as(C.c_void_p))
+        return st, r, hydro, f, counts
+
+
+class HkoHybridParams(C.Structure):
+    """hko_hybrid_params (oracle/hk_oracle.h)."""
+    _fields_ = [("eta0", C.c_double), ("eta1", C.c_double), ("delta0", C.c_double), ("mu0", C.c_double),
+                ("kappa0", C.c_double), ("signed_sum", C.c_int), ("update_regimes", C.c_int),
+                ("heat_ratio", C.c_double), ("esbgk_beta", C.c_double), ("nu_coeff", C.c_double),
+                ("pen_coeff", C.c_double), ("eps_weno", C.c_double)]
+
 
 class RefKernel:
     def __init__(self, lib, n, vmax, a1, a2, r_phys):

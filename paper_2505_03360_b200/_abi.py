@@ -73,6 +73,14 @@ class ObstacleSpec(C.Structure):
     def temperature(self) -> float:
         return self.pressure / self.rho
 
+class HybridParams(C.Structure):
+    """hk_hybrid_params (include/hykin_b200.h): thresholds, physics and collision flags of hk_hybrid_step."""
+    _fields_ = [("eta0", C.c_double), ("eta1", C.c_double), ("delta0", C.c_double), ("mu0", C.c_double),
+                ("kappa0", C.c_double), ("signed_sum", C.c_int), ("update_regimes", C.c_int),
+                ("heat_ratio", C.c_double), ("esbgk_beta", C.c_double), ("nu_coeff", C.c_double),
+                ("pen_coeff", C.c_double), ("eps_weno", C.c_double), ("coll_flags", C.c_uint32)]
+
+
 _lib = None
 
 
@@ -138,6 +146,8 @@ def lib() -> C.CDLL:
                                           vp]),
         "hk_synthesize_distributions": (C.c_int, [vp, C.c_int, dbl, i64, i64, C.POINTER(ObstacleSpec), vp, vp, vp, vp,
                                                   dbl, vp, i64, vp, C.POINTER(C.c_int64)]),
+        "hk_hybrid_step": (C.c_int, [vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, vp, vp, vp, C.POINTER(HybridParams),
+                                     C.POINTER(C.c_int64)]),
         "hk_apply_obstacle": (C.c_int, [vp, C.c_int, dbl, C.POINTER(ObstacleSpec), i64, i64, vp, vp, vp, vp, dbl,
                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     }

@@ -86,6 +86,8 @@ int hk_ctx_destroy(hk_ctx ctx) {
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->fix_scratch) cudaFree(ctx->fix_scratch);
     if (ctx->step_work) cudaFree(ctx->step_work);
+    if (ctx->hyb_small) cudaFree(ctx->hyb_small);
+    if (ctx->hyb_big) cudaFree(ctx->hyb_big);
     if (ctx->bad_flag) cudaFree(ctx->bad_flag);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->s_in) cudaStreamDestroy(ctx->s_in);

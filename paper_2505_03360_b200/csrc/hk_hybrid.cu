@@ -1,0 +1,437 @@
+// hk_hybrid.cu — the hybrid time step (SURVEY §8f "next" #1), sm_100a.
+//
+// The reference ships the per-cell pieces of its hybrid scheme but not the
+// step driver (simulation.cpp is absent): regime_update (src/regime.cpp:25-52),
+// convert_on_transition (:54-72), synthesize_hydro_state /
+// synthesize_distribution (src/coupling.cpp:57-93), the layer-0 TVD-RK2
+// (src/euler.cpp:172-181) and the PR(2,2,2) kinetic steps
+// (src/boltzmann.cpp:47-110, src/esbgk.cpp:47-99).  hk_hybrid_step composes
+// them as SPEC.md's run_scenario loop and PAPER.md Algorithm 1 describe
+// (indicator pass -> regime update + conversion -> per-layer stage updates
+// with cross-layer stencil synthesis); oracle/hk_oracle.c:hko_hybrid_step is
+// the CPU statement of the same step (include/hykin_b200.h has the contract).
+//
+// Device layout: the distribution field stays dense [cell][n^3] (the transport
+// sweep needs the spatial neighbours), but every per-cell kinetic operation
+// (stage solves, penalized residual = collision, IMEX combinations) runs on a
+// compact batch of the kinetic cells [K1 (ES-BGK) | K2 (Boltzmann)] gathered
+// once per step, so the ~80 % layer-0 cells of config 4 cost nothing there.
+// The dense field doubles as the transport input: the compact stage values
+// are scattered into it, the layer-0 halo holds the frozen Maxwellians.
+// Lists are built by one single-CTA ordered compaction (cell order, so the
+// batch order is deterministic); the host reads the list lengths once.
+// Compiled without FMA contraction: the conversions are bitwise the reference.
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "hk_cells.cuh"
+#include "hk_common.cuh"
+#include "hk_internal.h"
+
+namespace hk {
+namespace {
+
+constexpr int kLT = 1024;  // threads of the list kernels
+
+struct HybCounts {
+    unsigned long long bad;  // (cell << 8) | status, lowest first
+    int nk_old, n1, n2, nm, n01, n10, n0;
+};
+
+__device__ void fail_at(HybCounts* c, int64_t cell, int code) {
+    atomicMin(&c->bad, ((unsigned long long)cell << 8) | (unsigned)code);
+}
+
+// moments_from_conserved (src/coupling.cpp:7-13)
+__device__ bool mom_from_u(const double* u, double hr, double* m) {
+    if (!(u[0] > 0.0)) return false;
+    const double p = (hr - 1.0) * (u[3] - 0.5 * (u[1] * u[1] + u[2] * u[2]) / u[0]);
+    if (!(p > 0.0)) return false;
+    m[0] = u[0];
+    m[1] = u[1] / u[0];
+    m[2] = u[2] / u[0];
+    m[3] = 0.0;
+    m[4] = p / u[0];
+    return true;
+}
+
+// conserved_from_moments (src/coupling.cpp:15-22)
+__device__ void u_from_mom(const double* m, double hr, double* u) {
+    const double rho = m[0];
+    u[0] = rho;
+    u[1] = rho * m[1];
+    u[2] = rho * m[2];
+    const double u2 = m[1] * m[1] + m[2] * m[2] + m[3] * m[3];
+    u[3] = rho * m[4] / (hr - 1.0) + 0.5 * rho * u2;
+}
+
+// Ordered block compaction: returns this thread's slot among the predicated
+// threads of the chunk (running offset *base, updated for the next chunk).
+__device__ int block_slot(bool pred, int* warp_tot, int* base) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (lane == 0) warp_tot[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {
+        int v = warp_tot[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        warp_tot[32 + lane] = v;  // inclusive
+    }
+    __syncthreads();
+    const int before = (warp ? warp_tot[32 + warp - 1] : 0) + __popc(m & ((1u << lane) - 1u));
+    const int slot = *base + before;
+    __syncthreads();
+    if (threadIdx.x == kLT - 1) *base += warp_tot[32 + 31];
+    __syncthreads();
+    return slot;
+}
+
+// Pass A (t^n): the kinetic cells in cell order, pos[c] = batch index or -1.
+__global__ void __launch_bounds__(kLT) list_old_kernel(int64_t cells, const int8_t* __restrict__ r,
+                                                       int64_t* __restrict__ list, int* __restrict__ pos,
+                                                       HybCounts* cnt) {
+    __shared__ int wt[64];
+    __shared__ int base;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < cells; c0 += kLT) {
+        const int64_t c = c0 + threadIdx.x;
+        const bool kin = c < cells && r[c] != 0;
+        const int s = block_slot(kin, wt, &base);
+        if (c < cells) {
+            pos[c] = kin ? s : -1;
+            if (kin) list[s] = c;
+        }
+    }
+    if (threadIdx.x == 0) cnt->nk_old = base;
+}
+
+// Hydro view at t^n: mom5 of every cell (layer 0: moments_from_conserved(U);
+// kinetic: moments_of(f) from the compact batch), L1 distances of the kinetic cells.
+__global__ void view_kernel(int64_t cells, const int8_t* __restrict__ r, const double* __restrict__ U, double hr,
+                            const int* __restrict__ pos, const double* __restrict__ momk,
+                            const double* __restrict__ l1k, const int* __restrict__ stk, double* __restrict__ mom,
+                            double* __restrict__ l1, HybCounts* cnt) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    double* m = mom + 5 * c;
+    if (r[c] == 0) {
+        if (!mom_from_u(U + 4 * c, hr, m)) {
+            fail_at(cnt, c, HK_POSITIVITY);
+            for (int e = 0; e < 5; ++e) m[e] = 1.0;  // keeps the classifier finite; the step fails
+        }
+        l1[c] = 0.0;
+    } else {
+        const int k = pos[c];
+        for (int e = 0; e < 5; ++e) m[e] = momk[5 * k + e];
+        l1[c] = l1k[k];
+        if (stk[k]) {
+            fail_at(cnt, c, stk[k]);
+            m[0] = m[4] = 1.0;
+        }
+    }
+}
+
+// convert_on_transition (src/regime.cpp:54-72) 1 -> 0, the hydro view W fed to
+// the Euler step, transition counts.
+__global__ void convert_kernel(int64_t cells, const int8_t* __restrict__ r_old, const int8_t* __restrict__ r_new,
+                               double* __restrict__ U, const double* __restrict__ mom, double hr,
+                               double* __restrict__ W, HybCounts* cnt) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    const int ro = r_old[c], rn = r_new[c];
+    double* w = W + 4 * c;
+    if (ro == 0) {
+        for (int e = 0; e < 4; ++e) w[e] = U[4 * c + e];
+        if (rn != 0) atomicAdd(&cnt->n01, 1);
+    } else {
+        u_from_mom(mom + 5 * c, hr, w);
+        if (rn == 0) {
+            for (int e = 0; e < 4; ++e) U[4 * c + e] = w[e];
+            atomicAdd(&cnt->n10, 1);
+        }
+    }
+    if (rn == 0) atomicAdd(&cnt->n0, 1);
+}
+
+__device__ __forceinline__ bool kin_at(const int8_t* r, int nx, int ny, int i, int j) {
+    i = (i % nx + nx) % nx;
+    j = (j % ny + ny) % ny;
+    return r[(int64_t)j * nx + i] != 0;
+}
+
+// Pass B (after the update): batch [K1 | K2] in cell order with their Knudsen
+// numbers, and the Maxwellian targets: 0 -> 1 transitions and the layer-0
+// cells on the periodic +-2 transport stencil of a kinetic cell, with the
+// moments of their (post-conversion) hydro state.
+__global__ void __launch_bounds__(kLT) list_new_kernel(int nx, int ny, const int8_t* __restrict__ r_old,
+                                                       const int8_t* __restrict__ r_new,
+                                                       const double* __restrict__ U, double hr,
+                                                       const double* __restrict__ eps, int64_t* __restrict__ list,
+                                                       int64_t* __restrict__ tmp2, double* __restrict__ eps_k,
+                                                       int64_t* __restrict__ mlist, double* __restrict__ mmom,
+                                                       HybCounts* cnt) {
+    __shared__ int wt[64];
+    __shared__ int b1, b2, bm;
+    const int64_t cells = (int64_t)nx * ny;
+    if (threadIdx.x == 0) b1 = b2 = bm = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < cells; c0 += kLT) {
+        const int64_t c = c0 + threadIdx.x;
+        int rn = 0, ro = 0;
+        bool halo = false;
+        if (c < cells) {
+            rn = r_new[c];
+            ro = r_old[c];
+            if (rn == 0) {
+                const int i = int(c % nx), j = int(c / nx);
+                for (int d = 1; d <= 2 && !halo; ++d)
+                    halo = kin_at(r_new, nx, ny, i - d, j) || kin_at(r_new, nx, ny, i + d, j) ||
+                           kin_at(r_new, nx, ny, i, j - d) || kin_at(r_new, nx, ny, i, j + d);
+            }
+        }
+        const int s1 = block_slot(rn == 1, wt, &b1);
+        const int s2 = block_slot(rn == 2, wt, &b2);
+        const bool mw = halo || (ro == 0 && rn != 0);
+        const int sm = block_slot(mw, wt, &bm);
+        if (rn == 1) list[s1] = c;
+        if (rn == 2) tmp2[s2] = c;
+        if (mw) {
+            mlist[sm] = c;
+            if (!mom_from_u(U + 4 * c, hr, mmom + 5 * sm)) {
+                fail_at(cnt, c, HK_POSITIVITY);
+                for (int e = 0; e < 5; ++e) mmom[5 * sm + e] = 1.0;
+            }
+        }
+    }
+    __syncthreads();
+    const int n1 = b1, n2 = b2;
+    for (int k = threadIdx.x; k < n2; k += kLT) list[n1 + k] = tmp2[k];
+    __syncthreads();
+    for (int k = threadIdx.x; k < n1 + n2; k += kLT) eps_k[k] = eps[list[k]];
+    if (threadIdx.x == 0) {
+        cnt->n1 = n1;
+        cnt->n2 = n2;
+        cnt->nm = bm;
+    }
+}
+
+// Layer-0 cells take the Euler result; the layer map advances.
+__global__ void commit_kernel(int64_t cells, const int8_t* __restrict__ r_new, int8_t* __restrict__ r,
+                              const double* __restrict__ W, double* __restrict__ U, int euler) {
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= cells) return;
+    const int rn = r_new[c];
+    if (euler && rn == 0)
+        for (int e = 0; e < 4; ++e) U[4 * c + e] = W[4 * c + e];
+    r[c] = (int8_t)rn;
+}
+
+// Per-cell statuses of the batch (stage info: status | fallback << 8; residual status).
+__global__ void status_kernel(int64_t nk, const int64_t* __restrict__ list, const int* __restrict__ st,
+                              HybCounts* cnt) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= nk) return;
+    const int s = st[k] & 0xff;
+    if (s && s != HK_NUMERICAL_CONSISTENCY) fail_at(cnt, list[k], s);
+}
+
+unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
+
+// Grow-only device buffer owned by the context.
+int grow(hk_ctx ctx, void** p, size_t* have, size_t need, const char* what) {
+    if (need <= *have) return HK_OK;
+    if (*p) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(*p);
+        *p = nullptr;
+        *have = 0;
+    }
+    if (cudaMalloc(p, need) != cudaSuccess) return fail(ctx, HK_CUDA, std::string("hybrid step: cannot allocate ") + what);
+    *have = need;
+    return HK_OK;
+}
+
+template <class T>
+T* carve(char*& p, int64_t count) {
+    T* out = reinterpret_cast<T*>(p);
+    p += (sizeof(T) * count + 255) & ~size_t(255);
+    return out;
+}
+
+struct PR {
+    double a_ex10, a_im00, a_im10, a_im11;
+};
+PR pr222_t() {  // ImexTableau::pr222 (inc/imex.hpp:23-34)
+    const double C = 1.0 / std::sqrt(2.0);
+    const double delta = 1.0 - 1.0 / (2.0 * C);
+    return {1.0, 1.0 - C, C - delta, delta};
+}
+
+int read_counts(hk_ctx ctx, const HybCounts* dev, HybCounts& h, const char* what) {
+    int st = check_cuda(ctx, cudaMemcpyAsync(&h, dev, sizeof h, cudaMemcpyDeviceToHost, ctx->stream), what);
+    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), what);
+    if (!st && h.bad != ~0ull)
+        st = fail(ctx, int(h.bad & 0xff), std::string(what) + ": cell failed", int64_t(h.bad >> 8));
+    return st;
+}
+
+}  // namespace
+}  // namespace hk
+
+using namespace hk;
+
+extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx, double dy, double dt,
+                              const double* eps_dev, int8_t* r_dev, double* hydro_dev, double* f_dev,
+                              const hk_hybrid_params* p, int64_t* counts) {
+    if (!ctx || !k || !p) return HK_CONTRACT;
+    if (nx < 1 || ny < 1) return fail(ctx, HK_CONTRACT, "hybrid step: empty grid");
+    if (p->update_regimes && (!(p->eta0 > 0.0) || !(p->eta1 > 0.0) || !(p->delta0 > 0.0)))
+        return fail(ctx, HK_CONFIG, "regime thresholds eta0, eta1, delta0 must be positive");
+    cudaSetDevice(ctx->device);
+    ctx->err_cell = -1;
+    const int n = k->n;
+    const double vmax = k->vmax, hr = p->heat_ratio;
+    const int64_t cells = (int64_t)nx * ny, nb = (int64_t)n * n * n;
+    cudaStream_t s = ctx->stream;
+    int st;
+
+    // ---- per-cell workspace (fixed per grid) ----
+    const size_t small_need = 256 * 16 + (sizeof(double) * cells * (5 + 1 + 4 + 8 + 5 + 5 + 1 + 1) +
+                                          sizeof(int64_t) * cells * 4 + sizeof(int) * cells * 3 + cells * 2 + 4096);
+    if ((st = grow(ctx, &ctx->hyb_small, &ctx->hyb_small_bytes, small_need, "per-cell workspace"))) return st;
+    char* q = static_cast<char*>(ctx->hyb_small);
+    HybCounts* cnt = carve<HybCounts>(q, 1);
+    double* mom = carve<double>(q, 5 * cells);
+    double* l1 = carve<double>(q, cells);
+    double* W = carve<double>(q, 4 * cells);
+    double* ework = carve<double>(q, 8 * cells);
+    double* momk = carve<double>(q, 5 * cells);
+    double* mmom = carve<double>(q, 5 * cells);
+    double* l1k = carve<double>(q, cells);
+    double* eps_k = carve<double>(q, cells);
+    int64_t* list = carve<int64_t>(q, cells);
+    int64_t* tmp2 = carve<int64_t>(q, cells);
+    int64_t* mlist = carve<int64_t>(q, cells);
+    int64_t* list_old = carve<int64_t>(q, cells);
+    int* pos = carve<int>(q, cells);
+    int* stk = carve<int>(q, cells);
+    int* stk2 = carve<int>(q, cells);
+    int8_t* r_new = carve<int8_t>(q, cells);
+
+    HybCounts h0{};
+    h0.bad = ~0ull;
+    cudaMemcpyAsync(cnt, &h0, sizeof h0, cudaMemcpyHostToDevice, s);
+    cudaMemsetAsync(stk, 0, sizeof(int) * cells, s);
+
+    // ---- 1. indicator pass at t^n ----
+    list_old_kernel<<<1, kLT, 0, s>>>(cells, r_dev, list_old, pos, cnt);
+    if ((st = moments_launch(ctx, n, vmax, f_dev, cells, momk, nullptr, nullptr, l1k, stk, list_old, &cnt->nk_old)))
+        return st;
+    view_kernel<<<nblk(cells, 128), 128, 0, s>>>(cells, r_dev, hydro_dev, hr, pos, momk, l1k, stk, mom, l1, cnt);
+    ctx->launches += 2;
+    if (p->update_regimes) {
+        ClassifyParams cp{nx, ny, dx, dy, p->mu0, p->kappa0, p->eta0, p->eta1, p->delta0, p->signed_sum};
+        if ((st = classify_launch(ctx, cp, mom, eps_dev, l1, r_dev, r_new, nullptr, nullptr))) return st;
+    } else {
+        cudaMemcpyAsync(r_new, r_dev, cells, cudaMemcpyDeviceToDevice, s);
+    }
+    // ---- 2. conversion + the lists of the step ----
+    convert_kernel<<<nblk(cells, 128), 128, 0, s>>>(cells, r_dev, r_new, hydro_dev, mom, hr, W, cnt);
+    list_new_kernel<<<1, kLT, 0, s>>>(nx, ny, r_dev, r_new, hydro_dev, hr, eps_dev, list, tmp2, eps_k, mlist, mmom, cnt);
+    ctx->launches += 2;
+    if ((st = check_cuda(ctx, cudaGetLastError(), "hybrid lists"))) return st;
+    HybCounts h{};
+    if ((st = read_counts(ctx, cnt, h, "hybrid_step indicator pass"))) return st;
+    const int64_t n1 = h.n1, n2 = h.n2, nk = n1 + n2, nm = h.nm;
+    // Maxwellians of the 0 -> 1 cells and of the layer-0 transport halo
+    if (nm && (st = maxwellian_launch(ctx, n, vmax, mmom, nm, f_dev, nullptr, mlist, nullptr))) return st;
+
+    // ---- 3. layer 0: TVD-RK2 of the hydro view ----
+    const bool euler = h.n0 > 0;
+    if (euler && (st = hk_euler_tvd_rk2_step(ctx, W, nx, ny, dx, dy, dt, hr, p->eps_weno, ework))) return st;
+
+    // ---- 4. kinetic layers: PR(2,2,2) on the compact batch ----
+    if (nk) {
+        const size_t big_need = sizeof(double) * (size_t)nb * (size_t)(7 * nk + cells) + 8 * 256;
+        if ((st = grow(ctx, &ctx->hyb_big, &ctx->hyb_big_bytes, big_need, "kinetic workspace"))) return st;
+        char* b = static_cast<char*>(ctx->hyb_big);
+        double* fk = carve<double>(b, nk * nb);
+        double* Y = carve<double>(b, nk * nb);
+        double* k1 = carve<double>(b, nk * nb);
+        double* q1 = carve<double>(b, nk * nb);
+        double* tr = carve<double>(b, nk * nb);
+        double* res = carve<double>(b, nk * nb);
+        double* fa = carve<double>(b, nk * nb);
+        double* T = carve<double>(b, cells * nb);
+        const PR t = pr222_t();
+        cudaMemsetAsync(stk, 0, sizeof(int) * nk, s);
+        cudaMemsetAsync(stk2, 0, sizeof(int) * nk, s);
+        TransportParams tp{n, vmax, nx, ny, 0, dx, dy, p->eps_weno};
+        auto stages = [&](const double* fin, double a, double* out, double* k1o) -> int {
+            int e = HK_OK;
+            if (n1)
+                e = stage_launch(ctx, true, n, vmax, fin, out, n1, a, eps_k, 0.0, p->esbgk_beta, p->nu_coeff, stk,
+                                 nullptr, k1o, 1.0 / t.a_im00);
+            if (!e && n2)
+                e = stage_launch(ctx, false, n, vmax, fin + n1 * nb, out + n1 * nb, n2, a, eps_k + n1, 0.0, 0.0,
+                                 p->pen_coeff, stk + n1, nullptr, k1o ? k1o + n1 * nb : nullptr, 1.0 / t.a_im00);
+            return e;
+        };
+        auto residual = [&](const double* y) -> int {  // penalized_residual of the layer-2 part
+            if (!n2) return HK_OK;
+            int e = collision_launch(ctx, k, y + n1 * nb, res + n1 * nb, n2, p->coll_flags & ~HK_COLL_STRICT, nullptr);
+            return e ? e : residual_finish_launch(ctx, n, vmax, y + n1 * nb, res + n1 * nb, n2, p->pen_coeff, stk2 + n1);
+        };
+        auto transport = [&](const double* y) -> int {  // T(y) at the batch cells
+            int e = hk_scatter_cells(ctx, nb, y, list, nk, f_dev);
+            if (!e) e = transport_launch(ctx, tp, f_dev, T);
+            if (!e) e = hk_gather_cells(ctx, nb, T, list, nk, tr);
+            return e;
+        };
+        // q = tr (+ res / eps on the layer-2 part), via the IMEX combinations
+        auto explicit_part = [&](int op, double* o, const double* f0, const double* y) -> int {
+            int e = HK_OK;
+            if (n1) e = combine_launch(ctx, op, n1 * nb, nb, dt, eps_k, o, f0, y, q1, k1, tr, nullptr);
+            if (!e && n2)
+                e = combine_launch(ctx, op, n2 * nb, nb, dt, eps_k + n1, o + n1 * nb, f0 ? f0 + n1 * nb : nullptr,
+                                   y ? y + n1 * nb : nullptr, q1 + n1 * nb, k1 + n1 * nb, tr + n1 * nb, res + n1 * nb);
+            return e;
+        };
+        st = hk_gather_cells(ctx, nb, f_dev, list, nk, fk);                               // f^n of the batch
+        if (!st) st = stages(fk, t.a_im00 * dt, Y, k1);                                   // Y1, k1
+        if (!st) st = transport(Y);                                                       // T(Y1)
+        if (!st) st = residual(Y);                                                        // res(Y1)
+        if (!st) st = explicit_part(1, q1, nullptr, nullptr);                             // q1
+        if (!st) st = combine_launch(ctx, 2, nk * nb, nb, dt, eps_k, fa, fk, nullptr, q1, k1, nullptr, nullptr);
+        if (!st) st = stages(fa, t.a_im11 * dt, Y, nullptr);                              // Y2
+        if (!st) st = transport(Y);                                                       // T(Y2)
+        if (!st) st = residual(Y);                                                        // res(Y2)
+        if (!st) st = explicit_part(3, fk, nullptr, Y);                                   // final, in place
+        if (!st) st = hk_scatter_cells(ctx, nb, fk, list, nk, f_dev);
+        if (!st) {
+            status_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, stk, cnt);
+            status_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, stk2, cnt);
+            ctx->launches += 2;
+        }
+        if (st) return st;
+    }
+    commit_kernel<<<nblk(cells, 256), 256, 0, s>>>(cells, r_new, r_dev, W, hydro_dev, euler ? 1 : 0);
+    ctx->launches++;
+    if ((st = check_cuda(ctx, cudaGetLastError(), "hybrid commit"))) return st;
+    HybCounts e{};
+    if ((st = read_counts(ctx, cnt, e, "hybrid_step stage updates"))) return st;
+    if (counts) {
+        counts[0] = e.n0;
+        counts[1] = e.n1;
+        counts[2] = e.n2;
+        counts[3] = e.n01;
+        counts[4] = e.n10;
+        counts[5] = e.nm - e.n01;
+    }
+    return HK_OK;
+}

@@ -42,6 +42,11 @@ struct hk_ctx_s {
     // work fields of the device-resident IMEX steps (hk_steps.cu)
     void* step_work = nullptr;
     size_t step_bytes = 0;
+    // hybrid step workspaces (hk_hybrid.cu): per-cell arrays, kinetic batch + dense transport output
+    void* hyb_small = nullptr;
+    size_t hyb_small_bytes = 0;
+    void* hyb_big = nullptr;
+    size_t hyb_big_bytes = 0;
     // Nyquist-correction plane scratch (hk_nyqfix.cu)
     void* fix_scratch = nullptr;
     size_t fix_bytes = 0;

@@ -347,3 +347,37 @@ def obstacle_fields(kind: np.ndarray, n: int, seed_salt: int = 0, bad_cells=()):
     has = ((r != 0) & (kind != 1)).astype(np.uint8)
     f = np.where(has[:, None] != 0, rng.uniform(0.0, 1e-2, (cells, n ** 3)), 0.0)
     return r, hydro, f, has
+
+
+def config4_band(nx: int, ny: int, half_width: float = 0.025) -> np.ndarray:
+    """[nx*ny] bool: cells whose centre lies within half_width of an interface
+    (x = 0.5, y = 0.5 and the periodic wrap x = 0, y = 0) of config 4's [0,1]^2."""
+    x = (np.arange(nx) + 0.5) / nx
+    y = (np.arange(ny) + 0.5) / ny
+    dxi = np.minimum(np.abs(x - 0.5), np.minimum(x, 1.0 - x))
+    dyi = np.minimum(np.abs(y - 0.5), np.minimum(y, 1.0 - y))
+    X, Y = np.meshgrid(dxi, dyi)
+    return ((X < half_width) | (Y < half_width)).reshape(-1)
+
+
+def config4_hybrid_state(nx: int = 200, ny: int = 200, n: int = 32, half_width: float = 0.025,
+                         eps_fluid: float = 1e-3, eps_band: float = 1e-1, with_f: bool = True, seed_salt: int = 0):
+    """Initial state of config 4's hybrid run: quadrant Riemann data at rest
+    (tanh edges over 2 cells), Knudsen eps_fluid with eps_band on the interface
+    band, the band starting in layer 2 (the rest in layer 0) with f = the
+    Maxwellian of its hydro state.  Returns (hydro [cells,4], eps [cells],
+    r int8 [cells], f [cells, n^3] or None); f is dense with zero blocks on layer 0."""
+    hydro = config4_conserved(nx, ny, seed_salt=seed_salt, smooth=True)
+    rho = hydro[:, 0]
+    T = (2.0 / 3.0) * (hydro[:, 3] - 0.5 * (hydro[:, 1] ** 2 + hydro[:, 2] ** 2) / rho) / rho
+    hydro[:, 1:3] = 0.0  # at rest (BASELINE config 4: zero velocity)
+    hydro[:, 3] = 1.5 * rho * T
+    band = config4_band(nx, ny, half_width)
+    eps = np.where(band, eps_band, eps_fluid)
+    r = np.where(band, 2, 0).astype(np.int8)
+    f = None
+    if with_f:
+        f = np.zeros((nx * ny, n ** 3))
+        for c in np.nonzero(band)[0]:
+            f[c] = maxwellian(n, rho[c], (0.0, 0.0, 0.0), T[c])
+    return hydro, eps, r, f

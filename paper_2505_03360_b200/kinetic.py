@@ -338,3 +338,55 @@ def synthesize_distribution(nx: int, ny: int, vgrid: VelocityGrid, r, kind, hydr
                                                    kind.data_ptr(), hydro.data_ptr(), f.data_ptr(), heat_ratio,
                                                    idx.data_ptr(), idx.numel(), out.data_ptr(), C.byref(filled)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Hybrid time step (SURVEY §8f "next" #1; contract in include/hykin_b200.h)
+# ---------------------------------------------------------------------------
+@dataclass
+class HybridParams:
+    """Thresholds + physics of one hybrid step (ScenarioConfig, inc/hykin/scenario.hpp:39-63)."""
+    eta0: float = 1e-3
+    eta1: float = 1e-2
+    delta0: float = 1e-3
+    mu0: float = 1.0
+    kappa0: float = 1.0
+    signed_sum: bool = False
+    update_regimes: bool = True
+    heat_ratio: float = 5.0 / 3.0
+    esbgk_beta: float = -0.5
+    nu_coeff: float = 0.5 * math.pi
+    pen_coeff: float = 2.0 * math.pi
+    eps_weno: float = 1e-6
+    exact: bool = False  # collision of the residuals on the exact (two-transform) path
+
+    def to_c(self) -> "_abi.HybridParams":
+        return _abi.HybridParams(self.eta0, self.eta1, self.delta0, self.mu0, self.kappa0, int(self.signed_sum),
+                                 int(self.update_regimes), self.heat_ratio, self.esbgk_beta, self.nu_coeff,
+                                 self.pen_coeff, self.eps_weno, _abi.HK_COLL_EXACT if self.exact else 0)
+
+
+class HybridCounts(NamedTuple):
+    layer0: int
+    layer1: int
+    layer2: int
+    to_kinetic: int   # 0 -> 1 transitions
+    to_fluid: int     # 1 -> 0 transitions
+    halo_blocks: int  # layer-0 Maxwellian blocks synthesized for the transport stencil
+
+
+def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, dt: float, eps_cell, r, hydro, f,
+                params: HybridParams = HybridParams()) -> HybridCounts:
+    """One hybrid step in place on device tensors: r [cells] int8, hydro [cells, 4]
+    conserved, f [cells, n^3] dense, eps_cell [cells].  Algorithm 1 regime update,
+    convert_on_transition, Euler TVD-RK2 on layer 0, PR(2,2,2) ES-BGK / penalized
+    Boltzmann on layers 1 / 2 with the cross-layer transport halo."""
+    ctx = kernel.ctx
+    for t, dt_ in ((r, torch.int8), (hydro, torch.float64), (f, torch.float64)):
+        assert t.is_cuda and t.dtype == dt_ and t.is_contiguous()
+    e = eps_cell.to(device=f.device, dtype=torch.float64).contiguous()
+    counts = (C.c_int64 * 6)()
+    hp = params.to_c()
+    ctx.check(ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),
+                                      hydro.data_ptr(), f.data_ptr(), C.byref(hp), counts))
+    return HybridCounts(*[int(c) for c in counts])

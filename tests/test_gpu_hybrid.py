@@ -1,0 +1,95 @@
+"""GPU parity of the hybrid time step (hk_hybrid_step) against the oracle's
+restatement (oracle/hk_oracle.c:hko_hybrid_step, itself pinned to the
+single-layer steps by tests/test_hybrid_oracle.py): layer maps identical,
+hydro states of layer-0 cells to 1e-12, kinetic distributions to 1e-10
+relative L2 per cell, transition counts identical."""
+import numpy as np
+import pytest
+
+from paper_2505_03360_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_both(hk, oracle, nx, ny, n, a1, a2, band_layer, steps, params=None, state=None):
+    import torch
+    from paper_2505_03360_b200 import kinetic
+    hydro, eps, r, f = state if state is not None else inputs.config4_hybrid_state(nx, ny, n, half_width=1.0 / nx)
+    if band_layer is not None:
+        r = np.where(r != 0, band_layer, 0).astype(np.int8)
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    ok = oracle.kernel(n, inputs.VMAX, a1, a2, inputs.R_PHYS_MAX)
+    dx, dy = 1.0 / nx, 1.0 / ny
+    dt = 0.5 * dx / (inputs.VMAX - inputs.VMAX / n)
+    p = params or kinetic.HybridParams()
+    rd = torch.from_numpy(r).cuda()
+    hd = torch.from_numpy(hydro).cuda()
+    fd = torch.from_numpy(f).cuda()
+    ed = torch.from_numpy(eps).cuda()
+    ro, ho, fo = r, hydro, f
+    for s in range(steps):
+        r_before = ro
+        cg = kinetic.hybrid_step(kern, nx, ny, dx, dy, dt, ed, rd, hd, fd, p)
+        st, ro, ho, fo, co = oracle.hybrid_step(ok, nx, ny, dx, dy, dt, eps, ro, ho, fo, p)
+        assert st == 0
+        assert list(cg) == [int(c) for c in co], (s, cg, co)
+        rg = rd.cpu().numpy()
+        assert np.array_equal(rg, ro), s
+        hg = hd.cpu().numpy()
+        fl = ro == 0
+        assert np.max(np.abs(hg[fl] - ho[fl]) / np.abs(ho[fl]).max(axis=1, keepdims=True)) < 1e-12, s
+        fg = fd.cpu().numpy()
+        for c in np.nonzero(ro != 0)[0]:
+            e = np.linalg.norm(fg[c] - fo[c]) / np.linalg.norm(fo[c])
+            assert e < 1e-10, (s, c, e)
+        yield s, r_before, ro, cg
+
+
+def test_hybrid_config4_shape_n16(hk, oracle):
+    """Quadrant Riemann data, Boltzmann band, Algorithm 1 on: 2 steps with transitions."""
+    seen = []
+    for s, rb, ra, cg in _run_both(hk, oracle, 16, 12, 16, 4, 4, 2, 2):
+        seen.append(cg)
+    assert seen[0].layer2 > 0 and any(c.to_kinetic for c in seen)
+
+
+def test_hybrid_esbgk_band_n32(hk, oracle):
+    """N = 32 transport path, ES-BGK band (layer 1), Algorithm 1 on."""
+    for _ in _run_both(hk, oracle, 10, 8, 32, 4, 4, 1, 1):
+        pass
+
+
+def test_hybrid_frozen_layers(hk, oracle):
+    """update_regimes off: the given layer map is kept, all three layers present."""
+    from paper_2505_03360_b200 import kinetic
+    nx, ny, n = 12, 10, 16
+    hydro, eps, r, f = inputs.config4_hybrid_state(nx, ny, n, half_width=1.0 / nx)
+    r = r.copy()
+    r[(np.arange(nx * ny) % nx) < 3] = 1  # a layer-1 stripe next to the layer-2 band
+    kin = (r != 0) & ~np.any(f != 0, axis=1)
+    for c in np.nonzero(kin)[0]:
+        rho = hydro[c, 0]
+        T = hydro[c, 3] / (1.5 * rho)
+        f[c] = inputs.maxwellian(n, rho, (0.0, 0.0, 0.0), T)
+    for s, rb, ra, cg in _run_both(hk, oracle, nx, ny, n, 4, 4, None, 1,
+                                   params=kinetic.HybridParams(update_regimes=False), state=(hydro, eps, r, f)):
+        assert np.array_equal(rb, ra)
+
+
+def test_hybrid_all_fluid_and_positivity(hk):
+    import torch
+    from paper_2505_03360_b200 import kinetic
+    nx, ny, n = 8, 8, 16
+    hydro, eps, r, f = inputs.config4_hybrid_state(nx, ny, n, half_width=1e-9)
+    assert not np.any(r)
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, n, 4, 4, inputs.R_PHYS_MAX)
+    rd, hd, fd, ed = (torch.from_numpy(x).cuda() for x in (r, hydro, f, eps))
+    cg = kinetic.hybrid_step(kern, nx, ny, 1 / nx, 1 / ny, 1e-3, ed, rd, hd, fd, kinetic.HybridParams())
+    assert cg.layer0 == nx * ny and cg.layer1 + cg.layer2 == 0 and cg.halo_blocks == 0
+    bad = hydro.copy()
+    bad[37, 3] = -1.0  # negative pressure: moments_from_conserved throws positivity_error
+    hd = torch.from_numpy(bad).cuda()
+    with pytest.raises(hk.positivity_error):
+        kinetic.hybrid_step(kern, nx, ny, 1 / nx, 1 / ny, 1e-3, ed, rd, hd, fd, kinetic.HybridParams())

@@ -117,7 +117,7 @@ def config3(iters, nx=256, ny=256):
     return out
 
 
-def config4(iters):
+def config4(iters):  # pieces; config4_hybrid runs the full step
     """Config 4 pieces on one GPU: the layer-0 Euler TVD-RK2 step on the
     200 x 200 quadrant field, and Q (N = 32, M = 4 x 8) for the ~19 % band
     cells (eps = 0.1 within 0.025 of x = 0.5, y = 0.5 and the periodic wrap
@@ -157,6 +157,59 @@ def config4(iters):
             "euler_cell_steps_per_s": nx * ny / (t_e * 1e-3), "band_cell_updates_per_s": len(band) / (t_q * 1e-3),
             "roofline": {"bound": "fp64", "collision_achieved_tflops": ach,
                          "collision_frac": ach / hk.default_context().fp64_peak_tflops()}}
+
+
+def config4_hybrid(steps=20, full_sample=True):
+    """Config 4 end to end: `steps` hybrid steps (hk_hybrid_step: Algorithm 1,
+    transitions, Euler TVD-RK2 on layer 0, PR(2,2,2) ES-BGK / penalized
+    Boltzmann on layers 1 / 2 with the cross-layer transport halo) of the
+    200 x 200 quadrant Riemann problem, N = 32, M = 4 x 8, CFL 0.5, band in
+    layer 2 at t = 0.  With `full_sample`, one all-Boltzmann step of the same
+    field (every cell layer 2, regimes frozen) gives the paper's
+    hybrid / full-kinetic ratio (SPEC.md estimate_full_kinetic_time)."""
+    nx = ny = 200
+    n, a1, a2 = 32, 4, 8
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    k = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    hydro, eps, r, _ = inputs.config4_hybrid_state(nx, ny, n, with_f=False)
+    hd = torch.from_numpy(hydro).cuda()
+    ed = torch.from_numpy(eps).cuda()
+    rd = torch.from_numpy(r).cuda()
+    f = kinetic.conserved_to_maxwellian(hd, vg)
+    dx = 1.0 / nx
+    dt = 0.5 * dx / (inputs.VMAX - inputs.VMAX / n)  # CFL 0.5 on the fastest node
+    p = kinetic.HybridParams()
+    kinetic.hybrid_step(k, nx, ny, dx, dx, dt, ed, rd.clone(), hd.clone(), f.clone(), p)  # warm-up (workspaces)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    hist = []
+    e0.record()
+    for _ in range(steps):
+        hist.append(kinetic.hybrid_step(k, nx, ny, dx, dx, dt, ed, rd, hd, f, p))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    q_evals = sum(2 * c.layer2 for c in hist)
+    out = {"config": "config4: 200x200 quadrant Riemann problem, hybrid steps (Algorithm 1), N=32, M=4x8, CFL 0.5",
+           "steps": steps, "ms_total": ms, "ms_per_step": ms / steps,
+           "cell_steps_per_s": nx * ny * steps / (ms * 1e-3),
+           "boltzmann_cell_updates_per_s": q_evals / (ms * 1e-3),
+           "layers_first_step": list(hist[0][:3]), "layers_last_step": list(hist[-1][:3]),
+           "transitions_0to1": sum(c.to_kinetic for c in hist), "transitions_1to0": sum(c.to_fluid for c in hist),
+           "mean_kinetic_fraction": sum((c.layer1 + c.layer2) / (nx * ny) for c in hist) / steps}
+    if full_sample:
+        r2 = torch.full_like(rd, 2)
+        pf = kinetic.HybridParams(update_regimes=False)
+        kinetic.hybrid_step(k, nx, ny, dx, dx, dt, ed, r2, hd.clone(), f, pf)  # workspaces for 40000 kinetic cells
+        torch.cuda.synchronize()
+        e0.record()
+        kinetic.hybrid_step(k, nx, ny, dx, dx, dt, ed, r2, hd, f, pf)
+        e1.record()
+        torch.cuda.synchronize()
+        full = e0.elapsed_time(e1)
+        out["all_boltzmann_ms_per_step"] = full
+        out["hybrid_speedup_vs_all_boltzmann"] = full / (ms / steps)
+    return out
 
 
 def config5(iters, steps=True):
@@ -213,6 +266,8 @@ if __name__ == "__main__":
             r = config1(args.iters)
         elif c == "4":
             r = config4(args.iters)
+        elif c == "4h":
+            r = config4_hybrid()
         elif c == "5":
             r = config5(args.iters, steps=not args.no_steps)
         else:
