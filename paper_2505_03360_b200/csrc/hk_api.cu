@@ -36,6 +36,7 @@ int ensure_scratch(hk_ctx ctx, size_t bytes) {
         ctx->scratch = nullptr;
         ctx->scratch_bytes = 0;
     }
+    bytes += bytes / 4;  // headroom: batches that grow step by step (hybrid layer 2) do not re-allocate each time
     int st = check_cuda(ctx, cudaMalloc(&ctx->scratch, bytes), "scratch alloc");
     if (!st) ctx->scratch_bytes = bytes;
     return st;

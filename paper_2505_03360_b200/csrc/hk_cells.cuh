@@ -34,6 +34,10 @@ struct TransportParams {
     // FIRST two columns are the ghosts: 2 for separate halo buffers, the neighbour's
     // nx when lh / rh point straight at the neighbour rank's slab (NVLink peer memory)
     int lnx = 2, rnx = 2;
+    // optional row activity of the output strips (lane-per-column kernel only),
+    // [strips][ny] from transport_row_activity: rows of a strip with no cell of
+    // interest are skipped (their outputs are left unwritten)
+    const uint8_t* row_act = nullptr;
 };
 
 // Final PR(2,2,2) combination fused into the second transport of a step
@@ -56,6 +60,10 @@ int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const d
 // PR(2,2,2) second transport + final combination (x periodic); false if the
 // marching kernel does not apply (caller runs transport + combine instead).
 bool transport_final_supported(const TransportParams& p);
+// Row activity of the transport strips for a [ny][nx] cell mask (nonzero = the
+// output is needed); act holds transport_row_activity_bytes(nx, ny) bytes.
+size_t transport_row_activity_bytes(int nx, int ny);
+int transport_row_activity(hk_ctx ctx, int nx, int ny, const int8_t* mask, uint8_t* act);
 int transport_final_launch(hk_ctx ctx, const TransportParams& p, const double* y2, const FinalCombine& fc);
 int combine_launch(hk_ctx ctx, int op, int64_t count, int64_t nb, double dt, const double* eps, double* o,
                    const double* f, const double* y, const double* q1, const double* k1, const double* tr,

@@ -22,7 +22,10 @@
 // batch order is deterministic); the host reads the list lengths once.
 // Compiled without FMA contraction: the conversions are bitwise the reference.
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "hk_cells.cuh"
@@ -251,6 +254,7 @@ int grow(hk_ctx ctx, void** p, size_t* have, size_t need, const char* what) {
         *p = nullptr;
         *have = 0;
     }
+    need += need / 4;  // headroom: the kinetic batch grows step by step
     if (cudaMalloc(p, need) != cudaSuccess) return fail(ctx, HK_CUDA, std::string("hybrid step: cannot allocate ") + what);
     *have = need;
     return HK_OK;
@@ -271,6 +275,32 @@ PR pr222_t() {  // ImexTableau::pr222 (inc/imex.hpp:23-34)
     const double delta = 1.0 - 1.0 / (2.0 * C);
     return {1.0, 1.0 - C, C - delta, delta};
 }
+
+// HK_HYB_PROF=1: per-phase wall time (stream synchronised at each mark), stderr.
+struct PhaseProf {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t;
+    std::string line;
+    explicit PhaseProf(cudaStream_t st) : on(getenv("HK_HYB_PROF") != nullptr), s(st) {
+        if (on) {
+            cudaStreamSynchronize(s);
+            t = std::chrono::steady_clock::now();
+        }
+    }
+    void mark(const char* name) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        char buf[64];
+        snprintf(buf, sizeof buf, " %s %.2f", name, std::chrono::duration<double, std::milli>(now - t).count());
+        line += buf;
+        t = now;
+    }
+    ~PhaseProf() {
+        if (on) fprintf(stderr, "[hk hybrid prof ms]%s\n", line.c_str());
+    }
+};
 
 int read_counts(hk_ctx ctx, const HybCounts* dev, HybCounts& h, const char* what) {
     int st = check_cuda(ctx, cudaMemcpyAsync(&h, dev, sizeof h, cudaMemcpyDeviceToHost, ctx->stream), what);
@@ -299,6 +329,7 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     const int64_t cells = (int64_t)nx * ny, nb = (int64_t)n * n * n;
     cudaStream_t s = ctx->stream;
     int st;
+    PhaseProf prof(s);
 
     // ---- per-cell workspace (fixed per grid) ----
     const size_t small_need = 256 * 16 + (sizeof(double) * cells * (5 + 1 + 4 + 8 + 5 + 5 + 1 + 1) +
@@ -348,12 +379,15 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     HybCounts h{};
     if ((st = read_counts(ctx, cnt, h, "hybrid_step indicator pass"))) return st;
     const int64_t n1 = h.n1, n2 = h.n2, nk = n1 + n2, nm = h.nm;
+    prof.mark("indicators");
     // Maxwellians of the 0 -> 1 cells and of the layer-0 transport halo
     if (nm && (st = maxwellian_launch(ctx, n, vmax, mmom, nm, f_dev, nullptr, mlist, nullptr))) return st;
+    prof.mark("halo");
 
     // ---- 3. layer 0: TVD-RK2 of the hydro view ----
     const bool euler = h.n0 > 0;
     if (euler && (st = hk_euler_tvd_rk2_step(ctx, W, nx, ny, dx, dy, dt, hr, p->eps_weno, ework))) return st;
+    prof.mark("euler");
 
     // ---- 4. kinetic layers: PR(2,2,2) on the compact batch ----
     if (nk) {
@@ -372,6 +406,9 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
         cudaMemsetAsync(stk, 0, sizeof(int) * nk, s);
         cudaMemsetAsync(stk2, 0, sizeof(int) * nk, s);
         TransportParams tp{n, vmax, nx, ny, 0, dx, dy, p->eps_weno};
+        uint8_t* act = reinterpret_cast<uint8_t*>(ework);  // the Euler work is free again
+        if ((st = transport_row_activity(ctx, nx, ny, r_new, act))) return st;
+        tp.row_act = act;  // T is only gathered at the kinetic cells
         auto stages = [&](const double* fin, double a, double* out, double* k1o) -> int {
             int e = HK_OK;
             if (n1)
@@ -403,16 +440,25 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
             return e;
         };
         st = hk_gather_cells(ctx, nb, f_dev, list, nk, fk);                               // f^n of the batch
+        prof.mark("gather");
         if (!st) st = stages(fk, t.a_im00 * dt, Y, k1);                                   // Y1, k1
+        prof.mark("stage1");
         if (!st) st = transport(Y);                                                       // T(Y1)
+        prof.mark("transport1");
         if (!st) st = residual(Y);                                                        // res(Y1)
+        prof.mark("residual1");
         if (!st) st = explicit_part(1, q1, nullptr, nullptr);                             // q1
         if (!st) st = combine_launch(ctx, 2, nk * nb, nb, dt, eps_k, fa, fk, nullptr, q1, k1, nullptr, nullptr);
+        prof.mark("combine");
         if (!st) st = stages(fa, t.a_im11 * dt, Y, nullptr);                              // Y2
+        prof.mark("stage2");
         if (!st) st = transport(Y);                                                       // T(Y2)
+        prof.mark("transport2");
         if (!st) st = residual(Y);                                                        // res(Y2)
+        prof.mark("residual2");
         if (!st) st = explicit_part(3, fk, nullptr, Y);                                   // final, in place
         if (!st) st = hk_scatter_cells(ctx, nb, fk, list, nk, f_dev);
+        prof.mark("final");
         if (!st) {
             status_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, stk, cnt);
             status_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, stk2, cnt);

@@ -183,6 +183,11 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
                                                               double* __restrict__ out, const double* __restrict__ lh,
                                                               const double* __restrict__ rh, FinalCombine fc) {
     static_assert(NPT == 2, "double2 node pairs");
+    extern __shared__ uint8_t act_s[];  // this strip's row activity (row_act mode)
+    if (p.row_act) {
+        for (int t = threadIdx.x; t < p.ny; t += blockDim.x) act_s[t] = p.row_act[(int64_t)blockIdx.x * p.ny + t];
+        __syncthreads();
+    }
     const int n = p.n;
     const int64_t nb = (int64_t)n * n * n;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -246,6 +251,12 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
         c = __ldg(reinterpret_cast<const double2*>(fc.k1 + o));
     };
     if (FINAL && outlane) fin_loads(0, nf0, nf1, nf2);
+    // row activity under the optional mask (warp-uniform): a row is computed
+    // when one of the strip's output cells is masked in; its y face also when
+    // the next row is (the face is shared)
+    const bool masked = p.row_act != nullptr;
+    auto row_active = [&](int jj) -> bool { return !masked || act_s[jj] != 0; };
+    bool act = row_active(0), act_next = ny > 1 ? row_active(1) : false;
     for (int j = 0; j < ny; ++j) {
         if (j > 0) {
             w0 = w1; w1 = w2; w2 = w3; w3 = w4;
@@ -256,10 +267,23 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
             nw4 = ld(j + 3);  // row j+3 = w4 of row j+1
             if (FINAL && outlane) fin_loads(j + 1, nf0, nf1, nf2);
         }
+        const bool act_nn = j + 2 < ny ? row_active(j + 2) : false;
+        if (!act && !act_next) {  // nothing here, and the next row does not need this row's face
+            act = act_next;
+            act_next = act_nn;
+            continue;
+        }
         const double c[2] = {w2.x, w2.y};
         double fy[2], fx[2];
         fy[0] = yface(w0.x, w1.x, w2.x, w3.x, w4.x);
         fy[1] = yface(w0.y, w1.y, w2.y, w3.y, w4.y);
+        if (!act) {  // face only (the minus face of the next, active row)
+            fyp[0] = fy[0];
+            fyp[1] = fy[1];
+            act = act_next;
+            act_next = act_nn;
+            continue;
+        }
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
             const double cp1 = sh_dn(c[q], 1);
@@ -298,11 +322,35 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
         }
         fyp[0] = fy[0];
         fyp[1] = fy[1];
+        act = act_next;
+        act_next = act_nn;
     }
     (void)k3;
 }
 
+// act[b][j] = any cell of interest in row j of output strip b (columns 28 b .. 28 b + 27).
+__global__ void row_activity_kernel(int nx, int ny, const int8_t* __restrict__ mask, uint8_t* __restrict__ act) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int strips = (nx + TL_OUT - 1) / TL_OUT;
+    if (k >= (int64_t)strips * ny) return;
+    const int b = int(k / ny), j = int(k % ny);
+    const int i1 = min(nx, (b + 1) * TL_OUT);
+    uint8_t any = 0;
+    for (int i = b * TL_OUT; i < i1; ++i) any |= mask[(int64_t)j * nx + i] != 0;
+    act[k] = any;
+}
+
 }  // namespace
+
+size_t transport_row_activity_bytes(int nx, int ny) { return size_t((nx + TL_OUT - 1) / TL_OUT) * size_t(ny); }
+
+int transport_row_activity(hk_ctx ctx, int nx, int ny, const int8_t* mask, uint8_t* act) {
+    const int64_t total = (int64_t)transport_row_activity_bytes(nx, ny);
+    if (total <= 0) return HK_OK;
+    row_activity_kernel<<<unsigned((total + 255) / 256), 256, 0, ctx->stream>>>(nx, ny, mask, act);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "row activity");
+}
 
 int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
                            const double* rh, const FinalCombine* fin) {
@@ -310,10 +358,12 @@ int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const d
     static const bool lanes = !getenv("HK_TRANSPORT_MARCH");
     if (lanes) {  // lane-per-column kernel (default)
         const dim3 grid(unsigned((p.nx + TL_OUT - 1) / TL_OUT), unsigned((nb / 2 + 3) / 4));
+        const size_t smem = p.row_act ? size_t(p.ny) : 0;
+        if (smem > 48 * 1024) return fail(ctx, HK_UNSUPPORTED, "transport: row activity needs ny <= 49152");
         if (fin)
-            transport_lanes_kernel<true, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+            transport_lanes_kernel<true, 2><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
         else
-            transport_lanes_kernel<false, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+            transport_lanes_kernel<false, 2><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
         ctx->launches++;
         return check_cuda(ctx, cudaGetLastError(), "transport kernel");
     }

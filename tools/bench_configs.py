@@ -260,6 +260,8 @@ if __name__ == "__main__":
     ap.add_argument("--configs", default="1,3")
     ap.add_argument("--nx", type=int, default=256)
     ap.add_argument("--no-steps", action="store_true")
+    ap.add_argument("--hyb-steps", type=int, default=20)
+    ap.add_argument("--no-full", action="store_true")
     args = ap.parse_args()
     for c in args.configs.split(","):
         if c == "1":
@@ -267,7 +269,7 @@ if __name__ == "__main__":
         elif c == "4":
             r = config4(args.iters)
         elif c == "4h":
-            r = config4_hybrid()
+            r = config4_hybrid(args.hyb_steps, full_sample=not args.no_full)
         elif c == "5":
             r = config5(args.iters, steps=not args.no_steps)
         else:
