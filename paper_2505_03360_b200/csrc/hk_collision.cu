@@ -26,6 +26,7 @@
 //        recomputed on the EXACT path.  Two directions per round.
 // Phase factors of src/fft.cpp:19-28 cancel between to_spectral and
 // to_nodal (|phase| = 1) and are not applied.
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1111,11 +1112,20 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
 // Tiled: a block bounds GC cells; the |alpha_a| tables are staged in shared
 // memory once per block (K-chunks of KC), so they are read once per GC cells.
 constexpr int GC = 16, KC = 64, KS = KC + 1;  // KS: padded row stride (bank-conflict free)
+__device__ void guard_verdict_impl(int n, double jac, double w, double tau, double bnd, int64_t cell,
+                                   hk_cell_status* __restrict__ st, int64_t* __restrict__ list, int* __restrict__ count);
+__device__ __forceinline__ void guard_verdict(int n, double jac, double w, double tau, double bnd, int64_t cell,
+                                              hk_cell_status* st, int64_t* list, int* count) {
+    guard_verdict_impl(n, jac, w, tau, bnd, cell, st, list, count);
+}
 __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0, double jac, double w, double tau,
                                                     const double2* __restrict__ nyq, const double* __restrict__ abs_a,
                                                     const double* __restrict__ abs_ap, int64_t ncells,
                                                     hk_cell_status* __restrict__ st, int64_t* __restrict__ list,
-                                                    int* __restrict__ count) {
+                                                    int* __restrict__ count, double* __restrict__ part) {
+    // part != null: split-K over gridDim.y (small batches: a block per cell
+    // tile per slice of the Nyquist set), partial sums accumulated into
+    // part[cell][e][4] and the bound formed by guard_finish_kernel.
     extern __shared__ double gsm[];
     double* sF = gsm;                 // [GC][KC]
     double* sA = sF + GC * KC;        // [md][KS]
@@ -1132,7 +1142,10 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
     for (int m = 0; m < 2; ++m)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[m][c][0] = acc[m][c][1] = acc[m][c][2] = acc[m][c][3] = 0.0;
-    for (int k0 = 0; k0 < nn3; k0 += KC) {
+    const int kchunks = (nn3 + KC - 1) / KC;
+    const int kper = (kchunks + gridDim.y - 1) / gridDim.y;
+    const int kbeg = blockIdx.y * kper * KC, kend = min(nn3, (int)(blockIdx.y + 1) * kper * KC);
+    for (int k0 = kbeg; k0 < kend; k0 += KC) {
         __syncthreads();
         for (int i = threadIdx.x; i < GC * KC; i += blockDim.x) {
             const int c = i / KC, k = i % KC;
@@ -1172,6 +1185,22 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
             }
         }
     }
+    if (part) {
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            const int e = el + 64 * m;
+            if (e >= md) continue;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int64_t cell = c0 + 4 * cg + c;
+                if (cell >= ncells) continue;
+                double* pc = part + (cell * md + e) * 4;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) atomicAdd(pc + q, acc[m][c][q]);
+            }
+        }
+        return;
+    }
     __syncthreads();
     if (threadIdx.x < GC) bound[threadIdx.x] = 0.0;
     __syncthreads();
@@ -1186,11 +1215,34 @@ __global__ void __launch_bounds__(256) guard_kernel(int n, int md, double mult0,
         }
     }
     __syncthreads();
-    if (threadIdx.x < GC && c0 + threadIdx.x < ncells) {
-        const int64_t cell = c0 + threadIdx.x;
+    if (threadIdx.x < GC && c0 + threadIdx.x < ncells)
+        guard_verdict(n, jac, w, tau, bound[threadIdx.x], c0 + threadIdx.x, st, list, count);
+}
+
+// Split-K guard: the bound from the summed partials, one warp per cell.
+__global__ void guard_finish_kernel(int n, int md, double mult0, double jac, double w, double tau,
+                                    const double* __restrict__ part, int64_t ncells, hk_cell_status* __restrict__ st,
+                                    int64_t* __restrict__ list, int* __restrict__ count) {
+    const int64_t cell = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (cell >= ncells) return;
+    double b = 0.0;
+    for (int e = lane; e < md; e += 32) {
+        const double* pc = part + (cell * md + e) * 4;
+        b += (e == 0 ? mult0 : 1.0) * fmin(pc[0] * sqrt(pc[3]), sqrt(pc[2]) * pc[1]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(0xffffffffu, b, o);
+    if (lane == 0) guard_verdict(n, jac, w, tau, b, cell, st, list, count);
+}
+
+__device__ void guard_verdict_impl(int n, double jac, double w, double tau, double bnd, int64_t cell,
+                                   hk_cell_status* __restrict__ st, int64_t* __restrict__ list,
+                                   int* __restrict__ count) {
+    {
         hk_cell_status* sc = st + cell;
         const double qn = sqrt(sc->q_norm2);
-        const double abs_bound = jac * w * bound[threadIdx.x] * pow(double(n), 1.5);
+        const double abs_bound = jac * w * bnd * pow(double(n), 1.5);
         const double rel = qn > 0.0 ? abs_bound / qn : (abs_bound > 0.0 ? INFINITY : 0.0);
         sc->nyq_bound = rel;
         // reroute unless the bound is within tau of ||Q|| or below the exact
@@ -1350,7 +1402,14 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     const size_t st_bytes = st ? 0 : sizeof(hk_cell_status) * ncells;
     const size_t nyq_bytes = guard ? sizeof(double2) * nn3 * ncells : 0;
     const size_t list_bytes = guard ? sizeof(int64_t) * ncells : 0;
-    const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255) & ~size_t(255);
+    // split-K guard for batches too small to fill the SMs with cell tiles
+    const int64_t gtiles = (ncells + GC - 1) / GC;
+    const int kchunks = int((nn3 + KC - 1) / KC);
+    const int ksplit = (guard && gtiles < 2 * ctx->sm_count)
+                           ? int(std::min<int64_t>(kchunks, (2 * ctx->sm_count + gtiles - 1) / gtiles))
+                           : 1;
+    const size_t part_bytes = ksplit > 1 ? ((sizeof(double) * 4 * k->md * ncells + 255) & ~size_t(255)) : 0;
+    const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255 + part_bytes) & ~size_t(255);
     size_t xchg_bytes;
     if constexpr (N == 64)
         xchg_bytes = coll64_xchg_bytes(ctx) + 65536;
@@ -1363,6 +1422,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     double2* nyq = guard ? reinterpret_cast<double2*>(base + st_bytes) : nullptr;
     int64_t* list = guard ? reinterpret_cast<int64_t*>(base + st_bytes + nyq_bytes) : nullptr;
     int* count = reinterpret_cast<int*>(base + st_bytes + nyq_bytes + list_bytes);
+    double* part = ksplit > 1 ? reinterpret_cast<double*>(base + xchg_off - part_bytes) : nullptr;
     cudaMemsetAsync(st, 0, sizeof(hk_cell_status) * ncells, ctx->stream);
 
     CollArgs a{};
@@ -1416,8 +1476,15 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
                 const size_t gsmem = sizeof(double) * (GC * KC + 2 * k->md * KS + GC);
                 if (k->md > 128) return fail(ctx, HK_UNSUPPORTED, "guard: at most 128 distinct directions");
                 cudaFuncSetAttribute(guard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
-                guard_kernel<<<unsigned((ncells + GC - 1) / GC), 256, gsmem, ctx->stream>>>(
-                    N, k->md, k->mult0, k->jac, k->weight, kGuardTau, nyq, k->abs_a, k->abs_ap, ncells, st, list, count);
+                if (ksplit > 1) cudaMemsetAsync(part, 0, part_bytes, ctx->stream);
+                guard_kernel<<<dim3(unsigned(gtiles), unsigned(ksplit)), 256, gsmem, ctx->stream>>>(
+                    N, k->md, k->mult0, k->jac, k->weight, kGuardTau, nyq, k->abs_a, k->abs_ap, ncells, st, list, count,
+                    part);
+                if (ksplit > 1) {
+                    guard_finish_kernel<<<unsigned((ncells * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+                        N, k->md, k->mult0, k->jac, k->weight, kGuardTau, part, ncells, st, list, count);
+                    ctx->launches++;
+                }
             }
             timing_end(ctx);
             ctx->launches++;
