@@ -73,22 +73,25 @@ class XSlab:
             out[:, i0:i0 + nxl] = t.view(self.ny, nxl, nb)
         return out.view(self.ny * self.nx, nb).to(local.device)
 
-    def halo_buffers(self, nb: int, like: torch.Tensor):
-        shape = (self.ny, HALO, nb)
+    def halo_buffers(self, nb: int, like: torch.Tensor, width: int = HALO):
+        shape = (self.ny, width, nb)
         return torch.empty(shape, dtype=like.dtype, device=like.device), torch.empty(shape, dtype=like.dtype,
                                                                                    device=like.device)
 
-    def exchange(self, local: torch.Tensor, left: torch.Tensor, right: torch.Tensor, group=None, async_op=False):
+    def exchange(self, local: torch.Tensor, left: torch.Tensor, right: torch.Tensor, group=None, async_op=False,
+                 width: int = HALO):
         """Fills left/right halos from the neighbours' edge columns.
 
         Ops are issued in the order [send right edge -> right, recv left halo <- left,
         send left edge -> left, recv right halo <- right], so that with world = 2
         (left == right) the two messages between the pair match in order.
         Returns a list of works (async_op) or None after completion."""
+        if width > self.nxl:
+            raise ValueError(f"halo width {width} exceeds the slab width {self.nxl}")
         nb = local.shape[-1]
         f = local.view(self.ny, self.nxl, nb)
-        send_r = f[:, self.nxl - HALO:].contiguous()  # my last interior columns -> right's left halo
-        send_l = f[:, :HALO].contiguous()             # my first interior columns -> left's right halo
+        send_r = f[:, self.nxl - width:].contiguous()  # my last interior columns -> right's left halo
+        send_l = f[:, :width].contiguous()             # my first interior columns -> left's right halo
         if self.world == 1:
             left.copy_(send_r)
             right.copy_(send_l)
@@ -195,6 +198,59 @@ def penalized_imex_step_slab(part: XSlab, f: torch.Tensor, kernel, dx: float, dy
     transport(y, tr)
     comb(3, f, yv=y, qv=q1, kv=k1, tv=tr, rv=res)
     return f
+
+
+# Ghost width of the slab hybrid step: the exact dependency radius of one
+# hybrid step along x is 7 cells (regime update 1, halo Maxwellians +2, two
+# transport sweeps +2 each; the layer-0 TVD-RK2 needs 4), so a slab padded with
+# 8 exchanged columns per side and stepped as a local periodic torus gets
+# every interior cell exactly as the global torus would.
+HYB_GHOST = 8
+
+
+def hybrid_pad(part: XSlab, width: int, fields, halos):
+    """[ny][nxl + 2 width] padded copies of the local fields (each [cells, k]),
+    halos = [(left [ny][width][k], right [ny][width][k]), ...]."""
+    out = []
+    for t, (lh, rh) in zip(fields, halos):
+        k = t.shape[-1]
+        pad = torch.empty((part.ny, part.nxl + 2 * width, k), dtype=t.dtype, device=t.device)
+        pad[:, :width] = lh
+        pad[:, width:width + part.nxl] = t.view(part.ny, part.nxl, k)
+        pad[:, width + part.nxl:] = rh
+        out.append(pad.view(part.ny * (part.nxl + 2 * width), k))
+    return out
+
+
+def hybrid_unpad(part: XSlab, width: int, padded, fields):
+    for pad, t in zip(padded, fields):
+        k = t.shape[-1]
+        t.view(part.ny, part.nxl, k).copy_(pad.view(part.ny, part.nxl + 2 * width, k)[:, width:width + part.nxl])
+
+
+def hybrid_step_slab(part: XSlab, kernel, dx: float, dy: float, dt: float, eps_cell: torch.Tensor, r: torch.Tensor,
+                     hydro: torch.Tensor, f: torch.Tensor, params=None, group=None, width: int = HYB_GHOST,
+                     halos=None):
+    """hk_hybrid_step on one x-slab, in place (r [cells] int8, hydro [cells,4], f [cells,n^3],
+    eps [cells]; local cell order j*nxl + i).  One exchange of `width` columns of
+    (r, eps, hydro, f) per side, then the step on the padded local torus; the
+    interior is exactly the global step's.  Returns the global layer counts
+    [n0, n1, n2] (all-reduced).  `halos` (tests) supplies the exchanged columns
+    directly: [(left, right)] for r, eps, hydro, f as [ny][width][k]."""
+    from .kinetic import HybridParams, hybrid_step
+
+    params = params or HybridParams()
+    fields = [r.view(-1, 1), eps_cell.to(device=f.device, dtype=torch.float64).view(-1, 1), hydro, f]
+    if halos is None:
+        halos = []
+        for t in fields:
+            lh, rh = part.halo_buffers(t.shape[-1], t, width)
+            part.exchange(t, lh, rh, group, width=width)
+            halos.append((lh, rh))
+    pr, pe, ph, pf = hybrid_pad(part, width, fields, halos)
+    hybrid_step(kernel, part.nxl + 2 * width, part.ny, dx, dy, dt, pe.view(-1), pr.view(-1), ph, pf, params)
+    hybrid_unpad(part, width, [pr, ph, pf], [fields[0], hydro, f])
+    return regime_counts(r, group)
 
 
 class PeerHalo:

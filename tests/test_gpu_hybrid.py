@@ -93,3 +93,63 @@ def test_hybrid_all_fluid_and_positivity(hk):
     hd = torch.from_numpy(bad).cuda()
     with pytest.raises(hk.positivity_error):
         kinetic.hybrid_step(kern, nx, ny, 1 / nx, 1 / ny, 1e-3, ed, rd, hd, fd, kinetic.HybridParams())
+
+
+def _hybrid_setup(hk, nx, ny, n):
+    import torch
+    hydro, eps, r, f = inputs.config4_hybrid_state(nx, ny, n, half_width=1.0 / nx)
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, n, 4, 4, inputs.R_PHYS_MAX)
+    dx, dy = 1.0 / nx, 1.0 / ny
+    dt = 0.5 * dx / (inputs.VMAX - inputs.VMAX / n)
+    dev = [torch.from_numpy(x.copy()).cuda() for x in (r, hydro, f, eps)]
+    return kern, dx, dy, dt, dev
+
+
+def test_hybrid_slab_world1_equals_torus(hk):
+    """x-slab hybrid step (8 ghost columns, local periodic torus) at world 1 == the torus step."""
+    from paper_2505_03360_b200 import kinetic
+    from paper_2505_03360_b200.partition import XSlab, hybrid_step_slab
+    nx, ny, n = 20, 8, 16
+    kern, dx, dy, dt, (r, h, f, e) = _hybrid_setup(hk, nx, ny, n)
+    r2, h2, f2 = r.clone(), h.clone(), f.clone()
+    part = XSlab(nx, ny, 1, 0)
+    for _ in range(2):
+        kinetic.hybrid_step(kern, nx, ny, dx, dy, dt, e, r, h, f)
+        counts = hybrid_step_slab(part, kern, dx, dy, dt, e, r2, h2, f2)
+        assert list(counts.long().tolist()) == [int((r == k).sum()) for k in range(3)]
+        assert bool((r == r2).all())
+        kin = r != 0
+        assert float((h2 - h)[~kin].abs().max()) <= 1e-13 * float(h.abs().max())
+        assert float((f2 - f)[kin].abs().max()) <= 1e-13 * float(f.abs().max())
+
+
+def test_hybrid_two_slabs_equal_torus(hk):
+    """Two x-slabs stepped in one process with exchanged 8-column halos reproduce the torus step."""
+    import torch
+    from paper_2505_03360_b200 import kinetic
+    from paper_2505_03360_b200.partition import HYB_GHOST as W, XSlab, hybrid_step_slab
+    nx, ny, n = 22, 6, 16
+    kern, dx, dy, dt, (r, h, f, e) = _hybrid_setup(hk, nx, ny, n)
+    parts = [XSlab(nx, ny, 2, k) for k in range(2)]
+    loc = [[p.scatter(t.view(nx * ny, -1)) for t in (r, e, h, f)] for p in parts]
+    for _ in range(2):
+        halos = []
+        for k, p in enumerate(parts):
+            o = loc[1 - k]
+            hk_ = []
+            for fi in range(4):
+                nb = o[fi].shape[-1]
+                src = o[fi].view(ny, parts[1 - k].nxl, nb)
+                hk_.append((src[:, -W:].contiguous(), src[:, :W].contiguous()))
+            halos.append(hk_)
+        for k, p in enumerate(parts):
+            rl, el, hl, fl = loc[k]
+            hybrid_step_slab(p, kern, dx, dy, dt, el.view(-1), rl.view(-1), hl, fl, halos=halos[k])
+        kinetic.hybrid_step(kern, nx, ny, dx, dy, dt, e, r, h, f)
+    glob = [torch.cat([loc[k][fi].view(ny, parts[k].nxl, -1) for k in range(2)], 1).reshape(nx * ny, -1)
+            for fi in range(4)]
+    assert bool((glob[0].view(-1) == r).all())
+    kin = r != 0
+    assert float((glob[2] - h)[~kin].abs().max()) <= 1e-13 * float(h.abs().max())
+    assert float((glob[3] - f)[kin].abs().max()) <= 1e-13 * float(f.abs().max())

@@ -68,6 +68,52 @@ def test_halo_exchange_gloo(world, nx):
     assert sum(n for _, n in cols) == nx and all(cols[k][0] + cols[k][1] == cols[k + 1][0] for k in range(world - 1))
 
 
+def _wide_worker(rank, world, port, nx, ny, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_03360_b200.partition import XSlab, HYB_GHOST, hybrid_pad, hybrid_unpad
+        W = HYB_GHOST
+        g = torch.Generator().manual_seed(99)
+        glob_f = torch.randn((ny * nx, 6), generator=g, dtype=torch.float64)
+        glob_r = torch.randint(0, 3, (ny * nx, 1), generator=g).to(torch.int8)
+        part = XSlab(nx, ny, world, rank)
+        fields = [part.scatter(glob_r), part.scatter(glob_f)]
+        halos = []
+        for t in fields:
+            lh, rh = part.halo_buffers(t.shape[-1], t, W)
+            part.exchange(t, lh, rh, width=W)
+            halos.append((lh, rh))
+        pr, pf = hybrid_pad(part, W, fields, halos)
+        cols = [(part.i0 - W + k) % nx for k in range(part.nxl + 2 * W)]
+        ok = torch.equal(pr.view(ny, -1, 1), glob_r.view(ny, nx, 1)[:, cols])
+        ok = ok and torch.equal(pf.view(ny, -1, 6), glob_f.view(ny, nx, 6)[:, cols])
+        pf.mul_(2.0)
+        out = torch.zeros_like(fields[1])
+        hybrid_unpad(part, W, [pf], [out])
+        ok = ok and torch.equal(out, 2.0 * fields[1])
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,nx", [(2, 20), (3, 27)])
+def test_hybrid_slab_padding_gloo(world, nx):
+    """The slab hybrid step's padded local torus (8 exchanged columns per side,
+    int8 layers and fp64 fields) is the global periodic window of the slab."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_wide_worker, args=(r, world, port, nx, 3, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
 def test_slab_bounds():
     from paper_2505_03360_b200.partition import XSlab
     with pytest.raises(ValueError):
