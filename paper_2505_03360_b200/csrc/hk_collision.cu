@@ -1392,10 +1392,220 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     return st;
 }
 
+// ---------------------------------------------------------------------------
+// N = 16, EXACT (reference arithmetic), one cell per 2-CTA cluster with the
+// whole 16^3 spectrum in each CTA's shared memory: no transpose exchange at
+// all.  CTA r evaluates the directions e = r, r + 2, ... (CTA 1 also the loss
+// field): per direction the 512 threads transform both fields (alpha F and
+// alpha' F, one thread per pencil per field) along k3 (with the weights), k2
+// and k1 in place, then accumulate the complex gain of 8 nodes per thread in
+// registers.  The partial gains and the loss field meet in the cluster's L2
+// scratch; each CTA writes Q for half the nodes.  (The spectrum of a 16^3
+// cell reaches its Nyquist planes, so the fast path's guard reroutes every
+// such cell: the exact kernel is the production path at N = 16.)
+// ---------------------------------------------------------------------------
+struct Geo16 {
+    static constexpr int N = 16, R = 17, PL = N * R, BUF = N * PL;  // padded [k1][k2][k3]
+    static constexpr int NT = 512;
+    static constexpr size_t SMEM = size_t(3 * BUF) * sizeof(double2) + 64 * sizeof(double);
+};
+
+__device__ __forceinline__ int i16(int k1, int k2, int k3) { return k1 * Geo16::PL + k2 * Geo16::R + k3; }
+
+__global__ void __launch_bounds__(512, 1) coll16_exact_kernel(CollArgs a) {
+    using G = Geo16;
+    constexpr int N = 16, NB = 4096;
+    extern __shared__ __align__(16) double2 smem[];
+    double2* Fs = smem;
+    double2* const B0 = smem + G::BUF;      // alpha F  -> ga (and the loss field)
+    double2* const B1 = smem + 2 * G::BUF;  // alpha' F -> gb
+    double* red = reinterpret_cast<double*>(smem + 3 * G::BUF);
+    const unsigned r = cluster_rank(), cid = cluster_id_x(), ncl = n_clusters_x();
+    const int t = threadIdx.x, phi = t >> 8, p = t & 255, ph = p >> 4, pl = p & 15;
+    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
+    double2* X = a.xchg + (int64_t)cid * 3 * NB;  // [gain of CTA 0][gain of CTA 1][loss field], natural order
+    for (int64_t it = cid; it < count; it += ncl) {
+        const int64_t cell = a.list ? a.list[it] : it;
+        const double* fc = a.f + cell * NB;
+        // ---- F = FFT(f) / N^3 (both CTAs), k3 then k2 then k1 ----
+        for (int k = t; k < NB; k += G::NT) Fs[i16(k >> 8, (k >> 4) & 15, k & 15)] = make_double2(__ldg(fc + k), 0.0);
+        __syncthreads();
+        for (int pass = 0; pass < 3; ++pass) {
+            if (t < 256) {
+                double2* base = pass == 0 ? Fs + i16(ph, pl, 0) : (pass == 1 ? Fs + i16(ph, 0, pl) : Fs + i16(0, ph, pl));
+                const int st = pass == 0 ? 1 : (pass == 1 ? G::R : G::PL);
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = base[i * st];
+                fft_reg<N, false>(x);
+                const double sc = pass == 2 ? 1.0 / double(NB) : 1.0;
+#pragma unroll
+                for (int i = 0; i < N; ++i) base[i * st] = make_double2(x[i].x * sc, x[i].y * sc);
+            }
+            __syncthreads();
+        }
+        double2 g[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) g[i] = make_double2(0.0, 0.0);
+        const int n_dir = (a.md - (int)r + 1) / 2;  // directions r, r + 2, ...
+        const int n_ent = n_dir + (r == 1 ? 1 : 0);  // CTA 1 also transforms the loss field
+        for (int q = 0; q < n_ent; ++q) {
+            const bool loss = q == n_dir;
+            const int e = (int)r + 2 * q;
+            const bool act = !loss || phi == 0;
+            double2* B = phi ? B1 : B0;
+            if (act) {  // k3 pass with the weights: pencil (k1, k2) = (ph, pl)
+                const double* wt = loss ? a.loss : (phi ? a.alpha_p : a.alpha) + (int64_t)e * NB;
+                wt += ph * 256 + pl;  // [i1][i3][i2]
+                const double2* fr = Fs + i16(ph, pl, 0);
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                    const double w = __ldg(wt + i * N);
+                    const double2 F = fr[i];
+                    x[i] = make_double2(F.x * w, F.y * w);
+                }
+                fft_reg<N, true>(x);
+                double2* o = B + i16(ph, pl, 0);
+#pragma unroll
+                for (int i = 0; i < N; ++i) o[i] = x[i];
+            }
+            __syncthreads();
+            if (act) {  // k2 pass: pencil (k1, k3) = (ph, pl)
+                double2* o = B + i16(ph, 0, pl);
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = o[i * G::R];
+                fft_reg<N, true>(x);
+#pragma unroll
+                for (int i = 0; i < N; ++i) o[i * G::R] = x[i];
+            }
+            __syncthreads();
+            if (act) {  // k1 pass: pencil (k2, k3) = (ph, pl)
+                double2* o = B + i16(0, ph, pl);
+                double2 x[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = o[i * G::PL];
+                fft_reg<N, true>(x);
+#pragma unroll
+                for (int i = 0; i < N; ++i) o[i * G::PL] = x[i];
+            }
+            __syncthreads();
+            if (!loss) {  // gain += m ga gb on nodes (k1 = 8 phi + i, k2 = ph, k3 = pl)
+                const double m = e == 0 ? a.mult0 : 1.0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int ix = i16(8 * phi + i, ph, pl);
+                    const double2 ga = B0[ix], gb = B1[ix];
+                    g[i].x += m * (ga.x * gb.x - ga.y * gb.y);
+                    g[i].y += m * (ga.x * gb.y + ga.y * gb.x);
+                }
+                __syncthreads();  // buffers free for the next direction
+            }
+        }
+        // ---- partial gains (and the loss field) meet in the cluster's scratch ----
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st_cg16(X + (int64_t)r * NB + (8 * phi + i) * 256 + p, g[i]);
+        if (r == 1)
+            for (int k = t; k < NB; k += G::NT) st_cg16(X + 2 * NB + k, B0[i16(k >> 8, (k >> 4) & 15, k & 15)]);
+        cluster_arrive();
+        cluster_wait();
+        // ---- Q = jac (w gain - f loss) on k1 in [8 r, 8 r + 8) ----
+        double mre = 0.0, mim = 0.0, n2 = 0.0;
+        double* qc = a.q + cell * NB;
+        for (int k = (int)r * 2048 + t; k < ((int)r + 1) * 2048; k += G::NT) {
+            const double2 g0 = ld_cg16(X + k), g1 = ld_cg16(X + NB + k), L = ld_cg16(X + 2 * NB + k);
+            const double fv = __ldg(fc + k);
+            const double qre = a.jac * (a.w * (g0.x + g1.x) - fv * L.x);
+            const double qim = a.jac * (a.w * (g0.y + g1.y) - fv * L.y);
+            qc[k] = qre;
+            mre = fmax(mre, fabs(qre));
+            mim = fmax(mim, fabs(qim));
+            n2 += qre * qre;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
+            mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
+            n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+        }
+        const int warp = t >> 5, lane = t & 31;
+        if (lane == 0) {
+            red[warp] = mre;
+            red[16 + warp] = mim;
+            red[32 + warp] = n2;
+        }
+        __syncthreads();
+        if (t == 0 && a.st) {
+            double m1 = 0, m2 = 0, sum = 0;
+            for (int w = 0; w < 16; ++w) {
+                m1 = fmax(m1, red[w]);
+                m2 = fmax(m2, red[16 + w]);
+                sum += red[32 + w];
+            }
+            hk_cell_status* sc = a.st + cell;
+            atomic_max_nonneg(&sc->max_re, m1);
+            atomic_max_nonneg(&sc->max_im, m2);
+            atomicAdd(&sc->q_norm2, sum);
+            if (r == 0) atomicOr(&sc->flags, HK_CELL_EXACT);
+        }
+        cluster_arrive();  // the scratch and SMEM are free for the next cell
+        cluster_wait();
+    }
+}
+
+int launch_coll16(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) {
+    auto kern = coll16_exact_kernel;
+    const int key = 16 * 100 + 99;
+    int st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    if (!ctx->max_clusters.count(key)) {
+        if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)Geo16::SMEM), "smem attribute")))
+            return st;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * 256);
+        cfg.blockDim = dim3(Geo16::NT);
+        cfg.dynamicSmemBytes = Geo16::SMEM;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg), "max active clusters")))
+            return st;
+        if (ncl < 1) return fail(ctx, HK_CUDA, "N = 16 collision kernel cannot be resident");
+        ctx->max_clusters[key] = ncl;
+    }
+    int64_t ncl = ctx->max_clusters[key];
+    if (max_cells < ncl) ncl = max_cells;
+    if (ncl < 1) return HK_OK;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(2 * ncl));
+    cfg.blockDim = dim3(Geo16::NT);
+    cfg.dynamicSmemBytes = Geo16::SMEM;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    timing_begin(ctx, tag);
+    st = check_cuda(ctx, cudaLaunchKernelEx(&cfg, kern, args), "collision kernel launch");
+    timing_end(ctx);
+    ctx->launches++;
+    return st;
+}
+
 template <int N, int C>
 int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells, uint32_t flags,
              hk_cell_status* st) {
-    const bool exact = (flags & (HK_COLL_EXACT | HK_COLL_STRICT)) != 0;
+    // N = 16: every cell's spectrum reaches the Nyquist planes, so the guard
+    // would list them all; the exact kernel is the default there (the fast
+    // kernel stays reachable with HK_COLL_NOGUARD, the guarded fast path with
+    // HK_N16_GUARDED=1 for comparison).
+    static const bool n16_guarded = getenv("HK_N16_GUARDED") != nullptr;
+    const bool exact = (flags & (HK_COLL_EXACT | HK_COLL_STRICT)) != 0 ||
+                       (N == 16 && !(flags & HK_COLL_NOGUARD) && !n16_guarded);
     const bool guard = !exact && !(flags & HK_COLL_NOGUARD);
     const int64_t nn3 = 3LL * N * N;
     // scratch: [nyq |F| planes][reroute list][count]
@@ -1446,6 +1656,9 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     auto launch_exact = [&](const CollArgs& x, int tag) -> int {
         if constexpr (N == 64)
             return launch_coll64(ctx, x, true, ncells, tag);
+        else if constexpr (N == 16)
+            return getenv("HK_N16_CLUSTER8") ? launch_variant<N, C, true>(ctx, x, ncells, tag)
+                                             : launch_coll16(ctx, x, ncells, tag);
         else
             return launch_variant<N, C, true>(ctx, x, ncells, tag);
     };

@@ -257,6 +257,12 @@ __device__ __forceinline__ void cp_async8(uint32_t smem_dst, const void* gsrc) {
 __device__ __forceinline__ void st_cg16(double2* p, double2 v) {
     asm volatile("st.global.cg.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
+// L2-only 16-byte load (the producer is another SM of the cluster).
+__device__ __forceinline__ double2 ld_cg16(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p) : "memory");
+    return v;
+}
 
 // Named barrier over `count` threads (role groups of a warp-specialised CTA).
 __device__ __forceinline__ void named_bar(unsigned id, unsigned count) {

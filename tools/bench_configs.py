@@ -60,10 +60,10 @@ def config1(iters):
     peak = ctx.fp64_peak_tflops()
     ach = W * cells / (ms * 1e-3) / 1e12
     return {"config": "config1: 64 cells, 16^3, M=4x8, hard spheres, Q + forward Euler dt=0.01",
-            "path": "fast kernel + Nyquist guard (split-K for the small batch) + exact Nyquist correction of the listed cells (every 16^3 cell)",
+            "path": "exact kernel (16^3 spectrum in shared memory, one 2-CTA cluster per cell, directions split over the pair)",
             "ms_per_step": ms, "cell_updates_per_s": cells / (ms * 1e-3),
             "roofline": {"bound": "fp64", "achieved_tflops": ach, "peak_tflops": peak, "frac": ach / peak,
-                         "note": "64 cells on 148 SMs: fill-limited (32 clusters of 2 CTAs)"}}
+                         "note": "64 cells on 148 SMs: fill-limited (64 clusters of 2 CTAs, one cell each)"}}
 
 
 def config3(iters, nx=256, ny=256):
