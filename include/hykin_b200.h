@@ -73,6 +73,10 @@ int hk_ctx_create(int device, hk_ctx* out);
 int hk_ctx_destroy(hk_ctx ctx);
 /* stream: a cudaStream_t (NULL = legacy default stream). */
 int hk_ctx_set_stream(hk_ctx ctx, void* stream);
+/* Releases the context's cached device workspaces (collision scratch, IMEX /
+ * hybrid step work fields); they are re-allocated on the next call that needs
+ * them.  Synchronises the context's stream. */
+int hk_ctx_trim(hk_ctx ctx);
 /* Last error message and failing cell index (-1 if none). */
 int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len);
 /* Number of this library's kernel launches since context creation. */
@@ -111,6 +115,8 @@ int hk_kernel_info(hk_kernel k, double* out6);
  * direction) with a rigorous per-cell Nyquist guard: any cell whose dropped
  * term could exceed 5e-11 of max(||Q||_2, 2e-5 ||jac f L||_2) gets that term
  * computed exactly and added (Re Q then equals the exact path's).
+ * At n = 16 the default is the exact path (a 16^3 spectrum always reaches the
+ * Nyquist planes, the guard would list every cell).
  * HK_COLL_EXACT: the reference's arithmetic (two complex transforms per
  * direction) for every cell; HK_COLL_NOGUARD: fast path only.
  * HK_COLL_STRICT returns HK_NUMERICAL_CONSISTENCY (hk_last_error gives the

@@ -115,6 +115,10 @@ class Context:
             raise exc(msg, cell.value)
         raise exc(msg)
 
+    def trim(self):
+        """Frees the context's cached device workspaces (hk_ctx_trim)."""
+        self.check(self._lib.hk_ctx_trim(self.h))
+
     @property
     def launches(self) -> int:
         return int(self._lib.hk_launch_count(self.h))

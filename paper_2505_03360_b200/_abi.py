@@ -99,6 +99,7 @@ def lib() -> C.CDLL:
         "hk_ctx_create": (C.c_int, [C.c_int, C.POINTER(vp)]),
         "hk_ctx_destroy": (C.c_int, [vp]),
         "hk_ctx_set_stream": (C.c_int, [vp, vp]),
+        "hk_ctx_trim": (C.c_int, [vp]),
         "hk_last_error": (C.c_int, [vp, C.POINTER(i64), C.c_char_p, C.c_size_t]),
         "hk_launch_count": (i64, [vp]),
         "hk_ctx_set_timing": (C.c_int, [vp, C.c_int]),

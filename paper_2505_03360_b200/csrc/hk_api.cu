@@ -98,6 +98,23 @@ int hk_ctx_destroy(hk_ctx ctx) {
     return HK_OK;
 }
 
+int hk_ctx_trim(hk_ctx ctx) {
+    if (!ctx) return HK_CONTRACT;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    else cudaDeviceSynchronize();
+    void** bufs[] = {&ctx->scratch, &ctx->fix_scratch, &ctx->step_work, &ctx->hyb_small, &ctx->hyb_big};
+    size_t* sizes[] = {&ctx->scratch_bytes, &ctx->fix_bytes, &ctx->step_bytes, &ctx->hyb_small_bytes, &ctx->hyb_big_bytes};
+    for (int i = 0; i < 5; ++i) {
+        if (*bufs[i]) cudaFree(*bufs[i]);
+        *bufs[i] = nullptr;
+        *sizes[i] = 0;
+    }
+    ctx->last_list = nullptr;
+    ctx->last_count = nullptr;
+    return check_cuda(ctx, cudaGetLastError(), "trim");
+}
+
 int hk_ctx_set_stream(hk_ctx ctx, void* stream) {
     ctx->stream = static_cast<cudaStream_t>(stream);
     return HK_OK;

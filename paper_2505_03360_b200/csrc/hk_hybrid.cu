@@ -246,7 +246,7 @@ __global__ void status_kernel(int64_t nk, const int64_t* __restrict__ list, cons
 unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
 
 // Grow-only device buffer owned by the context.
-int grow(hk_ctx ctx, void** p, size_t* have, size_t need, const char* what) {
+int grow(hk_ctx ctx, void** p, size_t* have, size_t need, const char* what, size_t cap) {
     if (need <= *have) return HK_OK;
     if (*p) {
         cudaStreamSynchronize(ctx->stream);
@@ -254,7 +254,7 @@ int grow(hk_ctx ctx, void** p, size_t* have, size_t need, const char* what) {
         *p = nullptr;
         *have = 0;
     }
-    need += need / 4;  // headroom: the kinetic batch grows step by step
+    need = std::max(need, std::min(cap, need + need / 4));  // headroom: the kinetic batch grows step by step
     if (cudaMalloc(p, need) != cudaSuccess) return fail(ctx, HK_CUDA, std::string("hybrid step: cannot allocate ") + what);
     *have = need;
     return HK_OK;
@@ -334,7 +334,8 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     // ---- per-cell workspace (fixed per grid) ----
     const size_t small_need = 256 * 16 + (sizeof(double) * cells * (5 + 1 + 4 + 8 + 5 + 5 + 1 + 1) +
                                           sizeof(int64_t) * cells * 4 + sizeof(int) * cells * 3 + cells * 2 + 4096);
-    if ((st = grow(ctx, &ctx->hyb_small, &ctx->hyb_small_bytes, small_need, "per-cell workspace"))) return st;
+    if ((st = grow(ctx, &ctx->hyb_small, &ctx->hyb_small_bytes, small_need, "per-cell workspace", small_need)))
+        return st;
     char* q = static_cast<char*>(ctx->hyb_small);
     HybCounts* cnt = carve<HybCounts>(q, 1);
     double* mom = carve<double>(q, 5 * cells);
@@ -392,7 +393,8 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     // ---- 4. kinetic layers: PR(2,2,2) on the compact batch ----
     if (nk) {
         const size_t big_need = sizeof(double) * (size_t)nb * (size_t)(7 * nk + cells) + 8 * 256;
-        if ((st = grow(ctx, &ctx->hyb_big, &ctx->hyb_big_bytes, big_need, "kinetic workspace"))) return st;
+        const size_t big_max = sizeof(double) * (size_t)nb * (size_t)(8 * cells) + 8 * 256;  // every cell kinetic
+        if ((st = grow(ctx, &ctx->hyb_big, &ctx->hyb_big_bytes, big_need, "kinetic workspace", big_max))) return st;
         char* b = static_cast<char*>(ctx->hyb_big);
         double* fk = carve<double>(b, nk * nb);
         double* Y = carve<double>(b, nk * nb);

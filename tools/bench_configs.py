@@ -275,3 +275,5 @@ if __name__ == "__main__":
         else:
             r = config3(args.iters, args.nx, args.nx)
         print(json.dumps(r), flush=True)
+        torch.cuda.empty_cache()  # the next config starts from a clean device
+        hk.default_context().trim()

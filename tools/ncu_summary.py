@@ -6,15 +6,16 @@ rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(raw.splitlines()))
 h = r[0]
+units = dict(zip(h, r[1]))
 for row in r[2:]:
     d = dict(zip(h, row))
-    print(d["Kernel Name"], "time_ms", d.get("gpu__time_duration.sum"))
+    print(d["Kernel Name"], "time", d.get("gpu__time_duration.sum"), units.get("gpu__time_duration.sum", ""))
     for k in ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
               "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__throughput.avg.pct_of_peak_sustained_active",
               "lts__throughput.avg.pct_of_peak_sustained_elapsed", "dram__bytes_read.sum", "dram__bytes_write.sum",
               "lts__t_bytes.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread",
               "launch__grid_size", "sm__warps_active.avg.pct_of_peak_sustained_active"]:
-        print("  ", k, d.get(k))
+        print("  ", k, d.get(k), units.get(k, ""))
     st = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v) for k, v in d.items()
           if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued") and v.replace(".", "").isdigit()}
     tot = sum(st.values()) or 1
