@@ -178,13 +178,14 @@ __global__ void __launch_bounds__(32 * TIW, HK_TR_MINB) transport_march_kernel(T
 // face, so a row costs ONE x and ONE y reconstruction per node (2 instead of
 // 3); lanes 0, 1, 30, 31 are halo columns (no output).
 constexpr int TL_OUT = 28;
-template <bool FINAL, int NPT>
+
+template <bool FINAL, int NPT, bool MASK = false>
 __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p, int lg, const double* __restrict__ f,
                                                               double* __restrict__ out, const double* __restrict__ lh,
                                                               const double* __restrict__ rh, FinalCombine fc) {
     static_assert(NPT == 2, "double2 node pairs");
-    extern __shared__ uint8_t act_s[];  // this strip's row activity (row_act mode)
-    if (p.row_act) {
+    extern __shared__ uint8_t act_s[];  // this strip's row activity (MASK: p.row_act)
+    if (MASK) {
         for (int t = threadIdx.x; t < p.ny; t += blockDim.x) act_s[t] = p.row_act[(int64_t)blockIdx.x * p.ny + t];
         __syncthreads();
     }
@@ -254,8 +255,7 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
     // row activity under the optional mask (warp-uniform): a row is computed
     // when one of the strip's output cells is masked in; its y face also when
     // the next row is (the face is shared)
-    const bool masked = p.row_act != nullptr;
-    auto row_active = [&](int jj) -> bool { return !masked || act_s[jj] != 0; };
+    auto row_active = [&](int jj) -> bool { return !MASK || act_s[jj] != 0; };
     bool act = row_active(0), act_next = ny > 1 ? row_active(1) : false;
     for (int j = 0; j < ny; ++j) {
         if (j > 0) {
@@ -267,8 +267,8 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
             nw4 = ld(j + 3);  // row j+3 = w4 of row j+1
             if (FINAL && outlane) fin_loads(j + 1, nf0, nf1, nf2);
         }
-        const bool act_nn = j + 2 < ny ? row_active(j + 2) : false;
-        if (!act && !act_next) {  // nothing here, and the next row does not need this row's face
+        const bool act_nn = MASK && j + 2 < ny ? row_active(j + 2) : false;
+        if (MASK && !act && !act_next) {  // nothing here, and the next row does not need this row's face
             act = act_next;
             act_next = act_nn;
             continue;
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
         double fy[2], fx[2];
         fy[0] = yface(w0.x, w1.x, w2.x, w3.x, w4.x);
         fy[1] = yface(w0.y, w1.y, w2.y, w3.y, w4.y);
-        if (!act) {  // face only (the minus face of the next, active row)
+        if (MASK && !act) {  // face only (the minus face of the next, active row)
             fyp[0] = fy[0];
             fyp[1] = fy[1];
             act = act_next;
@@ -361,9 +361,11 @@ int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const d
         const size_t smem = p.row_act ? size_t(p.ny) : 0;
         if (smem > 48 * 1024) return fail(ctx, HK_UNSUPPORTED, "transport: row activity needs ny <= 49152");
         if (fin)
-            transport_lanes_kernel<true, 2><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+            transport_lanes_kernel<true, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+        else if (p.row_act)
+            transport_lanes_kernel<false, 2, true><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
         else
-            transport_lanes_kernel<false, 2><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+            transport_lanes_kernel<false, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
         ctx->launches++;
         return check_cuda(ctx, cudaGetLastError(), "transport kernel");
     }
