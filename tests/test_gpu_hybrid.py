@@ -153,3 +153,16 @@ def test_hybrid_two_slabs_equal_torus(hk):
     kin = r != 0
     assert float((glob[2] - h)[~kin].abs().max()) <= 1e-13 * float(h.abs().max())
     assert float((glob[3] - f)[kin].abs().max()) <= 1e-13 * float(f.abs().max())
+
+
+def test_hybrid_all_kinetic_algorithm1(hk, oracle):
+    """Every cell kinetic at t = 0 (band layer 2, the rest layer 1): Algorithm 1 moves
+    cells between layers 1 and 2 and down to 0; a 6 x 5 grid (stencils wrap twice)."""
+    nx, ny, n = 6, 5, 16
+    hydro, eps, r, f = inputs.config4_hybrid_state(nx, ny, n, half_width=1.0 / nx)
+    r = np.where(r != 0, 2, 1).astype(np.int8)
+    for c in np.nonzero(r == 1)[0]:
+        rho = hydro[c, 0]
+        f[c] = inputs.maxwellian(n, rho, (0.0, 0.0, 0.0), hydro[c, 3] / (1.5 * rho))
+    for s, rb, ra, cg in _run_both(hk, oracle, nx, ny, n, 4, 4, None, 2, state=(hydro, eps, r, f)):
+        pass
