@@ -320,6 +320,9 @@ typedef struct {
     double pen_coeff;           /* penalization beta = pen_coeff rho (2 pi) */
     double eps_weno;            /* 1e-6 */
     uint32_t coll_flags;        /* hk_collision_batch flags of the residuals */
+    int ghost_x;                /* x-slab use: columns i < ghost_x and i >= nx - ghost_x are exchanged
+                                   ghosts whose results are discarded; their residuals are only evaluated
+                                   where an interior cell depends on them (0: plain torus) */
 } hk_hybrid_params;
 int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx, double dy, double dt, const double* eps_dev,
                    int8_t* r_dev, double* hydro_dev, double* f_dev, const hk_hybrid_params* params, int64_t* counts);

@@ -78,7 +78,8 @@ class HybridParams(C.Structure):
     _fields_ = [("eta0", C.c_double), ("eta1", C.c_double), ("delta0", C.c_double), ("mu0", C.c_double),
                 ("kappa0", C.c_double), ("signed_sum", C.c_int), ("update_regimes", C.c_int),
                 ("heat_ratio", C.c_double), ("esbgk_beta", C.c_double), ("nu_coeff", C.c_double),
-                ("pen_coeff", C.c_double), ("eps_weno", C.c_double), ("coll_flags", C.c_uint32)]
+                ("pen_coeff", C.c_double), ("eps_weno", C.c_double), ("coll_flags", C.c_uint32),
+                ("ghost_x", C.c_int)]
 
 
 _lib = None

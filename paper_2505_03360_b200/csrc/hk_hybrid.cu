@@ -40,7 +40,13 @@ constexpr int kLT = 1024;  // threads of the list kernels
 struct HybCounts {
     unsigned long long bad;  // (cell << 8) | status, lowest first
     int nk_old, n1, n2, nm, n01, n10, n0;
+    int n2a, n2b;  // layer-2 batch classes (ghost_x > 0): A interior, B ghost distance <= 2, C the rest
 };
+
+// Distance of column i from the slab interior when gx ghost columns pad each side (0 = interior).
+__device__ __forceinline__ int ghost_dist(int i, int nx, int gx) {
+    return i < gx ? gx - i : (i >= nx - gx ? i - (nx - gx) + 1 : 0);
+}
 
 __device__ void fail_at(HybCounts* c, int64_t cell, int code) {
     atomicMin(&c->bad, ((unsigned long long)cell << 8) | (unsigned)code);
@@ -177,11 +183,12 @@ __global__ void __launch_bounds__(kLT) list_new_kernel(int nx, int ny, const int
                                                        const double* __restrict__ eps, int64_t* __restrict__ list,
                                                        int64_t* __restrict__ tmp2, double* __restrict__ eps_k,
                                                        int64_t* __restrict__ mlist, double* __restrict__ mmom,
-                                                       HybCounts* cnt) {
+                                                       HybCounts* cnt, int gx, int64_t* __restrict__ tmp2b,
+                                                       int64_t* __restrict__ tmp2c) {
     __shared__ int wt[64];
-    __shared__ int b1, b2, bm;
+    __shared__ int b1, b2, bm, b2b, b2c;
     const int64_t cells = (int64_t)nx * ny;
-    if (threadIdx.x == 0) b1 = b2 = bm = 0;
+    if (threadIdx.x == 0) b1 = b2 = bm = b2b = b2c = 0;
     __syncthreads();
     for (int64_t c0 = 0; c0 < cells; c0 += kLT) {
         const int64_t c = c0 + threadIdx.x;
@@ -197,12 +204,16 @@ __global__ void __launch_bounds__(kLT) list_new_kernel(int nx, int ny, const int
                            kin_at(r_new, nx, ny, i, j - d) || kin_at(r_new, nx, ny, i, j + d);
             }
         }
+        const int gd = c < cells ? ghost_dist(int(c % nx), nx, gx) : 0;
+        const int cls = gd == 0 ? 0 : (gd <= 2 ? 1 : 2);
         const int s1 = block_slot(rn == 1, wt, &b1);
-        const int s2 = block_slot(rn == 2, wt, &b2);
+        const int s2 = block_slot(rn == 2 && cls == 0, wt, &b2);
+        const int s2b = block_slot(rn == 2 && cls == 1, wt, &b2b);
+        const int s2c = block_slot(rn == 2 && cls == 2, wt, &b2c);
         const bool mw = halo || (ro == 0 && rn != 0);
         const int sm = block_slot(mw, wt, &bm);
         if (rn == 1) list[s1] = c;
-        if (rn == 2) tmp2[s2] = c;
+        if (rn == 2) (cls == 0 ? tmp2[s2] : (cls == 1 ? tmp2b[s2b] : tmp2c[s2c])) = c;
         if (mw) {
             mlist[sm] = c;
             if (!mom_from_u(U + 4 * c, hr, mmom + 5 * sm)) {
@@ -212,13 +223,17 @@ __global__ void __launch_bounds__(kLT) list_new_kernel(int nx, int ny, const int
         }
     }
     __syncthreads();
-    const int n1 = b1, n2 = b2;
-    for (int k = threadIdx.x; k < n2; k += kLT) list[n1 + k] = tmp2[k];
+    const int n1 = b1, n2a = b2, n2b = b2b, n2c = b2c, n2 = n2a + n2b + n2c;
+    for (int k = threadIdx.x; k < n2a; k += kLT) list[n1 + k] = tmp2[k];
+    for (int k = threadIdx.x; k < n2b; k += kLT) list[n1 + n2a + k] = tmp2b[k];
+    for (int k = threadIdx.x; k < n2c; k += kLT) list[n1 + n2a + n2b + k] = tmp2c[k];
     __syncthreads();
     for (int k = threadIdx.x; k < n1 + n2; k += kLT) eps_k[k] = eps[list[k]];
     if (threadIdx.x == 0) {
         cnt->n1 = n1;
         cnt->n2 = n2;
+        cnt->n2a = n2a;
+        cnt->n2b = n2b;
         cnt->nm = bm;
     }
 }
@@ -236,9 +251,10 @@ __global__ void commit_kernel(int64_t cells, const int8_t* __restrict__ r_new, i
 
 // Per-cell statuses of the batch (stage info: status | fallback << 8; residual status).
 __global__ void status_kernel(int64_t nk, const int64_t* __restrict__ list, const int* __restrict__ st,
-                              HybCounts* cnt) {
+                              HybCounts* cnt, int nx, int gx) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nk) return;
+    if (ghost_dist(int(list[k] % nx), nx, gx)) return;  // ghost results are discarded (their owner checks them)
     const int s = st[k] & 0xff;
     if (s && s != HK_NUMERICAL_CONSISTENCY) fail_at(cnt, list[k], s);
 }
@@ -333,7 +349,7 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
 
     // ---- per-cell workspace (fixed per grid) ----
     const size_t small_need = 256 * 16 + (sizeof(double) * cells * (5 + 1 + 4 + 8 + 5 + 5 + 1 + 1) +
-                                          sizeof(int64_t) * cells * 4 + sizeof(int) * cells * 3 + cells * 2 + 4096);
+                                          sizeof(int64_t) * cells * 6 + sizeof(int) * cells * 3 + cells * 2 + 4096);
     if ((st = grow(ctx, &ctx->hyb_small, &ctx->hyb_small_bytes, small_need, "per-cell workspace", small_need)))
         return st;
     char* q = static_cast<char*>(ctx->hyb_small);
@@ -350,6 +366,8 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     int64_t* tmp2 = carve<int64_t>(q, cells);
     int64_t* mlist = carve<int64_t>(q, cells);
     int64_t* list_old = carve<int64_t>(q, cells);
+    int64_t* tmp2b = carve<int64_t>(q, cells);
+    int64_t* tmp2c = carve<int64_t>(q, cells);
     int* pos = carve<int>(q, cells);
     int* stk = carve<int>(q, cells);
     int* stk2 = carve<int>(q, cells);
@@ -374,12 +392,17 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     }
     // ---- 2. conversion + the lists of the step ----
     convert_kernel<<<nblk(cells, 128), 128, 0, s>>>(cells, r_dev, r_new, hydro_dev, mom, hr, W, cnt);
-    list_new_kernel<<<1, kLT, 0, s>>>(nx, ny, r_dev, r_new, hydro_dev, hr, eps_dev, list, tmp2, eps_k, mlist, mmom, cnt);
+    const int gx = p->ghost_x;
+    if (gx < 0 || 2 * gx >= nx) return fail(ctx, HK_CONTRACT, "hybrid step: ghost_x must be in [0, nx / 2)");
+    list_new_kernel<<<1, kLT, 0, s>>>(nx, ny, r_dev, r_new, hydro_dev, hr, eps_dev, list, tmp2, eps_k, mlist, mmom, cnt,
+                                      gx, tmp2b, tmp2c);
     ctx->launches += 2;
     if ((st = check_cuda(ctx, cudaGetLastError(), "hybrid lists"))) return st;
     HybCounts h{};
     if ((st = read_counts(ctx, cnt, h, "hybrid_step indicator pass"))) return st;
     const int64_t n1 = h.n1, n2 = h.n2, nk = n1 + n2, nm = h.nm;
+    // layer-2 cells whose residual is needed: at Y1 classes A + B, at Y2 class A (all of K2 on a plain torus)
+    const int64_t n2_y1 = h.n2a + h.n2b, n2_y2 = h.n2a;
     prof.mark("indicators");
     // Maxwellians of the 0 -> 1 cells and of the layer-0 transport halo
     if (nm && (st = maxwellian_launch(ctx, n, vmax, mmom, nm, f_dev, nullptr, mlist, nullptr))) return st;
@@ -421,10 +444,10 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
                                  p->pen_coeff, stk + n1, nullptr, k1o ? k1o + n1 * nb : nullptr, 1.0 / t.a_im00);
             return e;
         };
-        auto residual = [&](const double* y) -> int {  // penalized_residual of the layer-2 part
-            if (!n2) return HK_OK;
-            int e = collision_launch(ctx, k, y + n1 * nb, res + n1 * nb, n2, p->coll_flags & ~HK_COLL_STRICT, nullptr);
-            return e ? e : residual_finish_launch(ctx, n, vmax, y + n1 * nb, res + n1 * nb, n2, p->pen_coeff, stk2 + n1);
+        auto residual = [&](const double* y, int64_t m2) -> int {  // penalized_residual of the first m2 layer-2 cells
+            if (!m2) return HK_OK;
+            int e = collision_launch(ctx, k, y + n1 * nb, res + n1 * nb, m2, p->coll_flags & ~HK_COLL_STRICT, nullptr);
+            return e ? e : residual_finish_launch(ctx, n, vmax, y + n1 * nb, res + n1 * nb, m2, p->pen_coeff, stk2 + n1);
         };
         auto transport = [&](const double* y) -> int {  // T(y) at the batch cells
             int e = hk_scatter_cells(ctx, nb, y, list, nk, f_dev);
@@ -433,38 +456,48 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
             return e;
         };
         // q = tr (+ res / eps on the layer-2 part), via the IMEX combinations
-        auto explicit_part = [&](int op, double* o, const double* f0, const double* y) -> int {
-            int e = HK_OK;
-            if (n1) e = combine_launch(ctx, op, n1 * nb, nb, dt, eps_k, o, f0, y, q1, k1, tr, nullptr);
-            if (!e && n2)
-                e = combine_launch(ctx, op, n2 * nb, nb, dt, eps_k + n1, o + n1 * nb, f0 ? f0 + n1 * nb : nullptr,
-                                   y ? y + n1 * nb : nullptr, q1 + n1 * nb, k1 + n1 * nb, tr + n1 * nb, res + n1 * nb);
+        // batch ranges [b0, b1) with (with_res) or without the residual term
+        auto explicit_part = [&](int op, double* o, const double* y, int64_t m2) -> int {
+            auto range = [&](int64_t b0, int64_t b1, bool with_res) -> int {
+                if (b1 <= b0) return HK_OK;
+                return combine_launch(ctx, op, (b1 - b0) * nb, nb, dt, eps_k + b0, o + b0 * nb, nullptr,
+                                      y ? y + b0 * nb : nullptr, q1 + b0 * nb, k1 + b0 * nb, tr + b0 * nb,
+                                      with_res ? res + b0 * nb : nullptr);
+            };
+            int e = range(0, n1, false);
+            if (!e) e = range(n1, n1 + m2, true);
+            if (!e) e = range(n1 + m2, nk, false);  // ghost cells whose result is not needed
             return e;
         };
         st = hk_gather_cells(ctx, nb, f_dev, list, nk, fk);                               // f^n of the batch
         prof.mark("gather");
+        auto check_status = [&](const int* arr) {  // statuses are overwritten by the next phase: fold them now
+            status_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, arr, cnt, nx, gx);
+            ctx->launches++;
+        };
         if (!st) st = stages(fk, t.a_im00 * dt, Y, k1);                                   // Y1, k1
+        if (!st) check_status(stk);
         prof.mark("stage1");
         if (!st) st = transport(Y);                                                       // T(Y1)
         prof.mark("transport1");
-        if (!st) st = residual(Y);                                                        // res(Y1)
+        if (!st) st = residual(Y, n2_y1);                                                 // res(Y1)
+        if (!st) check_status(stk2);
         prof.mark("residual1");
-        if (!st) st = explicit_part(1, q1, nullptr, nullptr);                             // q1
+        if (!st) st = explicit_part(1, q1, nullptr, n2_y1);                               // q1
         if (!st) st = combine_launch(ctx, 2, nk * nb, nb, dt, eps_k, fa, fk, nullptr, q1, k1, nullptr, nullptr);
         prof.mark("combine");
         if (!st) st = stages(fa, t.a_im11 * dt, Y, nullptr);                              // Y2
         prof.mark("stage2");
         if (!st) st = transport(Y);                                                       // T(Y2)
         prof.mark("transport2");
-        if (!st) st = residual(Y);                                                        // res(Y2)
+        if (!st) st = residual(Y, n2_y2);                                                 // res(Y2)
         prof.mark("residual2");
-        if (!st) st = explicit_part(3, fk, nullptr, Y);                                   // final, in place
+        if (!st) st = explicit_part(3, fk, Y, n2_y2);                                     // final, in place
         if (!st) st = hk_scatter_cells(ctx, nb, fk, list, nk, f_dev);
         prof.mark("final");
         if (!st) {
-            status_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, stk, cnt);
-            status_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, stk2, cnt);
-            ctx->launches += 2;
+            check_status(stk);   // stage 2
+            check_status(stk2);  // residual at Y2 (cells past n1 + n2_y2 keep their Y1 status: ghosts, skipped)
         }
         if (st) return st;
     }

@@ -359,11 +359,13 @@ class HybridParams:
     pen_coeff: float = 2.0 * math.pi
     eps_weno: float = 1e-6
     exact: bool = False  # collision of the residuals on the exact (two-transform) path
+    ghost_x: int = 0     # x-slab ghost columns per side (partition.hybrid_step_slab)
 
     def to_c(self) -> "_abi.HybridParams":
         return _abi.HybridParams(self.eta0, self.eta1, self.delta0, self.mu0, self.kappa0, int(self.signed_sum),
                                  int(self.update_regimes), self.heat_ratio, self.esbgk_beta, self.nu_coeff,
-                                 self.pen_coeff, self.eps_weno, _abi.HK_COLL_EXACT if self.exact else 0)
+                                 self.pen_coeff, self.eps_weno, _abi.HK_COLL_EXACT if self.exact else 0,
+                                 int(self.ghost_x))
 
 
 class HybridCounts(NamedTuple):

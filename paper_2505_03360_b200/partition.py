@@ -33,13 +33,21 @@ class XSlab:
     ny: int
     world: int
     rank: int
+    bounds: tuple = None  # optional column boundaries (world + 1 values, 0 .. nx); default: even split
 
     def __post_init__(self):
         if self.nx < self.world * HALO:
             raise ValueError(f"nx={self.nx} too small for {self.world} slabs with a {HALO}-column halo")
-        base, rem = divmod(self.nx, self.world)
-        self.nxl = base + (1 if self.rank < rem else 0)
-        self.i0 = self.rank * base + min(self.rank, rem)
+        if self.bounds is not None:
+            b = list(self.bounds)
+            if len(b) != self.world + 1 or b[0] != 0 or b[-1] != self.nx or any(b[q + 1] - b[q] < HALO for q in
+                                                                              range(self.world)):
+                raise ValueError(f"bounds {b} must split 0..{self.nx} into {self.world} slabs of >= {HALO} columns")
+            self.i0, self.nxl = b[self.rank], b[self.rank + 1] - b[self.rank]
+        else:
+            base, rem = divmod(self.nx, self.world)
+            self.nxl = base + (1 if self.rank < rem else 0)
+            self.i0 = self.rank * base + min(self.rank, rem)
         self.left = (self.rank - 1) % self.world
         self.right = (self.rank + 1) % self.world
 
@@ -208,6 +216,37 @@ def penalized_imex_step_slab(part: XSlab, f: torch.Tensor, kernel, dx: float, dy
 HYB_GHOST = 8
 
 
+def weighted_bounds(col_work, world: int, min_width: int = HYB_GHOST, ghost: int = 2):
+    """Column boundaries of `world` x-slabs that balance the per-slab work: col_work[i]
+    = work of column i (e.g. 2 x layer-2 cells + layer-1 cells / 10), a slab's work being
+    its columns' plus that of `ghost` extra columns per side (the ghost cells whose
+    residual the slab evaluates).  Exact min-max split by dynamic programming over the
+    boundaries (slab 0 starts at column 0); every slab keeps >= min_width columns."""
+    import numpy as np
+
+    w = np.asarray(col_work, dtype=np.float64)
+    nx = len(w)
+    if nx < world * min_width:
+        raise ValueError("grid too narrow for the requested slabs")
+    ext = np.concatenate([w[nx - ghost:], w, w[:ghost]]) if ghost else w
+    P = np.concatenate([[0.0], np.cumsum(ext)])
+    work = lambda a, e: P[e + 2 * ghost] - P[a]  # noqa: E731  columns a-ghost .. e+ghost-1 (periodic)
+    INF = float("inf")
+    best = np.full((world + 1, nx + 1), INF)
+    arg = np.zeros((world + 1, nx + 1), dtype=np.int64)
+    best[0, 0] = 0.0
+    for q in range(1, world + 1):
+        for e in range(q * min_width, nx - (world - q) * min_width + 1):
+            a = np.arange((q - 1) * min_width, e - min_width + 1)
+            cand = np.maximum(best[q - 1, a], work(a, e))
+            k = int(np.argmin(cand))
+            best[q, e], arg[q, e] = cand[k], a[k]
+    bounds = [nx]
+    for q in range(world, 0, -1):
+        bounds.append(int(arg[q, bounds[-1]]))
+    return tuple(reversed(bounds))
+
+
 def hybrid_pad(part: XSlab, width: int, fields, halos):
     """[ny][nxl + 2 width] padded copies of the local fields (each [cells, k]),
     halos = [(left [ny][width][k], right [ny][width][k]), ...]."""
@@ -237,9 +276,12 @@ def hybrid_step_slab(part: XSlab, kernel, dx: float, dy: float, dt: float, eps_c
     interior is exactly the global step's.  Returns the global layer counts
     [n0, n1, n2] (all-reduced).  `halos` (tests) supplies the exchanged columns
     directly: [(left, right)] for r, eps, hydro, f as [ny][width][k]."""
+    import dataclasses
+
     from .kinetic import HybridParams, hybrid_step
 
-    params = params or HybridParams()
+    # ghost results are discarded: their residuals only where an interior cell depends on them
+    params = dataclasses.replace(params or HybridParams(), ghost_x=width)
     fields = [r.view(-1, 1), eps_cell.to(device=f.device, dtype=torch.float64).view(-1, 1), hydro, f]
     if halos is None:
         halos = []

@@ -120,3 +120,26 @@ def test_slab_bounds():
         XSlab(3, 4, 2, 0)
     p = XSlab(512, 128, 8, 7)
     assert p.nxl == 64 and p.i0 == 448 and p.left == 6 and p.right == 0
+
+
+def test_weighted_bounds_balance():
+    """Work-weighted slab boundaries: valid split, >= 8 columns each, and a lower
+    maximum slab work than the even split on a banded work profile."""
+    import numpy as np
+    from paper_2505_03360_b200.partition import XSlab, weighted_bounds
+    nx, world = 200, 8
+    w = np.full(nx, 40.0)
+    w[95:105] = 400.0
+    w[:5] = w[-5:] = 400.0
+    b = weighted_bounds(w, world)
+    assert b[0] == 0 and b[-1] == nx and all(b[q + 1] - b[q] >= 8 for q in range(world))
+
+    def worst(bounds):
+        return max(w[np.arange(bounds[q] - 2, bounds[q + 1] + 2) % nx].sum() for q in range(world))
+
+    even = [q * nx // world for q in range(world)] + [nx]
+    assert worst(b) <= 0.85 * worst(even)
+    parts = [XSlab(nx, 4, world, q, b) for q in range(world)]
+    assert [p.i0 for p in parts] == list(b[:-1]) and sum(p.nxl for p in parts) == nx
+    with pytest.raises(ValueError):
+        XSlab(nx, 4, 2, 0, (0, 1, nx))

@@ -212,6 +212,59 @@ def config4_hybrid(steps=20, full_sample=True):
     return out
 
 
+def config4_slabs(world=8, steps=3, weighted=False):
+    """Config 4's hybrid step decomposed into `world` x-slabs (partition.hybrid_step_slab:
+    8 exchanged ghost columns per side, residuals only where the interior depends on
+    them), the slabs stepped one after another on this GPU with the halos copied
+    between them (the exchange an NCCL run would do).  Reports each slab's step time:
+    max over slabs ~ the per-GPU step time of a world-GPU run (exchange excluded),
+    and the redundant work of the decomposition against the single-GPU step."""
+    from paper_2505_03360_b200.partition import HYB_GHOST as W, XSlab, hybrid_step_slab, weighted_bounds
+    nx = ny = 200
+    n, a1, a2 = 32, 4, 8
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    k = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    hydro, eps, r, _ = inputs.config4_hybrid_state(nx, ny, n, with_f=False)
+    hd, ed, rd = (torch.from_numpy(x).cuda() for x in (hydro, eps, r))
+    f = kinetic.conserved_to_maxwellian(hd, vg)
+    dx = 1.0 / nx
+    dt = 0.5 * dx / (inputs.VMAX - inputs.VMAX / n)
+    bounds = None
+    if weighted:  # balance 2 x layer-2 + layer-1 / 10 cells per column (the t = 0 layer map)
+        rr = r.reshape(ny, nx)
+        bounds = weighted_bounds(2.0 * (rr == 2).sum(0) + 0.1 * (rr == 1).sum(0) + 0.01 * ny, world)
+    parts = [XSlab(nx, ny, world, q, bounds) for q in range(world)]
+    loc = [[p_.scatter(t.view(nx * ny, -1)) for t in (rd, ed, hd, f)] for p_ in parts]
+    del f
+    torch.cuda.empty_cache()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in parts]
+    per = [[] for _ in parts]
+    warm = 2  # warm-up steps: the layer-2 batches grow over the first steps (workspace growth)
+    for step in range(steps + warm):
+        halos = []
+        for q, p_ in enumerate(parts):
+            lt, rt = loc[(q - 1) % world], loc[(q + 1) % world]
+            lp, rp = parts[(q - 1) % world], parts[(q + 1) % world]
+            halos.append([(lt[fi].view(ny, lp.nxl, -1)[:, -W:].contiguous(),
+                           rt[fi].view(ny, rp.nxl, -1)[:, :W].contiguous()) for fi in range(4)])
+        for q, p_ in enumerate(parts):
+            rl, el, hl, fl = loc[q]
+            ev[q][0].record()
+            hybrid_step_slab(p_, k, dx, dx, dt, el.view(-1), rl.view(-1), hl, fl, halos=halos[q])
+            ev[q][1].record()
+        torch.cuda.synchronize()
+        if step >= warm:
+            for q in range(world):
+                per[q].append(ev[q][0].elapsed_time(ev[q][1]))
+    ms = [sum(v) / len(v) for v in per]
+    return {"config": f"config4 on {world} x-slabs (hybrid_step_slab, 8 ghost columns, "
+                      f"{'work-weighted' if weighted else 'even'} boundaries), slabs stepped in turn on 1 GPU",
+            "slab_columns": [p_.nxl for p_ in parts], "ms_per_slab_step": ms, "max_slab_ms": max(ms),
+            "sum_slab_ms": sum(ms),
+            "note": "max_slab_ms ~ per-GPU step time of a world-GPU run without the halo exchange; "
+                    "sum_slab_ms / single-GPU step = redundant-work factor of the decomposition"}
+
+
 def config5(iters, steps=True):
     """Config 5, one GPU's x-slab (64 x 128 cells, N = 64, M = 8 x 8): Q over
     the slab (fast path + guard) and, with `steps`, one PR(2,2,2) IMEX step of
@@ -268,6 +321,10 @@ if __name__ == "__main__":
             r = config1(args.iters)
         elif c == "4":
             r = config4(args.iters)
+        elif c == "4s":
+            r = config4_slabs()
+        elif c == "4w":
+            r = config4_slabs(weighted=True)
         elif c == "4h":
             r = config4_hybrid(args.hyb_steps, full_sample=not args.no_full)
         elif c == "5":
