@@ -850,7 +850,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                 named_bar(1, 128);  // every producer warp is done with its staging plane
                 for (int idx = t; idx < N * N * 4; idx += 128) {
                     const int j3l = idx % 4, j2 = (idx / 4) % N, j1 = idx / (4 * N);
-                    Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + 4 * pp + j3l], 0.0);
+                    Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(__ldg(fc + (j1 * N + j2) * N + r * P + 4 * pp + j3l), 0.0);
                 }
                 named_bar(1, 128);
                 {
@@ -1066,7 +1066,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                         for (int i = 0; i < 8; ++i) {
                             const int j1 = 8 * c + i;
                             const int64_t gi = ((int64_t)j1 * N + lane) * N + j3;
-                            const double lt = fc[gi] * y[j1].x;
+                            const double lt = __ldg(fc + gi) * y[j1].x;  // read-only path (47.6 -> 46.7 ms, config 2)
                             const double qre = a.jac * (a.w * gv[i] - lt);
                             qc[gi] = qre;
                             mre = fmax(mre, fabs(qre));
