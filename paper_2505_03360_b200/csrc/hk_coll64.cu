@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                 const int j3 = r * P + pl;
                 named_bar(1, 128);  // Pw free
                 for (int idx = u; idx < N * N; idx += 128)
-                    Pw[(idx / N) * ROW + (idx % N)] = make_double2(fc[(int64_t)idx * N + j3], 0.0);
+                    Pw[(idx / N) * ROW + (idx % N)] = make_double2(__ldg(fc + (int64_t)idx * N + j3), 0.0);
                 named_bar(1, 128);
                 {  // rows j1 = pp over j2 (DIF), back in natural order
                     double2* row = Pw + pp * ROW;
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                                     const int jj = 8 * c + i;
                                     const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
                                     const int64_t gi = ((int64_t)j1 * N + pp) * N + j3;
-                                    const double lt = fc[gi] * y[jj].x;
+                                    const double lt = __ldg(fc + gi) * y[jj].x;
                                     const double qre = a.jac * (a.w * gv[i] - lt);
                                     qc[gi] = qre;
                                     mre = fmax(mre, fabs(qre));
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
                                     const int jj = 4 * c + i;
                                     const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
                                     const int64_t gi = ((int64_t)j1 * N + pp) * N + j3;
-                                    const double fv = fc[gi];
+                                    const double fv = __ldg(fc + gi);
                                     const double qre = a.jac * (a.w * gv[2 * i] - fv * y[jj].x);
                                     const double qim = a.jac * (a.w * gv[2 * i + 1] - fv * y[jj].y);
                                     qc[gi] = qre;
@@ -566,7 +566,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                 const int j3 = r * P + pl;
                 named_bar(1, 128);  // Pw free
                 for (int idx = u; idx < N * N; idx += 128)
-                    Pw[(idx / N) * ROW + (idx % N)] = make_double2(fc[(int64_t)idx * N + j3], 0.0);
+                    Pw[(idx / N) * ROW + (idx % N)] = make_double2(__ldg(fc + (int64_t)idx * N + j3), 0.0);
                 named_bar(1, 128);
                 {  // rows j1 = pp over j2 (DIF), back in natural order
                     double2* row = Pw + pp * ROW;
@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                             const int jj = 8 * c + i;
                             const int j1 = jj < Q ? h * Q + jj : M + h * Q + (jj - Q);
                             const int64_t gi = ((int64_t)j1 * N + pp) * N + j3;
-                            const double lt = fc[gi] * y[jj].x;
+                            const double lt = __ldg(fc + gi) * y[jj].x;
                             const double qre = a.jac * (a.w * gv[i] - lt);
                             qc[gi] = qre;
                             mre = fmax(mre, fabs(qre));
