@@ -382,7 +382,7 @@ struct GeoP {
     static constexpr int PLANE = N * ROW;
     static constexpr int SLAB = P * PLANE;
 #ifndef HK_SLOTS
-#define HK_SLOTS 3  // measured: D = 2 60.8 ms, 3 51.9, 4 52.6, 5 52.9 (config 2, no guard)
+#define HK_SLOTS 2  // config 2: D = 2 46.2 ms, 3 46.8, 4 48.7 (final 12-warp kernel; the 8-warp kernel preferred 3)
 #endif
     static constexpr int D = HK_SLOTS;  // exchange slots in flight per team
     static_assert(P * N == 128, "one pencil per role thread");
