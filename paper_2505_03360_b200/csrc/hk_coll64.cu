@@ -33,11 +33,14 @@
 
 namespace hk {
 
+#ifndef HK_SLOTS64
+#define HK_SLOTS64 2  // config 5 slab: D = 2 1609 ms, 3 1636, 4 1665
+#endif
 struct Geo64 {
     static constexpr int N = 64, C = 32, P = 2, M = 32, Q = 16;
     static constexpr int ROW = N + 1;           // padded SMEM row (conflict-free columns)
     static constexpr int PLANE = N * ROW;       // double2 per landing plane
-    static constexpr int D = 4;                 // exchange slots per team
+    static constexpr int D = HK_SLOTS64;        // exchange slots per team
     static constexpr int64_t NB = (int64_t)N * N * N;
     static constexpr int BLK = P * N * N;       // double2 per destination CTA per field
     static constexpr int64_t SLOT = (int64_t)C * BLK;
