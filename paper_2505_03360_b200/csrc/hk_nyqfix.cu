@@ -34,7 +34,10 @@ struct GeoFix {
     static constexpr int PLANE = N * ROW;                          // double2, padded plane
     static constexpr int NN = N * N;
     static constexpr size_t SMEM1 = size_t(3) * PLANE * sizeof(double2);
-    static constexpr int T = N >= 64 ? 4 : (N >= 32 ? 8 : 16);    // j1 planes per apply work item
+#ifndef HK_NYQ_T32
+#define HK_NYQ_T32 16  // config-4 hybrid residual (7600 listed cells): T = 4 59.4 ms, 8 56.6, 16 55.8, 32 62.1
+#endif
+    static constexpr int T = N >= 64 ? 4 : (N >= 32 ? HK_NYQ_T32 : 16);  // j1 planes per apply work item
     static constexpr int MP = NN / 256;                            // (j2, j3) pairs per thread
     static constexpr int STAGE = NN + 2 * T * N;                   // double2 per direction in SMEM
     static constexpr size_t SMEM2 = size_t(2) * STAGE * sizeof(double2) + 64 * sizeof(double);
