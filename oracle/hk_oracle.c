@@ -55,75 +55,150 @@ void hko_unit_root(long k, long n, double* c, double* s) {
 
 static int is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
-static void fft_pow2_contig(int n, double* x, int sign, const double* tw) {
-    /* bit reversal */
+/* Twiddle tables e^{i 2 pi k/n}, k < n, one per power-of-two n, built once
+ * (same hko_unit_root values the per-call tables had) and read-only after. */
+static double* g_tw[31];
+static pthread_mutex_t g_tw_mu = PTHREAD_MUTEX_INITIALIZER;
+
+static const double* twiddles(int n) {
+    int lg = 0;
+    while ((1 << lg) < n) ++lg;
+    double* t = __atomic_load_n(&g_tw[lg], __ATOMIC_ACQUIRE);
+    if (t) return t;
+    pthread_mutex_lock(&g_tw_mu);
+    t = g_tw[lg];
+    if (!t) {
+        t = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+        for (int k = 0; k < n; ++k) hko_unit_root(k, n, &t[2 * k], &t[2 * k + 1]);
+        __atomic_store_n(&g_tw[lg], t, __ATOMIC_RELEASE);
+    }
+    pthread_mutex_unlock(&g_tw_mu);
+    return t;
+}
+
+/* Radix-2 DIT over B pencils at once: x is [n][B] complex (pencil b of row j
+ * at x[2*(j*B+b)]).  Every pencil sees exactly the butterfly sequence of the
+ * single-pencil transform (bit reversal, then len = 2, 4, ..., n), so the
+ * results are bitwise those of B separate 1-D transforms. */
+static void fft_pow2_multi(int n, int B, double* x, int sign, const double* tw) {
     for (int i = 1, j = 0; i < n; ++i) {
         int bit = n >> 1;
         for (; j & bit; bit >>= 1) j ^= bit;
         j ^= bit;
         if (i < j) {
-            double tr = x[2 * i], ti = x[2 * i + 1];
-            x[2 * i] = x[2 * j]; x[2 * i + 1] = x[2 * j + 1];
-            x[2 * j] = tr; x[2 * j + 1] = ti;
+            double* a = x + 2 * (size_t)i * B;
+            double* b = x + 2 * (size_t)j * B;
+            for (int q = 0; q < 2 * B; ++q) { double t = a[q]; a[q] = b[q]; b[q] = t; }
         }
     }
     for (int len = 2; len <= n; len <<= 1) {
         int half = len >> 1, step = n / len;
         for (int i = 0; i < n; i += len) {
             for (int j = 0; j < half; ++j) {
-                double wr = tw[2 * (j * step)], wi = sign * tw[2 * (j * step) + 1];
-                double* a = x + 2 * (i + j);
-                double* b = x + 2 * (i + j + half);
-                double br = b[0] * wr - b[1] * wi;
-                double bi = b[0] * wi + b[1] * wr;
-                b[0] = a[0] - br; b[1] = a[1] - bi;
-                a[0] = a[0] + br; a[1] = a[1] + bi;
+                const double wr = tw[2 * (j * step)], wi = sign * tw[2 * (j * step) + 1];
+                double* a = x + 2 * (size_t)(i + j) * B;
+                double* b = x + 2 * (size_t)(i + j + half) * B;
+                for (int q = 0; q < B; ++q) {
+                    double br = b[2 * q] * wr - b[2 * q + 1] * wi;
+                    double bi = b[2 * q] * wi + b[2 * q + 1] * wr;
+                    b[2 * q] = a[2 * q] - br; b[2 * q + 1] = a[2 * q + 1] - bi;
+                    a[2 * q] = a[2 * q] + br; a[2 * q + 1] = a[2 * q + 1] + bi;
+                }
             }
         }
     }
 }
 
-void hko_fft_1d(int n, double* data, long stride, int sign) {
-    double* buf = (double*)malloc(sizeof(double) * 4 * (size_t)n);
-    double* tw = buf + 2 * n;
-    for (int k = 0; k < n; ++k) hko_unit_root(k, n, &tw[2 * k], &tw[2 * k + 1]);
+static void dft_naive(int n, double* data, long stride, int sign, const double* tw, double* buf) {
     for (int j = 0; j < n; ++j) {
         buf[2 * j] = data[2 * j * stride];
         buf[2 * j + 1] = data[2 * j * stride + 1];
     }
+    for (int k = 0; k < n; ++k) {
+        double sr = 0.0, si = 0.0;
+        for (int j = 0; j < n; ++j) {
+            long m = ((long)j * k) % n;
+            double wr = tw[2 * m], wi = sign * tw[2 * m + 1];
+            sr += buf[2 * j] * wr - buf[2 * j + 1] * wi;
+            si += buf[2 * j] * wi + buf[2 * j + 1] * wr;
+        }
+        data[2 * k * stride] = sr;
+        data[2 * k * stride + 1] = si;
+    }
+}
+
+void hko_fft_1d(int n, double* data, long stride, int sign) {
     if (is_pow2(n)) {
-        fft_pow2_contig(n, buf, sign, tw);
+        const double* tw = twiddles(n);
+        if (stride == 1) {
+            fft_pow2_multi(n, 1, data, sign, tw);
+            return;
+        }
+        double* buf = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+        for (int j = 0; j < n; ++j) {
+            buf[2 * j] = data[2 * j * stride];
+            buf[2 * j + 1] = data[2 * j * stride + 1];
+        }
+        fft_pow2_multi(n, 1, buf, sign, tw);
         for (int j = 0; j < n; ++j) {
             data[2 * j * stride] = buf[2 * j];
             data[2 * j * stride + 1] = buf[2 * j + 1];
         }
-    } else {
-        for (int k = 0; k < n; ++k) {
-            double sr = 0.0, si = 0.0;
-            for (int j = 0; j < n; ++j) {
-                long m = ((long)j * k) % n;
-                double wr = tw[2 * m], wi = sign * tw[2 * m + 1];
-                sr += buf[2 * j] * wr - buf[2 * j + 1] * wi;
-                si += buf[2 * j] * wi + buf[2 * j + 1] * wr;
-            }
-            data[2 * k * stride] = sr;
-            data[2 * k * stride + 1] = si;
-        }
+        free(buf);
+        return;
     }
+    double* buf = (double*)malloc(sizeof(double) * 4 * (size_t)n);
+    double* tw = buf + 2 * n;
+    for (int k = 0; k < n; ++k) hko_unit_root(k, n, &tw[2 * k], &tw[2 * k + 1]);
+    dft_naive(n, data, stride, sign, tw, buf);
     free(buf);
 }
 
+/* Pencils p0 .. p0+B-1 of a strided axis: pencil p, element j at
+ * d[2*(p*pstride + j*stride)] with pstride = 1 (adjacent pencils), gathered
+ * into a [n][B] tile, transformed, scattered back. */
+static void fft_strided_block(int n, double* d, long stride, int B, double* tile, int sign,
+                              const double* tw) {
+    for (int j = 0; j < n; ++j)
+        memcpy(tile + 2 * (size_t)j * B, d + 2 * (size_t)j * stride, sizeof(double) * 2 * B);
+    fft_pow2_multi(n, B, tile, sign, tw);
+    for (int j = 0; j < n; ++j)
+        memcpy(d + 2 * (size_t)j * stride, tile + 2 * (size_t)j * B, sizeof(double) * 2 * B);
+}
+
+#define HKO_FFT_TILE 16
+
 void hko_fft_3d(int n, double* d, int sign) {
     const long n2 = (long)n * n;
-    for (long p = 0; p < n2; ++p) hko_fft_1d(n, d + 2 * p * n, 1, sign);         /* axis 3 */
-    for (int i1 = 0; i1 < n; ++i1)
-        for (int i3 = 0; i3 < n; ++i3) hko_fft_1d(n, d + 2 * (i1 * n2 + i3), n, sign); /* axis 2 */
-    for (long p = 0; p < n2; ++p) hko_fft_1d(n, d + 2 * p, n2, sign);             /* axis 1 */
+    if (!is_pow2(n)) {
+        for (long p = 0; p < n2; ++p) hko_fft_1d(n, d + 2 * p * n, 1, sign);         /* axis 3 */
+        for (int i1 = 0; i1 < n; ++i1)
+            for (int i3 = 0; i3 < n; ++i3) hko_fft_1d(n, d + 2 * (i1 * n2 + i3), n, sign); /* axis 2 */
+        for (long p = 0; p < n2; ++p) hko_fft_1d(n, d + 2 * p, n2, sign);             /* axis 1 */
+        return;
+    }
+    const double* tw = twiddles(n);
+    const int B = n < HKO_FFT_TILE ? n : HKO_FFT_TILE;
+    double* tile = (double*)malloc(sizeof(double) * 2 * (size_t)n * B);
+    for (long p = 0; p < n2; ++p) fft_pow2_multi(n, 1, d + 2 * p * n, sign, tw); /* axis 3 */
+    for (int i1 = 0; i1 < n; ++i1)                                               /* axis 2 */
+        for (int i3 = 0; i3 < n; i3 += B) fft_strided_block(n, d + 2 * (i1 * n2 + i3), n, B, tile, sign, tw);
+    for (long p = 0; p < n2; p += B) fft_strided_block(n, d + 2 * p, n2, B, tile, sign, tw); /* axis 1 */
+    free(tile);
 }
 
 void hko_fft_2d(int n, double* d, int sign) {
-    for (int i = 0; i < n; ++i) hko_fft_1d(n, d + 2 * (long)i * n, 1, sign);
-    for (int j = 0; j < n; ++j) hko_fft_1d(n, d + 2 * j, n, sign);
+    if (!is_pow2(n)) {
+        for (int i = 0; i < n; ++i) hko_fft_1d(n, d + 2 * (long)i * n, 1, sign);
+        for (int j = 0; j < n; ++j) hko_fft_1d(n, d + 2 * j, n, sign);
+        return;
+    }
+    const double* tw = twiddles(n);
+    const int B = n < HKO_FFT_TILE ? n : HKO_FFT_TILE;
+    double* tile = (double*)malloc(sizeof(double) * 2 * (size_t)n * B);
+    for (int i = 0; i < n; ++i) fft_pow2_multi(n, 1, d + 2 * (long)i * n, sign, tw);
+    for (int j = 0; j < n; j += B) fft_strided_block(n, d + 2 * j, n, B, tile, sign, tw);
+    free(tile);
 }
 
 /* ===================================================================== */

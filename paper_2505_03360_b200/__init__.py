@@ -279,7 +279,13 @@ def spectral_collision(f, kernel: SpectralKernel, out=None, *, exact: bool = Fal
         if fh.size % nb:
             raise contract_violation("f is not a whole number of velocity blocks")
         ncells = fh.size // nb
-        q = out if out is not None else np.empty_like(fh)
+        if out is None:
+            q = np.empty_like(fh)
+        else:
+            q = out
+            if not (isinstance(q, np.ndarray) and q.dtype == np.float64 and q.flags["C_CONTIGUOUS"]
+                    and q.flags["WRITEABLE"] and q.size == fh.size):
+                raise contract_violation("out must be a writeable C-contiguous float64 array of f's size")
         sth = _status_array_np(ncells)
         st = ctx._lib.hk_collision_batch_host(ctx.h, kernel.h, fh.ctypes.data, q.ctypes.data,
                                               ncells, flags, sth.ctypes.data)
@@ -293,7 +299,13 @@ def spectral_collision(f, kernel: SpectralKernel, out=None, *, exact: bool = Fal
     if f.numel() % nb:
         raise contract_violation("f is not a whole number of velocity blocks")
     ncells = f.numel() // nb
-    q = out if out is not None else torch.empty_like(f)
+    if out is None:
+        q = torch.empty_like(f)
+    else:
+        q = out
+        if not (isinstance(q, torch.Tensor) and q.dtype == torch.float64 and q.is_contiguous()
+                and q.device == f.device and q.numel() == f.numel()):
+            raise contract_violation("out must be a contiguous float64 tensor of f's size on f's device")
     stt = torch.zeros(ncells * _abi.CELL_STATUS_BYTES // 8, dtype=torch.float64, device=f.device)
     st = ctx._lib.hk_collision_batch(ctx.h, kernel.h, f.data_ptr(), q.data_ptr(), ncells, flags,
                                      stt.data_ptr())

@@ -338,6 +338,22 @@ static bool stream_memops_available() {
     return state == 1;
 }
 
+// True when [p, p + bytes) is page-locked host memory (cudaHostAlloc /
+// cudaHostRegister / torch pin_memory): both ends are checked.
+static bool host_range_pinned(const void* p, size_t bytes) {
+    if (!p || !bytes) return false;
+    const void* ends[2] = {p, static_cast<const char*>(p) + bytes - 1};
+    for (const void* q : ends) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        if (a.type != cudaMemoryTypeHost) return false;
+    }
+    return true;
+}
+
 static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host, int64_t ncells,
                                    uint32_t flags, hk_cell_status* st_host) {
     if (!stream_memops_available()) return HK_UNSUPPORTED;
@@ -410,13 +426,17 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
         ctx->sio_in_ready = nullptr;
         ctx->sio_out_done = nullptr;
         ctx->sio_used = false;
-        if (!st && !streamed) {
-            // kernel variant without streamed I/O: release the waiting D2H stream by
-            // completing the counters, then let the caller redo the batch chunked.
-            for (int64_t c = 0; c < nch; ++c)
-                p_write_value32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
-            st = HK_UNSUPPORTED;
-        }
+        if (!st && !streamed) st = HK_UNSUPPORTED;  // kernel variant without streamed I/O: caller redoes it chunked
+    }
+    if (st) {
+        // Nothing (or not everything) will complete the out_done counters the D2H
+        // stream waits on: a failed enqueue, a failed launch, or a kernel that did
+        // not stream.  Complete them from the compute stream so s_out drains and
+        // the error is returned instead of blocking in the synchronise below.
+        for (int64_t c = 0; c < nch; ++c)
+            p_write_value32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
+        for (int64_t c = 0; c < nch; ++c)
+            p_write_value32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + c), 1u, 0);
     }
     // rerouted cells: their exact Q overwrote q_dev after the streamed copy
     int count = 0;
@@ -459,7 +479,13 @@ int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, doubl
             (st = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking), "stream")))
             return st;
     }
-    if (k->n == 32 && !(flags & (HK_COLL_EXACT | HK_COLL_STRICT)) && ncells >= 256 && !getenv("HK_NO_STREAMED_IO")) {
+    // The streamed path queues D2H copies behind device-side waits BEFORE the
+    // kernel that releases them is launched: a copy to pageable memory is
+    // synchronous with the host, so it would block here forever.  Streamed I/O
+    // therefore needs every host buffer page-locked; anything else is chunked.
+    if (k->n == 32 && !(flags & (HK_COLL_EXACT | HK_COLL_STRICT)) && ncells >= 256 &&
+        host_range_pinned(f_host, bytes) && host_range_pinned(q_host, bytes) &&
+        (!st_host || host_range_pinned(st_host, sizeof(hk_cell_status) * ncells))) {
         st = collision_host_streamed(ctx, k, f_host, q_host, ncells, flags, st_host);
         if (st != HK_UNSUPPORTED) return st;
         cudaStreamSynchronize(ctx->stream);

@@ -336,6 +336,9 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
                               const hk_hybrid_params* p, int64_t* counts) {
     if (!ctx || !k || !p) return HK_CONTRACT;
     if (nx < 1 || ny < 1) return fail(ctx, HK_CONTRACT, "hybrid step: empty grid");
+    // every argument check precedes the first launch: a rejected call leaves the state untouched
+    if (p->ghost_x < 0 || 2 * p->ghost_x >= nx)
+        return fail(ctx, HK_CONTRACT, "hybrid step: ghost_x must be in [0, nx / 2)");
     if (p->update_regimes && (!(p->eta0 > 0.0) || !(p->eta1 > 0.0) || !(p->delta0 > 0.0)))
         return fail(ctx, HK_CONFIG, "regime thresholds eta0, eta1, delta0 must be positive");
     cudaSetDevice(ctx->device);
@@ -393,7 +396,6 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     // ---- 2. conversion + the lists of the step ----
     convert_kernel<<<nblk(cells, 128), 128, 0, s>>>(cells, r_dev, r_new, hydro_dev, mom, hr, W, cnt);
     const int gx = p->ghost_x;
-    if (gx < 0 || 2 * gx >= nx) return fail(ctx, HK_CONTRACT, "hybrid step: ghost_x must be in [0, nx / 2)");
     list_new_kernel<<<1, kLT, 0, s>>>(nx, ny, r_dev, r_new, hydro_dev, hr, eps_dev, list, tmp2, eps_k, mlist, mmom, cnt,
                                       gx, tmp2b, tmp2c);
     ctx->launches += 2;

@@ -384,9 +384,16 @@ def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, 
     convert_on_transition, Euler TVD-RK2 on layer 0, PR(2,2,2) ES-BGK / penalized
     Boltzmann on layers 1 / 2 with the cross-layer transport halo."""
     ctx = kernel.ctx
-    for t, dt_ in ((r, torch.int8), (hydro, torch.float64), (f, torch.float64)):
-        assert t.is_cuda and t.dtype == dt_ and t.is_contiguous()
+    cells = nx * ny
+    for name, t, dt_, width in (("r", r, torch.int8, 1), ("hydro", hydro, torch.float64, 4),
+                                ("f", f, torch.float64, kernel.modes())):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dt_ and t.is_contiguous()):
+            raise contract_violation(f"hybrid_step: {name} must be a contiguous {dt_} CUDA tensor")
+        if t.numel() != cells * width:
+            raise contract_violation(f"hybrid_step: {name} has {t.numel()} elements, expected {cells * width}")
     e = eps_cell.to(device=f.device, dtype=torch.float64).contiguous()
+    if e.numel() != cells:
+        raise contract_violation(f"hybrid_step: eps_cell has {e.numel()} elements, expected {cells}")
     counts = (C.c_int64 * 6)()
     hp = params.to_c()
     ctx.check(ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),

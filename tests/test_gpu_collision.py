@@ -180,3 +180,33 @@ def test_n32_conservation_matches_reference_level(n32, hk):
         for phi in phis:
             ours, ref = float((q[c] * phi).sum()), float((n32["q_ref"][c] * phi).sum())
             assert abs(ours - ref) <= 1e-10 * scale, (c, ours, ref)
+
+
+@pytest.mark.timeout(300)
+def test_n32_pageable_host_buffers(hk):
+    """Pageable (not page-locked) host buffers at a streamed-path size: the
+    library must route them to the chunked path (a streamed D2H copy into
+    pageable memory would block the host before the kernel that releases it is
+    launched) and return the device path's Q bitwise."""
+    import torch
+    vg = hk.make_velocity_grid(32, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, 32, 8, 8, inputs.R_PHYS_MAX)
+    f = inputs.config2_cells_torch(300, 32, device="cuda")
+    q_dev = hk.spectral_collision(f, kern).cpu().numpy()
+    fh = np.ascontiguousarray(f.cpu().numpy())
+    q_host = hk.spectral_collision(fh, kern)
+    assert np.array_equal(q_host, q_dev)
+
+
+def test_out_argument_is_checked(hk):
+    import torch
+    vg = hk.make_velocity_grid(16, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, 16, 4, 8, inputs.R_PHYS_MAX)
+    f = inputs.config1_cells(2, 16)
+    with pytest.raises(hk.contract_violation):
+        hk.spectral_collision(f, kern, out=np.empty((1, 16 ** 3)))
+    with pytest.raises(hk.contract_violation):
+        hk.spectral_collision(f, kern, out=np.empty(f.shape, dtype=np.float32))
+    fd = torch.from_numpy(f).cuda()
+    with pytest.raises(hk.contract_violation):
+        hk.spectral_collision(fd, kern, out=torch.empty(16 ** 3, dtype=torch.float64, device="cuda"))
