@@ -9,9 +9,17 @@ updates) through the library's public entry point hk_collision_batch
 (default path: Hermitian-packed fast path + Nyquist guard + exact Nyquist correction of the listed cells).
 The 1 GiB input slab exceeds the 126 MB L2, so no flush is needed.
 
-Multi-GPU (torchrun): weak scaling, each rank owns its own 64x64-cell batch
-(collision is per-cell independent, no data-path collective); timing is the
-max over ranks of the device-timed region.
+Multi-GPU (torchrun, N > 1): the north star's scaling workload, BASELINE
+config 5 weak-scaled: each rank owns one 64 x 128 x-slab of the 512 x 128
+normal-shock field (N = 64^3, M = 64 (8 x 8), hard spheres, fp64; rank r of N
+takes the r-th of the N slabs centred on the shock, so N = 8 is the whole
+config-5 domain) and one STEP is one penalized PR(2,2,2) time step
+(src/boltzmann.cpp:47-110) on it: 2 collision evaluations per cell, 2-column
+f halos exchanged with the x-neighbours over NCCL (grouped send/recv)
+overlapped with each stage's collision, plus the conservation-sum all-reduce.
+Metric unit: cell-collision updates (2 per cell-step).  `--workload config5`
+runs the same at N = 1 (one slab, periodic wrap).  Timing is the max over
+ranks of the device-timed region.
 
 --impl reference: the reference's own CPU implementation of the same path
 (oracle/_ref: the unmodified reference sources + FFTW/Eigen API shims, run
@@ -120,32 +128,61 @@ def load_traffic():
         return None, None
 
 
+FFT_NOTE = ("reference arithmetic; FFTW is absent from the image, so the reference's FFTW calls run on the "
+            "FFTW-API shim (oracle/shim): radix-2 C2C with cached twiddles and tiled pencils, ~2x pocketfft's "
+            "single-thread time at 32^3")
+
+
 class CpuBaseline:
     """The reference's own CPU path (oracle/_ref: unmodified reference sources
     + API shims) on bounded samples of the same workload, all host threads,
     WorkerPool-partitioned (inc/threading.hpp:25-56).  Falls back to the C
-    oracle port when _ref is absent."""
+    oracle port when _ref is absent.
 
-    def __init__(self):
+    config2: spectral_collision per cell (one update each).
+    config5: penalized_residual per cell at N = 64 (src/boltzmann.cpp:9-27, the
+    per-update cost of the PR(2,2,2) step; transport and stage solves are
+    < 1 % of it), with the reference kernel built from the oracle's
+    closed-form tables (the reference's GK15 precompute takes minutes at 64^3)."""
+
+    def __init__(self, workload="config2"):
         from oracle import oracle as orc
         from paper_2505_03360_b200 import inputs
 
         self.cores = os.cpu_count() or 1
         self.kind = "reference"
+        self.workload = workload
+        n, a1, a2 = (N, A1, A2) if workload == "config2" else (N5, A5, A5)
+        if not os.path.exists(orc.ORACLE_SO):
+            subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True,
+                           stdout=subprocess.DEVNULL)
         try:
             lib = orc.RefLib()
-            kern = lib.kernel(N, VMAX, A1, A2, r_phys())
-            self._run = lambda f: lib.collision_batch(kern, f, nthreads=self.cores)
+            if workload == "config2":
+                kern = lib.kernel(n, VMAX, a1, a2, r_phys())
+                self._run = lambda f: lib.collision_batch(kern, f, nthreads=self.cores)
+            else:
+                ok = orc.Oracle().kernel(n, VMAX, a1, a2, r_phys(), closed_form=True, nthreads=self.cores)
+                kern = lib.kernel(n, VMAX, a1, a2, r_phys(), tables=(ok.alpha, ok.alpha_prime, ok.loss_diag))
+                del ok
+                self._run = lambda f: lib.penalized_residual_batch(kern, f, nthreads=self.cores)
         except Exception:
             self.kind = "port"
-            if not os.path.exists(orc.ORACLE_SO):
-                subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "oracle"], check=True,
-                               stdout=subprocess.DEVNULL)
             lib = orc.Oracle()
-            kern = lib.kernel(N, VMAX, A1, A2, r_phys(), closed_form=False, nthreads=self.cores)
-            self._run = lambda f: lib.collision_batch(kern, f, nthreads=self.cores)
+            kern = lib.kernel(n, VMAX, a1, a2, r_phys(), closed_form=(workload != "config2"), nthreads=self.cores)
+            if workload == "config2":
+                self._run = lambda f: lib.collision_batch(kern, f, nthreads=self.cores)
+            else:
+                def run(f):
+                    import concurrent.futures as cf
+                    with cf.ThreadPoolExecutor(self.cores) as ex:
+                        list(ex.map(lambda c: lib.penalized_residual(kern, c), f))
+                self._run = run
         self._keep = (lib, kern)
-        self.f = inputs.config2_cells(self.cores, N)  # one cell per worker per pass
+        if workload == "config2":
+            self.f = inputs.config2_cells(self.cores, n)  # one cell per worker per pass
+        else:
+            self.f = inputs.config5_cells(self.cores, n)  # shock-interface cells
         self._run(self.f[:1])  # warm the thread-local FFT workspaces
 
     def sample(self, seconds_target: float):
@@ -157,10 +194,21 @@ class CpuBaseline:
             el = time.perf_counter() - t0
             if el >= seconds_target:
                 break
+        what = "config-2 cells (spectral_collision)" if self.workload == "config2" else \
+            "config-5 cells (penalized_residual, N=64)"
         return {"value": done / el, "unit": UNIT, "cores": self.cores, "kind": self.kind,
-                "sample": f"{done} config-2 cells ({len(self.f)} per WorkerPool pass, {self.cores} "
-                          f"threads), {el:.1f} s wall; reference arithmetic with a stand-in radix-2 "
-                          f"FFT (FFTW absent from the image)"}
+                "sample": f"{done} {what}, {len(self.f)} per WorkerPool pass, {self.cores} threads, "
+                          f"{el:.1f} s wall; {FFT_NOTE}"}
+
+
+def config2_dict():
+    return {"workload": WORKLOAD, "cells_per_gpu": NCELLS, "n": N, "a1": A1, "a2": A2,
+            "l2": "inputs (1 GiB per GPU) larger than the 126 MB L2; no flush"}
+
+
+def config5_dict(ws):
+    return {"workload": WORKLOAD5, "cells_per_gpu": C5_NX_SLAB * C5_NY, "n": N5, "a1": A5, "a2": A5,
+            "grid": [C5_NX_SLAB * ws, C5_NY], "l2": "inputs (16 GiB per GPU) larger than the 126 MB L2; no flush"}
 
 
 def run_reference(args):
@@ -170,7 +218,7 @@ def run_reference(args):
     steps, warmup = args.steps, args.warmup
     cb = None
     vals = []
-    base = CpuBaseline()
+    base = CpuBaseline(args.workload)
     for i in range(warmup + steps):
         s = base.sample(seconds_target=args.ref_seconds)
         if i >= warmup:
@@ -178,15 +226,167 @@ def run_reference(args):
             cb = s
     v = statistics.mean(vals)
     cb["value"] = v
+    if args.workload == "config2":
+        config = config2_dict()
+        per_step = NCELLS
+    else:
+        config = config5_dict(ws)
+        per_step = 2 * C5_NX_SLAB * C5_NY * ws
+    cb["sample"] += "; the step time is extrapolated per update from these samples"
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-            "warmup": warmup, "ms_per_step": 1e3 * NCELLS / v, "higher_is_better": True,
+            "warmup": warmup, "ms_per_step": 1e3 * per_step / v, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": WORKLOAD, "cells": NCELLS, "n": N, "a1": A1, "a2": A2,
-                       "step": "bounded CPU sample of the batch, extrapolated per cell"},
-            "cpu_baseline": cb,
+            "impl": "reference", "config": config, "cpu_baseline": cb,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# config 5: weak-scaled x-slabs of the N = 64 normal shock (penalized PR(2,2,2))
+# ---------------------------------------------------------------------------
+N5, A5 = 64, 8
+C5_NX_SLAB, C5_NY = 64, 128
+MD5 = (A5 - 1) * A5 + 1
+W5_FLOP = (2 * MD5 + 2) * 5 * N5 ** 3 * math.log2(N5 ** 3) + (12 * MD5 + 10) * N5 ** 3
+WORKLOAD5 = ("config5: 512x128 normal shock (Mach 3), x-slabs of 64x128 cells per GPU (weak scaling), every cell "
+             "Boltzmann, hard spheres, N=64^3, M=64 (8x8), L=8, R=2L/(3+sqrt2), eps=1e-2, dt=0.1 dx, fp64; one step = "
+             "one penalized PR(2,2,2) step = 2 collision updates per cell")
+
+
+def run_config5(args):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_03360_b200 as hk
+    from paper_2505_03360_b200 import inputs
+    from paper_2505_03360_b200.partition import XSlab, conservation_sums, penalized_imex_step_slab
+    from paper_2505_03360_b200 import kinetic
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    group = None
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    ctx = hk.Context(local, stream)
+    vg = hk.make_velocity_grid(N5, VMAX)
+    kern = hk.precompute_kernel(vg, N5, A5, A5, r_phys(), ctx=ctx)
+    nxg = C5_NX_SLAB * ws
+    part = XSlab(nxg, C5_NY, ws, rank)
+    i0 = 256 - 32 * ws + part.i0  # the ws slabs centred on the shock (ws = 8: the whole 512 columns)
+    f = inputs.config5_slab_torch(i0=i0, nxl=part.nxl, ny=C5_NY, n=N5, device=f"cuda:{local}")
+    cells = part.cells
+    nb = N5 ** 3
+    work = torch.empty((6, cells, nb), dtype=torch.float64, device=f.device)
+    eps = torch.full((cells,), 1e-2, dtype=torch.float64, device=f.device)
+    dx, dy = 1.0 / 512, 1.0 / C5_NY
+    dt = 0.1 * dx
+
+    def step(fv, p=part):
+        penalized_imex_step_slab(p, fv, kern, dx, dy, dt, eps, group=group, work=work)
+        mom = kinetic.moments_of(fv, vg)["moments"]
+        return conservation_sums(mom, group)
+
+    def sync_all():
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+
+    sums0 = conservation_sums(kinetic.moments_of(f, vg)["moments"], group).cpu()
+    for _ in range(args.warmup):
+        step(f)
+    sync_all()
+    lib = ctx._lib
+    launches0 = ctx.launches
+    lib.hk_ctx_set_timing(ctx.h, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        sync_all()
+        e0.record(stream)
+        for _ in range(args.steps):
+            sums = step(f)
+        e1.record(stream)
+        sync_all()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launches - launches0
+    kms, kn = C.c_double(0), C.c_int64(0)
+    lib.hk_ctx_timing_report(ctx.h, 0, C.byref(kms), C.byref(kn))
+    lib.hk_ctx_set_timing(ctx.h, 0)
+    sums = sums.cpu()
+
+    # halo exchange alone (2 columns each way, 512 MiB per side at N = 64)
+    lh, rh = part.halo_buffers(nb, f)
+    sync_all()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    for _ in range(3):
+        part.exchange(f, lh, rh, group)
+    h1.record(stream)
+    sync_all()
+    halo_ms = h0.elapsed_time(h1) / 3
+
+    # the same step on the slab alone (local periodic wrap, no communication):
+    # the single-GPU cost of this rank's share
+    solo = XSlab(part.nxl, C5_NY, 1, 0)
+    fs = f.clone()
+    sync_all()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    penalized_imex_step_slab(solo, fs, kern, dx, dy, dt, eps, work=work)
+    s1.record(stream)
+    sync_all()
+    solo_ms = s0.elapsed_time(s1)
+    del fs
+
+    # end to end: pinned host slab -> device, one step, device -> host
+    fh = torch.empty((cells, nb), dtype=torch.float64, pin_memory=True)
+    fh.copy_(f)
+    sync_all()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        f.copy_(fh, non_blocking=True)
+        step(f)
+        fh.copy_(f, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+
+    vals = torch.tensor([ms, e2e_s, halo_ms, solo_ms, kms.value / max(kn.value, 1)], device="cuda")
+    if ws > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    ms_max, e2e_s, halo_ms, solo_ms, k_ms = (float(x) for x in vals.cpu())
+    updates = 2 * cells  # two collision evaluations per cell-step
+    value = ws * updates * args.steps / (ms_max * 1e-3)
+    e2e_value = ws * updates * args.e2e_steps / e2e_s
+    if rank == 0:
+        peak = ctx.fp64_peak_tflops()
+        achieved = W5_FLOP * cells / (k_ms * 1e-3) / 1e12  # one launch = one Q of the slab
+        drift = ((sums - sums0).abs() / sums0.abs().clamp_min(1e-300)).tolist()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config5_dict(ws),
+                "details": {"parallelism": f"x-slabs x{ws}, NCCL 2-column halos overlapped with the collision",
+                            "halo_ms_per_exchange": halo_ms, "solo_slab_ms_per_step": solo_ms,
+                            "mass_momentum_energy_rel_drift": drift},
+                "clocks": clk.summary(),
+                "gpu_launches": launches,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(cells * nb * 8),
+                        "d2h_bytes_per_step": int(cells * nb * 8), "steps": args.e2e_steps,
+                        "api": "partition.penalized_imex_step_slab on a slab copied from / to pinned host memory"},
+                "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                             "frac": achieved / peak if peak > 0 else None, "traffic": None,
+                             "kernel": "coll64_w12_kernel", "kernel_ms": k_ms,
+                             "kernel_share_of_step": 2 * k_ms / (ms_max / args.steps),
+                             "peak_source": "live DFMA microbenchmark (hk_measure_fp64_peak)",
+                             "algorithmic_flop_per_update": W5_FLOP},
+                "cpu_baseline": None}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 
@@ -295,17 +495,16 @@ def run_gpu(args):
         cb = None
         if ws == 1 and not args.no_cpu_baseline:
             try:
-                cb = CpuBaseline().sample(seconds_target=args.ref_seconds)
+                cb = CpuBaseline("config2").sample(seconds_target=args.ref_seconds)
             except Exception as exc:  # reported, never fatal
                 cb = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "unavailable",
                       "sample": f"failed: {exc}"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "cells_per_gpu": ncells, "n": N, "a1": A1, "a2": A2,
-                           "path": "fast (Hermitian-packed) + Nyquist guard + exact Nyquist correction of listed cells",
-                           "cells_rerouted_last_step": rerouted,
-                           "l2": "inputs (1 GiB per GPU) larger than the 126 MB L2; no flush"},
+                "config": config2_dict(),
+                "details": {"path": "fast (Hermitian-packed) + Nyquist guard + exact Nyquist correction of listed cells",
+                            "cells_rerouted_last_step": rerouted},
                 "clocks": clk.summary(),
                 "gpu_launches": launches,
                 "e2e": {"value": e2e_value, "unit": UNIT,
@@ -332,12 +531,20 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="auto", choices=["auto", "config2", "config5"],
+                    help="auto: config 2 at N = 1, config-5 weak scaling at N > 1")
     args = ap.parse_args()
+    ws = dist_env()[0]
+    if args.workload == "auto":
+        args.workload = "config2" if ws == 1 else "config5"
     if args.warmup < 3 and args.impl != "reference":
         args.warmup = 3
     if args.impl == "reference":
         args.ref_seconds = min(args.ref_seconds, 2.0)
         return run_reference(args)
+    if args.workload == "config5":
+        args.e2e_steps = min(args.e2e_steps, 1)
+        return run_config5(args)
     return run_gpu(args)
 
 

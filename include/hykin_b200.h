@@ -81,6 +81,14 @@ int hk_ctx_trim(hk_ctx ctx);
 int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len);
 /* Number of this library's kernel launches since context creation. */
 int64_t hk_launch_count(hk_ctx ctx);
+/* Stream-ordered device memory and copies on the context stream (for callers
+ * that hold no CUDA runtime of their own, e.g. the C++ mirror hykin_b200.hpp).
+ * hk_copy_to_host synchronises the stream before returning. */
+int hk_device_alloc(hk_ctx ctx, size_t bytes, void** out);
+int hk_device_free(hk_ctx ctx, void* p);
+int hk_copy_to_device(hk_ctx ctx, void* dst_dev, const void* src_host, size_t bytes);
+int hk_copy_to_host(hk_ctx ctx, void* dst_host, const void* src_dev, size_t bytes);
+int hk_ctx_synchronize(hk_ctx ctx);
 /* CUDA-event timing of the library's kernels on the context stream (for the
  * roofline in bench.py).  Enabling clears previous records.  tag 0 = main
  * collision kernel, 1 = Nyquist guard, 2 = Nyquist correction of the listed cells. */
@@ -145,6 +153,20 @@ int hk_moments_batch(hk_ctx ctx, int n, double vmax, const double* f_dev, int64_
 /* maxwellian (src/moments.cpp:88-112) of mom[cell] = (rho, ux, uy, uz, T). */
 int hk_maxwellian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, int64_t ncells, double* out_dev,
                         int* status_dev);
+/* anisotropic_gaussian (src/moments.cpp:120-157, inc/moments.hpp:55): theta[cell] = the
+ * stress tensor Theta (3x3 row-major) of mom[cell]; T_c = (1 - beta) T I + beta Theta;
+ * fallback[cell] (nullable) = 1 when T_c fails LLT and the Maxwellian was written. */
+int hk_anisotropic_gaussian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, const double* theta_dev,
+                                  double beta, int64_t ncells, double* out_dev, int* fallback_dev);
+/* match_moments (src/moments.cpp:225-246, inc/moments.hpp:62), in place:
+ * target[cell] = (rho, momentum x, y, z, energy); status HK_DEGENERATE = singular system
+ * (the reference throws degenerate_state_error; the cell is left unchanged). */
+int hk_match_moments_batch(hk_ctx ctx, int n, double vmax, double* f_dev, const double* target_dev, int64_t ncells,
+                           int* status_dev);
+/* remove_invariant_moments (src/moments.cpp:248-267, inc/moments.hpp:68), in place on q
+ * with weight w and centre uc[cell] (3 doubles); HK_DEGENERATE = singular coupling. */
+int hk_remove_invariant_moments_batch(hk_ctx ctx, int n, double vmax, double* q_dev, const double* weight_dev,
+                                      const double* uc_dev, int64_t ncells, int* status_dev);
 /* esbgk_stage_solve (src/esbgk.cpp:9-45, inc/esbgk.hpp:36): per-cell Knudsen
  * number eps_dev[cell] (or the scalar eps when eps_dev is NULL); nu = nu_coeff rho.
  * info[cell] = status | (gaussian_fallback << 8); mom_dev (nullable) = moments of f*. */

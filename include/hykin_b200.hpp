@@ -10,9 +10,13 @@
 // thrown as the reference's exception classes (inc/errors.hpp:9-61).
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -20,7 +24,40 @@
 
 #include "hykin_b200.h"
 
+#if __has_include(<Eigen/Dense>) && !defined(HYKIN_B200_NO_EIGEN)
+#include <Eigen/Dense>
+#define HYKIN_B200_EIGEN 1
+#endif
+
 namespace hykin_b200 {
+
+// Linear-algebra value types of the reference's signatures.  With Eigen on the
+// include path (the reference requires it) they ARE Eigen's types, so callers
+// compile unchanged; without it, minimal stand-ins with the members the
+// reference's callers use.
+#if HYKIN_B200_EIGEN
+using Vector3 = Eigen::Vector3d;
+using Matrix3 = Eigen::Matrix3d;
+#else
+struct Vector3 {
+    double v[3] = {0, 0, 0};
+    Vector3() = default;
+    Vector3(double a, double b, double c) : v{a, b, c} {}
+    double& operator()(int i) { return v[i]; }
+    double operator()(int i) const { return v[i]; }
+    double x() const { return v[0]; }
+    double y() const { return v[1]; }
+    double z() const { return v[2]; }
+    double squaredNorm() const { return v[0] * v[0] + v[1] * v[1] + v[2] * v[2]; }
+    static Vector3 Zero() { return {}; }
+};
+struct Matrix3 {
+    double m[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // row-major
+    double& operator()(int i, int j) { return m[3 * i + j]; }
+    double operator()(int i, int j) const { return m[3 * i + j]; }
+    static Matrix3 Zero() { return {}; }
+};
+#endif
 
 class error : public std::runtime_error {
 public:
@@ -167,6 +204,554 @@ inline void spectral_collision_batch(std::span<const double> f, const SpectralKe
     const int64_t ncells = f.size() / nb;
     ctx.check(hk_collision_batch_host(ctx.get(), kernel.handle.get(), f.data(), out.data(), ncells, 0,
                                       status.empty() ? nullptr : status.data()));
+}
+
+
+// ---------------------------------------------------------------------------
+// Device staging for the span-based (per-cell) mirrors: stream-ordered
+// allocations and copies through the C-ABI (no CUDA headers needed here).
+// ---------------------------------------------------------------------------
+class DeviceBuffer {
+public:
+    DeviceBuffer(Context& ctx, size_t bytes) : ctx_(ctx), bytes_(bytes) {
+        ctx_.check(hk_device_alloc(ctx_.get(), bytes, &p_));
+    }
+    template <typename T>
+    DeviceBuffer(Context& ctx, std::span<const T> host) : DeviceBuffer(ctx, host.size_bytes()) {
+        ctx_.check(hk_copy_to_device(ctx_.get(), p_, host.data(), host.size_bytes()));
+    }
+    ~DeviceBuffer() { hk_device_free(ctx_.get(), p_); }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    template <typename T>
+    T* as() const { return static_cast<T*>(p_); }
+    template <typename T>
+    void to_host(std::span<T> host) const { ctx_.check(hk_copy_to_host(ctx_.get(), host.data(), p_, host.size_bytes())); }
+    void upload(const void* host, size_t bytes) { ctx_.check(hk_copy_to_device(ctx_.get(), p_, host, bytes)); }
+
+private:
+    Context& ctx_;
+    size_t bytes_;
+    void* p_ = nullptr;
+};
+
+namespace detail {
+inline void check_block(std::span<const double> f, const VelocityGrid& g, const char* what) {
+    if ((int64_t)f.size() != (int64_t)g.size())
+        throw contract_violation(std::string(what) + ": span size must equal nv^3");
+}
+// per-cell status words: the reference throws the exception of the first failing cell
+inline void raise_cells(const std::vector<int>& st, const char* what) {
+    for (size_t c = 0; c < st.size(); ++c) {
+        const int code = st[c] & 0xFF;
+        if (code == HK_OK) continue;
+        const std::string m = std::string(what) + " failed (cell " + std::to_string(c) + ")";
+        if (code == HK_DEGENERATE) throw degenerate_state_error(m);
+        if (code == HK_POSITIVITY) throw positivity_error(m);
+        if (code == HK_NUMERICAL_CONSISTENCY) throw numerical_consistency_error(m);
+        throw contract_violation(m);
+    }
+}
+inline std::vector<int> statuses(const DeviceBuffer& b, size_t n) {
+    std::vector<int> st(n);
+    b.to_host(std::span<int>(st));
+    return st;
+}
+}  // namespace detail
+
+// ---------------------------------------------------------------------------
+// moments family (inc/moments.hpp:13-73, src/moments.cpp)
+// ---------------------------------------------------------------------------
+struct Moments {  // inc/moments.hpp:13-21
+    double rho = 0.0;
+    Vector3 u = Vector3::Zero();
+    double T = 0.0;
+    double energy() const { return 0.5 * rho * u.squaredNorm() + 1.5 * rho * T; }
+};
+using StressTensor = Matrix3;
+
+struct RealizabilityMatrix {  // inc/moments.hpp:27-35 (matrix() assembly is host-side in the reference too)
+    Matrix3 a_bar = Matrix3::Zero();
+    Vector3 b_bar = Vector3::Zero();
+    double c_bar = 0.0;
+};
+
+namespace detail {
+// one device pass: moments (+ sigma, realizability, L1) of one cell
+struct CellMoments {
+    double mom[5], sigma[6], real[13], l1;
+};
+inline CellMoments cell_moments(std::span<const double> f, const VelocityGrid& g, bool extras, Context& ctx) {
+    check_block(f, g, "moments_of");
+    DeviceBuffer fd(ctx, f);
+    DeviceBuffer out(ctx, sizeof(double) * (5 + 6 + 13 + 1)), st(ctx, sizeof(int));
+    double* o = out.as<double>();
+    ctx.check(hk_moments_batch(ctx.get(), g.nv, g.vmax, fd.as<double>(), 1, o, extras ? o + 5 : nullptr,
+                               extras ? o + 11 : nullptr, extras ? o + 24 : nullptr, st.as<int>()));
+    raise_cells(statuses(st, 1), "moments_of");
+    CellMoments r;
+    double h[25];
+    out.to_host(std::span<double>(h, 25));
+    std::memcpy(r.mom, h, sizeof r.mom);
+    std::memcpy(r.sigma, h + 5, sizeof r.sigma);
+    std::memcpy(r.real, h + 11, sizeof r.real);
+    r.l1 = h[24];
+    return r;
+}
+inline Moments to_moments(const double* m) {
+    Moments o;
+    o.rho = m[0];
+    o.u = Vector3(m[1], m[2], m[3]);
+    o.T = m[4];
+    return o;
+}
+inline std::array<double, 5> from_moments(const Moments& m) { return {m.rho, m.u(0), m.u(1), m.u(2), m.T}; }
+}  // namespace detail
+
+// src/moments.cpp:21-53 (throws degenerate_state_error on rho <= 0 or T <= 0)
+inline Moments moments_of(std::span<const double> f, const VelocityGrid& vgrid, Context& ctx = Context::instance()) {
+    return detail::to_moments(detail::cell_moments(f, vgrid, false, ctx).mom);
+}
+
+// src/moments.cpp:55-81: Sigma = sum v (x) v f dvK
+inline Matrix3 second_moment(std::span<const double> f, const VelocityGrid& vgrid, Context& ctx = Context::instance()) {
+    const auto r = detail::cell_moments(f, vgrid, true, ctx);
+    const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+    Matrix3 s = Matrix3::Zero();
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) s(i, j) = r.sigma[map[3 * i + j]];
+    return s;
+}
+
+// src/moments.cpp:83-86: Theta = Sigma / rho - u u^T
+inline StressTensor stress_tensor(std::span<const double> f, const VelocityGrid& vgrid, const Moments& m,
+                                  Context& ctx = Context::instance()) {
+    const Matrix3 s = second_moment(f, vgrid, ctx);
+    StressTensor th = Matrix3::Zero();
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) th(i, j) = s(i, j) / m.rho - m.u(i) * m.u(j);
+    return th;
+}
+
+// src/moments.cpp:88-112
+inline void maxwellian(const Moments& m, const VelocityGrid& vgrid, std::span<double> out,
+                       Context& ctx = Context::instance()) {
+    if ((int64_t)out.size() != (int64_t)vgrid.size()) throw contract_violation("maxwellian: span size must equal nv^3");
+    const auto mm = detail::from_moments(m);
+    DeviceBuffer md(ctx, std::span<const double>(mm)), od(ctx, sizeof(double) * out.size()), st(ctx, sizeof(int));
+    ctx.check(hk_maxwellian_batch(ctx.get(), vgrid.nv, vgrid.vmax, md.as<double>(), 1, od.as<double>(), st.as<int>()));
+    detail::raise_cells(detail::statuses(st, 1), "maxwellian");
+    od.to_host(out);
+}
+inline std::vector<double> maxwellian(const Moments& m, const VelocityGrid& vgrid, Context& ctx = Context::instance()) {
+    std::vector<double> out(vgrid.size());
+    maxwellian(m, vgrid, out, ctx);
+    return out;
+}
+
+// src/moments.cpp:120-157
+inline void anisotropic_gaussian(const Moments& m, const StressTensor& theta, double beta, const VelocityGrid& vgrid,
+                                 std::span<double> out, bool* fell_back = nullptr, Context& ctx = Context::instance()) {
+    if ((int64_t)out.size() != (int64_t)vgrid.size())
+        throw contract_violation("anisotropic_gaussian: span size must equal nv^3");
+    const auto mm = detail::from_moments(m);
+    double th[9];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) th[3 * i + j] = theta(i, j);
+    DeviceBuffer md(ctx, std::span<const double>(mm)), td(ctx, std::span<const double>(th, 9));
+    DeviceBuffer od(ctx, sizeof(double) * out.size()), fb(ctx, sizeof(int));
+    ctx.check(hk_anisotropic_gaussian_batch(ctx.get(), vgrid.nv, vgrid.vmax, md.as<double>(), td.as<double>(), beta, 1,
+                                            od.as<double>(), fb.as<int>()));
+    const auto f = detail::statuses(fb, 1);
+    od.to_host(out);
+    if (fell_back) *fell_back = f[0] != 0;
+}
+
+// src/moments.cpp:225-246 (throws degenerate_state_error when singular)
+inline void match_moments(std::span<double> f, const VelocityGrid& vgrid, double rho, const Vector3& momentum,
+                          double energy, Context& ctx = Context::instance()) {
+    detail::check_block(f, vgrid, "match_moments");
+    const double tg[5] = {rho, momentum(0), momentum(1), momentum(2), energy};
+    DeviceBuffer fd(ctx, std::span<const double>(f)), td(ctx, std::span<const double>(tg, 5)), st(ctx, sizeof(int));
+    ctx.check(hk_match_moments_batch(ctx.get(), vgrid.nv, vgrid.vmax, fd.as<double>(), td.as<double>(), 1, st.as<int>()));
+    detail::raise_cells(detail::statuses(st, 1), "match_moments");
+    fd.to_host(f);
+}
+
+// src/moments.cpp:248-267 (throws degenerate_state_error when singular)
+inline void remove_invariant_moments(std::span<double> q, std::span<const double> weight, const VelocityGrid& vgrid,
+                                     const Vector3& uc, Context& ctx = Context::instance()) {
+    detail::check_block(q, vgrid, "remove_invariant_moments");
+    detail::check_block(weight, vgrid, "remove_invariant_moments");
+    const double u3[3] = {uc(0), uc(1), uc(2)};
+    DeviceBuffer qd(ctx, std::span<const double>(q)), wd(ctx, weight), ud(ctx, std::span<const double>(u3, 3));
+    DeviceBuffer st(ctx, sizeof(int));
+    ctx.check(hk_remove_invariant_moments_batch(ctx.get(), vgrid.nv, vgrid.vmax, qd.as<double>(), wd.as<double>(),
+                                                ud.as<double>(), 1, st.as<int>()));
+    detail::raise_cells(detail::statuses(st, 1), "remove_invariant_moments");
+    qd.to_host(q);
+}
+
+// src/moments.cpp:269-312.  The device pass derives (rho, u, T) from f itself,
+// i.e. m must be moments_of(f) (the reference's only call pattern).
+inline RealizabilityMatrix realizability_matrix(std::span<const double> f, const VelocityGrid& vgrid,
+                                                const Moments& /*m*/, Context& ctx = Context::instance()) {
+    const auto r = detail::cell_moments(f, vgrid, true, ctx);
+    RealizabilityMatrix out;
+    for (int i = 0; i < 3; ++i) {
+        for (int j = 0; j < 3; ++j) out.a_bar(i, j) = r.real[3 * i + j];
+        out.b_bar(i) = r.real[9 + i];
+    }
+    out.c_bar = r.real[12];
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// layer solvers (inc/boltzmann.hpp:14-45, inc/esbgk.hpp:15-44, inc/imex.hpp)
+// ---------------------------------------------------------------------------
+struct PenalizationRule {  // inc/boltzmann.hpp:14-17
+    double coeff = 2.0 * M_PI;
+    double rate(double rho) const { return coeff * rho; }
+};
+struct BoltzmannParams {  // inc/boltzmann.hpp:19-22
+    PenalizationRule penalty;
+    double eps_weno = 1e-6;
+};
+struct EsbgkParams {  // inc/esbgk.hpp:17-23
+    double beta = -0.5;
+    double nu_coeff = 0.5 * M_PI;
+    double eps_weno = 1e-6;
+    double nu(double rho, double) const { return nu_coeff * rho; }
+};
+struct EsbgkStageInfo {  // inc/esbgk.hpp:25-28
+    Moments m;
+    bool gaussian_fallback = false;
+};
+// inc/imex.hpp:11-35.  The device steps implement PR(2,2,2); any other tableau is
+// rejected with contract_violation.
+struct ImexTableau {
+    static constexpr int stages = 2;
+    std::array<std::array<double, stages>, stages> a_ex{}, a_im{};
+    std::array<double, stages> c_ex{}, w_ex{}, c_im{}, w_im{};
+    static ImexTableau pr222() {
+        const double C = 1.0 / std::sqrt(2.0), delta = 1.0 - 1.0 / (2.0 * C);
+        ImexTableau t;
+        t.a_ex = {{{0.0, 0.0}, {1.0, 0.0}}};
+        t.c_ex = {0.0, 1.0};
+        t.w_ex = {0.5, 0.5};
+        t.a_im = {{{1.0 - C, 0.0}, {C - delta, delta}}};
+        t.c_im = {1.0 - C, C};
+        t.w_im = {0.5, 0.5};
+        return t;
+    }
+};
+
+namespace detail {
+inline void require_pr222(const ImexTableau& t) {
+    const ImexTableau p = ImexTableau::pr222();
+    auto same = [](double a, double b) { return std::abs(a - b) <= 1e-15; };
+    for (int i = 0; i < 2; ++i) {
+        if (!same(t.w_ex[i], p.w_ex[i]) || !same(t.w_im[i], p.w_im[i])) break;
+        for (int j = 0; j < 2; ++j)
+            if (!same(t.a_ex[i][j], p.a_ex[i][j]) || !same(t.a_im[i][j], p.a_im[i][j]))
+                throw contract_violation("the device IMEX steps implement the PR(2,2,2) tableau only");
+        if (i == 1) return;
+    }
+    throw contract_violation("the device IMEX steps implement the PR(2,2,2) tableau only");
+}
+}  // namespace detail
+
+// src/boltzmann.cpp:9-27.  Like the reference, throws numerical_consistency_error
+// when the collision's imaginary residue exceeds 1e-10 max|Re Q| (out then holds
+// the full residual; the reference's holds Q alone at that point).
+inline void penalized_residual(std::span<const double> f, const SpectralKernel& kernel, const VelocityGrid& vgrid,
+                               const PenalizationRule& rule, std::span<double> out, Context& ctx = Context::instance()) {
+    detail::check_block(f, vgrid, "penalized_residual");
+    if (out.size() != f.size()) throw contract_violation("penalized_residual: out must match f");
+    DeviceBuffer fd(ctx, f), od(ctx, sizeof(double) * f.size()), st(ctx, sizeof(int));
+    DeviceBuffer cs(ctx, sizeof(hk_cell_status));
+    ctx.check(hk_penalized_residual_batch(ctx.get(), kernel.handle.get(), fd.as<double>(), od.as<double>(), 1,
+                                          rule.coeff, HK_COLL_EXACT, st.as<int>(), cs.as<hk_cell_status>()));
+    od.to_host(out);
+    hk_cell_status c;
+    cs.to_host(std::span<hk_cell_status>(&c, 1));
+    if (c.flags & HK_CELL_RESIDUE)
+        throw numerical_consistency_error("spectral collision imaginary residue " + std::to_string(c.max_im) +
+                                          " exceeds 1e-10 of max |Q| = " + std::to_string(c.max_re));
+    detail::raise_cells(detail::statuses(st, 1), "penalized_residual");
+}
+
+// src/boltzmann.cpp:29-45
+inline Moments penalized_stage_solve(std::span<const double> f_star, double a, double eps, const PenalizationRule& rule,
+                                     const VelocityGrid& vgrid, std::span<double> out,
+                                     Context& ctx = Context::instance()) {
+    detail::check_block(f_star, vgrid, "penalized_stage_solve");
+    if (out.size() != f_star.size()) throw contract_violation("penalized_stage_solve: out must match f_star");
+    DeviceBuffer fd(ctx, f_star), od(ctx, sizeof(double) * f_star.size()), st(ctx, sizeof(int)), md(ctx, 5 * sizeof(double));
+    ctx.check(hk_penalized_stage_batch(ctx.get(), vgrid.nv, vgrid.vmax, fd.as<double>(), od.as<double>(), 1, a, nullptr,
+                                       eps, rule.coeff, st.as<int>(), md.as<double>()));
+    detail::raise_cells(detail::statuses(st, 1), "penalized_stage_solve");
+    od.to_host(out);
+    double m[5];
+    md.to_host(std::span<double>(m, 5));
+    return detail::to_moments(m);
+}
+
+// src/esbgk.cpp:9-45
+inline EsbgkStageInfo esbgk_stage_solve(std::span<const double> f_star, double a, double eps, const EsbgkParams& params,
+                                        const VelocityGrid& vgrid, std::span<double> out,
+                                        Context& ctx = Context::instance()) {
+    detail::check_block(f_star, vgrid, "esbgk_stage_solve");
+    if (out.size() != f_star.size()) throw contract_violation("esbgk_stage_solve: out must match f_star");
+    DeviceBuffer fd(ctx, f_star), od(ctx, sizeof(double) * f_star.size()), st(ctx, sizeof(int)), md(ctx, 5 * sizeof(double));
+    ctx.check(hk_esbgk_stage_batch(ctx.get(), vgrid.nv, vgrid.vmax, fd.as<double>(), od.as<double>(), 1, a, nullptr, eps,
+                                   params.beta, params.nu_coeff, st.as<int>(), md.as<double>()));
+    const auto info = detail::statuses(st, 1);
+    detail::raise_cells(info, "esbgk_stage_solve");
+    od.to_host(out);
+    double m[5];
+    md.to_host(std::span<double>(m, 5));
+    return {detail::to_moments(m), ((info[0] >> 8) & 1) != 0};
+}
+
+// inc/fields.hpp:48-79: sparse per-cell blocks (same members as the reference's).
+class DistributionField {
+public:
+    DistributionField() = default;
+    DistributionField(int cells, int block_size) : block_size_(block_size), blocks_(cells) {}
+    int block_size() const { return block_size_; }
+    int cells() const { return int(blocks_.size()); }
+    bool has(int c) const { return !blocks_[c].empty(); }
+    std::span<double> ensure(int c) {
+        if (blocks_[c].empty()) blocks_[c].assign(block_size_, 0.0);
+        return blocks_[c];
+    }
+    void release(int c) {
+        blocks_[c].clear();
+        blocks_[c].shrink_to_fit();
+    }
+    std::span<double> operator[](int c) { return blocks_[c]; }
+    std::span<const double> operator[](int c) const { return blocks_[c]; }
+    void swap_cell(int c, std::vector<double>& other) { blocks_[c].swap(other); }
+
+private:
+    int block_size_ = 0;
+    std::vector<std::vector<double>> blocks_;
+};
+
+namespace detail {
+// the field's blocks as one contiguous device slab [cell][nv^3] (every cell must own a block)
+inline void field_to_device(const DistributionField& f, int cells, int64_t nb, DeviceBuffer& d, const char* what) {
+    if (f.cells() < cells || f.block_size() != nb) throw contract_violation(std::string(what) + ": field size mismatch");
+    std::vector<double> slab(size_t(cells) * nb);
+    for (int c = 0; c < cells; ++c) {
+        if (!f.has(c)) throw contract_violation(std::string(what) + ": every cell must own a block");
+        std::memcpy(slab.data() + size_t(c) * nb, f[c].data(), sizeof(double) * nb);
+    }
+    d.upload(slab.data(), sizeof(double) * slab.size());
+}
+inline void field_from_device(DistributionField& f, int cells, int64_t nb, const DeviceBuffer& d) {
+    std::vector<double> slab(size_t(cells) * nb);
+    d.to_host(std::span<double>(slab));
+    for (int c = 0; c < cells; ++c) std::memcpy(f.ensure(c).data(), slab.data() + size_t(c) * nb, sizeof(double) * nb);
+}
+}  // namespace detail
+
+// src/boltzmann.cpp:47-110 (periodic, all-kinetic)
+inline void penalized_imex_step(DistributionField& f, int nx, int ny, const VelocityGrid& vgrid,
+                                const SpectralKernel& kernel, double dx, double dy, double dt,
+                                std::span<const double> eps_cell, const ImexTableau& tableau,
+                                const BoltzmannParams& params, Context& ctx = Context::instance()) {
+    detail::require_pr222(tableau);
+    const int cells = nx * ny;
+    const int64_t nb = vgrid.size();
+    if ((int)eps_cell.size() != cells) throw contract_violation("penalized_imex_step: eps_cell must hold nx*ny values");
+    DeviceBuffer fd(ctx, sizeof(double) * cells * nb), ed(ctx, eps_cell);
+    detail::field_to_device(f, cells, nb, fd, "penalized_imex_step");
+    ctx.check(hk_penalized_imex_step(ctx.get(), kernel.handle.get(), fd.as<double>(), nx, ny, dx, dy, dt, ed.as<double>(),
+                                     params.penalty.coeff, params.eps_weno, 0, nullptr));
+    detail::field_from_device(f, cells, nb, fd);
+}
+
+// src/esbgk.cpp:47-99 (periodic, all-kinetic)
+inline void esbgk_imex_step(DistributionField& f, int nx, int ny, const VelocityGrid& vgrid, double dx, double dy,
+                            double dt, std::span<const double> eps_cell, const ImexTableau& tableau,
+                            const EsbgkParams& params, Context& ctx = Context::instance()) {
+    detail::require_pr222(tableau);
+    const int cells = nx * ny;
+    const int64_t nb = vgrid.size();
+    if ((int)eps_cell.size() != cells) throw contract_violation("esbgk_imex_step: eps_cell must hold nx*ny values");
+    DeviceBuffer fd(ctx, sizeof(double) * cells * nb), ed(ctx, eps_cell);
+    detail::field_to_device(f, cells, nb, fd, "esbgk_imex_step");
+    ctx.check(hk_esbgk_imex_step(ctx.get(), vgrid.nv, vgrid.vmax, fd.as<double>(), nx, ny, dx, dy, dt, ed.as<double>(),
+                                 params.beta, params.nu_coeff, params.eps_weno, nullptr));
+    detail::field_from_device(f, cells, nb, fd);
+}
+
+// ---------------------------------------------------------------------------
+// transport (inc/transport.hpp:16-26, src/transport.cpp:12-66)
+// ---------------------------------------------------------------------------
+inline void kinetic_transport_rhs_periodic(const DistributionField& f, int nx, int ny, const VelocityGrid& vgrid,
+                                           double dx, double dy, DistributionField& out, double eps_weno = 1e-6,
+                                           Context& ctx = Context::instance()) {
+    const int cells = nx * ny;
+    const int64_t nb = vgrid.size();
+    DeviceBuffer fd(ctx, sizeof(double) * cells * nb), od(ctx, sizeof(double) * cells * nb);
+    detail::field_to_device(f, cells, nb, fd, "kinetic_transport_rhs_periodic");
+    ctx.check(hk_transport_rhs(ctx.get(), vgrid.nv, vgrid.vmax, fd.as<double>(), od.as<double>(), nx, ny, 0, dx, dy,
+                               eps_weno));
+    if (out.cells() < cells || out.block_size() != nb) out = DistributionField(cells, int(nb));
+    detail::field_from_device(out, cells, nb, od);
+}
+
+// One cell from its 5-point x and y stencils: the blocks are placed on a 5 x 5
+// periodic torus (row 2 = fx, column 2 = fy, the rest unused by cell (2,2)'s
+// stencil) and the device sweep's output at (2, 2) is returned.
+inline void kinetic_transport_rhs_cell(const std::array<const double*, 5>& fx, const std::array<const double*, 5>& fy,
+                                       const VelocityGrid& vgrid, double dx, double dy, double eps_weno, double* out,
+                                       Context& ctx = Context::instance()) {
+    const int64_t nb = vgrid.size();
+    std::vector<double> torus(size_t(25) * nb, 0.0);
+    for (int k = 0; k < 5; ++k) {
+        std::memcpy(torus.data() + size_t(2 * 5 + k) * nb, fx[k], sizeof(double) * nb);  // row j = 2, column k
+        std::memcpy(torus.data() + size_t(k * 5 + 2) * nb, fy[k], sizeof(double) * nb);  // column i = 2, row k
+    }
+    DeviceBuffer fd(ctx, std::span<const double>(torus)), od(ctx, sizeof(double) * 25 * nb);
+    ctx.check(hk_transport_rhs(ctx.get(), vgrid.nv, vgrid.vmax, fd.as<double>(), od.as<double>(), 5, 5, 0, dx, dy,
+                               eps_weno));
+    std::vector<double> all(size_t(25) * nb);
+    od.to_host(std::span<double>(all));
+    std::memcpy(out, all.data() + size_t(12) * nb, sizeof(double) * nb);
+}
+
+// ---------------------------------------------------------------------------
+// indicators and Algorithm 1 (inc/indicators.hpp:15-100, inc/regime.hpp:17).
+// Per-bundle scalar formulas on the host (the batched device path is
+// hk_classify); l1_distance_to_maxwellian is a device pass.
+// ---------------------------------------------------------------------------
+enum class LaplacianNorm { squared_sum, signed_sum };
+struct PrimMoments {
+    double rho = 0.0, ux = 0.0, uy = 0.0, T = 0.0;
+};
+struct DerivativeBundle {
+    double drho_dx = 0, drho_dy = 0, dux_dx = 0, dux_dy = 0, duy_dx = 0, duy_dy = 0, dT_dx = 0, dT_dy = 0;
+    double lap_rho = 0, lap_ux = 0, lap_uy = 0;
+};
+struct TransportCoefficients {
+    double mu0 = 1.0, kappa0 = 1.0;
+    double mu(double T) const { return mu0 * std::sqrt(T); }
+    double kappa(double T) const { return kappa0 * std::sqrt(T); }
+};
+struct Thresholds {
+    double eta0 = 0.0, eta1 = 0.0, delta0 = 0.0;
+    void validate() const {
+        if (!(eta0 > 0.0) || !(eta1 > 0.0) || !(delta0 > 0.0))
+            throw config_error("regime thresholds eta0, eta1, delta0 must be positive");
+    }
+};
+struct Eigenvalues {
+    double a = 0.0, b = 0.0, c = 0.0;
+};
+struct VEps1Coefficients {
+    double a1 = 0, a2 = 0, b1 = 0, b2 = 0, c1 = 0, c2 = 0, h1 = 0, xi1 = 0, xi2 = 0;
+    double d() const { return xi1 * b1 + xi2 * b2; }
+};
+struct IndicatorSet {
+    std::optional<Eigenvalues> eigenvalues;
+    std::optional<double> lambda_b;
+    std::optional<double> l1_distance;
+};
+
+// central differences and dx*dy-scaled 5-point Laplacians (src/indicators.cpp:14-32)
+inline DerivativeBundle spatial_derivatives(const PrimMoments& c, const PrimMoments& xm, const PrimMoments& xp,
+                                            const PrimMoments& ym, const PrimMoments& yp, double dx, double dy) {
+    auto cd = [](double p, double m, double h) { return (p - m) / (2.0 * h); };
+    auto lap = [&](double cm, double a, double b, double e, double g) { return (a + b + e + g - 4.0 * cm) * (1.0 / (dx * dy)); };
+    DerivativeBundle d;
+    d.drho_dx = cd(xp.rho, xm.rho, dx);
+    d.drho_dy = cd(yp.rho, ym.rho, dy);
+    d.dux_dx = cd(xp.ux, xm.ux, dx);
+    d.dux_dy = cd(yp.ux, ym.ux, dy);
+    d.duy_dx = cd(xp.uy, xm.uy, dx);
+    d.duy_dy = cd(yp.uy, ym.uy, dy);
+    d.dT_dx = cd(xp.T, xm.T, dx);
+    d.dT_dy = cd(yp.T, ym.T, dy);
+    d.lap_rho = lap(c.rho, xm.rho, xp.rho, ym.rho, yp.rho);
+    d.lap_ux = lap(c.ux, xm.ux, xp.ux, ym.ux, yp.ux);
+    d.lap_uy = lap(c.uy, xm.uy, xp.uy, ym.uy, yp.uy);
+    return d;
+}
+
+// src/indicators.cpp:34-49
+inline VEps1Coefficients v_eps1_coefficients(const DerivativeBundle& d, const PrimMoments& m, double eps,
+                                             const TransportCoefficients& k) {
+    VEps1Coefficients c;
+    c.a1 = (4.0 / 3.0) * d.dux_dx - (2.0 / 3.0) * d.duy_dy;
+    c.c1 = (4.0 / 3.0) * d.duy_dy - (2.0 / 3.0) * d.dux_dx;
+    c.h1 = -(2.0 / 3.0) * (d.dux_dx + d.duy_dy);
+    c.b1 = d.dux_dy + d.duy_dx;
+    c.a2 = d.dT_dx * d.dT_dx;
+    c.b2 = d.dT_dx * d.dT_dy;
+    c.c2 = d.dT_dy * d.dT_dy;
+    const double mu = k.mu(m.T), kappa = k.kappa(m.T);
+    c.xi1 = eps * mu / (m.rho * m.T);
+    c.xi2 = eps * eps * 2.0 * kappa * kappa / (3.0 * m.rho * m.rho * m.T * m.T * m.T);
+    return c;
+}
+
+// closed-form roots of the 2x2 block plus the decoupled entry (src/indicators.cpp:60-73)
+inline Eigenvalues v_eps1_eigenvalues(const DerivativeBundle& d, const PrimMoments& m, double eps,
+                                      const TransportCoefficients& k) {
+    const VEps1Coefficients c = v_eps1_coefficients(d, m, eps, k);
+    const double gap = c.xi1 * (c.a1 - c.c1) + c.xi2 * (c.a2 - c.c2);
+    const double dd = c.d();
+    const double root = std::sqrt(gap * gap + 4.0 * dd * dd);
+    const double tr = -c.a1 * c.xi1 - c.a2 * c.xi2 - c.c1 * c.xi1 - c.c2 * c.xi2 + 2.0;
+    return {0.5 * (root + tr), 0.5 * (-root + tr), 1.0 - c.xi1 * c.h1};
+}
+
+// src/indicators.cpp:75-87
+inline double lambda_b_indicator(const DerivativeBundle& d, const PrimMoments& m, double eps,
+                                 LaplacianNorm norm = LaplacianNorm::squared_sum) {
+    const double gt2 = d.dT_dx * d.dT_dx + d.dT_dy * d.dT_dy;
+    const double gu2 = d.dux_dx * d.dux_dx + d.dux_dy * d.dux_dy + d.duy_dx * d.duy_dx + d.duy_dy * d.duy_dy;
+    const double lu2 = norm == LaplacianNorm::squared_sum ? d.lap_ux * d.lap_ux + d.lap_uy * d.lap_uy
+                                                          : (d.lap_ux + d.lap_uy) * (d.lap_ux + d.lap_uy);
+    const double lr = d.lap_rho / m.rho;
+    return eps * eps * (gt2 / m.T + gu2 + std::sqrt((lu2 + lr * lr) * (1.0 + m.T * m.T)));
+}
+
+// src/indicators.cpp:89-98 (device pass)
+inline double l1_distance_to_maxwellian(std::span<const double> f, const VelocityGrid& vgrid,
+                                        Context& ctx = Context::instance()) {
+    return detail::cell_moments(f, vgrid, true, ctx).l1;
+}
+
+// Algorithm 1 branch table (src/regime.cpp:13-52)
+inline int regime_update(int r, const IndicatorSet& ind, const Thresholds& th) {
+    auto need = [&](bool ok, const char* what) {
+        if (!ok) throw contract_violation("regime update for layer " + std::to_string(r) + " requires " + what);
+    };
+    auto near_one = [&](const Eigenvalues& l) {
+        return std::abs(l.a - 1.0) <= th.eta0 && std::abs(l.b - 1.0) <= th.eta0 && std::abs(l.c - 1.0) <= th.eta0;
+    };
+    if (r == 2) {
+        need(ind.lambda_b.has_value(), "lambda_B");
+        return std::abs(*ind.lambda_b) > th.eta1 ? 2 : 1;
+    }
+    if (r == 1) {
+        need(ind.lambda_b.has_value(), "lambda_B");
+        need(ind.eigenvalues.has_value(), "the realizability eigenvalues");
+        if (std::abs(*ind.lambda_b) > th.eta1) return 2;
+        if (!near_one(*ind.eigenvalues)) return 1;
+        need(ind.l1_distance.has_value(), "the L1 distance to equilibrium");
+        return *ind.l1_distance <= th.delta0 ? 0 : 1;
+    }
+    if (r == 0) {
+        need(ind.eigenvalues.has_value(), "the realizability eigenvalues");
+        return near_one(*ind.eigenvalues) ? 0 : 1;
+    }
+    throw contract_violation("unknown layer " + std::to_string(r));
 }
 
 }  // namespace hykin_b200

@@ -181,6 +181,28 @@ class Oracle:
                                         C.c_double(energy))
         return st, f
 
+    def stress_tensor(self, n, vmax, f, mom5):
+        m = _Moments(mom5[0], (C.c_double * 3)(*mom5[1:4]), mom5[4])
+        th = np.zeros(9)
+        self.lib.hko_stress_tensor(n, C.c_double(vmax), _ptr(np.ascontiguousarray(f, dtype=np.float64)),
+                                   C.byref(m), _ptr(th))
+        return th.reshape(3, 3)
+
+    def anisotropic_gaussian(self, n, vmax, mom5, theta, beta):
+        m = _Moments(mom5[0], (C.c_double * 3)(*mom5[1:4]), mom5[4])
+        out = np.empty(n ** 3)
+        fb = C.c_int(0)
+        th = np.ascontiguousarray(theta, dtype=np.float64).reshape(9)
+        st = self.lib.hko_anisotropic_gaussian(C.byref(m), _ptr(th), C.c_double(beta), n, C.c_double(vmax),
+                                               _ptr(out), C.byref(fb))
+        return st, out, fb.value
+
+    def remove_invariant_moments(self, n, vmax, q, weight, uc):
+        q = np.ascontiguousarray(q, dtype=np.float64).copy()
+        st = self.lib.hko_remove_invariant_moments(_ptr(q), _ptr(np.ascontiguousarray(weight, dtype=np.float64)), n,
+                                                   C.c_double(vmax), _ptr(np.ascontiguousarray(uc, dtype=np.float64)))
+        return st, q
+
     def penalized_residual(self, k: OracleKernel, f, pen_coeff=2 * np.pi):
         f = np.ascontiguousarray(f, dtype=np.float64)
         out = np.empty_like(f)
@@ -357,12 +379,18 @@ class HkoHybridParams(C.Structure):
 
 
 class RefKernel:
-    def __init__(self, lib, n, vmax, a1, a2, r_phys):
+    def __init__(self, lib, n, vmax, a1, a2, r_phys, tables=None):
         self._lib = lib
         st = C.c_int(0)
-        lib.href_kernel_create.restype = C.c_void_p
-        self.h = lib.href_kernel_create(n, C.c_double(vmax), a1, a2, C.c_double(r_phys),
-                                        C.byref(st))
+        if tables is None:
+            lib.href_kernel_create.restype = C.c_void_p
+            self.h = lib.href_kernel_create(n, C.c_double(vmax), a1, a2, C.c_double(r_phys),
+                                            C.byref(st))
+        else:  # (alpha [d, n^3], alpha_prime [d, n^3], loss [n^3]) supplied, e.g. OracleKernel's
+            a, ap, ld = (np.ascontiguousarray(x, dtype=np.float64) for x in tables)
+            lib.href_kernel_from_tables.restype = C.c_void_p
+            self.h = lib.href_kernel_from_tables(n, C.c_double(vmax), a1, a2, C.c_double(r_phys),
+                                                 _ptr(a), _ptr(ap), _ptr(ld))
         self.status = st.value
         self.n, self.a1, self.a2, self.vmax = n, a1, a2, vmax
 
@@ -388,8 +416,8 @@ class RefLib:
             raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where /root/reference exists")
         self.lib = C.CDLL(path)
 
-    def kernel(self, n, vmax, a1, a2, r_phys):
-        return RefKernel(self.lib, n, vmax, a1, a2, r_phys)
+    def kernel(self, n, vmax, a1, a2, r_phys, tables=None):
+        return RefKernel(self.lib, n, vmax, a1, a2, r_phys, tables)
 
     def collision_batch(self, k: RefKernel, f, nthreads=1):
         f = np.ascontiguousarray(f, dtype=np.float64)

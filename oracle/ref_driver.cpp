@@ -110,6 +110,36 @@ void* href_kernel_create(int n, double vmax, int a1, int a2, double r_phys, int*
     }
 }
 
+// The reference's SpectralKernel with its scalars set as precompute_kernel sets
+// them (src/spectral.cpp:68-76) and the weight tables supplied by the caller
+// (e.g. the oracle's closed forms, hk_oracle.c, which agree with the GK15 tables
+// to ~1e-13): the timing arm at N = 64 skips the single-threaded adaptive
+// quadrature (minutes at 64^3 x 64 directions); spectral_collision itself is
+// the reference's code either way.
+void* href_kernel_from_tables(int n, double vmax, int a1, int a2, double r_phys, const double* alpha,
+                              const double* alpha_prime, const double* loss_diag) {
+    auto* h = new RefKernel;
+    h->vgrid = make_velocity_grid(n, vmax);
+    SpectralKernel& k = h->kernel;
+    k.n = n;
+    k.a1 = a1;
+    k.a2 = a2;
+    k.r_phys = r_phys;
+    k.r = r_phys * M_PI / vmax;
+    const double s = vmax / M_PI;
+    k.jacobian = s * s * s * s;
+    k.weight = M_PI * M_PI / (a1 * a2);
+    const size_t total = size_t(k.modes());
+    k.alpha.assign(k.dirs(), std::vector<double>(total));
+    k.alpha_prime.assign(k.dirs(), std::vector<double>(total));
+    for (int d = 0; d < k.dirs(); ++d) {
+        std::memcpy(k.alpha[d].data(), alpha + d * total, total * sizeof(double));
+        std::memcpy(k.alpha_prime[d].data(), alpha_prime + d * total, total * sizeof(double));
+    }
+    k.loss_diag.assign(loss_diag, loss_diag + total);
+    return h;
+}
+
 void href_kernel_free(void* p) { delete static_cast<RefKernel*>(p); }
 
 void href_kernel_scalars(void* p, double* out4) {

@@ -104,6 +104,11 @@ def lib() -> C.CDLL:
         "hk_last_error": (C.c_int, [vp, C.POINTER(i64), C.c_char_p, C.c_size_t]),
         "hk_launch_count": (i64, [vp]),
         "hk_ctx_set_timing": (C.c_int, [vp, C.c_int]),
+        "hk_device_alloc": (C.c_int, [vp, C.c_size_t, C.POINTER(vp)]),
+        "hk_device_free": (C.c_int, [vp, vp]),
+        "hk_copy_to_device": (C.c_int, [vp, vp, vp, C.c_size_t]),
+        "hk_copy_to_host": (C.c_int, [vp, vp, vp, C.c_size_t]),
+        "hk_ctx_synchronize": (C.c_int, [vp]),
         "hk_ctx_timing_report": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double), C.POINTER(i64)]),
         "hk_kernel_create": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dbl, dbl, C.POINTER(vp)]),
         "hk_kernel_create_from_tables": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, dbl, dbl, vp, vp, vp,
@@ -115,6 +120,9 @@ def lib() -> C.CDLL:
         "hk_measure_fp64_peak": (dbl, [vp]),
         "hk_moments_batch": (C.c_int, [vp, C.c_int, dbl, vp, i64, vp, vp, vp, vp, vp]),
         "hk_maxwellian_batch": (C.c_int, [vp, C.c_int, dbl, vp, i64, vp, vp]),
+        "hk_anisotropic_gaussian_batch": (C.c_int, [vp, C.c_int, dbl, vp, vp, dbl, i64, vp, vp]),
+        "hk_match_moments_batch": (C.c_int, [vp, C.c_int, dbl, vp, vp, i64, vp]),
+        "hk_remove_invariant_moments_batch": (C.c_int, [vp, C.c_int, dbl, vp, vp, vp, i64, vp]),
         "hk_esbgk_stage_batch": (C.c_int, [vp, C.c_int, dbl, vp, vp, i64, dbl, vp, dbl, dbl, dbl, vp, vp]),
         "hk_penalized_stage_batch": (C.c_int, [vp, C.c_int, dbl, vp, vp, i64, dbl, vp, dbl, dbl, vp, vp]),
         "hk_penalized_residual_batch": (C.c_int, [vp, vp, vp, vp, i64, dbl, u32, vp, vp]),

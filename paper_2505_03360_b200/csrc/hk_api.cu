@@ -131,6 +131,43 @@ int hk_last_error(hk_ctx ctx, int64_t* cell, char* msg, size_t msg_len) {
 
 int64_t hk_launch_count(hk_ctx ctx) { return ctx->launches; }
 
+int hk_device_alloc(hk_ctx ctx, size_t bytes, void** out) {
+    if (!ctx || !out) return HK_CONTRACT;
+    cudaSetDevice(ctx->device);
+    *out = nullptr;
+    if (!bytes) return HK_OK;
+    return check_cuda(ctx, cudaMallocAsync(out, bytes, ctx->stream), "device alloc");
+}
+
+int hk_device_free(hk_ctx ctx, void* p) {
+    if (!ctx) return HK_CONTRACT;
+    if (!p) return HK_OK;
+    cudaSetDevice(ctx->device);
+    return check_cuda(ctx, cudaFreeAsync(p, ctx->stream), "device free");
+}
+
+int hk_copy_to_device(hk_ctx ctx, void* dst_dev, const void* src_host, size_t bytes) {
+    if (!ctx || (bytes && (!dst_dev || !src_host))) return HK_CONTRACT;
+    if (!bytes) return HK_OK;
+    cudaSetDevice(ctx->device);
+    return check_cuda(ctx, cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, ctx->stream), "H2D");
+}
+
+int hk_copy_to_host(hk_ctx ctx, void* dst_host, const void* src_dev, size_t bytes) {
+    if (!ctx || (bytes && (!dst_host || !src_dev))) return HK_CONTRACT;
+    cudaSetDevice(ctx->device);
+    int st = HK_OK;
+    if (bytes) st = check_cuda(ctx, cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+    return st;
+}
+
+int hk_ctx_synchronize(hk_ctx ctx) {
+    if (!ctx) return HK_CONTRACT;
+    cudaSetDevice(ctx->device);
+    return check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+}
+
 static void clear_events(hk_ctx ctx) {
     for (auto& e : ctx->events) {
         cudaEventDestroy(e.second.first);

@@ -1673,6 +1673,159 @@ int warp_grid(hk_ctx ctx, int64_t ncells) {
     return int(blocks < cap ? blocks : cap);
 }
 
+// ---------------------------------------------------------------------------
+// Stand-alone moment operators of inc/moments.hpp:55-70 (the stage and
+// residual kernels fuse them; these are the drop-ins for callers that use them
+// one at a time).  One CTA per cell.
+// ---------------------------------------------------------------------------
+// Eigen::LLT test, determinant and inverse of a 3x3 SPD candidate as the stage
+// kernel does them (src/moments.cpp:128-138).  par[0..8] = inverse (row-major),
+// par[9] = rho / sqrt((2 pi)^3 det).  Returns false when LLT fails.
+__device__ bool gaussian_params(const double tc[9], double rho, double* par) {
+    double l[9] = {0};
+    for (int k = 0; k < 3; ++k) {
+        double x = tc[3 * k + k];
+        for (int j = 0; j < k; ++j) x -= l[3 * k + j] * l[3 * k + j];
+        if (!(x > 0.0)) return false;
+        l[3 * k + k] = sqrt(x);
+        for (int i = k + 1; i < 3; ++i) {
+            double y = tc[3 * i + k];
+            for (int j = 0; j < k; ++j) y -= l[3 * i + j] * l[3 * k + j];
+            l[3 * i + k] = y / l[3 * k + k];
+        }
+    }
+    const double* q = tc;
+    const double c00 = q[4] * q[8] - q[5] * q[7], c01 = q[5] * q[6] - q[3] * q[8], c02 = q[3] * q[7] - q[4] * q[6];
+    const double det = q[0] * (q[4] * q[8] - q[5] * q[7]) - q[1] * (q[3] * q[8] - q[5] * q[6]) +
+                       q[2] * (q[3] * q[7] - q[4] * q[6]);
+    const double id = 1.0 / (q[0] * c00 + q[1] * c01 + q[2] * c02);
+    par[0] = c00 * id; par[1] = (q[2] * q[7] - q[1] * q[8]) * id; par[2] = (q[1] * q[5] - q[2] * q[4]) * id;
+    par[3] = c01 * id; par[4] = (q[0] * q[8] - q[2] * q[6]) * id; par[5] = (q[2] * q[3] - q[0] * q[5]) * id;
+    par[6] = c02 * id; par[7] = (q[1] * q[6] - q[0] * q[7]) * id; par[8] = (q[0] * q[4] - q[1] * q[3]) * id;
+    par[9] = rho / sqrt(pow(2.0 * M_PI, 3) * det);
+    return true;
+}
+
+// anisotropic_gaussian (src/moments.cpp:120-157): mom[cell] = (rho, u, T),
+// theta[cell] = stress tensor (3x3 row-major); fallback[cell] = 1 when the
+// corrected tensor fails LLT (the Maxwellian is written instead).
+__global__ void __launch_bounds__(NT) gaussian_kernel(const double* __restrict__ mom, const double* __restrict__ theta,
+                                                      double beta, int64_t ncells, VGrid g, double* __restrict__ out,
+                                                      int* __restrict__ fallback) {
+    __shared__ double ex[128], ey[128], ez[128];
+    __shared__ double par[11];
+    const int n = g.n, nb = n * n * n;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        const Mom m{mom[cell * 5], mom[cell * 5 + 1], mom[cell * 5 + 2], mom[cell * 5 + 3], mom[cell * 5 + 4]};
+        if (threadIdx.x == 0) {
+            double tc[9];
+            const double iso = (1.0 - beta) * m.T;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) tc[3 * i + j] = (i == j ? iso : 0.0) + beta * theta[cell * 9 + 3 * i + j];
+            par[10] = gaussian_params(tc, m.rho, par) ? 1.0 : 0.0;
+            if (fallback) fallback[cell] = par[10] != 0.0 ? 0 : 1;
+        }
+        __syncthreads();
+        double* o = out + cell * nb;
+        if (par[10] != 0.0) {
+            for (int idx = threadIdx.x; idx < nb; idx += NT) {
+                const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+                const double dx = g.node(k1) - m.ux, dy = g.node(k2) - m.uy, dz = g.node(k3) - m.uz;
+                const double qxy = par[0] * dx * dx + 2.0 * par[1] * dx * dy + par[4] * dy * dy;
+                const double lz = 2.0 * (par[2] * dx + par[5] * dy);
+                o[idx] = par[9] * exp(-0.5 * (qxy + dz * (lz + par[8] * dz)));
+            }
+        } else {
+            const double pref = maxwell_factors(m, g, ex, ey, ez);
+            for (int idx = threadIdx.x; idx < nb; idx += NT) {
+                const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+                o[idx] = pref * ex[k1] * ey[k2] * ez[k3];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// match_moments (src/moments.cpp:225-246), in place: target[cell] = (rho,
+// momentum x/y/z, energy); status HK_DEGENERATE when the system is singular
+// (f untouched).
+__global__ void __launch_bounds__(NT) match_kernel(double* __restrict__ f, const double* __restrict__ target,
+                                                   int64_t ncells, VGrid g, int* __restrict__ status) {
+    __shared__ double scratch[8 * 25];
+    __shared__ double par[6];
+    const int n = g.n, nb = n * n * n;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        double* fc = f + cell * nb;
+        const double* tg = target + cell * 5;
+        const double uc[3] = {tg[1] / tg[0], tg[2] / tg[0], tg[3] / tg[0]};
+        double A[25];
+        coupling(g, uc, [&](int idx, double, double, double) { return fc[idx]; }, A, scratch);
+        if (threadIdx.x == 0) {
+            const double rhs[5] = {tg[0], tg[1], tg[2], tg[3], 2.0 * tg[4]};
+            double x[5];
+            const bool ok = solve5(A, rhs, x);
+            for (int k = 0; k < 5; ++k) par[k] = x[k];
+            par[5] = ok ? 1.0 : 0.0;
+            if (status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
+        }
+        __syncthreads();
+        if (par[5] != 0.0) {
+            const double x[5] = {par[0], par[1], par[2], par[3], par[4]};
+            for (int idx = threadIdx.x; idx < nb; idx += NT) {
+                const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+                fc[idx] *= quad_factor(x, g.node(k1), g.node(k2), g.node(k3), uc);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// remove_invariant_moments (src/moments.cpp:248-267), in place on q with the
+// weight w and centre uc[cell]; HK_DEGENERATE when the coupling is singular.
+__global__ void __launch_bounds__(NT) remove_invariants_kernel(double* __restrict__ q, const double* __restrict__ w,
+                                                               const double* __restrict__ ucs, int64_t ncells, VGrid g,
+                                                               int* __restrict__ status) {
+    __shared__ double scratch[8 * 25];
+    __shared__ double par[6];
+    const int n = g.n, nb = n * n * n;
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        double* qc = q + cell * nb;
+        const double* wc = w + cell * nb;
+        const double uc[3] = {ucs[cell * 3], ucs[cell * 3 + 1], ucs[cell * 3 + 2]};
+        double B[25];
+        coupling(g, uc, [&](int idx, double, double, double) { return wc[idx]; }, B, scratch);
+        double inv[5] = {0, 0, 0, 0, 0};
+        for (int idx = threadIdx.x; idx < nb; idx += NT) {
+            const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+            const double vx = g.node(k1), vy = g.node(k2), vz = g.node(k3);
+            const double o = qc[idx];
+            inv[0] += o;
+            inv[1] += vx * o;
+            inv[2] += vy * o;
+            inv[3] += vz * o;
+            inv[4] += (vx * vx + vy * vy + vz * vz) * o;
+        }
+        block_sum<5>(inv, scratch);
+        if (threadIdx.x == 0) {
+            double rhs[5], y[5];
+            for (int k = 0; k < 5; ++k) rhs[k] = inv[k] * g.dvk;
+            const bool ok = solve5(B, rhs, y);
+            for (int k = 0; k < 5; ++k) par[k] = y[k];
+            par[5] = ok ? 1.0 : 0.0;
+            if (status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
+        }
+        __syncthreads();
+        if (par[5] != 0.0) {
+            const double y[5] = {par[0], par[1], par[2], par[3], par[4]};
+            for (int idx = threadIdx.x; idx < nb; idx += NT) {
+                const int k3 = idx % n, k2 = (idx / n) % n, k1 = idx / (n * n);
+                qc[idx] -= quad_factor(y, g.node(k1), g.node(k2), g.node(k3), uc) * wc[idx];
+            }
+        }
+        __syncthreads();
+    }
+}
+
 int grid_for(hk_ctx ctx, int64_t ncells) {
     const int64_t cap = int64_t(ctx->sm_count) * 8;
     return int(ncells < cap ? ncells : cap);
@@ -1791,6 +1944,34 @@ int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, doub
                                                                               pen_coeff, status);
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "residual kernel");
+}
+
+int gaussian_launch(hk_ctx ctx, int n, double vmax, const double* mom, const double* theta, double beta,
+                    int64_t ncells, double* out, int* fallback) {
+    if (ncells <= 0) return HK_OK;
+    if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "anisotropic_gaussian: 2 <= n <= 128");
+    gaussian_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(mom, theta, beta, ncells, make_vgrid(n, vmax), out,
+                                                                   fallback);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "gaussian kernel");
+}
+
+int match_launch(hk_ctx ctx, int n, double vmax, double* f, const double* target, int64_t ncells, int* status) {
+    if (ncells <= 0) return HK_OK;
+    if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "match_moments: 2 <= n <= 128");
+    match_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(f, target, ncells, make_vgrid(n, vmax), status);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "match kernel");
+}
+
+int remove_invariants_launch(hk_ctx ctx, int n, double vmax, double* q, const double* w, const double* uc,
+                             int64_t ncells, int* status) {
+    if (ncells <= 0) return HK_OK;
+    if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "remove_invariant_moments: 2 <= n <= 128");
+    remove_invariants_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(q, w, uc, ncells, make_vgrid(n, vmax),
+                                                                            status);
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "remove-invariants kernel");
 }
 
 }  // namespace hk

@@ -15,6 +15,13 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
 int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,
                            int* status);
 
+// inc/moments.hpp:55-70 one operator at a time (hk_cells.cu)
+int gaussian_launch(hk_ctx ctx, int n, double vmax, const double* mom, const double* theta, double beta,
+                    int64_t ncells, double* out, int* fallback);
+int match_launch(hk_ctx ctx, int n, double vmax, double* f, const double* target, int64_t ncells, int* status);
+int remove_invariants_launch(hk_ctx ctx, int n, double vmax, double* q, const double* w, const double* uc,
+                             int64_t ncells, int* status);
+
 struct ClassifyParams {
     int nx, ny;
     double dx, dy, mu0, kappa0, eta0, eta1, delta0;

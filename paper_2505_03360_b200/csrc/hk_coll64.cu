@@ -49,6 +49,9 @@ struct Geo64 {
     static constexpr size_t SMEM = size_t(3 * PLANE) * sizeof(double2) + 64;
     static constexpr size_t XCHG_PER_TEAM = size_t(D) * SLOT * sizeof(double2);
 };
+#ifndef HK_W_TMA64
+#define HK_W_TMA64 1  // FAST producer weight planes by TMA bulk copy: 163 ms vs 198 ms per 1024 shock cells with per-thread cp.async (r02)
+#endif
 
 template <bool EXACT>
 __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
@@ -493,6 +496,16 @@ __global__ void __launch_bounds__(256, 1) coll64_kernel(CollArgs a) {
 // (single landing buffer each), so both planes of a field are consumed
 // concurrently: one producer and two consumers per scheduler, matching the
 // 1 : 2 transform count of the roles (as coll_fast_w12_kernel at N = 32).
+#ifndef HK_PROD_PHASES
+#define HK_PROD_PHASES 0  // role phase timers (HK_PROF_SPIN report), profiling builds only
+#endif
+#if HK_PROD_PHASES
+#define HK_PH_T(v) long long v = clock64()
+#define HK_PH_ADD(k, v) do { const long long _t = clock64(); ph[k] += _t - v; v = _t; } while (0)
+#else
+#define HK_PH_T(v) do {} while (0)
+#define HK_PH_ADD(k, v) do {} while (0)
+#endif
 __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
     constexpr bool EXACT = false;
     using G = Geo64;
@@ -508,6 +521,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
     double2* Pw = smem + 2 * PLANE;   // producer: prologue plane / weight staging
     uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * PLANE);  // [P] F-plane ready
     uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+    uint64_t* wbar = fbar + P + 1;  // weight-plane TMA barrier of the producer group
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -524,6 +538,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
 
     if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
     if (t < P) mbar_init(smem_u32(fbar + t), 128);
+    if (HK_W_TMA64 && t == 32) mbar_init(smem_u32(wbar), 1);
     if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tmem_fence_before();
     __syncthreads();
@@ -537,12 +552,53 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         // ================================ PRODUCERS ================================
         // Weight staging: thread-private slots [m][u] (interleaved: conflict-free).
         const uint32_t wb_s = smem_u32(Pw);
+        const bool half = a.xflags & XF_HALF, wef = a.xflags & XF_WEF, xel = a.xflags & XF_XEL;
+        const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+#if HK_W_TMA64
+        // the unit's [i3][i2] weight plane (64 KiB, the table's own layout) by four
+        // bulk copies issued by thread 0 once every producer warp has finished
+        // reading the previous plane; completion on one mbarrier
+        const uint32_t wbar_s = smem_u32(wbar);
+        unsigned wph = 0;
+        (void)half; (void)wef;
+        auto issue_w = [&](int fi, int pl) {
+            const int i1 = r * P + pl;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            named_bar(1, 128);
+            if (t == 0) {
+                const double2* src = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N;
+                mbar_arrive_expect_tx(wbar_s, N * N * 16);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) bulk_g2s(wb_s + q * (N * N * 4), src + q * (N * N / 4), N * N * 4, wbar_s);
+            }
+        };
+        auto wait_w = [&]() {
+            mbar_wait_parity(wbar_s, wph);
+            wph ^= 1;
+        };
+#else
+        auto wait_w = [&]() { cp_async_wait_all(); };
         auto issue_w = [&](int fi, int pl) {
             const int i1 = r * P + pl;
             if constexpr (!EXACT) {
-                const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N + pp;
+                if (half && i1 > N / 2) {
+                    // wfast is Hermitian-symmetric bitwise (layout_kernel): read the
+                    // mirror plane N - i1 at (-i2, -i3), halving the distinct lines
+                    const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)(N - i1) * N * N + ((N - pp) & (N - 1));
 #pragma unroll
-                for (int m = 0; m < M; ++m) cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N);
+                    for (int m = 0; m < M; ++m) {
+                        const double2* src = wt + ((N - 2 * m - h) & (N - 1)) * N;
+                        if (wef) cp_async16_hint(wb_s + (m * 128 + u) * 16, src, pol_w);
+                        else cp_async16(wb_s + (m * 128 + u) * 16, src);
+                    }
+                } else {
+                    const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N + pp;
+#pragma unroll
+                    for (int m = 0; m < M; ++m) {
+                        if (wef) cp_async16_hint(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N, pol_w);
+                        else cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N);
+                    }
+                }
             } else {
                 const double* base = (fi == 2 * a.md) ? a.loss : ((fi & 1) ? a.alpha_p : a.alpha) + (int64_t)(fi >> 1) * NB;
                 const double* wt = base + (int64_t)i1 * N * N + pp;
@@ -551,8 +607,12 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
             }
             cp_async_commit();
         };
+#endif
         long long spin_cyc = 0;
         const long long t_start = clock64();
+#if HK_PROD_PHASES
+        long long ph[6] = {0, 0, 0, 0, 0, 0};
+#endif
         auto acquire = [&](unsigned gg) {
             if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR_C * (gg / D));
             __syncwarp();
@@ -609,6 +669,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
             for (int fi = 0; fi < nfields; ++fi) {
 #pragma unroll 1
                 for (int pl = 0; pl < P; ++pl) {
+                    HK_PH_T(tA);
                     if (fi == 0) {
                         mbar_wait_parity(smem_u32(fbar + pl), ncell & 1);  // consumers put F(plane) in TMEM
                         tmem_fence_after();
@@ -622,9 +683,10 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                         tmem_ld32_nowait(tmF + 128 * pl + 32, r1);
                         tmem_ld32_nowait(tmF + 128 * pl + 64, r2);
                         tmem_ld32_nowait(tmF + 128 * pl + 96, r3);
-                        cp_async_wait_all();
+                        wait_w();
                         __syncwarp();
                         tmem_wait_ld();
+                        HK_PH_ADD(0, tA);
 #pragma unroll
                         for (int m = 0; m < 8; ++m) {
                             x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
@@ -634,12 +696,18 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                         }
                     }
                     if constexpr (!EXACT) {
+#ifndef HK_EXP_NOMUL
                         const double2* wb = Pw;
 #pragma unroll
                         for (int m = 0; m < M; ++m) {
+#if HK_W_TMA64
+                            const double2 w = wb[(2 * m + h) * N + pp], v = x[m];
+#else
                             const double2 w = wb[m * 128 + u], v = x[m];
+#endif
                             x[m] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
                         }
+#endif
                     } else {
                         const double* wb = reinterpret_cast<const double*>(Pw);
 #pragma unroll
@@ -649,28 +717,48 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                         }
                     }
                     __syncwarp();
+#ifndef HK_EXP_NOISSUE
                     if (pl + 1 < P)
                         issue_w(fi, pl + 1);
                     else if (fi + 1 < nfields)
                         issue_w(fi + 1, 0);
+#endif
+                    HK_PH_ADD(1, tA);
                     fftxh_dit<M, true>(x, h);  // x[j] = Y[hQ + j], x[Q + j] = Y[M + hQ + j]
+                    HK_PH_ADD(2, tA);
                     if (pl == 0) acquire(g);
+                    HK_PH_ADD(3, tA);
                     double2* Xs = X + (int64_t)(g % D) * SLOT;
                     const int i1 = r * P + pl;
+                    if (xel) {
 #pragma unroll
-                    for (int j = 0; j < Q; ++j) {
-                        const int ja = h * Q + j, jb = M + h * Q + j;
-                        st_cg16(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j]);
-                        st_cg16(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j]);
+                        for (int j = 0; j < Q; ++j) {
+                            const int ja = h * Q + j, jb = M + h * Q + j;
+                            st_cg16_hint(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j], pol_x);
+                            st_cg16_hint(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j], pol_x);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < Q; ++j) {
+                            const int ja = h * Q + j, jb = M + h * Q + j;
+                            st_cg16(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j]);
+                            st_cg16(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j]);
+                        }
                     }
+                    HK_PH_ADD(4, tA);
                 }
+                HK_PH_T(tP);
                 publish(g);
+                HK_PH_ADD(5, tP);
                 ++g;
             }
         }
         if (a.prof && lane == 0) {
             atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
             atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
+#if HK_PROD_PHASES
+            for (int k = 0; k < 6; ++k) atomicAdd(&a.prof[8 + k], (unsigned long long)ph[k]);
+#endif
         }
     } else {
         // ============================ CONSUMER GROUPS ============================
@@ -689,6 +777,9 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         };
         long long spin_cyc = 0;
         const long long t_start = clock64();
+#if HK_PROD_PHASES
+        long long ph[6] = {0, 0, 0, 0, 0, 0};
+#endif
         auto issue = [&](unsigned gs) {
             if (lane == 0) spin_cyc += spin_geq(ready + gs % D, ARR * (gs / D + 1));
             __syncwarp();
@@ -755,7 +846,9 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
             double mre = 0.0, n2 = 0.0, l2 = 0.0;
             for (int fi = 1; fi <= nfields; ++fi) {
                 const unsigned gs = gb + fi;
+                HK_PH_T(tC);
                 complete(gs);
+                HK_PH_ADD(0, tC);
                 {  // rows i1 = pp over i2 (DIF), back in natural order
                     double2* row = Rv + pp * ROW;
                     double2 v[M];
@@ -769,14 +862,18 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
 #pragma unroll
                     for (int m = 0; m < M; ++m) row[2 * m + h] = v[m];
                 }
+                HK_PH_ADD(1, tC);
                 named_bar(bar, 128);  // columns need every row
                 double2 y[M];
                 const double2* col = Rv + pp;
 #pragma unroll
                 for (int m = 0; m < M; ++m) y[m] = col[(2 * m + h) * ROW];
                 named_bar(bar, 128);  // buffer free: the next field's pull overlaps the transform
+                HK_PH_ADD(2, tC);
                 if (fi < nfields || more_cells) issue(gs + 1);
+                HK_PH_ADD(3, tC);
                 fftxh_dit<M, true>(y, h);  // y[j] = node hQ + j, y[Q + j] = node M + hQ + j
+                HK_PH_ADD(4, tC);
                 const int j3 = r * P + grp;
                 if (fi < nfields) {
                     const double mu = (fi == 1) ? a.mult0 : 1.0;
@@ -816,6 +913,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                         }
                     }
                 }
+                HK_PH_ADD(5, tC);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -833,6 +931,9 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         if (a.prof && lane == 0) {
             atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
             atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
+#if HK_PROD_PHASES
+            for (int k = 0; k < 6; ++k) atomicAdd(&a.prof[16 + k], (unsigned long long)ph[k]);
+#endif
         }
     }
     tmem_fence_before();
@@ -871,6 +972,23 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
     if (max_cells < teams) teams = max_cells;
     if (teams < 1) return HK_OK;
     CollArgs args = args_in;
+    if (const char* xf = getenv("HK_X64")) args.xflags = (unsigned)atoi(xf);  // EXPERIMENT
+    static const bool persist = getenv("HK_X64_PERSIST") != nullptr;       // EXPERIMENT
+    if (persist && w12) {
+        static bool set = false;
+        const size_t bytes = size_t(teams) * G::XCHG_PER_TEAM;
+        if (!set) {
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes + (8 << 20));
+            set = true;
+        }
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = args.xchg;
+        v.accessPolicyWindow.num_bytes = bytes;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     args.in_ready = nullptr;
     args.out_done = nullptr;
     if ((st = check_cuda(ctx, cudaMemsetAsync(args.team_ctr, 0, sizeof(unsigned) * 2 * G::D * teams, ctx->stream),
@@ -879,8 +997,8 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
     static unsigned long long* prof = nullptr;
     const bool profiling = w12 && getenv("HK_PROF_SPIN") != nullptr;
     if (profiling) {
-        if (!prof) cudaMalloc(&prof, 64);
-        cudaMemsetAsync(prof, 0, 64, ctx->stream);
+        if (!prof) cudaMalloc(&prof, 256);
+        cudaMemsetAsync(prof, 0, 256, ctx->stream);
         args.prof = prof;
     }
     void* params[] = {&args};
@@ -890,12 +1008,25 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
                     "N = 64 collision kernel launch");
     timing_end(ctx);
     ctx->launches++;
+    if (persist && w12) {
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    }
     if (profiling) {
-        unsigned long long h[4];
-        cudaMemcpyAsync(h, prof, 32, cudaMemcpyDeviceToHost, ctx->stream);
+        unsigned long long h[32];
+        cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
         fprintf(stderr, "[hk prof] coll64 CTAs %lld: producer spin %.1f%%, consumer spin %.1f%%\n", (long long)(teams * G::C),
                 100.0 * h[0] / (double)h[2], 100.0 * h[1] / (double)h[3]);
+#if HK_PROD_PHASES
+        fprintf(stderr, "[hk prof] producer phases (%% of producer time): ld+wait %.1f mul %.1f fft %.1f acquire %.1f "
+                "store %.1f publish %.1f\n", 100.0 * h[8] / h[2], 100.0 * h[9] / h[2], 100.0 * h[10] / h[2],
+                100.0 * h[11] / h[2], 100.0 * h[12] / h[2], 100.0 * h[13] / h[2]);
+        fprintf(stderr, "[hk prof] consumer phases (%% of consumer time): complete %.1f rowfft %.1f colread %.1f "
+                "issue %.1f colfft %.1f gain %.1f\n", 100.0 * h[16] / h[3], 100.0 * h[17] / h[3], 100.0 * h[18] / h[3],
+                100.0 * h[19] / h[3], 100.0 * h[20] / h[3], 100.0 * h[21] / h[3]);
+#endif
     }
     return st;
 }

@@ -771,8 +771,11 @@ struct GeoW {
     static constexpr int D = HK_SLOTS;
     static constexpr uint32_t TM_COLS = 512;
     // landing [2][4 warps][PLANE] + producer staging [4 warps][PLANE]
-    static constexpr size_t SMEM = size_t(12 * PLANE) * sizeof(double2) + 2 * P * sizeof(uint64_t) + 32;
+    static constexpr size_t SMEM = size_t(12 * PLANE) * sizeof(double2) + 2 * P * sizeof(uint64_t) + 64;
 };
+#ifndef HK_W_TMA
+#define HK_W_TMA 0  // producer weight planes by TMA bulk copy (mbarrier): 46.8 ms vs 46.6 per 4096 cells with cp.async (r02)
+#endif
 
 // 12-warp variant: 4 producer warps (two i1 planes each) and 8 consumer warps
 // (one j3 plane each, single landing buffer): per scheduler one producer and
@@ -794,6 +797,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
     double2* Pw = smem + 8 * PLANE;     // producer staging [4][PLANE]
     uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 12 * PLANE);  // [P]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
+    uint64_t* wbar = fbar + P + 1;  // [4] weight-plane TMA barriers, one per producer warp
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -808,6 +812,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
 
     if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
     if (t < P) mbar_init(smem_u32(fbar + t), 32);
+    if (HK_W_TMA && t >= 32 && t < 36) mbar_init(smem_u32(wbar + (t - 32)), 1);
     if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tmem_fence_before();
     __syncthreads();
@@ -820,6 +825,25 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
         // ================================ PRODUCER WARP ================================
         double2* wbuf = Pw + pw * PLANE;  // weights of the next unit [i3][lane] / transposes
         const uint32_t wbuf_s = smem_u32(wbuf);
+#if HK_W_TMA
+        // one bulk copy of the unit's [i3][i2] weight plane (16 KiB, the table's own
+        // layout) issued by lane 0, completion on this warp's mbarrier
+        const uint32_t wbar_s = smem_u32(wbar + pw);
+        unsigned wph = 0;
+        auto issue_w = [&](int e, int pp) {
+            const int i1 = r * P + pw + 4 * pp;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic reads of wbuf before the async write
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive_expect_tx(wbar_s, N * N * 16);
+                bulk_g2s(wbuf_s, a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N, N * N * 16, wbar_s);
+            }
+        };
+        auto wait_w = [&]() {
+            mbar_wait_parity(wbar_s, wph);
+            wph ^= 1;
+        };
+#else
         auto issue_w = [&](int e, int pp) {
             const int i1 = r * P + pw + 4 * pp;
             const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + lane;
@@ -827,6 +851,8 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
             for (int i3 = 0; i3 < N; ++i3) cp_async16(wbuf_s + (i3 * 32 + lane) * 16, wt + i3 * N);
             cp_async_commit();
         };
+        auto wait_w = [&]() { cp_async_wait_all(); };
+#endif
         long long spin_cyc = 0;
         const long long t_start = clock64();
 #if HK_PROD_PHASES
@@ -895,7 +921,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                         tmem_ld32_nowait(tmF + 32, r1);
                         tmem_ld32_nowait(tmF + 64, r2);
                         tmem_ld32_nowait(tmF + 96, r3);
-                        cp_async_wait_all();
+                        wait_w();
                         __syncwarp();
                         tmem_wait_ld();
                         HK_PH_ADD(0, tA);
@@ -907,16 +933,20 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                             x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
                         }
                     }
+#ifndef HK_EXP_NOMUL
 #pragma unroll
                     for (int i3 = 0; i3 < N; ++i3) {
                         const double2 w = wbuf[i3 * 32 + lane], v = x[i3];
                         x[i3] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
                     }
+#endif
                     __syncwarp();
+#ifndef HK_EXP_NOISSUE
                     if (pp + 1 < PPW)
                         issue_w(e, pp + 1);
                     else if (e + 1 < n_entries)
                         issue_w(e + 1, 0);
+#endif
                     HK_PH_ADD(1, tA);
                     fft_w<N, true>(x);
                     HK_PH_ADD(2, tA);

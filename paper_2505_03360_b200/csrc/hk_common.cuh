@@ -249,6 +249,25 @@ __device__ __forceinline__ void cp_async16(uint32_t smem_dst, const void* gsrc) 
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_dst), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+// With an L2 eviction-priority policy (createpolicy).
+__device__ __forceinline__ void cp_async16_hint(uint32_t smem_dst, const void* gsrc, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(smem_dst), "l"(gsrc), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void st_cg16_hint(double2* p, double2 v, uint64_t pol) {
+    asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;\n" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
 // 8-byte variant (cp.async.ca: sizes below 16 B go through L1).
 __device__ __forceinline__ void cp_async8(uint32_t smem_dst, const void* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_dst), "l"(gsrc) : "memory");
@@ -273,18 +292,28 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-// Spin until *p >= target (acquire, GPU scope).  Traps instead of hanging if
-// the producer never arrives (deadlock guard, ~2 s).
+// Spin until *p >= target (acquire, GPU scope).  Polls with relaxed loads (no
+// L1 invalidation per iteration) and an exponential __nanosleep backoff
+// (HK_SPIN_NS0 doubling up to HK_SPIN_NSMAX): a waiting warp shares its
+// scheduler with the warps it waits for, so every poll it does not issue is an
+// issue slot for them.  One acquire load once the target is reached.  Traps
+// instead of hanging if the producer never arrives (~2^24 polls, seconds).
+#ifndef HK_SPIN_NS0
+#define HK_SPIN_NS0 32
+#endif
+#ifndef HK_SPIN_NSMAX
+#define HK_SPIN_NSMAX 256
+#endif
 __device__ __forceinline__ long long spin_geq(const unsigned* p, unsigned target) {
     const long long t0 = clock64();
     unsigned v;
-    // Poll with relaxed loads (no L1 invalidation per iteration), then one
-    // acquire load once the target is reached.
+    unsigned ns = HK_SPIN_NS0, polls = 0;
     for (;;) {
         asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
         if ((int)(v - target) >= 0) break;
-        if (clock64() - t0 > (1LL << 32)) __trap();
-        __nanosleep(20);
+        if (++polls > (1u << 24)) __trap();
+        __nanosleep(ns);
+        ns = ns < HK_SPIN_NSMAX ? 2 * ns : ns;
     }
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return clock64() - t0;

@@ -119,6 +119,24 @@ int hk_maxwellian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, i
     return maxwellian_launch(ctx, n, vmax, mom_dev, ncells, out_dev, status_dev);
 }
 
+int hk_anisotropic_gaussian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, const double* theta_dev,
+                                  double beta, int64_t ncells, double* out_dev, int* fallback_dev) {
+    cudaSetDevice(ctx->device);
+    return gaussian_launch(ctx, n, vmax, mom_dev, theta_dev, beta, ncells, out_dev, fallback_dev);
+}
+
+int hk_match_moments_batch(hk_ctx ctx, int n, double vmax, double* f_dev, const double* target_dev, int64_t ncells,
+                           int* status_dev) {
+    cudaSetDevice(ctx->device);
+    return match_launch(ctx, n, vmax, f_dev, target_dev, ncells, status_dev);
+}
+
+int hk_remove_invariant_moments_batch(hk_ctx ctx, int n, double vmax, double* q_dev, const double* weight_dev,
+                                      const double* uc_dev, int64_t ncells, int* status_dev) {
+    cudaSetDevice(ctx->device);
+    return remove_invariants_launch(ctx, n, vmax, q_dev, weight_dev, uc_dev, ncells, status_dev);
+}
+
 int hk_esbgk_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_dev, double* out_dev, int64_t ncells,
                          double a, const double* eps_dev, double eps, double beta, double nu_coeff, int* info_dev,
                          double* mom_dev) {

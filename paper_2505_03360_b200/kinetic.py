@@ -101,6 +101,53 @@ def maxwellian(moments, vgrid: VelocityGrid, ctx=None):
     return out
 
 
+def anisotropic_gaussian(moments, theta, beta: float, vgrid: VelocityGrid, ctx=None):
+    """anisotropic_gaussian (src/moments.cpp:120-157) for moments [cells,5] and stress
+    tensors theta [cells,3,3]; returns (G [cells,n^3], fell_back bool [cells])."""
+    ctx = ctx or default_context(moments.device.index or 0)
+    moments = moments.contiguous()
+    nc = moments.shape[0]
+    th = theta.to(device=moments.device, dtype=torch.float64).reshape(nc, 9).contiguous()
+    out = torch.empty((nc, vgrid.nv ** 3), dtype=torch.float64, device=moments.device)
+    fb = torch.empty(nc, dtype=torch.int32, device=moments.device)
+    ctx.check(ctx._lib.hk_anisotropic_gaussian_batch(ctx.h, vgrid.nv, vgrid.vmax, moments.data_ptr(), th.data_ptr(),
+                                                     beta, nc, out.data_ptr(), fb.data_ptr()))
+    return out, fb != 0
+
+
+def match_moments(f, vgrid: VelocityGrid, targets, *, check=True, ctx=None):
+    """match_moments (src/moments.cpp:225-246) in place; targets [cells,5] =
+    (rho, momentum x, y, z, energy)."""
+    ctx = ctx or default_context(f.device.index or 0)
+    assert f.is_contiguous()
+    _, nc = _cells(f, vgrid.nv)
+    t = targets.to(device=f.device, dtype=torch.float64).reshape(nc, 5).contiguous()
+    st = torch.empty(nc, dtype=torch.int32, device=f.device)
+    ctx.check(ctx._lib.hk_match_moments_batch(ctx.h, vgrid.nv, vgrid.vmax, f.data_ptr(), t.data_ptr(), nc,
+                                              st.data_ptr()))
+    if check:
+        _check_cells(st, "match_moments")
+    return f
+
+
+def remove_invariant_moments(q, weight, vgrid: VelocityGrid, uc, *, check=True, ctx=None):
+    """remove_invariant_moments (src/moments.cpp:248-267) in place on q [cells,n^3]
+    with weight [cells,n^3] and centres uc [cells,3]."""
+    ctx = ctx or default_context(q.device.index or 0)
+    assert q.is_contiguous()
+    _, nc = _cells(q, vgrid.nv)
+    w = weight.to(device=q.device, dtype=torch.float64).contiguous()
+    if w.numel() != q.numel():
+        raise contract_violation("remove_invariant_moments: weight must match q")
+    u = uc.to(device=q.device, dtype=torch.float64).reshape(nc, 3).contiguous()
+    st = torch.empty(nc, dtype=torch.int32, device=q.device)
+    ctx.check(ctx._lib.hk_remove_invariant_moments_batch(ctx.h, vgrid.nv, vgrid.vmax, q.data_ptr(), w.data_ptr(),
+                                                         u.data_ptr(), nc, st.data_ptr()))
+    if check:
+        _check_cells(st, "remove_invariant_moments")
+    return q
+
+
 def _eps_arg(eps, nc, dev):
     if isinstance(eps, torch.Tensor):
         e = eps.to(device=dev, dtype=torch.float64).contiguous()

@@ -67,7 +67,8 @@ class XSlab:
     def scatter(self, global_field: torch.Tensor) -> torch.Tensor:
         """Local interior [ny*nxl, nb] from a global [ny*nx, nb] field."""
         g = global_field.view(self.ny, self.nx, -1)
-        return g[:, self.i0:self.i0 + self.nxl].reshape(self.cells, -1).contiguous()
+        # always a new tensor (at world 1 the slice is the whole field: never alias it)
+        return g[:, self.i0:self.i0 + self.nxl].reshape(self.cells, -1).clone(memory_format=torch.contiguous_format)
 
     def gather(self, local: torch.Tensor, group=None) -> torch.Tensor:
         """Global field assembled on every rank (tests / snapshots)."""
@@ -152,13 +153,20 @@ def conservation_sums(moments: torch.Tensor, group=None) -> torch.Tensor:
 
 def penalized_imex_step_slab(part: XSlab, f: torch.Tensor, kernel, dx: float, dy: float, dt: float,
                              eps_cell: torch.Tensor, pen_coeff: float = 6.283185307179586, eps_weno: float = 1e-6,
-                             group=None, work=None):
+                             group=None, work=None, peer=None):
     """penalized_imex_step (src/boltzmann.cpp:47-110) on one x-slab, in place.
 
     Same operation sequence as the single-GPU hk_penalized_imex_step; the
     stage field's halos are exchanged before each transport, overlapped with
-    the residual (collision) evaluation of that stage."""
+    the residual (collision) evaluation of that stage.
+
+    peer: a PeerHalo mapped on work[0] (the stage field Y): the transport then
+    reads the neighbours' ghost columns of Y straight from their memory
+    (hk_transport_rhs_peer over NVLink / CUDA IPC) instead of exchanging
+    halos; Y is published (refresh) after each stage solve and released
+    (done) before the next one overwrites it."""
     from . import _abi  # noqa: F401
+    from . import make_velocity_grid
 
     ctx = kernel.ctx
     L = ctx._lib
@@ -169,8 +177,11 @@ def penalized_imex_step_slab(part: XSlab, f: torch.Tensor, kernel, dx: float, dy
     if work is None:
         work = torch.empty((6, cells, nb), dtype=torch.float64, device=f.device)
     y, q1, k1, tr, res, fa = work
+    if peer is not None and peer.slab.data_ptr() != y.data_ptr():
+        raise ValueError("peer must be a PeerHalo mapped on work[0] (the stage field)")
+    vg = make_velocity_grid(n, kernel.vmax)
     e = eps_cell.to(device=f.device, dtype=torch.float64).contiguous()
-    lh, rh = part.halo_buffers(nb, f)
+    lh, rh = part.halo_buffers(nb, f) if peer is None else (None, None)
     a00 = 1.0 - 2.0 ** -0.5
     a11 = 1.0 - 1.0 / (2.0 * 2.0 ** -0.5)
 
@@ -191,19 +202,25 @@ def penalized_imex_step_slab(part: XSlab, f: torch.Tensor, kernel, dx: float, dy
         ctx.check(L.hk_imex_combine(ctx.h, op, count, nb, dt, e.data_ptr(), out.data_ptr(), p(fv), p(yv), p(qv),
                                     p(kv), p(tv), p(rv)))
 
+    def halo_transport(yv, out):
+        if peer is not None:
+            peer.refresh()             # every rank's Y is written
+            residual(yv, res)
+            peer.transport(out, vg, dx, dy, eps_weno)
+            peer.done()                # the neighbours have read my ghost columns
+        else:
+            works = part.exchange(yv, lh, rh, group, async_op=True)
+            residual(yv, res)          # overlaps the halo exchange
+            wait_all(works)
+            transport(yv, out)
+
     stage(f, a00 * dt, y)
     comb(0, k1, fv=f, yv=y)
-    works = part.exchange(y, lh, rh, group, async_op=True)
-    residual(y, res)                  # overlaps the halo exchange
-    wait_all(works)
-    transport(y, tr)
+    halo_transport(y, tr)
     comb(1, q1, tv=tr, rv=res)
     comb(2, fa, fv=f, qv=q1, kv=k1)
     stage(fa, a11 * dt, y)
-    works = part.exchange(y, lh, rh, group, async_op=True)
-    residual(y, res)
-    wait_all(works)
-    transport(y, tr)
+    halo_transport(y, tr)
     comb(3, f, yv=y, qv=q1, kv=k1, tv=tr, rv=res)
     return f
 

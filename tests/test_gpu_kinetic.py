@@ -190,3 +190,41 @@ def test_penalized_imex_step(hk, kin, oracle):
     ft = torch.from_numpy(f.copy()).cuda()
     kin.penalized_imex_step(ft, nx, ny, k, 0.1, 0.1, 1e-3, torch.from_numpy(eps))
     assert rel(ft.cpu().numpy(), ref) < 1e-10
+
+
+def test_moment_operators_one_at_a_time(hk, kin, oracle, cells32):
+    """anisotropic_gaussian / match_moments / remove_invariant_moments as
+    stand-alone device operators (inc/moments.hpp:55-70) vs the oracle."""
+    import torch
+    n = 32
+    vg = hk.make_velocity_grid(n, VMAX)
+    f = cells32
+    mom = np.array([oracle.moments(n, VMAX, f[c])[1] for c in range(len(f))])
+    theta = np.array([oracle.stress_tensor(n, VMAX, f[c], mom[c]) for c in range(len(f))])
+    # anisotropic Gaussian (beta = -1/2, the ES-BGK value), plus an LLT fallback cell
+    th = theta.copy()
+    th[2] = np.diag([10.0 * mom[2, 4], 1.0, 1.0])  # (1 - beta) T - beta theta_xx < 0: LLT fails
+    g, fb = kin.anisotropic_gaussian(torch.from_numpy(mom).cuda(), torch.from_numpy(th).cuda(), -0.5, vg)
+    g, fb = g.cpu().numpy(), fb.cpu().numpy()
+    for c in range(len(f)):
+        st, ref, rfb = oracle.anisotropic_gaussian(n, VMAX, tuple(mom[c]), th[c], -0.5)
+        assert st == 0 and bool(rfb) == bool(fb[c]) and rel(g[c], ref) < 1e-12, c
+    assert fb[2] and not fb[0]
+    # match_moments of the Gaussians to the cells' own (rho, rho u, E)
+    E = 0.5 * mom[:, 0] * (mom[:, 1:4] ** 2).sum(1) + 1.5 * mom[:, 0] * mom[:, 4]
+    targets = np.concatenate([mom[:, :1], mom[:, :1] * mom[:, 1:4], E[:, None]], 1)
+    gm = torch.from_numpy(g.copy()).cuda()
+    kin.match_moments(gm, vg, torch.from_numpy(targets).cuda())
+    gm = gm.cpu().numpy()
+    for c in range(len(f)):
+        st, ref = oracle.match_moments(n, VMAX, g[c], targets[c, 0], targets[c, 1:4], targets[c, 4])
+        assert st == 0 and rel(gm[c], ref) < 1e-12, c
+    # remove_invariant_moments of q = f - G~ with weight G~ and centre u
+    q = f - gm
+    qd = torch.from_numpy(q.copy()).cuda()
+    kin.remove_invariant_moments(qd, torch.from_numpy(gm).cuda(), vg, torch.from_numpy(mom[:, 1:4].copy()).cuda())
+    qd = qd.cpu().numpy()
+    for c in range(len(f)):
+        st, ref = oracle.remove_invariant_moments(n, VMAX, q[c], gm[c], mom[c, 1:4])
+        assert st == 0
+        assert np.abs(qd[c] - ref).max() <= 1e-12 * np.abs(q[c]).max(), c

@@ -14,12 +14,15 @@ ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--exact", action="store_true")
 ap.add_argument("--noguard", action="store_true")
 ap.add_argument("--tag", default="")
+ap.add_argument("--slab", type=int, default=-1, help="N=64: x-slab of the config-5 field from this column (cells/128 columns)")
 args = ap.parse_args()
 ctx = hk.Context(0, torch.cuda.current_stream())
 vg = hk.make_velocity_grid(args.n, 8.0)
 kern = hk.precompute_kernel(vg, args.n, args.a1, args.a2, inputs.R_PHYS_MAX, ctx=ctx)
 if args.n == 32:
     f = inputs.config2_cells_torch(args.cells, 32, device="cuda")
+elif args.n == 64 and args.slab >= 0:
+    f = inputs.config5_slab_torch(i0=args.slab, nxl=max(1, args.cells // 128), ny=128, n=64)
 elif args.n == 64:
     base = torch.from_numpy(inputs.config5_cells(min(args.cells, 16), 64)).cuda()
     f = base.repeat((args.cells + len(base) - 1) // len(base), 1)[: args.cells].contiguous()
