@@ -429,7 +429,6 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
         CUresult r0 = p_write_value32((CUstream)ctx->s_in, (CUdeviceptr)flags_dev, 0, 0);
         CUresult r1 = p_wait_value32((CUstream)ctx->s_out, (CUdeviceptr)flags_dev, 0, CU_STREAM_WAIT_VALUE_GEQ);
         if (r0 != CUDA_SUCCESS || r1 != CUDA_SUCCESS) {
-            if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] stream memory ops unavailable (%d, %d)\n", (int)r0, (int)r1);
             cudaStreamSynchronize(ctx->s_in);
             cudaStreamSynchronize(ctx->s_out);
             cudaEventDestroy(e0);

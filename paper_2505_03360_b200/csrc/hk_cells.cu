@@ -1838,20 +1838,13 @@ int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncel
                    const int* count_dev) {
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "moments: 2 <= n <= 128");
-    static const int mom_var = getenv("HK_MOM_VAR") ? atoi(getenv("HK_MOM_VAR")) : 2;  // variant: CTA size x CTAs per SM x loads in flight (3.99 ms at config 3; 3 -> 4.72)
-    if (warp_path(n) && n >= 8 && mom_var > 0) {
-        static const int per_sm[7] = {3, 1, 2, 3, 4, 6, 2};
-        const int64_t cap = int64_t(ctx->sm_count) * per_sm[mom_var <= 6 ? mom_var : 3];
+    // 256-thread CTAs, 2 per SM, 16 loads in flight per thread (config 3: 3.99 ms;
+    // measured and removed: 512 x 1 x 16, 256 x 4 x 8 4.72 ms, 128 x 6 x 8, 512 x 2 x 8, 256 x 3 x 8)
+    if (warp_path(n) && n >= 8) {
+        const int64_t cap = int64_t(ctx->sm_count) * 2;
         const int grid = int(ncells < cap ? ncells : cap);
-        const VGrid g = make_vgrid(n, vmax);
-        switch (mom_var) {  // CTA size, CTAs per SM, loads in flight per thread
-        case 1: moments_cta_kernel<512, 1, 16><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
-        case 2: moments_cta_kernel<256, 2, 16><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
-        case 4: moments_cta_kernel<256, 4, 8><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
-        case 5: moments_cta_kernel<128, 6, 8><<<grid, 128, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
-        case 6: moments_cta_kernel<512, 2, 8><<<grid, 512, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
-        default: moments_cta_kernel<256, 3, 8><<<grid, 256, 0, ctx->stream>>>(f, ncells, g, log2i(n), mom, sigma, real, l1, status, src_idx, count_dev); break;
-        }
+        moments_cta_kernel<256, 2, 16><<<grid, 256, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), log2i(n), mom, sigma,
+                                                                      real, l1, status, src_idx, count_dev);
     } else if (warp_path(n))
         moments_warp_kernel<<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), log2i(n),
                                                                                   mom, sigma, real, l1, status, src_idx, count_dev);
@@ -1878,19 +1871,14 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "stage: 2 <= n <= 128");
     const VGrid g = make_vgrid(n, vmax);
-    static const bool stage_warp = getenv("HK_STAGE_WARP") != nullptr;
-    if (warp_path(n) && n >= 8 && !stage_warp) {
-        static const int sv = getenv("HK_STAGE_VAR") ? atoi(getenv("HK_STAGE_VAR")) : 2;  // config 3 (L2 hints, register solve5): 2 -> 9.9 ms, 3 -> 10.9, 5 -> 10.2, 6 -> 10.4
-        const int64_t cap = int64_t(ctx->sm_count) * sv;
+    if (warp_path(n) && n >= 8) {
+        // 256-thread CTAs, 2 per SM (config 3, L2 hints, register solve5: 9.9 ms; measured and
+        // removed: 3 per SM 10.9, 128-thread CTAs 5 / 6 per SM 10.2 / 10.4)
+        const int64_t cap = int64_t(ctx->sm_count) * 2;
         const int grid = int(ncells < cap ? ncells : cap);
         const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32 + 2 * n + 6 * n + 2 * n);
-        // sv: CTAs per SM; 2, 3 -> 256-thread CTAs, 4..6 -> 128-thread CTAs
-        auto kern = sv == 3   ? (esbgk ? stage_cta_kernel<true, 256, 3> : stage_cta_kernel<false, 256, 3>)
-                    : sv == 4 ? (esbgk ? stage_cta_kernel<true, 128, 4> : stage_cta_kernel<false, 128, 4>)
-                    : sv == 5 ? (esbgk ? stage_cta_kernel<true, 128, 5> : stage_cta_kernel<false, 128, 5>)
-                    : sv == 6 ? (esbgk ? stage_cta_kernel<true, 128, 6> : stage_cta_kernel<false, 128, 6>)
-                              : (esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>);
-        const int mt = (sv >= 4 && sv <= 6) ? 128 : 256;
+        auto kern = esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>;
+        const int mt = 256;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, mt, smem, ctx->stream>>>(fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info,
                                               mom_out, k1_out, k1_scale);

@@ -32,9 +32,7 @@ struct CollArgs {
     const unsigned* in_ready;
     unsigned* out_done;
     int64_t chunk;
-    unsigned xflags;  // N = 64 kernel options (XF_*)
 };
-enum : unsigned { XF_HALF = 1u, XF_WEF = 2u, XF_XEL = 4u };
 
 // hk_coll64.cu: N = 64 team kernel (C = 32 CTAs per cell, cooperative launch).
 // Bytes of exchange scratch per launch, and the launcher (exact = two complex

@@ -552,15 +552,12 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         // ================================ PRODUCERS ================================
         // Weight staging: thread-private slots [m][u] (interleaved: conflict-free).
         const uint32_t wb_s = smem_u32(Pw);
-        const bool half = a.xflags & XF_HALF, wef = a.xflags & XF_WEF, xel = a.xflags & XF_XEL;
-        const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
 #if HK_W_TMA64
         // the unit's [i3][i2] weight plane (64 KiB, the table's own layout) by four
         // bulk copies issued by thread 0 once every producer warp has finished
         // reading the previous plane; completion on one mbarrier
         const uint32_t wbar_s = smem_u32(wbar);
         unsigned wph = 0;
-        (void)half; (void)wef;
         auto issue_w = [&](int fi, int pl) {
             const int i1 = r * P + pl;
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -580,31 +577,9 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         auto wait_w = [&]() { cp_async_wait_all(); };
         auto issue_w = [&](int fi, int pl) {
             const int i1 = r * P + pl;
-            if constexpr (!EXACT) {
-                if (half && i1 > N / 2) {
-                    // wfast is Hermitian-symmetric bitwise (layout_kernel): read the
-                    // mirror plane N - i1 at (-i2, -i3), halving the distinct lines
-                    const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)(N - i1) * N * N + ((N - pp) & (N - 1));
+            const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N + pp;
 #pragma unroll
-                    for (int m = 0; m < M; ++m) {
-                        const double2* src = wt + ((N - 2 * m - h) & (N - 1)) * N;
-                        if (wef) cp_async16_hint(wb_s + (m * 128 + u) * 16, src, pol_w);
-                        else cp_async16(wb_s + (m * 128 + u) * 16, src);
-                    }
-                } else {
-                    const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N + pp;
-#pragma unroll
-                    for (int m = 0; m < M; ++m) {
-                        if (wef) cp_async16_hint(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N, pol_w);
-                        else cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N);
-                    }
-                }
-            } else {
-                const double* base = (fi == 2 * a.md) ? a.loss : ((fi & 1) ? a.alpha_p : a.alpha) + (int64_t)(fi >> 1) * NB;
-                const double* wt = base + (int64_t)i1 * N * N + pp;
-#pragma unroll
-                for (int m = 0; m < M; ++m) cp_async8(wb_s + (m * 128 + u) * 8, wt + (2 * m + h) * N);
-            }
+            for (int m = 0; m < M; ++m) cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N);
             cp_async_commit();
         };
 #endif
@@ -730,20 +705,11 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
                     HK_PH_ADD(3, tA);
                     double2* Xs = X + (int64_t)(g % D) * SLOT;
                     const int i1 = r * P + pl;
-                    if (xel) {
 #pragma unroll
-                        for (int j = 0; j < Q; ++j) {
-                            const int ja = h * Q + j, jb = M + h * Q + j;
-                            st_cg16_hint(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j], pol_x);
-                            st_cg16_hint(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j], pol_x);
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < Q; ++j) {
-                            const int ja = h * Q + j, jb = M + h * Q + j;
-                            st_cg16(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j]);
-                            st_cg16(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j]);
-                        }
+                    for (int j = 0; j < Q; ++j) {
+                        const int ja = h * Q + j, jb = M + h * Q + j;
+                        st_cg16(Xs + (int64_t)(ja / P) * BLK + ((ja % P) * N + i1) * N + pp, x[j]);
+                        st_cg16(Xs + (int64_t)(jb / P) * BLK + ((jb % P) * N + i1) * N + pp, x[Q + j]);
                     }
                     HK_PH_ADD(4, tA);
                 }
@@ -949,11 +915,11 @@ size_t coll64_xchg_bytes(hk_ctx ctx) {
 
 int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_cells, int tag) {
     using G = Geo64;
-    static const bool eight = getenv("HK_C64_8W") != nullptr;  // 8-warp FAST kernel for comparison
-    const bool w12 = !exact && !eight;
-    auto kern = exact ? coll64_kernel<true> : (w12 ? coll64_w12_kernel : coll64_kernel<false>);
-    const int nthreads = w12 ? 384 : 256;
-    const int key = 6400 + (exact ? 1 : 0) + (w12 ? 2 : 0);
+    // FAST: the 12-warp kernel; EXACT: the 8-warp two-transform kernel.  (The
+    // 8-warp FAST kernel was measured slower and is not launched.)
+    auto kern = exact ? coll64_kernel<true> : coll64_w12_kernel;
+    const int nthreads = exact ? 256 : 384;
+    const int key = 6400 + (exact ? 1 : 2);
     int st;
     if (!ctx->max_clusters.count(key)) {
         if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM),
@@ -962,9 +928,7 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
         int per_sm = 0;
         if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, G::SMEM), "occupancy")))
             return st;
-        int teams = per_sm >= 1 ? ctx->sm_count / G::C : 0;
-        if (const char* m = getenv("HK_TEAMS64")) teams = atoi(m);  // experiment override (<= sm_count / C)
-        if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] coll64 kernel (exact %d): per_sm %d teams %d\n", exact, per_sm, teams);
+        const int teams = per_sm >= 1 ? ctx->sm_count / G::C : 0;
         if (teams < 1) return fail(ctx, HK_CUDA, "N = 64 collision kernel cannot be resident");
         ctx->max_clusters[key] = teams;
     }
@@ -972,30 +936,17 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
     if (max_cells < teams) teams = max_cells;
     if (teams < 1) return HK_OK;
     CollArgs args = args_in;
-    if (const char* xf = getenv("HK_X64")) args.xflags = (unsigned)atoi(xf);  // EXPERIMENT
-    static const bool persist = getenv("HK_X64_PERSIST") != nullptr;       // EXPERIMENT
-    if (persist && w12) {
-        static bool set = false;
-        const size_t bytes = size_t(teams) * G::XCHG_PER_TEAM;
-        if (!set) {
-            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes + (8 << 20));
-            set = true;
-        }
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.base_ptr = args.xchg;
-        v.accessPolicyWindow.num_bytes = bytes;
-        v.accessPolicyWindow.hitRatio = 1.0f;
-        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
-    }
     args.in_ready = nullptr;
     args.out_done = nullptr;
     if ((st = check_cuda(ctx, cudaMemsetAsync(args.team_ctr, 0, sizeof(unsigned) * 2 * G::D * teams, ctx->stream),
                          "team counters")))
         return st;
     static unsigned long long* prof = nullptr;
-    const bool profiling = w12 && getenv("HK_PROF_SPIN") != nullptr;
+#if HK_PROFILING
+    const bool profiling = !exact && getenv("HK_PROF_SPIN") != nullptr;  // profiling builds only
+#else
+    const bool profiling = false;
+#endif
     if (profiling) {
         if (!prof) cudaMalloc(&prof, 256);
         cudaMemsetAsync(prof, 0, 256, ctx->stream);
@@ -1008,11 +959,6 @@ int launch_coll64(hk_ctx ctx, const CollArgs& args_in, bool exact, int64_t max_c
                     "N = 64 collision kernel launch");
     timing_end(ctx);
     ctx->launches++;
-    if (persist && w12) {
-        cudaStreamAttrValue v{};
-        v.accessPolicyWindow.num_bytes = 0;
-        cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
-    }
     if (profiling) {
         unsigned long long h[32];
         cudaMemcpyAsync(h, prof, sizeof h, cudaMemcpyDeviceToHost, ctx->stream);

@@ -48,9 +48,6 @@ constexpr double kGuardTau = 5e-11;
 // is as accurate as the exact path would be and is not rerouted.
 constexpr double kGuardFloor = 2e-5;
 
-// internal flag: route the FAST path through the 256-thread SMEM kernel
-constexpr uint32_t HK_COLL_LEGACY_FAST = 1u << 16;
-
 template <int N, int C>
 struct Geo {
     static constexpr int P = N / C;
@@ -375,364 +372,9 @@ __global__ void __launch_bounds__(256, 1) coll_kernel(CollArgs a) {
 // The spectrum slab F (written by consumers, read by producers) and the gain
 // accumulators live in TMEM; thread t of either role owns lane t % 128.
 // ---------------------------------------------------------------------------
-template <int N, int C>
-struct GeoP {
-    static constexpr int P = N / C;
-    static constexpr int ROW = N + 1;
-    static constexpr int PLANE = N * ROW;
-    static constexpr int SLAB = P * PLANE;
 #ifndef HK_SLOTS
-#define HK_SLOTS 2  // config 2: D = 2 46.2 ms, 3 46.8, 4 48.7 (final 12-warp kernel; the 8-warp kernel preferred 3)
+#define HK_SLOTS 2  // exchange slots per team, config 2: D = 2 46.2 ms, 3 46.8, 4 48.7
 #endif
-    static constexpr int D = HK_SLOTS;  // exchange slots in flight per team
-    static_assert(P * N == 128, "one pencil per role thread");
-    static constexpr uint32_t TM_COLS = 256;
-    static constexpr size_t SMEM = size_t(3 * SLAB) * sizeof(double2) + 8 * sizeof(double) + 32;
-    static constexpr size_t XCHG_PER_TEAM = size_t(D) * C * P * N * N * sizeof(double2);
-};
-
-// ---------------------------------------------------------------------------
-// FAST path, warp-autonomous pipeline (production kernel for N = 32).
-// Teams of C CTAs exchanging through L2 slots, F and gain in TMEM; every
-// warp is its own pipeline over ONE plane: producer warp p handles the 32
-// pencils (i1 = rP + p, i2 = lane), consumer warp c the j3 plane c; the only
-// CTA-wide barrier left is the cooperative f load of the prologue.  Next-round
-// weights are prefetched with cp.async into the producer warp's shared-memory
-// plane, so the L2 latency of the tables overlaps the current round.
-// Slot counters count warps: 8 CTAs x 4 warps = 32 arrivals per use.
-// ---------------------------------------------------------------------------
-// DEFER (off by default, HK_FAST_KERNEL=d): a producer warp publishes field e
-// only after computing field e+1, so the release fence finds the stores long
-// completed — measured 10 % slower: the consumers already wait on `ready`
-// (17.5 % of cycles vs 12 % producer spin on `done`, HK_PROF_SPIN), so the
-// team is latency-coupled and later publication costs more than the fence.
-// (Also measured and removed: moving every other field's i2 transform from
-// the consumers to the producers to balance the 2:1 transform count: 27 %
-// slower, the producers became the late side.)
-template <int N, int C, bool DEFER>
-__global__ void __launch_bounds__(256, 1) coll_fast_warp_kernel(CollArgs a) {
-    using G = GeoP<N, C>;
-    constexpr int P = G::P, ROW = G::ROW, PLANE = G::PLANE, D = G::D;
-    static_assert(P == 4 && N == 32, "one plane per warp: N = 32, P = 4");
-    constexpr int64_t NB = (int64_t)N * N * N;
-    constexpr int BLK = P * N * N;
-    constexpr int64_t SLOT = (int64_t)C * BLK;
-    constexpr unsigned ARR = C * P;  // arrivals per slot use
-    extern __shared__ __align__(16) double2 smem[];
-    double2* Rvb = smem;               // consumer landing [2][P planes][N][ROW]
-    double2* Pw = smem + 2 * G::SLAB;  // producer: prologue block / per-warp weight planes
-    uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * G::SLAB);  // [P]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
-
-    const int t = threadIdx.x;
-    const int warp = t >> 5, lane = t & 31;
-    const int pw = warp & 3;  // plane of this warp (either role)
-    const bool producer = t < 128;
-    const unsigned team = blockIdx.x / C, r = blockIdx.x % C, nteams = gridDim.x / C;
-    const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
-    double2* X = a.xchg + (int64_t)team * D * SLOT;
-    unsigned* ready = a.team_ctr + (int64_t)team * 2 * D;
-    unsigned* done = ready + D;
-
-    if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
-    if (t < P) mbar_init(smem_u32(fbar + t), 32);
-    if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    const uint32_t tm = *tslot + ((uint32_t)(32 * pw) << 16);
-    const uint32_t tmF = tm, tmG = tm + 4 * N;
-    const int n_entries = a.md + 1;
-    unsigned g = 0, ncell = 0;
-
-    if (producer) {
-        // ================================ PRODUCER WARP ================================
-        const int i1 = r * P + pw, i2 = lane;
-        double2* wbuf = Pw + pw * PLANE;  // [i3][lane] weights of the next round
-        const uint32_t wbuf_s = smem_u32(wbuf);
-        auto issue_w = [&](int e) {
-            const double2* wt = a.wfast + (int64_t)e * NB + (int64_t)i1 * N * N + i2;
-#pragma unroll
-            for (int i3 = 0; i3 < N; ++i3) cp_async16(wbuf_s + (i3 * 32 + lane) * 16, wt + i3 * N);
-            cp_async_commit();
-        };
-        long long spin_cyc = 0;
-        const long long t_start = clock64();
-        auto acquire = [&](unsigned gg) {
-            if (lane == 0) spin_cyc += spin_geq(done + gg % D, ARR * (gg / D));
-            __syncwarp();
-        };
-        auto publish = [&](unsigned gg) {
-            __syncwarp();
-            if (lane == 0) signal_add(ready + gg % D);
-        };
-        unsigned pend = ~0u;  // DEFER: field stored but not yet published
-        auto flush = [&]() {
-            if (pend != ~0u) publish(pend);
-            pend = ~0u;
-        };
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            // ---- prologue: f block (cooperative), 2-D forward transform of plane j3l = pw ----
-            flush();  // previous cell's loss field
-            if (a.in_ready && t == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);  // host chunk has landed
-            named_bar(1, 128);  // every producer warp is done with its weight plane
-            for (int idx = t; idx < N * N * P; idx += 128) {
-                const int j3l = idx % P, j2 = (idx / P) % N, j1 = idx / (P * N);
-                Pw[j3l * PLANE + j1 * ROW + j2] = make_double2(fc[(j1 * N + j2) * N + r * P + j3l], 0.0);
-            }
-            named_bar(1, 128);
-            {
-                double2* row = Pw + pw * PLANE + lane * ROW;  // (j3l = pw, j1 = lane)
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = row[i];
-                fft_reg<N, false>(x);
-#pragma unroll
-                for (int i = 0; i < N; ++i) row[i] = x[i];
-            }
-            __syncwarp();
-            {
-                const int j3 = r * P + pw, k2 = lane;
-                const double2* col = Pw + pw * PLANE + k2;
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = col[i * ROW];
-                fft_reg<N, false>(x);
-                __syncwarp();  // plane reads done: the weight prefetch may overwrite it
-                issue_w(0);
-                acquire(g);
-                double2* Xs = X + (int64_t)(g % D) * SLOT;
-#pragma unroll
-                for (int k1 = 0; k1 < N; ++k1)
-                    st_cg16(Xs + (int64_t)(k1 / P) * BLK + ((k1 % P) * N + k2) * N + j3, x[k1]);
-                publish(g);
-                ++g;
-            }
-            mbar_wait_parity(smem_u32(fbar + pw), ncell & 1);  // consumers put F(plane) in TMEM
-            tmem_fence_after();
-            // ---- phase A for every field ----
-            for (int e = 0; e < n_entries; ++e) {
-                // F (this pencil's 32 complex = 128 TMEM columns): four x32 loads, ONE wait,
-                // issued before the weights are read so the TMEM latency overlaps them
-                double2 x[N];
-                {
-                    uint32_t r0[32], r1[32], r2[32], r3[32];
-                    tmem_ld32_nowait(tmF, r0);
-                    tmem_ld32_nowait(tmF + 32, r1);
-                    tmem_ld32_nowait(tmF + 64, r2);
-                    tmem_ld32_nowait(tmF + 96, r3);
-                    cp_async_wait_all();
-                    __syncwarp();
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) {
-                        x[m] = make_double2(tmem_pair(r0[4 * m], r0[4 * m + 1]), tmem_pair(r0[4 * m + 2], r0[4 * m + 3]));
-                        x[8 + m] = make_double2(tmem_pair(r1[4 * m], r1[4 * m + 1]), tmem_pair(r1[4 * m + 2], r1[4 * m + 3]));
-                        x[16 + m] = make_double2(tmem_pair(r2[4 * m], r2[4 * m + 1]), tmem_pair(r2[4 * m + 2], r2[4 * m + 3]));
-                        x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
-                    }
-                }
-#pragma unroll
-                for (int i3 = 0; i3 < N; ++i3) {
-                    const double2 w = wbuf[i3 * 32 + lane], v = x[i3];
-                    x[i3] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
-                }
-                __syncwarp();
-                if (e + 1 < n_entries) issue_w(e + 1);
-                fft_reg<N, true>(x);
-                if (DEFER) flush();  // field e-1: its stores completed during this FFT
-                acquire(g);
-                double2* Xs = X + (int64_t)(g % D) * SLOT;
-#pragma unroll
-                for (int j3 = 0; j3 < N; ++j3)
-                    st_cg16(Xs + (int64_t)(j3 / P) * BLK + ((j3 % P) * N + i1) * N + i2, x[j3]);
-                if (DEFER)
-                    pend = g;
-                else
-                    publish(g);
-                ++g;
-            }
-        }
-        flush();
-        if (a.prof && lane == 0) {
-            atomicAdd(&a.prof[0], (unsigned long long)spin_cyc);
-            atomicAdd(&a.prof[2], (unsigned long long)(clock64() - t_start));
-        }
-    } else {
-        // ================================ CONSUMER WARP ================================
-        const int pl = pw;  // my plane: k1l (prologue) / j3l (rounds)
-        long long spin_cyc = 0;
-        const long long t_start = clock64();
-        auto pull = [&](unsigned gg) {
-            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + pl * N * N;
-            const uint32_t d0 = smem_u32(Rvb + (gg & 1) * G::SLAB + pl * PLANE);
-#pragma unroll 8
-            for (int k = 0; k < N; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
-            cp_async_commit();
-        };
-        auto issue = [&](unsigned gg) {  // wait until every producer warp published gg, then pull
-            if (lane == 0) spin_cyc += spin_geq(ready + gg % D, ARR * (gg / D + 1));
-            __syncwarp();
-            pull(gg);
-        };
-        auto try_issue = [&](unsigned gg) -> bool {  // pull gg if it is already published
-            unsigned v = 0;
-            if (lane == 0) asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(ready + gg % D) : "memory");
-            v = __shfl_sync(0xffffffffu, v, 0);
-            if ((int)(v - ARR * (gg / D + 1)) < 0) return false;
-            pull(gg);
-            return true;
-        };
-        auto complete = [&](unsigned gg) {
-            cp_async_wait_all();
-            __syncwarp();
-            if (lane == 0) signal_add_relaxed(done + gg % D);
-        };
-        if ((int64_t)team < count) issue(g);
-        for (int64_t it = team; it < count; it += nteams, ++ncell) {
-            const int64_t cell = a.list ? a.list[it] : it;
-            const double* fc = a.f + cell * NB;
-            // ---- prologue: forward over k3 of rows (k1l = pl, k2 = lane), F -> TMEM ----
-            complete(g);
-            {
-                const double2* row = Rvb + (g & 1) * G::SLAB + pl * PLANE + lane * ROW;
-                const int k1 = r * P + pl, k2 = lane;
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = row[i];
-                fft_reg<N, false>(x);
-                const double s = 1.0 / double(NB);
-#pragma unroll
-                for (int c = 0; c < N / 4; ++c) {
-                    double v[8];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        v[2 * i] = x[4 * c + i].x * s;
-                        v[2 * i + 1] = x[4 * c + i].y * s;
-                    }
-                    tmem_st16(tmF + 16 * c, v);
-                }
-                if (a.nyq) {
-                    constexpr int H = N / 2;
-                    double2* ny = a.nyq + cell * 3 * N * N;
-                    ny[2 * N * N + k1 * N + k2] = make_double2(s * x[H].x, s * x[H].y);
-                    if (k2 == H) {
-#pragma unroll
-                        for (int c = 0; c < N; ++c) ny[1 * N * N + k1 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                    }
-                    if (k1 == H) {
-#pragma unroll
-                        for (int c = 0; c < N; ++c) ny[k2 * N + c] = make_double2(s * x[c].x, s * x[c].y);
-                    }
-                }
-                const double z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-                for (int c = 0; c < N / 8; ++c) tmem_st16(tmG + 16 * c, z);
-                tmem_wait_st();
-                tmem_fence_before();
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(fbar + pl)) : "memory");
-            }
-            __syncwarp();
-            issue(g + 1);  // field 0 (needs F, published above)
-            ++g;
-            // ---- phase B for every field ----
-            for (int e = 0; e < n_entries; ++e) {
-                const bool is_loss = (e == a.md);
-                double2* Rv = Rvb + (g & 1) * G::SLAB + pl * PLANE;
-                complete(g);
-                const bool more = (e + 1 < n_entries) || (it + nteams < count);
-                // prefetch g+1 if it is published; otherwise transform g first
-                // instead of idling on the counter (second chance after the rows)
-                bool pending = more && !try_issue(g + 1);
-                {  // inverse FFT over i2: row i1 = lane of my j3 plane
-                    double2* row = Rv + lane * ROW;
-                    double2 y[N];
-#pragma unroll
-                    for (int i = 0; i < N; ++i) y[i] = row[i];
-                    fft_reg<N, true>(y);
-#pragma unroll
-                    for (int i = 0; i < N; ++i) row[i] = y[i];
-                }
-                __syncwarp();
-                if (pending) pending = !try_issue(g + 1);
-                double2 y[N];
-                {  // inverse FFT over i1: column j2 = lane
-                    const double2* col = Rv + lane;
-#pragma unroll
-                    for (int i = 0; i < N; ++i) y[i] = col[i * ROW];
-                    fft_reg<N, true>(y);
-                }
-                __syncwarp();  // reads of this buffer complete before it is refilled
-                if (pending) issue(g + 1);
-                if (!is_loss) {
-                    const double m = (e == 0) ? a.mult0 : 1.0;
-                    uint32_t g0[32], g1[32];  // the 32 gain accumulators: two x32 loads, one wait
-                    tmem_ld32_nowait(tmG, g0);
-                    tmem_ld32_nowait(tmG + 32, g1);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < N / 8; ++c) {
-                        double gv[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int k = 16 * (c & 1) + 2 * i;
-                            const double old = (c < 2) ? tmem_pair(g0[k], g0[k + 1]) : tmem_pair(g1[k], g1[k + 1]);
-                            gv[i] = old + m * (y[8 * c + i].x * y[8 * c + i].y);
-                        }
-                        tmem_st16(tmG + 16 * c, gv);
-                    }
-                    tmem_wait_st();
-                    ++g;
-                } else {
-                    // ---- epilogue: Q = jac (w gain - f loss) for nodes (j1, j2 = lane, j3 = rP + pl) ----
-                    double* qc = a.q + cell * NB;
-                    double mre = 0.0, n2 = 0.0, l2 = 0.0;
-#pragma unroll
-                    for (int c = 0; c < N / 8; ++c) {
-                        double gv[8];
-                        tmem_ld16(tmG + 16 * c, gv);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const int j1 = 8 * c + i;
-                            const int64_t gi = ((int64_t)j1 * N + lane) * N + r * P + pl;
-                            const double lt = fc[gi] * y[j1].x;
-                            const double qre = a.jac * (a.w * gv[i] - lt);
-                            qc[gi] = qre;
-                            mre = fmax(mre, fabs(qre));
-                            n2 += qre * qre;
-                            l2 += lt * lt;
-                        }
-                    }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) {
-                        mre = fmax(mre, __shfl_xor_sync(0xffffffffu, mre, o));
-                        n2 += __shfl_xor_sync(0xffffffffu, n2, o);
-                        l2 += __shfl_xor_sync(0xffffffffu, l2, o);
-                    }
-                    if (lane == 0 && a.st) {
-                        hk_cell_status* sc = a.st + cell;
-                        atomic_max_nonneg(&sc->max_re, mre);
-                        atomicAdd(&sc->q_norm2, n2);
-                        atomicAdd(&sc->loss_norm2, a.jac * a.jac * l2);
-                    }
-                    __syncwarp();
-                    if (lane == 0 && a.out_done) signal_add(a.out_done + cell / a.chunk);  // q rows visible
-                    ++g;
-                }
-            }
-        }
-        if (a.prof && lane == 0) {
-            atomicAdd(&a.prof[1], (unsigned long long)spin_cyc);
-            atomicAdd(&a.prof[3], (unsigned long long)(clock64() - t_start));
-        }
-    }
-    tmem_fence_before();
-    __syncthreads();
-    tmem_fence_after();
-    if (warp == 0) tmem_dealloc(*tslot, G::TM_COLS);
-}
 
 // ---------------------------------------------------------------------------
 // FAST path, warp-autonomous pipeline with TWO planes per warp: a team of
@@ -1350,22 +992,16 @@ int launch_variant(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag)
 
 template <int N, int C>
 int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int tag) {
-    using G = GeoP<N, C>;
-    // Default: the 12-warp kernel (teams of 4 on all SMs).  HK_FAST_KERNEL=8
-    // selects the 8-warp kernel (teams of 8, 144 SMs; 52.0 vs 49.0 ms at
-    // config 2), =d the 8-warp kernel with deferred publish (+10 %).  Measured
-    // and removed: CTA-synchronous pipeline, 2-CTA/SM TMEM cluster, split
-    // pencils over lane pairs, two planes per warp with 4 + 4 warps.
-    const char* kv = getenv("HK_FAST_KERNEL");
-    const int variant = !kv ? 5 : (kv[0] == '8' ? 1 : (kv[0] == 'd' ? 3 : 5));
-    constexpr int CW = 4;  // team size of the 12-warp kernel
-    auto kern = variant == 1 ? coll_fast_warp_kernel<N, C, false>
-              : variant == 3 ? coll_fast_warp_kernel<N, C, true>
-                             : coll_fast_w12_kernel<N, CW>;
-    const int nthreads = variant == 5 ? 384 : 256;
-    const int TC = variant == 5 ? CW : C;  // CTAs per team
-    const size_t smem = variant == 5 ? GeoW<N, CW>::SMEM : G::SMEM;
-    const int key = N * 100 + C * 2 + 2000 + variant;
+    // The 12-warp kernel, teams of CW = 4 CTAs on all SMs.  Measured and removed
+    // (DESIGN.md §4.1): the 8-warp kernel (52.0 vs 49.0 ms at config 2), its
+    // deferred-publish variant (+10 %), a CTA-synchronous pipeline, a 2-CTA/SM
+    // TMEM cluster, split pencils over lane pairs, two planes per warp with 4 + 4 warps.
+    constexpr int CW = 4;
+    using G = GeoW<N, CW>;
+    auto kern = coll_fast_w12_kernel<N, CW>;
+    const int nthreads = 384;
+    const size_t smem = G::SMEM;
+    const int key = N * 100 + C * 2 + 2005;
     int st;
     if (!ctx->max_clusters.count(key)) {
         if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
@@ -1374,9 +1010,7 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
         int per_sm = 0;
         if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, smem), "occupancy")))
             return st;
-        int teams = (per_sm >= 1 ? 1 : 0) * ctx->sm_count / TC;  // one CTA per SM (TMEM, SMEM)
-        if (const char* m = getenv("HK_TEAMS")) teams = atoi(m);  // experiment override
-        if (getenv("HK_DEBUG")) fprintf(stderr, "[hk] pipe kernel: per_sm %d teams %d\n", per_sm, teams);
+        const int teams = (per_sm >= 1 ? 1 : 0) * ctx->sm_count / CW;  // one CTA per SM (TMEM, SMEM)
         if (teams < 1) return fail(ctx, HK_CUDA, "pipelined collision kernel cannot be resident");
         ctx->max_clusters[key] = teams;
     }
@@ -1384,7 +1018,7 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     if (max_cells < teams) teams = max_cells;
     if (teams < 1) return HK_OK;
     CollArgs args = args_in;
-    if (ctx->sio_in_ready) {  // streamed host I/O (every warp kernel)  // streamed host I/O (warp kernels only)
+    if (ctx->sio_in_ready) {  // streamed host I/O
         args.in_ready = ctx->sio_in_ready;
         args.out_done = ctx->sio_out_done;
         args.chunk = ctx->sio_chunk;
@@ -1394,7 +1028,11 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
                          "team counters")))
         return st;
     static unsigned long long* prof = nullptr;
-    const bool profiling = getenv("HK_PROF_SPIN") != nullptr;
+#if HK_PROFILING
+    const bool profiling = getenv("HK_PROF_SPIN") != nullptr;  // profiling builds only
+#else
+    const bool profiling = false;
+#endif
     if (profiling) {
         if (!prof) cudaMalloc(&prof, 256);
         cudaMemsetAsync(prof, 0, 256, ctx->stream);
@@ -1402,7 +1040,7 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
     }
     void* params[] = {&args};
     timing_begin(ctx, tag);
-    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * TC)), dim3(nthreads), params,
+    st = check_cuda(ctx, cudaLaunchCooperativeKernel((const void*)kern, dim3(unsigned(teams * CW)), dim3(nthreads), params,
                                                      smem, ctx->stream),
                     "pipelined collision kernel launch");
     timing_end(ctx);
@@ -1416,8 +1054,8 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
                     "stores %.1f, publish %.1f\n", 100.0 * h[8] / h[2], 100.0 * h[9] / h[2], 100.0 * h[10] / h[2],
                     100.0 * h[11] / h[2], 100.0 * h[12] / h[2], 100.0 * h[13] / h[2]);
         fprintf(stderr, "[hk prof] CTAs %lld: producer spin %.1f%% of %.3g cyc/CTA, consumer spin %.1f%% of %.3g cyc/CTA\n",
-                (long long)(teams * TC), 100.0 * h[0] / (double)h[2], h[2] / double(teams * TC), 100.0 * h[1] / (double)h[3],
-                h[3] / double(teams * TC));
+                (long long)(teams * CW), 100.0 * h[0] / (double)h[2], h[2] / double(teams * CW), 100.0 * h[1] / (double)h[3],
+                h[3] / double(teams * CW));
     }
     return st;
 }
@@ -1631,11 +1269,9 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
              hk_cell_status* st) {
     // N = 16: every cell's spectrum reaches the Nyquist planes, so the guard
     // would list them all; the exact kernel is the default there (the fast
-    // kernel stays reachable with HK_COLL_NOGUARD, the guarded fast path with
-    // HK_N16_GUARDED=1 for comparison).
-    static const bool n16_guarded = getenv("HK_N16_GUARDED") != nullptr;
+    // kernel stays reachable with HK_COLL_NOGUARD).
     const bool exact = (flags & (HK_COLL_EXACT | HK_COLL_STRICT)) != 0 ||
-                       (N == 16 && !(flags & HK_COLL_NOGUARD) && !n16_guarded);
+                       (N == 16 && !(flags & HK_COLL_NOGUARD));
     const bool guard = !exact && !(flags & HK_COLL_NOGUARD);
     const int64_t nn3 = 3LL * N * N;
     // scratch: [nyq |F| planes][reroute list][count]
@@ -1650,11 +1286,19 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
                            : 1;
     const size_t part_bytes = ksplit > 1 ? ((sizeof(double) * 4 * k->md * ncells + 255) & ~size_t(255)) : 0;
     const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255 + part_bytes) & ~size_t(255);
+    // exchange scratch of the kernel that runs (+ 64 KiB of team counters at the end)
     size_t xchg_bytes;
-    if constexpr (N == 64)
+    if constexpr (N == 64) {
         xchg_bytes = coll64_xchg_bytes(ctx) + 65536;
-    else
-        xchg_bytes = size_t(2 * ctx->sm_count / C + 1) * Geo<N, C>::XCHG_PER_CLUSTER + 65536;
+    } else {
+        const size_t cluster_kernel = size_t(2 * ctx->sm_count / C + 1) * Geo<N, C>::XCHG_PER_CLUSTER;
+        size_t team_kernel = 0;
+        if constexpr (N == 32 && C == 8) {
+            constexpr int CW = 4;
+            team_kernel = size_t(ctx->sm_count / CW) * GeoW<N, CW>::D * CW * (N / CW) * N * N * sizeof(double2);
+        }
+        xchg_bytes = (exact ? cluster_kernel : std::max(cluster_kernel, team_kernel)) + 65536;
+    }
     int s;
     if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
     char* base = static_cast<char*>(ctx->scratch);
@@ -1687,8 +1331,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
         if constexpr (N == 64)
             return launch_coll64(ctx, x, true, ncells, tag);
         else if constexpr (N == 16)
-            return getenv("HK_N16_CLUSTER8") ? launch_variant<N, C, true>(ctx, x, ncells, tag)
-                                             : launch_coll16(ctx, x, ncells, tag);
+            return launch_coll16(ctx, x, ncells, tag);
         else
             return launch_variant<N, C, true>(ctx, x, ncells, tag);
     };
@@ -1702,10 +1345,8 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
             done = true;
         }
         if constexpr (N == 32 && C == 8) {
-            if (!(flags & HK_COLL_LEGACY_FAST)) {
-                if ((s = launch_fast_pipe<N, C>(ctx, a, ncells, 0))) return s;
-                done = true;
-            }
+            if ((s = launch_fast_pipe<N, C>(ctx, a, ncells, 0))) return s;
+            done = true;
         }
         if constexpr (N != 64) {
             if (!done) {
@@ -1732,19 +1373,12 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
             timing_end(ctx);
             ctx->launches++;
             if ((s = check_cuda(ctx, cudaGetLastError(), "guard kernel"))) return s;
-            if (getenv("HK_GUARD_EXACT")) {  // comparison path: recompute the listed cells exactly
-                CollArgs b = a;
-                b.nyq = nullptr;
-                b.list = list;
-                b.list_count = count;
-                if ((s = launch_exact(b, 2))) return s;
-            } else {  // add the exact Nyquist term to the listed cells (hk_nyqfix.cu)
-                timing_begin(ctx, 2);
-                s = launch_nyq_fix(ctx, N, list, count, ncells, nyq, k->abs_a, k->abs_ap, k->md, k->mult0, k->jac,
-                                   k->weight, q, st);
-                timing_end(ctx);
-                if (s) return s;
-            }
+            // add the exact Nyquist term to the listed cells (hk_nyqfix.cu)
+            timing_begin(ctx, 2);
+            s = launch_nyq_fix(ctx, N, list, count, ncells, nyq, k->abs_a, k->abs_ap, k->md, k->mult0, k->jac,
+                               k->weight, q, st);
+            timing_end(ctx);
+            if (s) return s;
         }
     }
     {

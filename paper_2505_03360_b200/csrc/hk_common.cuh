@@ -10,6 +10,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef HK_PROFILING
+#define HK_PROFILING 0  // 1: HK_PROF_SPIN / HK_HYB_PROF reports (profiling builds only)
+#endif
+
 namespace hk {
 
 namespace cg = cooperative_groups;

@@ -186,8 +186,7 @@ int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, doub
     const int64_t total = (int64_t)p.nx * p.ny * p.n * p.n * p.n;
     if (total <= 0) return HK_OK;
     const int64_t nb = (int64_t)p.n * p.n * p.n;
-    static const bool old_path = getenv("HK_TRANSPORT_NODE") != nullptr;
-    if (!old_path && (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3) {
+    if ((p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3) {  // lane-per-column sweep (hk_transport.cu)
         int lg = 0;
         while ((1 << lg) < p.n) ++lg;
         return transport_march_launch(ctx, p, lg, f, out, lh, rh);

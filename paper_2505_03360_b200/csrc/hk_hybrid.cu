@@ -292,13 +292,13 @@ PR pr222_t() {  // ImexTableau::pr222 (inc/imex.hpp:23-34)
     return {1.0, 1.0 - C, C - delta, delta};
 }
 
-// HK_HYB_PROF=1: per-phase wall time (stream synchronised at each mark), stderr.
+// HK_HYB_PROF=1 (profiling builds, -DHK_PROFILING=1): per-phase wall time (stream synchronised at each mark), stderr.
 struct PhaseProf {
     bool on;
     cudaStream_t s;
     std::chrono::steady_clock::time_point t;
     std::string line;
-    explicit PhaseProf(cudaStream_t st) : on(getenv("HK_HYB_PROF") != nullptr), s(st) {
+    explicit PhaseProf(cudaStream_t st) : on(HK_PROFILING && getenv("HK_HYB_PROF") != nullptr), s(st) {
         if (on) {
             cudaStreamSynchronize(s);
             t = std::chrono::steady_clock::now();

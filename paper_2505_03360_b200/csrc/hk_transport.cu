@@ -65,115 +65,13 @@ __device__ __forceinline__ double cweno3_face(double um, double uc, double up, d
     return fma(inv, RIGHT ? fma(pc, mid, side) : fma(pc, mid, -side), uc);
 }
 
-// Transport sweep, y-marching (replaces the per-node kernel above for the
-// production path).  Thread (lane, ty) owns velocity node idx = 32 chunk +
-// lane of column i = IW group + ty and marches j = 0 .. ny-1: the y stencil
-// is a 5-value sliding window in registers (one new load per step) and the
-// upwind face computed at step j is the minus face of step j+1, so a step
-// costs one y reconstruction instead of two; the x neighbours are read by the
-// neighbouring column threads of the same CTA (L1 hits).  HBM traffic ~ one
-// read and one write of the field.
-constexpr int TIW = 8;  // columns per CTA
-#ifndef HK_TR_MINB
-#define HK_TR_MINB 2
-#endif
-template <bool FINAL>
-__global__ void __launch_bounds__(32 * TIW, HK_TR_MINB) transport_march_kernel(TransportParams p, int lg, const double* __restrict__ f,
-                                                                   double* __restrict__ out, const double* __restrict__ lh,
-                                                                   const double* __restrict__ rh, FinalCombine fc) {
-    const int n = p.n;
-    const int64_t nb = (int64_t)n * n * n;
-    const int lane = threadIdx.x, ty = threadIdx.y;
-    const int i = blockIdx.y * TIW + ty;
-    if (i >= p.nx) return;
-    const int64_t idx = (int64_t)blockIdx.x * 32 + lane;
-    const int k1 = (int)(idx >> (2 * lg)), k2 = (int)((idx >> lg) & (n - 1));
-    const double dv = 2.0 * p.vmax / n;
-    const double vx = -p.vmax + (k1 + 0.5) * dv, vy = -p.vmax + (k2 + 0.5) * dv;
-    const double inv_dx = 1.0 / p.dx, inv_dy = 1.0 / p.dy, eps = p.eps_weno;
-    const int xh = p.x_halo > 0 ? p.x_halo : 0;
-    const int nxi = p.nx + 2 * xh;
-    const int ny = p.ny;
-    auto at = [&](int ii, int jj) -> double {  // f at interior column ii (may be -2..nx+1), row jj (periodic)
-        jj = jj < 0 ? jj + ny : (jj >= ny ? jj - ny : jj);
-        if (p.x_halo < 0) {
-            if (ii < 0) return __ldg(lh + ((int64_t)jj * p.lnx + (p.lnx + ii)) * nb + idx);
-            if (ii >= p.nx) return __ldg(rh + ((int64_t)jj * p.rnx + (ii - p.nx)) * nb + idx);
-        } else if (p.x_halo == 0) {
-            ii = ii < 0 ? ii + p.nx : (ii >= p.nx ? ii - p.nx : ii);
-        }
-        return __ldg(f + ((int64_t)jj * nxi + ii + xh) * nb + idx);
-    };
-    // y window w[0..4] = f(i, j-2 .. j+2); upwind y face of the previous step
-    double w0 = at(i, -2), w1 = at(i, -1), w2 = at(i, 0), w3 = at(i, 1), w4 = at(i, 2);
-    const bool ypos = vy > 0.0, xpos = vx > 0.0;
-    double fy_prev;
-    {
-        double l, r;
-        if (ypos) {  // right face of cell j-1 = cweno3(w0, w1, w2).right
-            cweno3_faces(w0, w1, w2, eps, l, r);
-            fy_prev = r;
-        } else {     // left face of cell j = cweno3(w1, w2, w3).left
-            cweno3_faces(w1, w2, w3, eps, l, r);
-            fy_prev = l;
-        }
-    }
-    // Per-row loads are issued one row ahead (software pipelining): the
-    // marching loop is otherwise latency-bound on them.
-    auto row_loads = [&](int jj, double& nw4, double (&nx4)[4], double (&nf)[3]) {
-        nw4 = at(i, jj + 2);
-        nx4[0] = at(i - 2, jj); nx4[1] = at(i - 1, jj); nx4[2] = at(i + 1, jj); nx4[3] = at(i + 2, jj);
-        if constexpr (FINAL) {
-            const int64_t o = ((int64_t)jj * p.nx + i) * nb + idx;
-            nf[0] = fc.f[o]; nf[1] = __ldg(fc.q1 + o); nf[2] = __ldg(fc.k1 + o);
-        }
-    };
-    double cx4[4], cf[3] = {0, 0, 0}, cw4;
-    row_loads(0, cw4, cx4, cf);
-    for (int j = 0; j < ny; ++j) {
-        if (j > 0) {
-            w0 = w1; w1 = w2; w2 = w3; w3 = w4;
-            w4 = cw4;
-        }
-        const double xm2 = cx4[0], xm1 = cx4[1], xp1 = cx4[2], xp2 = cx4[3];
-        const double fv = cf[0], q1 = cf[1], k1 = cf[2];
-        if (j + 1 < ny) row_loads(j + 1, cw4, cx4, cf);
-        double fy_next, l, r;
-        if (ypos) {  // right face of cell j
-            cweno3_faces(w1, w2, w3, eps, l, r);
-            fy_next = r;
-        } else {     // left face of cell j+1
-            cweno3_faces(w2, w3, w4, eps, l, r);
-            fy_next = l;
-        }
-        double fxp, fxm;
-        if (xpos) {
-            cweno3_faces(xm1, w2, xp1, eps, l, fxp);
-            cweno3_faces(xm2, xm1, w2, eps, l, fxm);
-        } else {
-            cweno3_faces(w2, xp1, xp2, eps, fxp, r);
-            cweno3_faces(xm1, w2, xp1, eps, fxm, r);
-        }
-        const double fx = vx * (fxp - fxm), fy = vy * (fy_next - fy_prev);
-        const double tr = -fx * inv_dx - fy * inv_dy;
-        const int64_t o = ((int64_t)j * p.nx + i) * nb + idx;
-        if constexpr (!FINAL) {
-            out[o] = tr;
-            (void)fv; (void)q1; (void)k1;
-        } else {  // f += dt (w0 q1 + w1 q2) + w0 k1 + w1 k2 at this node (Y2 = w2)
-            const int64_t cell = (int64_t)j * p.nx + i;
-            const double q2 = fc.res ? tr + fc.res[o] / fc.eps[cell] : tr;
-            const double facc = fv + fc.dt * fc.a_ex10 * q1 + fc.a_im10 * k1;
-            const double k2 = (w2 - facc) * (1.0 / fc.a_im11);
-            fc.f[o] = fv + (fc.dt * (fc.w_ex0 * q1 + fc.w_ex1 * q2) + fc.w_im0 * k1 + fc.w_im1 * k2);
-        }
-        fy_prev = fy_next;
-    }
-}
-
-// Lane-per-column variant: lane l of a warp owns column i = 28 b - 2 + l for
-// NPT consecutive velocity nodes and marches down the rows like the kernel
-// above.  The x neighbours' centre values come from the neighbouring lanes
+// Transport sweep (production path): lanes march the rows j = 0 .. ny-1 with
+// the y stencil as a 5-value sliding window in registers (one new load per
+// step); the upwind face computed at step j is the minus face of step j+1, so
+// a step costs one y reconstruction instead of two.  (A thread-per-column
+// variant with x neighbours through L1 was measured slower and removed.)
+// Lane-per-column sweep: lane l of a warp owns column i = 28 b - 2 + l for
+// NPT consecutive velocity nodes and marches down the rows.  The x neighbours' centre values come from the neighbouring lanes
 // (shuffles, no loads), and the x minus face of lane l is lane l-1's plus
 // face, so a row costs ONE x and ONE y reconstruction per node (2 instead of
 // 3); lanes 0, 1, 30, 31 are halo columns (no output).
@@ -355,32 +253,22 @@ int transport_row_activity(hk_ctx ctx, int nx, int ny, const int8_t* mask, uint8
 int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
                            const double* rh, const FinalCombine* fin) {
     const int64_t nb = (int64_t)p.n * p.n * p.n;
-    static const bool lanes = !getenv("HK_TRANSPORT_MARCH");
-    if (lanes) {  // lane-per-column kernel (default)
-        const dim3 grid(unsigned((p.nx + TL_OUT - 1) / TL_OUT), unsigned((nb / 2 + 3) / 4));
-        const size_t smem = p.row_act ? size_t(p.ny) : 0;
-        if (smem > 48 * 1024) return fail(ctx, HK_UNSUPPORTED, "transport: row activity needs ny <= 49152");
-        if (fin)
-            transport_lanes_kernel<true, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
-        else if (p.row_act)
-            transport_lanes_kernel<false, 2, true><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
-        else
-            transport_lanes_kernel<false, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
-        ctx->launches++;
-        return check_cuda(ctx, cudaGetLastError(), "transport kernel");
-    }
-    const dim3 grid(unsigned(nb / 32), unsigned((p.nx + TIW - 1) / TIW));
+    const dim3 grid(unsigned((p.nx + TL_OUT - 1) / TL_OUT), unsigned((nb / 2 + 3) / 4));
+    const size_t smem = p.row_act ? size_t(p.ny) : 0;
+    if (smem > 48 * 1024) return fail(ctx, HK_UNSUPPORTED, "transport: row activity needs ny <= 49152");
     if (fin)
-        transport_march_kernel<true><<<grid, dim3(32, TIW), 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+        transport_lanes_kernel<true, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+    else if (p.row_act)
+        transport_lanes_kernel<false, 2, true><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
     else
-        transport_march_kernel<false><<<grid, dim3(32, TIW), 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+        transport_lanes_kernel<false, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "transport kernel");
 }
 
 bool transport_final_supported(const TransportParams& p) {
     const int64_t nb = (int64_t)p.n * p.n * p.n;
-    return (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3 && p.x_halo == 0 && !getenv("HK_TRANSPORT_NODE");
+    return (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3 && p.x_halo == 0;
 }
 
 int transport_final_launch(hk_ctx ctx, const TransportParams& p, const double* y2, const FinalCombine& fc) {
