@@ -345,6 +345,18 @@ typedef struct {
     int ghost_x;                /* x-slab use: columns i < ghost_x and i >= nx - ghost_x are exchanged
                                    ghosts whose results are discarded; their residuals are only evaluated
                                    where an interior cell depends on them (0: plain torus) */
+    /* Optional residual hook (NULL: evaluated here).  Called twice per step, at Y1
+     * and Y2, ALWAYS (also with m2 = 0 and null pointers, so that ranks that balance
+     * the work collectively stay in step): y_dev [m2][n^3] are the stage values of
+     * the layer-2 cells whose residual the step needs, in batch order; the hook
+     * writes penalized_residual(y) (src/boltzmann.cpp:9-27) to res_dev [m2][n^3]
+     * and a status per cell to status_dev [m2] (HK_OK or the HK_* code), with
+     * every device operation ordered on `stream` (the context's), and returns
+     * HK_OK or an error code.  partition.hybrid_step_slab uses it to spread the
+     * layer-2 cells of all x-slabs evenly over the ranks (dynamic load balancing). */
+    int (*residual_fn)(void* user, const double* y_dev, double* res_dev, int64_t m2, int* status_dev,
+                       void* stream);
+    void* residual_user;
 } hk_hybrid_params;
 int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx, double dy, double dt, const double* eps_dev,
                    int8_t* r_dev, double* hydro_dev, double* f_dev, const hk_hybrid_params* params, int64_t* counts);

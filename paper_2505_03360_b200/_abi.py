@@ -79,7 +79,11 @@ class HybridParams(C.Structure):
                 ("kappa0", C.c_double), ("signed_sum", C.c_int), ("update_regimes", C.c_int),
                 ("heat_ratio", C.c_double), ("esbgk_beta", C.c_double), ("nu_coeff", C.c_double),
                 ("pen_coeff", C.c_double), ("eps_weno", C.c_double), ("coll_flags", C.c_uint32),
-                ("ghost_x", C.c_int)]
+                ("ghost_x", C.c_int), ("residual_fn", C.c_void_p), ("residual_user", C.c_void_p)]
+
+
+# int (*)(void* user, const double* y, double* res, int64_t m2, int* status, void* stream)
+RESIDUAL_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
 
 
 _lib = None

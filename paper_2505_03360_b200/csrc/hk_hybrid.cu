@@ -447,6 +447,11 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
             return e;
         };
         auto residual = [&](const double* y, int64_t m2) -> int {  // penalized_residual of the first m2 layer-2 cells
+            if (p->residual_fn) {
+                const int e = p->residual_fn(p->residual_user, m2 ? y + n1 * nb : nullptr, m2 ? res + n1 * nb : nullptr,
+                                             m2, m2 ? stk2 + n1 : nullptr, (void*)s);
+                return e ? fail(ctx, e, "hybrid step: residual hook failed") : HK_OK;
+            }
             if (!m2) return HK_OK;
             int e = collision_launch(ctx, k, y + n1 * nb, res + n1 * nb, m2, p->coll_flags & ~HK_COLL_STRICT, nullptr);
             return e ? e : residual_finish_launch(ctx, n, vmax, y + n1 * nb, res + n1 * nb, m2, p->pen_coeff, stk2 + n1);
@@ -502,6 +507,10 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
             check_status(stk2);  // residual at Y2 (cells past n1 + n2_y2 keep their Y1 status: ghosts, skipped)
         }
         if (st) return st;
+    } else if (p->residual_fn) {  // no kinetic cell here: still take part in both (collective) hook calls
+        for (int k2 = 0; k2 < 2; ++k2)
+            if ((st = p->residual_fn(p->residual_user, nullptr, nullptr, 0, nullptr, (void*)s)))
+                return fail(ctx, st, "hybrid step: residual hook failed");
     }
     commit_kernel<<<nblk(cells, 256), 256, 0, s>>>(cells, r_new, r_dev, W, hydro_dev, euler ? 1 : 0);
     ctx->launches++;

@@ -412,7 +412,37 @@ class HybridParams:
         return _abi.HybridParams(self.eta0, self.eta1, self.delta0, self.mu0, self.kappa0, int(self.signed_sum),
                                  int(self.update_regimes), self.heat_ratio, self.esbgk_beta, self.nu_coeff,
                                  self.pen_coeff, self.eps_weno, _abi.HK_COLL_EXACT if self.exact else 0,
-                                 int(self.ghost_x))
+                                 int(self.ghost_x), None, None)
+
+
+class _DeviceArray:
+    """A raw device pointer as a CUDA-array-interface object (zero-copy torch view)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr or 0, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def device_view(ptr: int, shape, dtype=torch.float64, device=None) -> torch.Tensor:
+    """torch tensor over `ptr` (no copy); empty when shape has a zero."""
+    if not ptr or 0 in tuple(shape):
+        return torch.empty(tuple(shape), dtype=dtype, device=device or "cuda")
+    typestr = {torch.float64: "<f8", torch.int32: "<i4"}[dtype]
+    return torch.as_tensor(_DeviceArray(ptr, shape, typestr), device=device or "cuda")
+
+
+def penalized_residual_rows(kernel: SpectralKernel, y: torch.Tensor, pen_coeff: float = 2.0 * math.pi,
+                            exact: bool = False):
+    """penalized_residual (src/boltzmann.cpp:9-27) of the rows of y [m, n^3] ->
+    (res [m, n^3], status int32 [m]) without raising (the hybrid step's hook form)."""
+    ctx = kernel.ctx
+    out = torch.empty_like(y)
+    st = torch.zeros(y.shape[0], dtype=torch.int32, device=y.device)
+    if y.shape[0]:
+        ctx.check(ctx._lib.hk_penalized_residual_batch(ctx.h, kernel.h, y.data_ptr(), out.data_ptr(), y.shape[0],
+                                                       pen_coeff, _abi.HK_COLL_EXACT if exact else 0, st.data_ptr(),
+                                                       None))
+    return out, st
 
 
 class HybridCounts(NamedTuple):
@@ -425,11 +455,15 @@ class HybridCounts(NamedTuple):
 
 
 def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, dt: float, eps_cell, r, hydro, f,
-                params: HybridParams = HybridParams()) -> HybridCounts:
+                params: HybridParams = HybridParams(), residual_hook=None) -> HybridCounts:
     """One hybrid step in place on device tensors: r [cells] int8, hydro [cells, 4]
     conserved, f [cells, n^3] dense, eps_cell [cells].  Algorithm 1 regime update,
     convert_on_transition, Euler TVD-RK2 on layer 0, PR(2,2,2) ES-BGK / penalized
-    Boltzmann on layers 1 / 2 with the cross-layer transport halo."""
+    Boltzmann on layers 1 / 2 with the cross-layer transport halo.
+
+    residual_hook(y, res, status): optional evaluator of the layer-2 residuals
+    (hk_hybrid_params.residual_fn): y / res [m2, n^3] and status int32 [m2]
+    device views; called twice per step, also with m2 = 0."""
     ctx = kernel.ctx
     cells = nx * ny
     for name, t, dt_, width in (("r", r, torch.int8, 1), ("hydro", hydro, torch.float64, 4),
@@ -443,6 +477,24 @@ def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, 
         raise contract_violation(f"hybrid_step: eps_cell has {e.numel()} elements, expected {cells}")
     counts = (C.c_int64 * 6)()
     hp = params.to_c()
-    ctx.check(ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),
-                                      hydro.data_ptr(), f.data_ptr(), C.byref(hp), counts))
+    errors = []
+    if residual_hook is not None:
+        nb = kernel.modes()
+
+        def _hook(user, y_ptr, res_ptr, m2, st_ptr, stream):
+            try:
+                residual_hook(device_view(y_ptr, (m2, nb), device=f.device), device_view(res_ptr, (m2, nb), device=f.device),
+                              device_view(st_ptr, (m2,), torch.int32, device=f.device))
+                return 0
+            except Exception as exc:  # reported after the call (a C frame cannot unwind Python)
+                errors.append(exc)
+                return _abi.HK_CONTRACT
+
+        cb = _abi.RESIDUAL_FN(_hook)
+        hp.residual_fn = C.cast(cb, C.c_void_p)
+    st = ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),
+                                 hydro.data_ptr(), f.data_ptr(), C.byref(hp), counts)
+    if errors:
+        raise errors[0]
+    ctx.check(st)
     return HybridCounts(*[int(c) for c in counts])

@@ -286,16 +286,24 @@ def hybrid_unpad(part: XSlab, width: int, padded, fields):
 
 def hybrid_step_slab(part: XSlab, kernel, dx: float, dy: float, dt: float, eps_cell: torch.Tensor, r: torch.Tensor,
                      hydro: torch.Tensor, f: torch.Tensor, params=None, group=None, width: int = HYB_GHOST,
-                     halos=None):
+                     halos=None, balance: bool = False, residual_hook=None):
     """hk_hybrid_step on one x-slab, in place (r [cells] int8, hydro [cells,4], f [cells,n^3],
     eps [cells]; local cell order j*nxl + i).  One exchange of `width` columns of
     (r, eps, hydro, f) per side, then the step on the padded local torus; the
     interior is exactly the global step's.  Returns the global layer counts
     [n0, n1, n2] (all-reduced).  `halos` (tests) supplies the exchanged columns
-    directly: [(left, right)] for r, eps, hydro, f as [ny][width][k]."""
+    directly: [(left, right)] for r, eps, hydro, f as [ny][width][k].
+
+    balance (SURVEY §8f "next" #3): the layer-2 residuals of the step (the
+    collision evaluations, its dominant cost when Boltzmann cells cluster at
+    an interface) are spread evenly over the ranks: balanced_apply ships the
+    surplus stage values of over-loaded ranks to under-loaded ones, evaluates
+    dense batches and returns the results; per-cell operators are
+    deterministic, so the step is bitwise the unbalanced one.
+    residual_hook: an explicit hk_hybrid_params.residual_fn (see kinetic.hybrid_step)."""
     import dataclasses
 
-    from .kinetic import HybridParams, hybrid_step
+    from .kinetic import HybridParams, hybrid_step, penalized_residual_rows
 
     # ghost results are discarded: their residuals only where an interior cell depends on them
     params = dataclasses.replace(params or HybridParams(), ghost_x=width)
@@ -306,8 +314,17 @@ def hybrid_step_slab(part: XSlab, kernel, dx: float, dy: float, dt: float, eps_c
             lh, rh = part.halo_buffers(t.shape[-1], t, width)
             part.exchange(t, lh, rh, group, width=width)
             halos.append((lh, rh))
+    if balance and residual_hook is None:
+        def residual_hook(y, res, status):
+            fn = lambda rows: penalized_residual_rows(kernel, rows, params.pen_coeff, params.exact)[0]  # noqa: E731
+            cells = torch.arange(y.shape[0], dtype=torch.int64, device=y.device)
+            out, _ = balanced_apply(y, cells, fn, group)
+            if y.shape[0]:
+                res.copy_(out)
+                status.zero_()
     pr, pe, ph, pf = hybrid_pad(part, width, fields, halos)
-    hybrid_step(kernel, part.nxl + 2 * width, part.ny, dx, dy, dt, pe.view(-1), pr.view(-1), ph, pf, params)
+    hybrid_step(kernel, part.nxl + 2 * width, part.ny, dx, dy, dt, pe.view(-1), pr.view(-1), ph, pf, params,
+                residual_hook=residual_hook)
     hybrid_unpad(part, width, [pr, ph, pf], [fields[0], hydro, f])
     return regime_counts(r, group)
 
@@ -423,16 +440,26 @@ def balanced_apply(local: torch.Tensor, cells: torch.Tensor, fn, group=None):
     out_split = [send[rank][s] for s in range(world)]
     in_split = [send[s][rank] for s in range(world)]
     nb = local.shape[1]
-    if local.is_cuda:
+    if local.is_cuda and len(cells):
         from .kinetic import gather_cells
         batch = gather_cells(local, cells)
     else:
         batch = local[cells]
+    host_stage = local.is_cuda and dist.get_backend(group) == "gloo"  # gloo moves host tensors only (tests)
+
+    def a2a(out, inp, osplit, isplit):
+        if host_stage:
+            o = out.cpu()
+            dist.all_to_all_single(o, inp.cpu(), osplit, isplit, group=group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, osplit, isplit, group=group)
+
     ship = batch[keep:].contiguous()
     recv = torch.empty((sum(in_split), nb), dtype=local.dtype, device=local.device)
-    dist.all_to_all_single(recv, ship, in_split, out_split, group=group)
+    a2a(recv, ship, in_split, out_split)
     work = torch.cat([batch[:keep], recv]) if recv.numel() else batch[:keep]
     res = fn(work)
     back = torch.empty((sum(out_split), nb), dtype=local.dtype, device=local.device)
-    dist.all_to_all_single(back, res[keep:].contiguous(), out_split, in_split, group=group)
+    a2a(back, res[keep:].contiguous(), out_split, in_split)
     return torch.cat([res[:keep], back]), send

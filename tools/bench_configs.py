@@ -270,6 +270,108 @@ def config4_slabs(world=8, steps=3, weighted=False):
                     "sum_slab_ms / single-GPU step = redundant-work factor of the decomposition"}
 
 
+def config4_slabs_balanced(world=8, steps=3):
+    """config4_slabs with the layer-2 residuals load-balanced across the slabs
+    (partition.balanced_apply through hk_hybrid_step's residual hook), emulated on
+    one GPU: each slab's step is timed with its own residuals evaluated locally
+    (CUDA events around the hook's evaluation give R_q), then the balanced
+    per-rank residual batch (ceil(total / world) cells per call) is timed on real
+    stage values (R_bal), and each slab's balanced step time is
+    T_q - R_q + R_bal + the two all-to-alls of the shipped cells at 700 GB/s."""
+    import math as _m
+    from paper_2505_03360_b200.partition import HYB_GHOST as W, XSlab, hybrid_step_slab
+    nx = ny = 200
+    n, a1, a2 = 32, 4, 8
+    nb = n ** 3
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    k = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    hydro, eps, r, _ = inputs.config4_hybrid_state(nx, ny, n, with_f=False)
+    hd, ed, rd = (torch.from_numpy(x).cuda() for x in (hydro, eps, r))
+    f = kinetic.conserved_to_maxwellian(hd, vg)
+    dx = 1.0 / nx
+    dt = 0.5 * dx / (inputs.VMAX - inputs.VMAX / n)
+    parts = [XSlab(nx, ny, world, q) for q in range(world)]
+    loc = [[p_.scatter(t.view(nx * ny, -1)) for t in (rd, ed, hd, f)] for p_ in parts]
+    del f
+    torch.cuda.empty_cache()
+    mode = {"collect": False}
+    store = [[None, None] for _ in parts]
+    rec = []  # per timed step: [(m, residual ms) per call] per slab
+
+    def make_hook(q, calls):
+        def hook(y, res, status):
+            kcall = len(calls)
+            if mode["collect"]:
+                store[q][kcall] = y.clone()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out, st = kinetic.penalized_residual_rows(k, y)
+            e1.record()
+            if y.shape[0]:
+                res.copy_(out)
+                status.copy_(st)
+            calls.append((y.shape[0], e0, e1))
+        return hook
+
+    def step(timed):
+        halos = []
+        for q, p_ in enumerate(parts):
+            lt, rt = loc[(q - 1) % world], loc[(q + 1) % world]
+            lp, rp = parts[(q - 1) % world], parts[(q + 1) % world]
+            halos.append([(lt[fi].view(ny, lp.nxl, -1)[:, -W:].contiguous(),
+                           rt[fi].view(ny, rp.nxl, -1)[:, :W].contiguous()) for fi in range(4)])
+        out = []
+        for q, p_ in enumerate(parts):
+            rl, el, hl, fl = loc[q]
+            calls = []
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            hybrid_step_slab(p_, k, dx, dx, dt, el.view(-1), rl.view(-1), hl, fl, halos=halos[q],
+                             residual_hook=make_hook(q, calls))
+            s1.record()
+            out.append((s0, s1, calls))
+        torch.cuda.synchronize()
+        if timed:
+            rec.append([(s0.elapsed_time(s1), [(m, e0.elapsed_time(e1)) for m, e0, e1 in calls]) for s0, s1, calls in out])
+
+    for _ in range(2):
+        step(False)
+    mode["collect"] = True
+    step(False)
+    mode["collect"] = False
+    for _ in range(steps):
+        step(True)
+    T = [sum(rec[t][q][0] for t in range(steps)) / steps for q in range(world)]
+    Rq = [sum(sum(ms for _, ms in rec[t][q][1]) for t in range(steps)) / steps for q in range(world)]
+    ms_bal, a2a = [], []
+    for kc in range(2):
+        tot = sum(rec[0][q][1][kc][0] for q in range(world))
+        avg = _m.ceil(tot / world)
+        pool = torch.cat([store[q][kc] for q in range(world) if store[q][kc] is not None and store[q][kc].shape[0]])
+        rows = pool[:avg].contiguous() if avg else pool[:0]
+        kinetic.penalized_residual_rows(k, rows)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            kinetic.penalized_residual_rows(k, rows)
+        e1.record()
+        torch.cuda.synchronize()
+        ms_bal.append(e0.elapsed_time(e1) / 3)
+        shipped = max(abs(rec[0][q][1][kc][0] - avg) for q in range(world))
+        a2a.append(2 * shipped * nb * 8 / 700e9 * 1e3)
+    est = [T[q] - Rq[q] + sum(ms_bal) + sum(a2a) for q in range(world)]
+    return {"config": f"config4 on {world} x-slabs, layer-2 residuals load-balanced (balanced_apply via the "
+                      f"hk_hybrid_step residual hook), emulated on 1 GPU",
+            "slab_columns": [p_.nxl for p_ in parts], "unbalanced_ms_per_slab_step": T,
+            "residual_ms_per_slab_step": Rq, "layer2_rows_per_call": [[rec[0][q][1][kc][0] for q in range(world)]
+                                                                        for kc in range(2)],
+            "balanced_residual_ms_per_call": ms_bal, "alltoall_ms_per_call_at_700GBps": a2a,
+            "ms_per_slab_step": est, "max_slab_ms": max(est), "sum_slab_ms": sum(est),
+            "note": "ms_per_slab_step = T_q - R_q + balanced residual time + all-to-all estimate; "
+                    "max_slab_ms ~ per-GPU step time of an 8-GPU run without the halo exchange"}
+
+
 def config5(iters, steps=True):
     """Config 5, one GPU's x-slab (64 x 128 cells, N = 64, M = 8 x 8): Q over
     the slab (fast path + guard) and, with `steps`, one PR(2,2,2) IMEX step of
@@ -330,6 +432,8 @@ if __name__ == "__main__":
             r = config4_slabs()
         elif c == "4w":
             r = config4_slabs(weighted=True)
+        elif c == "4b":
+            r = config4_slabs_balanced()
         elif c == "4h":
             r = config4_hybrid(args.hyb_steps, full_sample=not args.no_full)
         elif c == "5":
