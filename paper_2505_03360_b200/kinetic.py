@@ -432,12 +432,13 @@ def device_view(ptr: int, shape, dtype=torch.float64, device=None) -> torch.Tens
 
 
 def penalized_residual_rows(kernel: SpectralKernel, y: torch.Tensor, pen_coeff: float = 2.0 * math.pi,
-                            exact: bool = False):
+                            exact: bool = False, out=None, status=None):
     """penalized_residual (src/boltzmann.cpp:9-27) of the rows of y [m, n^3] ->
-    (res [m, n^3], status int32 [m]) without raising (the hybrid step's hook form)."""
+    (res [m, n^3], status int32 [m]) without raising (the hybrid step's hook form);
+    out / status: preallocated destinations (no allocation on the hook path)."""
     ctx = kernel.ctx
-    out = torch.empty_like(y)
-    st = torch.zeros(y.shape[0], dtype=torch.int32, device=y.device)
+    out = torch.empty_like(y) if out is None else out
+    st = torch.zeros(y.shape[0], dtype=torch.int32, device=y.device) if status is None else status
     if y.shape[0]:
         ctx.check(ctx._lib.hk_penalized_residual_batch(ctx.h, kernel.h, y.data_ptr(), out.data_ptr(), y.shape[0],
                                                        pen_coeff, _abi.HK_COLL_EXACT if exact else 0, st.data_ptr(),

@@ -316,12 +316,7 @@ def hybrid_step_slab(part: XSlab, kernel, dx: float, dy: float, dt: float, eps_c
             halos.append((lh, rh))
     if balance and residual_hook is None:
         def residual_hook(y, res, status):
-            fn = lambda rows: penalized_residual_rows(kernel, rows, params.pen_coeff, params.exact)[0]  # noqa: E731
-            cells = torch.arange(y.shape[0], dtype=torch.int64, device=y.device)
-            out, _ = balanced_apply(y, cells, fn, group)
-            if y.shape[0]:
-                res.copy_(out)
-                status.zero_()
+            balanced_residual(kernel, y, res, status, params.pen_coeff, params.exact, group)
     pr, pe, ph, pf = hybrid_pad(part, width, fields, halos)
     hybrid_step(kernel, part.nxl + 2 * width, part.ny, dx, dy, dt, pe.view(-1), pr.view(-1), ph, pf, params,
                 residual_hook=residual_hook)
@@ -463,3 +458,57 @@ def balanced_apply(local: torch.Tensor, cells: torch.Tensor, fn, group=None):
     back = torch.empty((sum(out_split), nb), dtype=local.dtype, device=local.device)
     a2a(back, res[keep:].contiguous(), out_split, in_split)
     return torch.cat([res[:keep], back]), send
+
+
+def balanced_residual(kernel, y: torch.Tensor, res: torch.Tensor, status: torch.Tensor, pen_coeff: float = 6.283185307179586,
+                      exact: bool = False, group=None):
+    """res = penalized_residual(y) for this rank's layer-2 batch y [m, n^3], the
+    work of all ranks' batches spread evenly (balance_plan): the first `keep`
+    rows are evaluated here straight into res, the surplus rows go out in one
+    all-to-all, the received rows are evaluated as one dense batch and their
+    results come back in a second all-to-all (into res[keep:]).  Statuses of
+    shipped rows are evaluated by the receiving rank, which raises on failure.
+    Returns the plan.  Collective: every rank calls it, also with m = 0."""
+    from .kinetic import penalized_residual_rows
+
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    m = y.shape[0]
+    if world == 1:
+        penalized_residual_rows(kernel, y, pen_coeff, exact, out=res, status=status)
+        return [[m]]
+    rank = dist.get_rank(group)
+    counts = [None] * world
+    dist.all_gather_object(counts, int(m), group=group)
+    send = balance_plan(counts)
+    keep = counts[rank] - sum(send[rank])
+    out_split = [send[rank][s] for s in range(world)]
+    in_split = [send[s][rank] for s in range(world)]
+    nb = kernel.modes()
+    host_stage = y.is_cuda and dist.get_backend(group) == "gloo"
+
+    def a2a(out, inp, osplit, isplit):
+        if not sum(osplit) and not sum(isplit):
+            return
+        if host_stage:
+            o = out.cpu()
+            dist.all_to_all_single(o, inp.cpu(), osplit, isplit, group=group)
+            out.copy_(o)
+        else:
+            dist.all_to_all_single(out, inp, osplit, isplit, group=group)
+
+    dev = kernel_device(kernel, y)
+    recv = torch.empty((sum(in_split), nb), dtype=torch.float64, device=dev)
+    a2a(recv, y[keep:], in_split, out_split)
+    if keep:
+        penalized_residual_rows(kernel, y[:keep], pen_coeff, exact, out=res[:keep], status=status[:keep])
+    back, back_st = penalized_residual_rows(kernel, recv, pen_coeff, exact)
+    a2a(res[keep:], back, out_split, in_split)
+    st_back = torch.empty(m - keep, dtype=torch.float64, device=dev)  # the evaluating ranks' statuses
+    a2a(st_back.view(-1, 1), back_st.to(torch.float64).view(-1, 1), out_split, in_split)
+    if m > keep:
+        status[keep:].copy_(st_back.to(torch.int32))
+    return send
+
+
+def kernel_device(kernel, like: torch.Tensor):
+    return like.device if like.numel() else torch.device("cuda", kernel.ctx.device)

@@ -13,7 +13,7 @@ import torch.distributed as dist
 
 import paper_2505_03360_b200 as hk
 from paper_2505_03360_b200 import inputs, kinetic
-from paper_2505_03360_b200.partition import HYB_GHOST as W, XSlab, balanced_apply, hybrid_step_slab
+from paper_2505_03360_b200.partition import HYB_GHOST as W, XSlab, balanced_residual, hybrid_step_slab
 
 rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
 dist.init_process_group("gloo")  # the balanced exchange is staged through host memory on gloo
@@ -47,12 +47,7 @@ def run(balance):
     plans = []
 
     def hook(y, res, status):
-        fn = lambda rows: kinetic.penalized_residual_rows(kern, rows)[0]  # noqa: E731
-        out, plan = balanced_apply(y, torch.arange(y.shape[0], dtype=torch.int64, device=y.device), fn)
-        plans.append(plan)
-        if y.shape[0]:
-            res.copy_(out)
-            status.zero_()
+        plans.append(balanced_residual(kern, y, res, status))
 
     rl, el, hl, fl = loc
     counts = hybrid_step_slab(part, kern, dx, dy, dt, el.view(-1), rl.view(-1), hl, fl, halos=halos_of(glob),
