@@ -1230,6 +1230,267 @@ __global__ void __launch_bounds__(MT, MINB) moments_cta_kernel(const double* __r
 }
 
 // ---------------------------------------------------------------------------
+// penalized_residual epilogue (src/boltzmann.cpp:14-26), one CTA per cell,
+// TWO streaming passes: q holds Q(f) on entry and
+//   Q + beta (f - M~) - (y0 + y.d + y4 |d|^2) M~
+// on exit.  The moment-matching and invariant-removal coupling matrices
+// (src/moments.cpp:164-189) are sums of polynomials times the Maxwellian M,
+// which is separable along (vx, vy, vz) in shifted coordinates, so both are
+// assembled from 1-D sums  C_a = sum_k (v_k - uc)^a e(k),  D_a = sum_k (v_k - u)^a e(k)
+// (a <= 4 / 6, e the per-axis Maxwellian factors) instead of two passes over
+// the N^3 nodes; the invariant moments of Q + beta (f - M~) follow from pass-1
+// sums of q and f and the closed-form moments of M~ (same quantities as the
+// reference's node sums, different rounding).  Pass 1 reads f and q in column
+// form (5 sums each), pass 2 reads both again and writes q.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double2 ld2_hint(const double* ptr, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;\n" : "=d"(v.x), "=d"(v.y) : "l"(ptr), "l"(pol));
+    return v;
+}
+
+// sum of coef_i coef_j X[a_i + a_j] Y[b_i + b_j] Z[c_i + c_j] over two term lists
+struct PolyT {
+    double c;
+    int a, b, z;
+};
+__device__ double poly_pair_sum(const PolyT* p, int np, const PolyT* q, int nq, const double* X, const double* Y,
+                                const double* Z) {
+    double acc = 0.0;
+    for (int i = 0; i < np; ++i)
+        for (int j = 0; j < nq; ++j)
+            acc += p[i].c * q[j].c * X[p[i].a + q[j].a] * Y[p[i].b + q[j].b] * Z[p[i].z + q[j].z];
+    return acc;
+}
+// phi = (1, v, |v|^2) written in coordinates w = v - s (shift s): lists of terms
+__device__ int phi_terms(int r, const double s[3], PolyT* o) {
+    if (r == 0) { o[0] = {1.0, 0, 0, 0}; return 1; }
+    if (r <= 3) {
+        o[0] = {1.0, r == 1, r == 2, r == 3};
+        o[1] = {s[r - 1], 0, 0, 0};
+        return 2;
+    }
+    o[0] = {1.0, 2, 0, 0}; o[1] = {1.0, 0, 2, 0}; o[2] = {1.0, 0, 0, 2};
+    o[3] = {2.0 * s[0], 1, 0, 0}; o[4] = {2.0 * s[1], 0, 1, 0}; o[5] = {2.0 * s[2], 0, 0, 1};
+    o[6] = {s[0] * s[0] + s[1] * s[1] + s[2] * s[2], 0, 0, 0};
+    return 7;
+}
+// psi = (1, w, |w|^2) in the same coordinates
+__device__ int psi_terms(int c, PolyT* o) {
+    if (c == 0) { o[0] = {1.0, 0, 0, 0}; return 1; }
+    if (c <= 3) { o[0] = {1.0, c == 1, c == 2, c == 3}; return 1; }
+    o[0] = {1.0, 2, 0, 0}; o[1] = {1.0, 0, 2, 0}; o[2] = {1.0, 0, 0, 2};
+    return 3;
+}
+
+#ifndef HK_RES_MT
+#define HK_RES_MT 256
+#endif
+#ifndef HK_RES_MINB
+#define HK_RES_MINB 2
+#endif
+template <int MT, int MINB>
+__global__ void __launch_bounds__(MT, MINB) residual_cta_kernel(const double* __restrict__ f, double* __restrict__ q,
+                                                                int64_t ncells, VGrid g, int lg, double pen_coeff,
+                                                                int* __restrict__ status) {
+    __shared__ double red[MT / 32][10];
+    __shared__ double tab[3][128];       // Maxwellian factors e_x, e_y, e_z
+    __shared__ double sums[2][3][8];     // C_a (uc-centred, a <= 4) and D_a (u-centred, a <= 6) per axis
+    __shared__ double par[24];           // [0] status, [1..5] m, [6] pref, [7..11] x, [12..16] y, [17] beta, [18..20] uc
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = g.n, nb = n * n * n;
+    const uint64_t pol_keep = l2_evict_last(), pol_last = l2_evict_first();
+    for (int64_t cell = blockIdx.x; cell < ncells; cell += gridDim.x) {
+        const double* fc = f + cell * nb;
+        double* qc = q + cell * nb;
+        // ---- pass 1: (1, v, |v|^2) sums of f and of q, column form ----
+        double S[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) S[k] = 0.0;
+        for (int cp = t; cp < (n << lg) / 2; cp += MT) {
+            const int col = 2 * cp, k2 = col >> lg, k3 = col & (n - 1);
+            double A[2][2][3] = {};  // [f | q][node of the pair][sum_k1 vx^a w], a <= 2
+#pragma unroll 4
+            for (int k1 = 0; k1 < n; ++k1) {
+                const int64_t o = ((int64_t)k1 << (2 * lg)) + col;
+                const double2 wf = ldg2_hint(fc + o, pol_keep), wq = ld2_hint(qc + o, pol_keep);
+                const double vx = g.node(k1), xx = vx * vx;
+                A[0][0][0] += wf.x; A[0][0][1] += vx * wf.x; A[0][0][2] += xx * wf.x;
+                A[0][1][0] += wf.y; A[0][1][1] += vx * wf.y; A[0][1][2] += xx * wf.y;
+                A[1][0][0] += wq.x; A[1][0][1] += vx * wq.x; A[1][0][2] += xx * wq.x;
+                A[1][1][0] += wq.y; A[1][1][1] += vx * wq.y; A[1][1][2] += xx * wq.y;
+            }
+            const double vy = g.node(k2);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double vz = g.node(k3 + h), r2 = vy * vy + vz * vz;
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    double* s = S + 5 * w;
+                    s[0] += A[w][h][0];
+                    s[1] += A[w][h][1];
+                    s[2] += vy * A[w][h][0];
+                    s[3] += vz * A[w][h][0];
+                    s[4] += A[w][h][2] + r2 * A[w][h][0];
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 10; ++k)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) S[k] += __shfl_xor_sync(0xffffffffu, S[k], o);
+        if (lane == 0)
+#pragma unroll
+            for (int k = 0; k < 10; ++k) red[warp][k] = S[k];
+        __syncthreads();
+        if (t == 0) {
+            for (int k = 0; k < 10; ++k) {
+                double v = 0.0;
+                for (int w2 = 0; w2 < MT / 32; ++w2) v += red[w2][k];
+                S[k] = v;
+            }
+            Mom m;
+            const double s11[11] = {S[0], S[1], S[2], S[3], S[4], 0, 0, 0, 0, 0, 0};
+            const int st = moments_from_sums(s11, g, m);
+            par[0] = st;
+            par[1] = m.rho; par[2] = m.ux; par[3] = m.uy; par[4] = m.uz; par[5] = m.T;
+            for (int k = 0; k < 10; ++k) red[0][k] = S[k];  // keep the block sums for thread 0's solves
+        }
+        __syncthreads();
+        if (par[0] != 0.0) {
+            if (t == 0 && status) status[cell] = (int)par[0];
+            __syncthreads();
+            continue;
+        }
+        const Mom m{par[1], par[2], par[3], par[4], par[5]};
+        const double mom3[3] = {m.rho * m.ux, m.rho * m.uy, m.rho * m.uz};
+        const double uc[3] = {mom3[0] / m.rho, mom3[1] / m.rho, mom3[2] / m.rho};  // match_moments' centre
+        const double u3[3] = {m.ux, m.uy, m.uz};                                      // remove_invariant_moments' centre
+        {   // Maxwellian factors (src/moments.cpp:93-102) and the 1-D shifted power sums
+            const double inv2T = 0.5 / m.T;
+            for (int k = t; k < n; k += MT) {
+                const double v = g.node(k);
+                tab[0][k] = exp(-(v - m.ux) * (v - m.ux) * inv2T);
+                tab[1][k] = exp(-(v - m.uy) * (v - m.uy) * inv2T);
+                tab[2][k] = exp(-(v - m.uz) * (v - m.uz) * inv2T);
+            }
+            __syncthreads();
+            if (t < 6) {  // (set, axis): C (uc-centred) for t < 3, D (u-centred) for t >= 3
+                const int set = t / 3, ax = t % 3;
+                const double sh = set ? u3[ax] : uc[ax];
+                double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+                for (int k = 0; k < n; ++k) {
+                    const double w = g.node(k) - sh, e = tab[ax][k];
+                    double p = e;
+#pragma unroll
+                    for (int a = 0; a < 7; ++a) {
+                        acc[a] += p;
+                        p *= w;
+                    }
+                }
+                for (int a = 0; a < 7; ++a) sums[set][ax][a] = acc[a];
+            }
+            __syncthreads();
+        }
+        if (t == 0) {
+            const double pref = m.rho / pow(2.0 * M_PI * m.T, 1.5);  // maxwell_factors' prefactor
+            const double sc = pref * g.dvk;
+            PolyT pt[7], qt[7];
+            // match_moments of M (src/moments.cpp:225-246): A_rc = sum phi_r psi_c M dvK, coordinates c = v - uc
+            double A[25];
+            for (int r = 0; r < 5; ++r) {
+                const int np = phi_terms(r, uc, pt);
+                for (int c = 0; c < 5; ++c) {
+                    const int nq = psi_terms(c, qt);
+                    A[5 * r + c] = sc * poly_pair_sum(pt, np, qt, nq, sums[0][0], sums[0][1], sums[0][2]);
+                }
+            }
+            const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
+            double x[5];
+            bool ok = solve5(A, rhs, x);
+            // M~ = M (x0 + x.c + x4 |c|^2) written in d = v - u: c = d + delta, delta = u - uc
+            const double dl[3] = {u3[0] - uc[0], u3[1] - uc[1], u3[2] - uc[2]};
+            PolyT mt[5];
+            mt[0] = {x[0] + x[1] * dl[0] + x[2] * dl[1] + x[3] * dl[2] + x[4] * (dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]), 0, 0, 0};
+            mt[1] = {x[1] + 2.0 * x[4] * dl[0], 1, 0, 0};
+            mt[2] = {x[2] + 2.0 * x[4] * dl[1], 0, 1, 0};
+            mt[3] = {x[3] + 2.0 * x[4] * dl[2], 0, 0, 1};
+            mt[4] = {x[4], 2, 0, 0};
+            PolyT mt_all[7] = {mt[0], mt[1], mt[2], mt[3], mt[4], {x[4], 0, 2, 0}, {x[4], 0, 0, 2}};
+            // remove_invariant_moments (src/moments.cpp:248-267) with weight M~, centre u:
+            // B_rc = sum phi_r psi_c M~ dvK (coordinates d), rhs = invariants of Q + beta (f - M~)
+            const double beta = pen_coeff * m.rho;
+            double B[25], inv[5];
+            for (int r = 0; r < 5; ++r) {
+                const int np = phi_terms(r, u3, pt);
+                // phi_r x (M~ polynomial): product term list
+                PolyT pm[49];
+                int npm = 0;
+                for (int i = 0; i < np; ++i)
+                    for (int j = 0; j < 7; ++j) pm[npm++] = {pt[i].c * mt_all[j].c, pt[i].a + mt_all[j].a, pt[i].b + mt_all[j].b,
+                                                             pt[i].z + mt_all[j].z};
+                for (int c = 0; c < 5; ++c) {
+                    const int nq = psi_terms(c, qt);
+                    B[5 * r + c] = sc * poly_pair_sum(pm, npm, qt, nq, sums[1][0], sums[1][1], sums[1][2]);
+                }
+                const PolyT one = {1.0, 0, 0, 0};
+                const double mtil = sc * poly_pair_sum(pm, npm, &one, 1, sums[1][0], sums[1][1], sums[1][2]);
+                inv[r] = (red[0][5 + r] + beta * red[0][r]) * g.dvk - beta * mtil;
+            }
+            double y[5] = {0, 0, 0, 0, 0};
+            if (ok) ok = solve5(B, inv, y);
+            par[0] = ok ? HK_OK : HK_DEGENERATE;
+            par[6] = pref;
+            for (int k = 0; k < 5; ++k) {
+                par[7 + k] = x[k];
+                par[12 + k] = y[k];
+            }
+            par[17] = beta;
+            if (status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
+        }
+        __syncthreads();
+        if (par[0] == 0.0) {
+            // ---- pass 2: q <- q + beta (f - M~) - (y0 + y.d + y4 |d|^2) M~ ----
+            const double pref = par[6], beta = par[17];
+            const double x0 = par[7], x1 = par[8], x2 = par[9], x3 = par[10], x4 = par[11];
+            const double y0 = par[12], y1 = par[13], y2 = par[14], y3 = par[15], y4 = par[16];
+            for (int cp = t; cp < (n << lg) / 2; cp += MT) {
+                const int col = 2 * cp, k2 = col >> lg, k3 = col & (n - 1);
+                const double vy = g.node(k2);
+                const double cy = vy - uc[1], dy = vy - u3[1];
+                double pz[2], cz[2], dz[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const double vz = g.node(k3 + h);
+                    cz[h] = vz - uc[2];
+                    dz[h] = vz - u3[2];
+                    pz[h] = pref * tab[1][k2] * tab[2][k3 + h];
+                }
+#pragma unroll 4
+                for (int k1 = 0; k1 < n; ++k1) {
+                    const int64_t o = ((int64_t)k1 << (2 * lg)) + col;
+                    const double2 wf = ldg2_hint(fc + o, pol_last);
+                    double2 wq = ld2_hint(qc + o, pol_last);
+                    const double vx = g.node(k1), ex = tab[0][k1];
+                    const double cx = vx - uc[0], dx = vx - u3[0];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const double Mv = pz[h] * ex;
+                        const double mt = Mv * (x0 + x1 * cx + x2 * cy + x3 * cz[h] + x4 * (cx * cx + cy * cy + cz[h] * cz[h]));
+                        const double corr = (y0 + y1 * dx + y2 * dy + y3 * dz[h] + y4 * (dx * dx + dy * dy + dz[h] * dz[h])) * mt;
+                        const double fv = h ? wf.y : wf.x;
+                        double& qv = h ? wq.y : wq.x;
+                        qv = qv + beta * (fv - mt) - corr;
+                    }
+                    st2_hint(qc + o, wq, pol_last);
+                }
+            }
+        }
+        __syncthreads();  // red / tab / sums / par reused by the next cell
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Stage solves (penalized / ES-BGK), one 256-thread CTA per cell, 3 CTAs per
 // SM (the cells in flight stay in L2 between the first and last pass).  A
 // thread owns groups of 4 consecutive k3 nodes of one (k1, k2) pencil.  The
@@ -1924,7 +2185,16 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
 int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,
                            int* status) {
     if (ncells <= 0) return HK_OK;
-    if (warp_path(n))
+#ifndef HK_RES_WARP
+#define HK_RES_WARP 0
+#endif
+    if (!HK_RES_WARP && warp_path(n) && n >= 8) {
+        // one CTA per cell, two streaming passes (the coupling matrices from 1-D sums)
+        const int64_t cap = int64_t(ctx->sm_count) * HK_RES_MINB;
+        const int grid = int(ncells < cap ? ncells : cap);
+        residual_cta_kernel<HK_RES_MT, HK_RES_MINB><<<grid, HK_RES_MT, 0, ctx->stream>>>(f, q, ncells, make_vgrid(n, vmax),
+                                                                                      log2i(n), pen_coeff, status);
+    } else if (warp_path(n))
         residual_finish_warp_kernel<<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(
             f, q, ncells, make_vgrid(n, vmax), log2i(n), pen_coeff, status);
     else

@@ -493,8 +493,16 @@ def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, 
 
         cb = _abi.RESIDUAL_FN(_hook)
         hp.residual_fn = C.cast(cb, C.c_void_p)
-    st = ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),
-                                 hydro.data_ptr(), f.data_ptr(), C.byref(hp), counts)
+    import gc
+    gc_was = gc.isenabled()
+    if residual_hook is not None:
+        gc.disable()  # no collector pause inside the hook while the step's kernels wait on it
+    try:
+        st = ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),
+                                     hydro.data_ptr(), f.data_ptr(), C.byref(hp), counts)
+    finally:
+        if gc_was:
+            gc.enable()
     if errors:
         raise errors[0]
     ctx.check(st)

@@ -272,12 +272,13 @@ def config4_slabs(world=8, steps=3, weighted=False):
 
 def config4_slabs_balanced(world=8, steps=3):
     """config4_slabs with the layer-2 residuals load-balanced across the slabs
-    (partition.balanced_apply through hk_hybrid_step's residual hook), emulated on
-    one GPU: each slab's step is timed with its own residuals evaluated locally
-    (CUDA events around the hook's evaluation give R_q), then the balanced
-    per-rank residual batch (ceil(total / world) cells per call) is timed on real
-    stage values (R_bal), and each slab's balanced step time is
-    T_q - R_q + R_bal + the two all-to-alls of the shipped cells at 700 GB/s."""
+    (partition.balanced_residual through hk_hybrid_step's residual hook), emulated
+    on one GPU: each slab's plain step is timed (T_q), the same steps with a hook
+    evaluating the residuals locally give the residual time R_q (CUDA events
+    around the evaluation), the balanced per-rank residual batch
+    (ceil(total / world) cells per call) is timed on real stage values (R_bal),
+    and each slab's balanced step time is T_q - R_q + R_bal + the two
+    all-to-alls of the shipped cells at 700 GB/s."""
     import math as _m
     from paper_2505_03360_b200.partition import HYB_GHOST as W, XSlab, hybrid_step_slab
     nx = ny = 200
@@ -310,7 +311,7 @@ def config4_slabs_balanced(world=8, steps=3):
             calls.append((y.shape[0], e0, e1))
         return hook
 
-    def step(timed):
+    def step(timed, hooked=True):
         halos = []
         for q, p_ in enumerate(parts):
             lt, rt = loc[(q - 1) % world], loc[(q + 1) % world]
@@ -324,21 +325,25 @@ def config4_slabs_balanced(world=8, steps=3):
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record()
             hybrid_step_slab(p_, k, dx, dx, dt, el.view(-1), rl.view(-1), hl, fl, halos=halos[q],
-                             residual_hook=make_hook(q, calls))
+                             residual_hook=make_hook(q, calls) if hooked else None)
             s1.record()
             out.append((s0, s1, calls))
         torch.cuda.synchronize()
-        if timed:
+        if timed and hooked:
             rec.append([(s0.elapsed_time(s1), [(m, e0.elapsed_time(e1)) for m, e0, e1 in calls]) for s0, s1, calls in out])
+        if timed and not hooked:
+            plain.append([s0.elapsed_time(s1) for s0, s1, _ in out])
 
+    plain = []
     for _ in range(2):
         step(False)
     mode["collect"] = True
     step(False)
     mode["collect"] = False
-    for _ in range(steps):
-        step(True)
-    T = [sum(rec[t][q][0] for t in range(steps)) / steps for q in range(world)]
+    for _ in range(steps):  # alternate: plain steps time T_q, hooked steps time the residuals R_q
+        step(True, hooked=False)
+        step(True, hooked=True)
+    T = [sum(plain[t][q] for t in range(steps)) / steps for q in range(world)]
     Rq = [sum(sum(ms for _, ms in rec[t][q][1]) for t in range(steps)) / steps for q in range(world)]
     ms_bal, a2a = [], []
     for kc in range(2):
@@ -361,6 +366,7 @@ def config4_slabs_balanced(world=8, steps=3):
     return {"config": f"config4 on {world} x-slabs, layer-2 residuals load-balanced (balanced_apply via the "
                       f"hk_hybrid_step residual hook), emulated on 1 GPU",
             "slab_columns": [p_.nxl for p_ in parts], "unbalanced_ms_per_slab_step": T,
+            "hooked_ms_per_slab_step": [sum(rec[t][q][0] for t in range(steps)) / steps for q in range(world)],
             "residual_ms_per_slab_step": Rq, "layer2_rows_per_call": [[rec[0][q][1][kc][0] for q in range(world)]
                                                                         for kc in range(2)],
             "balanced_residual_ms_per_call": ms_bal, "alltoall_ms_per_call_at_700GBps": a2a,
