@@ -42,7 +42,8 @@ typedef enum {
     HK_NCCL = 7,                  /* collective failure (no reference analogue) */
     HK_POSITIVITY = 8,            /* hykin::positivity_error */
     HK_UNSUPPORTED = 9,           /* size not implemented on this path */
-    HK_SCENARIO_END = 10          /* hykin::scenario_end_error */
+    HK_SCENARIO_END = 10,         /* hykin::scenario_end_error */
+    HK_IO = 11                    /* hykin::io_error */
 } hk_status;
 
 /* Per-cell verdict written by the collision kernels (device or host array). */
@@ -360,6 +361,18 @@ typedef struct {
 } hk_hybrid_params;
 int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx, double dy, double dt, const double* eps_dev,
                    int8_t* r_dev, double* hydro_dev, double* f_dev, const hk_hybrid_params* params, int64_t* counts);
+
+/* write_snapshot (src/snapshot.cpp is listed by the reference's
+ * CMake but not shipped): in directory `dir`, moments_<step>.csv (i,j,x,y,rho,ux,uy,T,P,
+ * one row per cell, c = j nx + i, cell centres), regimes_<step>.txt (ny lines of nx
+ * layers; -1 where kind_dev marks HK_CELL_OBSTACLE, kind_dev nullable) and
+ * meta_<step>.json (step, time, grids, heat ratio, config_json echoed verbatim or
+ * null).  Layer-0 cells: prim_from_conserved of hydro_dev; kinetic cells:
+ * prim_from_moments of moments_of(f_dev).  HK_POSITIVITY / HK_DEGENERATE with the
+ * lowest non-physical cell, HK_IO (io_error) when the files cannot be written. */
+int hk_write_snapshot(hk_ctx ctx, int n, double vmax, int64_t nx, int64_t ny, double dx, double dy,
+                      const int8_t* r_dev, const uint8_t* kind_dev, const double* hydro_dev, const double* f_dev,
+                      double heat_ratio, int64_t step, double time, const char* dir, const char* config_json);
 
 /* ---- multi-GPU: NCCL communicator of a context ------------
  * One process per GPU.  Rank 0 calls hk_comm_unique_id, the host side ships

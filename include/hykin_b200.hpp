@@ -87,6 +87,10 @@ class numerical_consistency_error : public error {
 public:
     using error::error;
 };
+class io_error : public error {
+public:
+    using error::error;
+};
 class device_error : public error {
 public:
     using error::error;
@@ -117,6 +121,7 @@ public:
         case HK_CONTRACT: throw contract_violation(m);
         case HK_POSITIVITY: throw positivity_error(m);
         case HK_UNSUPPORTED: throw config_error(m);
+        case HK_IO: throw io_error(m);
         default: throw device_error(m);
         }
     }

@@ -66,6 +66,10 @@ class scenario_end_error(error):
     """A moving obstacle left the domain (src/coupling.cpp:113-118)."""
 
 
+class io_error(error):
+    """hykin::io_error (inc/errors.hpp)."""
+
+
 class device_error(error):
     """CUDA failure (no reference analogue; the reference is CPU-only)."""
 
@@ -81,6 +85,7 @@ _STATUS_EXC = {
     _abi.HK_POSITIVITY: positivity_error,
     _abi.HK_UNSUPPORTED: config_error,
     _abi.HK_SCENARIO_END: scenario_end_error,
+    _abi.HK_IO: io_error,
 }
 
 

@@ -24,6 +24,7 @@ HK_NCCL = 7
 HK_POSITIVITY = 8
 HK_UNSUPPORTED = 9
 HK_SCENARIO_END = 10
+HK_IO = 11
 
 HK_COMM_ID_BYTES = 128
 HK_IPC_HANDLE_BYTES = 64
@@ -160,6 +161,8 @@ def lib() -> C.CDLL:
                                           vp]),
         "hk_synthesize_distributions": (C.c_int, [vp, C.c_int, dbl, i64, i64, C.POINTER(ObstacleSpec), vp, vp, vp, vp,
                                                   dbl, vp, i64, vp, C.POINTER(C.c_int64)]),
+        "hk_write_snapshot": (C.c_int, [vp, C.c_int, dbl, i64, i64, dbl, dbl, vp, vp, vp, vp, dbl, i64, dbl,
+                                        C.c_char_p, C.c_char_p]),
         "hk_hybrid_step": (C.c_int, [vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, vp, vp, vp, C.POINTER(HybridParams),
                                      C.POINTER(C.c_int64)]),
         "hk_apply_obstacle": (C.c_int, [vp, C.c_int, dbl, C.POINTER(ObstacleSpec), i64, i64, vp, vp, vp, vp, dbl,

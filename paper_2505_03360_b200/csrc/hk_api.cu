@@ -213,7 +213,7 @@ static int kernel_common(hk_ctx ctx, int n, int a1, int a2, double vmax, double 
     if (r_phys > r_max * (1.0 + 1e-12))
         return fail(ctx, HK_ALIASING, "support radius exceeds the aliasing bound 2L/(3+sqrt(2))");
     if (r_phys <= 0.0) return fail(ctx, HK_CONFIG, "support radius must be positive");
-    if (n != 16 && n != 32 && n != 64) return fail(ctx, HK_UNSUPPORTED, "device collision path supports n = 16, 32, 64");
+    if (n > 160) return fail(ctx, HK_UNSUPPORTED, "device collision path supports n <= 160");
     auto* k = new hk_kernel_s;
     k->ctx = ctx;
     k->n = n;

@@ -41,6 +41,11 @@ struct CollArgs {
 size_t coll64_xchg_bytes(hk_ctx ctx);
 int launch_coll64(hk_ctx ctx, const CollArgs& args, bool exact, int64_t max_cells, int tag);
 
+// hk_collgen.cu: the reference arithmetic for any n outside {16, 32, 64}
+// (direct DFTs, chunked work fields); writes Q and the per-cell verdict.
+int launch_coll_generic(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells, hk_cell_status* st);
+__global__ void residue_kernel(int64_t ncells, hk_cell_status* st);
+
 // hk_nyqfix.cu: exact Nyquist correction of the fast result for the cells on a
 // device list (the guard's reroute list).
 int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int64_t max_cells, const double2* nyqF,

@@ -1401,8 +1401,26 @@ int collision_launch(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_
         return run_size<32, 8>(ctx, k, f, q, ncells, flags, st);
     case 64:
         return run_size<64, 32>(ctx, k, f, q, ncells, flags, st);
-    default:
-        return fail(ctx, HK_UNSUPPORTED, "collision path implemented for n = 16, 32, 64");
+    default: {
+        // any other n: the reference arithmetic on direct DFTs (hk_collgen.cu)
+        hk_cell_status* s_dev = st;
+        int e = HK_OK;
+        void* tmp = nullptr;
+        if (!s_dev) {
+            if ((e = check_cuda(ctx, cudaMallocAsync(&tmp, sizeof(hk_cell_status) * ncells, ctx->stream), "alloc st")))
+                return e;
+            s_dev = static_cast<hk_cell_status*>(tmp);
+        }
+        cudaMemsetAsync(s_dev, 0, sizeof(hk_cell_status) * ncells, ctx->stream);
+        e = launch_coll_generic(ctx, k, f, q, ncells, s_dev);
+        if (!e) {
+            residue_kernel<<<unsigned((ncells + 255) / 256), 256, 0, ctx->stream>>>(ncells, s_dev);
+            ctx->launches++;
+            e = check_cuda(ctx, cudaGetLastError(), "residue kernel");
+        }
+        if (tmp) cudaFreeAsync(tmp, ctx->stream);
+        return e;
+    }
     }
 }
 

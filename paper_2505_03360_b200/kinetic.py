@@ -507,3 +507,22 @@ def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, 
         raise errors[0]
     ctx.check(st)
     return HybridCounts(*[int(c) for c in counts])
+
+
+# ---- snapshot I/O -----------------------------------------
+def write_snapshot(directory: str, step: int, time: float, vgrid: VelocityGrid, nx: int, ny: int, dx: float, dy: float,
+                   r, hydro, f, kind=None, heat_ratio: float = 5.0 / 3.0, config: dict = None, ctx=None):
+    """write_snapshot: moments_<step>.csv (i,j,x,y,rho,ux,uy,T,P), regimes_<step>.txt
+    (layers, -1 = obstacle) and meta_<step>.json in `directory` (hk_write_snapshot).
+    Raises io_error when the files cannot be written."""
+    import json
+    ctx = ctx or default_context(f.device.index or 0)
+    for name, t, dt_ in (("r", r, torch.int8), ("hydro", hydro, torch.float64), ("f", f, torch.float64)):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dt_ and t.is_contiguous()):
+            raise contract_violation(f"write_snapshot: {name} must be a contiguous {dt_} CUDA tensor")
+    if kind is not None and not (kind.is_cuda and kind.dtype == torch.uint8 and kind.is_contiguous()):
+        raise contract_violation("write_snapshot: kind must be a contiguous uint8 CUDA tensor")
+    cfg = json.dumps(config).encode() if config is not None else None
+    ctx.check(ctx._lib.hk_write_snapshot(ctx.h, vgrid.nv, vgrid.vmax, nx, ny, dx, dy, r.data_ptr(), _ptr(kind),
+                                         hydro.data_ptr(), f.data_ptr(), heat_ratio, int(step), float(time),
+                                         str(directory).encode(), cfg))

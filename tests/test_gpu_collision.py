@@ -210,3 +210,24 @@ def test_out_argument_is_checked(hk):
     fd = torch.from_numpy(f).cuda()
     with pytest.raises(hk.contract_violation):
         hk.spectral_collision(fd, kern, out=torch.empty(16 ** 3, dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("n,a1,a2", [(8, 2, 4), (12, 2, 3), (24, 3, 4)])
+def test_general_n_matches_oracle(hk, oracle, n, a1, a2):
+    """Any n (src/spectral.cpp:53-57 accepts every size; FFTW plans any length):
+    the generic device path (direct DFTs, hk_collgen.cu), including n with odd
+    prime factors, against the oracle built on the reference's GK15 tables."""
+    import torch
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    ko = oracle.kernel(n, inputs.VMAX, a1, a2, inputs.R_PHYS_MAX, closed_form=False)
+    f = inputs.config1_cells(3, n)
+    q_ref, st_ref, res_ref = oracle.collision_batch(ko, f)
+    q, st = hk.spectral_collision(torch.from_numpy(f).cuda(), kern, return_status=True)
+    q = q.cpu().numpy()
+    for c in range(len(f)):
+        assert rel_l2(q[c], q_ref[c]) < TOL, (n, c)
+    res = st["max_im"] / np.maximum(st["max_re"], 1e-300)
+    np.testing.assert_allclose(res, res_ref, rtol=1e-4, atol=1e-13)
+    qh = hk.spectral_collision(f, kern)  # host entry point, same path
+    assert np.array_equal(qh, q)
