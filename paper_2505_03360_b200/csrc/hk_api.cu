@@ -94,6 +94,7 @@ int hk_ctx_destroy(hk_ctx ctx) {
     if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
     if (ctx->sio_flags) cudaFree(ctx->sio_flags);
     if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
+    if (ctx->s_side) cudaStreamDestroy(ctx->s_side);
     delete ctx;
     return HK_OK;
 }

@@ -1335,8 +1335,75 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
         else
             return launch_variant<N, C, true>(ctx, x, ncells, tag);
     };
+    // Nyquist guard + exact correction of the listed cells for cells [c0, c0 + nc)
+    // of the batch (device list / count of that range at list + c0 / cnt)
+    auto guard_fix = [&](int64_t c0, int64_t nc, int* cnt) -> int {
+        int e;
+        const int64_t gt = (nc + GC - 1) / GC;
+        const int ks = (gt < 2 * ctx->sm_count) ? int(std::min<int64_t>(kchunks, (2 * ctx->sm_count + gt - 1) / gt)) : 1;
+        double* pt = (ks > 1 && part) ? part + c0 * 4 * k->md : nullptr;
+        const int ksu = pt ? ks : 1;
+        cudaMemsetAsync(cnt, 0, sizeof(int), ctx->stream);
+        timing_begin(ctx, 1);
+        const size_t gsmem = sizeof(double) * (GC * KC + 2 * k->md * KS + GC);
+        if (k->md > 128) return fail(ctx, HK_UNSUPPORTED, "guard: at most 128 distinct directions");
+        cudaFuncSetAttribute(guard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
+        if (pt) cudaMemsetAsync(pt, 0, sizeof(double) * 4 * k->md * nc, ctx->stream);
+        guard_kernel<<<dim3(unsigned(gt), unsigned(ksu)), 256, gsmem, ctx->stream>>>(
+            N, k->md, k->mult0, k->jac, k->weight, kGuardTau, nyq + c0 * nn3, k->abs_a, k->abs_ap, nc, st + c0, list + c0,
+            cnt, pt);
+        if (pt) {
+            guard_finish_kernel<<<unsigned((nc * 32 + 255) / 256), 256, 0, ctx->stream>>>(
+                N, k->md, k->mult0, k->jac, k->weight, kGuardTau, pt, nc, st + c0, list + c0, cnt);
+            ctx->launches++;
+        }
+        timing_end(ctx);
+        ctx->launches++;
+        if ((e = check_cuda(ctx, cudaGetLastError(), "guard kernel"))) return e;
+        // add the exact Nyquist term to the listed cells (hk_nyqfix.cu)
+        timing_begin(ctx, 2);
+        e = launch_nyq_fix(ctx, N, list + c0, cnt, nc, nyq + c0 * nn3, k->abs_a, k->abs_ap, k->md, k->mult0, k->jac,
+                           k->weight, q + c0 * (int64_t)N * N * N, st + c0);
+        timing_end(ctx);
+        return e;
+    };
     if (exact) {
         if ((s = launch_exact(a, 0))) return s;
+    } else if (N == 64 && guard && ncells >= 2048) {
+        // N = 64: the team kernel leaves sm_count % 32 SMs idle (20 on a B200); the
+        // batch runs in chunks and the guard + correction of chunk c runs on a
+        // side stream on those SMs while the team kernel works on chunk c + 1
+        a.nyq = nyq;
+        if (!ctx->s_side &&
+            (s = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_side, cudaStreamNonBlocking), "side stream")))
+            return s;
+        constexpr int kChunks = 4;
+        const int64_t csz = (ncells + kChunks - 1) / kChunks;
+        cudaStream_t main_s = ctx->stream;
+        cudaEvent_t ev[kChunks + 1];
+        for (auto& e : ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        int nch = 0;
+        for (int64_t c0 = 0; c0 < ncells && !s; c0 += csz, ++nch) {
+            const int64_t nc = std::min(csz, ncells - c0);
+            CollArgs b = a;
+            b.f = f + c0 * (int64_t)N * N * N;
+            b.q = q + c0 * (int64_t)N * N * N;
+            b.ncells = nc;
+            b.st = st + c0;
+            b.nyq = nyq + c0 * nn3;
+            if ((s = launch_coll64(ctx, b, false, nc, 0))) break;
+            cudaEventRecord(ev[nch], main_s);
+            cudaStreamWaitEvent(ctx->s_side, ev[nch], 0);
+            ctx->stream = ctx->s_side;  // the chunk's guard + correction on the side stream
+            s = guard_fix(c0, nc, count + 1 + nch);
+            ctx->stream = main_s;
+        }
+        cudaEventRecord(ev[kChunks], ctx->s_side);
+        cudaStreamWaitEvent(main_s, ev[kChunks], 0);
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (s) return s;
+        ctx->last_list = nullptr;  // lists are per chunk here
+        ctx->last_count = nullptr;
     } else {
         a.nyq = nyq;
         bool done = false;
@@ -1353,33 +1420,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
                 if ((s = launch_variant<N, C, false>(ctx, a, ncells, 0))) return s;
             }
         }
-        if (guard) {
-            cudaMemsetAsync(count, 0, sizeof(int), ctx->stream);
-            timing_begin(ctx, 1);
-            {
-                const size_t gsmem = sizeof(double) * (GC * KC + 2 * k->md * KS + GC);
-                if (k->md > 128) return fail(ctx, HK_UNSUPPORTED, "guard: at most 128 distinct directions");
-                cudaFuncSetAttribute(guard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
-                if (ksplit > 1) cudaMemsetAsync(part, 0, part_bytes, ctx->stream);
-                guard_kernel<<<dim3(unsigned(gtiles), unsigned(ksplit)), 256, gsmem, ctx->stream>>>(
-                    N, k->md, k->mult0, k->jac, k->weight, kGuardTau, nyq, k->abs_a, k->abs_ap, ncells, st, list, count,
-                    part);
-                if (ksplit > 1) {
-                    guard_finish_kernel<<<unsigned((ncells * 32 + 255) / 256), 256, 0, ctx->stream>>>(
-                        N, k->md, k->mult0, k->jac, k->weight, kGuardTau, part, ncells, st, list, count);
-                    ctx->launches++;
-                }
-            }
-            timing_end(ctx);
-            ctx->launches++;
-            if ((s = check_cuda(ctx, cudaGetLastError(), "guard kernel"))) return s;
-            // add the exact Nyquist term to the listed cells (hk_nyqfix.cu)
-            timing_begin(ctx, 2);
-            s = launch_nyq_fix(ctx, N, list, count, ncells, nyq, k->abs_a, k->abs_ap, k->md, k->mult0, k->jac,
-                               k->weight, q, st);
-            timing_end(ctx);
-            if (s) return s;
-        }
+        if (guard && (s = guard_fix(0, ncells, count))) return s;
     }
     {
         residue_kernel<<<unsigned((ncells + 255) / 256), 256, 0, ctx->stream>>>(ncells, st);

@@ -27,6 +27,8 @@ struct hk_ctx_s {
     std::map<int, int> max_clusters;  // key: kernel variant id
     // copy streams of the host (e2e) entry point: H2D / D2H overlap compute
     cudaStream_t s_in = nullptr, s_out = nullptr;
+    // side stream of the N = 64 collision (guard + Nyquist correction beside the team kernel)
+    cudaStream_t s_side = nullptr;
     // streamed-I/O flags for the next collision launch (host entry point), and
     // the guard's reroute list / count of the last launch (device pointers)
     const unsigned* sio_in_ready = nullptr;

@@ -103,3 +103,19 @@ def test_n64_equilibrium_cells(cfg5, hk):
         assert scale > 0
         gap = np.linalg.norm(qf[c] - qe[c])
         assert gap <= max(TOL * np.linalg.norm(qe[c]), 1e-14 * scale), c
+
+
+def test_n64_chunked_batch_equals_small_batches(cfg5, hk):
+    """Batches of >= 2048 cells run in chunks with the guard + Nyquist correction
+    of each chunk on a side stream beside the team kernel: every cell's Q and
+    verdict equal (bitwise) those of the same cell evaluated in a small batch."""
+    import torch
+    f = inputs.config5_slab_torch(i0=240, nxl=16, ny=128, n=N)  # 2048 cells across the shock
+    q, st = hk.spectral_collision(f, cfg5, return_status=True)
+    listed = np.nonzero(st["flags"] & 4)[0]
+    assert len(listed) > 0
+    pick = sorted(set([0, 1, 511, 512, 1023, 1024, 1535, 1536, 2047] + list(listed[:: max(1, len(listed) // 6)])))
+    idx = torch.tensor(pick, device="cuda")
+    qs, sts = hk.spectral_collision(f[idx].contiguous(), cfg5, return_status=True)
+    assert torch.equal(q[idx], qs)
+    assert np.array_equal(st["flags"][pick], sts["flags"])
