@@ -65,8 +65,10 @@ def test_invalid_configurations_raise_reference_exceptions(hk):
     with pytest.raises(hk.config_error):
         hk.precompute_kernel(vg, 16, 4, 4, inputs.R_PHYS_MAX)  # n != grid size
     vg48 = hk.make_velocity_grid(48, inputs.VMAX)
-    with pytest.raises(hk.config_error):  # no device path for n = 48 (HK_UNSUPPORTED)
-        hk.precompute_kernel(vg48, 48, 4, 4, inputs.R_PHYS_MAX)
+    assert hk.precompute_kernel(vg48, 48, 2, 2, inputs.R_PHYS_MAX).n == 48  # general n (hk_collgen.cu)
+    vg192 = hk.make_velocity_grid(192, inputs.VMAX)
+    with pytest.raises(hk.config_error):  # beyond the device path's size limit (HK_UNSUPPORTED)
+        hk.precompute_kernel(vg192, 192, 4, 4, inputs.R_PHYS_MAX)
     with pytest.raises(hk.config_error):
         hk.make_velocity_grid(1, inputs.VMAX)
 
