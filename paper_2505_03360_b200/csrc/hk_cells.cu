@@ -1539,13 +1539,22 @@ constexpr int kStageU1 = HK_STAGE_U1, kStageU2 = HK_STAGE_U2, kStageU3 = HK_STAG
 #if HK_STAGE_PROF
 __device__ unsigned long long g_stage_prof[5];
 #endif
-template <bool ESBGK, int MT, int MINB>
+// Explicit accumulation fused into the stage input (ACC): the stage solves
+// f* = f + cq q1 + ck k1 (the PR(2,2,2) f_acc of src/boltzmann.cpp:80-81 /
+// src/esbgk.cpp:68-72), formed on the fly in passes 1 and 3 instead of a
+// separate combination pass writing f_acc (one field write + read saved).
+struct AccIn {
+    const double* q1;
+    const double* k1;
+    double cq, ck;
+};
+template <bool ESBGK, int MT, int MINB, bool ACC = false>
 __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __restrict__ fin, double* __restrict__ out,
                                                              int64_t ncells, VGrid g, int lg, double a,
                                                              const double* __restrict__ eps_cell, double eps_scalar,
                                                              double beta, double coeff, int* __restrict__ info,
                                                              double* __restrict__ mom_out, double* __restrict__ k1_out,
-                                                             double k1_scale) {
+                                                             double k1_scale, AccIn acc) {
     extern __shared__ double dsm[];
     const int n = g.n, nb = n * n * n, ngroups = nb >> 2;
     double* Ptab = dsm;            // [n*n]
@@ -1597,9 +1606,14 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 const int col = 2 * cp, k2 = col >> lg, k3 = col & (n - 1);
                 const double* fcol = fc + col;
                 double A[2][3] = {{0, 0, 0}, {0, 0, 0}};
-#pragma unroll kStageU1
+#pragma unroll (ACC ? 4 : kStageU1)
                 for (int k1 = 0; k1 < n; ++k1) {
-                    const double2 w = ldg2_hint(fcol + ((int64_t)k1 << (2 * lg)), pol_last);
+                    double2 w = ldg2_hint(fcol + ((int64_t)k1 << (2 * lg)), pol_last);
+                    if constexpr (ACC) {
+                        const int64_t o = cell * nb + col + ((int64_t)k1 << (2 * lg));
+                        const double2 qv = ldg2_hint(acc.q1 + o, pol_last), kv = ldg2_hint(acc.k1 + o, pol_last);
+                        w = make_double2(w.x + acc.cq * qv.x + acc.ck * kv.x, w.y + acc.cq * qv.y + acc.ck * kv.y);
+                    }
                     const double2 p = xpow[k1];
                     A[0][0] += w.x; A[1][0] += w.y;
                     A[0][1] += p.x * w.x; A[1][1] += p.x * w.y;
@@ -1639,8 +1653,16 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
             if (st == HK_OK)
                 for (int q = t; q < ngroups; q += MT) {
                     const int idx = 4 * q;
-                    *reinterpret_cast<double2*>(oc + idx) = ldg2(fc + idx);
-                    *reinterpret_cast<double2*>(oc + idx + 2) = ldg2(fc + idx + 2);
+                    double2 va = ldg2(fc + idx), vb = ldg2(fc + idx + 2);
+                    if constexpr (ACC) {
+                        const int64_t o = cell * nb + idx;
+                        const double2 qa = ldg2(acc.q1 + o), qb = ldg2(acc.q1 + o + 2);
+                        const double2 ka = ldg2(acc.k1 + o), kb = ldg2(acc.k1 + o + 2);
+                        va = make_double2(va.x + acc.cq * qa.x + acc.ck * ka.x, va.y + acc.cq * qa.y + acc.ck * ka.y);
+                        vb = make_double2(vb.x + acc.cq * qb.x + acc.ck * kb.x, vb.y + acc.cq * qb.y + acc.ck * kb.y);
+                    }
+                    *reinterpret_cast<double2*>(oc + idx) = va;
+                    *reinterpret_cast<double2*>(oc + idx + 2) = vb;
                     if (k1_out) {  // identity stage: k1 = 0
                         *reinterpret_cast<double2*>(k1_out + cell * nb + idx) = make_double2(0.0, 0.0);
                         *reinterpret_cast<double2*>(k1_out + cell * nb + idx + 2) = make_double2(0.0, 0.0);
@@ -1867,7 +1889,15 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
                 const double vx = g.node(k1), vy = g.node(k2);
                 const double2 fa = ldg2_hint(fc + idx, pol_first), fb = ldg2_hint(fc + idx + 2, pol_first);
-                const double fv[4] = {fa.x, fa.y, fb.x, fb.y};
+                double fv[4] = {fa.x, fa.y, fb.x, fb.y};
+                if constexpr (ACC) {
+                    const int64_t o = cell * nb + idx;
+                    const double2 qa = ldg2_hint(acc.q1 + o, pol_first), qb = ldg2_hint(acc.q1 + o + 2, pol_first);
+                    const double2 ka = ldg2_hint(acc.k1 + o, pol_first), kb = ldg2_hint(acc.k1 + o + 2, pol_first);
+                    const double qv[4] = {qa.x, qa.y, qb.x, qb.y}, kv[4] = {ka.x, ka.y, kb.x, kb.y};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) fv[j] = fv[j] + acc.cq * qv[j] + acc.ck * kv[j];
+                }
                 const double cx = vx - uc[0], cy = vy - uc[1];
                 const double pxy = x[0] + x[1] * cx + x[2] * cy + x[4] * (cx * cx + cy * cy);
                 double o[4];
@@ -2126,6 +2156,25 @@ int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t
     return check_cuda(ctx, cudaGetLastError(), "maxwellian kernel");
 }
 
+bool stage_acc_supported(int n) { return warp_path(n) && n >= 8; }
+
+int stage_acc_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* f, const double* q1, const double* k1,
+                     double cq, double ck, double* out, int64_t ncells, double a, const double* eps_cell, double beta,
+                     double coeff, int* info) {
+    if (ncells <= 0) return HK_OK;
+    if (!stage_acc_supported(n)) return fail(ctx, HK_UNSUPPORTED, "fused stage: n a power of two >= 8");
+    const VGrid g = make_vgrid(n, vmax);
+    const int64_t cap = int64_t(ctx->sm_count) * 2;
+    const int grid = int(ncells < cap ? ncells : cap);
+    const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32 + 2 * n + 6 * n + 2 * n);
+    auto kern = esbgk ? stage_cta_kernel<true, 256, 2, true> : stage_cta_kernel<false, 256, 2, true>;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 256, smem, ctx->stream>>>(f, out, ncells, g, log2i(n), a, eps_cell, 0.0, beta, coeff, info, nullptr,
+                                           nullptr, 0.0, AccIn{q1, k1, cq, ck});
+    ctx->launches++;
+    return check_cuda(ctx, cudaGetLastError(), "fused stage kernel");
+}
+
 int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,
                  const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out,
                  double* k1_out, double k1_scale) {
@@ -2142,7 +2191,7 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
         const int mt = 256;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, mt, smem, ctx->stream>>>(fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info,
-                                              mom_out, k1_out, k1_scale);
+                                              mom_out, k1_out, k1_scale, AccIn{});
 #if HK_STAGE_PROF
         {
             unsigned long long h[5];

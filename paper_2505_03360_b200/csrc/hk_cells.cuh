@@ -12,6 +12,12 @@ int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t
 int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, double* out, int64_t ncells, double a,
                  const double* eps_cell, double eps_scalar, double beta, double coeff, int* info, double* mom_out,
                  double* k1_out = nullptr, double k1_scale = 0.0);
+// Stage solve of f* = f + cq q1 + ck k1 formed on the fly (the PR(2,2,2) second
+// stage without a separate f_acc pass); stage_acc_supported(n): n a power of two >= 8.
+bool stage_acc_supported(int n);
+int stage_acc_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* f, const double* q1, const double* k1,
+                     double cq, double ck, double* out, int64_t ncells, double a, const double* eps_cell, double beta,
+                     double coeff, int* info);
 int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,
                            int* status);
 

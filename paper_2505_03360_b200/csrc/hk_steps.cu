@@ -207,8 +207,14 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
     if (!st) st = transport_launch(ctx, tp, w.y, boltz ? w.tr : w.q1);                     // T(Y1)
     if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y1)
     if (!st && boltz) st = combine(ctx, Q1, count, nb, t, dt, eps_dev, w.q1, 0, 0, 0, 0, w.tr, R);  // q1
-    if (!st) st = combine(ctx, FACC, count, nb, t, dt, eps_dev, w.fa, f, 0, w.q1, w.k1, 0, 0);  // f_acc
-    if (!st) st = stage(w.fa, t.a_im11 * dt, w.y, nullptr);                                // Y2
+    if (stage_acc_supported(n)) {  // Y2 = stage(f_acc), f_acc = f + dt a_ex10 q1 + a_im10 k1 formed in the stage
+        if (!st)
+            st = stage_acc_launch(ctx, !boltz, n, vmax, f, w.q1, w.k1, dt * t.a_ex10, t.a_im10, w.y, cells,
+                                  t.a_im11 * dt, eps_dev, boltz ? 0.0 : beta, coeff, nullptr);
+    } else {
+        if (!st) st = combine(ctx, FACC, count, nb, t, dt, eps_dev, w.fa, f, 0, w.q1, w.k1, 0, 0);  // f_acc
+        if (!st) st = stage(w.fa, t.a_im11 * dt, w.y, nullptr);                                // Y2
+    }
     if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y2)
     if (!st && transport_final_supported(tp)) {  // T(Y2) + final combination, one kernel
         const FinalCombine fc{f, w.q1, w.k1, R, eps_dev, dt, t.a_ex10, t.a_im10, t.a_im11, t.w_ex0, t.w_ex1, t.w_im0,

@@ -110,7 +110,7 @@ def test_n64_chunked_batch_equals_small_batches(cfg5, hk):
     of each chunk on a side stream beside the team kernel: every cell's Q and
     verdict equal (bitwise) those of the same cell evaluated in a small batch."""
     import torch
-    f = inputs.config5_slab_torch(i0=252, nxl=16, ny=128, n=N)  # 2048 cells across the shock
+    f = inputs.config5_slab_torch(i0=272, nxl=16, ny=128, n=N)  # 2048 downstream cells (guard-listed ones)
     q, st = hk.spectral_collision(f, cfg5, return_status=True)
     listed = np.nonzero(st["flags"] & 4)[0]
     assert len(listed) > 0
