@@ -1297,6 +1297,7 @@ __global__ void __launch_bounds__(MT, MINB) residual_cta_kernel(const double* __
     __shared__ double tab[3][128];       // Maxwellian factors e_x, e_y, e_z
     __shared__ double sums[2][3][8];     // C_a (uc-centred, a <= 4) and D_a (u-centred, a <= 6) per axis
     __shared__ double par[24];           // [0] status, [1..5] m, [6] pref, [7..11] x, [12..16] y, [17] beta, [18..20] uc
+    __shared__ double mat[32];           // coupling matrix entries / invariants, one per lane of warp 0
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int n = g.n, nb = n * n * n;
     const uint64_t pol_keep = l2_evict_last(), pol_last = l2_evict_first();
@@ -1392,61 +1393,72 @@ __global__ void __launch_bounds__(MT, MINB) residual_cta_kernel(const double* __
             }
             __syncthreads();
         }
-        if (t == 0) {
+        // ---- coupling matrices and solves: warp 0, one matrix entry per lane ----
+        if (warp == 0) {
             const double pref = m.rho / pow(2.0 * M_PI * m.T, 1.5);  // maxwell_factors' prefactor
             const double sc = pref * g.dvk;
-            PolyT pt[7], qt[7];
+            PolyT pt[7], qt[3];
             // match_moments of M (src/moments.cpp:225-246): A_rc = sum phi_r psi_c M dvK, coordinates c = v - uc
-            double A[25];
-            for (int r = 0; r < 5; ++r) {
-                const int np = phi_terms(r, uc, pt);
-                for (int c = 0; c < 5; ++c) {
-                    const int nq = psi_terms(c, qt);
-                    A[5 * r + c] = sc * poly_pair_sum(pt, np, qt, nq, sums[0][0], sums[0][1], sums[0][2]);
-                }
+            if (lane < 25) {
+                const int r0 = lane / 5, c0 = lane % 5;
+                const int np = phi_terms(r0, uc, pt), nq = psi_terms(c0, qt);
+                mat[lane] = sc * poly_pair_sum(pt, np, qt, nq, sums[0][0], sums[0][1], sums[0][2]);
             }
-            const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
-            double x[5];
-            bool ok = solve5(A, rhs, x);
+            __syncwarp();
+            if (lane == 0) {
+                double A[25];
+                for (int k = 0; k < 25; ++k) A[k] = mat[k];
+                const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
+                double x[5] = {0, 0, 0, 0, 0};
+                const bool ok = solve5(A, rhs, x);
+                for (int k = 0; k < 5; ++k) par[7 + k] = x[k];
+                par[0] = ok ? HK_OK : HK_DEGENERATE;
+            }
+            __syncwarp();
             // M~ = M (x0 + x.c + x4 |c|^2) written in d = v - u: c = d + delta, delta = u - uc
+            const double x[5] = {par[7], par[8], par[9], par[10], par[11]};
             const double dl[3] = {u3[0] - uc[0], u3[1] - uc[1], u3[2] - uc[2]};
-            PolyT mt[5];
-            mt[0] = {x[0] + x[1] * dl[0] + x[2] * dl[1] + x[3] * dl[2] + x[4] * (dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]), 0, 0, 0};
-            mt[1] = {x[1] + 2.0 * x[4] * dl[0], 1, 0, 0};
-            mt[2] = {x[2] + 2.0 * x[4] * dl[1], 0, 1, 0};
-            mt[3] = {x[3] + 2.0 * x[4] * dl[2], 0, 0, 1};
-            mt[4] = {x[4], 2, 0, 0};
-            PolyT mt_all[7] = {mt[0], mt[1], mt[2], mt[3], mt[4], {x[4], 0, 2, 0}, {x[4], 0, 0, 2}};
+            const PolyT mt[7] = {{x[0] + x[1] * dl[0] + x[2] * dl[1] + x[3] * dl[2] +
+                                      x[4] * (dl[0] * dl[0] + dl[1] * dl[1] + dl[2] * dl[2]), 0, 0, 0},
+                                 {x[1] + 2.0 * x[4] * dl[0], 1, 0, 0},
+                                 {x[2] + 2.0 * x[4] * dl[1], 0, 1, 0},
+                                 {x[3] + 2.0 * x[4] * dl[2], 0, 0, 1},
+                                 {x[4], 2, 0, 0},
+                                 {x[4], 0, 2, 0},
+                                 {x[4], 0, 0, 2}};
             // remove_invariant_moments (src/moments.cpp:248-267) with weight M~, centre u:
-            // B_rc = sum phi_r psi_c M~ dvK (coordinates d), rhs = invariants of Q + beta (f - M~)
+            // B_rc = sum phi_r psi_c M~ dvK (coordinates d); lanes 25..29: the moments of M~
             const double beta = pen_coeff * m.rho;
-            double B[25], inv[5];
-            for (int r = 0; r < 5; ++r) {
-                const int np = phi_terms(r, u3, pt);
-                // phi_r x (M~ polynomial): product term list
+            if (lane < 30) {
+                const int r0 = lane < 25 ? lane / 5 : lane - 25;
+                const int np = phi_terms(r0, u3, pt);
                 PolyT pm[49];
                 int npm = 0;
-                for (int i = 0; i < np; ++i)
-                    for (int j = 0; j < 7; ++j) pm[npm++] = {pt[i].c * mt_all[j].c, pt[i].a + mt_all[j].a, pt[i].b + mt_all[j].b,
-                                                             pt[i].z + mt_all[j].z};
-                for (int c = 0; c < 5; ++c) {
-                    const int nq = psi_terms(c, qt);
-                    B[5 * r + c] = sc * poly_pair_sum(pm, npm, qt, nq, sums[1][0], sums[1][1], sums[1][2]);
+                for (int i2 = 0; i2 < np; ++i2)
+                    for (int j2 = 0; j2 < 7; ++j2)
+                        pm[npm++] = {pt[i2].c * mt[j2].c, pt[i2].a + mt[j2].a, pt[i2].b + mt[j2].b, pt[i2].z + mt[j2].z};
+                if (lane < 25) {
+                    const int nq = psi_terms(lane % 5, qt);
+                    mat[lane] = sc * poly_pair_sum(pm, npm, qt, nq, sums[1][0], sums[1][1], sums[1][2]);
+                } else {
+                    const PolyT one = {1.0, 0, 0, 0};
+                    const double mtil = sc * poly_pair_sum(pm, npm, &one, 1, sums[1][0], sums[1][1], sums[1][2]);
+                    mat[lane] = (red[0][5 + r0] + beta * red[0][r0]) * g.dvk - beta * mtil;  // invariants of Q + beta (f - M~)
                 }
-                const PolyT one = {1.0, 0, 0, 0};
-                const double mtil = sc * poly_pair_sum(pm, npm, &one, 1, sums[1][0], sums[1][1], sums[1][2]);
-                inv[r] = (red[0][5 + r] + beta * red[0][r]) * g.dvk - beta * mtil;
             }
-            double y[5] = {0, 0, 0, 0, 0};
-            if (ok) ok = solve5(B, inv, y);
-            par[0] = ok ? HK_OK : HK_DEGENERATE;
-            par[6] = pref;
-            for (int k = 0; k < 5; ++k) {
-                par[7 + k] = x[k];
-                par[12 + k] = y[k];
+            __syncwarp();
+            if (lane == 0) {
+                double B[25], inv[5], y[5] = {0, 0, 0, 0, 0};
+                for (int k = 0; k < 25; ++k) B[k] = mat[k];
+                for (int k = 0; k < 5; ++k) inv[k] = mat[25 + k];
+                bool ok = par[0] == HK_OK;
+                if (ok) ok = solve5(B, inv, y);
+                par[0] = ok ? HK_OK : HK_DEGENERATE;
+                par[6] = pref;
+                for (int k = 0; k < 5; ++k) par[12 + k] = y[k];
+                par[17] = beta;
+                if (status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
             }
-            par[17] = beta;
-            if (status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
         }
         __syncthreads();
         if (par[0] == 0.0) {

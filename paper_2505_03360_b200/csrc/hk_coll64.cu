@@ -46,9 +46,12 @@ struct Geo64 {
     static constexpr int64_t SLOT = (int64_t)C * BLK;
     static constexpr unsigned ARR = C * 4;      // warp arrivals per slot use (each role)
     static constexpr uint32_t TM_COLS = 512;
-    static constexpr size_t SMEM = size_t(3 * PLANE) * sizeof(double2) + 64;
+    static constexpr size_t SMEM = size_t(3 * PLANE) * sizeof(double2) + 128;
     static constexpr size_t XCHG_PER_TEAM = size_t(D) * SLOT * sizeof(double2);
 };
+#ifndef HK_PULL_TMA64
+#define HK_PULL_TMA64 1  // consumer plane pulls by TMA bulk row copies instead of per-thread cp.async
+#endif
 #ifndef HK_W_TMA64
 #define HK_W_TMA64 1  // FAST producer weight planes by TMA bulk copy: 163 ms vs 198 ms per 1024 shock cells with per-thread cp.async (r02)
 #endif
@@ -522,6 +525,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
     uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * PLANE);  // [P] F-plane ready
     uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
     uint64_t* wbar = fbar + P + 1;  // weight-plane TMA barrier of the producer group
+    uint64_t* cbar = fbar + P + 2;  // [8] consumer pull barriers (HK_PULL_TMA64)
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -539,6 +543,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
     if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
     if (t < P) mbar_init(smem_u32(fbar + t), 128);
     if (HK_W_TMA64 && t == 32) mbar_init(smem_u32(wbar), 1);
+    if (HK_PULL_TMA64 && t >= 64 && t < 72) mbar_init(smem_u32(cbar + (t - 64)), 1);
     if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tmem_fence_before();
     __syncthreads();
@@ -731,6 +736,21 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         const int grp = (warp - 4) >> 2;   // = my j3 / k1 plane (P = 2)
         const unsigned bar = 2 + grp;      // named barrier of my group (128 threads)
         double2* Rv = Rvb + grp * PLANE;
+#if HK_PULL_TMA64
+        // my 16 rows (1 KiB each) of plane grp by bulk copies, one per lane of the
+        // first half-warp, into the padded landing rows; completion on this warp's mbarrier
+        const uint32_t cbar_s = smem_u32(cbar + (warp - 4));
+        unsigned cph = 0;
+        auto pull = [&](unsigned gs) {
+            const double2* src = X + (int64_t)(gs % D) * SLOT + (int64_t)r * BLK + (int64_t)grp * N * N + 16 * rw * N;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(cbar_s, 16 * N * 16);
+            __syncwarp();
+            if (lane < 16) bulk_g2s(smem_u32(Rv + (16 * rw + lane) * ROW), src + lane * N, N * 16, cbar_s);
+        };
+#else
         auto pull = [&](unsigned gs) {     // my 16 rows of plane grp of slot gs
             const double2* src = X + (int64_t)(gs % D) * SLOT + (int64_t)r * BLK + (int64_t)grp * N * N + 16 * rw * N;
             const uint32_t d0 = smem_u32(Rv + 16 * rw * ROW);
@@ -741,6 +761,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
             }
             cp_async_commit();
         };
+#endif
         long long spin_cyc = 0;
         const long long t_start = clock64();
 #if HK_PROD_PHASES
@@ -752,7 +773,12 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
             pull(gs);
         };
         auto complete = [&](unsigned gs) {
+#if HK_PULL_TMA64
+            mbar_wait_parity(cbar_s, cph);
+            cph ^= 1;
+#else
             cp_async_wait_all();
+#endif
             __syncwarp();
             if (lane == 0) signal_add_relaxed(done + gs % D);
             named_bar(bar, 128);  // every warp's rows of my plane have landed

@@ -415,6 +415,9 @@ struct GeoW {
     // landing [2][4 warps][PLANE] + producer staging [4 warps][PLANE]
     static constexpr size_t SMEM = size_t(12 * PLANE) * sizeof(double2) + 2 * P * sizeof(uint64_t) + 64;
 };
+#ifndef HK_PULL_TMA
+#define HK_PULL_TMA 1  // consumer plane pulls by TMA bulk row copies instead of per-thread cp.async
+#endif
 #ifndef HK_W_TMA
 #define HK_W_TMA 0  // producer weight planes by TMA bulk copy (mbarrier): 46.8 ms vs 46.6 per 4096 cells with cp.async (r02)
 #endif
@@ -440,6 +443,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
     uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 12 * PLANE);  // [P]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
     uint64_t* wbar = fbar + P + 1;  // [4] weight-plane TMA barriers, one per producer warp
+    uint64_t* cbar = fbar + P + 5;  // [8] consumer pull barriers (HK_PULL_TMA)
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -455,6 +459,7 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
     if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
     if (t < P) mbar_init(smem_u32(fbar + t), 32);
     if (HK_W_TMA && t >= 32 && t < 36) mbar_init(smem_u32(wbar + (t - 32)), 1);
+    if (HK_PULL_TMA && t >= 64 && t < 72) mbar_init(smem_u32(cbar + (t - 64)), 1);
     if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tmem_fence_before();
     __syncthreads();
@@ -620,6 +625,21 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
         const long long t_start = clock64();
         double2* Rv = Rvb + cw * PLANE;  // single landing buffer of my plane
         const uint32_t tmF = tm + 128 * (cw >> 2), tmG = tm + 256 + 64 * (cw >> 2);
+#if HK_PULL_TMA
+        // the plane's 32 rows (512 B each) by bulk copies, one per lane, into the
+        // padded landing rows; completion on this warp's mbarrier
+        const uint32_t cbar_s = smem_u32(cbar + cw);
+        unsigned cph = 0;
+        auto pull = [&](unsigned gg) {
+            const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + cw * N * N;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // my reads of Rv before the async write
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");      // the acquired slot to the async proxy
+            __syncwarp();
+            if (lane == 0) mbar_arrive_expect_tx(cbar_s, N * N * 16);
+            __syncwarp();
+            bulk_g2s(smem_u32(Rv) + lane * ROW * 16, src + lane * N, N * 16, cbar_s);
+        };
+#else
         auto pull = [&](unsigned gg) {
             const double2* src = X + (int64_t)(gg % D) * SLOT + (int64_t)r * BLK + cw * N * N;
             const uint32_t d0 = smem_u32(Rv);
@@ -627,13 +647,19 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
             for (int k = 0; k < N; ++k) cp_async16(d0 + (k * ROW + lane) * 16, src + k * N + lane);
             cp_async_commit();
         };
+#endif
         auto issue = [&](unsigned gg) {
             if (lane == 0) spin_cyc += spin_geq(ready + gg % D, ARR * (gg / D + 1));
             __syncwarp();
             pull(gg);
         };
         auto complete = [&](unsigned gg) {
+#if HK_PULL_TMA
+            mbar_wait_parity(cbar_s, cph);
+            cph ^= 1;
+#else
             cp_async_wait_all();
+#endif
             __syncwarp();
             if (lane == 0) signal_add_relaxed(done + gg % D);
         };
