@@ -1620,11 +1620,16 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 double A[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll (ACC ? 4 : kStageU1)
                 for (int k1 = 0; k1 < n; ++k1) {
-                    double2 w = ldg2_hint(fcol + ((int64_t)k1 << (2 * lg)), pol_last);
-                    if constexpr (ACC) {
-                        const int64_t o = cell * nb + col + ((int64_t)k1 << (2 * lg));
-                        const double2 qv = ldg2_hint(acc.q1 + o, pol_last), kv = ldg2_hint(acc.k1 + o, pol_last);
-                        w = make_double2(w.x + acc.cq * qv.x + acc.ck * kv.x, w.y + acc.cq * qv.y + acc.ck * kv.y);
+                    double2 w;
+                    if constexpr (ACC) {  // f_acc formed here and parked in `out` for pass 3 (L2-resident)
+                        const int64_t o = col + ((int64_t)k1 << (2 * lg));
+                        const double2 fv = ldg2_hint(fcol + ((int64_t)k1 << (2 * lg)), pol_first);
+                        const double2 qv = ldg2_hint(acc.q1 + cell * nb + o, pol_first);
+                        const double2 kv = ldg2_hint(acc.k1 + cell * nb + o, pol_first);
+                        w = make_double2(fv.x + acc.cq * qv.x + acc.ck * kv.x, fv.y + acc.cq * qv.y + acc.ck * kv.y);
+                        st2_hint(oc + o, w, pol_last);
+                    } else {
+                        w = ldg2_hint(fcol + ((int64_t)k1 << (2 * lg)), pol_last);
                     }
                     const double2 p = xpow[k1];
                     A[0][0] += w.x; A[1][0] += w.y;
@@ -1662,19 +1667,11 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
         const double A = a * (coeff * m.rho);  // a nu (nu = coeff rho) | a beta_pen (beta = coeff rho)
         if (st != HK_OK || !(A > 0.0)) {
             if (t == 0 && info) info[cell] = st;
-            if (st == HK_OK)
+            if (st == HK_OK && !ACC)  // identity stage (with ACC, pass 1 already left f_acc in out)
                 for (int q = t; q < ngroups; q += MT) {
                     const int idx = 4 * q;
-                    double2 va = ldg2(fc + idx), vb = ldg2(fc + idx + 2);
-                    if constexpr (ACC) {
-                        const int64_t o = cell * nb + idx;
-                        const double2 qa = ldg2(acc.q1 + o), qb = ldg2(acc.q1 + o + 2);
-                        const double2 ka = ldg2(acc.k1 + o), kb = ldg2(acc.k1 + o + 2);
-                        va = make_double2(va.x + acc.cq * qa.x + acc.ck * ka.x, va.y + acc.cq * qa.y + acc.ck * ka.y);
-                        vb = make_double2(vb.x + acc.cq * qb.x + acc.ck * kb.x, vb.y + acc.cq * qb.y + acc.ck * kb.y);
-                    }
-                    *reinterpret_cast<double2*>(oc + idx) = va;
-                    *reinterpret_cast<double2*>(oc + idx + 2) = vb;
+                    *reinterpret_cast<double2*>(oc + idx) = ldg2(fc + idx);
+                    *reinterpret_cast<double2*>(oc + idx + 2) = ldg2(fc + idx + 2);
                     if (k1_out) {  // identity stage: k1 = 0
                         *reinterpret_cast<double2*>(k1_out + cell * nb + idx) = make_double2(0.0, 0.0);
                         *reinterpret_cast<double2*>(k1_out + cell * nb + idx + 2) = make_double2(0.0, 0.0);
@@ -1900,16 +1897,15 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 const int idx = 4 * q;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
                 const double vx = g.node(k1), vy = g.node(k2);
-                const double2 fa = ldg2_hint(fc + idx, pol_first), fb = ldg2_hint(fc + idx + 2, pol_first);
-                double fv[4] = {fa.x, fa.y, fb.x, fb.y};
-                if constexpr (ACC) {
-                    const int64_t o = cell * nb + idx;
-                    const double2 qa = ldg2_hint(acc.q1 + o, pol_first), qb = ldg2_hint(acc.q1 + o + 2, pol_first);
-                    const double2 ka = ldg2_hint(acc.k1 + o, pol_first), kb = ldg2_hint(acc.k1 + o + 2, pol_first);
-                    const double qv[4] = {qa.x, qa.y, qb.x, qb.y}, kv[4] = {ka.x, ka.y, kb.x, kb.y};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) fv[j] = fv[j] + acc.cq * qv[j] + acc.ck * kv[j];
+                double2 fa, fb;
+                if constexpr (ACC) {  // f_acc parked in out by pass 1 (written by other threads: the solve barrier orders it)
+                    fa = *reinterpret_cast<const double2*>(oc + idx);
+                    fb = *reinterpret_cast<const double2*>(oc + idx + 2);
+                } else {
+                    fa = ldg2_hint(fc + idx, pol_first);
+                    fb = ldg2_hint(fc + idx + 2, pol_first);
                 }
+                const double fv[4] = {fa.x, fa.y, fb.x, fb.y};
                 const double cx = vx - uc[0], cy = vy - uc[1];
                 const double pxy = x[0] + x[1] * cx + x[2] * cy + x[4] * (cx * cx + cy * cy);
                 double o[4];

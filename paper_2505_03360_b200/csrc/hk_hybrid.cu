@@ -491,9 +491,19 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
         if (!st) check_status(stk2);
         prof.mark("residual1");
         if (!st) st = explicit_part(1, q1, nullptr, n2_y1);                               // q1
-        if (!st) st = combine_launch(ctx, 2, nk * nb, nb, dt, eps_k, fa, fk, nullptr, q1, k1, nullptr, nullptr);
         prof.mark("combine");
-        if (!st) st = stages(fa, t.a_im11 * dt, Y, nullptr);                              // Y2
+        if (stage_acc_supported(n)) {  // Y2 = stage(f + dt a_ex10 q1 + a_im10 k1), f_acc formed in the stage
+            const double cq = dt * t.a_ex10, ck = t.a_im10;
+            if (!st && n1)
+                st = stage_acc_launch(ctx, true, n, vmax, fk, q1, k1, cq, ck, Y, n1, t.a_im11 * dt, eps_k, p->esbgk_beta,
+                                      p->nu_coeff, stk);
+            if (!st && n2)
+                st = stage_acc_launch(ctx, false, n, vmax, fk + n1 * nb, q1 + n1 * nb, k1 + n1 * nb, cq, ck, Y + n1 * nb,
+                                      n2, t.a_im11 * dt, eps_k + n1, 0.0, p->pen_coeff, stk + n1);
+        } else {
+            if (!st) st = combine_launch(ctx, 2, nk * nb, nb, dt, eps_k, fa, fk, nullptr, q1, k1, nullptr, nullptr);
+            if (!st) st = stages(fa, t.a_im11 * dt, Y, nullptr);                          // Y2
+        }
         prof.mark("stage2");
         if (!st) st = transport(Y);                                                       // T(Y2)
         prof.mark("transport2");
