@@ -204,6 +204,20 @@ int hk_esbgk_imex_step(hk_ctx ctx, int n, double vmax, double* f_dev, int nx, in
 int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int ny, double dx, double dy, double dt,
                            const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
                            double* work_dev);
+/* PR(2,2,2) steps of one x-slab [ny][nx_local][n^3] of a periodic grid split over
+ * the ranks of the context's communicator (hk_ctx_comm_init; without one, or with one
+ * rank, the slab is its own periodic neighbour): before each transport the two edge
+ * columns of the stage field travel to / from the x-neighbours over NCCL on a
+ * separate stream, overlapped with that stage's residual (collision), and the
+ * transport reads them from halo buffers (the reference's in-process neighbour
+ * reads of src/transport.cpp:51-66 across ranks).  Same arithmetic as the periodic
+ * steps above otherwise; work_dev: 6 nx_local ny n^3 doubles or NULL. */
+int hk_penalized_imex_step_slab(hk_ctx ctx, hk_kernel k, double* f_dev, int nx_local, int ny, double dx, double dy,
+                                double dt, const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
+                                double* work_dev);
+int hk_esbgk_imex_step_slab(hk_ctx ctx, int n, double vmax, double* f_dev, int nx_local, int ny, double dx, double dy,
+                            double dt, const double* eps_dev, double beta, double nu_coeff, double eps_weno,
+                            double* work_dev);
 /* Transport of an x-slab [ny][nx][n^3] whose two ghost columns per side come from
  * separate buffers left/right [ny][2][n^3] (filled by the NCCL halo exchange). */
 int hk_transport_rhs_slab(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_dev,

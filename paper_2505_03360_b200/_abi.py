@@ -137,6 +137,9 @@ def lib() -> C.CDLL:
         "hk_esbgk_imex_step": (C.c_int, [vp, C.c_int, dbl, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, dbl, dbl, dbl,
                                          vp]),
         "hk_penalized_imex_step": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, dbl, dbl, u32, vp]),
+        "hk_penalized_imex_step_slab": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, dbl, dbl, u32, vp]),
+        "hk_esbgk_imex_step_slab": (C.c_int, [vp, C.c_int, dbl, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, dbl, dbl, dbl,
+                                              vp]),
         "hk_axpby": (C.c_int, [vp, i64, vp, vp, dbl, vp, dbl, vp]),
         "hk_transport_rhs_slab": (C.c_int, [vp, C.c_int, dbl, vp, vp, vp, vp, C.c_int, C.c_int, dbl, dbl, dbl]),
         "hk_imex_combine": (C.c_int, [vp, C.c_int, i64, i64, dbl, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -89,12 +89,14 @@ int hk_ctx_destroy(hk_ctx ctx) {
     if (ctx->step_work) cudaFree(ctx->step_work);
     if (ctx->hyb_small) cudaFree(ctx->hyb_small);
     if (ctx->hyb_big) cudaFree(ctx->hyb_big);
+    if (ctx->halo_work) cudaFree(ctx->halo_work);
     if (ctx->bad_flag) cudaFree(ctx->bad_flag);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->s_in) cudaStreamDestroy(ctx->s_in);
     if (ctx->sio_flags) cudaFree(ctx->sio_flags);
     if (ctx->s_out) cudaStreamDestroy(ctx->s_out);
     if (ctx->s_side) cudaStreamDestroy(ctx->s_side);
+    if (ctx->s_comm) cudaStreamDestroy(ctx->s_comm);
     delete ctx;
     return HK_OK;
 }
@@ -104,9 +106,10 @@ int hk_ctx_trim(hk_ctx ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
-    void** bufs[] = {&ctx->scratch, &ctx->fix_scratch, &ctx->step_work, &ctx->hyb_small, &ctx->hyb_big};
-    size_t* sizes[] = {&ctx->scratch_bytes, &ctx->fix_bytes, &ctx->step_bytes, &ctx->hyb_small_bytes, &ctx->hyb_big_bytes};
-    for (int i = 0; i < 5; ++i) {
+    void** bufs[] = {&ctx->scratch, &ctx->fix_scratch, &ctx->step_work, &ctx->hyb_small, &ctx->hyb_big, &ctx->halo_work};
+    size_t* sizes[] = {&ctx->scratch_bytes, &ctx->fix_bytes, &ctx->step_bytes, &ctx->hyb_small_bytes, &ctx->hyb_big_bytes,
+                       &ctx->halo_bytes};
+    for (int i = 0; i < 6; ++i) {
         if (*bufs[i]) cudaFree(*bufs[i]);
         *bufs[i] = nullptr;
         *sizes[i] = 0;

@@ -29,6 +29,10 @@ struct hk_ctx_s {
     cudaStream_t s_in = nullptr, s_out = nullptr;
     // side stream of the N = 64 collision (guard + Nyquist correction beside the team kernel)
     cudaStream_t s_side = nullptr;
+    // halo stream and halo buffers of the native x-slab IMEX steps (hk_steps.cu)
+    cudaStream_t s_comm = nullptr;
+    void* halo_work = nullptr;
+    size_t halo_bytes = 0;
     // streamed-I/O flags for the next collision launch (host entry point), and
     // the guard's reroute list / count of the last launch (device pointers)
     const unsigned* sio_in_ready = nullptr;

@@ -181,7 +181,7 @@ int hk_transport_rhs(hk_ctx ctx, int n, double vmax, const double* f_dev, double
 // Shared driver of both PR(2,2,2) steps on a periodic all-kinetic field.
 static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, double* f, int nx, int ny, double dx,
                      double dy, double dt, const double* eps_dev, double beta, double coeff, double eps_weno,
-                     uint32_t flags, double* work_dev) {
+                     uint32_t flags, double* work_dev, bool slab = false) {
     cudaSetDevice(ctx->device);
     const int64_t cells = (int64_t)nx * ny, nb = (int64_t)n * n * n, count = cells * nb;
     const PR222 t = pr222();
@@ -189,6 +189,23 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
     double* owned = nullptr;
     int st = get_work(ctx, work_dev, count, w, &owned);
     if (st) return st;
+    // x-slab: the two [ny][2][n^3] halo buffers (context-owned, grow-only)
+    double *lh = nullptr, *rh = nullptr;
+    if (slab) {
+        const size_t need = sizeof(double) * 4 * (size_t)ny * nb;
+        if (need > ctx->halo_bytes) {
+            if (ctx->halo_work) {
+                cudaStreamSynchronize(ctx->stream);
+                cudaFree(ctx->halo_work);
+                ctx->halo_work = nullptr;
+                ctx->halo_bytes = 0;
+            }
+            if ((st = check_cuda(ctx, cudaMalloc(&ctx->halo_work, need), "halo buffers"))) return st;
+            ctx->halo_bytes = need;
+        }
+        lh = static_cast<double*>(ctx->halo_work);
+        rh = lh + 2 * (int64_t)ny * nb;
+    }
     TransportParams tp{n, vmax, nx, ny, 0, dx, dy, eps_weno};
     auto stage = [&](const double* fin, double a, double* out, double* k1) {
         return boltz ? stage_launch(ctx, false, n, vmax, fin, out, cells, a, eps_dev, 0.0, 0.0, coeff, nullptr, nullptr,
@@ -200,12 +217,54 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
         int s = hk_collision_batch(ctx, k, y, out, cells, flags & ~HK_COLL_STRICT, nullptr);
         return s ? s : residual_finish_launch(ctx, n, vmax, y, out, cells, coeff, nullptr);
     };
+    // x-slab halos of the stage field y: issued on the comm stream as soon as the
+    // stage is written, overlapped with the residual (collision) on the main
+    // stream; the transport waits for them.  With a communicator of >1 rank the
+    // two edge columns travel over NCCL (hk_halo_exchange); otherwise the slab is
+    // its own periodic neighbour (local copies).
+    cudaEvent_t ev_y = nullptr, ev_h = nullptr;
+    if (slab) {
+        if (!ctx->s_comm &&
+            (st = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_comm, cudaStreamNonBlocking), "comm stream")))
+            return st;
+        cudaEventCreateWithFlags(&ev_y, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming);
+    }
+    auto halo_begin = [&](const double* y) -> int {
+        if (!slab) return HK_OK;
+        cudaEventRecord(ev_y, ctx->stream);
+        cudaStreamWaitEvent(ctx->s_comm, ev_y, 0);
+        int e;
+        if (ctx->comm && ctx->nranks > 1) {
+            cudaStream_t main_s = ctx->stream;
+            ctx->stream = ctx->s_comm;
+            e = hk_halo_exchange(ctx, n, y, nx, ny, lh, rh);
+            ctx->stream = main_s;
+        } else {
+            const size_t rowb = sizeof(double) * nx * nb, twob = sizeof(double) * 2 * nb;
+            e = check_cuda(ctx, cudaMemcpy2DAsync(lh, twob, y + (nx - 2) * nb, rowb, twob, ny, cudaMemcpyDeviceToDevice,
+                                                  ctx->s_comm), "halo copy");
+            if (!e)
+                e = check_cuda(ctx, cudaMemcpy2DAsync(rh, twob, y, rowb, twob, ny, cudaMemcpyDeviceToDevice, ctx->s_comm),
+                               "halo copy");
+        }
+        cudaEventRecord(ev_h, ctx->s_comm);
+        return e;
+    };
+    auto transport = [&](const double* y, double* out) -> int {
+        if (!slab) return transport_launch(ctx, tp, y, out);
+        cudaStreamWaitEvent(ctx->stream, ev_h, 0);
+        TransportParams ts = tp;
+        ts.x_halo = -2;
+        return transport_launch(ctx, ts, y, out, lh, rh);
+    };
     double* R = boltz ? w.res : nullptr;
     // Stage 1 (k1 fused into the stage kernel), explicit q1; ES-BGK has no
     // residual, so T(Y1) is q1 itself.
     if (!st) st = stage(f, t.a_im00 * dt, w.y, w.k1);                                      // Y1, k1
-    if (!st) st = transport_launch(ctx, tp, w.y, boltz ? w.tr : w.q1);                     // T(Y1)
-    if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y1)
+    if (!st) st = halo_begin(w.y);
+    if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y1), overlaps the halos
+    if (!st) st = transport(w.y, boltz ? w.tr : w.q1);                                     // T(Y1)
     if (!st && boltz) st = combine(ctx, Q1, count, nb, t, dt, eps_dev, w.q1, 0, 0, 0, 0, w.tr, R);  // q1
     if (stage_acc_supported(n)) {  // Y2 = stage(f_acc), f_acc = f + dt a_ex10 q1 + a_im10 k1 formed in the stage
         if (!st)
@@ -215,14 +274,20 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
         if (!st) st = combine(ctx, FACC, count, nb, t, dt, eps_dev, w.fa, f, 0, w.q1, w.k1, 0, 0);  // f_acc
         if (!st) st = stage(w.fa, t.a_im11 * dt, w.y, nullptr);                                // Y2
     }
+    if (!st) st = halo_begin(w.y);
     if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y2)
-    if (!st && transport_final_supported(tp)) {  // T(Y2) + final combination, one kernel
+    if (!st && !slab && transport_final_supported(tp)) {  // T(Y2) + final combination, one kernel
         const FinalCombine fc{f, w.q1, w.k1, R, eps_dev, dt, t.a_ex10, t.a_im10, t.a_im11, t.w_ex0, t.w_ex1, t.w_im0,
                               t.w_im1};
         st = transport_final_launch(ctx, tp, w.y, fc);
     } else {
-        if (!st) st = transport_launch(ctx, tp, w.y, w.tr);                                // T(Y2)
+        if (!st) st = transport(w.y, w.tr);                                                // T(Y2)
         if (!st) st = combine(ctx, FINAL, count, nb, t, dt, eps_dev, f, 0, w.y, w.q1, w.k1, w.tr, R);
+    }
+    if (slab) {
+        cudaStreamWaitEvent(ctx->stream, ev_h, 0);  // error paths: the comm stream's copies are done before reuse
+        cudaEventDestroy(ev_y);
+        cudaEventDestroy(ev_h);
     }
     if (owned) cudaFreeAsync(owned, ctx->stream);
     return st;
@@ -272,6 +337,28 @@ int hk_axpby(hk_ctx ctx, int64_t count, double* out_dev, const double* x_dev, do
              const double* z_dev) {
     cudaSetDevice(ctx->device);
     return axpby_launch(ctx, count, out_dev, x_dev, a, y_dev, b, z_dev);
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int hk_penalized_imex_step_slab(hk_ctx ctx, hk_kernel k, double* f_dev, int nx_local, int ny, double dx, double dy,
+                                double dt, const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
+                                double* work_dev) {
+    if (!ctx || !k) return HK_CONTRACT;
+    if (nx_local < 2 || ny < 1) return fail(ctx, HK_CONTRACT, "slab step: need nx_local >= 2 columns");
+    return imex_step(ctx, k, true, k->n, k->vmax, f_dev, nx_local, ny, dx, dy, dt, eps_dev, 0.0, pen_coeff, eps_weno,
+                     flags, work_dev, true);
+}
+
+int hk_esbgk_imex_step_slab(hk_ctx ctx, int n, double vmax, double* f_dev, int nx_local, int ny, double dx, double dy,
+                            double dt, const double* eps_dev, double beta, double nu_coeff, double eps_weno,
+                            double* work_dev) {
+    if (!ctx) return HK_CONTRACT;
+    if (nx_local < 2 || ny < 1) return fail(ctx, HK_CONTRACT, "slab step: need nx_local >= 2 columns");
+    return imex_step(ctx, nullptr, false, n, vmax, f_dev, nx_local, ny, dx, dy, dt, eps_dev, beta, nu_coeff, eps_weno, 0,
+                     work_dev, true);
 }
 
 }  // extern "C"

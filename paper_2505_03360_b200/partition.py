@@ -225,6 +225,37 @@ def penalized_imex_step_slab(part: XSlab, f: torch.Tensor, kernel, dx: float, dy
     return f
 
 
+def imex_step_slab_native(part: XSlab, f: torch.Tensor, kernel, dx: float, dy: float, dt: float,
+                          eps_cell: torch.Tensor, pen_coeff: float = 6.283185307179586, eps_weno: float = 1e-6,
+                          exact: bool = False, work=None):
+    """penalized_imex_step (src/boltzmann.cpp:47-110) on one x-slab, in place, driven
+    in C++ (hk_penalized_imex_step_slab): the halos travel over the context's own NCCL
+    communicator (Context.comm_init; without one the slab wraps onto itself) on a
+    separate stream, overlapped with each stage's collision."""
+    from . import _abi
+
+    ctx = kernel.ctx
+    if not (f.is_cuda and f.dtype == torch.float64 and f.is_contiguous()):
+        raise ValueError("f must be a contiguous float64 CUDA tensor")
+    e = eps_cell.to(device=f.device, dtype=torch.float64).contiguous()
+    ctx.check(ctx._lib.hk_penalized_imex_step_slab(ctx.h, kernel.h, f.data_ptr(), part.nxl, part.ny, dx, dy, dt,
+                                                   e.data_ptr(), pen_coeff, eps_weno,
+                                                   _abi.HK_COLL_EXACT if exact else 0,
+                                                   None if work is None else work.data_ptr()))
+    return f
+
+
+def native_comm_init(ctx, group=None):
+    """Gives the context its own NCCL communicator over the ranks of `group`
+    (rank 0's unique id travels over torch.distributed)."""
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    rank = dist.get_rank(group) if world > 1 else 0
+    uid = [ctx.comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0, group=group)
+    ctx.comm_init(world, rank, uid[0])
+
+
 # Ghost width of the slab hybrid step: the exact dependency radius of one
 # hybrid step along x is 7 cells (regime update 1, halo Maxwellians +2, two
 # transport sweeps +2 each; the layer-0 TVD-RK2 needs 4), so a slab padded with
