@@ -74,6 +74,14 @@ int hk_ctx_create(int device, hk_ctx* out) {
     auto* c = new hk_ctx_s;
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    // The host entry points allocate their device slabs stream-ordered every call
+    // (cudaMallocAsync): keep the pool's memory mapped between calls instead of
+    // returning it to the OS at each synchronisation (hk_ctx_trim trims it).
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     *out = c;
     return HK_OK;
 }
@@ -106,6 +114,8 @@ int hk_ctx_trim(hk_ctx ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     else cudaDeviceSynchronize();
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     void** bufs[] = {&ctx->scratch, &ctx->fix_scratch, &ctx->step_work, &ctx->hyb_small, &ctx->hyb_big, &ctx->halo_work};
     size_t* sizes[] = {&ctx->scratch_bytes, &ctx->fix_bytes, &ctx->step_bytes, &ctx->hyb_small_bytes, &ctx->hyb_big_bytes,
                        &ctx->halo_bytes};
