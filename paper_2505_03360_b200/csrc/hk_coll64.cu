@@ -525,7 +525,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
     uint64_t* fbar = reinterpret_cast<uint64_t*>(smem + 3 * PLANE);  // [P] F-plane ready
     uint32_t* tslot = reinterpret_cast<uint32_t*>(fbar + P);
     uint64_t* wbar = fbar + P + 1;  // weight-plane TMA barrier of the producer group
-    uint64_t* cbar = fbar + P + 2;  // [8] consumer pull barriers (HK_PULL_TMA64)
+    uint64_t* cbar = fbar + P + 5;  // [8] consumer pull barriers (HK_PULL_TMA64)
 
     const int t = threadIdx.x;
     const int warp = t >> 5, lane = t & 31;
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
 
     if (warp == 0) tmem_alloc(tslot, G::TM_COLS);
     if (t < P) mbar_init(smem_u32(fbar + t), 128);
-    if (HK_W_TMA64 && t == 32) mbar_init(smem_u32(wbar), 1);
+    if (HK_W_TMA64 && t >= 32 && t < 36) mbar_init(smem_u32(wbar + (t - 32)), 1);
     if (HK_PULL_TMA64 && t >= 64 && t < 72) mbar_init(smem_u32(cbar + (t - 64)), 1);
     if (t == 0) asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     tmem_fence_before();
@@ -558,20 +558,20 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         // Weight staging: thread-private slots [m][u] (interleaved: conflict-free).
         const uint32_t wb_s = smem_u32(Pw);
 #if HK_W_TMA64
-        // the unit's [i3][i2] weight plane (64 KiB, the table's own layout) by four
-        // bulk copies issued by thread 0 once every producer warp has finished
-        // reading the previous plane; completion on one mbarrier
-        const uint32_t wbar_s = smem_u32(wbar);
+        // each producer warp fetches its own 16 pencils' weights of the unit's plane,
+        // one contiguous 16 KiB block of the warp-blocked table ([i1][i2/16][i3][i2%16],
+        // hk_weights.cu), by one bulk copy completing on its own mbarrier: no barrier
+        // across the producer warps
+        const uint32_t wbar_s = smem_u32(wbar + rw);
+        const uint32_t wq_s = wb_s + rw * (N * 16 * 16);
         unsigned wph = 0;
         auto issue_w = [&](int fi, int pl) {
             const int i1 = r * P + pl;
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            named_bar(1, 128);
-            if (t == 0) {
-                const double2* src = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N;
-                mbar_arrive_expect_tx(wbar_s, N * N * 16);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) bulk_g2s(wb_s + q * (N * N * 4), src + q * (N * N / 4), N * N * 4, wbar_s);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // my reads of the block before the async write
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive_expect_tx(wbar_s, N * 16 * 16);
+                bulk_g2s(wq_s, a.wfast + (int64_t)fi * NB + ((int64_t)i1 * 4 + rw) * (N * 16), N * 16 * 16, wbar_s);
             }
         };
         auto wait_w = [&]() {
@@ -580,11 +580,11 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
         };
 #else
         auto wait_w = [&]() { cp_async_wait_all(); };
-        auto issue_w = [&](int fi, int pl) {
+        auto issue_w = [&](int fi, int pl) {  // warp-blocked table: pencil pp's column in block rw
             const int i1 = r * P + pl;
-            const double2* wt = a.wfast + (int64_t)fi * NB + (int64_t)i1 * N * N + pp;
+            const double2* wt = a.wfast + (int64_t)fi * NB + ((int64_t)i1 * 4 + rw) * (N * 16) + (pp & 15);
 #pragma unroll
-            for (int m = 0; m < M; ++m) cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * N);
+            for (int m = 0; m < M; ++m) cp_async16(wb_s + (m * 128 + u) * 16, wt + (2 * m + h) * 16);
             cp_async_commit();
         };
 #endif
@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(384, 1) coll64_w12_kernel(CollArgs a) {
 #pragma unroll
                         for (int m = 0; m < M; ++m) {
 #if HK_W_TMA64
-                            const double2 w = wb[(2 * m + h) * N + pp], v = x[m];
+                            const double2 w = wb[rw * (N * 16) + (2 * m + h) * 16 + (pp & 15)], v = x[m];
 #else
                             const double2 w = wb[m * 128 + u], v = x[m];
 #endif

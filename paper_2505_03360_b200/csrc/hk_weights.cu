@@ -10,7 +10,8 @@
 //  2. build_kernel_tables: from raw tables (closed form, or the reference's
 //     own tables uploaded verbatim) build the device layouts:
 //        exact  alpha / alpha_p / loss   [entry][i1][i3][i2]
-//        fast   (alpha_s, alpha'_s)      Hermitian-symmetrised, entry md = (loss_s, 0)
+//        fast   (alpha_s, alpha'_s)      Hermitian-symmetrised, entry md = (loss_s, 0);
+//                                         at n = 64 [entry][i1][i2 / 16][i3][i2 % 16] (warp blocks)
 //        nyquist alpha_a, alpha'_a  antisymmetric parts on the three Nyquist planes
 //                                   (signed: the guard takes |.|, the correction kernel the values).
 #include <cmath>
@@ -83,6 +84,9 @@ __global__ void layout_kernel(int n, int a2, int md, const double* __restrict__ 
     const int m1 = (n - i1) % n, m2 = (n - i2) % n, m3 = (n - i3) % n;
     const int64_t midx = ((int64_t)m1 * n + m2) * n + m3;
     const int64_t dev = ((int64_t)i1 * n + i3) * n + i2;  // [i1][i3][i2]
+    // fast table at n = 64: [i1][i2 / 16][i3][i2 % 16], so the 16 pencils of one
+    // producer warp of coll64_w12_kernel are one contiguous 16 KiB block (one bulk copy)
+    const int64_t fdev = n == 64 ? (((int64_t)i1 * 4 + (i2 >> 4)) * n + i3) * 16 + (i2 & 15) : dev;
     const int h = n / 2;
     const int64_t nn = (int64_t)n * n;
     for (int e = 0; e < md; ++e) {
@@ -91,7 +95,7 @@ __global__ void layout_kernel(int n, int a2, int md, const double* __restrict__ 
         const double ap = rap[(int64_t)d * total + idx], apm = rap[(int64_t)d * total + midx];
         alpha[(int64_t)e * total + dev] = a;
         alpha_p[(int64_t)e * total + dev] = ap;
-        wfast[(int64_t)e * total + dev] = make_double2(0.5 * (a + am), 0.5 * (ap + apm));
+        wfast[(int64_t)e * total + fdev] = make_double2(0.5 * (a + am), 0.5 * (ap + apm));
         const double aa = 0.5 * (a - am), aap = 0.5 * (ap - apm);  // signed antisymmetric parts
         double* pa = abs_a + (int64_t)e * 3 * nn;
         double* pap = abs_ap + (int64_t)e * 3 * nn;
@@ -108,7 +112,7 @@ __global__ void layout_kernel(int n, int a2, int md, const double* __restrict__ 
         }
     }
     loss[dev] = rl[idx];
-    wfast[(int64_t)md * total + dev] = make_double2(0.5 * (rl[idx] + rl[midx]), 0.0);
+    wfast[(int64_t)md * total + fdev] = make_double2(0.5 * (rl[idx] + rl[midx]), 0.0);
 }
 
 }  // namespace
