@@ -4,6 +4,7 @@
 #include <cuda.h>
 
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -407,7 +408,17 @@ static bool host_range_pinned(const void* p, size_t bytes) {
 
 static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host, int64_t ncells,
                                    uint32_t flags, hk_cell_status* st_host) {
+#if HK_PROFILING
+    if (getenv("HK_PROF_HOST")) fprintf(stderr, "[hk prof host] streamed path: memops %d\n", (int)stream_memops_available());
+#endif
     if (!stream_memops_available()) return HK_UNSUPPORTED;
+#if HK_PROFILING
+    const auto t_in = std::chrono::steady_clock::now();
+    auto ms_since = [&](std::chrono::steady_clock::time_point a) {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+    };
+    double t_enq = 0, t_launch = 0, t_sync = 0, t_tail = 0;
+#endif
     const size_t nb = size_t(k->n) * k->n * k->n;
     const size_t bytes = sizeof(double) * nb * ncells;
     // 32 chunks: the unoverlapped pipeline fill (first H2D) and drain (last D2H) are 1/32 of the copies
@@ -436,8 +447,7 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
     cudaEventRecord(e0, ctx->stream);
     cudaStreamWaitEvent(ctx->s_in, e0, 0);
     cudaStreamWaitEvent(ctx->s_out, e0, 0);
-    // Enqueue the copy streams first (H2D + ready flags, waits + D2H): nothing
-    // is launched until the stream memory operations are known to work.
+    // Probe the stream memory operations before anything depends on them.
     const unsigned per_cell = 8u * 4u;  // consumer plane epilogues per cell (= N planes of j3, every warp kernel)
     {
         CUresult r0 = p_write_value32((CUstream)ctx->s_in, (CUdeviceptr)flags_dev, 0, 0);
@@ -451,6 +461,33 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
             cudaFreeAsync(st_dev, ctx->stream);
             return HK_UNSUPPORTED;  // stream memory operations unavailable: chunked path
         }
+    }
+    // Launch the persistent kernel FIRST (it waits on the in_ready flags), then
+    // queue the copies.  Nothing between the launch and the last copy may
+    // synchronise the device, or the kernel would wait forever for flags the
+    // host has not queued yet: scratch is sized before the launch (run_size),
+    // and the kernels queued behind it are loaded now, because a lazy module
+    // load on their first launch waits for the device to go idle.
+    hk::preload_guard_kernels(k->n);
+    ctx->sio_in_ready = flags_dev;
+    ctx->sio_out_done = flags_dev + nch;
+    ctx->sio_chunk = chunk;
+    ctx->sio_used = false;
+    st = hk_collision_batch(ctx, k, f_dev, q_dev, ncells, flags, st_dev);
+    const bool streamed = ctx->sio_used;
+    ctx->sio_in_ready = nullptr;
+    ctx->sio_out_done = nullptr;
+    ctx->sio_used = false;
+#if HK_PROFILING
+    t_launch = ms_since(t_in);
+#endif
+    if (!st && !streamed) {  // a kernel variant without streamed I/O ran on an empty slab: redo it chunked
+        cudaStreamSynchronize(ctx->stream);
+        cudaEventDestroy(e0);
+        cudaFreeAsync(f_dev, ctx->stream);
+        cudaFreeAsync(q_dev, ctx->stream);
+        cudaFreeAsync(st_dev, ctx->stream);
+        return HK_UNSUPPORTED;
     }
     for (int64_t c = 0; c < nch && !st; ++c) {
         const int64_t c0 = c * chunk, nc = (ncells - c0) < chunk ? (ncells - c0) : chunk;
@@ -466,23 +503,14 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
             st = check_cuda(ctx, cudaMemcpyAsync(q_host + c0 * nb, q_dev + c0 * nb, sizeof(double) * nb * nc,
                                                  cudaMemcpyDeviceToHost, ctx->s_out), "D2H q");
     }
-    if (!st) {
-        ctx->sio_in_ready = flags_dev;
-        ctx->sio_out_done = flags_dev + nch;
-        ctx->sio_chunk = chunk;
-        ctx->sio_used = false;
-        st = hk_collision_batch(ctx, k, f_dev, q_dev, ncells, flags, st_dev);
-        const bool streamed = ctx->sio_used;
-        ctx->sio_in_ready = nullptr;
-        ctx->sio_out_done = nullptr;
-        ctx->sio_used = false;
-        if (!st && !streamed) st = HK_UNSUPPORTED;  // kernel variant without streamed I/O: caller redoes it chunked
-    }
+#if HK_PROFILING
+    t_enq = ms_since(t_in);
+#endif
     if (st) {
-        // Nothing (or not everything) will complete the out_done counters the D2H
-        // stream waits on: a failed enqueue, a failed launch, or a kernel that did
-        // not stream.  Complete them from the compute stream so s_out drains and
-        // the error is returned instead of blocking in the synchronise below.
+        // Nothing (or not everything) will complete the counters the copy streams and
+        // the kernel wait on: a failed launch or a failed copy enqueue.  Complete them
+        // from the compute stream so everything drains and the error is returned
+        // instead of blocking in the synchronise below.
         for (int64_t c = 0; c < nch; ++c)
             p_write_value32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
         for (int64_t c = 0; c < nch; ++c)
@@ -492,6 +520,9 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
     int count = 0;
     std::vector<int64_t> list;
     if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+#if HK_PROFILING
+    t_sync = ms_since(t_in);
+#endif
     if (!st && ctx->last_count) {
         st = check_cuda(ctx, cudaMemcpy(&count, ctx->last_count, sizeof(int), cudaMemcpyDeviceToHost), "D2H count");
         if (!st && count > 0) {
@@ -509,6 +540,12 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
     const int s1 = check_cuda(ctx, cudaStreamSynchronize(ctx->s_out), "sync out");
     const int s2 = check_cuda(ctx, cudaStreamSynchronize(ctx->s_in), "sync in");
     if (!st) st = s1 ? s1 : s2;
+#if HK_PROFILING
+    t_tail = ms_since(t_in);
+    if (getenv("HK_PROF_HOST"))
+        fprintf(stderr, "[hk prof host] launch %.2f enqueue %.2f compute-sync %.2f all-copies %.2f ms (%lld cells, %lld chunks)\n",
+                t_launch, t_enq, t_sync, t_tail, (long long)ncells, (long long)nch);
+#endif
     cudaEventDestroy(e0);
     cudaFreeAsync(f_dev, ctx->stream);
     cudaFreeAsync(q_dev, ctx->stream);
@@ -529,14 +566,17 @@ int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, doubl
             (st = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_out, cudaStreamNonBlocking), "stream")))
             return st;
     }
-    // The streamed path queues D2H copies behind device-side waits BEFORE the
-    // kernel that releases them is launched: a copy to pageable memory is
-    // synchronous with the host, so it would block here forever.  Streamed I/O
-    // therefore needs every host buffer page-locked; anything else is chunked.
+    // The streamed path queues the chunks' D2H copies behind device-side waits
+    // on counters the running kernel publishes: a copy to pageable memory is
+    // synchronous with the host (staged), so streamed I/O needs f and q
+    // page-locked (anything else is chunked); the status array is copied after
+    // the kernel has completed and may be pageable.
     if (k->n == 32 && !(flags & (HK_COLL_EXACT | HK_COLL_STRICT)) && ncells >= 256 &&
-        host_range_pinned(f_host, bytes) && host_range_pinned(q_host, bytes) &&
-        (!st_host || host_range_pinned(st_host, sizeof(hk_cell_status) * ncells))) {
+        host_range_pinned(f_host, bytes) && host_range_pinned(q_host, bytes)) {
         st = collision_host_streamed(ctx, k, f_host, q_host, ncells, flags, st_host);
+#if HK_PROFILING
+        if (getenv("HK_PROF_HOST")) fprintf(stderr, "[hk prof host] streamed path returned %d\n", st);
+#endif
         if (st != HK_UNSUPPORTED) return st;
         cudaStreamSynchronize(ctx->stream);
     }

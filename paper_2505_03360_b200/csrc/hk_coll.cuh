@@ -48,6 +48,9 @@ __global__ void residue_kernel(int64_t ncells, hk_cell_status* st);
 
 // hk_nyqfix.cu: exact Nyquist correction of the fast result for the cells on a
 // device list (the guard's reroute list).
+void nyq_fix_preload(int n);
+void preload_guard_kernels(int n);
+int nyq_fix_reserve(hk_ctx ctx, int n, int md, int64_t max_cells);
 int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int64_t max_cells, const double2* nyqF,
                    const double* ta, const double* tap, int md, double mult0, double jac, double w, double* q,
                    hk_cell_status* st);

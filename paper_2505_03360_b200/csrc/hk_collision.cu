@@ -516,7 +516,10 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
         for (int64_t it = team; it < count; it += nteams, ++ncell) {
             const int64_t cell = a.list ? a.list[it] : it;
             const double* fc = a.f + cell * NB;
-            if (a.in_ready && t == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);  // host chunk has landed
+            if (a.in_ready && pw == 0) {  // host chunk has landed (warp 0 reconverges before the named barrier)
+                if (lane == 0) spin_geq(a.in_ready + cell / a.chunk, 1u);
+                __syncwarp();
+            }
             // ---- prologue: 2-D forward transforms of j3 planes 4 pp + (0..3) ----
 #pragma unroll 1
             for (int pp = 0; pp < PPW; ++pp) {
@@ -965,6 +968,18 @@ __global__ void residue_kernel(int64_t ncells, hk_cell_status* st) {
         s->flags |= HK_CELL_RESIDUE;
 }
 
+// Under lazy module loading (the CUDA 12 default) the first launch of a kernel
+// loads it, and loading may wait for the device to go idle.  The streamed host
+// path launches a persistent kernel that waits on host-fed flags, so every
+// kernel launched behind it (guard, correction, residue) is loaded first.
+void preload_guard_kernels(int n) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, guard_kernel);
+    cudaFuncGetAttributes(&fa, guard_finish_kernel);
+    cudaFuncGetAttributes(&fa, residue_kernel);
+    nyq_fix_preload(n);
+}
+
 namespace {
 
 template <int N, int C, bool EXACT>
@@ -1327,6 +1342,8 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     }
     int s;
     if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
+    // every allocation of the call happens before the first launch (see nyq_fix_reserve)
+    if (guard && (s = nyq_fix_reserve(ctx, N, k->md, N == 64 && ncells >= 2048 ? (ncells + 3) / 4 : ncells))) return s;
     char* base = static_cast<char*>(ctx->scratch);
     if (!st) st = reinterpret_cast<hk_cell_status*>(base);
     double2* nyq = guard ? reinterpret_cast<double2*>(base + st_bytes) : nullptr;

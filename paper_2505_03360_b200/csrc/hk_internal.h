@@ -96,6 +96,7 @@ int closed_form_raw_tables(hk_ctx ctx, hk_kernel k, double* raw_alpha_dev,
                            double* raw_alpha_p_dev, double* raw_loss_dev);
 
 // hk_collision.cu
+void preload_guard_kernels(int n);  // hk_collision.cu: load the kernels queued behind a streamed launch
 int collision_launch(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells,
                      uint32_t flags, hk_cell_status* st);
 

@@ -218,9 +218,11 @@ __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __rest
     }
 }
 
-int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int64_t max_cells, const double2* nyqF,
-                   const double* ta, const double* tap, int md, double mult0, double jac, double w, double* q,
-                   hk_cell_status* st) {
+// Grows the plane scratch for up to max_cells listed cells.  Growing
+// synchronises the device (cudaFree / cudaMalloc), so run_size reserves it
+// BEFORE launching the collision kernel: a kernel waiting on host-fed flags
+// (the streamed host path) must never sit behind an implicit synchronisation.
+int nyq_fix_reserve(hk_ctx ctx, int n, int md, int64_t max_cells) {
     if (max_cells < 1) return HK_OK;
     const size_t per_cell = size_t(md) * 3 * n * n * sizeof(double2);
     int64_t chunk = int64_t((size_t(2) << 30) / per_cell);
@@ -238,6 +240,30 @@ int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int
         if (s) return s;
         ctx->fix_bytes = need;
     }
+    return HK_OK;
+}
+
+// Forces the lazy load of the correction kernels for size n (see preload_guard_kernels).
+void nyq_fix_preload(int n) {
+    cudaFuncAttributes fa;
+    switch (n) {
+    case 16: cudaFuncGetAttributes(&fa, nyq_planes_kernel<16>); cudaFuncGetAttributes(&fa, nyq_apply_kernel<16>); break;
+    case 32: cudaFuncGetAttributes(&fa, nyq_planes_kernel<32>); cudaFuncGetAttributes(&fa, nyq_apply_kernel<32>); break;
+    case 64: cudaFuncGetAttributes(&fa, nyq_planes_kernel<64>); cudaFuncGetAttributes(&fa, nyq_apply_kernel<64>); break;
+    default: break;
+    }
+}
+
+int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int64_t max_cells, const double2* nyqF,
+                   const double* ta, const double* tap, int md, double mult0, double jac, double w, double* q,
+                   hk_cell_status* st) {
+    if (max_cells < 1) return HK_OK;
+    const size_t per_cell = size_t(md) * 3 * n * n * sizeof(double2);
+    int64_t chunk = int64_t((size_t(2) << 30) / per_cell);
+    if (chunk < 1) chunk = 1;
+    if (chunk > max_cells) chunk = max_cells;
+    int s0 = nyq_fix_reserve(ctx, n, md, max_cells);
+    if (s0) return s0;
     double2* planes = static_cast<double2*>(ctx->fix_scratch);
     auto run = [&](auto k1, size_t smem1, int per_sm1, auto k2, size_t smem2) -> int {
         int s;
