@@ -92,7 +92,9 @@ int hk_copy_to_host(hk_ctx ctx, void* dst_host, const void* src_dev, size_t byte
 int hk_ctx_synchronize(hk_ctx ctx);
 /* CUDA-event timing of the library's kernels on the context stream (for the
  * roofline in bench.py).  Enabling clears previous records.  tag 0 = main
- * collision kernel, 1 = Nyquist guard, 2 = Nyquist correction of the listed cells. */
+ * collision kernel, 1 = Nyquist guard, 2 = Nyquist correction of the listed
+ * cells; PR(2,2,2) steps: 10 = stage 1, 11 = transport of Y1, 12 = stage 2
+ * (f_acc fused), 13 = transport of Y2 (+ final combination). */
 int hk_ctx_set_timing(hk_ctx ctx, int on);
 int hk_ctx_timing_report(hk_ctx ctx, int tag, double* total_ms, int64_t* launches);
 

@@ -57,6 +57,15 @@ struct TransportParams {
 // (src/boltzmann.cpp:99-108, src/esbgk.cpp:90-97): with T = T(Y2) computed in
 // place,  q2 = T + res/eps,  f_acc = f + dt a_ex10 q1 + a_im10 k1,
 // k2 = (Y2 - f_acc)/a_im11,  f += dt (w0 q1 + w1 q2) + w0 k1 + w1 k2.
+// Elementwise PR(2,2,2) work fused into a transport sweep T(y) (hk_transport.cu).
+//   mode 1: f <- f + dt (w_ex0 q1 + w_ex1 q2) + w_im0 k1 + w_im1 k2, q2 = T(y) + res / eps,
+//           k2 = (y - f_acc) / a_im11, f_acc = f + dt a_ex10 q1 + a_im10 k1   (src/boltzmann.cpp:80-105)
+//   mode 2: y = Y1, q1 = T(Y1) + res / eps, k1 = (Y1 - f) k1_scale:
+//           fa <- f_acc,  f <- G = f + dt w_ex0 q1 + w_im0 k1 - (w_im1 / a_im11) f_acc
+//   mode 3: y = Y2 (the stage of f_acc):  f <- G + dt w_ex1 q2 + (w_im1 / a_im11) Y2
+// Modes 2 + 3 are mode 1 regrouped: the final update is linear in (f, q1, k1),
+// so the transport of Y1 folds those three fields into two (f_acc for the
+// second stage, G in place of f) and neither q1 nor k1 is ever stored.
 struct FinalCombine {
     double* f;               // in/out
     const double* q1;
@@ -64,6 +73,9 @@ struct FinalCombine {
     const double* res;       // nullable (ES-BGK)
     const double* eps;       // per cell
     double dt, a_ex10, a_im10, a_im11, w_ex0, w_ex1, w_im0, w_im1;
+    int mode = 1;
+    double* fa = nullptr;    // mode 2: f_acc out
+    double k1_scale = 0.0;   // mode 2: 1 / a_im00
 };
 int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh = nullptr,
                      const double* rh = nullptr);
@@ -73,6 +85,8 @@ int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const d
 // PR(2,2,2) second transport + final combination (x periodic); false if the
 // marching kernel does not apply (caller runs transport + combine instead).
 bool transport_final_supported(const TransportParams& p);
+int transport_fused_launch(hk_ctx ctx, const TransportParams& p, const double* y, const FinalCombine& fc,
+                           const double* lh = nullptr, const double* rh = nullptr);
 // Row activity of the transport strips for a [ny][nx] cell mask (nonzero = the
 // output is needed); act holds transport_row_activity_bytes(nx, ny) bytes.
 size_t transport_row_activity_bytes(int nx, int ny);

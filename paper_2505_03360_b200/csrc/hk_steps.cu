@@ -259,17 +259,59 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
         return transport_launch(ctx, ts, y, out, lh, rh);
     };
     double* R = boltz ? w.res : nullptr;
+    auto timed = [&](int tag, auto&& fn) {  // hk_ctx_set_timing: per-part step times (tags 10..13)
+        timing_begin(ctx, tag);
+        const int e = fn();
+        timing_end(ctx);
+        return e;
+    };
+    TransportParams tps = tp;
+    if (slab) tps.x_halo = -2;
+    if (stage_acc_supported(n) && transport_final_supported(tps)) {
+        // Regrouped step (FinalCombine modes 2 / 3): four field kernels, and
+        // neither q1 nor k1 is stored.  T(Y1) writes f_acc and, in place of f,
+        // G = f + dt w_ex0 q1 + w_im0 k1 - (w_im1 / a_im11) f_acc; T(Y2) finishes
+        // f = G + dt w_ex1 q2 + (w_im1 / a_im11) Y2, which is the reference's
+        // final update (src/boltzmann.cpp:100-105, src/esbgk.cpp:92-97) with
+        // k2 = (Y2 - f_acc) / a_im11 expanded.
+        FinalCombine fm{f, nullptr, nullptr, R, eps_dev, dt, t.a_ex10, t.a_im10, t.a_im11, t.w_ex0, t.w_ex1, t.w_im0,
+                        t.w_im1};
+        fm.fa = w.fa;
+        fm.k1_scale = 1.0 / t.a_im00;
+        auto fused = [&](const double* y, int mode) -> int {
+            fm.mode = mode;
+            if (slab) cudaStreamWaitEvent(ctx->stream, ev_h, 0);
+            return transport_fused_launch(ctx, tps, y, fm, lh, rh);
+        };
+        if (!st) st = timed(10, [&] { return stage(f, t.a_im00 * dt, w.y, nullptr); });  // Y1
+        if (!st) st = halo_begin(w.y);
+        if (!st && boltz) st = residual(w.y, w.res);                                     // res(Y1), overlaps the halos
+        if (!st) st = timed(11, [&] { return fused(w.y, 2); });                          // T(Y1) -> f_acc, G
+        if (!st) st = timed(12, [&] { return stage(w.fa, t.a_im11 * dt, w.y, nullptr); });  // Y2
+        if (!st) st = halo_begin(w.y);
+        if (!st && boltz) st = residual(w.y, w.res);                                     // res(Y2)
+        if (!st) st = timed(13, [&] { return fused(w.y, 3); });                          // T(Y2) -> f
+        if (slab) {
+            cudaStreamWaitEvent(ctx->stream, ev_h, 0);
+            cudaEventDestroy(ev_y);
+            cudaEventDestroy(ev_h);
+        }
+        if (owned) cudaFreeAsync(owned, ctx->stream);
+        return st;
+    }
     // Stage 1 (k1 fused into the stage kernel), explicit q1; ES-BGK has no
     // residual, so T(Y1) is q1 itself.
-    if (!st) st = stage(f, t.a_im00 * dt, w.y, w.k1);                                      // Y1, k1
+    if (!st) st = timed(10, [&] { return stage(f, t.a_im00 * dt, w.y, w.k1); });            // Y1, k1
     if (!st) st = halo_begin(w.y);
     if (!st && boltz) st = residual(w.y, w.res);                                           // res(Y1), overlaps the halos
-    if (!st) st = transport(w.y, boltz ? w.tr : w.q1);                                     // T(Y1)
+    if (!st) st = timed(11, [&] { return transport(w.y, boltz ? w.tr : w.q1); });           // T(Y1)
     if (!st && boltz) st = combine(ctx, Q1, count, nb, t, dt, eps_dev, w.q1, 0, 0, 0, 0, w.tr, R);  // q1
     if (stage_acc_supported(n)) {  // Y2 = stage(f_acc), f_acc = f + dt a_ex10 q1 + a_im10 k1 formed in the stage
         if (!st)
-            st = stage_acc_launch(ctx, !boltz, n, vmax, f, w.q1, w.k1, dt * t.a_ex10, t.a_im10, w.y, cells,
-                                  t.a_im11 * dt, eps_dev, boltz ? 0.0 : beta, coeff, nullptr);
+            st = timed(12, [&] {
+                return stage_acc_launch(ctx, !boltz, n, vmax, f, w.q1, w.k1, dt * t.a_ex10, t.a_im10, w.y, cells,
+                                        t.a_im11 * dt, eps_dev, boltz ? 0.0 : beta, coeff, nullptr);
+            });
     } else {
         if (!st) st = combine(ctx, FACC, count, nb, t, dt, eps_dev, w.fa, f, 0, w.q1, w.k1, 0, 0);  // f_acc
         if (!st) st = stage(w.fa, t.a_im11 * dt, w.y, nullptr);                                // Y2
@@ -279,9 +321,9 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
     if (!st && !slab && transport_final_supported(tp)) {  // T(Y2) + final combination, one kernel
         const FinalCombine fc{f, w.q1, w.k1, R, eps_dev, dt, t.a_ex10, t.a_im10, t.a_im11, t.w_ex0, t.w_ex1, t.w_im0,
                               t.w_im1};
-        st = transport_final_launch(ctx, tp, w.y, fc);
+        st = timed(13, [&] { return transport_final_launch(ctx, tp, w.y, fc); });
     } else {
-        if (!st) st = transport(w.y, w.tr);                                                // T(Y2)
+        if (!st) st = timed(13, [&] { return transport(w.y, w.tr); });                      // T(Y2)
         if (!st) st = combine(ctx, FINAL, count, nb, t, dt, eps_dev, f, 0, w.y, w.q1, w.k1, w.tr, R);
     }
     if (slab) {

@@ -77,7 +77,7 @@ __device__ __forceinline__ double cweno3_face(double um, double uc, double up, d
 // 3); lanes 0, 1, 30, 31 are halo columns (no output).
 constexpr int TL_OUT = 28;
 
-template <bool FINAL, int NPT, bool MASK = false>
+template <int MODE, int NPT, bool MASK = false>
 __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p, int lg, const double* __restrict__ f,
                                                               double* __restrict__ out, const double* __restrict__ lh,
                                                               const double* __restrict__ rh, FinalCombine fc) {
@@ -143,13 +143,17 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
         fyp[1] = cweno3_face<false>(w1.y, w2.y, w3.y, eps);
     }
     double2 nw4 = make_double2(0, 0), nf0 = nw4, nf1 = nw4, nf2 = nw4;
+    // the cell-local inputs of the fused modes, loaded one row ahead (f / G is
+    // read and rewritten by this lane only: plain loads, in place)
     auto fin_loads = [&](int jj, double2& a, double2& b, double2& c) {
         const int64_t o = ((int64_t)jj * p.nx + i) * nb + idx;
         a = *reinterpret_cast<const double2*>(fc.f + o);
-        b = __ldg(reinterpret_cast<const double2*>(fc.q1 + o));
-        c = __ldg(reinterpret_cast<const double2*>(fc.k1 + o));
+        if constexpr (MODE == 1) {
+            b = __ldg(reinterpret_cast<const double2*>(fc.q1 + o));
+            c = __ldg(reinterpret_cast<const double2*>(fc.k1 + o));
+        }
     };
-    if (FINAL && outlane) fin_loads(0, nf0, nf1, nf2);
+    if (MODE && outlane) fin_loads(0, nf0, nf1, nf2);
     // row activity under the optional mask (warp-uniform): a row is computed
     // when one of the strip's output cells is masked in; its y face also when
     // the next row is (the face is shared)
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
         const double2 cf = nf0, cq = nf1, ck = nf2;
         if (j + 1 < ny) {
             nw4 = ld(j + 3);  // row j+3 = w4 of row j+1
-            if (FINAL && outlane) fin_loads(j + 1, nf0, nf1, nf2);
+            if (MODE && outlane) fin_loads(j + 1, nf0, nf1, nf2);
         }
         const bool act_nn = MASK && j + 2 < ny ? row_active(j + 2) : false;
         if (MASK && !act && !act_next) {  // nothing here, and the next row does not need this row's face
@@ -201,8 +205,35 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
             double tr[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) tr[q] = -fx[q] * inv_dx - vy * (fy[q] - fyp[q]) * inv_dy;
-            if constexpr (!FINAL) {
+            if constexpr (MODE == 0) {
                 *reinterpret_cast<double2*>(out + o) = make_double2(tr[0], tr[1]);
+            } else if constexpr (MODE == 2) {  // T(Y1): f_acc and G (FinalCombine)
+                const int64_t cell = (int64_t)j * p.nx + i;
+                const double ie = fc.res ? 1.0 / fc.eps[cell] : 0.0;
+                const double fv[2] = {cf.x, cf.y}, y1[2] = {w2.x, w2.y};
+                const double cy = fc.w_im1 / fc.a_im11;
+                double fa2[2], g2[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double q1 = fc.res ? tr[q] + fc.res[o + q] * ie : tr[q];
+                    const double k1 = (y1[q] - fv[q]) * fc.k1_scale;
+                    fa2[q] = fv[q] + fc.dt * fc.a_ex10 * q1 + fc.a_im10 * k1;
+                    g2[q] = fv[q] + (fc.dt * (fc.w_ex0 * q1) + fc.w_im0 * k1) - cy * fa2[q];
+                }
+                *reinterpret_cast<double2*>(fc.fa + o) = make_double2(fa2[0], fa2[1]);
+                *reinterpret_cast<double2*>(fc.f + o) = make_double2(g2[0], g2[1]);
+            } else if constexpr (MODE == 3) {  // T(Y2): f = G + dt w_ex1 q2 + (w_im1 / a_im11) Y2
+                const int64_t cell = (int64_t)j * p.nx + i;
+                const double ie = fc.res ? 1.0 / fc.eps[cell] : 0.0;
+                const double gv[2] = {cf.x, cf.y}, y2[2] = {w2.x, w2.y};
+                const double cy = fc.w_im1 / fc.a_im11;
+                double o2[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double q2 = fc.res ? tr[q] + fc.res[o + q] * ie : tr[q];
+                    o2[q] = gv[q] + (fc.dt * (fc.w_ex1 * q2) + cy * y2[q]);
+                }
+                *reinterpret_cast<double2*>(fc.f + o) = make_double2(o2[0], o2[1]);
             } else {
                 const int64_t cell = (int64_t)j * p.nx + i;
                 const double ie = fc.res ? 1.0 / fc.eps[cell] : 0.0;
@@ -256,19 +287,31 @@ int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const d
     const dim3 grid(unsigned((p.nx + TL_OUT - 1) / TL_OUT), unsigned((nb / 2 + 3) / 4));
     const size_t smem = p.row_act ? size_t(p.ny) : 0;
     if (smem > 48 * 1024) return fail(ctx, HK_UNSUPPORTED, "transport: row activity needs ny <= 49152");
-    if (fin)
-        transport_lanes_kernel<true, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+    if (fin && fin->mode == 2)
+        transport_lanes_kernel<2, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+    else if (fin && fin->mode == 3)
+        transport_lanes_kernel<3, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+    else if (fin)
+        transport_lanes_kernel<1, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
     else if (p.row_act)
-        transport_lanes_kernel<false, 2, true><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+        transport_lanes_kernel<0, 2, true><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
     else
-        transport_lanes_kernel<false, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+        transport_lanes_kernel<0, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "transport kernel");
 }
 
 bool transport_final_supported(const TransportParams& p) {
     const int64_t nb = (int64_t)p.n * p.n * p.n;
-    return (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3 && p.x_halo == 0;
+    return (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3 && (p.x_halo == 0 || p.x_halo == -2);
+}
+
+int transport_fused_launch(hk_ctx ctx, const TransportParams& p, const double* y, const FinalCombine& fc,
+                           const double* lh, const double* rh) {
+    if (!transport_final_supported(p)) return fail(ctx, HK_UNSUPPORTED, "fused transport: lane sweep shapes only");
+    int lg = 0;
+    while ((1 << lg) < p.n) ++lg;
+    return transport_march_launch(ctx, p, lg, y, nullptr, lh, rh, &fc);
 }
 
 int transport_final_launch(hk_ctx ctx, const TransportParams& p, const double* y2, const FinalCombine& fc) {
