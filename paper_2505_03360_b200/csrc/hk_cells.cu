@@ -587,24 +587,12 @@ __global__ void __launch_bounds__(NT) residual_finish_kernel(const double* __res
 }
 
 // ===========================================================================
-// Warp-per-cell variants (n a power of two, 4 <= n <= 64): one warp streams a
-// cell's block as double2 pairs with independent loads in flight, reduces
-// with shuffles only (no CTA barriers), and lane 0 does the scalar solves
-// while the other warps of the SM keep streaming.  These are the production
-// kernels for the 16^3 / 32^3 grids; the CTA-per-cell kernels above remain
-// for other n.
+// Streaming CTA-per-cell kernels (n a power of two, 8 <= n <= 64; the
+// production path): 256 threads stream a cell's block as double2 pairs with
+// many loads in flight, two CTAs per SM; the kernels above (thread-per-cell
+// loops) serve every other n.  (Warp-per-cell variants were measured slower
+// at n >= 8 and removed; they spilled.)
 // ===========================================================================
-constexpr int WPB = 8;  // warps (cells in flight) per block
-#ifndef HK_CELL_UNROLL
-#define HK_CELL_UNROLL 4
-#endif
-#ifndef HK_MOM_MINB
-#define HK_MOM_MINB 4
-#endif
-#ifndef HK_STAGE_MINB
-#define HK_STAGE_MINB 3
-#endif
-constexpr int kCellUnroll = HK_CELL_UNROLL;
 
 template <int K>
 __device__ __forceinline__ void warp_sum(double (&v)[K]) {
@@ -612,20 +600,6 @@ __device__ __forceinline__ void warp_sum(double (&v)[K]) {
     for (int k = 0; k < K; ++k)
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-}
-
-__device__ __forceinline__ double bcast(double v) { return __shfl_sync(0xffffffffu, v, 0); }
-
-// Calls fn(idx, k1, k2, k3) for element pairs (idx, idx + 1), k3 even.
-template <typename FN>
-__device__ __forceinline__ void for_pairs(int n, int lg, FN fn) {
-    const int npairs = (n * n * n) >> 1;
-    const int lane = threadIdx.x & 31;
-#pragma unroll kCellUnroll
-    for (int p = lane; p < npairs; p += 32) {
-        const int idx = 2 * p;
-        fn(idx, idx >> (2 * lg), (idx >> lg) & (n - 1), idx & (n - 1));
-    }
 }
 
 __device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
@@ -665,71 +639,10 @@ __device__ __forceinline__ void st2_hint(double* ptr, double2 v, uint64_t pol) {
 #endif
 }
 
-__device__ void raw_sums_w(const double* __restrict__ f, const VGrid& g, int lg, double (&s)[11]) {
-#pragma unroll
-    for (int k = 0; k < 11; ++k) s[k] = 0.0;
-    for_pairs(g.n, lg, [&](int idx, int k1, int k2, int k3) {
-        const double vx = g.node(k1), vy = g.node(k2), vz0 = g.node(k3), vz1 = g.node(k3 + 1);
-        const double2 w = ldg2(f + idx);
-        const double c0 = w.x + w.y, cz = vz0 * w.x + vz1 * w.y, c2 = vz0 * vz0 * w.x + vz1 * vz1 * w.y;
-        s[0] += c0;
-        s[1] += vx * c0;
-        s[2] += vy * c0;
-        s[3] += cz;
-        s[4] += (vx * vx + vy * vy) * c0 + c2;
-        s[5] += vx * vx * c0;
-        s[6] += vx * vy * c0;
-        s[7] += vx * cz;
-        s[8] += vy * vy * c0;
-        s[9] += vy * cz;
-        s[10] += c2;
-    });
-    warp_sum<11>(s);
-}
-
-// Per-warp separable Maxwellian factors (src/moments.cpp:93-102).
-__device__ double maxwell_factors_w(const Mom& m, const VGrid& g, double* ex, double* ey, double* ez) {
-    const int lane = threadIdx.x & 31;
-    const double inv2T = 0.5 / m.T;
-    for (int k = lane; k < g.n; k += 32) {
-        const double v = g.node(k);
-        ex[k] = exp(-(v - m.ux) * (v - m.ux) * inv2T);
-        ey[k] = exp(-(v - m.uy) * (v - m.uy) * inv2T);
-        ez[k] = exp(-(v - m.uz) * (v - m.uz) * inv2T);
-    }
-    __syncwarp();
-    return m.rho / pow(2.0 * M_PI * m.T, 1.5);
-}
-
 // Coupling matrix from the 14 weighted monomial moments of w (degree <= 4)
 // instead of 25 direct products: A = sum phi psi^T w with psi affine in
 // (1, v, |v|^2) (src/moments.cpp:164-189 evaluates the same sums directly).
 __device__ void coupling_from_monomials(const double (&M)[14], const double uc[3], double dvk, double (&A)[25]);
-
-template <typename WF>
-__device__ void coupling_w(const VGrid& g, int lg, const double uc[3], WF wfun, double (&A)[25]) {
-    double M[14];  // M0, M1[3], M2[xx xy xz yy yz zz], M3[3] (= sum v^2 v_i w), M4
-#pragma unroll
-    for (int i = 0; i < 14; ++i) M[i] = 0.0;
-    for_pairs(g.n, lg, [&](int idx, int k1, int k2, int k3) {
-        const double vx = g.node(k1), vy = g.node(k2);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const double vz = g.node(k3 + q);
-            const double w = wfun(idx + q, k1, k2, k3 + q, vx, vy, vz);
-            const double v2 = vx * vx + vy * vy + vz * vz;
-            const double wx = vx * w, wy = vy * w, wz = vz * w;
-            M[0] += w;
-            M[1] += wx; M[2] += wy; M[3] += wz;
-            M[4] += vx * wx; M[5] += vy * wx; M[6] += vz * wx;
-            M[7] += vy * wy; M[8] += vz * wy; M[9] += vz * wz;
-            M[10] += v2 * wx; M[11] += v2 * wy; M[12] += v2 * wz;
-            M[13] += v2 * v2 * w;
-        }
-    });
-    warp_sum<14>(M);
-    coupling_from_monomials(M, uc, g.dvk, A);
-}
 
 // A_rc = sum phi_r psi_c w dvK from the 14 weighted monomial moments of w.
 __device__ void coupling_from_monomials(const double (&M)[14], const double uc[3], double dvk, double (&A)[25]) {
@@ -758,298 +671,8 @@ __device__ void coupling_from_monomials(const double (&M)[14], const double uc[3
     for (int i = 0; i < 25; ++i) A[i] *= dvk;
 }
 
-__global__ void __launch_bounds__(32 * WPB, HK_MOM_MINB) moments_warp_kernel(const double* __restrict__ f, int64_t ncells, VGrid g,
-                                                              int lg, double* __restrict__ mom,
-                                                              double* __restrict__ sigma, double* __restrict__ real,
-                                                              double* __restrict__ l1, int* __restrict__ status,
-                                                              const int64_t* __restrict__ src_idx,
-                                                              const int* __restrict__ count_dev) {
-    __shared__ double tab[WPB][3][64];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* ex = tab[wid][0];
-    double* ey = tab[wid][1];
-    double* ez = tab[wid][2];
-    if (count_dev) ncells = min(ncells, (int64_t)*count_dev);
-    for (int64_t cell = (int64_t)blockIdx.x * WPB + wid; cell < ncells; cell += (int64_t)gridDim.x * WPB) {
-        const double* fc = f + (src_idx ? src_idx[cell] : cell) * g.n * g.n * g.n;
-        double s[11];
-        raw_sums_w(fc, g, lg, s);
-        Mom m;
-        const int st = moments_from_sums(s, g, m);
-        if (lane == 0) {
-            if (mom) {
-                double* o = mom + cell * 5;
-                o[0] = m.rho; o[1] = m.ux; o[2] = m.uy; o[3] = m.uz; o[4] = m.T;
-            }
-            if (sigma)
-                for (int k = 0; k < 6; ++k) sigma[cell * 6 + k] = s[5 + k] * g.dvk;
-            if (status) status[cell] = st;
-        }
-        if (st != HK_OK || (!real && !l1)) continue;
-        const double pref = l1 ? maxwell_factors_w(m, g, ex, ey, ez) : 0.0;
-        const double ist = 1.0 / sqrt(m.T);
-        double r[11];
-#pragma unroll
-        for (int k = 0; k < 11; ++k) r[k] = 0.0;
-        for_pairs(g.n, lg, [&](int idx, int k1, int k2, int k3) {
-            const double Vx = (g.node(k1) - m.ux) * ist, Vy = (g.node(k2) - m.uy) * ist;
-            const double2 w2 = ldg2(fc + idx);
-            const double pxy = l1 ? pref * ex[k1] * ey[k2] : 0.0;
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const double w = q ? w2.y : w2.x;
-                const double Vz = (g.node(k3 + q) - m.uz) * ist;
-                const double V2 = Vx * Vx + Vy * Vy + Vz * Vz;
-                r[0] += Vx * Vx * w;
-                r[1] += Vx * Vy * w;
-                r[2] += Vx * Vz * w;
-                r[3] += Vy * Vy * w;
-                r[4] += Vy * Vz * w;
-                r[5] += Vz * Vz * w;
-                const double bw = 0.5 * (V2 - 5.0) * w;
-                r[6] += bw * Vx;
-                r[7] += bw * Vy;
-                r[8] += bw * Vz;
-                const double e = 0.5 * V2 - 2.5;
-                r[9] += e * e * w;
-                if (l1) r[10] += fabs(w - pxy * ez[k3 + q]);
-            }
-        });
-        warp_sum<11>(r);
-        if (lane == 0) {
-            if (real) {
-                const double sc = g.dvk / m.rho;
-                double s2[6];
-                for (int k = 0; k < 6; ++k) s2[k] = r[k] * sc;
-                const double tr3 = (s2[0] + s2[3] + s2[5]) / 3.0;
-                double* o = real + cell * 13;
-                o[0] = s2[0] - tr3; o[1] = s2[1]; o[2] = s2[2];
-                o[3] = s2[1]; o[4] = s2[3] - tr3; o[5] = s2[4];
-                o[6] = s2[2]; o[7] = s2[4]; o[8] = s2[5] - tr3;
-                o[9] = r[6] * sc; o[10] = r[7] * sc; o[11] = r[8] * sc;
-                o[12] = 0.4 * r[9] * sc;
-            }
-            if (l1) l1[cell] = r[10] * g.dvk;
-        }
-        __syncwarp();
-    }
-}
 
-template <bool ESBGK>
-__global__ void __launch_bounds__(32 * WPB, HK_STAGE_MINB) stage_warp_kernel(const double* __restrict__ fin, double* __restrict__ out,
-                                                            int64_t ncells, VGrid g, int lg, double a,
-                                                            const double* __restrict__ eps_cell, double eps_scalar,
-                                                            double beta, double coeff, int* __restrict__ info,
-                                                            double* __restrict__ mom_out) {
-    __shared__ double tab[WPB][3][64];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* ex = tab[wid][0];
-    double* ey = tab[wid][1];
-    double* ez = tab[wid][2];
-    const int n = g.n, nb = n * n * n;
-    for (int64_t cell = (int64_t)blockIdx.x * WPB + wid; cell < ncells; cell += (int64_t)gridDim.x * WPB) {
-        const double* fc = fin + cell * nb;
-        double* oc = out + cell * nb;
-        const double eps = eps_cell ? eps_cell[cell] : eps_scalar;
-        double s[11];
-        raw_sums_w(fc, g, lg, s);
-        Mom m;
-        int st = moments_from_sums(s, g, m);
-        if (lane == 0 && mom_out) {
-            double* o = mom_out + cell * 5;
-            o[0] = m.rho; o[1] = m.ux; o[2] = m.uy; o[3] = m.uz; o[4] = m.T;
-        }
-        const double A = a * (coeff * m.rho);  // a nu (nu = coeff rho) | a beta_pen (beta = coeff rho)
-        if (st != HK_OK || !(A > 0.0)) {
-            if (lane == 0 && info) info[cell] = st;
-            if (st == HK_OK)
-                for_pairs(n, lg, [&](int idx, int, int, int) {
-                    *reinterpret_cast<double2*>(oc + idx) = ldg2(fc + idx);
-                });
-            continue;
-        }
-        // ES-BGK: Sigma blend, corrected tensor, LLT test, inverse (lane 0, broadcast)
-        double par[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-        int gauss = 0;
-        if (ESBGK) {
-            if (lane == 0) {
-                const double omb = 1.0 - beta;
-                const double u[3] = {m.ux, m.uy, m.uz};
-                const int map[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
-                double tc[9];
-                const double denom = eps + omb * A, oa = omb * A;
-                const double iso = (1.0 - beta) * m.T;
-                for (int i = 0; i < 3; ++i)
-                    for (int j = 0; j < 3; ++j) {
-                        const double sstar = s[5 + map[3 * i + j]] * g.dvk;
-                        const double siso = m.rho * ((i == j ? m.T : 0.0) + u[i] * u[j]);
-                        const double theta = (eps * sstar + oa * siso) / denom / m.rho - u[i] * u[j];
-                        tc[3 * i + j] = (i == j ? iso : 0.0) + beta * theta;
-                    }
-                double l[9] = {0};
-                bool ok = true;
-                for (int k = 0; k < 3 && ok; ++k) {
-                    double x = tc[3 * k + k];
-                    for (int j = 0; j < k; ++j) x -= l[3 * k + j] * l[3 * k + j];
-                    if (!(x > 0.0)) { ok = false; break; }
-                    l[3 * k + k] = sqrt(x);
-                    for (int i = k + 1; i < 3; ++i) {
-                        double y = tc[3 * i + k];
-                        for (int j = 0; j < k; ++j) y -= l[3 * i + j] * l[3 * k + j];
-                        l[3 * i + k] = y / l[3 * k + k];
-                    }
-                }
-                if (ok) {
-                    const double* q = tc;
-                    const double c00 = q[4] * q[8] - q[5] * q[7], c01 = q[5] * q[6] - q[3] * q[8], c02 = q[3] * q[7] - q[4] * q[6];
-                    const double det = q[0] * (q[4] * q[8] - q[5] * q[7]) - q[1] * (q[3] * q[8] - q[5] * q[6]) +
-                                       q[2] * (q[3] * q[7] - q[4] * q[6]);
-                    const double id = 1.0 / (q[0] * c00 + q[1] * c01 + q[2] * c02);
-                    par[0] = c00 * id; par[1] = (q[2] * q[7] - q[1] * q[8]) * id; par[2] = (q[1] * q[5] - q[2] * q[4]) * id;
-                    par[3] = (q[0] * q[8] - q[2] * q[6]) * id; par[4] = (q[2] * q[3] - q[0] * q[5]) * id;
-                    par[5] = (q[0] * q[4] - q[1] * q[3]) * id;  // inv00 inv01 inv02 inv11 inv12 inv22
-                    par[6] = m.rho / sqrt(pow(2.0 * M_PI, 3) * det);
-                    gauss = 1;
-                }
-            }
-            gauss = __shfl_sync(0xffffffffu, gauss, 0);
-#pragma unroll
-            for (int k = 0; k < 7; ++k) par[k] = bcast(par[k]);
-        }
-        const int fallback = (ESBGK && !gauss) ? 1 : 0;
-        double pref = 0.0;
-        if (!gauss) pref = maxwell_factors_w(m, g, ex, ey, ez);
-        auto eq = [&](int, int k1, int k2, int k3, double vx, double vy, double vz) -> double {
-            if (!gauss) return pref * ex[k1] * ey[k2] * ez[k3];
-            const double dx = vx - m.ux, dy = vy - m.uy, dz = vz - m.uz;
-            const double qxy = par[0] * dx * dx + 2.0 * par[1] * dx * dy + par[3] * dy * dy;
-            const double lz = 2.0 * (par[2] * dx + par[4] * dy);
-            return par[6] * exp(-0.5 * (qxy + dz * (lz + par[5] * dz)));
-        };
-        const double mom3[3] = {m.rho * m.ux, m.rho * m.uy, m.rho * m.uz};
-        const double uc[3] = {mom3[0] / m.rho, mom3[1] / m.rho, mom3[2] / m.rho};
-        double Amat[25];
-        coupling_w(g, lg, uc, eq, Amat);
-        double x[5] = {0, 0, 0, 0, 0};
-        int ok = 0;
-        if (lane == 0) {
-            const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
-            ok = solve5(Amat, rhs, x) ? 1 : 0;
-            st = ok ? HK_OK : HK_DEGENERATE;
-            if (info) info[cell] = st | (fallback << 8);
-        }
-        ok = __shfl_sync(0xffffffffu, ok, 0);
-        if (!ok) continue;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) x[k] = bcast(x[k]);
-        const double wf = eps / (eps + A), wg = A / (eps + A);
-        for_pairs(n, lg, [&](int idx, int k1, int k2, int k3) {
-            const double vx = g.node(k1), vy = g.node(k2);
-            const double2 fv = ldg2(fc + idx);
-            double2 o;
-            {
-                const double vz = g.node(k3);
-                o.x = wf * fv.x + wg * (eq(idx, k1, k2, k3, vx, vy, vz) * quad_factor(x, vx, vy, vz, uc));
-            }
-            {
-                const double vz = g.node(k3 + 1);
-                o.y = wf * fv.y + wg * (eq(idx + 1, k1, k2, k3 + 1, vx, vy, vz) * quad_factor(x, vx, vy, vz, uc));
-            }
-            *reinterpret_cast<double2*>(oc + idx) = o;
-        });
-    }
-}
 
-__global__ void __launch_bounds__(32 * WPB, HK_STAGE_MINB) residual_finish_warp_kernel(const double* __restrict__ f,
-                                                                      double* __restrict__ q, int64_t ncells, VGrid g,
-                                                                      int lg, double pen_coeff,
-                                                                      int* __restrict__ status) {
-    __shared__ double tab[WPB][3][64];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double* ex = tab[wid][0];
-    double* ey = tab[wid][1];
-    double* ez = tab[wid][2];
-    const int n = g.n, nb = n * n * n;
-    for (int64_t cell = (int64_t)blockIdx.x * WPB + wid; cell < ncells; cell += (int64_t)gridDim.x * WPB) {
-        const double* fc = f + cell * nb;
-        double* qc = q + cell * nb;
-        double s[11];
-        raw_sums_w(fc, g, lg, s);
-        Mom m;
-        const int st0 = moments_from_sums(s, g, m);
-        if (st0 != HK_OK) {
-            if (lane == 0 && status) status[cell] = st0;
-            continue;
-        }
-        const double beta = pen_coeff * m.rho;
-        const double pref = maxwell_factors_w(m, g, ex, ey, ez);
-        const double mom3[3] = {m.rho * m.ux, m.rho * m.uy, m.rho * m.uz};
-        const double uc[3] = {mom3[0] / m.rho, mom3[1] / m.rho, mom3[2] / m.rho};
-        auto maxw = [&](int, int k1, int k2, int k3, double, double, double) -> double {
-            return pref * ex[k1] * ey[k2] * ez[k3];
-        };
-        double Amat[25];
-        coupling_w(g, lg, uc, maxw, Amat);
-        double x[5] = {0, 0, 0, 0, 0};
-        int ok = 0;
-        if (lane == 0) {
-            const double rhs[5] = {m.rho, mom3[0], mom3[1], mom3[2], 2.0 * energy_of(m)};
-            ok = solve5(Amat, rhs, x) ? 1 : 0;
-        }
-        ok = __shfl_sync(0xffffffffu, ok, 0);
-        if (!ok) {
-            if (lane == 0 && status) status[cell] = HK_DEGENERATE;
-            continue;
-        }
-#pragma unroll
-        for (int k = 0; k < 5; ++k) x[k] = bcast(x[k]);
-        const double u3[3] = {m.ux, m.uy, m.uz};
-        auto mt = [&](int i, int k1, int k2, int k3, double vx, double vy, double vz) -> double {
-            return maxw(i, k1, k2, k3, vx, vy, vz) * quad_factor(x, vx, vy, vz, uc);
-        };
-        double B[25];
-        coupling_w(g, lg, u3, mt, B);
-        double inv[5] = {0, 0, 0, 0, 0};
-        for_pairs(n, lg, [&](int idx, int k1, int k2, int k3) {
-            const double vx = g.node(k1), vy = g.node(k2);
-            const double2 fv = ldg2(fc + idx);
-            double2 qv = *reinterpret_cast<const double2*>(qc + idx);
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const double vz = g.node(k3 + c);
-                const double o = (c ? qv.y : qv.x) + beta * ((c ? fv.y : fv.x) - mt(idx + c, k1, k2, k3 + c, vx, vy, vz));
-                if (c) qv.y = o; else qv.x = o;
-                inv[0] += o;
-                inv[1] += vx * o;
-                inv[2] += vy * o;
-                inv[3] += vz * o;
-                inv[4] += (vx * vx + vy * vy + vz * vz) * o;
-            }
-            *reinterpret_cast<double2*>(qc + idx) = qv;
-        });
-        warp_sum<5>(inv);
-        double y[5] = {0, 0, 0, 0, 0};
-        if (lane == 0) {
-            double rhs[5];
-            for (int k = 0; k < 5; ++k) rhs[k] = inv[k] * g.dvk;
-            ok = solve5(B, rhs, y) ? 1 : 0;
-            if (status) status[cell] = ok ? HK_OK : HK_DEGENERATE;
-        }
-        ok = __shfl_sync(0xffffffffu, ok, 0);
-        if (!ok) continue;
-#pragma unroll
-        for (int k = 0; k < 5; ++k) y[k] = bcast(y[k]);
-        __syncwarp();
-        for_pairs(n, lg, [&](int idx, int k1, int k2, int k3) {
-            const double vx = g.node(k1), vy = g.node(k2);
-            double2 qv = *reinterpret_cast<const double2*>(qc + idx);
-            const double vz0 = g.node(k3), vz1 = g.node(k3 + 1);
-            qv.x -= quad_factor(y, vx, vy, vz0, u3) * mt(idx, k1, k2, k3, vx, vy, vz0);
-            qv.y -= quad_factor(y, vx, vy, vz1, u3) * mt(idx + 1, k1, k2, k3 + 1, vx, vy, vz1);
-            *reinterpret_cast<double2*>(qc + idx) = qv;
-        });
-    }
-}
 
 // ---------------------------------------------------------------------------
 // moments + second moment + realizability + L1, one 512-thread CTA per cell,
@@ -1892,13 +1515,18 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 __syncthreads();
             }
             // ---- pass 3: out = wf f + wg G (x0 + x.c + x4 |c|^2) ----
+            // Groups in reverse: the planes pass 1 loaded last are re-read first,
+            // while they are most likely still in L2 (config 3: 9.91 -> 9.76 ms;
+            // keeping the first 11 planes in shared memory instead cost 0.5 ms).
 #pragma unroll kStageU3
-            for (int q = t; q < ngroups; q += MT) {
+            for (int qb = ((ngroups - 1) / MT) * MT; qb >= 0; qb -= MT) {
+                const int q = qb + t;
+                if (q >= ngroups) continue;
                 const int idx = 4 * q;
                 const int k1 = idx >> (2 * lg), k2 = (idx >> lg) & (n - 1), k3 = idx & (n - 1);
                 const double vx = g.node(k1), vy = g.node(k2);
                 double2 fa, fb;
-                if constexpr (ACC) {  // f_acc parked in out by pass 1 (written by other threads: the solve barrier orders it)
+                if constexpr (ACC) {  // f_acc parked in out by pass 1 (other threads: the solve barrier orders it)
                     fa = *reinterpret_cast<const double2*>(oc + idx);
                     fb = *reinterpret_cast<const double2*>(oc + idx + 2);
                 } else {
@@ -1961,15 +1589,11 @@ __global__ void k1_kernel(int64_t count, double* __restrict__ k1, const double* 
         k1[i] = (y[i] - f[i]) * scale;
 }
 
-bool warp_path(int n) { return n >= 4 && n <= 64 && (n & (n - 1)) == 0; }
+bool warp_path(int n) { return n >= 8 && n <= 64 && (n & (n - 1)) == 0; }
 int log2i(int n) {
     int l = 0;
     while ((1 << l) < n) ++l;
     return l;
-}
-int warp_grid(hk_ctx ctx, int64_t ncells) {
-    const int64_t blocks = (ncells + WPB - 1) / WPB, cap = int64_t(ctx->sm_count) * 8;
-    return int(blocks < cap ? blocks : cap);
 }
 
 // ---------------------------------------------------------------------------
@@ -2139,15 +1763,12 @@ int moments_launch(hk_ctx ctx, int n, double vmax, const double* f, int64_t ncel
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "moments: 2 <= n <= 128");
     // 256-thread CTAs, 2 per SM, 16 loads in flight per thread (config 3: 3.99 ms;
     // measured and removed: 512 x 1 x 16, 256 x 4 x 8 4.72 ms, 128 x 6 x 8, 512 x 2 x 8, 256 x 3 x 8)
-    if (warp_path(n) && n >= 8) {
+    if (warp_path(n)) {
         const int64_t cap = int64_t(ctx->sm_count) * 2;
         const int grid = int(ncells < cap ? ncells : cap);
         moments_cta_kernel<256, 2, 16><<<grid, 256, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), log2i(n), mom, sigma,
                                                                       real, l1, status, src_idx, count_dev);
-    } else if (warp_path(n))
-        moments_warp_kernel<<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), log2i(n),
-                                                                                  mom, sigma, real, l1, status, src_idx, count_dev);
-    else
+    } else
         moments_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(f, ncells, make_vgrid(n, vmax), mom, sigma, real,
                                                                       l1, status, src_idx, count_dev);
     ctx->launches++;
@@ -2164,7 +1785,9 @@ int maxwellian_launch(hk_ctx ctx, int n, double vmax, const double* mom, int64_t
     return check_cuda(ctx, cudaGetLastError(), "maxwellian kernel");
 }
 
-bool stage_acc_supported(int n) { return warp_path(n) && n >= 8; }
+size_t stage_smem(int n) { return sizeof(double) * (2 * n * n + n + 8 * 16 + 32 + 2 * n + 6 * n + 2 * n); }
+
+bool stage_acc_supported(int n) { return warp_path(n); }
 
 int stage_acc_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* f, const double* q1, const double* k1,
                      double cq, double ck, double* out, int64_t ncells, double a, const double* eps_cell, double beta,
@@ -2174,7 +1797,7 @@ int stage_acc_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* f
     const VGrid g = make_vgrid(n, vmax);
     const int64_t cap = int64_t(ctx->sm_count) * 2;
     const int grid = int(ncells < cap ? ncells : cap);
-    const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32 + 2 * n + 6 * n + 2 * n);
+    const size_t smem = stage_smem(n);
     auto kern = esbgk ? stage_cta_kernel<true, 256, 2, true> : stage_cta_kernel<false, 256, 2, true>;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, 256, smem, ctx->stream>>>(f, out, ncells, g, log2i(n), a, eps_cell, 0.0, beta, coeff, info, nullptr,
@@ -2189,12 +1812,12 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
     if (ncells <= 0) return HK_OK;
     if (n < 2 || n > 128) return fail(ctx, HK_UNSUPPORTED, "stage: 2 <= n <= 128");
     const VGrid g = make_vgrid(n, vmax);
-    if (warp_path(n) && n >= 8) {
+    if (warp_path(n)) {
         // 256-thread CTAs, 2 per SM (config 3, L2 hints, register solve5: 9.9 ms; measured and
         // removed: 3 per SM 10.9, 128-thread CTAs 5 / 6 per SM 10.2 / 10.4)
         const int64_t cap = int64_t(ctx->sm_count) * 2;
         const int grid = int(ncells < cap ? ncells : cap);
-        const size_t smem = sizeof(double) * (2 * n * n + n + 8 * 16 + 32 + 2 * n + 6 * n + 2 * n);
+        const size_t smem = stage_smem(n);
         auto kern = esbgk ? stage_cta_kernel<true, 256, 2> : stage_cta_kernel<false, 256, 2>;
         const int mt = 256;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2214,13 +1837,6 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
 #endif
         ctx->launches++;
         return check_cuda(ctx, cudaGetLastError(), "stage kernel");
-    } else if (warp_path(n)) {
-        if (esbgk)
-            stage_warp_kernel<true><<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(
-                fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info, mom_out);
-        else
-            stage_warp_kernel<false><<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(
-                fin, out, ncells, g, log2i(n), a, eps_cell, eps_scalar, beta, coeff, info, mom_out);
     } else if (esbgk)
         stage_kernel<true><<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(fin, out, ncells, g, a, eps_cell, eps_scalar,
                                                                           beta, coeff, info, mom_out);
@@ -2242,19 +1858,13 @@ int stage_launch(hk_ctx ctx, bool esbgk, int n, double vmax, const double* fin, 
 int residual_finish_launch(hk_ctx ctx, int n, double vmax, const double* f, double* q, int64_t ncells, double pen_coeff,
                            int* status) {
     if (ncells <= 0) return HK_OK;
-#ifndef HK_RES_WARP
-#define HK_RES_WARP 0
-#endif
-    if (!HK_RES_WARP && warp_path(n) && n >= 8) {
+    if (warp_path(n)) {
         // one CTA per cell, two streaming passes (the coupling matrices from 1-D sums)
         const int64_t cap = int64_t(ctx->sm_count) * HK_RES_MINB;
         const int grid = int(ncells < cap ? ncells : cap);
         residual_cta_kernel<HK_RES_MT, HK_RES_MINB><<<grid, HK_RES_MT, 0, ctx->stream>>>(f, q, ncells, make_vgrid(n, vmax),
                                                                                       log2i(n), pen_coeff, status);
-    } else if (warp_path(n))
-        residual_finish_warp_kernel<<<warp_grid(ctx, ncells), 32 * WPB, 0, ctx->stream>>>(
-            f, q, ncells, make_vgrid(n, vmax), log2i(n), pen_coeff, status);
-    else
+    } else
         residual_finish_kernel<<<grid_for(ctx, ncells), NT, 0, ctx->stream>>>(f, q, ncells, make_vgrid(n, vmax),
                                                                               pen_coeff, status);
     ctx->launches++;

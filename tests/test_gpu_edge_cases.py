@@ -108,3 +108,25 @@ def test_tiny_periodic_grids_transport(hk, oracle):
         # nx = ny = 1 is a uniform field: the exact right-hand side is 0
         scale = max(np.abs(ref).max(), np.abs(fh).max() / 0.1)
         assert np.abs(got - ref).max() <= 1e-13 * scale, (nx, ny)
+
+
+@pytest.mark.parametrize("n", [4, 6])
+def test_small_grids_take_the_generic_cell_kernels(hk, oracle, n):
+    """n < 8 (and any n not a power of two) runs the thread-per-cell kernels:
+    moments, the ES-BGK and penalized stages against the oracle."""
+    import torch
+    from paper_2505_03360_b200 import kinetic
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    fh = inputs.config3_cells(3, 2, n)[0]
+    f = torch.from_numpy(fh).cuda()
+    out = kinetic.moments_of(f, vg)
+    for c in range(fh.shape[0]):
+        np.testing.assert_allclose(out["moments"].cpu().numpy()[c], oracle.moments(n, inputs.VMAX, fh[c])[1],
+                                   rtol=1e-12, atol=1e-14)  # u_z ~ 1e-18 is a rounding zero
+    es, _ = kinetic.esbgk_stage_solve(f, 1e-2, 1e-2, kinetic.EsbgkParams(), vg)
+    pen, _ = kinetic.penalized_stage_solve(f, 1e-2, 1e-2, kinetic.PenalizationRule(), vg)
+    for c in range(fh.shape[0]):
+        ref_es = oracle.esbgk_stage_solve(n, inputs.VMAX, fh[c], 1e-2, 1e-2)[0]
+        ref_pen = oracle.penalized_stage_solve(n, inputs.VMAX, fh[c], 1e-2, 1e-2)[0]
+        assert rel_l2(es.cpu().numpy()[c], ref_es) < 1e-12
+        assert rel_l2(pen.cpu().numpy()[c], ref_pen) < 1e-12
