@@ -28,23 +28,6 @@ __device__ __forceinline__ double rcp_nr(double x) {
     return fma(r, e, r);
 }
 
-__device__ __forceinline__ void cweno3_faces(double um, double uc, double up, double eps, double& left, double& right) {
-    const double sl = uc - um, sr = up - uc;
-    const double b = 0.5 * (up - um);
-    const double c = up - 2.0 * uc + um;
-    const double dl = (eps + sl * sl), dr = (eps + sr * sr), dc = (eps + ((13.0 / 3.0) * c * c + b * b));
-    const double l2 = dl * dl, r2 = dr * dr, c2 = dc * dc;
-    const double pl = 0.25 * (c2 * r2), pc = 0.5 * (l2 * r2), pr = 0.25 * (l2 * c2);
-    const double inv = rcp_nr(pl + pc + pr);
-    const double al = pl * inv, ac = pc * inv, ar = pr * inv;
-    const double pc_a = uc - c * (1.0 / 12.0);
-    const double c0 = al * uc + ar * uc + ac * pc_a;
-    const double c1 = al * sl + ar * sr + ac * b;
-    const double cc = ac * c;
-    left = c0 - 0.5 * c1 + 0.25 * cc;
-    right = c0 + 0.5 * c1 + 0.25 * cc;
-}
-
 // One face only (the upwind one), the same CWENO3 value in fewer operations:
 // with the weights summing to one, c0 = uc - a_c c / 12, so
 //   right = uc + (1/S) [ (p_l s_l + p_r s_r) / 2 + p_c (b / 2 + c / 6) ]
@@ -284,6 +267,7 @@ int transport_row_activity(hk_ctx ctx, int nx, int ny, const int8_t* mask, uint8
 int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const double* f, double* out, const double* lh,
                            const double* rh, const FinalCombine* fin) {
     const int64_t nb = (int64_t)p.n * p.n * p.n;
+    // 4 warps per CTA (measured: 2 or 8 warps per CTA, or loads two rows ahead, are slower)
     const dim3 grid(unsigned((p.nx + TL_OUT - 1) / TL_OUT), unsigned((nb / 2 + 3) / 4));
     const size_t smem = p.row_act ? size_t(p.ny) : 0;
     if (smem > 48 * 1024) return fail(ctx, HK_UNSUPPORTED, "transport: row activity needs ny <= 49152");
