@@ -100,11 +100,24 @@ def config3(iters, nx=256, ny=256):
         kinetic.esbgk_imex_step(f, nx, ny, vg, 1.0 / nx, 1.0 / ny, 1e-3, eps)
 
     t_s = timed(step, max(1, iters // 2))
+    # per-part times of the step (hk_ctx_set_timing tags 10..13, CUDA events on the context stream)
+    import ctypes as _C
+    ctx = hk.default_context()
+    ctx._lib.hk_ctx_set_timing(ctx.h, 1)
+    step()
+    torch.cuda.synchronize()
+    parts = {}
+    for tag, name in ((10, "stage1"), (11, "transport_Y1_to_facc_G"), (12, "stage2"), (13, "transport_Y2_final")):
+        ms_, nl = _C.c_double(), _C.c_int64()
+        ctx._lib.hk_ctx_timing_report(ctx.h, tag, _C.byref(ms_), _C.byref(nl))
+        parts[name] = ms_.value / max(1, nl.value)
+    ctx._lib.hk_ctx_set_timing(ctx.h, 0)
     b_read = cells * n ** 3 * 8
     layers = [int((res["c"][0] == k).sum()) for k in range(3)]
     out = {"config": "config3: 256x256 cells, 32^3, classify + ES-BGK stage (a=dt=1e-3, eps=1e-2, Pr=2/3)",
            "ms": {"moments_realizability_l1": t_m, "classify": t_c, "esbgk_stage": t_e, "transport_rhs": t_t,
                   "esbgk_imex_step": t_s},
+           "esbgk_step_parts_ms": parts,
            "ms_per_step": t_m + t_c + t_e, "cell_steps_per_s": cells / ((t_m + t_c + t_e) * 1e-3),
            "layers_after_classify": layers,
            "roofline": {"bound": "hbm", "peak_gbs": HBM,

@@ -25,3 +25,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:resi
   python tools/time_residual.py --cells 2048 > $O/ncu_resid_$TAG.log 2>&1; echo "ncu residual rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:coll16 -c 1 -o $O/coll16_$TAG -f \
   python tools/bench_configs.py --configs 1 --iters 1 > $O/ncu16_$TAG.log 2>&1; echo "ncu N=16 rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:stage_cta -s 2 -c 1 -o $O/stage_$TAG -f \
+  python tools/esbgk_step.py stage > $O/ncu_stage_$TAG.log 2>&1; echo "ncu stage rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:transport_lanes -s 6 -c 2 -o $O/transport_$TAG -f \
+  python tools/esbgk_step.py step > $O/ncu_transport_$TAG.log 2>&1; echo "ncu transport rc=$?"
