@@ -24,8 +24,15 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
 rows = list(csv.reader(src.splitlines()))
 if len(rows) > 2:
     h = rows[1]
-    data = [dict(zip(h, x)) for x in rows[2:] if len(x) == len(h)]
     key = "Warp Stall Sampling (All Samples)"
+
+    def num(x):
+        try:
+            return float(x or 0)
+        except ValueError:  # a repeated header row (multi-kernel report)
+            return None
+    data = [dict(zip(h, x)) for x in rows[2:] if len(x) == len(h)]
+    data = [d for d in data if num(d.get(key)) is not None]
     tot = sum(float(d[key] or 0) for d in data) or 1
     g = defaultdict(float)
     for d in data:
