@@ -154,6 +154,21 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
         }
         const bool act_nn = MASK && j + 2 < ny ? row_active(j + 2) : false;
         if (MASK && !act && !act_next) {  // nothing here, and the next row does not need this row's face
+            if (!act_nn) {
+                // a run of inactive rows: jump to L = (next active row) - 1, whose face
+                // is the first one needed, instead of streaming the rows between
+                int r = j + 3;
+                while (r < ny && !row_active(r)) ++r;
+                if (r >= ny) break;  // no active row left in this strip
+                const int L = r - 1;
+                if (L > j + 2) {  // otherwise the plain march gets there as cheaply
+                    w1 = ld(L - 2); w2 = ld(L - 1); w3 = ld(L); w4 = ld(L + 1); nw4 = ld(L + 2);
+                    j = L - 1;
+                    act = false;
+                    act_next = true;
+                    continue;
+                }
+            }
             act = act_next;
             act_next = act_nn;
             continue;
