@@ -329,6 +329,8 @@ __device__ __forceinline__ void signal_add_relaxed(unsigned* p) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_group0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 // RAW signal ("my stores are visible"): release at GPU scope.
 __device__ __forceinline__ void signal_add(unsigned* p) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(p) : "memory");

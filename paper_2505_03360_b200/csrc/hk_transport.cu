@@ -60,11 +60,20 @@ __device__ __forceinline__ double cweno3_face(double um, double uc, double up, d
 // 3); lanes 0, 1, 30, 31 are halo columns (no output).
 constexpr int TL_OUT = 28;
 
-template <int MODE, int NPT, bool MASK = false>
+// STAGED: the rows the march needs next (the y-field's row j+3 and the
+// fused modes' cell-local row j+1) arrive through a ring of shared-memory
+// slots filled RING_ROWS - 1 rows ahead with cp.async (L2 -> SMEM, no
+// registers held, L1 bypassed), four threads per cell so a warp's copy spans
+// 8 cells x 64 B instead of 32 cells x 16 B.  One CTA barrier per row.
+constexpr int RING_ROWS = 8, RING_CS = 10;  // slots (a power of two); doubles per cell row (8 + pad: conflict-free 16 B reads)
+template <int MODE, int NPT, bool MASK = false, bool STAGED = false>
 __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p, int lg, const double* __restrict__ f,
                                                               double* __restrict__ out, const double* __restrict__ lh,
                                                               const double* __restrict__ rh, FinalCombine fc) {
     static_assert(NPT == 2, "double2 node pairs");
+    static_assert(!(STAGED && (MASK || MODE == 1)), "staged: unmasked, one cell-local input");
+    __shared__ __align__(16) double ringS[STAGED ? RING_ROWS * 32 * RING_CS : 2];
+    __shared__ __align__(16) double ringF[STAGED && MODE ? RING_ROWS * 32 * RING_CS : 2];
     extern __shared__ uint8_t act_s[];  // this strip's row activity (MASK: p.row_act)
     if (MASK) {
         for (int t = threadIdx.x; t < p.ny; t += blockDim.x) act_s[t] = p.row_act[(int64_t)blockIdx.x * p.ny + t];
@@ -85,11 +94,8 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
     const int xh = p.x_halo > 0 ? p.x_halo : 0;
     const int nxi = p.nx + 2 * xh;
     const int ny = p.ny;
-    // this lane's column source: interior (periodic wrap), halo buffer, or ghost column
-    const double* colbase;
-    int64_t rowstride;
-    {
-        int ii = i;
+    // a column's source: interior (periodic wrap), halo buffer, or ghost column
+    auto col_src = [&](int ii, const double*& colbase, int64_t& rowstride) {
         if (p.x_halo < 0) {
             ii = ii < -2 ? -2 : (ii > p.nx + 1 ? p.nx + 1 : ii);  // lanes past the halo are never used
             if (ii < 0) { colbase = lh + (int64_t)(p.lnx + ii) * nb; rowstride = (int64_t)p.lnx * nb; }
@@ -104,12 +110,55 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
             colbase = f + (int64_t)(ii + xh) * nb;
             rowstride = (int64_t)nxi * nb;
         }
-        colbase += idx;
-    }
+    };
+    const double* colbase;
+    int64_t rowstride;
+    col_src(i, colbase, rowstride);
+    colbase += idx;
     auto ld = [&](int jj) -> double2 {
         jj = jj < 0 ? jj + ny : (jj >= ny ? jj - ny : jj);
         return __ldg(reinterpret_cast<const double2*>(colbase + (int64_t)jj * rowstride));
     };
+    // STAGED loader role: thread t copies 16 B (nodes idx0 + 2 h, h = t & 3) of cell lc = t >> 2
+    const int lc = threadIdx.x >> 2, lh4 = threadIdx.x & 3;
+    const int64_t idx0 = (int64_t)blockIdx.y * 8;
+    const double* lbase = nullptr;
+    int64_t lrs = 0;
+    const int li = blockIdx.x * TL_OUT - 2 + lc;
+    const bool lfin = STAGED && MODE && lc >= 2 && lc < 2 + TL_OUT && li < p.nx;
+    // loader cursors (advanced one row per issue): y row it + 3 (periodic), cell-local row it + 1
+    const double *lsrc = nullptr, *lwrap = nullptr, *fsrc = nullptr;
+    int64_t fstride = 0;
+    int jnext = 3 % (ny > 0 ? ny : 1);
+    if constexpr (STAGED) {
+        col_src(li, lbase, lrs);
+        lbase += idx0 + 2 * lh4;
+        lsrc = lbase + (int64_t)jnext * lrs;
+        lwrap = lbase;
+        if (MODE) {
+            fstride = (int64_t)p.nx * nb;
+            fsrc = fc.f + ((int64_t)p.nx + li) * nb + idx0 + 2 * lh4;
+        }
+    }
+    const uint32_t lsm = smem_u32(&ringS[lc * RING_CS + 2 * lh4]), lsmf = smem_u32(&ringF[lc * RING_CS + 2 * lh4]);
+    constexpr uint32_t SLOT_B = 32 * RING_CS * sizeof(double);
+    auto issue = [&](int it) {  // ring slot it % RING_ROWS <- y row it + 3 and cell-local row it + 1
+        if (it < ny) {
+            const uint32_t so = (it & (RING_ROWS - 1)) * SLOT_B;
+            cp_async16(lsm + so, lsrc);
+            if (++jnext == ny) {
+                jnext = 0;
+                lsrc = lwrap;
+            } else {
+                lsrc += lrs;
+            }
+            if (lfin && it + 1 < ny) cp_async16(lsmf + so, fsrc);
+            fsrc += fstride;
+        }
+        cp_async_commit();
+    };
+    if constexpr (STAGED)
+        for (int it = 0; it < RING_ROWS - 1; ++it) issue(it);
     auto sh_up = [&](double v, int d) { return __shfl_up_sync(0xffffffffu, v, d); };
     auto sh_dn = [&](double v, int d) { return __shfl_down_sync(0xffffffffu, v, d); };
     double2 w0 = ld(-2), w1 = ld(-1), w2 = ld(0), w3 = ld(1), w4 = ld(2);
@@ -148,7 +197,16 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
             w4 = nw4;
         }
         const double2 cf = nf0, cq = nf1, ck = nf2;
-        if (j + 1 < ny) {
+        if constexpr (STAGED) {
+            cp_async_wait_group<RING_ROWS - 2>();  // this thread's copies of slot j landed
+            __syncthreads();                       // everyone's; and everyone is done with slot j - 1
+            issue(j + RING_ROWS - 1);              // into slot j - 1
+            if (j + 1 < ny) {
+                const int so = (j & (RING_ROWS - 1)) * 32 * RING_CS + lane * RING_CS + 2 * w;
+                nw4 = *reinterpret_cast<const double2*>(&ringS[so]);
+                if (MODE && outlane) nf0 = *reinterpret_cast<const double2*>(&ringF[so]);
+            }
+        } else if (j + 1 < ny) {
             nw4 = ld(j + 3);  // row j+3 = w4 of row j+1
             if (MODE && outlane) fin_loads(j + 1, nf0, nf1, nf2);
         }
@@ -286,16 +344,24 @@ int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const d
     const dim3 grid(unsigned((p.nx + TL_OUT - 1) / TL_OUT), unsigned((nb / 2 + 3) / 4));
     const size_t smem = p.row_act ? size_t(p.ny) : 0;
     if (smem > 48 * 1024) return fail(ctx, HK_UNSUPPORTED, "transport: row activity needs ny <= 49152");
-    if (fin && fin->mode == 2)
-        transport_lanes_kernel<2, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
-    else if (fin && fin->mode == 3)
-        transport_lanes_kernel<3, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
-    else if (fin)
+#ifndef HK_TR_STAGED
+#define HK_TR_STAGED 1
+#endif
+    const bool staged = HK_TR_STAGED && nb % 8 == 0;  // grid.y * 8 == nb: every warp marches (CTA barriers)
+    if (fin && fin->mode == 2) {
+        if (staged) transport_lanes_kernel<2, 2, false, true><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+        else transport_lanes_kernel<2, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+    } else if (fin && fin->mode == 3) {
+        if (staged) transport_lanes_kernel<3, 2, false, true><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+        else transport_lanes_kernel<3, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
+    } else if (fin) {
         transport_lanes_kernel<1, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, *fin);
-    else if (p.row_act)
+    } else if (p.row_act) {
         transport_lanes_kernel<0, 2, true><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
-    else
-        transport_lanes_kernel<0, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+    } else {
+        if (staged) transport_lanes_kernel<0, 2, false, true><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+        else transport_lanes_kernel<0, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+    }
     ctx->launches++;
     return check_cuda(ctx, cudaGetLastError(), "transport kernel");
 }
