@@ -200,7 +200,8 @@ int hk_transport_rhs(hk_ctx ctx, int n, double vmax, const double* f_dev, double
                      int x_halo, double dx, double dy, double eps_weno);
 /* esbgk_imex_step (src/esbgk.cpp:47-99) / penalized_imex_step (src/boltzmann.cpp:47-110):
  * one PR(2,2,2) step of a periodic all-kinetic field, in place.  work_dev: 6 nx ny n^3
- * doubles or NULL (allocated from the stream-ordered pool). */
+ * doubles (3 suffice for n a power of two >= 8 with ny >= 3: the regrouped step keeps
+ * Y, f_acc and the residual only) or NULL (context-owned, grow-only). */
 int hk_esbgk_imex_step(hk_ctx ctx, int n, double vmax, double* f_dev, int nx, int ny, double dx, double dy, double dt,
                        const double* eps_dev, double beta, double nu_coeff, double eps_weno, double* work_dev);
 int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int ny, double dx, double dy, double dt,
@@ -213,7 +214,7 @@ int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int n
  * separate stream, overlapped with that stage's residual (collision), and the
  * transport reads them from halo buffers (the reference's in-process neighbour
  * reads of src/transport.cpp:51-66 across ranks).  Same arithmetic as the periodic
- * steps above otherwise; work_dev: 6 nx_local ny n^3 doubles or NULL. */
+ * steps above otherwise; work_dev: as for the periodic steps (6, or 3, nx_local ny n^3 doubles) or NULL. */
 int hk_penalized_imex_step_slab(hk_ctx ctx, hk_kernel k, double* f_dev, int nx_local, int ny, double dx, double dy,
                                 double dt, const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
                                 double* work_dev);

@@ -70,11 +70,11 @@ struct Work {
 
 // Work fields of a step: the caller's buffer, else a context-owned one kept
 // across steps (grow-only; re-allocating ~100 GB per step costs seconds).
-int get_work(hk_ctx ctx, double* user, int64_t count, Work& w, double** owned) {
+int get_work(hk_ctx ctx, double* user, int64_t count, Work& w, double** owned, int nfields = 6) {
     *owned = nullptr;
     double* base = user;
     if (!base) {
-        const size_t need = sizeof(double) * count * 6;
+        const size_t need = sizeof(double) * count * nfields;
         if (need > ctx->step_bytes) {
             if (ctx->step_work) {
                 cudaStreamSynchronize(ctx->stream);
@@ -88,7 +88,10 @@ int get_work(hk_ctx ctx, double* user, int64_t count, Work& w, double** owned) {
         }
         base = static_cast<double*>(ctx->step_work);
     }
-    w = {base, base + count, base + 2 * count, base + 3 * count, base + 4 * count, base + 5 * count};
+    if (nfields == 3)  // the regrouped step: Y, f_acc, residual
+        w = {base, nullptr, nullptr, nullptr, base + 2 * count, base + count};
+    else
+        w = {base, base + count, base + 2 * count, base + 3 * count, base + 4 * count, base + 5 * count};
     return HK_OK;
 }
 
@@ -185,9 +188,12 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
     cudaSetDevice(ctx->device);
     const int64_t cells = (int64_t)nx * ny, nb = (int64_t)n * n * n, count = cells * nb;
     const PR222 t = pr222();
+    TransportParams tps{n, vmax, nx, ny, slab ? -2 : 0, dx, dy, eps_weno};
+    // the regrouped step (below) needs 3 work fields (Y, f_acc, residual), the general one 6
+    const bool regroup = stage_acc_supported(n) && transport_final_supported(tps);
     Work w;
     double* owned = nullptr;
-    int st = get_work(ctx, work_dev, count, w, &owned);
+    int st = get_work(ctx, work_dev, count, w, &owned, regroup ? 3 : 6);
     if (st) return st;
     // x-slab: the two [ny][2][n^3] halo buffers (context-owned, grow-only)
     double *lh = nullptr, *rh = nullptr;
@@ -265,9 +271,7 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
         timing_end(ctx);
         return e;
     };
-    TransportParams tps = tp;
-    if (slab) tps.x_halo = -2;
-    if (stage_acc_supported(n) && transport_final_supported(tps)) {
+    if (regroup) {
         // Regrouped step (FinalCombine modes 2 / 3): four field kernels, and
         // neither q1 nor k1 is stored.  T(Y1) writes f_acc and, in place of f,
         // G = f + dt w_ex0 q1 + w_im0 k1 - (w_im1 / a_im11) f_acc; T(Y2) finishes
