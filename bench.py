@@ -40,6 +40,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's init banner ("NCCL version ...", NCCL_DEBUG=VERSION) goes to stdout, where
+# rank 0's one JSON line must stand alone: keep NCCL at warnings (stderr).
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 N, A1, A2 = 32, 8, 8
 NCELLS = 64 * 64
