@@ -173,7 +173,10 @@ int hk_copy_to_host(hk_ctx ctx, void* dst_host, const void* src_dev, size_t byte
     cudaSetDevice(ctx->device);
     int st = HK_OK;
     if (bytes) st = check_cuda(ctx, cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+    {
+        const int sc = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+        if (!st) st = sc;
+    }
     return st;
 }
 
@@ -354,7 +357,10 @@ int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_d
         hk_cell_status* dev = st_dev ? st_dev : static_cast<hk_cell_status*>(ctx->scratch);
         hk_cell_status* h = new hk_cell_status[ncells > 0 ? ncells : 1];
         st = check_cuda(ctx, cudaMemcpyAsync(h, dev, sizeof(hk_cell_status) * ncells, cudaMemcpyDeviceToHost, ctx->stream), "D2H status");
-        if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+        {
+        const int sc = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+        if (!st) st = sc;
+    }
         if (!st) st = strict_verdict(ctx, h, ncells);
         delete[] h;
         return st;
@@ -509,17 +515,21 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
     if (st) {
         // Nothing (or not everything) will complete the counters the copy streams and
         // the kernel wait on: a failed launch or a failed copy enqueue.  Complete them
-        // from the compute stream so everything drains and the error is returned
-        // instead of blocking in the synchronise below.
+        // from the H2D stream (not the compute stream: a running persistent kernel
+        // would sit in front of the writes and wait for them) so everything drains
+        // and the error is returned instead of blocking in the synchronise below.
         for (int64_t c = 0; c < nch; ++c)
-            p_write_value32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
+            p_write_value32((CUstream)ctx->s_in, (CUdeviceptr)(flags_dev + c), 1u, 0);
         for (int64_t c = 0; c < nch; ++c)
-            p_write_value32((CUstream)ctx->stream, (CUdeviceptr)(flags_dev + c), 1u, 0);
+            p_write_value32((CUstream)ctx->s_in, (CUdeviceptr)(flags_dev + nch + c), 0x7fffffffu, 0);
     }
     // rerouted cells: their exact Q overwrote q_dev after the streamed copy
     int count = 0;
     std::vector<int64_t> list;
-    if (!st) st = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+    {
+        const int sc = check_cuda(ctx, cudaStreamSynchronize(ctx->stream), "sync");
+        if (!st) st = sc;
+    }
 #if HK_PROFILING
     t_sync = ms_since(t_in);
 #endif
