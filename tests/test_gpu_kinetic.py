@@ -228,3 +228,32 @@ def test_moment_operators_one_at_a_time(hk, kin, oracle, cells32):
         st, ref = oracle.remove_invariant_moments(n, VMAX, q[c], gm[c], mom[c, 1:4])
         assert st == 0
         assert np.abs(qd[c] - ref).max() <= 1e-12 * np.abs(q[c]).max(), c
+
+
+def test_imex_steps_run_in_three_work_fields(hk, kin):
+    """The regrouped PR(2,2,2) steps (n a power of two >= 8, ny >= 3) keep Y, f_acc and
+    the residual only: a caller's work buffer of 3 fields gives the same step, bitwise,
+    as the context-owned one (include/hykin_b200.h: hk_esbgk_imex_step)."""
+    import torch
+    n, nx, ny = 16, 4, 3
+    vg = hk.make_velocity_grid(n, VMAX)
+    f0, _ = inputs.config3_cells(nx, ny, n)
+    eps = torch.full((nx * ny,), 1e-2, dtype=torch.float64, device="cuda")
+    ctx = hk.default_context()
+    P = kin.EsbgkParams()
+    a = torch.from_numpy(f0.copy()).cuda()
+    kin.esbgk_imex_step(a, nx, ny, vg, 0.1, 0.1, 1e-3, eps)
+    b = torch.from_numpy(f0.copy()).cuda()
+    work = torch.full((3, nx * ny, n ** 3), float("nan"), dtype=torch.float64, device="cuda")
+    ctx.check(ctx._lib.hk_esbgk_imex_step(ctx.h, n, VMAX, b.data_ptr(), nx, ny, 0.1, 0.1, 1e-3, eps.data_ptr(),
+                                          P.beta, P.nu_coeff, P.eps_weno, work.data_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    k = hk.precompute_kernel(vg, n, 2, 4, inputs.R_PHYS_MAX)
+    c = torch.from_numpy(f0.copy()).cuda()
+    kin.penalized_imex_step(c, nx, ny, k, 0.1, 0.1, 1e-3, eps)
+    d = torch.from_numpy(f0.copy()).cuda()
+    ctx.check(ctx._lib.hk_penalized_imex_step(ctx.h, k.h, d.data_ptr(), nx, ny, 0.1, 0.1, 1e-3, eps.data_ptr(),
+                                              kin.PenalizationRule().coeff, 1e-6, 0, work.data_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(c, d)
