@@ -311,7 +311,8 @@ def spectral_collision(f, kernel: SpectralKernel, out=None, *, exact: bool = Fal
         if not (isinstance(q, torch.Tensor) and q.dtype == torch.float64 and q.is_contiguous()
                 and q.device == f.device and q.numel() == f.numel()):
             raise contract_violation("out must be a contiguous float64 tensor of f's size on f's device")
-    stt = torch.zeros(ncells * _abi.CELL_STATUS_BYTES // 8, dtype=torch.float64, device=f.device)
+    # every field is written by the library (zeroed or computed): no fill launch here
+    stt = torch.empty(ncells * _abi.CELL_STATUS_BYTES // 8, dtype=torch.float64, device=f.device)
     st = ctx._lib.hk_collision_batch(ctx.h, kernel.h, f.data_ptr(), q.data_ptr(), ncells, flags,
                                      stt.data_ptr())
     ctx.check(st)

@@ -95,6 +95,7 @@ int hk_ctx_destroy(hk_ctx ctx) {
     comm_destroy(ctx);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->fix_scratch) cudaFree(ctx->fix_scratch);
+    if (ctx->c16_ctr) cudaFree(ctx->c16_ctr);
     if (ctx->step_work) cudaFree(ctx->step_work);
     if (ctx->hyb_small) cudaFree(ctx->hyb_small);
     if (ctx->hyb_big) cudaFree(ctx->hyb_big);

@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "hk_common.cuh"
 #include "hk_internal.h"
@@ -1102,132 +1103,61 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
 }
 
 // ---------------------------------------------------------------------------
-// N = 16, EXACT (reference arithmetic), one cell per 2-CTA cluster with the
-// whole 16^3 spectrum in each CTA's shared memory: no transpose exchange at
-// all.  CTA r evaluates the directions e = r, r + 2, ... (CTA 1 also the loss
-// field): per direction the 512 threads transform both fields (alpha F and
-// alpha' F, one thread per pencil per field) along k3 (with the weights), k2
-// and k1 in place, then accumulate the complex gain of 8 nodes per thread in
-// registers.  The partial gains and the loss field meet in the cluster's L2
-// scratch; each CTA writes Q for half the nodes.  (The spectrum of a 16^3
-// cell reaches its Nyquist planes, so the fast path's guard reroutes every
-// such cell: the exact kernel is the production path at N = 16.)
+// N = 16, EXACT (reference arithmetic).  A cell's work is md + 1 items (the
+// distinct directions, then the loss field); the items of the whole batch are
+// split evenly over one persistent 256-thread CTA per SM (config 1: 64 cells x
+// 26 items = 11.2 items per SM instead of one cell per 2-CTA cluster on 128
+// SMs), so a CTA covers a run of consecutive items that may start or end
+// inside a cell.  Per cell the CTA transforms F = FFT(f)/N^3 into shared
+// memory once; per item thread p owns pencil p of BOTH fields (alpha F,
+// alpha' F): the k3 pass reads F once and applies both weight rows, the k2 and
+// k1 passes run in place (two independent 16-point transforms per thread, the
+// register file's ILP instead of more warps), and after the k1 pass the thread
+// holds ga and gb on its 16 nodes and accumulates the complex gain there: no
+// product pass, no exchange, 3 barriers per item.  The loss item finishes the
+// cell's partial sum, w gain - f loss.  A cell owned by one CTA is written from
+// registers; a split cell leaves each contributor's partial in L2 scratch and
+// the last contributor to arrive (per-cell counter) sums them in CTA order
+// (deterministic) and writes Q.  (The spectrum of a 16^3 cell reaches its
+// Nyquist planes, so the fast path's guard would reroute every such cell: the
+// exact kernel is the production path at N = 16.)
 // ---------------------------------------------------------------------------
 struct Geo16 {
     static constexpr int N = 16, R = 17, PL = N * R, BUF = N * PL;  // padded [k1][k2][k3]
-    static constexpr int NT = 512;
-    static constexpr size_t SMEM = size_t(3 * BUF) * sizeof(double2) + 64 * sizeof(double);
+    static constexpr int NT = 256;
+    static constexpr size_t SMEM = size_t(3 * BUF) * sizeof(double2) + 32 * sizeof(double);
+    static constexpr size_t SLOT = size_t(N) * N * N * sizeof(double2);  // one partial-sum slot
 };
 
 __device__ __forceinline__ int i16(int k1, int k2, int k3) { return k1 * Geo16::PL + k2 * Geo16::R + k3; }
 
-__global__ void __launch_bounds__(512, 1) coll16_exact_kernel(CollArgs a) {
+// owner CTA of item i when T items are split over G CTAs as [k T / G, (k + 1) T / G)
+__device__ __forceinline__ int64_t item_owner(int64_t i, int64_t T, int64_t G) { return ((i + 1) * G + T - 1) / T - 1; }
+
+__global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
     using G = Geo16;
     constexpr int N = 16, NB = 4096;
     extern __shared__ __align__(16) double2 smem[];
-    double2* Fs = smem;
+    double2* const Fs = smem;
     double2* const B0 = smem + G::BUF;      // alpha F  -> ga (and the loss field)
     double2* const B1 = smem + 2 * G::BUF;  // alpha' F -> gb
-    double* red = reinterpret_cast<double*>(smem + 3 * G::BUF);
-    const unsigned r = cluster_rank(), cid = cluster_id_x(), ncl = n_clusters_x();
-    const int t = threadIdx.x, phi = t >> 8, p = t & 255, ph = p >> 4, pl = p & 15;
+    double* const red = reinterpret_cast<double*>(smem + 3 * G::BUF);
+    __shared__ int last_flag;
+    const int t = threadIdx.x, ph = t >> 4, pl = t & 15;
+    const int warp = t >> 5, lane = t & 31;
     const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
-    double2* X = a.xchg + (int64_t)cid * 3 * NB;  // [gain of CTA 0][gain of CTA 1][loss field], natural order
-    for (int64_t it = cid; it < count; it += ncl) {
-        const int64_t cell = a.list ? a.list[it] : it;
-        const double* fc = a.f + cell * NB;
-        // ---- F = FFT(f) / N^3 (both CTAs), k3 then k2 then k1 ----
-        for (int k = t; k < NB; k += G::NT) Fs[i16(k >> 8, (k >> 4) & 15, k & 15)] = make_double2(__ldg(fc + k), 0.0);
-        __syncthreads();
-        for (int pass = 0; pass < 3; ++pass) {
-            if (t < 256) {
-                double2* base = pass == 0 ? Fs + i16(ph, pl, 0) : (pass == 1 ? Fs + i16(ph, 0, pl) : Fs + i16(0, ph, pl));
-                const int st = pass == 0 ? 1 : (pass == 1 ? G::R : G::PL);
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = base[i * st];
-                fft_reg<N, false>(x);
-                const double sc = pass == 2 ? 1.0 / double(NB) : 1.0;
-#pragma unroll
-                for (int i = 0; i < N; ++i) base[i * st] = make_double2(x[i].x * sc, x[i].y * sc);
-            }
-            __syncthreads();
-        }
-        double2 g[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) g[i] = make_double2(0.0, 0.0);
-        const int n_dir = (a.md - (int)r + 1) / 2;  // directions r, r + 2, ...
-        const int n_ent = n_dir + (r == 1 ? 1 : 0);  // CTA 1 also transforms the loss field
-        for (int q = 0; q < n_ent; ++q) {
-            const bool loss = q == n_dir;
-            const int e = (int)r + 2 * q;
-            const bool act = !loss || phi == 0;
-            double2* B = phi ? B1 : B0;
-            if (act) {  // k3 pass with the weights: pencil (k1, k2) = (ph, pl)
-                const double* wt = loss ? a.loss : (phi ? a.alpha_p : a.alpha) + (int64_t)e * NB;
-                wt += ph * 256 + pl;  // [i1][i3][i2]
-                const double2* fr = Fs + i16(ph, pl, 0);
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) {
-                    const double w = __ldg(wt + i * N);
-                    const double2 F = fr[i];
-                    x[i] = make_double2(F.x * w, F.y * w);
-                }
-                fft_reg<N, true>(x);
-                double2* o = B + i16(ph, pl, 0);
-#pragma unroll
-                for (int i = 0; i < N; ++i) o[i] = x[i];
-            }
-            __syncthreads();
-            if (act) {  // k2 pass: pencil (k1, k3) = (ph, pl)
-                double2* o = B + i16(ph, 0, pl);
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = o[i * G::R];
-                fft_reg<N, true>(x);
-#pragma unroll
-                for (int i = 0; i < N; ++i) o[i * G::R] = x[i];
-            }
-            __syncthreads();
-            if (act) {  // k1 pass: pencil (k2, k3) = (ph, pl)
-                double2* o = B + i16(0, ph, pl);
-                double2 x[N];
-#pragma unroll
-                for (int i = 0; i < N; ++i) x[i] = o[i * G::PL];
-                fft_reg<N, true>(x);
-#pragma unroll
-                for (int i = 0; i < N; ++i) o[i * G::PL] = x[i];
-            }
-            __syncthreads();
-            if (!loss) {  // gain += m ga gb on nodes (k1 = 8 phi + i, k2 = ph, k3 = pl)
-                const double m = e == 0 ? a.mult0 : 1.0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int ix = i16(8 * phi + i, ph, pl);
-                    const double2 ga = B0[ix], gb = B1[ix];
-                    g[i].x += m * (ga.x * gb.x - ga.y * gb.y);
-                    g[i].y += m * (ga.x * gb.y + ga.y * gb.x);
-                }
-                __syncthreads();  // buffers free for the next direction
-            }
-        }
-        // ---- partial gains (and the loss field) meet in the cluster's scratch ----
-#pragma unroll
-        for (int i = 0; i < 8; ++i) st_cg16(X + (int64_t)r * NB + (8 * phi + i) * 256 + p, g[i]);
-        if (r == 1)
-            for (int k = t; k < NB; k += G::NT) st_cg16(X + 2 * NB + k, B0[i16(k >> 8, (k >> 4) & 15, k & 15)]);
-        cluster_arrive();
-        cluster_wait();
-        // ---- Q = jac (w gain - f loss) on k1 in [8 r, 8 r + 8) ----
+    const int64_t P = a.md + 1, T = count * P, NG = gridDim.x, k = blockIdx.x;
+    const int64_t i0 = k * T / NG, i1 = (k + 1) * T / NG;
+    const int64_t first_cell = i0 / P;
+
+    // Q = jac Re(acc) on this thread's nodes (k1, (k2, k3) = t), status of the cell
+    auto finish = [&](int64_t cell, const double2 (&acc)[N]) {
         double mre = 0.0, mim = 0.0, n2 = 0.0;
         double* qc = a.q + cell * NB;
-        for (int k = (int)r * 2048 + t; k < ((int)r + 1) * 2048; k += G::NT) {
-            const double2 g0 = ld_cg16(X + k), g1 = ld_cg16(X + NB + k), L = ld_cg16(X + 2 * NB + k);
-            const double fv = __ldg(fc + k);
-            const double qre = a.jac * (a.w * (g0.x + g1.x) - fv * L.x);
-            const double qim = a.jac * (a.w * (g0.y + g1.y) - fv * L.y);
-            qc[k] = qre;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double qre = a.jac * acc[j].x, qim = a.jac * acc[j].y;
+            qc[j * 256 + t] = qre;
             mre = fmax(mre, fabs(qre));
             mim = fmax(mim, fabs(qim));
             n2 += qre * qre;
@@ -1238,68 +1168,206 @@ __global__ void __launch_bounds__(512, 1) coll16_exact_kernel(CollArgs a) {
             mim = fmax(mim, __shfl_xor_sync(0xffffffffu, mim, o));
             n2 += __shfl_xor_sync(0xffffffffu, n2, o);
         }
-        const int warp = t >> 5, lane = t & 31;
         if (lane == 0) {
             red[warp] = mre;
-            red[16 + warp] = mim;
-            red[32 + warp] = n2;
+            red[8 + warp] = mim;
+            red[16 + warp] = n2;
         }
         __syncthreads();
-        if (t == 0 && a.st) {
+        if (t == 0 && a.st) {  // the cell's only writer: the whole verdict, residue bit included
             double m1 = 0, m2 = 0, sum = 0;
-            for (int w = 0; w < 16; ++w) {
+            for (int w = 0; w < 8; ++w) {
                 m1 = fmax(m1, red[w]);
-                m2 = fmax(m2, red[16 + w]);
-                sum += red[32 + w];
+                m2 = fmax(m2, red[8 + w]);
+                sum += red[16 + w];
             }
-            hk_cell_status* sc = a.st + cell;
-            atomic_max_nonneg(&sc->max_re, m1);
-            atomic_max_nonneg(&sc->max_im, m2);
-            atomicAdd(&sc->q_norm2, sum);
-            if (r == 0) atomicOr(&sc->flags, HK_CELL_EXACT);
+            hk_cell_status v;
+            v.max_re = m1;
+            v.max_im = m2;
+            v.q_norm2 = sum;
+            v.nyq_bound = 0.0;
+            v.flags = HK_CELL_EXACT | (m2 > 1e-10 * fmax(m1, 1e-300) ? HK_CELL_RESIDUE : 0u);
+            v.reserved = 0;
+            v.loss_norm2 = 0.0;
+            a.st[cell] = v;
         }
-        cluster_arrive();  // the scratch and SMEM are free for the next cell
-        cluster_wait();
+        __syncthreads();  // red is reused
+    };
+
+    for (int64_t i = i0; i < i1;) {
+        const int64_t c = i / P;
+        const int qa = int(i - c * P), qb = int(i1 - c * P < P ? i1 - c * P : P);  // items [qa, qb) of cell c here
+        const int64_t cell = a.list ? a.list[c] : c;
+        const double* fc = a.f + cell * NB;
+        // ---- F = FFT(f) / N^3 into Fs, k3 then k2 then k1 ----
+        for (int kk = t; kk < NB; kk += G::NT) Fs[i16(kk >> 8, (kk >> 4) & 15, kk & 15)] = make_double2(__ldg(fc + kk), 0.0);
+        __syncthreads();
+        for (int pass = 0; pass < 3; ++pass) {
+            double2* base = pass == 0 ? Fs + i16(ph, pl, 0) : (pass == 1 ? Fs + i16(ph, 0, pl) : Fs + i16(0, ph, pl));
+            const int st = pass == 0 ? 1 : (pass == 1 ? G::R : G::PL);
+            double2 x[N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) x[j] = base[j * st];
+            fft_reg<N, false>(x);
+            const double sc = pass == 2 ? 1.0 / double(NB) : 1.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) base[j * st] = make_double2(x[j].x * sc, x[j].y * sc);
+            __syncthreads();
+        }
+        double2 acc[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[j] = make_double2(0.0, 0.0);
+        for (int q = qa; q < qb; ++q) {
+            const bool loss = q == a.md;  // CTA-uniform
+            double2 xa[N], xb[N];
+            {  // k3 pass with the weights: pencil (k1, k2) = (ph, pl)
+                const int64_t off = (int64_t)q * NB + ph * 256 + pl;  // [i1][i3][i2]
+                const double* wa = loss ? a.loss + ph * 256 + pl : a.alpha + off;
+                const double* wb = a.alpha_p + off;
+                const double2* fr = Fs + i16(ph, pl, 0);
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    const double2 F = fr[j];
+                    const double w0 = __ldg(wa + j * N);
+                    xa[j] = make_double2(F.x * w0, F.y * w0);
+                    if (!loss) {
+                        const double w1 = __ldg(wb + j * N);
+                        xb[j] = make_double2(F.x * w1, F.y * w1);
+                    }
+                }
+                fft_fma<N, true>(xa);
+                double2* oa = B0 + i16(ph, pl, 0);
+#pragma unroll
+                for (int j = 0; j < N; ++j) oa[j] = xa[j];
+                if (!loss) {
+                    fft_fma<N, true>(xb);
+                    double2* ob = B1 + i16(ph, pl, 0);
+#pragma unroll
+                    for (int j = 0; j < N; ++j) ob[j] = xb[j];
+                }
+            }
+            __syncthreads();
+            {  // k2 pass: pencil (k1, k3) = (ph, pl)
+                double2* oa = B0 + i16(ph, 0, pl);
+                double2* ob = B1 + i16(ph, 0, pl);
+#pragma unroll
+                for (int j = 0; j < N; ++j) xa[j] = oa[j * G::R];
+                if (!loss) {
+#pragma unroll
+                    for (int j = 0; j < N; ++j) xb[j] = ob[j * G::R];
+                }
+                fft_fma<N, true>(xa);
+#pragma unroll
+                for (int j = 0; j < N; ++j) oa[j * G::R] = xa[j];
+                if (!loss) {
+                    fft_fma<N, true>(xb);
+#pragma unroll
+                    for (int j = 0; j < N; ++j) ob[j * G::R] = xb[j];
+                }
+            }
+            __syncthreads();
+            {  // k1 pass: pencil (k2, k3) = (ph, pl) = t, the thread's own nodes
+                const double2* oa = B0 + i16(0, ph, pl);
+                const double2* ob = B1 + i16(0, ph, pl);
+#pragma unroll
+                for (int j = 0; j < N; ++j) xa[j] = oa[j * G::PL];
+                if (!loss) {
+#pragma unroll
+                    for (int j = 0; j < N; ++j) xb[j] = ob[j * G::PL];
+                }
+            }
+            __syncthreads();  // the buffers are free for the next item's k3 pass
+            fft_fma<N, true>(xa);
+            if (!loss) {  // gain += m ga gb
+                fft_fma<N, true>(xb);
+                const double m = q == 0 ? a.mult0 : 1.0;
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    acc[j].x += m * (xa[j].x * xb[j].x - xa[j].y * xb[j].y);
+                    acc[j].y += m * (xa[j].x * xb[j].y + xa[j].y * xb[j].x);
+                }
+            } else {  // the cell's last item: acc = w gain - f loss
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    const double fv = __ldg(fc + j * 256 + t);
+                    acc[j] = make_double2(a.w * acc[j].x - fv * xa[j].x, a.w * acc[j].y - fv * xa[j].y);
+                }
+            }
+        }
+        if (qb < P) {  // the loss item is elsewhere: this partial is w gain
+#pragma unroll
+            for (int j = 0; j < N; ++j) acc[j] = make_double2(a.w * acc[j].x, a.w * acc[j].y);
+        }
+        if (qa == 0 && qb == P) {
+            finish(cell, acc);
+        } else {
+            // split cell: park the partial, the last contributor sums them in CTA order
+            double2* slot = a.xchg + (2 * k + (c == first_cell ? 0 : 1)) * (int64_t)NB;
+#pragma unroll
+            for (int j = 0; j < N; ++j) st_cg16(slot + j * 256 + t, acc[j]);
+            const int64_t kf = item_owner(c * P, T, NG), kl = item_owner(c * P + P - 1, T, NG);
+            __threadfence();
+            __syncthreads();
+            if (t == 0) {
+                unsigned* ctr = a.team_ctr + 2 * kf + (c == (kf * T / NG) / P ? 0 : 1);
+                const unsigned old = atomicAdd(ctr, 1u);
+                last_flag = old == unsigned(kl - kf);
+                if (last_flag) *ctr = 0;  // leave the counter clean
+                __threadfence();
+            }
+            __syncthreads();
+            if (last_flag) {
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc[j] = make_double2(0.0, 0.0);
+                for (int64_t kc = kf; kc <= kl; ++kc) {
+                    const double2* s = a.xchg + (2 * kc + (c == (kc * T / NG) / P ? 0 : 1)) * (int64_t)NB;
+#pragma unroll
+                    for (int j = 0; j < N; ++j) {
+                        const double2 v = ld_cg16(s + j * 256 + t);
+                        acc[j].x += v.x;
+                        acc[j].y += v.y;
+                    }
+                }
+                finish(cell, acc);
+            }
+        }
+        i = c * P + qb;
     }
 }
 
+size_t coll16_xchg_bytes(hk_ctx ctx) { return size_t(2) * ctx->sm_count * Geo16::SLOT; }
+
 int launch_coll16(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) {
     auto kern = coll16_exact_kernel;
-    const int key = 16 * 100 + 99;
+    const int key = 16 * 100 + 98;
     int st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
     if (!ctx->max_clusters.count(key)) {
         if ((st = check_cuda(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                        (int)Geo16::SMEM), "smem attribute")))
             return st;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * 256);
-        cfg.blockDim = dim3(Geo16::NT);
-        cfg.dynamicSmemBytes = Geo16::SMEM;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        int ncl = 0;
-        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg), "max active clusters")))
+        int per_sm = 0;
+        if ((st = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Geo16::NT, Geo16::SMEM),
+                             "occupancy")))
             return st;
-        if (ncl < 1) return fail(ctx, HK_CUDA, "N = 16 collision kernel cannot be resident");
-        ctx->max_clusters[key] = ncl;
+        if (per_sm < 1) return fail(ctx, HK_CUDA, "N = 16 collision kernel cannot be resident");
+        ctx->max_clusters[key] = ctx->sm_count;  // one CTA per SM (the partial slots are sized for it)
     }
-    int64_t ncl = ctx->max_clusters[key];
-    if (max_cells < ncl) ncl = max_cells;
-    if (ncl < 1) return HK_OK;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(2 * ncl));
-    cfg.blockDim = dim3(Geo16::NT);
-    cfg.dynamicSmemBytes = Geo16::SMEM;
-    cfg.stream = ctx->stream;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    int64_t grid = ctx->max_clusters[key];
+    const int64_t items = max_cells * (args.md + 1);
+    if (items < grid) grid = items;
+    if (grid < 1) return HK_OK;
+    // split-cell counters: zeroed once, left clean by every launch (the last contributor resets its counter)
+    if (!ctx->c16_ctr) {
+        if ((st = check_cuda(ctx, cudaMalloc(&ctx->c16_ctr, sizeof(unsigned) * 2 * ctx->sm_count), "split-cell counters")))
+            return st;
+        if ((st = check_cuda(ctx, cudaMemset(ctx->c16_ctr, 0, sizeof(unsigned) * 2 * ctx->sm_count), "split-cell counters")))
+            return st;
+    }
+    CollArgs x = args;
+    x.team_ctr = ctx->c16_ctr;
     timing_begin(ctx, tag);
-    st = check_cuda(ctx, cudaLaunchKernelEx(&cfg, kern, args), "collision kernel launch");
+    coll16_exact_kernel<<<unsigned(grid), Geo16::NT, Geo16::SMEM, ctx->stream>>>(x);
+    st = check_cuda(ctx, cudaGetLastError(), "collision kernel launch");
     timing_end(ctx);
     ctx->launches++;
     return st;
@@ -1338,7 +1406,9 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
             constexpr int CW = 4;
             team_kernel = size_t(ctx->sm_count / CW) * GeoW<N, CW>::D * CW * (N / CW) * N * N * sizeof(double2);
         }
-        xchg_bytes = (exact ? cluster_kernel : std::max(cluster_kernel, team_kernel)) + 65536;
+        size_t exact_kernel = cluster_kernel;
+        if constexpr (N == 16) exact_kernel = coll16_xchg_bytes(ctx);
+        xchg_bytes = (exact ? exact_kernel : std::max(cluster_kernel, team_kernel)) + 65536;
     }
     int s;
     if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
@@ -1350,7 +1420,9 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     int64_t* list = guard ? reinterpret_cast<int64_t*>(base + st_bytes + nyq_bytes) : nullptr;
     int* count = reinterpret_cast<int*>(base + st_bytes + nyq_bytes + list_bytes);
     double* part = ksplit > 1 ? reinterpret_cast<double*>(base + xchg_off - part_bytes) : nullptr;
-    cudaMemsetAsync(st, 0, sizeof(hk_cell_status) * ncells, ctx->stream);
+    // the N = 16 exact kernel writes every cell's whole verdict (residue bit included) itself
+    const bool self_verdict = N == 16 && exact;
+    if (!self_verdict) cudaMemsetAsync(st, 0, sizeof(hk_cell_status) * ncells, ctx->stream);
 
     CollArgs a{};
     a.f = f;
@@ -1465,7 +1537,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
         }
         if (guard && (s = guard_fix(0, ncells, count))) return s;
     }
-    {
+    if (!self_verdict) {
         residue_kernel<<<unsigned((ncells + 255) / 256), 256, 0, ctx->stream>>>(ncells, st);
         ctx->launches++;
         if ((s = check_cuda(ctx, cudaGetLastError(), "residue kernel"))) return s;

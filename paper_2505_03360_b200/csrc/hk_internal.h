@@ -55,6 +55,8 @@ struct hk_ctx_s {
     size_t hyb_big_bytes = 0;
     // Nyquist-correction plane scratch (hk_nyqfix.cu)
     void* fix_scratch = nullptr;
+    // N = 16 split-cell counters (hk_collision.cu), zeroed once and kept clean by the kernel
+    unsigned* c16_ctr = nullptr;
     size_t fix_bytes = 0;
     // NCCL communicator (hk_comm.cu; ncclComm_t, loaded at run time)
     void* comm = nullptr;

@@ -42,6 +42,32 @@ def test_n16_exact_matches_oracle(n16, hk):
     assert np.array_equal((st["flags"] & 2) != 0, n16["st_ref"] == 4)
 
 
+@pytest.mark.parametrize("ncells", [1, 2, 5, 7, 64, 211])
+def test_n16_item_split_batches(hk, oracle, ncells):
+    """The N = 16 kernel spreads the batch's md + 1 items per cell evenly over
+    one CTA per SM, so cells are split across CTAs at batch-size-dependent
+    points (1 cell: 26 items on 26 CTAs; 211 cells: 37 items per CTA).  Every
+    split pattern must give the oracle's Q and status, and a repeated call the
+    same bits (partials are summed in CTA order, not arrival order)."""
+    import torch
+    n, a1, a2 = 16, 4, 8
+    vg = hk.make_velocity_grid(n, inputs.VMAX)
+    kern = hk.precompute_kernel(vg, n, a1, a2, inputs.R_PHYS_MAX)
+    ko = oracle.kernel(n, inputs.VMAX, a1, a2, inputs.R_PHYS_MAX, closed_form=True)
+    f = inputs.config1_cells(ncells, n)
+    sel = sorted({0, ncells // 3, ncells // 2, ncells - 1})
+    q_ref, _, _ = oracle.collision_batch(ko, np.ascontiguousarray(f[sel]))
+    fd = torch.from_numpy(f).cuda()
+    q, st = hk.spectral_collision(fd, kern, return_status=True)
+    q = q.cpu().numpy()
+    for i, c in enumerate(sel):
+        assert rel_l2(q[c], q_ref[i]) < TOL, (ncells, c)
+    assert np.all(st["flags"] & 1)
+    np.testing.assert_allclose(st["q_norm2"], (q ** 2).sum(axis=1), rtol=1e-12)
+    q2 = hk.spectral_collision(fd, kern).cpu().numpy()
+    assert np.array_equal(q, q2)
+
+
 def test_n16_default_path_reroutes_and_matches(n16, hk):
     import torch
     f = torch.from_numpy(n16["f"]).cuda()
