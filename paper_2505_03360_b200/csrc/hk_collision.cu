@@ -1104,23 +1104,22 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
 
 // ---------------------------------------------------------------------------
 // N = 16, EXACT (reference arithmetic).  A cell's work is md + 1 items (the
-// distinct directions, then the loss field); the items of the whole batch are
-// split evenly over one persistent 256-thread CTA per SM (config 1: 64 cells x
-// 26 items = 11.2 items per SM instead of one cell per 2-CTA cluster on 128
-// SMs), so a CTA covers a run of consecutive items that may start or end
-// inside a cell.  Per cell the CTA transforms F = FFT(f)/N^3 into shared
-// memory once; per item thread p owns pencil p of BOTH fields (alpha F,
-// alpha' F): the k3 pass reads F once and applies both weight rows, the k2 and
-// k1 passes run in place (two independent 16-point transforms per thread, the
-// register file's ILP instead of more warps), and after the k1 pass the thread
-// holds ga and gb on its 16 nodes and accumulates the complex gain there: no
-// product pass, no exchange, 3 barriers per item.  The loss item finishes the
-// cell's partial sum, w gain - f loss.  A cell owned by one CTA is written from
-// registers; a split cell leaves each contributor's partial in L2 scratch and
-// the last contributor to arrive (per-cell counter) sums them in CTA order
-// (deterministic) and writes Q.  (The spectrum of a 16^3 cell reaches its
-// Nyquist planes, so the fast path's guard would reroute every such cell: the
-// exact kernel is the production path at N = 16.)
+// distinct directions, then the loss field) in two FIXED halves, U0 = w gain
+// over items [0, H) and U1 = w gain - f loss over [H, md + 1); the batch's
+// halves are split evenly over one persistent 256-thread CTA per SM (config 1:
+// 128 halves on 128 SMs).  Per cell the CTA transforms F = FFT(f)/N^3 into
+// shared memory once; per item thread p owns pencil p of BOTH fields
+// (alpha F, alpha' F): the k3 pass reads F once and applies both weight rows,
+// the k2 and k1 passes run in place (two independent 16-point transforms per
+// thread, the register file's ILP instead of more warps), and after the k1
+// pass the thread holds ga and gb on its 16 nodes and accumulates the complex
+// gain there: no product pass, no exchange, 3 barriers per item.
+// Q = jac Re(U0 + U1) always, whether both halves ran on one CTA (U0 parked in
+// L2 meanwhile) or on two (the later one adds them, per-cell counter): a
+// cell's bits never depend on the batch it is in (load balancing and x-slab
+// steps stay bitwise the single-batch step).  (The spectrum of a 16^3 cell
+// reaches its Nyquist planes, so the fast path's guard would reroute every
+// such cell: the exact kernel is the production path at N = 16.)
 // ---------------------------------------------------------------------------
 struct Geo16 {
     static constexpr int N = 16, R = 17, PL = N * R, BUF = N * PL;  // padded [k1][k2][k3]
@@ -1146,9 +1145,14 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
     const int t = threadIdx.x, ph = t >> 4, pl = t & 15;
     const int warp = t >> 5, lane = t & 31;
     const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
-    const int64_t P = a.md + 1, T = count * P, NG = gridDim.x, k = blockIdx.x;
-    const int64_t i0 = k * T / NG, i1 = (k + 1) * T / NG;
-    const int64_t first_cell = i0 / P;
+    // units: the two fixed halves of a cell's items, [0, H) and [H, P) (the loss item last)
+    const int P = a.md + 1, H = (P + 1) / 2;
+    const int64_t T = count * 2, NG = gridDim.x, k = blockIdx.x;
+    const int64_t u0 = k * T / NG, u1 = (k + 1) * T / NG;
+    auto slot_of = [&](int64_t kc, int64_t u) {  // partial slot of unit u on CTA kc: its first unit -> 0, else 1
+        return a.xchg + (3 * kc + (u == kc * T / NG ? 0 : 1)) * (int64_t)NB;
+    };
+    double2* const park = a.xchg + (3 * k + 2) * (int64_t)NB;  // a whole cell's first half while its second runs
 
     // Q = jac Re(acc) on this thread's nodes (k1, (k2, k3) = t), status of the cell
     auto finish = [&](int64_t cell, const double2 (&acc)[N]) {
@@ -1194,25 +1198,29 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
         __syncthreads();  // red is reused
     };
 
-    for (int64_t i = i0; i < i1;) {
-        const int64_t c = i / P;
-        const int qa = int(i - c * P), qb = int(i1 - c * P < P ? i1 - c * P : P);  // items [qa, qb) of cell c here
+    int64_t cur = -1;
+    for (int64_t u = u0; u < u1; ++u) {
+        const int64_t c = u >> 1;
+        const int half = int(u & 1), qa = half ? H : 0, qb = half ? P : H;  // items [qa, qb) of cell c
         const int64_t cell = a.list ? a.list[c] : c;
         const double* fc = a.f + cell * NB;
-        // ---- F = FFT(f) / N^3 into Fs, k3 then k2 then k1 ----
-        for (int kk = t; kk < NB; kk += G::NT) Fs[i16(kk >> 8, (kk >> 4) & 15, kk & 15)] = make_double2(__ldg(fc + kk), 0.0);
-        __syncthreads();
-        for (int pass = 0; pass < 3; ++pass) {
-            double2* base = pass == 0 ? Fs + i16(ph, pl, 0) : (pass == 1 ? Fs + i16(ph, 0, pl) : Fs + i16(0, ph, pl));
-            const int st = pass == 0 ? 1 : (pass == 1 ? G::R : G::PL);
-            double2 x[N];
-#pragma unroll
-            for (int j = 0; j < N; ++j) x[j] = base[j * st];
-            fft_reg<N, false>(x);
-            const double sc = pass == 2 ? 1.0 / double(NB) : 1.0;
-#pragma unroll
-            for (int j = 0; j < N; ++j) base[j * st] = make_double2(x[j].x * sc, x[j].y * sc);
+        if (c != cur) {  // ---- F = FFT(f) / N^3 into Fs, k3 then k2 then k1 ----
+            cur = c;
+            for (int kk = t; kk < NB; kk += G::NT)
+                Fs[i16(kk >> 8, (kk >> 4) & 15, kk & 15)] = make_double2(__ldg(fc + kk), 0.0);
             __syncthreads();
+            for (int pass = 0; pass < 3; ++pass) {
+                double2* base = pass == 0 ? Fs + i16(ph, pl, 0) : (pass == 1 ? Fs + i16(ph, 0, pl) : Fs + i16(0, ph, pl));
+                const int st = pass == 0 ? 1 : (pass == 1 ? G::R : G::PL);
+                double2 x[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) x[j] = base[j * st];
+                fft_reg<N, false>(x);
+                const double sc = pass == 2 ? 1.0 / double(NB) : 1.0;
+#pragma unroll
+                for (int j = 0; j < N; ++j) base[j * st] = make_double2(x[j].x * sc, x[j].y * sc);
+                __syncthreads();
+            }
         }
         double2 acc[N];
 #pragma unroll
@@ -1294,48 +1302,55 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
                 }
             }
         }
-        if (qb < P) {  // the loss item is elsewhere: this partial is w gain
+        if (!half) {  // the first half holds no loss item: its partial is w gain
 #pragma unroll
             for (int j = 0; j < N; ++j) acc[j] = make_double2(a.w * acc[j].x, a.w * acc[j].y);
         }
-        if (qa == 0 && qb == P) {
-            finish(cell, acc);
+        // Q = jac Re(U0 + U1) in every case: the bits of a cell never depend on its batch
+        const bool both_here = 2 * c >= u0 && 2 * c + 1 < u1;
+        if (both_here) {
+            if (!half) {
+#pragma unroll
+                for (int j = 0; j < N; ++j) st_cg16(park + j * 256 + t, acc[j]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    const double2 v = ld_cg16(park + j * 256 + t);
+                    acc[j] = make_double2(v.x + acc[j].x, v.y + acc[j].y);
+                }
+                finish(cell, acc);
+            }
         } else {
-            // split cell: park the partial, the last contributor sums them in CTA order
-            double2* slot = a.xchg + (2 * k + (c == first_cell ? 0 : 1)) * (int64_t)NB;
+            // split cell: park this half in L2, the later of the two CTAs adds U0 + U1
+            double2* slot = slot_of(k, u);
 #pragma unroll
             for (int j = 0; j < N; ++j) st_cg16(slot + j * 256 + t, acc[j]);
-            const int64_t kf = item_owner(c * P, T, NG), kl = item_owner(c * P + P - 1, T, NG);
+            const int64_t kf = item_owner(2 * c, T, NG), kl = item_owner(2 * c + 1, T, NG);
             __threadfence();
             __syncthreads();
             if (t == 0) {
-                unsigned* ctr = a.team_ctr + 2 * kf + (c == (kf * T / NG) / P ? 0 : 1);
+                unsigned* ctr = a.team_ctr + 2 * kf + (2 * c == kf * T / NG ? 0 : 1);
                 const unsigned old = atomicAdd(ctr, 1u);
-                last_flag = old == unsigned(kl - kf);
+                last_flag = old == 1u;
                 if (last_flag) *ctr = 0;  // leave the counter clean
                 __threadfence();
             }
             __syncthreads();
             if (last_flag) {
+                const double2* s0 = slot_of(kf, 2 * c);
+                const double2* s1 = slot_of(kl, 2 * c + 1);
 #pragma unroll
-                for (int j = 0; j < N; ++j) acc[j] = make_double2(0.0, 0.0);
-                for (int64_t kc = kf; kc <= kl; ++kc) {
-                    const double2* s = a.xchg + (2 * kc + (c == (kc * T / NG) / P ? 0 : 1)) * (int64_t)NB;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) {
-                        const double2 v = ld_cg16(s + j * 256 + t);
-                        acc[j].x += v.x;
-                        acc[j].y += v.y;
-                    }
+                for (int j = 0; j < N; ++j) {
+                    const double2 v0 = ld_cg16(s0 + j * 256 + t), v1 = ld_cg16(s1 + j * 256 + t);
+                    acc[j] = make_double2(v0.x + v1.x, v0.y + v1.y);
                 }
                 finish(cell, acc);
             }
         }
-        i = c * P + qb;
     }
 }
 
-size_t coll16_xchg_bytes(hk_ctx ctx) { return size_t(2) * ctx->sm_count * Geo16::SLOT; }
+size_t coll16_xchg_bytes(hk_ctx ctx) { return size_t(3) * ctx->sm_count * Geo16::SLOT; }
 
 int launch_coll16(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) {
     auto kern = coll16_exact_kernel;
@@ -1353,8 +1368,8 @@ int launch_coll16(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) 
         ctx->max_clusters[key] = ctx->sm_count;  // one CTA per SM (the partial slots are sized for it)
     }
     int64_t grid = ctx->max_clusters[key];
-    const int64_t items = max_cells * (args.md + 1);
-    if (items < grid) grid = items;
+    const int64_t units = max_cells * 2;
+    if (units < grid) grid = units;
     if (grid < 1) return HK_OK;
     // split-cell counters: zeroed once, left clean by every launch (the last contributor resets its counter)
     if (!ctx->c16_ctr) {

@@ -44,11 +44,11 @@ def test_n16_exact_matches_oracle(n16, hk):
 
 @pytest.mark.parametrize("ncells", [1, 2, 5, 7, 64, 211])
 def test_n16_item_split_batches(hk, oracle, ncells):
-    """The N = 16 kernel spreads the batch's md + 1 items per cell evenly over
-    one CTA per SM, so cells are split across CTAs at batch-size-dependent
-    points (1 cell: 26 items on 26 CTAs; 211 cells: 37 items per CTA).  Every
-    split pattern must give the oracle's Q and status, and a repeated call the
-    same bits (partials are summed in CTA order, not arrival order)."""
+    """The N = 16 kernel spreads the batch's cell halves evenly over one CTA per
+    SM, so a cell's two halves run on one CTA or on two depending on the batch
+    size (1 cell: 2 CTAs; 211 cells: 2.85 halves per CTA).  Every pattern must
+    give the oracle's Q and status, a repeated call the same bits, and a cell
+    the same bits alone as inside the batch."""
     import torch
     n, a1, a2 = 16, 4, 8
     vg = hk.make_velocity_grid(n, inputs.VMAX)
@@ -66,6 +66,10 @@ def test_n16_item_split_batches(hk, oracle, ncells):
     np.testing.assert_allclose(st["q_norm2"], (q ** 2).sum(axis=1), rtol=1e-12)
     q2 = hk.spectral_collision(fd, kern).cpu().numpy()
     assert np.array_equal(q, q2)
+    # a cell's bits do not depend on the batch it is in (fixed halves, U0 + U1)
+    for c in sel:
+        q1 = hk.spectral_collision(fd[c:c + 1], kern).cpu().numpy()
+        assert np.array_equal(q1[0], q[c]), (ncells, c)
 
 
 def test_n16_default_path_reroutes_and_matches(n16, hk):

@@ -60,10 +60,10 @@ def config1(iters):
     peak = ctx.fp64_peak_tflops()
     ach = W * cells / (ms * 1e-3) / 1e12
     return {"config": "config1: 64 cells, 16^3, M=4x8, hard spheres, Q + forward Euler dt=0.01",
-            "path": "exact kernel (one persistent CTA per SM over the batch's md + 1 items per cell, 16^3 spectrum in shared memory, split cells summed by the last contributor)",
+            "path": "exact kernel (a cell's items in two fixed halves over one persistent CTA per SM, 16^3 spectrum in shared memory, Q = jac Re(U0 + U1))",
             "ms_per_step": ms, "cell_updates_per_s": cells / (ms * 1e-3),
             "roofline": {"bound": "fp64", "achieved_tflops": ach, "peak_tflops": peak, "frac": ach / peak,
-                         "note": "64 cells x 26 items on 148 SMs (11.2 items per SM); 8 warps per SM, barrier-phased shared-memory passes"}}
+                         "note": "64 cells = 128 halves of 13 items on 148 SMs; 8 warps per SM, barrier-phased shared-memory passes"}}
 
 
 def config3(iters, nx=256, ny=256):

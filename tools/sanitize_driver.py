@@ -25,7 +25,7 @@ def coll(n, a1, a2, f, **kw):
     return q
 
 
-if op == "coll16":  # N = 16 exact (2-CTA cluster kernel)
+if op == "coll16":  # N = 16 exact (cell halves over persistent CTAs)
     coll(16, 4, 8, inputs.config1_cells(2, 16))
 elif op == "coll32":  # N = 32 fast 12-warp team kernel + guard + Nyquist correction (listed cells present)
     f = np.concatenate([inputs.config2_cells(3, 32), inputs.config5_cells(3, 32, columns=[300, 400, 511])])
