@@ -105,11 +105,31 @@ __global__ void __launch_bounds__(256) nyq_planes_kernel(const int64_t* __restri
         const int64_t cell = list[it];
         const double2* Fc = nyqF + cell * 3 * NN;
         __syncthreads();  // previous item's planes written out
-        for (int i = t; i < 3 * NN; i += blockDim.x) {
-            const int64_t toff = (int64_t)d * 3 * NN + i;
-            const double a = __ldg(ta + toff), b = __ldg(tap + toff);
-            const double2 F = Fc[i];
-            sm[(i / NN) * PLANE + ((i % NN) / N) * ROW + (i % N)] = make_double2(a * F.x - b * F.y, a * F.y + b * F.x);
+        // the restricted product (alpha_a + i alpha'_a) F on the three planes; the loads
+        // of a batch of KB entries per thread are issued together (one L2 round trip per
+        // batch instead of one per entry: 22.7 -> ~5 us per item at N = 32)
+        constexpr int KB = 12;
+        const double* ta_d = ta + (int64_t)d * 3 * NN;
+        const double* tap_d = tap + (int64_t)d * 3 * NN;
+        for (int i0 = 0; i0 < 3 * NN; i0 += KB * 256) {
+            double av[KB], bv[KB];
+            double2 Fv[KB];
+#pragma unroll
+            for (int k = 0; k < KB; ++k) {
+                const int i = i0 + k * 256 + t;
+                if (i < 3 * NN) {
+                    av[k] = __ldg(ta_d + i);
+                    bv[k] = __ldg(tap_d + i);
+                    Fv[k] = Fc[i];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KB; ++k) {
+                const int i = i0 + k * 256 + t;
+                if (i < 3 * NN)
+                    sm[(i / NN) * PLANE + ((i % NN) / N) * ROW + (i % N)] =
+                        make_double2(av[k] * Fv[k].x - bv[k] * Fv[k].y, av[k] * Fv[k].y + bv[k] * Fv[k].x);
+            }
         }
         __syncthreads();
         smem_fft_pass<N>(sm, 3 * N, ROW, 1);             // rows of the three planes
@@ -135,6 +155,9 @@ __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __rest
     extern __shared__ __align__(16) double2 sm[];
     double* red = reinterpret_cast<double*>(sm + 2 * STAGE);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    static_assert(256 % N == 0 && T % 2 == 0, "pair layout: j2 = t / N + (256 / N) m");
+    const int j2_0 = t / N, j3 = t % N;
+    const double s2 = (j2_0 & 1) ? -1.0 : 1.0, s3 = (j3 & 1) ? -1.0 : 1.0, tau = s2 * s3;
     int64_t avail = (int64_t)*count - chunk0;
     if (avail > chunk_n) avail = chunk_n;
     for (int64_t wi = blockIdx.x; wi < avail * SLABS; wi += gridDim.x) {
@@ -167,18 +190,26 @@ __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __rest
             const double2* P1 = P0 + NN;
             const double2* P2 = P1 + T * N;
             const double mu = (d == 0) ? mult0 : 1.0;
+            // A B with A = s1 z0.y + s2 z1.y + s3 z2.y (B: the .x parts) equals A' B' with
+            // A' = s1 (s2 z0.y) + z1.y + (s2 s3) z2.y: s2 = (-1)^j2 and s3 = (-1)^j3 are fixed
+            // per thread (j2 = t / N + 256 m / N, j3 = t % N), s1 = (-1)^j1 per plane tt.
+            // z1 depends on (tt, j3) only: one load per plane for all MP pairs.
+            double2 z0[MP];
 #pragma unroll
             for (int m = 0; m < MP; ++m) {
-                const int p = t + 256 * m, j2 = p / N, j3 = p % N;
-                const double2 z0 = P0[p];
-                const double s2 = (j2 & 1) ? -1.0 : 1.0, s3 = (j3 & 1) ? -1.0 : 1.0;
+                const double2 v = P0[t + 256 * m];
+                z0[m] = make_double2(s2 * v.x, s2 * v.y);
+            }
 #pragma unroll
-                for (int tt = 0; tt < T; ++tt) {
-                    const double s1 = ((j1_0 + tt) & 1) ? -1.0 : 1.0;
-                    const double2 z1 = P1[tt * N + j3], z2 = P2[tt * N + j2];
-                    const double A = s1 * z0.y + s2 * z1.y + s3 * z2.y;
-                    const double B = s1 * z0.x + s2 * z1.x + s3 * z2.x;  // = -hb_i
-                    acc[m * T + tt] += mu * (A * B);                     // = -m ga_i hb_i
+            for (int tt = 0; tt < T; ++tt) {
+                const double2 z1 = P1[tt * N + j3];
+#pragma unroll
+                for (int m = 0; m < MP; ++m) {
+                    const double2 z2 = P2[tt * N + j2_0 + (256 / N) * m];
+                    const bool odd = ((j1_0 + tt) & 1) != 0;  // j1_0 is even: compile-time per tt
+                    const double A = fma(tau, z2.y, odd ? z1.y - z0[m].y : z1.y + z0[m].y);
+                    const double B = fma(tau, z2.x, odd ? z1.x - z0[m].x : z1.x + z0[m].x);  // = -hb_i
+                    acc[m * T + tt] = fma(mu * A, B, acc[m * T + tt]);                   // += -m ga_i hb_i
                 }
             }
         }
