@@ -264,6 +264,7 @@ static int finish_kernel(hk_ctx ctx, hk_kernel k, double* ra, double* rap, doubl
 }
 
 int hk_kernel_create(hk_ctx ctx, int n, int a1, int a2, double vmax, double r_phys, hk_kernel* out) {
+    HK_RANGE("hk_kernel_create");
     hk_kernel k;
     int st = kernel_common(ctx, n, a1, a2, vmax, r_phys, &k);
     if (st) return st;
@@ -347,6 +348,7 @@ static int strict_verdict(hk_ctx ctx, const hk_cell_status* st_host, int64_t nce
 
 int hk_collision_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* q_dev, int64_t ncells,
                        uint32_t flags, hk_cell_status* st_dev) {
+    HK_RANGE("hk_collision_batch");
     if (!ctx || !k) return HK_CONTRACT;
     if (ncells < 0) return fail(ctx, HK_CONTRACT, "negative cell count");
     cudaSetDevice(ctx->device);
@@ -566,6 +568,7 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
 
 int hk_collision_batch_host(hk_ctx ctx, hk_kernel k, const double* f_host, double* q_host,
                             int64_t ncells, uint32_t flags, hk_cell_status* st_host) {
+    HK_RANGE("hk_collision_batch_host");
     if (!ctx || !k) return HK_CONTRACT;
     if (ncells <= 0) return HK_OK;
     cudaSetDevice(ctx->device);

@@ -105,6 +105,7 @@ int hk_ctx_comm_init(hk_ctx ctx, int nranks, int rank, const void* id) {
 
 int hk_halo_exchange(hk_ctx ctx, int n, const double* f_dev, int64_t nx_local, int64_t ny, double* left_dev,
                      double* right_dev) {
+    HK_RANGE("hk_halo_exchange");
     if (!ctx->comm) return fail(ctx, HK_CONTRACT, "hk_halo_exchange: context has no communicator (hk_ctx_comm_init)");
     if (n < 2 || nx_local < 2 || ny < 1 || !f_dev || !left_dev || !right_dev)
         return fail(ctx, HK_CONTRACT, "hk_halo_exchange: need nx_local >= 2 columns and non-null buffers");
@@ -132,6 +133,7 @@ int hk_halo_exchange(hk_ctx ctx, int n, const double* f_dev, int64_t nx_local, i
 }
 
 int hk_allreduce_scalars(hk_ctx ctx, double* buf_dev, int64_t count, int op) {
+    HK_RANGE("hk_allreduce_scalars");
     if (!ctx->comm) return fail(ctx, HK_CONTRACT, "hk_allreduce_scalars: context has no communicator");
     if (count < 0 || (count > 0 && !buf_dev)) return fail(ctx, HK_CONTRACT, "hk_allreduce_scalars: bad buffer");
     if (op != HK_REDUCE_SUM && op != HK_REDUCE_MAX) return fail(ctx, HK_CONTRACT, "hk_allreduce_scalars: op must be SUM or MAX");

@@ -230,6 +230,7 @@ int hk_euler_rhs_periodic(hk_ctx ctx, const double* u_dev, int nx, int ny, doubl
 
 int hk_euler_tvd_rk2_step(hk_ctx ctx, double* u_dev, int nx, int ny, double dx, double dy, double dt, double xi,
                           double eps_weno, double* work_dev) {
+    HK_RANGE("hk_euler_tvd_rk2_step");
     if (nx < 1 || ny < 1) return fail(ctx, HK_CONTRACT, "euler: empty grid");
     cudaSetDevice(ctx->device);
     const int64_t n4 = 4LL * nx * ny;

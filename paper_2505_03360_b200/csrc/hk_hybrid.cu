@@ -334,6 +334,7 @@ using namespace hk;
 extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx, double dy, double dt,
                               const double* eps_dev, int8_t* r_dev, double* hydro_dev, double* f_dev,
                               const hk_hybrid_params* p, int64_t* counts) {
+    HK_RANGE("hk_hybrid_step");
     if (!ctx || !k || !p) return HK_CONTRACT;
     if (nx < 1 || ny < 1) return fail(ctx, HK_CONTRACT, "hybrid step: empty grid");
     // every argument check precedes the first launch: a rejected call leaves the state untouched

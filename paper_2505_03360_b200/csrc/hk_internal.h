@@ -11,6 +11,17 @@
 
 #include "../../include/hykin_b200.h"
 
+// NVTX range over a C-ABI entry point (header-only NVTX 3; no cost unless a
+// profiler attaches): nsys / ncu --nvtx show the library's calls by name.
+#include <nvtx3/nvToolsExt.h>
+struct HkRange {
+    explicit HkRange(const char* name) { nvtxRangePushA(name); }
+    ~HkRange() { nvtxRangePop(); }
+    HkRange(const HkRange&) = delete;
+    HkRange& operator=(const HkRange&) = delete;
+};
+#define HK_RANGE(name) HkRange hk_range_scope_(name)
+
 struct hk_ctx_s {
     int device = 0;
     cudaStream_t stream = nullptr;

@@ -194,6 +194,7 @@ int hk_classify_cells(hk_ctx ctx, int64_t nx, int64_t ny, const hk_obstacle_spec
 int hk_apply_obstacle(hk_ctx ctx, int n, double vmax, hk_obstacle_spec* spec, int64_t nx, int64_t ny, int8_t* r_dev,
                       uint8_t* kind_dev, double* hydro_dev, double* f_dev, double heat_ratio, int* covered,
                       int* vacated) {
+    HK_RANGE("hk_apply_obstacle");
     if (covered) *covered = 0;
     if (vacated) *vacated = 0;
     int st = check_spec(ctx, spec, nx, ny, "apply_obstacle");

@@ -46,6 +46,7 @@ extern "C" int hk_write_snapshot(hk_ctx ctx, int n, double vmax, int64_t nx, int
                                  const int8_t* r_dev, const uint8_t* kind_dev, const double* hydro_dev,
                                  const double* f_dev, double heat_ratio, int64_t step, double time, const char* dir,
                                  const char* config_json) {
+    HK_RANGE("hk_write_snapshot");
     if (!ctx || !r_dev || !hydro_dev || !f_dev || !dir) return HK_CONTRACT;
     if (nx < 1 || ny < 1) return fail(ctx, HK_CONTRACT, "write_snapshot: empty grid");
     cudaSetDevice(ctx->device);

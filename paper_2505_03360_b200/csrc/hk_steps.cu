@@ -112,30 +112,35 @@ extern "C" {
 
 int hk_moments_batch(hk_ctx ctx, int n, double vmax, const double* f_dev, int64_t ncells, double* mom_dev,
                      double* sigma_dev, double* real_dev, double* l1_dev, int* status_dev) {
+    HK_RANGE("hk_moments_batch");
     cudaSetDevice(ctx->device);
     return moments_launch(ctx, n, vmax, f_dev, ncells, mom_dev, sigma_dev, real_dev, l1_dev, status_dev);
 }
 
 int hk_maxwellian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, int64_t ncells, double* out_dev,
                         int* status_dev) {
+    HK_RANGE("hk_maxwellian_batch");
     cudaSetDevice(ctx->device);
     return maxwellian_launch(ctx, n, vmax, mom_dev, ncells, out_dev, status_dev);
 }
 
 int hk_anisotropic_gaussian_batch(hk_ctx ctx, int n, double vmax, const double* mom_dev, const double* theta_dev,
                                   double beta, int64_t ncells, double* out_dev, int* fallback_dev) {
+    HK_RANGE("hk_anisotropic_gaussian_batch");
     cudaSetDevice(ctx->device);
     return gaussian_launch(ctx, n, vmax, mom_dev, theta_dev, beta, ncells, out_dev, fallback_dev);
 }
 
 int hk_match_moments_batch(hk_ctx ctx, int n, double vmax, double* f_dev, const double* target_dev, int64_t ncells,
                            int* status_dev) {
+    HK_RANGE("hk_match_moments_batch");
     cudaSetDevice(ctx->device);
     return match_launch(ctx, n, vmax, f_dev, target_dev, ncells, status_dev);
 }
 
 int hk_remove_invariant_moments_batch(hk_ctx ctx, int n, double vmax, double* q_dev, const double* weight_dev,
                                       const double* uc_dev, int64_t ncells, int* status_dev) {
+    HK_RANGE("hk_remove_invariant_moments_batch");
     cudaSetDevice(ctx->device);
     return remove_invariants_launch(ctx, n, vmax, q_dev, weight_dev, uc_dev, ncells, status_dev);
 }
@@ -143,6 +148,7 @@ int hk_remove_invariant_moments_batch(hk_ctx ctx, int n, double vmax, double* q_
 int hk_esbgk_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_dev, double* out_dev, int64_t ncells,
                          double a, const double* eps_dev, double eps, double beta, double nu_coeff, int* info_dev,
                          double* mom_dev) {
+    HK_RANGE("hk_esbgk_stage_batch");
     cudaSetDevice(ctx->device);
     return stage_launch(ctx, true, n, vmax, f_star_dev, out_dev, ncells, a, eps_dev, eps, beta, nu_coeff, info_dev,
                         mom_dev);
@@ -151,6 +157,7 @@ int hk_esbgk_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_de
 int hk_penalized_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_star_dev, double* out_dev,
                              int64_t ncells, double a, const double* eps_dev, double eps, double pen_coeff,
                              int* info_dev, double* mom_dev) {
+    HK_RANGE("hk_penalized_stage_batch");
     cudaSetDevice(ctx->device);
     return stage_launch(ctx, false, n, vmax, f_star_dev, out_dev, ncells, a, eps_dev, eps, 0.0, pen_coeff, info_dev,
                         mom_dev);
@@ -158,6 +165,7 @@ int hk_penalized_stage_batch(hk_ctx ctx, int n, double vmax, const double* f_sta
 
 int hk_penalized_residual_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, double* out_dev, int64_t ncells,
                                 double pen_coeff, uint32_t flags, int* status_dev, hk_cell_status* st_dev) {
+    HK_RANGE("hk_penalized_residual_batch");
     cudaSetDevice(ctx->device);
     int st = hk_collision_batch(ctx, k, f_dev, out_dev, ncells, flags & ~HK_COLL_STRICT, st_dev);
     if (st) return st;
@@ -167,6 +175,7 @@ int hk_penalized_residual_batch(hk_ctx ctx, hk_kernel k, const double* f_dev, do
 int hk_classify(hk_ctx ctx, int nx, int ny, double dx, double dy, const double* mom_dev, const double* eps_dev,
                 const double* l1_dev, const int8_t* r_in_dev, int8_t* r_out_dev, double* ind_dev, int* status_dev,
                 double eta0, double eta1, double delta0, double mu0, double kappa0, int signed_sum) {
+    HK_RANGE("hk_classify");
     cudaSetDevice(ctx->device);
     if (!(eta0 > 0.0) || !(eta1 > 0.0) || !(delta0 > 0.0))  // Thresholds::validate (src/indicators.cpp:9-12)
         return fail(ctx, HK_CONFIG, "regime thresholds eta0, eta1, delta0 must be positive");
@@ -176,6 +185,7 @@ int hk_classify(hk_ctx ctx, int nx, int ny, double dx, double dy, const double* 
 
 int hk_transport_rhs(hk_ctx ctx, int n, double vmax, const double* f_dev, double* out_dev, int nx, int ny,
                      int x_halo, double dx, double dy, double eps_weno) {
+    HK_RANGE("hk_transport_rhs");
     cudaSetDevice(ctx->device);
     TransportParams p{n, vmax, nx, ny, x_halo, dx, dy, eps_weno};
     return transport_launch(ctx, p, f_dev, out_dev);
@@ -341,6 +351,7 @@ static int imex_step(hk_ctx ctx, hk_kernel k, bool boltz, int n, double vmax, do
 
 int hk_esbgk_imex_step(hk_ctx ctx, int n, double vmax, double* f_dev, int nx, int ny, double dx, double dy, double dt,
                        const double* eps_dev, double beta, double nu_coeff, double eps_weno, double* work_dev) {
+    HK_RANGE("hk_esbgk_imex_step");
     return imex_step(ctx, nullptr, false, n, vmax, f_dev, nx, ny, dx, dy, dt, eps_dev, beta, nu_coeff, eps_weno, 0,
                      work_dev);
 }
@@ -348,6 +359,7 @@ int hk_esbgk_imex_step(hk_ctx ctx, int n, double vmax, double* f_dev, int nx, in
 int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int ny, double dx, double dy, double dt,
                            const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
                            double* work_dev) {
+    HK_RANGE("hk_penalized_imex_step");
     return imex_step(ctx, k, true, k->n, k->vmax, f_dev, nx, ny, dx, dy, dt, eps_dev, 0.0, pen_coeff, eps_weno, flags,
                      work_dev);
 }
@@ -355,6 +367,7 @@ int hk_penalized_imex_step(hk_ctx ctx, hk_kernel k, double* f_dev, int nx, int n
 int hk_transport_rhs_peer(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_slab_dev,
                           int left_nx, const double* right_slab_dev, int right_nx, double* out_dev, int nx, int ny,
                           double dx, double dy, double eps_weno) {
+    HK_RANGE("hk_transport_rhs_peer");
     if (left_nx < 2 || right_nx < 2 || !left_slab_dev || !right_slab_dev)
         return fail(ctx, HK_CONTRACT, "transport_rhs_peer: neighbour slabs need >= 2 columns");
     cudaSetDevice(ctx->device);
@@ -367,6 +380,7 @@ int hk_transport_rhs_peer(hk_ctx ctx, int n, double vmax, const double* f_dev, c
 int hk_transport_rhs_slab(hk_ctx ctx, int n, double vmax, const double* f_dev, const double* left_dev,
                           const double* right_dev, double* out_dev, int nx, int ny, double dx, double dy,
                           double eps_weno) {
+    HK_RANGE("hk_transport_rhs_slab");
     cudaSetDevice(ctx->device);
     TransportParams p{n, vmax, nx, ny, -2, dx, dy, eps_weno};
     return transport_launch(ctx, p, f_dev, out_dev, left_dev, right_dev);
@@ -392,6 +406,7 @@ extern "C" {
 int hk_penalized_imex_step_slab(hk_ctx ctx, hk_kernel k, double* f_dev, int nx_local, int ny, double dx, double dy,
                                 double dt, const double* eps_dev, double pen_coeff, double eps_weno, uint32_t flags,
                                 double* work_dev) {
+    HK_RANGE("hk_penalized_imex_step_slab");
     if (!ctx || !k) return HK_CONTRACT;
     if (nx_local < 2 || ny < 1) return fail(ctx, HK_CONTRACT, "slab step: need nx_local >= 2 columns");
     return imex_step(ctx, k, true, k->n, k->vmax, f_dev, nx_local, ny, dx, dy, dt, eps_dev, 0.0, pen_coeff, eps_weno,
@@ -401,6 +416,7 @@ int hk_penalized_imex_step_slab(hk_ctx ctx, hk_kernel k, double* f_dev, int nx_l
 int hk_esbgk_imex_step_slab(hk_ctx ctx, int n, double vmax, double* f_dev, int nx_local, int ny, double dx, double dy,
                             double dt, const double* eps_dev, double beta, double nu_coeff, double eps_weno,
                             double* work_dev) {
+    HK_RANGE("hk_esbgk_imex_step_slab");
     if (!ctx) return HK_CONTRACT;
     if (nx_local < 2 || ny < 1) return fail(ctx, HK_CONTRACT, "slab step: need nx_local >= 2 columns");
     return imex_step(ctx, nullptr, false, n, vmax, f_dev, nx_local, ny, dx, dy, dt, eps_dev, beta, nu_coeff, eps_weno, 0,

@@ -262,6 +262,7 @@ int hk_synthesize_distributions(hk_ctx ctx, int n, double vmax, int64_t nx, int6
                                 const int8_t* r_dev, const uint8_t* kind_dev, const double* hydro_dev, double* f_dev,
                                 double heat_ratio, const int64_t* idx_dev, int64_t count, double* out_dev,
                                 int64_t* filled) {
+    HK_RANGE("hk_synthesize_distributions");
     if (filled) *filled = 0;
     int st = check_args(ctx, n, nx, ny, "synthesize_distribution");
     if (st) return st;
