@@ -1124,7 +1124,9 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
 struct Geo16 {
     static constexpr int N = 16, R = 17, PL = N * R, BUF = N * PL;  // padded [k1][k2][k3]
     static constexpr int NT = 256;
-    static constexpr size_t SMEM = size_t(3 * BUF) * sizeof(double2) + 32 * sizeof(double);
+    static constexpr uint32_t TM_COLS = 128;  // F pencils: 64 columns per thread, warps w and w + 4 share lanes
+    // B0, B1 (padded fields) + the item's two weight rows (TMA) + reductions
+    static constexpr size_t SMEM = size_t(2 * BUF) * sizeof(double2) + size_t(2 * N * N * N + 32) * sizeof(double);
     static constexpr size_t SLOT = size_t(N) * N * N * sizeof(double2);  // one partial-sum slot
 };
 
@@ -1136,14 +1138,27 @@ __device__ __forceinline__ int64_t item_owner(int64_t i, int64_t T, int64_t G) {
 __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
     using G = Geo16;
     constexpr int N = 16, NB = 4096;
-    extern __shared__ __align__(16) double2 smem[];
-    double2* const Fs = smem;
-    double2* const B0 = smem + G::BUF;      // alpha F  -> ga (and the loss field)
-    double2* const B1 = smem + 2 * G::BUF;  // alpha' F -> gb
-    double* const red = reinterpret_cast<double*>(smem + 3 * G::BUF);
+    extern __shared__ __align__(128) double2 smem[];
+    double2* const B0 = smem;               // alpha F  -> ga (and the loss field); the forward transform's workspace
+    double2* const B1 = smem + G::BUF;      // alpha' F -> gb
+    double* const W0 = reinterpret_cast<double*>(smem + 2 * G::BUF);  // the item's alpha (or loss) row, [i1][i3][i2]
+    double* const W1 = W0 + NB;                                        // the item's alpha' row
+    double* const red = W1 + NB;
     __shared__ int last_flag;
+    __shared__ __align__(8) uint64_t wbar;
+    __shared__ uint32_t tslot;
     const int t = threadIdx.x, ph = t >> 4, pl = t & 15;
     const int warp = t >> 5, lane = t & 31;
+    const uint32_t wbar_s = smem_u32(&wbar);
+    if (warp == 0) tmem_alloc(&tslot, G::TM_COLS);
+    if (t == 0) {
+        mbar_init(wbar_s, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+    const uint32_t tF = tslot + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);  // F pencil (ph, pl)
     const int64_t count = a.list_count ? (int64_t)*a.list_count : a.ncells;
     // units: the two fixed halves of a cell's items, [0, H) and [H, P) (the loss item last)
     const int P = a.md + 1, H = (P + 1) / 2;
@@ -1153,6 +1168,21 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
         return a.xchg + (3 * kc + (u == kc * T / NG ? 0 : 1)) * (int64_t)NB;
     };
     double2* const park = a.xchg + (3 * k + 2) * (int64_t)NB;  // a whole cell's first half while its second runs
+    // The two weight rows of an item arrive by TMA bulk copies (thread 0) while the
+    // previous item's k2 / k1 passes run: no L2 latency at the start of a k3 pass.
+    auto issue_w = [&](int q) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // earlier generic reads of W0 / W1
+        if (q < a.md) {
+            mbar_arrive_expect_tx(wbar_s, 2u * NB * sizeof(double));
+            bulk_g2s(smem_u32(W0), a.alpha + (int64_t)q * NB, NB * sizeof(double), wbar_s);
+            bulk_g2s(smem_u32(W1), a.alpha_p + (int64_t)q * NB, NB * sizeof(double), wbar_s);
+        } else {
+            mbar_arrive_expect_tx(wbar_s, NB * sizeof(double));
+            bulk_g2s(smem_u32(W0), a.loss, NB * sizeof(double), wbar_s);
+        }
+    };
+    unsigned wphase = 0;
+    if (t == 0 && u0 < u1) issue_w((u0 & 1) ? H : 0);
 
     // Q = jac Re(acc) on this thread's nodes (k1, (k2, k3) = t), status of the cell
     auto finish = [&](int64_t cell, const double2 (&acc)[N]) {
@@ -1204,13 +1234,13 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
         const int half = int(u & 1), qa = half ? H : 0, qb = half ? P : H;  // items [qa, qb) of cell c
         const int64_t cell = a.list ? a.list[c] : c;
         const double* fc = a.f + cell * NB;
-        if (c != cur) {  // ---- F = FFT(f) / N^3 into Fs, k3 then k2 then k1 ----
+        if (c != cur) {  // ---- F = FFT(f) / N^3 in B0 (k3, k2, k1), then pencil (ph, pl) -> TMEM ----
             cur = c;
             for (int kk = t; kk < NB; kk += G::NT)
-                Fs[i16(kk >> 8, (kk >> 4) & 15, kk & 15)] = make_double2(__ldg(fc + kk), 0.0);
+                B0[i16(kk >> 8, (kk >> 4) & 15, kk & 15)] = make_double2(__ldg(fc + kk), 0.0);
             __syncthreads();
             for (int pass = 0; pass < 3; ++pass) {
-                double2* base = pass == 0 ? Fs + i16(ph, pl, 0) : (pass == 1 ? Fs + i16(ph, 0, pl) : Fs + i16(0, ph, pl));
+                double2* base = pass == 0 ? B0 + i16(ph, pl, 0) : (pass == 1 ? B0 + i16(ph, 0, pl) : B0 + i16(0, ph, pl));
                 const int st = pass == 0 ? 1 : (pass == 1 ? G::R : G::PL);
                 double2 x[N];
 #pragma unroll
@@ -1221,6 +1251,21 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
                 for (int j = 0; j < N; ++j) base[j * st] = make_double2(x[j].x * sc, x[j].y * sc);
                 __syncthreads();
             }
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                double v[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const double2 F = B0[i16(ph, pl, 4 * ch + i)];
+                    v[2 * i] = F.x;
+                    v[2 * i + 1] = F.y;
+                }
+                tmem_st16(tF + 16 * ch, v);
+            }
+            tmem_wait_st();
+            tmem_fence_before();
+            __syncthreads();  // B0 is free for the first item's k3 pass
+            tmem_fence_after();
         }
         double2 acc[N];
 #pragma unroll
@@ -1228,19 +1273,25 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
         for (int q = qa; q < qb; ++q) {
             const bool loss = q == a.md;  // CTA-uniform
             double2 xa[N], xb[N];
-            {  // k3 pass with the weights: pencil (k1, k2) = (ph, pl)
-                const int64_t off = (int64_t)q * NB + ph * 256 + pl;  // [i1][i3][i2]
-                const double* wa = loss ? a.loss + ph * 256 + pl : a.alpha + off;
-                const double* wb = a.alpha_p + off;
-                const double2* fr = Fs + i16(ph, pl, 0);
+            {  // k3 pass with the weights: pencil (k1, k2) = (ph, pl), F from TMEM, weights from SMEM
+                mbar_wait_parity(wbar_s, wphase);
+                wphase ^= 1;
+                const double* wa = W0 + ph * 256 + pl;  // [i1][i3][i2]
+                const double* wb = W1 + ph * 256 + pl;
 #pragma unroll
-                for (int j = 0; j < N; ++j) {
-                    const double2 F = fr[j];
-                    const double w0 = __ldg(wa + j * N);
-                    xa[j] = make_double2(F.x * w0, F.y * w0);
-                    if (!loss) {
-                        const double w1 = __ldg(wb + j * N);
-                        xb[j] = make_double2(F.x * w1, F.y * w1);
+                for (int ch = 0; ch < 4; ++ch) {
+                    double v[8];
+                    tmem_ld16(tF + 16 * ch, v);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int j = 4 * ch + i;
+                        const double2 F = make_double2(v[2 * i], v[2 * i + 1]);
+                        const double w0 = wa[j * N];
+                        xa[j] = make_double2(F.x * w0, F.y * w0);
+                        if (!loss) {
+                            const double w1 = wb[j * N];
+                            xb[j] = make_double2(F.x * w1, F.y * w1);
+                        }
                     }
                 }
                 fft_fma<N, true>(xa);
@@ -1255,6 +1306,10 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
                 }
             }
             __syncthreads();
+            if (t == 0) {  // W0 / W1 are free: the next item's rows (this unit's, or the next unit's first)
+                if (q + 1 < qb) issue_w(q + 1);
+                else if (u + 1 < u1) issue_w(((u + 1) & 1) ? H : 0);
+            }
             {  // k2 pass: pencil (k1, k3) = (ph, pl)
                 double2* oa = B0 + i16(ph, 0, pl);
                 double2* ob = B1 + i16(ph, 0, pl);
@@ -1348,6 +1403,9 @@ __global__ void __launch_bounds__(256, 1) coll16_exact_kernel(CollArgs a) {
             }
         }
     }
+    tmem_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tslot, G::TM_COLS);
 }
 
 size_t coll16_xchg_bytes(hk_ctx ctx) { return size_t(3) * ctx->sm_count * Geo16::SLOT; }
