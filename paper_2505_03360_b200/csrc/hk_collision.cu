@@ -1107,9 +1107,11 @@ int launch_fast_pipe(hk_ctx ctx, const CollArgs& args_in, int64_t max_cells, int
 // distinct directions, then the loss field) in two FIXED halves, U0 = w gain
 // over items [0, H) and U1 = w gain - f loss over [H, md + 1); the batch's
 // halves are split evenly over one persistent 256-thread CTA per SM (config 1:
-// 128 halves on 128 SMs).  Per cell the CTA transforms F = FFT(f)/N^3 into
-// shared memory once; per item thread p owns pencil p of BOTH fields
-// (alpha F, alpha' F): the k3 pass reads F once and applies both weight rows,
+// 128 halves on 128 SMs).  Per cell the CTA transforms F = FFT(f)/N^3 once
+// and parks each thread's pencil in TMEM; an item's two weight rows arrive by
+// TMA bulk copies while the previous item's k2 / k1 passes run.  Per item
+// thread p owns pencil p of BOTH fields (alpha F, alpha' F): the k3 pass takes
+// F from TMEM and applies both weight rows,
 // the k2 and k1 passes run in place (two independent 16-point transforms per
 // thread, the register file's ILP instead of more warps), and after the k1
 // pass the thread holds ga and gb on its 16 nodes and accumulates the complex
