@@ -378,6 +378,18 @@ typedef struct {
 } hk_hybrid_params;
 int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx, double dy, double dt, const double* eps_dev,
                    int8_t* r_dev, double* hydro_dev, double* f_dev, const hk_hybrid_params* params, int64_t* counts);
+/* hk_hybrid_step on one x-slab of a grid split over the ranks of the context's
+ * communicator (hk_ctx_comm_init; without one the slab is its own periodic
+ * neighbour): fields [ny][nx_local] (cell j nx_local + i), in place.  One
+ * exchange of `ghost` columns of (r, eps, hydro, f) per side (NCCL send/recv
+ * into a padded copy), the step on the padded local torus with ghost_x = ghost,
+ * the interior copied back: with ghost >= 7 (the step's x-dependency radius)
+ * the interior equals the global step's.  counts (nullable) receives the
+ * global layer counts [n0, n1, n2] after the step (all-reduced).  The host
+ * logic of partition.hybrid_step_slab, in C++. */
+int hk_hybrid_step_slab(hk_ctx ctx, hk_kernel k, int nx_local, int ny, double dx, double dy, double dt,
+                        const double* eps_dev, int8_t* r_dev, double* hydro_dev, double* f_dev,
+                        const hk_hybrid_params* params, int ghost, int64_t* counts);
 
 /* write_snapshot (src/snapshot.cpp is listed by the reference's
  * CMake but not shipped): in directory `dir`, moments_<step>.csv (i,j,x,y,rho,ux,uy,T,P,

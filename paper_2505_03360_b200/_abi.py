@@ -168,6 +168,8 @@ def lib() -> C.CDLL:
                                         C.c_char_p, C.c_char_p]),
         "hk_hybrid_step": (C.c_int, [vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, vp, vp, vp, C.POINTER(HybridParams),
                                      C.POINTER(C.c_int64)]),
+        "hk_hybrid_step_slab": (C.c_int, [vp, vp, C.c_int, C.c_int, dbl, dbl, dbl, vp, vp, vp, vp,
+                                          C.POINTER(HybridParams), C.c_int, C.POINTER(C.c_int64)]),
         "hk_apply_obstacle": (C.c_int, [vp, C.c_int, dbl, C.POINTER(ObstacleSpec), i64, i64, vp, vp, vp, vp, dbl,
                                         C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     }

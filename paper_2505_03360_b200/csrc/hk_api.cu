@@ -96,6 +96,7 @@ int hk_ctx_destroy(hk_ctx ctx) {
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->fix_scratch) cudaFree(ctx->fix_scratch);
     if (ctx->c16_ctr) cudaFree(ctx->c16_ctr);
+    if (ctx->slab_pad) cudaFree(ctx->slab_pad);
     if (ctx->step_work) cudaFree(ctx->step_work);
     if (ctx->hyb_small) cudaFree(ctx->hyb_small);
     if (ctx->hyb_big) cudaFree(ctx->hyb_big);
@@ -118,10 +119,11 @@ int hk_ctx_trim(hk_ctx ctx) {
     else cudaDeviceSynchronize();
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-    void** bufs[] = {&ctx->scratch, &ctx->fix_scratch, &ctx->step_work, &ctx->hyb_small, &ctx->hyb_big, &ctx->halo_work};
+    void** bufs[] = {&ctx->scratch, &ctx->fix_scratch, &ctx->step_work, &ctx->hyb_small, &ctx->hyb_big, &ctx->halo_work,
+                     &ctx->slab_pad};
     size_t* sizes[] = {&ctx->scratch_bytes, &ctx->fix_bytes, &ctx->step_bytes, &ctx->hyb_small_bytes, &ctx->hyb_big_bytes,
-                       &ctx->halo_bytes};
-    for (int i = 0; i < 6; ++i) {
+                       &ctx->halo_bytes, &ctx->slab_pad_bytes};
+    for (int i = 0; i < 7; ++i) {
         if (*bufs[i]) cudaFree(*bufs[i]);
         *bufs[i] = nullptr;
         *sizes[i] = 0;

@@ -72,6 +72,37 @@ void comm_destroy(hk_ctx ctx) {
     if (ctx) ctx->comm = nullptr;
 }
 
+int halo_columns_padded(hk_ctx ctx, const void* src, size_t cb, int64_t nx, int64_t ny, int w, void* pad) {
+    const char* s = static_cast<const char*>(src);
+    char* d = static_cast<char*>(pad);
+    const size_t row = size_t(nx) * cb, prow = size_t(nx + 2 * w) * cb, wb = size_t(w) * cb;
+    if (!ctx->comm || ctx->nranks < 2) {  // the slab is its own periodic neighbour
+        int st = check_cuda(ctx, cudaMemcpy2DAsync(d, prow, s + row - wb, row, wb, ny, cudaMemcpyDeviceToDevice, ctx->stream),
+                            "slab halo copy");
+        if (!st)
+            st = check_cuda(ctx, cudaMemcpy2DAsync(d + wb + row, prow, s, row, wb, ny, cudaMemcpyDeviceToDevice, ctx->stream),
+                            "slab halo copy");
+        return st;
+    }
+    if (!nccl().loaded) return fail(ctx, HK_NCCL, "libnccl.so.2 not found");
+    const int left = (ctx->rank - 1 + ctx->nranks) % ctx->nranks, right = (ctx->rank + 1) % ctx->nranks;
+    auto comm = static_cast<ncclComm_t>(ctx->comm);
+    auto& api = nccl();
+    int st = check_nccl(ctx, api.GroupStart(), "ncclGroupStart");
+    if (st) return st;
+    // same posting order as hk_halo_exchange: to the left, to the right, from the right, from the left
+    for (int64_t j = 0; j < ny && !st; ++j)
+        st = check_nccl(ctx, api.Send(s + j * row, wb, ncclInt8, left, comm, ctx->stream), "ncclSend");
+    for (int64_t j = 0; j < ny && !st; ++j)
+        st = check_nccl(ctx, api.Send(s + j * row + row - wb, wb, ncclInt8, right, comm, ctx->stream), "ncclSend");
+    for (int64_t j = 0; j < ny && !st; ++j)
+        st = check_nccl(ctx, api.Recv(d + j * prow + wb + row, wb, ncclInt8, right, comm, ctx->stream), "ncclRecv");
+    for (int64_t j = 0; j < ny && !st; ++j)
+        st = check_nccl(ctx, api.Recv(d + j * prow, wb, ncclInt8, left, comm, ctx->stream), "ncclRecv");
+    const int st2 = check_nccl(ctx, api.GroupEnd(), "ncclGroupEnd");
+    return st ? st : st2;
+}
+
 }  // namespace hk
 
 using namespace hk;

@@ -538,3 +538,92 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
     }
     return HK_OK;
 }
+
+// ---------------------------------------------------------------------------
+// hk_hybrid_step on one x-slab, host logic in C++ (the C-ABI twin of
+// partition.hybrid_step_slab): one exchange of `ghost` columns of (r, eps,
+// hydro, f) per side straight into a padded [ny][nx_local + 2 ghost] copy of
+// the slab (NCCL send/recv on the context communicator, or the slab's own wrap
+// without one), the step on the padded local torus with ghost_x = ghost (ghost
+// cells get only the residuals an interior cell depends on), the interior
+// copied back, and the layer counts of the interior all-reduced over the
+// communicator.  With ghost >= the step's x-dependency radius (7 cells;
+// partition.HYB_GHOST = 8) the interior equals the global step's.
+// ---------------------------------------------------------------------------
+namespace hk {
+namespace {
+__global__ void layer_count_kernel(int64_t cells, const int8_t* __restrict__ r, double* __restrict__ out) {
+    __shared__ unsigned c[3];
+    if (threadIdx.x < 3) c[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cells; i += (int64_t)gridDim.x * blockDim.x) {
+        const int v = r[i];
+        if (v >= 0 && v <= 2) atomicAdd(&c[v], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3 && c[threadIdx.x]) atomicAdd(out + threadIdx.x, double(c[threadIdx.x]));
+}
+}  // namespace
+}  // namespace hk
+
+extern "C" int hk_hybrid_step_slab(hk_ctx ctx, hk_kernel k, int nx_local, int ny, double dx, double dy, double dt,
+                                   const double* eps_dev, int8_t* r_dev, double* hydro_dev, double* f_dev,
+                                   const hk_hybrid_params* p, int ghost, int64_t* counts) {
+    HK_RANGE("hk_hybrid_step_slab");
+    if (!ctx || !k || !p) return HK_CONTRACT;
+    if (ghost < 1 || nx_local < ghost || ny < 1)
+        return fail(ctx, HK_CONTRACT, "hybrid slab step: need 1 <= ghost <= nx_local and ny >= 1");
+    cudaSetDevice(ctx->device);
+    const int w = ghost, nxp = nx_local + 2 * w;
+    const int64_t nb = (int64_t)k->n * k->n * k->n, cells = (int64_t)nx_local * ny, cp = (int64_t)nxp * ny;
+    // padded workspace: [counts 3][r cp][eps cp][hydro 4 cp][f nb cp], 256-byte aligned pieces
+    auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+    const size_t need = al(3 * sizeof(double)) + al(cp) + al(sizeof(double) * cp) + al(sizeof(double) * 4 * cp) +
+                        al(sizeof(double) * (size_t)nb * cp);
+    int st;
+    if ((st = grow(ctx, &ctx->slab_pad, &ctx->slab_pad_bytes, need, "padded slab", need))) return st;
+    char* q = static_cast<char*>(ctx->slab_pad);
+    double* cnt = carve<double>(q, 3);
+    int8_t* r_p = carve<int8_t>(q, cp);
+    double* e_p = carve<double>(q, cp);
+    double* h_p = carve<double>(q, 4 * cp);
+    double* f_p = carve<double>(q, nb * cp);
+    struct Field {
+        const void* src;
+        void* pad;
+        size_t cb;
+    };
+    const Field fields[4] = {{r_dev, r_p, 1}, {eps_dev, e_p, sizeof(double)}, {hydro_dev, h_p, 4 * sizeof(double)},
+                             {f_dev, f_p, sizeof(double) * (size_t)nb}};
+    cudaStream_t s = ctx->stream;
+    for (const Field& fl : fields) {  // interior, then the ghost columns
+        const size_t row = fl.cb * nx_local, prow = fl.cb * nxp;
+        if ((st = check_cuda(ctx, cudaMemcpy2DAsync(static_cast<char*>(fl.pad) + fl.cb * w, prow, fl.src, row, row, ny,
+                                                    cudaMemcpyDeviceToDevice, s), "slab padding")))
+            return st;
+        if ((st = halo_columns_padded(ctx, fl.src, fl.cb, nx_local, ny, w, fl.pad))) return st;
+    }
+    hk_hybrid_params q2 = *p;
+    q2.ghost_x = w;
+    if ((st = hk_hybrid_step(ctx, k, nxp, ny, dx, dy, dt, e_p, r_p, h_p, f_p, &q2, nullptr))) return st;
+    const Field back[3] = {{r_p, r_dev, 1}, {h_p, hydro_dev, 4 * sizeof(double)}, {f_p, f_dev, sizeof(double) * (size_t)nb}};
+    for (const Field& fl : back) {
+        const size_t row = fl.cb * nx_local, prow = fl.cb * nxp;
+        if ((st = check_cuda(ctx, cudaMemcpy2DAsync(fl.pad, row, static_cast<const char*>(fl.src) + fl.cb * w, prow, row, ny,
+                                                    cudaMemcpyDeviceToDevice, s), "slab unpadding")))
+            return st;
+    }
+    // layer counts of the interior, summed over the ranks
+    cudaMemsetAsync(cnt, 0, 3 * sizeof(double), s);
+    layer_count_kernel<<<unsigned(std::min<int64_t>((cells + 255) / 256, 4LL * ctx->sm_count)), 256, 0, s>>>(cells, r_dev, cnt);
+    ctx->launches++;
+    if ((st = check_cuda(ctx, cudaGetLastError(), "layer counts"))) return st;
+    if (ctx->comm && ctx->nranks > 1 && (st = hk_allreduce_scalars(ctx, cnt, 3, HK_REDUCE_SUM))) return st;
+    double h[3];
+    if ((st = check_cuda(ctx, cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, s), "counts D2H")) ||
+        (st = check_cuda(ctx, cudaStreamSynchronize(s), "counts sync")))
+        return st;
+    if (counts)
+        for (int i = 0; i < 3; ++i) counts[i] = (int64_t)h[i];
+    return HK_OK;
+}

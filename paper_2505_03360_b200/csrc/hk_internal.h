@@ -68,6 +68,9 @@ struct hk_ctx_s {
     void* fix_scratch = nullptr;
     // N = 16 split-cell counters (hk_collision.cu), zeroed once and kept clean by the kernel
     unsigned* c16_ctr = nullptr;
+    // padded x-slab of the native hybrid slab step (hk_hybrid.cu), grow-only
+    void* slab_pad = nullptr;
+    size_t slab_pad_bytes = 0;
     size_t fix_bytes = 0;
     // NCCL communicator (hk_comm.cu; ncclComm_t, loaded at run time)
     void* comm = nullptr;
@@ -122,5 +125,10 @@ double fp64_peak(hk_ctx ctx);
 
 // hk_comm.cu
 void comm_destroy(hk_ctx ctx);
+// Ghost columns of an x-slab field [ny][nx][cb bytes] into the padded copy
+// [ny][nx + 2 w][cb] (columns [0, w) <- the left rank's last w, [w + nx, nx + 2 w)
+// <- the right rank's first w; periodic over ranks), on the context stream: NCCL
+// send/recv with a communicator of > 1 rank, else the slab's own wrap.
+int halo_columns_padded(hk_ctx ctx, const void* src, size_t cb, int64_t nx, int64_t ny, int w, void* pad);
 
 }  // namespace hk

@@ -455,16 +455,9 @@ class HybridCounts(NamedTuple):
     halo_blocks: int  # layer-0 Maxwellian blocks synthesized for the transport stencil
 
 
-def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, dt: float, eps_cell, r, hydro, f,
-                params: HybridParams = HybridParams(), residual_hook=None) -> HybridCounts:
-    """One hybrid step in place on device tensors: r [cells] int8, hydro [cells, 4]
-    conserved, f [cells, n^3] dense, eps_cell [cells].  Algorithm 1 regime update,
-    convert_on_transition, Euler TVD-RK2 on layer 0, PR(2,2,2) ES-BGK / penalized
-    Boltzmann on layers 1 / 2 with the cross-layer transport halo.
-
-    residual_hook(y, res, status): optional evaluator of the layer-2 residuals
-    (hk_hybrid_params.residual_fn): y / res [m2, n^3] and status int32 [m2]
-    device views; called twice per step, also with m2 = 0."""
+def _hybrid_call(kernel: SpectralKernel, nx: int, ny: int, eps_cell, r, hydro, f, params: HybridParams,
+                 residual_hook, call):
+    """Argument checks, the residual hook as a C callback, then call(e, hp) (hk_hybrid_step[_slab])."""
     ctx = kernel.ctx
     cells = nx * ny
     for name, t, dt_, width in (("r", r, torch.int8, 1), ("hydro", hydro, torch.float64, 4),
@@ -476,7 +469,6 @@ def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, 
     e = eps_cell.to(device=f.device, dtype=torch.float64).contiguous()
     if e.numel() != cells:
         raise contract_violation(f"hybrid_step: eps_cell has {e.numel()} elements, expected {cells}")
-    counts = (C.c_int64 * 6)()
     hp = params.to_c()
     errors = []
     if residual_hook is not None:
@@ -498,15 +490,48 @@ def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, 
     if residual_hook is not None:
         gc.disable()  # no collector pause inside the hook while the step's kernels wait on it
     try:
-        st = ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),
-                                     hydro.data_ptr(), f.data_ptr(), C.byref(hp), counts)
+        st = call(e, hp)
     finally:
         if gc_was:
             gc.enable()
     if errors:
         raise errors[0]
     ctx.check(st)
+
+
+def hybrid_step(kernel: SpectralKernel, nx: int, ny: int, dx: float, dy: float, dt: float, eps_cell, r, hydro, f,
+                params: HybridParams = HybridParams(), residual_hook=None) -> HybridCounts:
+    """One hybrid step in place on device tensors: r [cells] int8, hydro [cells, 4]
+    conserved, f [cells, n^3] dense, eps_cell [cells].  Algorithm 1 regime update,
+    convert_on_transition, Euler TVD-RK2 on layer 0, PR(2,2,2) ES-BGK / penalized
+    Boltzmann on layers 1 / 2 with the cross-layer transport halo.
+
+    residual_hook(y, res, status): optional evaluator of the layer-2 residuals
+    (hk_hybrid_params.residual_fn): y / res [m2, n^3] and status int32 [m2]
+    device views; called twice per step, also with m2 = 0."""
+    ctx = kernel.ctx
+    counts = (C.c_int64 * 6)()
+    _hybrid_call(kernel, nx, ny, eps_cell, r, hydro, f, params, residual_hook,
+                 lambda e, hp: ctx._lib.hk_hybrid_step(ctx.h, kernel.h, nx, ny, dx, dy, dt, e.data_ptr(), r.data_ptr(),
+                                                      hydro.data_ptr(), f.data_ptr(), C.byref(hp), counts))
     return HybridCounts(*[int(c) for c in counts])
+
+
+def hybrid_step_slab_native(kernel: SpectralKernel, nx_local: int, ny: int, dx: float, dy: float, dt: float, eps_cell,
+                            r, hydro, f, params: HybridParams = HybridParams(), ghost: int = 8,
+                            residual_hook=None) -> list:
+    """hk_hybrid_step_slab: the x-slab hybrid step with its host logic in C++ (the
+    ghost columns of r, eps, hydro, f exchanged over the context's NCCL
+    communicator into a padded copy, or the slab's own wrap without one; the step
+    on the padded torus; the interior copied back).  Returns the global layer
+    counts [n0, n1, n2] after the step."""
+    ctx = kernel.ctx
+    counts = (C.c_int64 * 3)()
+    _hybrid_call(kernel, nx_local, ny, eps_cell, r, hydro, f, params, residual_hook,
+                 lambda e, hp: ctx._lib.hk_hybrid_step_slab(ctx.h, kernel.h, nx_local, ny, dx, dy, dt, e.data_ptr(),
+                                                           r.data_ptr(), hydro.data_ptr(), f.data_ptr(), C.byref(hp),
+                                                           ghost, counts))
+    return [int(c) for c in counts]
 
 
 # ---- snapshot I/O (SPEC.md:604-613) -----------------------------------------

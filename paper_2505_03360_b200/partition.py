@@ -317,7 +317,7 @@ def hybrid_unpad(part: XSlab, width: int, padded, fields):
 
 def hybrid_step_slab(part: XSlab, kernel, dx: float, dy: float, dt: float, eps_cell: torch.Tensor, r: torch.Tensor,
                      hydro: torch.Tensor, f: torch.Tensor, params=None, group=None, width: int = HYB_GHOST,
-                     halos=None, balance: bool = False, residual_hook=None):
+                     halos=None, balance: bool = False, residual_hook=None, native: bool = False):
     """hk_hybrid_step on one x-slab, in place (r [cells] int8, hydro [cells,4], f [cells,n^3],
     eps [cells]; local cell order j*nxl + i).  One exchange of `width` columns of
     (r, eps, hydro, f) per side, then the step on the padded local torus; the
@@ -331,23 +331,32 @@ def hybrid_step_slab(part: XSlab, kernel, dx: float, dy: float, dt: float, eps_c
     surplus stage values of over-loaded ranks to under-loaded ones, evaluates
     dense batches and returns the results; per-cell operators are
     deterministic, so the step is bitwise the unbalanced one.
-    residual_hook: an explicit hk_hybrid_params.residual_fn (see kinetic.hybrid_step)."""
+    residual_hook: an explicit hk_hybrid_params.residual_fn (see kinetic.hybrid_step).
+    native: the exchange, padding, step and counts in C++ (hk_hybrid_step_slab) over the
+    kernel context's NCCL communicator (hk_ctx_comm_init; a single rank wraps onto
+    itself), bitwise this function's result."""
     import dataclasses
 
-    from .kinetic import HybridParams, hybrid_step, penalized_residual_rows
+    from .kinetic import HybridParams, hybrid_step, hybrid_step_slab_native, penalized_residual_rows
 
     # ghost results are discarded: their residuals only where an interior cell depends on them
     params = dataclasses.replace(params or HybridParams(), ghost_x=width)
     fields = [r.view(-1, 1), eps_cell.to(device=f.device, dtype=torch.float64).view(-1, 1), hydro, f]
+    if balance and residual_hook is None:
+        def residual_hook(y, res, status):
+            balanced_residual(kernel, y, res, status, params.pen_coeff, params.exact, group)
+    if native:
+        if halos is not None:
+            raise ValueError("native: the halos travel over the context's communicator")
+        counts = hybrid_step_slab_native(kernel, part.nxl, part.ny, dx, dy, dt, fields[1].view(-1), r, hydro, f,
+                                         params, ghost=width, residual_hook=residual_hook)
+        return torch.tensor(counts, dtype=torch.float64, device=f.device)
     if halos is None:
         halos = []
         for t in fields:
             lh, rh = part.halo_buffers(t.shape[-1], t, width)
             part.exchange(t, lh, rh, group, width=width)
             halos.append((lh, rh))
-    if balance and residual_hook is None:
-        def residual_hook(y, res, status):
-            balanced_residual(kernel, y, res, status, params.pen_coeff, params.exact, group)
     pr, pe, ph, pf = hybrid_pad(part, width, fields, halos)
     hybrid_step(kernel, part.nxl + 2 * width, part.ny, dx, dy, dt, pe.view(-1), pr.view(-1), ph, pf, params,
                 residual_hook=residual_hook)

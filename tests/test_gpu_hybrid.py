@@ -124,6 +124,22 @@ def test_hybrid_slab_world1_equals_torus(hk):
         assert float((f2 - f)[kin].abs().max()) <= 1e-13 * float(f.abs().max())
 
 
+def test_hybrid_slab_native_is_the_python_slab_step(hk):
+    """hk_hybrid_step_slab (exchange / padding / counts in C++) at world 1 (the slab
+    wraps onto itself) is bitwise partition.hybrid_step_slab's Python host logic."""
+    import torch
+    from paper_2505_03360_b200.partition import XSlab, hybrid_step_slab
+    nx, ny, n = 20, 8, 16
+    kern, dx, dy, dt, (r, h, f, e) = _hybrid_setup(hk, nx, ny, n)
+    r2, h2, f2 = r.clone(), h.clone(), f.clone()
+    part = XSlab(nx, ny, 1, 0)
+    for _ in range(2):
+        c1 = hybrid_step_slab(part, kern, dx, dy, dt, e, r, h, f)
+        c2 = hybrid_step_slab(part, kern, dx, dy, dt, e, r2, h2, f2, native=True)
+        assert torch.equal(c1, c2)
+        assert torch.equal(r, r2) and torch.equal(h, h2) and torch.equal(f, f2)
+
+
 def test_hybrid_two_slabs_equal_torus(hk):
     """Two x-slabs stepped in one process with exchanged 8-column halos reproduce the torus step."""
     import torch
