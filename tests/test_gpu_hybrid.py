@@ -140,6 +140,19 @@ def test_hybrid_slab_native_is_the_python_slab_step(hk):
         assert torch.equal(r, r2) and torch.equal(h, h2) and torch.equal(f, f2)
 
 
+def test_hybrid_slab_native_argument_checks(hk):
+    """hk_hybrid_step_slab rejects a ghost width it cannot fill before touching the state."""
+    import pytest
+    from paper_2505_03360_b200 import kinetic
+    nx, ny, n = 6, 4, 16
+    kern, dx, dy, dt, (r, h, f, e) = _hybrid_setup(hk, nx, ny, n)
+    before = [t.clone() for t in (r, h, f)]
+    for ghost in (0, nx + 1):
+        with pytest.raises(hk.contract_violation):
+            kinetic.hybrid_step_slab_native(kern, nx, ny, dx, dy, dt, e, r, h, f, ghost=ghost)
+    assert all(bool((a == b).all()) for a, b in zip(before, (r, h, f)))
+
+
 def test_hybrid_two_slabs_equal_torus(hk):
     """Two x-slabs stepped in one process with exchanged 8-column halos reproduce the torus step."""
     import torch
