@@ -1448,6 +1448,15 @@ int launch_coll16(hk_ctx ctx, const CollArgs& args, int64_t max_cells, int tag) 
     return st;
 }
 
+// N = 64 batches of >= 2048 cells run in this many chunks, each chunk's guard +
+// correction on a side stream beside the next chunk's team kernel; only the
+// last chunk's correction is exposed.
+#ifndef HK_C64_CHUNKS
+#define HK_C64_CHUNKS 8
+#endif
+constexpr int kChunks64 = HK_C64_CHUNKS;
+static_assert(kChunks64 <= 14, "chunk counters live in the 64-byte count block");
+
 template <int N, int C>
 int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells, uint32_t flags,
              hk_cell_status* st) {
@@ -1488,7 +1497,8 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     int s;
     if ((s = ensure_scratch(ctx, xchg_off + xchg_bytes))) return s;
     // every allocation of the call happens before the first launch (see nyq_fix_reserve)
-    if (guard && (s = nyq_fix_reserve(ctx, N, k->md, N == 64 && ncells >= 2048 ? (ncells + 3) / 4 : ncells))) return s;
+    if (guard && (s = nyq_fix_reserve(ctx, N, k->md, N == 64 && ncells >= 2048 ? (ncells + kChunks64 - 1) / kChunks64 : ncells)))
+        return s;
     char* base = static_cast<char*>(ctx->scratch);
     if (!st) st = reinterpret_cast<hk_cell_status*>(base);
     double2* nyq = guard ? reinterpret_cast<double2*>(base + st_bytes) : nullptr;
@@ -1567,7 +1577,7 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
         if (!ctx->s_side &&
             (s = check_cuda(ctx, cudaStreamCreateWithFlags(&ctx->s_side, cudaStreamNonBlocking), "side stream")))
             return s;
-        constexpr int kChunks = 4;
+        constexpr int kChunks = kChunks64;
         const int64_t csz = (ncells + kChunks - 1) / kChunks;
         cudaStream_t main_s = ctx->stream;
         cudaEvent_t ev[kChunks + 1];
