@@ -37,9 +37,15 @@ struct GeoFix {
 #ifndef HK_NYQ_T32
 #define HK_NYQ_T32 16  // config-4 hybrid residual (7600 listed cells): T = 4 59.4 ms, 8 56.6, 16 55.8, 32 62.1
 #endif
-    static constexpr int T = N >= 64 ? 4 : (N >= 32 ? HK_NYQ_T32 : 16);  // j1 planes per apply work item
-    static constexpr int MP = NN / 256;                            // (j2, j3) pairs per thread
-    static constexpr int STAGE = NN + 2 * T * N;                   // double2 per direction in SMEM
+    // apply work item: T j1-planes x a B x B block of (j2, j3) pairs (B = N up to 32): its
+    // three plane pieces per direction (B x B of plane 0, T x B of planes 1 and 2) are
+    // 1/T + 2/B of a value per node (N = 64 with whole 64 x 64 planes and T = 4 re-staged
+    // plane 0 sixteen times per cell: 72 -> 32 KiB per direction and item)
+    static constexpr int T = N >= 32 ? HK_NYQ_T32 : 16;  // j1 planes per apply work item
+    static constexpr int B = N < 32 ? N : 32;             // (j2, j3) block edge
+    static constexpr int MP = B * B / 256;                // (j2, j3) pairs per thread
+    static constexpr int NBLK = (N / B) * (N / B);        // blocks per plane
+    static constexpr int STAGE = B * B + 2 * T * B;       // double2 per direction in SMEM
     static constexpr size_t SMEM2 = size_t(2) * STAGE * sizeof(double2) + 64 * sizeof(double);
 };
 
@@ -141,8 +147,9 @@ __global__ void __launch_bounds__(256) nyq_planes_kernel(const int64_t* __restri
     }
 }
 
-// Phase 2: per (listed cell, j1 slab) accumulate -sum_d m_d ga_i hb_i over all
-// directions in registers (thread: MP (j2, j3) pairs x T planes), then Q += jac w acc.
+// Phase 2: per (listed cell, j1 slab, (j2, j3) block) accumulate -sum_d m_d ga_i hb_i
+// over all directions in registers (thread: MP (j2, j3) pairs x T planes), then
+// Q += jac w acc.
 template <int N>
 __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
                                                            int64_t chunk0, int64_t chunk_n,
@@ -150,29 +157,40 @@ __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __rest
                                                            double jac, double w, double* __restrict__ q,
                                                            hk_cell_status* __restrict__ st) {
     using G = GeoFix<N>;
-    constexpr int NN = G::NN, T = G::T, MP = G::MP, STAGE = G::STAGE, SLABS = N / T;
+    constexpr int NN = G::NN, T = G::T, B = G::B, MP = G::MP, STAGE = G::STAGE, SLABS = N / T, NBLK = G::NBLK;
     constexpr int64_t NB = (int64_t)N * N * N;
     extern __shared__ __align__(16) double2 sm[];
     double* red = reinterpret_cast<double*>(sm + 2 * STAGE);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    static_assert(256 % N == 0 && T % 2 == 0, "pair layout: j2 = t / N + (256 / N) m");
-    const int j2_0 = t / N, j3 = t % N;
-    const double s2 = (j2_0 & 1) ? -1.0 : 1.0, s3 = (j3 & 1) ? -1.0 : 1.0, tau = s2 * s3;
+    static_assert(256 % B == 0 && ((256 / B) % 2 == 0 || MP == 1) && T % 2 == 0 && N % B == 0,
+                  "pair layout: j2 = j2b + t / B + (256 / B) m, j3 = j3b + t % B");
+    const int j2l = t / B, j3l = t % B;  // this thread's pairs in the block: (j2l + (256 / B) m, j3l)
     int64_t avail = (int64_t)*count - chunk0;
     if (avail > chunk_n) avail = chunk_n;
-    for (int64_t wi = blockIdx.x; wi < avail * SLABS; wi += gridDim.x) {
-        const int64_t lc = wi / SLABS;
-        const int slab = (int)(wi % SLABS), j1_0 = slab * T;
+    for (int64_t wi = blockIdx.x; wi < avail * SLABS * NBLK; wi += gridDim.x) {
+        const int64_t lc = wi / (SLABS * NBLK);
+        const int rem = (int)(wi % (SLABS * NBLK)), slab = rem / NBLK, blk = rem % NBLK;
+        const int j1_0 = slab * T, j2b = (blk / (N / B)) * B, j3b = (blk % (N / B)) * B;
+        const int j2_0 = j2b + j2l, j3 = j3b + j3l;
+        const double s2 = (j2_0 & 1) ? -1.0 : 1.0, s3 = (j3 & 1) ? -1.0 : 1.0, tau = s2 * s3;
         const int64_t cell = list[chunk0 + lc];
         const double2* pc = planes + lc * md * 3 * NN;
-        // stage direction d: plane 0 (full), rows j1_0.. of planes 1 and 2
+        // stage direction d: the block of plane 0 ([j2][j3]), rows j1_0.. of planes 1
+        // ([j1][j3], the block's j3 range) and 2 ([j1][j2], its j2 range), 16 B per copy
         auto stage = [&](int d, int buf) {
             const double2* src = pc + (int64_t)d * 3 * NN;
             const uint32_t dst = smem_u32(sm + buf * STAGE);
             for (int i = t; i < STAGE; i += blockDim.x) {
-                const double2* g = i < NN ? src + i
-                                 : (i < NN + T * N ? src + NN + j1_0 * N + (i - NN)
-                                                   : src + 2 * NN + j1_0 * N + (i - NN - T * N));
+                const double2* g;
+                if (i < B * B) {
+                    g = src + (j2b + i / B) * N + j3b + i % B;
+                } else if (i < B * B + T * B) {
+                    const int k = i - B * B;
+                    g = src + NN + (j1_0 + k / B) * N + j3b + k % B;
+                } else {
+                    const int k = i - B * B - T * B;
+                    g = src + 2 * NN + (j1_0 + k / B) * N + j2b + k % B;
+                }
                 cp_async16(dst + i * 16, g);
             }
             cp_async_commit();
@@ -187,12 +205,13 @@ __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __rest
             __syncthreads();  // direction d landed for every thread; buffer d+1 free
             if (d + 1 < md) stage(d + 1, (d + 1) & 1);
             const double2* P0 = sm + (d & 1) * STAGE;
-            const double2* P1 = P0 + NN;
-            const double2* P2 = P1 + T * N;
+            const double2* P1 = P0 + B * B;
+            const double2* P2 = P1 + T * B;
             const double mu = (d == 0) ? mult0 : 1.0;
             // A B with A = s1 z0.y + s2 z1.y + s3 z2.y (B: the .x parts) equals A' B' with
             // A' = s1 (s2 z0.y) + z1.y + (s2 s3) z2.y: s2 = (-1)^j2 and s3 = (-1)^j3 are fixed
-            // per thread (j2 = t / N + 256 m / N, j3 = t % N), s1 = (-1)^j1 per plane tt.
+            // per thread (j2 = j2b + t / B + (256 / B) m with 256 / B even, j3 = j3b + t % B),
+            // s1 = (-1)^j1 per plane tt.
             // z1 depends on (tt, j3) only: one load per plane for all MP pairs.
             double2 z0[MP];
 #pragma unroll
@@ -202,14 +221,14 @@ __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __rest
             }
 #pragma unroll
             for (int tt = 0; tt < T; ++tt) {
-                const double2 z1 = P1[tt * N + j3];
+                const double2 z1 = P1[tt * B + j3l];
 #pragma unroll
                 for (int m = 0; m < MP; ++m) {
-                    const double2 z2 = P2[tt * N + j2_0 + (256 / N) * m];
+                    const double2 z2 = P2[tt * B + j2l + (256 / B) * m];
                     const bool odd = ((j1_0 + tt) & 1) != 0;  // j1_0 is even: compile-time per tt
-                    const double A = fma(tau, z2.y, odd ? z1.y - z0[m].y : z1.y + z0[m].y);
-                    const double B = fma(tau, z2.x, odd ? z1.x - z0[m].x : z1.x + z0[m].x);  // = -hb_i
-                    acc[m * T + tt] = fma(mu * A, B, acc[m * T + tt]);                   // += -m ga_i hb_i
+                    const double Aq = fma(tau, z2.y, odd ? z1.y - z0[m].y : z1.y + z0[m].y);
+                    const double Bq = fma(tau, z2.x, odd ? z1.x - z0[m].x : z1.x + z0[m].x);  // = -hb_i
+                    acc[m * T + tt] = fma(mu * Aq, Bq, acc[m * T + tt]);                 // += -m ga_i hb_i
                 }
             }
         }
@@ -217,7 +236,7 @@ __global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __rest
         double* qc = q + cell * NB;
 #pragma unroll
         for (int m = 0; m < MP; ++m) {
-            const int p = t + 256 * m;
+            const int p = (j2_0 + (256 / B) * m) * N + j3;
 #pragma unroll
             for (int tt = 0; tt < T; ++tt) {
                 const int64_t gi = (int64_t)(j1_0 + tt) * NN + p;

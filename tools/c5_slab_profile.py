@@ -8,8 +8,9 @@ from paper_2505_03360_b200 import inputs
 n = 64
 vg = hk.make_velocity_grid(n, inputs.VMAX)
 k = hk.precompute_kernel(vg, n, 8, 8, inputs.R_PHYS_MAX)
+slabs = [int(a) for a in sys.argv[1:]] or [0, 224, 448]
 out = {}
-for i0 in (0, 224, 448):
+for i0 in slabs:
     f = inputs.config5_slab_torch(i0, 64, 128, n)
     q = torch.empty_like(f)
     hk.spectral_collision(f, k, out=q)
