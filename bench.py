@@ -132,9 +132,10 @@ def load_traffic():
         return None, None
 
 
-FFT_NOTE = ("reference arithmetic; FFTW is absent from the image, so the reference's FFTW calls run on the "
-            "FFTW-API shim (oracle/shim): radix-2 C2C with cached twiddles and tiled pencils, ~2x pocketfft's "
-            "single-thread time at 32^3")
+FFT_NOTE = ("reference arithmetic, built -O3 as the reference's Release build (+ AVX2, no FMA contraction); FFTW "
+            "is absent from the image, so the reference's FFTW calls run on the FFTW-API shim (oracle/shim): radix-2 "
+            "C2C with cached twiddles and 32-pencil tiles, ~0.5 ms per 32^3 transform single-thread (~1.2x "
+            "pocketfft's time)")
 
 
 class CpuBaseline:
