@@ -1471,13 +1471,38 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     const size_t st_bytes = st ? 0 : sizeof(hk_cell_status) * ncells;
     const size_t nyq_bytes = guard ? sizeof(double2) * nn3 * ncells : 0;
     const size_t list_bytes = guard ? sizeof(int64_t) * ncells : 0;
-    // split-K guard for batches too small to fill the SMs with cell tiles
-    const int64_t gtiles = (ncells + GC - 1) / GC;
+    // split-K guard: the K slices (a divisor of the chunk count, so no slice is empty)
+    // are chosen for whole waves of resident CTAs (a 1.15-wave grid runs at ~58 %)
     const int kchunks = int((nn3 + KC - 1) / KC);
-    const int ksplit = (guard && gtiles < 2 * ctx->sm_count)
-                           ? int(std::min<int64_t>(kchunks, (2 * ctx->sm_count + gtiles - 1) / gtiles))
-                           : 1;
-    const size_t part_bytes = ksplit > 1 ? ((sizeof(double) * 4 * k->md * ncells + 255) & ~size_t(255)) : 0;
+    const size_t gsmem = sizeof(double) * (GC * KC + 2 * k->md * KS + GC);
+    auto guard_ksplit = [&](int64_t gt) -> int {
+        const int key = 5000 + k->md;
+        if (!ctx->max_clusters.count(key)) {
+            int per_sm = 0;
+            cudaFuncSetAttribute(guard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, guard_kernel, 256, gsmem);
+            ctx->max_clusters[key] = std::max(1, per_sm) * ctx->sm_count;
+        }
+        const double resident = ctx->max_clusters[key];
+        int best = 1;
+        double best_eff = 0.0;
+        for (int d = 1; d <= kchunks; ++d) {
+            if (kchunks % d) continue;
+            const double w = double(gt) * d / resident;
+            if (w > 12.0 && d > 1) break;
+            const double eff = w / std::ceil(w);
+            if (eff > best_eff + 0.02) {
+                best_eff = eff;
+                best = d;
+            }
+            if (eff >= 0.9) break;
+        }
+        return best;
+    };
+    const int ksplit = guard ? guard_ksplit((ncells + GC - 1) / GC) : 1;
+    const bool chunked64 = N == 64 && guard && ncells >= 2048;  // per-chunk guards choose their own split
+    const size_t part_bytes =
+        (ksplit > 1 || chunked64) ? ((sizeof(double) * 4 * k->md * ncells + 255) & ~size_t(255)) : 0;
     const size_t xchg_off = (st_bytes + nyq_bytes + list_bytes + 64 + 255 + part_bytes) & ~size_t(255);
     // exchange scratch of the kernel that runs (+ 64 KiB of team counters at the end)
     size_t xchg_bytes;
@@ -1540,13 +1565,12 @@ int run_size(hk_ctx ctx, hk_kernel k, const double* f, double* q, int64_t ncells
     auto guard_fix = [&](int64_t c0, int64_t nc, int* cnt) -> int {
         int e;
         const int64_t gt = (nc + GC - 1) / GC;
-        const int ks = (gt < 2 * ctx->sm_count) ? int(std::min<int64_t>(kchunks, (2 * ctx->sm_count + gt - 1) / gt)) : 1;
+        if (k->md > 128) return fail(ctx, HK_UNSUPPORTED, "guard: at most 128 distinct directions");
+        const int ks = guard_ksplit(gt);
         double* pt = (ks > 1 && part) ? part + c0 * 4 * k->md : nullptr;
         const int ksu = pt ? ks : 1;
         cudaMemsetAsync(cnt, 0, sizeof(int), ctx->stream);
         timing_begin(ctx, 1);
-        const size_t gsmem = sizeof(double) * (GC * KC + 2 * k->md * KS + GC);
-        if (k->md > 128) return fail(ctx, HK_UNSUPPORTED, "guard: at most 128 distinct directions");
         cudaFuncSetAttribute(guard_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsmem);
         if (pt) cudaMemsetAsync(pt, 0, sizeof(double) * 4 * k->md * nc, ctx->stream);
         guard_kernel<<<dim3(unsigned(gt), unsigned(ksu)), 256, gsmem, ctx->stream>>>(
