@@ -20,6 +20,7 @@
 //                      node accumulated over all directions in registers, then
 //                      one read-modify-write of Q.
 // The list is processed in chunks sized to bound the scratch (~2 GiB).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -33,9 +34,9 @@ struct GeoFix {
     static constexpr int ROW = N + 1;
     static constexpr int PLANE = N * ROW;                          // double2, padded plane
     static constexpr int NN = N * N;
-    static constexpr size_t SMEM1 = size_t(3) * PLANE * sizeof(double2);
+    static constexpr size_t SMEM1 = size_t(3) * (N <= 16 ? 4 : (N <= 32 ? 2 : 1)) * PLANE * sizeof(double2);
 #ifndef HK_NYQ_T32
-#define HK_NYQ_T32 16  // config-4 hybrid residual (7600 listed cells): T = 4 59.4 ms, 8 56.6, 16 55.8, 32 62.1
+#define HK_NYQ_T32 8  // j1 planes per apply item at N >= 32 (with 2 CTAs per SM; r02: 16 at 1 CTA per SM)
 #endif
     // apply work item: T j1-planes x a B x B block of (j2, j3) pairs (B = N up to 32): its
     // three plane pieces per direction (B x B of plane 0, T x B of planes 1 and 2) are
@@ -94,56 +95,64 @@ __device__ __forceinline__ void smem_fft_pass(double2* base, int npen, int pstri
 
 // Phase 1: Z_p = IFFT2((alpha_a + i alpha'_a) F |_{S_p}) = -B_p + i A_p for every
 // (listed cell, direction) of the chunk -> planes[w][3][N][N], w = local cell * md + d.
+// A work item takes DP directions of one cell at once (N = 32: 2, so the FFT
+// passes keep 192 of the 256 threads busy instead of 96).
+template <int N>
+struct PlanesDP {
+    static constexpr int DP = N <= 16 ? 4 : (N <= 32 ? 2 : 1);
+};
 template <int N>
 __global__ void __launch_bounds__(256) nyq_planes_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
                                                          int64_t chunk0, int64_t chunk_n, const double2* __restrict__ nyqF,
                                                          const double* __restrict__ ta, const double* __restrict__ tap,
                                                          int md, double2* __restrict__ planes) {
     using G = GeoFix<N>;
-    constexpr int ROW = G::ROW, PLANE = G::PLANE, NN = G::NN;
+    constexpr int ROW = G::ROW, PLANE = G::PLANE, NN = G::NN, DP = PlanesDP<N>::DP;
     extern __shared__ __align__(16) double2 sm[];
     const int t = threadIdx.x;
     int64_t avail = (int64_t)*count - chunk0;
     if (avail > chunk_n) avail = chunk_n;
-    for (int64_t wi = blockIdx.x; wi < avail * md; wi += gridDim.x) {
-        const int64_t it = chunk0 + wi / md;
-        const int d = (int)(wi % md);
-        const int64_t cell = list[it];
+    const int groups = (md + DP - 1) / DP;  // direction groups per cell
+    for (int64_t wi = blockIdx.x; wi < avail * groups; wi += gridDim.x) {
+        const int64_t lc = wi / groups;
+        const int d0 = (int)(wi % groups) * DP, nd = md - d0 < DP ? md - d0 : DP;
+        const int64_t cell = list[chunk0 + lc];
         const double2* Fc = nyqF + cell * 3 * NN;
         __syncthreads();  // previous item's planes written out
-        // the restricted product (alpha_a + i alpha'_a) F on the three planes; the loads
-        // of a batch of KB entries per thread are issued together (one L2 round trip per
-        // batch instead of one per entry: 22.7 -> ~5 us per item at N = 32)
+        // the restricted products (alpha_a + i alpha'_a) F on the three planes of each
+        // direction; the loads of a batch of KB entries per thread are issued together
+        // (one L2 round trip per batch instead of one per entry)
         constexpr int KB = 12;
-        const double* ta_d = ta + (int64_t)d * 3 * NN;
-        const double* tap_d = tap + (int64_t)d * 3 * NN;
-        for (int i0 = 0; i0 < 3 * NN; i0 += KB * 256) {
+        const double* ta_d = ta + (int64_t)d0 * 3 * NN;
+        const double* tap_d = tap + (int64_t)d0 * 3 * NN;
+        const int tot = nd * 3 * NN;
+        for (int i0 = 0; i0 < tot; i0 += KB * 256) {
             double av[KB], bv[KB];
             double2 Fv[KB];
 #pragma unroll
             for (int k = 0; k < KB; ++k) {
                 const int i = i0 + k * 256 + t;
-                if (i < 3 * NN) {
+                if (i < tot) {
                     av[k] = __ldg(ta_d + i);
                     bv[k] = __ldg(tap_d + i);
-                    Fv[k] = Fc[i];
+                    Fv[k] = Fc[i % (3 * NN)];
                 }
             }
 #pragma unroll
             for (int k = 0; k < KB; ++k) {
                 const int i = i0 + k * 256 + t;
-                if (i < 3 * NN)
+                if (i < tot)
                     sm[(i / NN) * PLANE + ((i % NN) / N) * ROW + (i % N)] =
                         make_double2(av[k] * Fv[k].x - bv[k] * Fv[k].y, av[k] * Fv[k].y + bv[k] * Fv[k].x);
             }
         }
         __syncthreads();
-        smem_fft_pass<N>(sm, 3 * N, ROW, 1);             // rows of the three planes
+        smem_fft_pass<N>(sm, 3 * nd * N, ROW, 1);             // rows of the 3 nd planes
         __syncthreads();
-        smem_fft_pass<N>(sm, 3 * N, 1, ROW, N, PLANE);   // columns
+        smem_fft_pass<N>(sm, 3 * nd * N, 1, ROW, N, PLANE);   // columns
         __syncthreads();
-        double2* out = planes + wi * 3 * NN;
-        for (int i = t; i < 3 * NN; i += blockDim.x) out[i] = sm[(i / NN) * PLANE + ((i % NN) / N) * ROW + (i % N)];
+        double2* out = planes + (lc * md + d0) * 3 * NN;
+        for (int i = t; i < tot; i += blockDim.x) out[i] = sm[(i / NN) * PLANE + ((i % NN) / N) * ROW + (i % N)];
     }
 }
 
@@ -151,7 +160,10 @@ __global__ void __launch_bounds__(256) nyq_planes_kernel(const int64_t* __restri
 // over all directions in registers (thread: MP (j2, j3) pairs x T planes), then
 // Q += jac w acc.
 template <int N>
-__global__ void __launch_bounds__(256, 1) nyq_apply_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
+#ifndef HK_NYQ_APPLY_MINB
+#define HK_NYQ_APPLY_MINB 2  // apply CTAs per SM (T = 8: <= 128 registers)
+#endif
+__global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
                                                            int64_t chunk0, int64_t chunk_n,
                                                            const double2* __restrict__ planes, int md, double mult0,
                                                            double jac, double w, double* __restrict__ q,
@@ -315,23 +327,29 @@ int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int
     int s0 = nyq_fix_reserve(ctx, n, md, max_cells);
     if (s0) return s0;
     double2* planes = static_cast<double2*>(ctx->fix_scratch);
-    auto run = [&](auto k1, size_t smem1, int per_sm1, auto k2, size_t smem2) -> int {
+    // persistent grids of exactly the resident CTAs (registers / shared memory decide)
+    auto run = [&](auto k1, size_t smem1, auto k2, size_t smem2) -> int {
         int s;
         if ((s = check_cuda(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem")) ||
             (s = check_cuda(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), "smem")))
             return s;
+        int r1 = 0, r2 = 0;
+        if ((s = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, k1, 256, smem1), "occupancy")) ||
+            (s = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k2, 256, smem2), "occupancy")))
+            return s;
+        const unsigned g1 = unsigned(ctx->sm_count * std::max(r1, 1)), g2 = unsigned(ctx->sm_count * std::max(r2, 1));
         for (int64_t c0 = 0; c0 < max_cells; c0 += chunk) {
-            k1<<<unsigned(ctx->sm_count * per_sm1), 256, smem1, ctx->stream>>>(list, count, c0, chunk, nyqF, ta, tap, md, planes);
-            k2<<<unsigned(ctx->sm_count), 256, smem2, ctx->stream>>>(list, count, c0, chunk, planes, md, mult0, jac, w, q, st);
+            k1<<<g1, 256, smem1, ctx->stream>>>(list, count, c0, chunk, nyqF, ta, tap, md, planes);
+            k2<<<g2, 256, smem2, ctx->stream>>>(list, count, c0, chunk, planes, md, mult0, jac, w, q, st);
             ctx->launches += 2;
             if ((s = check_cuda(ctx, cudaGetLastError(), "nyq_fix kernels"))) return s;
         }
         return HK_OK;
     };
     switch (n) {
-    case 16: return run(nyq_planes_kernel<16>, GeoFix<16>::SMEM1, 8, nyq_apply_kernel<16>, GeoFix<16>::SMEM2);
-    case 32: return run(nyq_planes_kernel<32>, GeoFix<32>::SMEM1, 4, nyq_apply_kernel<32>, GeoFix<32>::SMEM2);
-    case 64: return run(nyq_planes_kernel<64>, GeoFix<64>::SMEM1, 1, nyq_apply_kernel<64>, GeoFix<64>::SMEM2);
+    case 16: return run(nyq_planes_kernel<16>, GeoFix<16>::SMEM1, nyq_apply_kernel<16>, GeoFix<16>::SMEM2);
+    case 32: return run(nyq_planes_kernel<32>, GeoFix<32>::SMEM1, nyq_apply_kernel<32>, GeoFix<32>::SMEM2);
+    case 64: return run(nyq_planes_kernel<64>, GeoFix<64>::SMEM1, nyq_apply_kernel<64>, GeoFix<64>::SMEM2);
     default: return fail(ctx, HK_UNSUPPORTED, "nyq_fix: n = 16, 32, 64");
     }
 }
