@@ -51,6 +51,9 @@ struct TransportParams {
     // [strips][ny] from transport_row_activity: rows of a strip with no cell of
     // interest are skipped (their outputs are left unwritten)
     const uint8_t* row_act = nullptr;
+    // optional compact output (lane-per-column kernel, plain T only): cell c's
+    // result goes to out + out_pos[c] n^3, cells with out_pos[c] < 0 are not written
+    const int* out_pos = nullptr;
 };
 
 // Final PR(2,2,2) combination fused into the second transport of a step
@@ -77,6 +80,8 @@ struct FinalCombine {
     double* fa = nullptr;    // mode 2: f_acc out
     double k1_scale = 0.0;   // mode 2: 1 / a_im00
 };
+// true when transport_launch takes the lane-per-column sweep for these shapes (out_pos honoured)
+bool transport_lanes_path(const TransportParams& p);
 int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh = nullptr,
                      const double* rh = nullptr);
 // hk_transport.cu: y-marching transport (n a power of two, n^3 % 32 == 0, ny >= 3)

@@ -179,14 +179,21 @@ int classify_launch(hk_ctx ctx, const ClassifyParams& p, const double* mom, cons
     return check_cuda(ctx, cudaGetLastError(), "classify kernel");
 }
 
+bool transport_lanes_path(const TransportParams& p) {
+    const int64_t nb = (int64_t)p.n * p.n * p.n;
+    return (p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3;
+}
+
 int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh,
                      const double* rh) {
+    if (p.out_pos && !transport_lanes_path(p))
+        return fail(ctx, HK_CONTRACT, "transport: compact output needs the lane-per-column sweep");
     if (p.x_halo == 1 || p.x_halo < -2 || p.x_halo == -1 || (p.x_halo == -2 && (!lh || !rh)))
         return fail(ctx, HK_CONTRACT, "transport: x_halo must be 0, -2 (separate halo buffers) or >= 2");
     const int64_t total = (int64_t)p.nx * p.ny * p.n * p.n * p.n;
     if (total <= 0) return HK_OK;
     const int64_t nb = (int64_t)p.n * p.n * p.n;
-    if ((p.n & (p.n - 1)) == 0 && nb % 32 == 0 && p.ny >= 3) {  // lane-per-column sweep (hk_transport.cu)
+    if (transport_lanes_path(p)) {  // lane-per-column sweep (hk_transport.cu)
         int lg = 0;
         while ((1 << lg) < p.n) ++lg;
         return transport_march_launch(ctx, p, lg, f, out, lh, rh);

@@ -259,6 +259,12 @@ __global__ void status_kernel(int64_t nk, const int64_t* __restrict__ list, cons
     if (s && s != HK_NUMERICAL_CONSISTENCY) fail_at(cnt, list[k], s);
 }
 
+// pos[list[b]] = b for the batch rows (pos preset to -1)
+__global__ void inverse_list_kernel(int64_t nk, const int64_t* __restrict__ list, int* __restrict__ pos) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b < nk) pos[list[b]] = int(b);
+}
+
 unsigned nblk(int64_t n, int t) { return unsigned((n + t - 1) / t); }
 
 // Grow-only device buffer owned by the context.
@@ -418,8 +424,13 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
 
     // ---- 4. kinetic layers: PR(2,2,2) on the compact batch ----
     if (nk) {
-        const size_t big_need = sizeof(double) * (size_t)nb * (size_t)(7 * nk + cells) + 8 * 256;
-        const size_t big_max = sizeof(double) * (size_t)nb * (size_t)(8 * cells) + 8 * 256;  // every cell kinetic
+        TransportParams tp{n, vmax, nx, ny, 0, dx, dy, p->eps_weno};
+        // the lane sweep writes T straight into the batch rows (pos: cell -> batch row);
+        // otherwise a dense T field is gathered
+        const bool compact_T = transport_lanes_path(tp);
+        const int64_t t_cells = compact_T ? 0 : cells;
+        const size_t big_need = sizeof(double) * (size_t)nb * (size_t)(7 * nk + t_cells) + 8 * 256;
+        const size_t big_max = sizeof(double) * (size_t)nb * (size_t)(7 * cells + t_cells) + 8 * 256;  // all kinetic
         if ((st = grow(ctx, &ctx->hyb_big, &ctx->hyb_big_bytes, big_need, "kinetic workspace", big_max))) return st;
         char* b = static_cast<char*>(ctx->hyb_big);
         double* fk = carve<double>(b, nk * nb);
@@ -429,11 +440,16 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
         double* tr = carve<double>(b, nk * nb);
         double* res = carve<double>(b, nk * nb);
         double* fa = carve<double>(b, nk * nb);
-        double* T = carve<double>(b, cells * nb);
+        double* T = compact_T ? nullptr : carve<double>(b, cells * nb);
+        if (compact_T) {  // pos (free since the indicator pass) becomes the inverse of list
+            cudaMemsetAsync(pos, 0xff, sizeof(int) * cells, s);
+            inverse_list_kernel<<<nblk(nk, 256), 256, 0, s>>>(nk, list, pos);
+            ctx->launches++;
+            tp.out_pos = pos;
+        }
         const PR t = pr222_t();
         cudaMemsetAsync(stk, 0, sizeof(int) * nk, s);
         cudaMemsetAsync(stk2, 0, sizeof(int) * nk, s);
-        TransportParams tp{n, vmax, nx, ny, 0, dx, dy, p->eps_weno};
         uint8_t* act = reinterpret_cast<uint8_t*>(ework);  // the Euler work is free again
         if ((st = transport_row_activity(ctx, nx, ny, r_new, act))) return st;
         tp.row_act = act;  // T is only gathered at the kinetic cells
@@ -459,8 +475,8 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
         };
         auto transport = [&](const double* y) -> int {  // T(y) at the batch cells
             int e = hk_scatter_cells(ctx, nb, y, list, nk, f_dev);
-            if (!e) e = transport_launch(ctx, tp, f_dev, T);
-            if (!e) e = hk_gather_cells(ctx, nb, T, list, nk, tr);
+            if (!e) e = transport_launch(ctx, tp, f_dev, compact_T ? tr : T);
+            if (!e && !compact_T) e = hk_gather_cells(ctx, nb, T, list, nk, tr);
             return e;
         };
         // q = tr (+ res / eps on the layer-2 part), via the IMEX combinations

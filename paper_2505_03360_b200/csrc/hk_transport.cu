@@ -262,7 +262,12 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
 #pragma unroll
             for (int q = 0; q < 2; ++q) tr[q] = -fx[q] * inv_dx - vy * (fy[q] - fyp[q]) * inv_dy;
             if constexpr (MODE == 0) {
-                *reinterpret_cast<double2*>(out + o) = make_double2(tr[0], tr[1]);
+                if (p.out_pos) {  // compact output: the batch row of this cell, if any
+                    const int b = p.out_pos[(int64_t)j * p.nx + i];
+                    if (b >= 0) *reinterpret_cast<double2*>(out + (int64_t)b * nb + idx) = make_double2(tr[0], tr[1]);
+                } else {
+                    *reinterpret_cast<double2*>(out + o) = make_double2(tr[0], tr[1]);
+                }
             } else if constexpr (MODE == 2) {  // T(Y1): f_acc and G (FinalCombine)
                 const int64_t cell = (int64_t)j * p.nx + i;
                 const double ie = fc.res ? 1.0 / fc.eps[cell] : 0.0;
