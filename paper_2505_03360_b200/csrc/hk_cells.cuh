@@ -54,6 +54,10 @@ struct TransportParams {
     // optional compact output (lane-per-column kernel, plain T only): cell c's
     // result goes to out + out_pos[c] n^3, cells with out_pos[c] < 0 are not written
     const int* out_pos = nullptr;
+    // optional batch-resident input (lane kernel, x_halo == 0): cells with in_pos[c] >= 0
+    // are read from in_batch + in_pos[c] n^3, the others from the dense field
+    const int* in_pos = nullptr;
+    const double* in_batch = nullptr;
 };
 
 // Final PR(2,2,2) combination fused into the second transport of a step

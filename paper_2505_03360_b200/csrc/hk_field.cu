@@ -186,8 +186,10 @@ bool transport_lanes_path(const TransportParams& p) {
 
 int transport_launch(hk_ctx ctx, const TransportParams& p, const double* f, double* out, const double* lh,
                      const double* rh) {
-    if (p.out_pos && !transport_lanes_path(p))
-        return fail(ctx, HK_CONTRACT, "transport: compact output needs the lane-per-column sweep");
+    if ((p.out_pos || p.in_pos) && !transport_lanes_path(p))
+        return fail(ctx, HK_CONTRACT, "transport: batch input / output needs the lane-per-column sweep");
+    if (p.in_pos && (p.x_halo != 0 || !p.in_batch))
+        return fail(ctx, HK_CONTRACT, "transport: batch input needs a periodic field and the batch");
     if (p.x_halo == 1 || p.x_halo < -2 || p.x_halo == -1 || (p.x_halo == -2 && (!lh || !rh)))
         return fail(ctx, HK_CONTRACT, "transport: x_halo must be 0, -2 (separate halo buffers) or >= 2");
     const int64_t total = (int64_t)p.nx * p.ny * p.n * p.n * p.n;

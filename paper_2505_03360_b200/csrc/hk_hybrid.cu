@@ -474,9 +474,15 @@ extern "C" int hk_hybrid_step(hk_ctx ctx, hk_kernel k, int nx, int ny, double dx
             return e ? e : residual_finish_launch(ctx, n, vmax, y + n1 * nb, res + n1 * nb, m2, p->pen_coeff, stk2 + n1);
         };
         auto transport = [&](const double* y) -> int {  // T(y) at the batch cells
+            if (compact_T) {  // the sweep reads y from the batch rows and writes T to them: no copies
+                TransportParams ty = tp;
+                ty.in_pos = pos;
+                ty.in_batch = y;
+                return transport_launch(ctx, ty, f_dev, tr);
+            }
             int e = hk_scatter_cells(ctx, nb, y, list, nk, f_dev);
-            if (!e) e = transport_launch(ctx, tp, f_dev, compact_T ? tr : T);
-            if (!e && !compact_T) e = hk_gather_cells(ctx, nb, T, list, nk, tr);
+            if (!e) e = transport_launch(ctx, tp, f_dev, T);
+            if (!e) e = hk_gather_cells(ctx, nb, T, list, nk, tr);
             return e;
         };
         // q = tr (+ res / eps on the layer-2 part), via the IMEX combinations

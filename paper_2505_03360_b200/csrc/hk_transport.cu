@@ -115,8 +115,17 @@ __global__ void __launch_bounds__(128) transport_lanes_kernel(TransportParams p,
     int64_t rowstride;
     col_src(i, colbase, rowstride);
     colbase += idx;
+    // optional batch-resident input (periodic x only): a cell with in_pos >= 0 is read
+    // from its batch row instead of the dense field
+    const int iw = ((i % p.nx) + p.nx) % p.nx;
     auto ld = [&](int jj) -> double2 {
         jj = jj < 0 ? jj + ny : (jj >= ny ? jj - ny : jj);
+        if (p.in_pos) {
+            const int64_t c = (int64_t)jj * p.nx + iw;
+            const int bb = __ldg(p.in_pos + c);
+            const double* src = bb >= 0 ? p.in_batch + (int64_t)bb * nb + idx : f + c * nb + idx;
+            return __ldg(reinterpret_cast<const double2*>(src));
+        }
         return __ldg(reinterpret_cast<const double2*>(colbase + (int64_t)jj * rowstride));
     };
     // STAGED loader role: thread t copies 16 B (nodes idx0 + 2 h, h = t & 3) of cell lc = t >> 2
