@@ -373,7 +373,8 @@ int transport_march_launch(hk_ctx ctx, const TransportParams& p, int lg, const d
     } else if (p.row_act) {
         transport_lanes_kernel<0, 2, true><<<grid, 128, smem, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
     } else {
-        if (staged) transport_lanes_kernel<0, 2, false, true><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
+        if (staged && !p.in_pos)  // the staged ring copies dense rows: batch input takes the plain march
+            transport_lanes_kernel<0, 2, false, true><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
         else transport_lanes_kernel<0, 2><<<grid, 128, 0, ctx->stream>>>(p, lg, f, out, lh, rh, FinalCombine{});
     }
     ctx->launches++;
