@@ -432,9 +432,9 @@ static int collision_host_streamed(hk_ctx ctx, hk_kernel k, const double* f_host
 #endif
     const size_t nb = size_t(k->n) * k->n * k->n;
     const size_t bytes = sizeof(double) * nb * ncells;
-    // 64 chunks: the unoverlapped pipeline fill (first H2D) and drain (last D2H) are 1/64 of the copies
-    // (config 2: 64 cells = 16 MiB, ~0.3 ms each way; 32 chunks cost ~0.6 ms more per call)
-    const int64_t chunk = ncells >= 4096 ? (ncells + 63) / 64
+    // 128 chunks: the unoverlapped pipeline fill (first H2D) and drain (last D2H) are 1/128 of the copies
+    // (config 2: 32 cells = 8 MiB, ~0.15 ms each way; 32 chunks cost ~0.9 ms more per call)
+    const int64_t chunk = ncells >= 4096 ? (ncells + 127) / 128
                           : (ncells >= 2048 ? (ncells + 31) / 32 : (ncells >= 1024 ? (ncells + 15) / 16 : ncells));
     const int64_t nch = (ncells + chunk - 1) / chunk;
     double *f_dev = nullptr, *q_dev = nullptr;
