@@ -73,8 +73,9 @@ __device__ void block_sum(double (&v)[K], double* scratch /* [8][K] */) {
 // oracle/hk_oracle.c:hko_solve5.  Returns false when singular.
 // Register-resident form: every index is a compile-time constant after
 // unrolling; the data-dependent pivot row / column swaps are selects (no
-// local memory).  Same pivot order (first maximum in column-major scan), same
-// operations per element as the scalar algorithm.
+// local memory).  Same pivot order (first maximum in column-major scan) as the
+// scalar algorithm; the multipliers use one reciprocal of the pivot per step
+// (a_ik * (1 / a_kk): within an ulp of the division, a shorter latency chain).
 __device__ __forceinline__ bool solve5(const double a_in[25], const double rhs[5], double x[5]) {
     double a[5][5];
     int rp[5], cp[5];
@@ -133,9 +134,10 @@ __device__ __forceinline__ bool solve5(const double a_in[25], const double rhs[5
                 cp[k] = sw ? cp[c] : ti;
                 cp[c] = sw ? ti : cp[c];
             }
+            const double rkk = 1.0 / a[k][k];  // one division per step (the multipliers: l_ik = a_ik / a_kk)
 #pragma unroll
             for (int i = k + 1; i < 5; ++i) {
-                a[i][k] /= a[k][k];
+                a[i][k] *= rkk;
 #pragma unroll
                 for (int j = k + 1; j < 5; ++j) a[i][j] -= a[i][k] * a[k][j];
             }
@@ -158,11 +160,14 @@ __device__ __forceinline__ bool solve5(const double a_in[25], const double rhs[5
     for (int i = 0; i < 5; ++i)
 #pragma unroll
         for (int j = 0; j < i; ++j) y[i] -= a[i][j] * y[j];
+    double rd[5];  // the diagonal's reciprocals, independent of each other: off the back-substitution chain
+#pragma unroll
+    for (int i = 0; i < 5; ++i) rd[i] = 1.0 / a[i][i];
 #pragma unroll
     for (int i = 4; i >= 0; --i) {
 #pragma unroll
         for (int j = i + 1; j < 5; ++j) y[i] -= a[i][j] * y[j];
-        y[i] /= a[i][i];
+        y[i] *= rd[i];
     }
 #pragma unroll
     for (int o = 0; o < 5; ++o) {
@@ -1314,11 +1319,15 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                 double tc[9];
                 const double denom = eps + omb * A, oa = omb * A;
                 const double iso = (1.0 - beta) * m.T;
+                const double idr = 1.0 / (denom * m.rho);  // one division for the 9 entries
+                // the 9 entries are independent: unrolled
+#pragma unroll
                 for (int i = 0; i < 3; ++i)
+#pragma unroll
                     for (int j = 0; j < 3; ++j) {
                         const double sstar = s11[5 + map[3 * i + j]] * g.dvk;
                         const double siso = m.rho * ((i == j ? m.T : 0.0) + u[i] * u[j]);
-                        const double theta = (eps * sstar + oa * siso) / denom / m.rho - u[i] * u[j];
+                        const double theta = (eps * sstar + oa * siso) * idr - u[i] * u[j];
                         tc[3 * i + j] = (i == j ? iso : 0.0) + beta * theta;
                     }
                 double l[9] = {0};
@@ -1343,7 +1352,7 @@ __global__ void __launch_bounds__(MT, MINB) stage_cta_kernel(const double* __res
                     par[1] = c00 * id; par[2] = (q[2] * q[7] - q[1] * q[8]) * id; par[3] = (q[1] * q[5] - q[2] * q[4]) * id;
                     par[4] = (q[0] * q[8] - q[2] * q[6]) * id; par[5] = (q[2] * q[3] - q[0] * q[5]) * id;
                     par[6] = (q[0] * q[4] - q[1] * q[3]) * id;  // S11 S12 S13 S22 S23 S33
-                    par[7] = m.rho / sqrt(pow(2.0 * M_PI, 3) * det);
+                    par[7] = m.rho / sqrt(248.05021344239853 * det);  // (2 pi)^3
                     par[0] = 1.0;
                 }
             }
