@@ -584,13 +584,21 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                             x[24 + m] = make_double2(tmem_pair(r3[4 * m], r3[4 * m + 1]), tmem_pair(r3[4 * m + 2], r3[4 * m + 3]));
                         }
                     }
-#ifndef HK_EXP_NOMUL
+                    // the weight products fused into the transform's first radix-2 stage
+                    // (bit-reversed input, trivial twiddles): a = F_a w_a, o0 = a + F_b w_b by
+                    // FMA, o1 = 2 a - o0 (10 fp64 instructions per pair instead of 12)
+                    double2 y[N];
 #pragma unroll
-                    for (int i3 = 0; i3 < N; ++i3) {
-                        const double2 w = wbuf[i3 * 32 + lane], v = x[i3];
-                        x[i3] = make_double2(v.x * w.x - v.y * w.y, v.x * w.y + v.y * w.x);
+                    for (int i = 0; i < N; i += 2) {
+                        const int ia = bitrev<N>(i), ib = bitrev<N>(i + 1);
+                        const double2 wa = wbuf[ia * 32 + lane], wb = wbuf[ib * 32 + lane];
+                        const double2 Fa = x[ia], Fb = x[ib];
+                        const double2 a = make_double2(Fa.x * wa.x - Fa.y * wa.y, Fa.x * wa.y + Fa.y * wa.x);
+                        const double2 o0 = make_double2(__fma_rn(Fb.x, wb.x, __fma_rn(-Fb.y, wb.y, a.x)),
+                                                        __fma_rn(Fb.x, wb.y, __fma_rn(Fb.y, wb.x, a.y)));
+                        y[i] = o0;
+                        y[i + 1] = make_double2(__fma_rn(2.0, a.x, -o0.x), __fma_rn(2.0, a.y, -o0.y));
                     }
-#endif
                     __syncwarp();
 #ifndef HK_EXP_NOISSUE
                     if (pp + 1 < PPW)
@@ -599,7 +607,9 @@ __global__ void __launch_bounds__(384, 1) coll_fast_w12_kernel(CollArgs a) {
                         issue_w(e + 1, 0);
 #endif
                     HK_PH_ADD(1, tA);
-                    fft_w<N, true>(x);
+                    fft_fma_stage<N, 4, true>(y);
+#pragma unroll
+                    for (int i = 0; i < N; ++i) x[i] = y[i];
                     HK_PH_ADD(2, tA);
                     if (pp == 0) acquire(g);
                     HK_PH_ADD(3, tA);
