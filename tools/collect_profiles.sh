@@ -13,4 +13,6 @@ for k in coll_fast:collision_fast coll64:collision64 coll16:collision16 resid:re
   src=${k%%:*}; dst=${k##*:}
   [ -f $G/${src}_$TAG.ncu-rep ] && python3 tools/ncu_summary.py $G/${src}_$TAG.ncu-rep > $P/${OUT}_${dst}_ncu.txt
 done
+[ -f $G/hybrid_parts_$TAG.txt ] && tail -n 1 $G/hybrid_parts_$TAG.txt > $P/${OUT}_config4_hybrid_parts.txt
+[ -f $G/c5_slabs_$TAG.json ] && tail -n 1 $G/c5_slabs_$TAG.json > $P/${OUT}_config5_slabs.json
 echo collected into $P/${OUT}_*

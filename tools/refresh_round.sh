@@ -29,3 +29,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:stag
   python tools/esbgk_step.py stage > $O/ncu_stage_$TAG.log 2>&1; echo "ncu stage rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:transport_lanes -s 6 -c 2 -o $O/transport_$TAG -f \
   python tools/esbgk_step.py step > $O/ncu_transport_$TAG.log 2>&1; echo "ncu transport rc=$?"
+timeout 300 python tools/hybrid_parts.py > $O/hybrid_parts_$TAG.txt 2>&1; echo "hybrid parts rc=$?"
+timeout 600 python tools/c5_slab_profile.py > $O/c5_slabs_$TAG.json 2>&1; echo "config-5 slabs rc=$?"
