@@ -153,14 +153,16 @@ def test_n32_host_path(n32, hk):
         assert rel_l2(q[c], n32["q_ref"][c]) < TOL, c
 
 
-def test_n32_streamed_host_path_matches_device_path(hk):
+@pytest.mark.parametrize("ncells", [1100, 4100])
+def test_n32_streamed_host_path_matches_device_path(hk, ncells):
     """The e2e entry point (one persistent launch fed chunk by chunk from pinned
     host memory, results streamed back) gives the device path's Q bitwise,
-    including the cells the Nyquist guard reroutes."""
+    including the cells the Nyquist guard reroutes (1100 cells: 16 chunks;
+    4100 cells: 128 chunks of 33, the last one ragged)."""
     import torch
     vg = hk.make_velocity_grid(32, inputs.VMAX)
     kern = hk.precompute_kernel(vg, 32, 8, 8, inputs.R_PHYS_MAX)
-    f = inputs.config2_cells_torch(1100, 32, device="cuda")
+    f = inputs.config2_cells_torch(ncells, 32, device="cuda")
     q_dev, st_dev = hk.spectral_collision(f, kern, return_status=True)
     fh = f.cpu().pin_memory()
     qh = torch.empty_like(fh).pin_memory()
