@@ -143,3 +143,19 @@ def test_weighted_bounds_balance():
     assert [p.i0 for p in parts] == list(b[:-1]) and sum(p.nxl for p in parts) == nx
     with pytest.raises(ValueError):
         XSlab(nx, 4, 2, 0, (0, 1, nx))
+
+
+def test_native_slab_step_rejects_explicit_halos():
+    """hybrid_step_slab(native=True) moves its halos over the context's own
+    communicator: explicit halo tensors are a caller error (raised before any
+    device work)."""
+    import pytest
+    import torch
+    from paper_2505_03360_b200.partition import XSlab, hybrid_step_slab
+    part = XSlab(8, 4, 1, 0)
+    r = torch.zeros(32, dtype=torch.int8)
+    e = torch.zeros(32, dtype=torch.float64)
+    h = torch.zeros((32, 4), dtype=torch.float64)
+    f = torch.zeros((32, 8), dtype=torch.float64)
+    with pytest.raises(ValueError):
+        hybrid_step_slab(part, None, 0.1, 0.1, 0.01, e, r, h, f, halos=[], native=True)
