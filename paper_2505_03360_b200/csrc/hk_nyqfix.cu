@@ -20,6 +20,7 @@
 //                      node accumulated over all directions in registers, then
 //                      one read-modify-write of Q.
 // The list is processed in chunks sized to bound the scratch (~2 GiB).
+#include <type_traits>
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -219,7 +220,6 @@ __global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const
             const double2* P0 = sm + (d & 1) * STAGE;
             const double2* P1 = P0 + B * B;
             const double2* P2 = P1 + T * B;
-            const double mu = (d == 0) ? mult0 : 1.0;
             // A B with A = s1 z0.y + s2 z1.y + s3 z2.y (B: the .x parts) equals A' B' with
             // A' = s1 (s2 z0.y) + z1.y + (s2 s3) z2.y: s2 = (-1)^j2 and s3 = (-1)^j3 are fixed
             // per thread (j2 = j2b + t / B + (256 / B) m with 256 / B even, j3 = j3b + t % B),
@@ -231,18 +231,27 @@ __global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const
                 const double2 v = P0[t + 256 * m];
                 z0[m] = make_double2(s2 * v.x, s2 * v.y);
             }
+            // direction 0 carries the multiplicity mult0; the others (1.0 * A == A)
+            // take the same arithmetic without the multiply
+            auto accumulate = [&](auto with_mu) {
 #pragma unroll
-            for (int tt = 0; tt < T; ++tt) {
-                const double2 z1 = P1[tt * B + j3l];
+                for (int tt = 0; tt < T; ++tt) {
+                    const double2 z1 = P1[tt * B + j3l];
 #pragma unroll
-                for (int m = 0; m < MP; ++m) {
-                    const double2 z2 = P2[tt * B + j2l + (256 / B) * m];
-                    const bool odd = ((j1_0 + tt) & 1) != 0;  // j1_0 is even: compile-time per tt
-                    const double Aq = fma(tau, z2.y, odd ? z1.y - z0[m].y : z1.y + z0[m].y);
-                    const double Bq = fma(tau, z2.x, odd ? z1.x - z0[m].x : z1.x + z0[m].x);  // = -hb_i
-                    acc[m * T + tt] = fma(mu * Aq, Bq, acc[m * T + tt]);                 // += -m ga_i hb_i
+                    for (int m = 0; m < MP; ++m) {
+                        const double2 z2 = P2[tt * B + j2l + (256 / B) * m];
+                        const bool odd = ((j1_0 + tt) & 1) != 0;  // j1_0 is even: compile-time per tt
+                        const double Aq = fma(tau, z2.y, odd ? z1.y - z0[m].y : z1.y + z0[m].y);
+                        const double Bq = fma(tau, z2.x, odd ? z1.x - z0[m].x : z1.x + z0[m].x);  // = -hb_i
+                        acc[m * T + tt] = fma(decltype(with_mu)::value ? mult0 * Aq : Aq, Bq,
+                                              acc[m * T + tt]);  // += -m ga_i hb_i
+                    }
                 }
-            }
+            };
+            if (d == 0)
+                accumulate(std::true_type{});
+            else
+                accumulate(std::false_type{});
         }
         double mre = 0.0, n2 = 0.0;
         double* qc = q + cell * NB;
@@ -280,6 +289,10 @@ __global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const
     }
 }
 
+#ifndef HK_NYQ_CHUNK_BYTES
+#define HK_NYQ_CHUNK_BYTES (size_t(2) << 30)  // plane scratch per chunk of listed cells
+#endif
+
 // Grows the plane scratch for up to max_cells listed cells.  Growing
 // synchronises the device (cudaFree / cudaMalloc), so run_size reserves it
 // BEFORE launching the collision kernel: a kernel waiting on host-fed flags
@@ -287,7 +300,7 @@ __global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const
 int nyq_fix_reserve(hk_ctx ctx, int n, int md, int64_t max_cells) {
     if (max_cells < 1) return HK_OK;
     const size_t per_cell = size_t(md) * 3 * n * n * sizeof(double2);
-    int64_t chunk = int64_t((size_t(2) << 30) / per_cell);
+    int64_t chunk = int64_t(size_t(HK_NYQ_CHUNK_BYTES) / per_cell);
     if (chunk < 1) chunk = 1;
     if (chunk > max_cells) chunk = max_cells;
     const size_t need = per_cell * chunk;
@@ -321,7 +334,7 @@ int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int
                    hk_cell_status* st) {
     if (max_cells < 1) return HK_OK;
     const size_t per_cell = size_t(md) * 3 * n * n * sizeof(double2);
-    int64_t chunk = int64_t((size_t(2) << 30) / per_cell);
+    int64_t chunk = int64_t(size_t(HK_NYQ_CHUNK_BYTES) / per_cell);
     if (chunk < 1) chunk = 1;
     if (chunk > max_cells) chunk = max_cells;
     int s0 = nyq_fix_reserve(ctx, n, md, max_cells);
