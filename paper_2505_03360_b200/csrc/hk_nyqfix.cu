@@ -54,11 +54,14 @@ struct GeoFix {
 // Inverse 1-D transforms of `npen` pencils in shared memory, in place, natural
 // order: pencil p starts at base + (p / ppg) gstride + (p % ppg) pstride, its
 // elements are estride apart.
+#ifndef HK_NYQ_SPLIT32
+#define HK_NYQ_SPLIT32 1  // N = 32 plane transforms on split pencils (64 data registers, 2 CTAs per SM)
+#endif
 template <int N>
 __device__ __forceinline__ void smem_fft_pass(double2* base, int npen, int pstride, int estride, int ppg = 1 << 30,
                                               int gstride = 0) {
     auto at = [&](int p) { return base + (size_t)(p / ppg) * gstride + (size_t)(p % ppg) * pstride; };
-    if constexpr (N <= 32) {
+    if constexpr (N <= (HK_NYQ_SPLIT32 ? 16 : 32)) {
         for (int p = threadIdx.x; p < npen; p += blockDim.x) {
             double2* x0 = at(p);
             double2 v[N];
@@ -68,7 +71,7 @@ __device__ __forceinline__ void smem_fft_pass(double2* base, int npen, int pstri
 #pragma unroll
             for (int i = 0; i < N; ++i) x0[i * estride] = v[i];
         }
-    } else {  // N = 64: one pencil per lane pair (l, l ^ 16)
+    } else {  // N = 32, 64: one pencil per lane pair (l, l ^ 16), N / 2 values per thread
         constexpr int M = N / 2, Q = M / 2;
         const int lane = threadIdx.x & 31, h = lane >> 4;
         const int slot0 = (threadIdx.x >> 5) * 16 + (lane & 15);
@@ -101,9 +104,14 @@ __device__ __forceinline__ void smem_fft_pass(double2* base, int npen, int pstri
 template <int N>
 struct PlanesDP {
     static constexpr int DP = N <= 16 ? 4 : (N <= 32 ? 2 : 1);
+    static constexpr int MINB = N == 32 && HK_NYQ_SPLIT32 ? 2 : 1;  // N = 32: split pencils, 2 CTAs per SM
+#ifndef HK_NYQ_KB32
+#define HK_NYQ_KB32 4  // N = 32 at 128 registers: 6 and 8 spill
+#endif
+    static constexpr int KB = N == 32 && HK_NYQ_SPLIT32 ? HK_NYQ_KB32 : 12;  // product entries per thread per batch
 };
 template <int N>
-__global__ void __launch_bounds__(256) nyq_planes_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
+__global__ void __launch_bounds__(256, PlanesDP<N>::MINB) nyq_planes_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
                                                          int64_t chunk0, int64_t chunk_n, const double2* __restrict__ nyqF,
                                                          const double* __restrict__ ta, const double* __restrict__ tap,
                                                          int md, double2* __restrict__ planes) {
@@ -123,7 +131,7 @@ __global__ void __launch_bounds__(256) nyq_planes_kernel(const int64_t* __restri
         // the restricted products (alpha_a + i alpha'_a) F on the three planes of each
         // direction; the loads of a batch of KB entries per thread are issued together
         // (one L2 round trip per batch instead of one per entry)
-        constexpr int KB = 12;
+        constexpr int KB = PlanesDP<N>::KB;
         const double* ta_d = ta + (int64_t)d0 * 3 * NN;
         const double* tap_d = tap + (int64_t)d0 * 3 * NN;
         const int tot = nd * 3 * NN;
