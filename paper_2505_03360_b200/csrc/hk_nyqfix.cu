@@ -36,6 +36,9 @@ struct GeoFix {
     static constexpr int PLANE = N * ROW;                          // double2, padded plane
     static constexpr int NN = N * N;
     static constexpr size_t SMEM1 = size_t(3) * (N <= 16 ? 4 : (N <= 32 ? 2 : 1)) * PLANE * sizeof(double2);
+#ifndef HK_NYQ_APPLY_NT
+#define HK_NYQ_APPLY_NT 256  // apply threads per CTA
+#endif
 #ifndef HK_NYQ_T32
 #define HK_NYQ_T32 8  // j1 planes per apply item at N >= 32 (with 2 CTAs per SM; r02: 16 at 1 CTA per SM)
 #endif
@@ -45,7 +48,8 @@ struct GeoFix {
     // plane 0 sixteen times per cell: 72 -> 32 KiB per direction and item)
     static constexpr int T = N >= 32 ? HK_NYQ_T32 : 16;  // j1 planes per apply work item
     static constexpr int B = N < 32 ? N : 32;             // (j2, j3) block edge
-    static constexpr int MP = B * B / 256;                // (j2, j3) pairs per thread
+    static constexpr int ANT = N >= 32 ? HK_NYQ_APPLY_NT : 256;  // apply threads per CTA
+    static constexpr int MP = B * B / ANT;                // (j2, j3) pairs per apply thread
     static constexpr int NBLK = (N / B) * (N / B);        // blocks per plane
     static constexpr int STAGE = B * B + 2 * T * B;       // double2 per direction in SMEM
     static constexpr size_t SMEM2 = size_t(2) * STAGE * sizeof(double2) + 64 * sizeof(double);
@@ -172,20 +176,21 @@ template <int N>
 #ifndef HK_NYQ_APPLY_MINB
 #define HK_NYQ_APPLY_MINB 2  // apply CTAs per SM (T = 8: <= 128 registers)
 #endif
-__global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
+__global__ void __launch_bounds__(GeoFix<N>::ANT, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const int64_t* __restrict__ list, const int* __restrict__ count,
                                                            int64_t chunk0, int64_t chunk_n,
                                                            const double2* __restrict__ planes, int md, double mult0,
                                                            double jac, double w, double* __restrict__ q,
                                                            hk_cell_status* __restrict__ st) {
     using G = GeoFix<N>;
+    constexpr int NT = G::ANT;
     constexpr int NN = G::NN, T = G::T, B = G::B, MP = G::MP, STAGE = G::STAGE, SLABS = N / T, NBLK = G::NBLK;
     constexpr int64_t NB = (int64_t)N * N * N;
     extern __shared__ __align__(16) double2 sm[];
     double* red = reinterpret_cast<double*>(sm + 2 * STAGE);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    static_assert(256 % B == 0 && ((256 / B) % 2 == 0 || MP == 1) && T % 2 == 0 && N % B == 0,
-                  "pair layout: j2 = j2b + t / B + (256 / B) m, j3 = j3b + t % B");
-    const int j2l = t / B, j3l = t % B;  // this thread's pairs in the block: (j2l + (256 / B) m, j3l)
+    static_assert(NT % B == 0 && ((NT / B) % 2 == 0 || MP == 1) && T % 2 == 0 && N % B == 0,
+                  "pair layout: j2 = j2b + t / B + (NT / B) m, j3 = j3b + t % B");
+    const int j2l = t / B, j3l = t % B;  // this thread's pairs in the block: (j2l + (NT / B) m, j3l)
     int64_t avail = (int64_t)*count - chunk0;
     if (avail > chunk_n) avail = chunk_n;
     for (int64_t wi = blockIdx.x; wi < avail * SLABS * NBLK; wi += gridDim.x) {
@@ -230,13 +235,13 @@ __global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const
             const double2* P2 = P1 + T * B;
             // A B with A = s1 z0.y + s2 z1.y + s3 z2.y (B: the .x parts) equals A' B' with
             // A' = s1 (s2 z0.y) + z1.y + (s2 s3) z2.y: s2 = (-1)^j2 and s3 = (-1)^j3 are fixed
-            // per thread (j2 = j2b + t / B + (256 / B) m with 256 / B even, j3 = j3b + t % B),
+            // per thread (j2 = j2b + t / B + (NT / B) m with NT / B even, j3 = j3b + t % B),
             // s1 = (-1)^j1 per plane tt.
             // z1 depends on (tt, j3) only: one load per plane for all MP pairs.
             double2 z0[MP];
 #pragma unroll
             for (int m = 0; m < MP; ++m) {
-                const double2 v = P0[t + 256 * m];
+                const double2 v = P0[t + NT * m];
                 z0[m] = make_double2(s2 * v.x, s2 * v.y);
             }
             // direction 0 carries the multiplicity mult0; the others (1.0 * A == A)
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const
                     const double2 z1 = P1[tt * B + j3l];
 #pragma unroll
                     for (int m = 0; m < MP; ++m) {
-                        const double2 z2 = P2[tt * B + j2l + (256 / B) * m];
+                        const double2 z2 = P2[tt * B + j2l + (NT / B) * m];
                         const bool odd = ((j1_0 + tt) & 1) != 0;  // j1_0 is even: compile-time per tt
                         const double Aq = fma(tau, z2.y, odd ? z1.y - z0[m].y : z1.y + z0[m].y);
                         const double Bq = fma(tau, z2.x, odd ? z1.x - z0[m].x : z1.x + z0[m].x);  // = -hb_i
@@ -265,7 +270,7 @@ __global__ void __launch_bounds__(256, HK_NYQ_APPLY_MINB) nyq_apply_kernel(const
         double* qc = q + cell * NB;
 #pragma unroll
         for (int m = 0; m < MP; ++m) {
-            const int p = (j2_0 + (256 / B) * m) * N + j3;
+            const int p = (j2_0 + (NT / B) * m) * N + j3;
 #pragma unroll
             for (int tt = 0; tt < T; ++tt) {
                 const int64_t gi = (int64_t)(j1_0 + tt) * NN + p;
@@ -349,28 +354,28 @@ int launch_nyq_fix(hk_ctx ctx, int n, const int64_t* list, const int* count, int
     if (s0) return s0;
     double2* planes = static_cast<double2*>(ctx->fix_scratch);
     // persistent grids of exactly the resident CTAs (registers / shared memory decide)
-    auto run = [&](auto k1, size_t smem1, auto k2, size_t smem2) -> int {
+    auto run = [&](auto k1, size_t smem1, auto k2, size_t smem2, int nt2) -> int {
         int s;
         if ((s = check_cuda(ctx, cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1), "smem")) ||
             (s = check_cuda(ctx, cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2), "smem")))
             return s;
         int r1 = 0, r2 = 0;
         if ((s = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r1, k1, 256, smem1), "occupancy")) ||
-            (s = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k2, 256, smem2), "occupancy")))
+            (s = check_cuda(ctx, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r2, k2, nt2, smem2), "occupancy")))
             return s;
         const unsigned g1 = unsigned(ctx->sm_count * std::max(r1, 1)), g2 = unsigned(ctx->sm_count * std::max(r2, 1));
         for (int64_t c0 = 0; c0 < max_cells; c0 += chunk) {
             k1<<<g1, 256, smem1, ctx->stream>>>(list, count, c0, chunk, nyqF, ta, tap, md, planes);
-            k2<<<g2, 256, smem2, ctx->stream>>>(list, count, c0, chunk, planes, md, mult0, jac, w, q, st);
+            k2<<<g2, nt2, smem2, ctx->stream>>>(list, count, c0, chunk, planes, md, mult0, jac, w, q, st);
             ctx->launches += 2;
             if ((s = check_cuda(ctx, cudaGetLastError(), "nyq_fix kernels"))) return s;
         }
         return HK_OK;
     };
     switch (n) {
-    case 16: return run(nyq_planes_kernel<16>, GeoFix<16>::SMEM1, nyq_apply_kernel<16>, GeoFix<16>::SMEM2);
-    case 32: return run(nyq_planes_kernel<32>, GeoFix<32>::SMEM1, nyq_apply_kernel<32>, GeoFix<32>::SMEM2);
-    case 64: return run(nyq_planes_kernel<64>, GeoFix<64>::SMEM1, nyq_apply_kernel<64>, GeoFix<64>::SMEM2);
+    case 16: return run(nyq_planes_kernel<16>, GeoFix<16>::SMEM1, nyq_apply_kernel<16>, GeoFix<16>::SMEM2, GeoFix<16>::ANT);
+    case 32: return run(nyq_planes_kernel<32>, GeoFix<32>::SMEM1, nyq_apply_kernel<32>, GeoFix<32>::SMEM2, GeoFix<32>::ANT);
+    case 64: return run(nyq_planes_kernel<64>, GeoFix<64>::SMEM1, nyq_apply_kernel<64>, GeoFix<64>::SMEM2, GeoFix<64>::ANT);
     default: return fail(ctx, HK_UNSUPPORTED, "nyq_fix: n = 16, 32, 64");
     }
 }
